@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark: TGSP-GMRES solve on BASELINE configs[1] (C2) on B200.
+
+A "step" = one full right-preconditioned GMRES(20) solve to 1e-6 with the
+two-grid sweeping preconditioner (the north_star hot path), inputs resident
+in HBM.  ``value`` = fine DOF/s summed over ranks (n_fine * solves / time,
+time = max over ranks of CUDA-event time).  ``e2e`` = the same metric
+through the public API with the right-hand side in host memory and the
+solution copied back (H2D + D2H inside the timed region).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 1] [--scale 1]
+
+``--impl reference`` times the CPU oracle port of the reference algorithm
+(oracle/, numpy + scipy SuperLU exactly like the reference) on a bounded
+sample of the same workload.  N>1: one process per GPU (torchrun); the
+path's sweep is a sequential chain, so ranks run independent replicas of the
+solve (weak scaling, no data-path collective) -- see DESIGN.md.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+HBM_FALLBACK_GBS = 6650.0   # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+L2_BYTES = 126 * 2**20
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", type=int, default=1, help="BASELINE configs index (0-based)")
+    p.add_argument("--scale", type=int, default=1, help="divide the grid size (debug)")
+    p.add_argument("--cpu-iters", type=int, default=3,
+                   help="GMRES iterations in the bounded CPU-oracle sample")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--orth", default="cgs2")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+def dist_info():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        try:
+            d = json.loads(f.read_text())
+            return float(d["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return HBM_FALLBACK_GBS, "fallback"
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons (NVML) while the timed region runs."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting", 0x10: "sync_boost"}
+
+    def __init__(self, device_index):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def workload_name(p):
+    op = {"fd5": "5-point fine op (SURVEY F2 ii)", "fe9": "9-point compact fine op",
+          "fe27": "27-point compact fine op"}[p.fine]
+    return (f"{p.name}: {p.mesh.dim}-D {'x'.join(map(str, p.mesh.unknowns))} fine DOF incl. PML, "
+            f"{op}, TGSP X-sweep J={p.subdomains}, nu={p.nu}, GMRES({p.restart}) to {p.tol:g}")
+
+
+# ---------------------------------------------------------------------------
+def cpu_sample(problem, hh, its_target, iters):
+    """Bounded sample of the CPU oracle (reference algorithm, SuperLU slabs):
+    ``iters`` GMRES iterations on the same problem, extrapolated by
+    per-iteration time to the full solve of ``its_target`` iterations."""
+    from oracle import tgsp_oracle as orc
+    t0 = time.perf_counter()
+    tg = orc.from_hierarchy(hh)
+    tg.fine.csr, tg.part.op.csr        # assemble the CSR matrices outside the sample
+    setup = time.perf_counter() - t0
+    f = problem.f[0].ravel()
+    t0 = time.perf_counter()
+    _, its, _, _, _ = orc.gmres(lambda v: tg.fine.csr @ v, tg.as_preconditioner(), f,
+                                tol=1e-300, max_iter=iters, restart=problem.restart)
+    dt = time.perf_counter() - t0
+    per_it = dt / (its + 1)           # its x (A M v + orth) + final (M dv, f - A u)
+    projected = per_it * (its_target + 1)
+    return {"value": problem.n_fine / projected, "projected_solve_s": projected,
+            "per_iteration_s": per_it, "sample_s": dt, "oracle_setup_s": setup,
+            "sample_iterations": its}
+
+
+def run_reference(args):
+    world, rank, _ = dist_info()
+    if rank != 0:
+        return
+    import paper_1412_0464_b200 as hb
+    from paper_1412_0464_b200.configs import config
+    p = config(args.config, args.scale)
+    hh = hb.build_hierarchy(p.mesh, p.model, None, hb.SmootherConfig(p.omega_jac, p.nu),
+                            hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains),
+                            device=False)
+    its_target = {0: 9, 1: 48}.get(args.config, 50) if args.scale == 1 else 30
+    vals = []
+    for s in range(args.warmup + args.steps):
+        r = cpu_sample(p, hh, its_target, args.cpu_iters)
+        if s >= args.warmup:
+            vals.append(r)
+    value = float(np.median([r["value"] for r in vals]))
+    ms = float(np.median([r["projected_solve_s"] for r in vals])) * 1e3
+    cores = 1
+    line = {
+        "impl": "reference", "metric": "TGSP-GMRES fine DOF/s (solve to 1e-6 rel-res)",
+        "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": workload_name(p), "fine_dof": p.n_fine},
+        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.cpu_iters} GMRES iterations of the numpy/scipy "
+                                   f"oracle (SuperLU slab solves, as the reference) "
+                                   f"extrapolated per iteration to a {its_target}-iteration "
+                                   f"solve; host has {os.cpu_count()} cores, 1 used"},
+        "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    world, rank, local = dist_info()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    import paper_1412_0464_b200 as hb
+    from paper_1412_0464_b200._lib import context
+    from paper_1412_0464_b200.configs import config
+
+    p = config(args.config, args.scale)
+    t0 = time.perf_counter()
+    keep = (rank == 0 and world == 1 and not args.no_cpu_baseline)
+    cycle, _ = hb.build_two_grid(p.mesh, p.model, smoother=hb.SmootherConfig(p.omega_jac, p.nu),
+                                 coarse="sweep",
+                                 sweep=hb.SweepOptions(p.w_dd, p.s_dd, "x",
+                                                       subdomains=p.subdomains),
+                                 keep_slab_ops=keep)
+    dev = cycle.device()
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    ctx = context()
+    nrhs_total = p.f.shape[0]
+    mine = [r for r in range(nrhs_total) if r % world == rank] or [rank % nrhs_total]
+    f_dev = [torch.from_numpy(p.f[r].ravel()).cuda() for r in mine]
+    cfg = hb.GmresConfig(p.tol, p.max_iter, p.restart)
+    prec = cycle.as_preconditioner()
+
+    def solve(fd):
+        return hb.gmres(cycle.fine_csr, prec, fd, cfg, orth=args.orth)
+
+    # warm-up
+    reports = []
+    for _ in range(args.warmup):
+        for fd in f_dev:
+            solve(fd)
+    # ---- timed region: K steps (each step solves this rank's right-hand sides)
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ctx.profile_reset()
+    ctx.profile(True)
+    launches0 = ctx.launches
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            for fd in f_dev:
+                u, rep = solve(fd)
+                reports.append(rep)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.launches - launches0
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    if world > 1:
+        torch.distributed.barrier()
+    ms_local = ev0.elapsed_time(ev1)
+    ms = ms_local
+    if world > 1:
+        t = torch.tensor([ms_local], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    solves = args.steps * len(f_dev) * world
+    value = p.n_fine * solves / (ms / 1e3)
+    its = [r.iterations for r in reports]
+    # true residual of the last solve
+    u_h = u.cpu().numpy()
+    f0 = p.f[mine[-1]].ravel()
+    true_res = float(np.linalg.norm(f0 - cycle.fine_csr @ u_h) / np.linalg.norm(f0))
+
+    # ---- e2e: public API with host buffers (H2D + D2H inside the timed region)
+    f_host = [torch.from_numpy(p.f[r].ravel()).pin_memory().numpy() for r in mine]
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        for fh in f_host:
+            u_out, _ = hb.gmres(cycle.fine_csr, prec, fh, cfg, orth=args.orth)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = p.n_fine * solves / (e2e_ms / 1e3)
+
+    # ---- roofline of the dominant kernel class (profiler events over the timed region)
+    peak, peak_kind = peaks()
+    total_ms = sum(v["ms"] for v in prof.values()) or 1.0
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(dom)
+        except Exception:
+            traffic = None
+
+    def roof(names):
+        ms_ = sum(prof[k]["ms"] for k in names if k in prof)
+        by = sum(prof[k]["bytes"] for k in names if k in prof)
+        n = sum(prof[k]["launches"] for k in names if k in prof)
+        if not n or ms_ <= 0:
+            return None
+        ach = (by / n) / ((ms_ / n) / 1e3) / 1e9
+        return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "peak_kind": peak_kind,
+                "bytes_per_launch": by / n, "ms_per_launch": ms_ / n, "launches": n}
+
+    roofline = roof([dom])
+    roofline["kernel"] = dom
+    roofline["traffic"] = traffic
+    stencil_roof = roof(["stencil", "residual", "jacobi", "jacobi2z"])
+    shares = {k: {"share": v["ms"] / total_ms, "ms": v["ms"], "launches": v["launches"],
+                  "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None}
+              for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = cpu_sample(p, cycle.hierarchy, int(np.median(its)), args.cpu_iters)
+        cpu = {"value": r["value"], "unit": "DOF/s", "cores": 1, "kind": "port",
+               "sample": f"{r['sample_iterations']} GMRES iterations of the numpy/scipy oracle "
+                         f"(SuperLU slab solves like the reference) in {r['sample_s']:.1f} s, "
+                         f"extrapolated per iteration to the {int(np.median(its))}-iteration "
+                         f"solve; host has {os.cpu_count()} cores, 1 used",
+               "projected_solve_s": r["projected_solve_s"]}
+
+    if rank == 0:
+        fac_gb = dev.sweep.factor_bytes / 1e9
+        line = {
+            "metric": "TGSP-GMRES fine DOF/s (solve to 1e-6 rel-res)",
+            "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c128", "data": "synthetic",
+            "config": {"workload": workload_name(p), "fine_dof": p.n_fine,
+                       "coarse_dof": int(np.prod(cycle.coarse_op.shape)),
+                       "subdomains": p.subdomains, "rhs_per_rank": len(f_dev),
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": f"working set > L2 (slab factors {fac_gb:.2f} GB + basis + operators "
+                             f"stream every step); no flush"},
+            "solve_s": ms / 1e3 / (args.steps * len(f_dev)),
+            "setup_s": setup_s,
+            "iterations": int(np.median(its)),
+            "true_residual": true_res,
+            "e2e": {"value": e2e_value, "unit": "DOF/s",
+                    "h2d_bytes_per_step": 16 * p.n_fine * len(f_dev),
+                    "d2h_bytes_per_step": 16 * p.n_fine * len(f_dev)},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "roofline_stencil": stencil_roof,
+            "kernel_shares": shares,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

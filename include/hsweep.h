@@ -1,0 +1,155 @@
+/*
+ * libhsweep -- C ABI of the B200-native TGSP-GMRES hot path.
+ *
+ * Drop-in boundary for the reference package `helmsweep` (arXiv 1412.0464,
+ * /root/reference/pkg/src/helmsweep).  Every entry point replaces one
+ * reference interface on the GMRES -> two-grid -> sweep path; the citation is
+ * on each declaration.  Plain C types only: opaque handles, device pointers
+ * (`void*` to complex128 interleaved re/im, numpy's memory layout), host
+ * scalars and host index arrays.  All work is stream-ordered on the context
+ * stream (hs_ctx_set_stream); nothing here synchronises unless it says so.
+ *
+ * Status codes map onto the reference's exception classes:
+ *   HS_E_SHAPE / HS_E_ARG -> ValueError     HS_E_ZERO_PIVOT -> ZeroDivisionError
+ *   HS_E_ZERO_DIAG -> ZeroDivisionError     HS_E_NONFINITE  -> FloatingPointError
+ *   HS_E_BUFFER -> RuntimeError             HS_E_CUDA       -> RuntimeError
+ * hs_last_error() returns the message, hs_last_error_index() the row / node.
+ */
+#ifndef HSWEEP_H
+#define HSWEEP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  HS_OK = 0,
+  HS_E_SHAPE = 1,
+  HS_E_ZERO_PIVOT = 2,
+  HS_E_ZERO_DIAG = 3,
+  HS_E_NONFINITE = 4,
+  HS_E_CUDA = 5,
+  HS_E_ARG = 6,
+  HS_E_BUFFER = 7
+};
+
+enum { HS_VARIANT_UD = 0, HS_VARIANT_X = 1 };
+
+typedef struct hs_ctx hs_ctx;
+typedef struct hs_stencil hs_stencil;
+typedef struct hs_transfer hs_transfer;
+typedef struct hs_sweep hs_sweep;
+typedef struct hs_cycle hs_cycle;
+
+/* ---- context ------------------------------------------------------------ */
+int hs_ctx_create(int device, hs_ctx** out);
+int hs_ctx_destroy(hs_ctx* ctx);
+int hs_ctx_set_stream(hs_ctx* ctx, void* cuda_stream);
+const char* hs_last_error(hs_ctx* ctx);
+long long hs_last_error_index(hs_ctx* ctx);
+long long hs_launch_count(hs_ctx* ctx);           /* kernels launched so far */
+int hs_synchronize(hs_ctx* ctx);
+int hs_version(void);
+
+/* ---- built-in profiler (tracing) -------------------------------
+ * When enabled, every launch is bracketed by CUDA events on the context
+ * stream and attributed to a kernel class:
+ *   0 stencil  1 residual  2 jacobi  3 jacobi2z (2 steps from zero)
+ *   4 restrict 5 prolong   6 sweep_gather 7 sweep_front
+ *   8 krylov_dot 9 krylov_update 10 krylov_other 11 setup
+ * hs_profile_read synchronises, folds pending events in and copies per-class
+ * milliseconds, algorithmic HBM bytes and launch counts (arrays of nclass). */
+int hs_profile_enable(hs_ctx* ctx, int on);
+int hs_profile_reset(hs_ctx* ctx);
+int hs_profile_read(hs_ctx* ctx, int nclass, double* ms, double* bytes, long long* counts);
+
+/* ---- compact-stencil operators ------------------------------------------
+ * StencilOperator(shape, coeffs)            reference discretize.py:57-107
+ * `offsets`: S x dim int8, row-major; `coeffs`: host pointer to S contiguous
+ * arrays of prod(shape) complex128 in the same order.  Uploaded once. */
+int hs_stencil_create(hs_ctx* ctx, int dim, const int64_t* shape, int S,
+                      const int8_t* offsets, const double* coeffs, hs_stencil** out);
+int hs_stencil_destroy(hs_ctx* ctx, hs_stencil* op);
+/* y = A x            stencil_apply / fine_csr @ v   discretize.py:110-117, twogrid.py:140-141 */
+int hs_stencil_apply(hs_ctx* ctx, const hs_stencil* op, const void* x, void* y, int nrhs);
+/* r = f - A u        the residual lines twogrid.py:153, sweepdd.py:343 */
+int hs_stencil_residual(hs_ctx* ctx, const hs_stencil* op, const void* f, const void* u,
+                        void* r, int nrhs);
+/* u <- u + omega (f - A u)/diag, `steps` times (in place);
+ * u_is_zero != 0 means u enters as zero (the pre-smoother's start)
+ * jacobi_smooth / TwoGridCycle._smooth       twogrid.py:41-50, 143-148 */
+int hs_jacobi(hs_ctx* ctx, const hs_stencil* op, void* u, const void* f, double omega,
+              int steps, int u_is_zero, int nrhs);
+
+/* ---- tent transfers -----------------------------------------------------
+ * CoarseningMap -> prolongation_matrix       mesh.py:107-123, twogrid.py:53-79
+ * fp_concat: per-axis fine_point_of_coarse arrays concatenated (lengths in
+ * fp_len[dim]); refined_concat: per-axis refined_cell (length fp_len[a]-1). */
+int hs_transfer_create(hs_ctx* ctx, int dim, const int64_t* fp_len, const int64_t* fp_concat,
+                       const uint8_t* refined_concat, hs_transfer** out);
+int hs_transfer_destroy(hs_ctx* ctx, hs_transfer* t);
+/* rc = scale * P^T r                         twogrid.py:154 (restrict: 89-93 with scale 1) */
+int hs_restrict(hs_ctx* ctx, const hs_transfer* t, const void* r_fine, void* rc, double scale,
+                int nrhs);
+/* rc = scale * P^T (f - A u)                 twogrid.py:153-154 fused */
+int hs_restrict_residual(hs_ctx* ctx, const hs_transfer* t, const hs_stencil* op,
+                         const void* u, const void* f, void* rc, double scale, int nrhs);
+/* u += P uc  (beta = 0: u = P uc)            twogrid.py:156 (prolongate: 82-86) */
+int hs_prolong_add(hs_ctx* ctx, const hs_transfer* t, const void* uc, void* u, int accumulate,
+                   int nrhs);
+
+/* ---- sweeping preconditioner --------------------------------------------
+ * build_partition + per-slab factorize       sweepdd.py:192-218, sparselin.py:40-68
+ * coarse: the global level operator (transmission blocks and the mid-sweep
+ * residual read it, sweepdd.py:133-141, 175-176).  slab_ops[j]: the slab
+ * operators (sweepdd.py:211 / discretize.py:685-723), slab j spanning grid
+ * points slab_lo[j]..slab_hi[j] (1-based).  Factorises every slab on the
+ * device (batched block-tridiagonal LU); fails with HS_E_ZERO_PIVOT. */
+int hs_sweep_create(hs_ctx* ctx, const hs_stencil* coarse, int J, const int64_t* beta,
+                    const int64_t* beta_tilde, const int64_t* slab_lo, const int64_t* slab_hi,
+                    const hs_stencil* const* slab_ops, hs_sweep** out);
+int hs_sweep_destroy(hs_ctx* ctx, hs_sweep* s);
+/* u = Sweep(f); variant HS_VARIANT_X (prec_x, sweepdd.py:322-359) or
+ * HS_VARIANT_UD (prec_ud, sweepdd.py:312-319).  f and u: device, coarse shape. */
+int hs_sweep_apply(hs_ctx* ctx, hs_sweep* s, int variant, const void* f, void* u);
+/* bytes of device memory held by the slab factors (diagnostic) */
+long long hs_sweep_factor_bytes(hs_sweep* s);
+
+/* ---- two-grid cycle ------------------------------------------------------
+ * TwoGridCycle(fine, P, smoother, SweepCoarseSolver)   twogrid.py:119-164, 196-229 */
+int hs_cycle_create(hs_ctx* ctx, const hs_stencil* fine, const hs_transfer* t,
+                    const hs_stencil* coarse, hs_sweep* sweep, double omega_jac, int nu,
+                    double restrict_scale, int variant, hs_cycle** out);
+int hs_cycle_destroy(hs_ctx* ctx, hs_cycle* c);
+/* u = M f : vcycle / tgsp_apply / as_preconditioner   twogrid.py:150-176 */
+int hs_vcycle(hs_ctx* ctx, hs_cycle* c, const void* f, void* u);
+/* w = A M f (the GMRES operator, krylov.py:125-126) */
+int hs_vcycle_apply_a(hs_ctx* ctx, hs_cycle* c, const void* f, void* w);
+
+/* ---- GMRES vector kernels (krylov.py:46-102) ------------------------------
+ * V: device basis, k vectors of length n with leading dimension ldv (elements).
+ * Results to device pointers; deterministic two-stage reductions. */
+/* h[i] = vdot(V_i, w) (i < k); h[k] = (||w||^2, 0) */
+int hs_block_dot(hs_ctx* ctx, const void* V, int64_t ldv, int k, const void* w, int64_t n,
+                 void* h);
+/* w -= sum_i h[i] V_i (i < k); nrm2[0] = (||w||^2, 0) */
+int hs_block_update(hs_ctx* ctx, const void* V, int64_t ldv, int k, const void* h, void* w,
+                    int64_t n, void* nrm2);
+/* out = sum_i y[i] V_i  (y: device, k complex) */
+int hs_lincomb(hs_ctx* ctx, const void* V, int64_t ldv, int k, const void* y, void* out,
+               int64_t n);
+/* x = alpha * x (alpha host complex) */
+int hs_scale(hs_ctx* ctx, void* x, int64_t n, double alpha_re, double alpha_im);
+/* y = a x + b y */
+int hs_axpby(hs_ctx* ctx, double a_re, double a_im, const void* x, double b_re, double b_im,
+             void* y, int64_t n);
+/* out[0] = (||x||^2, nonfinite_count) */
+int hs_norm2(hs_ctx* ctx, const void* x, int64_t n, void* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HSWEEP_H */

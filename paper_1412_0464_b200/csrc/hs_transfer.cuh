@@ -1,0 +1,30 @@
+#pragma once
+#include "hs_common.cuh"
+
+namespace hs {
+
+// Per-axis tent-transfer tables (canonical 3 axes, fastest last).
+struct TransferDesc {
+  int64_t nf[3], nc[3];
+  const int* ctr[3];      // [nc]  fine centre index of coarse unknown I
+  const double* wl[3];    // [nc]  weight of fine centre-1 (0 or 1/2)
+  const double* wr[3];    // [nc]  weight of fine centre+1 (0 or 1/2)
+  const int* par[3];      // [2*nf] coarse parents of fine unknown (or -1)
+  const double* pw[3];    // [2*nf] parent weights
+};
+
+struct Transfer {
+  int dim = 0;
+  TransferDesc d{};
+  char* buf = nullptr;
+};
+
+int transfer_create(Ctx* c, int dim, const int64_t* fp_len, const int64_t* fp_concat,
+                    const uint8_t* refined_concat, Transfer** out);
+void transfer_destroy(Transfer* t);
+int transfer_restrict(Ctx* c, const Transfer* t, const double2* r, double2* rc, double scale,
+                      int nrhs);
+int transfer_prolong(Ctx* c, const Transfer* t, const double2* uc, double2* u, int accumulate,
+                     int nrhs);
+
+}  // namespace hs

@@ -1,0 +1,218 @@
+"""Device-side handles over libhsweep: operators, transfers, sweep, cycle.
+
+Vectors: numpy arrays are copied to the device (and results copied back as
+numpy); torch CUDA complex128 tensors are used zero-copy and results are
+returned as torch tensors.  Everything is stream-ordered on torch's current
+stream.  Device memory of handles is released when the handle is collected.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import context, i64
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def to_device(x, n: int | None = None, ctx=None):
+    """(tensor on device, was_numpy).  complex128, contiguous, flat view."""
+    torch = _torch()
+    ctx = ctx or context()
+    if isinstance(x, torch.Tensor):
+        t = x
+        if t.device.type != "cuda" or t.dtype != torch.complex128 or not t.is_contiguous():
+            t = t.to(device=f"cuda:{ctx.device}", dtype=torch.complex128).contiguous()
+        t = t.reshape(-1)
+        was_np = False
+    else:
+        a = np.ascontiguousarray(np.asarray(x, dtype=complex)).reshape(-1)
+        t = torch.from_numpy(a).to(f"cuda:{ctx.device}", non_blocking=False)
+        was_np = True
+    if n is not None and t.numel() != n:
+        raise ValueError(f"vector has {t.numel()} entries, expected {n}")
+    return t, was_np
+
+
+def from_device(t, was_numpy: bool, shape=None):
+    if was_numpy:
+        a = t.detach().cpu().numpy()
+        return a.reshape(shape) if shape is not None else a
+    return t.reshape(shape) if shape is not None else t
+
+
+def ptr(t) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr())
+
+
+def empty(n: int, ctx=None):
+    torch = _torch()
+    ctx = ctx or context()
+    return torch.empty(n, dtype=torch.complex128, device=f"cuda:{ctx.device}")
+
+
+class _Handle:
+    _destroy = None
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and self._destroy:
+            try:
+                getattr(self.ctx.lib, self._destroy)(self.ctx.h, h)
+            except Exception:  # interpreter shutdown
+                pass
+            self.h = None
+
+
+class DeviceStencil(_Handle):
+    """Uploaded compact-stencil operator (reference StencilOperator)."""
+
+    _destroy = "hs_stencil_destroy"
+
+    def __init__(self, shape, offsets, coeffs, ctx=None):
+        self.ctx = ctx or context()
+        self.shape = tuple(int(s) for s in shape)
+        self.n = int(np.prod(self.shape))
+        offs = np.ascontiguousarray(np.asarray(offsets, dtype=np.int8).reshape(-1, len(shape)))
+        co = np.ascontiguousarray(np.asarray(coeffs, dtype=complex).reshape(len(offs), self.n))
+        self.offsets = [tuple(int(v) for v in o) for o in offs]
+        shp, pshp = i64(self.shape)
+        h = C.c_void_p()
+        self.ctx.call("hs_stencil_create", len(self.shape), pshp, len(offs),
+                      offs.ctypes.data_as(C.POINTER(C.c_int8)),
+                      co.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)), C.byref(h))
+        self.h = h
+
+    @classmethod
+    def from_host(cls, op, ctx=None):
+        offs = sorted(op.coeffs)
+        return cls(op.shape, offs, np.stack([op.coeffs[o].reshape(-1) for o in offs]), ctx)
+
+    def apply(self, x, shape=None, nrhs: int = 1):
+        xt, was_np = to_device(x, self.n * nrhs, self.ctx)
+        y = empty(self.n * nrhs, self.ctx)
+        self.ctx.call("hs_stencil_apply", self.h, ptr(xt), ptr(y), nrhs)
+        if shape is None and was_np and np.ndim(x) > 1:
+            shape = np.shape(x)
+        return from_device(y, was_np, shape)
+
+    __call__ = apply
+
+    def __matmul__(self, x):
+        return self.apply(x)
+
+    def residual(self, f, u, out=None):
+        ft, _ = to_device(f, self.n, self.ctx)
+        ut, _ = to_device(u, self.n, self.ctx)
+        r = out if out is not None else empty(self.n, self.ctx)
+        self.ctx.call("hs_stencil_residual", self.h, ptr(ft), ptr(ut), ptr(r), 1)
+        return r
+
+    def jacobi(self, u, f, omega, steps, u_is_zero=False):
+        """In-place on a device tensor u (flat)."""
+        self.ctx.call("hs_jacobi", self.h, ptr(u), ptr(f), float(omega), int(steps),
+                      int(bool(u_is_zero)), 1)
+        return u
+
+
+class DeviceTransfer(_Handle):
+    """Tent prolongation / restriction tables from a CoarseningMap."""
+
+    _destroy = "hs_transfer_destroy"
+
+    def __init__(self, cmap, ctx=None):
+        self.ctx = ctx or context()
+        fps = [np.asarray(f, dtype=np.int64) for f in cmap.fine_point_of_coarse]
+        refs = [np.asarray(r, dtype=np.uint8) for r in cmap.refined_cell]
+        self.fine_shape = tuple(int(f[-1]) - 1 for f in fps)
+        self.coarse_shape = tuple(len(f) - 2 for f in fps)
+        self.nf = int(np.prod(self.fine_shape))
+        self.nc = int(np.prod(self.coarse_shape))
+        lens, plen = i64([len(f) for f in fps])
+        cat, pcat = i64(np.concatenate(fps))
+        rc = np.ascontiguousarray(np.concatenate(refs), dtype=np.uint8)
+        h = C.c_void_p()
+        self.ctx.call("hs_transfer_create", len(fps), plen, pcat,
+                      rc.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(h))
+        self.h = h
+
+    def restrict(self, r, scale=1.0):
+        rt, was_np = to_device(r, self.nf, self.ctx)
+        out = empty(self.nc, self.ctx)
+        self.ctx.call("hs_restrict", self.h, ptr(rt), ptr(out), float(scale), 1)
+        return from_device(out, was_np, self.coarse_shape if was_np else None)
+
+    def prolong(self, uc, u=None):
+        ut, was_np = to_device(uc, self.nc, self.ctx)
+        out = empty(self.nf, self.ctx) if u is None else u
+        self.ctx.call("hs_prolong_add", self.h, ptr(ut), ptr(out), int(u is not None), 1)
+        return from_device(out, was_np, self.fine_shape if was_np else None)
+
+
+class DeviceSweep(_Handle):
+    """Factorised slabs + UD/X schedules of one partition (device)."""
+
+    _destroy = "hs_sweep_destroy"
+
+    def __init__(self, coarse: DeviceStencil, J, beta, beta_tilde, slab_lo, slab_hi,
+                 slab_ops, ctx=None):
+        self.ctx = ctx or context()
+        self.coarse = coarse
+        self.slab_ops = list(slab_ops)   # keep alive during factorisation
+        self.shape = coarse.shape
+        self.n = coarse.n
+        self.J = int(J)
+        b, pb = i64(beta)
+        bt, pbt = i64(beta_tilde)
+        lo, plo = i64(slab_lo)
+        hi, phi = i64(slab_hi)
+        arr = (C.c_void_p * self.J)(*[op.h for op in self.slab_ops])
+        h = C.c_void_p()
+        self.ctx.call("hs_sweep_create", coarse.h, self.J, pb, pbt, plo, phi, arr, C.byref(h))
+        self.h = h
+        # the factors are self-contained on the device: slab coefficient copies can go
+        self.slab_ops = None
+
+    @property
+    def factor_bytes(self) -> int:
+        return int(self.ctx.lib.hs_sweep_factor_bytes(self.h))
+
+    def apply(self, f, variant="x"):
+        v = _lib.HS_VARIANT_X if variant == "x" else _lib.HS_VARIANT_UD
+        ft, was_np = to_device(f, self.n, self.ctx)
+        u = empty(self.n, self.ctx)
+        self.ctx.call("hs_sweep_apply", self.h, v, ptr(ft), ptr(u))
+        return u, was_np
+
+
+class DeviceCycle(_Handle):
+    """The TGSP two-grid cycle (fine smoother + transfers + coarse sweep)."""
+
+    _destroy = "hs_cycle_destroy"
+
+    def __init__(self, fine: DeviceStencil, transfer: DeviceTransfer, coarse: DeviceStencil,
+                 sweep: DeviceSweep, omega_jac, nu, restrict_scale, variant, ctx=None):
+        self.ctx = ctx or context()
+        self.fine, self.transfer, self.coarse, self.sweep = fine, transfer, coarse, sweep
+        self.n = fine.n
+        v = _lib.HS_VARIANT_X if variant == "x" else _lib.HS_VARIANT_UD
+        h = C.c_void_p()
+        self.ctx.call("hs_cycle_create", fine.h, transfer.h, coarse.h, sweep.h,
+                      float(omega_jac), int(nu), float(restrict_scale), v, C.byref(h))
+        self.h = h
+
+    def vcycle_dev(self, f_dev, out=None):
+        u = out if out is not None else empty(self.n, self.ctx)
+        self.ctx.call("hs_vcycle", self.h, ptr(f_dev), ptr(u))
+        return u
+
+    def apply_a_dev(self, f_dev, out=None):
+        w = out if out is not None else empty(self.n, self.ctx)
+        self.ctx.call("hs_vcycle_apply_a", self.h, ptr(f_dev), ptr(w))
+        return w

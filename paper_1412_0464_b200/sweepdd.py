@@ -1,0 +1,274 @@
+"""Sweeping domain-decomposition preconditioner: partition (host setup) and
+its device application.
+
+Drop-in names of reference ``sweepdd.py``:
+
+* ``HelmholtzLevel``, ``fine_level``, ``coarse_level``   :33-87
+* ``TransmissionMatrix``, ``extract_transmission``      :98-141, :221-230
+* ``spaced_interfaces``, ``default_subdomain_count``    :179-189
+* ``build_partition``                                    :192-218
+* ``prec_ud``, ``prec_x``, ``SweepingPreconditioner``    :312-359, :437-467
+
+Setup (geometry, slab operator assembly) runs on the host; the slabs are
+factorised on the device at ``build_partition`` time and every application
+runs the CUDA slab-solve chains (``csrc/hs_sweep.cu``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .discretize import (StencilOperator, WaveModel, assemble_fe_pml_coarse, assemble_fine,
+                         assemble_opt_fd_coarse, assemble_sponge, default_table,
+                         interior_spacing, subdomain_fd_operator, subdomain_fe_operator,
+                         _nodes_to_cells)
+from .mesh import PML, SPONGE, CoarseningMap, Mesh
+
+
+@dataclass
+class HelmholtzLevel:
+    op: StencilOperator
+    kind: str
+    mesh: Mesh | None = None
+    model: WaveModel | None = None
+    cmap: CoarseningMap | None = None
+    k_cells: np.ndarray | None = None
+    table: object = None
+
+    def subdomain_operator(self, core_lo, core_hi, w_dd, s_dd, open_left, open_right):
+        if self.kind == "fd":
+            return subdomain_fd_operator(self.mesh, self.model, core_lo, core_hi, w_dd, s_dd,
+                                         open_left, open_right)
+        if self.kind == "fe":
+            return subdomain_fe_operator(self.mesh, self.model, self.k_cells, self.table,
+                                         core_lo, core_hi, w_dd, s_dd, open_left, open_right)
+        raise ValueError(f"unknown level kind {self.kind!r}")
+
+
+def fine_level(mesh: Mesh, model: WaveModel, op: StencilOperator | None = None):
+    if op is None:
+        sponge = any(s.kind == SPONGE for pair in mesh.layers for s in pair)
+        op = assemble_sponge(mesh, model) if sponge else assemble_fine(mesh, model)
+    return HelmholtzLevel(op, "fd", mesh=mesh, model=model)
+
+
+def coarse_level(mesh_c: Mesh, cmap: CoarseningMap, model_c: WaveModel, op=None,
+                 k_cells=None, table=None):
+    """FE rows on PML-coarsened meshes, else h^d-scaled optimized FD."""
+    has_pml = any(s.kind == PML for pair in mesh_c.layers for s in pair)
+    table = table or default_table(mesh_c.dim)
+    if has_pml:
+        if k_cells is None:
+            k_cells = _nodes_to_cells(model_c.k)
+        if op is None:
+            op = assemble_fe_pml_coarse(mesh_c, cmap, model_c, k_cells, table)
+    else:
+        k_cells = None
+        if op is None:
+            op = assemble_opt_fd_coarse(mesh_c, model_c, table).scaled(
+                interior_spacing(mesh_c) ** mesh_c.dim, fe_scaled=True)
+    return HelmholtzLevel(op, "fe", mesh=mesh_c, model=model_c, cmap=cmap, k_cells=k_cells,
+                          table=table)
+
+
+# ---------------------------------------------------------------------------
+# transmission (data view; the device reads the global operator rows directly)
+
+@dataclass
+class TransmissionMatrix:
+    point: int
+    block01: dict
+    block10: dict
+    sign: int
+
+    def dense(self):
+        """Full 2m x 2m matrix (small sizes only; inspection helper)."""
+        blk = self.block01 or self.block10
+        shape = next(iter(blk.values())).shape if blk else ()
+        m = int(np.prod(shape)) if shape else 1
+        t = np.zeros((2 * m, 2 * m), dtype=complex)
+        for j in range(m):
+            e = np.zeros(m)
+            e[j] = 1.0
+            e = e.reshape(shape)
+            t[:m, m + j] = self.sign * _face_apply(self.block01, e).ravel()
+            t[m:, j] = -self.sign * _face_apply(self.block10, e).ravel()
+        return t
+
+
+def _face_apply(block, v):
+    out = np.zeros(np.shape(v), dtype=complex)
+    for off, c in block.items():
+        if len(off) == 0:
+            out = out + c * v
+            continue
+        dst = tuple(slice(max(0, -o), n - max(0, o)) for o, n in zip(off, np.shape(v)))
+        src = tuple(slice(max(0, o), n - max(0, -o)) for o, n in zip(off, np.shape(v)))
+        out[dst] += c[dst] * v[src]
+    return out
+
+
+def _extract(op: StencilOperator, b: int, sign: int) -> TransmissionMatrix:
+    x0 = b - 1
+    b01 = {off[1:]: c[x0] for off, c in op.coeffs.items() if off[0] == 1}
+    b10 = {off[1:]: c[x0 + 1] for off, c in op.coeffs.items() if off[0] == -1}
+    return TransmissionMatrix(b, b01, b10, sign)
+
+
+# ---------------------------------------------------------------------------
+# partition
+
+def default_subdomain_count(n_unknowns: int, w_dd: int) -> int:
+    return n_unknowns // (2 * w_dd + 1)
+
+
+def spaced_interfaces(n_unknowns: int, J: int) -> np.ndarray:
+    """Interfaces as even as possible; the remainder goes to the leading slabs."""
+    w, r = divmod(n_unknowns, J)
+    widths = np.full(J, w, dtype=int)
+    widths[:r] += 1
+    return np.concatenate([[0], np.cumsum(widths)]).astype(int)
+
+
+@dataclass
+class Subdomain:
+    j: int
+    pt_lo: int
+    pt_hi: int
+    core_lo: int
+    core_hi: int
+    op: StencilOperator | None
+
+
+@dataclass
+class Partition:
+    level: HelmholtzLevel
+    J: int
+    beta: np.ndarray
+    beta_tilde: np.ndarray
+    w_dd: int
+    s_dd: float
+    subs: list
+    _device: object = field(default=None, repr=False)
+
+    @property
+    def shape(self):
+        return self.level.op.shape
+
+    @property
+    def t_fwd(self):
+        return {j: _extract(self.level.op, int(self.beta[j - 1]), +1) for j in range(2, self.J + 1)}
+
+    @property
+    def t_bwd(self):
+        return {j: _extract(self.level.op, int(self.beta_tilde[j]), -1) for j in range(1, self.J)}
+
+    def device(self):
+        """Factorise every slab on the device (once) and return the handle."""
+        if self._device is None:
+            from .device import DeviceStencil, DeviceSweep
+            coarse = self.level.op.device()
+            slab_ops = [DeviceStencil.from_host(sd.op, coarse.ctx) for sd in self.subs]
+            self._device = DeviceSweep(coarse, self.J, self.beta, self.beta_tilde,
+                                       [sd.pt_lo for sd in self.subs],
+                                       [sd.pt_hi for sd in self.subs], slab_ops, coarse.ctx)
+            del slab_ops
+        return self._device
+
+    def apply_global(self, u):
+        return self.level.op.apply(u)
+
+
+def partition_geometry(n1: int, J: int, tilde_right: bool = False):
+    if J < 2:
+        raise ValueError(f"{J} subdomains: the sweep needs at least 2")
+    beta = spaced_interfaces(n1, J)
+    if np.any(np.diff(beta) < 2):
+        raise ValueError("subdomain thinner than 2 cells")
+    bt = beta.copy()
+    bt[1:J] = beta[1:J] + (1 if tilde_right else -1)
+    return beta, bt
+
+
+def build_partition(level: HelmholtzLevel, w_dd: int = 4, s_dd: float = 20.0,
+                    J: int | None = None, tilde_right: bool = False,
+                    device: bool = True, keep_slab_ops: bool = True) -> Partition:
+    """Staggered interfaces, slab operators (host) and device factorisations."""
+    n1 = level.op.shape[0]
+    if J is None:
+        J = default_subdomain_count(n1, w_dd)
+    beta, bt = partition_geometry(n1, J, tilde_right)
+    subs = []
+    for j in range(1, J + 1):
+        core_lo = min(beta[j - 1], bt[j - 1]) + 1
+        core_hi = max(beta[j], bt[j])
+        op_j, lo, hi = level.subdomain_operator(int(core_lo), int(core_hi), w_dd, s_dd,
+                                                j > 1, j < J)
+        subs.append(Subdomain(j, int(lo), int(hi), int(core_lo), int(core_hi), op_j))
+    part = Partition(level, J, beta, bt, w_dd, s_dd, subs)
+    if device:
+        part.device()
+        if not keep_slab_ops:      # the factors live on the device now
+            for sd in subs:
+                sd.op = None
+    return part
+
+
+def extract_transmission(part: Partition, j: int, direction: str) -> TransmissionMatrix:
+    if direction == "forward":
+        if not 1 < j <= part.J:
+            raise ValueError(f"forward transmission needs 1 < j <= J, got {j}")
+        return _extract(part.level.op, int(part.beta[j - 1]), +1)
+    if direction == "backward":
+        if not 1 <= j < part.J:
+            raise ValueError(f"backward transmission needs 1 <= j < J, got {j}")
+        return _extract(part.level.op, int(part.beta_tilde[j]), -1)
+    raise ValueError(f"direction must be forward or backward, got {direction!r}")
+
+
+# ---------------------------------------------------------------------------
+# applications (device)
+
+def _apply(part: Partition, f, variant: str):
+    from .device import from_device
+    shape = part.shape
+    u, was_np = part.device().apply(f, variant)
+    if was_np:
+        return from_device(u, True, shape)
+    return u.reshape(f.shape) if hasattr(f, "shape") else u
+
+
+def prec_ud(part: Partition, f):
+    return _apply(part, f, "ud")
+
+
+def prec_x(part: Partition, f, parallel: bool = False):
+    """X sweep; the two half-sweep fronts always run concurrently on the device
+    (``parallel`` is accepted for drop-in compatibility; results are identical)."""
+    if part.J % 2 != 0:
+        raise ValueError(f"X-sweep needs an even subdomain count, got {part.J}")
+    return _apply(part, f, "x")
+
+
+@dataclass
+class SweepingPreconditioner:
+    part: Partition
+    variant: str = "ud"
+    cells: object = None
+    parallel: bool = False
+
+    def __post_init__(self):
+        if self.variant not in ("ud", "x", "nx"):
+            raise ValueError(f"unknown sweep variant {self.variant!r}")
+        if self.variant == "x" and self.part.J % 2 != 0:
+            raise ValueError(f"X-sweep needs an even subdomain count, got {self.part.J}")
+        if self.variant == "nx":
+            raise ValueError("NX sweep is not implemented on the device (out of scope, "
+                             "SURVEY 8(f))")
+
+    def __call__(self, f):
+        flat = np.ndim(f) == 1 if not hasattr(f, "dim") else f.dim() == 1
+        u = prec_x(self.part, f) if self.variant == "x" else prec_ud(self.part, f)
+        return u.reshape(-1) if flat else u

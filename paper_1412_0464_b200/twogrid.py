@@ -1,0 +1,282 @@
+"""Two-grid sweeping preconditioner (TGSP): drop-in for reference ``twogrid.py``.
+
+* ``SmootherConfig``, ``jacobi_smooth``                 :27-50
+* ``prolongation_matrix``, ``prolongate``, ``restrict`` :53-93
+* ``TwoGridCycle`` (vcycle, as_preconditioner)          :119-164
+* ``tgsp_apply``, ``vcycle``                            :167-176
+* ``SweepOptions``, ``build_two_grid``                  :179-229
+
+``build_two_grid`` assembles the hierarchy on the host (setup), uploads it and
+factorises the coarse slabs on the device.  Every cycle application is a
+chain of CUDA kernels (``hs_vcycle``): fused two-step pre-smoothing from zero,
+residual, h^d-scaled restriction, the X/UD sweep, prolongation-correction,
+post-smoothing.  Inputs may be numpy arrays (copied in/out) or torch CUDA
+complex128 tensors (zero-copy).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse as sp
+
+from .discretize import (StencilOperator, WaveModel, coarsen_wavenumber,
+                         wavenumber_cell_midpoints)
+from .mesh import CoarseningMap, Mesh, coarsen_mesh
+from .sweepdd import (HelmholtzLevel, Partition, SweepingPreconditioner, build_partition,
+                      coarse_level, fine_level)
+
+
+@dataclass(frozen=True)
+class SmootherConfig:
+    omega_jac: float = 0.8
+    nu: int = 3
+
+    def __post_init__(self):
+        if not 0.0 < self.omega_jac <= 1.0:
+            raise ValueError(f"relaxation weight must be in (0, 1], got {self.omega_jac}")
+        if self.nu < 0:
+            raise ValueError(f"smoothing step count must be >= 0, got {self.nu}")
+
+
+@dataclass(frozen=True)
+class SweepOptions:
+    w_dd: int = 4
+    s_dd: float = 20.0
+    variant: str = "ud"
+    n_cell: int | None = None
+    subdomains: int | None = None
+    parallel: bool = False
+
+
+def default_dd_strength(w_dd: int) -> float:
+    return 5.0 * w_dd
+
+
+def jacobi_smooth(op: StencilOperator, u, f, omega: float, steps: int):
+    """u <- u + omega D^-1 (f - A u), ``steps`` times, on the GPU."""
+    from .device import from_device, to_device
+    diag = op.diagonal()
+    zero = np.argwhere(diag == 0)
+    if zero.size:
+        raise ZeroDivisionError(f"zero operator diagonal at node {tuple(zero[0])}")
+    dev = op.device()
+    ut, was_np = to_device(u, op.n, dev.ctx)
+    ut = ut.clone()
+    ft, _ = to_device(f, op.n, dev.ctx)
+    dev.jacobi(ut, ft, omega, steps)
+    return from_device(ut, was_np, op.shape if was_np else None)
+
+
+# ---------------------------------------------------------------------------
+# transfers
+
+def _prolong_1d(fp, refined) -> sp.csr_matrix:
+    """1-D tent prolongation (host matrix; inspection / drop-in helper)."""
+    fp = np.asarray(fp)
+    n_f, n_c = int(fp[-1]) - 1, len(fp) - 2
+    rows = list(fp[1:n_c + 1] - 1)
+    cols = list(range(n_c))
+    vals = [1.0] * n_c
+    for cell in np.flatnonzero(np.asarray(refined)):
+        for cp in (cell, cell + 1):
+            if 1 <= cp <= n_c:
+                rows.append(fp[cell])
+                cols.append(cp - 1)
+                vals.append(0.5)
+    return sp.csr_matrix((vals, (rows, cols)), shape=(n_f, n_c))
+
+
+def prolongation_matrix(cmap: CoarseningMap) -> sp.csr_matrix:
+    p = _prolong_1d(cmap.fine_point_of_coarse[0], cmap.refined_cell[0])
+    for a in range(1, cmap.dim):
+        p = sp.kron(p, _prolong_1d(cmap.fine_point_of_coarse[a], cmap.refined_cell[a]),
+                    format="csr")
+    return p
+
+
+def prolongate(cmap: CoarseningMap, u_coarse):
+    """Coarse-to-fine tent interpolation on the GPU (field in, field out)."""
+    from .device import DeviceTransfer
+    t = DeviceTransfer(cmap)
+    was_np = not hasattr(u_coarse, "data_ptr")
+    out = t.prolong(np.asarray(u_coarse, dtype=complex) if was_np else u_coarse)
+    return out.reshape(t.fine_shape)
+
+
+def restrict(cmap: CoarseningMap, r_fine):
+    """Fine-to-coarse transfer P^T on the GPU."""
+    from .device import DeviceTransfer
+    t = DeviceTransfer(cmap)
+    was_np = not hasattr(r_fine, "data_ptr")
+    out = t.restrict(np.asarray(r_fine, dtype=complex) if was_np else r_fine)
+    return out.reshape(t.coarse_shape)
+
+
+# ---------------------------------------------------------------------------
+# coarse solvers
+
+class SweepCoarseSolver:
+    """One sweep application, never iterated."""
+
+    def __init__(self, prec: SweepingPreconditioner):
+        self.prec = prec
+        self.shape = prec.part.shape
+
+    def solve(self, rc):
+        return self.prec(rc.reshape(self.shape) if hasattr(rc, "reshape") else rc)
+
+
+class FineOperator:
+    """Device fine operator usable as ``apply_a`` (``fine_csr @ v``)."""
+
+    def __init__(self, op: StencilOperator):
+        self.op = op
+        self.shape = (op.n, op.n)
+
+    def __matmul__(self, v):
+        return self.op.device().apply(v)
+
+    def __call__(self, v):
+        return self @ v
+
+
+@dataclass
+class TwoGridCycle:
+    """Fixed linear V-cycle (pre-smoothing from zero), executed on the GPU."""
+
+    fine_op: StencilOperator
+    coarse_op: StencilOperator
+    cmap: CoarseningMap
+    smoother: SmootherConfig
+    coarse_solver: object
+    restrict_scale: float = 1.0
+    variant: str = "x"
+    fine_csr: object = None
+    _dev: object = field(default=None, repr=False)
+
+    def __post_init__(self):
+        if self.fine_csr is None:
+            self.fine_csr = FineOperator(self.fine_op)
+
+    @property
+    def p_matrix(self):
+        return prolongation_matrix(self.cmap)
+
+    @property
+    def r_matrix(self):
+        return self.p_matrix.T
+
+    def device(self):
+        if self._dev is None:
+            from .device import DeviceCycle, DeviceTransfer
+            fine = self.fine_op.device()
+            part = self.coarse_solver.prec.part
+            sweep = part.device()
+            self._dev = DeviceCycle(fine, DeviceTransfer(self.cmap, fine.ctx),
+                                    self.coarse_op.device(), sweep, self.smoother.omega_jac,
+                                    self.smoother.nu, self.restrict_scale, self.variant,
+                                    fine.ctx)
+        return self._dev
+
+    def vcycle(self, f):
+        from .device import from_device, to_device
+        dev = self.device()
+        ft, was_np = to_device(f, dev.n, dev.ctx)
+        u = dev.vcycle_dev(ft)
+        if was_np:
+            return from_device(u, True, self.fine_op.shape)
+        return u.reshape(f.shape)
+
+    def as_preconditioner(self):
+        dev_cycle = self
+
+        class _Prec:
+            cycle = dev_cycle
+
+            def __call__(self, v):
+                out = dev_cycle.vcycle(v)
+                return out.reshape(-1)
+
+        return _Prec()
+
+
+def vcycle(cycle: TwoGridCycle, f):
+    return cycle.vcycle(f)
+
+
+def tgsp_apply(cycle: TwoGridCycle, f):
+    if not isinstance(cycle.coarse_solver, SweepCoarseSolver):
+        raise ValueError("tgsp_apply needs a cycle with a sweeping coarse solver")
+    return cycle.vcycle(f)
+
+
+@dataclass
+class HostHierarchy:
+    """Everything build_two_grid assembles on the host (the device's inputs)."""
+
+    mesh: Mesh
+    fine_op: StencilOperator
+    coarse_op: StencilOperator
+    cmap: CoarseningMap
+    clevel: HelmholtzLevel
+    partition: Partition
+    smoother: SmootherConfig
+    sweep: SweepOptions
+    restrict_scale: float
+
+    @property
+    def beta(self):
+        return self.partition.beta
+
+    @property
+    def beta_tilde(self):
+        return self.partition.beta_tilde
+
+    @property
+    def slabs(self):
+        return [(sd.pt_lo, sd.pt_hi, sd.op) for sd in self.partition.subs]
+
+
+def build_hierarchy(mesh: Mesh, model: WaveModel, fine_op=None, smoother=None, sweep=None,
+                    table=None, device=True, keep_slab_ops=True) -> HostHierarchy:
+    """Host assembly of the TGSP hierarchy (reference twogrid.py:196-229)."""
+    flevel = fine_level(mesh, model, fine_op)
+    mesh_c, cmap = coarsen_mesh(mesh)
+    model_c = WaveModel(model.omega, coarsen_wavenumber(model.k, cmap))
+    k_cells = wavenumber_cell_midpoints(model.k, cmap)
+    clevel = coarse_level(mesh_c, cmap, model_c, k_cells=k_cells, table=table)
+    if smoother is None:
+        smoother = SmootherConfig(omega_jac=0.8 if mesh.dim == 2 else 0.6, nu=3)
+    sweep = sweep or SweepOptions()
+    part = build_partition(clevel, sweep.w_dd, sweep.s_dd, J=sweep.subdomains, device=device,
+                           keep_slab_ops=keep_slab_ops)
+    h = float(mesh.spacing[0][0])
+    return HostHierarchy(mesh, flevel.op, clevel.op, cmap, clevel, part, smoother, sweep,
+                         h ** mesh.dim)
+
+
+def build_two_grid(mesh: Mesh, model: WaveModel, fine_op: StencilOperator | None = None,
+                   smoother: SmootherConfig | None = None, coarse: str = "exact",
+                   sweep: SweepOptions | None = None, table=None, keep_slab_ops=True):
+    """Assemble the two-grid hierarchy; returns (cycle, coarse level).
+
+    ``coarse="sweep"`` is the TGSP path (device).  ``coarse="exact"`` (a
+    sparse direct coarse solve) is out of this build's scope.
+    """
+    if coarse == "exact":
+        raise ValueError("coarse solver 'exact' is outside the GPU path; use coarse='sweep'")
+    if coarse != "sweep":
+        raise ValueError(f"coarse solver must be 'exact' or 'sweep', got {coarse!r}")
+    sweep = sweep or SweepOptions()
+    if sweep.variant not in ("ud", "x"):
+        raise ValueError(f"sweep variant {sweep.variant!r} is not implemented on the device")
+    hh = build_hierarchy(mesh, model, fine_op, smoother, sweep, table,
+                         keep_slab_ops=keep_slab_ops)
+    prec = SweepingPreconditioner(hh.partition, sweep.variant, parallel=sweep.parallel)
+    cycle = TwoGridCycle(hh.fine_op, hh.coarse_op, hh.cmap, hh.smoother,
+                         SweepCoarseSolver(prec), restrict_scale=hh.restrict_scale,
+                         variant=sweep.variant)
+    cycle.hierarchy = hh
+    return cycle, hh.clevel

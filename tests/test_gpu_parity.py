@@ -1,0 +1,211 @@
+"""GPU parity: the CUDA path (through libhsweep's C ABI) vs the reference's
+golden vectors and the CPU oracle on the same seeded inputs.
+
+Tolerances: operator apply / smoother / transfers 1e-13 relative L2
+(complex128 rounding only); sweeps 1e-11; TGSP apply 1e-10 (north_star);
+GMRES iteration count +-1 and final true relative residual <= 1e-6.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import CASES, SOLVED, c1_anchors, crand, load_case, rel
+from cases import case, hierarchy, point_rhs
+
+pytestmark = pytest.mark.gpu
+
+
+def _build(name):
+    import paper_1412_0464_b200 as hb
+    mesh, model, fine_op, sm, sw = case(name)
+    if mesh.dim == 3:
+        return None
+    cycle, clevel = hb.build_two_grid(mesh, model, fine_op=fine_op, smoother=sm,
+                                      coarse="sweep", sweep=sw)
+    return cycle
+
+
+@pytest.fixture(scope="module", params=CASES)
+def golden(request):
+    return request.param, load_case(request.param)
+
+
+def test_stencil_apply(golden):
+    from paper_1412_0464_b200.device import DeviceStencil
+    _, d = golden
+    fine = DeviceStencil(d["fine_shape"], d["fine_offsets"], d["fine_coeffs"])
+    coarse = DeviceStencil(d["coarse_shape"], d["coarse_offsets"], d["coarse_coeffs"])
+    assert rel(fine.apply(d["probe_x"]), d["apply_fine"]) < 1e-13
+    assert rel(coarse.apply(d["probe_xc"]), d["apply_coarse"]) < 1e-13
+
+
+def test_residual_and_jacobi(golden):
+    import torch
+    from paper_1412_0464_b200.device import DeviceStencil, to_device
+    _, d = golden
+    fine = DeviceStencil(d["fine_shape"], d["fine_offsets"], d["fine_coeffs"])
+    r = fine.residual(d["probe_f"], d["probe_x"]).cpu().numpy()
+    assert rel(r, d["probe_f"].ravel() - d["apply_fine"].ravel()) < 1e-13
+    u, _ = to_device(d["probe_x"], fine.n)
+    f, _ = to_device(d["probe_f"], fine.n)
+    u = u.clone()
+    fine.jacobi(u, f, float(d["omega_jac"]), 2)
+    assert rel(u.cpu().numpy(), d["jacobi2"]) < 1e-13
+    # pre-smoothing from zero (fused two-step kernel) vs the oracle's loop
+    from oracle import tgsp_oracle as orc
+    op = orc.Op(d["fine_offsets"], d["fine_coeffs"])
+    for steps in (1, 2, 3):
+        z = torch.zeros_like(u)
+        fine.jacobi(z, f, float(d["omega_jac"]), steps, u_is_zero=True)
+        ref = orc.jacobi(op, np.zeros(op.shape, complex), d["probe_f"], float(d["omega_jac"]),
+                         steps)
+        assert rel(z.cpu().numpy(), ref) < 1e-13, steps
+
+
+def test_transfers(golden):
+    from paper_1412_0464_b200.device import DeviceTransfer
+    from paper_1412_0464_b200.mesh import CoarseningMap
+    _, d = golden
+    dim = len(d["fine_shape"])
+    cmap = CoarseningMap(tuple(d[f"fp{a}"] for a in range(dim)),
+                         tuple(d[f"refined{a}"] for a in range(dim)), tuple([None] * dim))
+    t = DeviceTransfer(cmap)
+    assert rel(t.restrict(d["probe_f"], float(d["restrict_scale"])), d["restrict"]) < 1e-13
+    assert rel(t.prolong(d["probe_xc"]), d["prolong"]) < 1e-13
+
+
+def test_sweeps(golden):
+    name, d = golden
+    if len(d["fine_shape"]) == 3:
+        pytest.skip("3-D sweep: not on the device yet (DESIGN.md)")
+    import paper_1412_0464_b200 as hb
+    hh = hierarchy(name, device=True)
+    part = hh.partition
+    if part.J % 2 == 0:
+        assert rel(hb.prec_x(part, d["probe_xc"]), d["sweep_x"]) < 1e-11
+    assert rel(hb.prec_ud(part, d["probe_xc"]), d["sweep_ud"]) < 1e-11
+
+
+def test_tgsp_apply(golden):
+    name, d = golden
+    cycle = _build(name)
+    if cycle is None:
+        pytest.skip("3-D sweep: not on the device yet")
+    import paper_1412_0464_b200 as hb
+    out = hb.tgsp_apply(cycle, d["tgsp_z"])
+    assert rel(out, d["tgsp_out"]) < 1e-10
+
+
+@pytest.mark.parametrize("name", SOLVED)
+def test_gmres_iterations(name):
+    import paper_1412_0464_b200 as hb
+    d = load_case(name)
+    cycle = _build(name)
+    mesh = case(name)[0]
+    f = point_rhs(mesh)
+    for orth in ("cgs2", "mgs"):
+        u, rep = hb.gmres(cycle.fine_csr, cycle.as_preconditioner(), f.ravel(),
+                          hb.GmresConfig(tol=1e-6, max_iter=200, restart=20), orth=orth)
+        assert abs(rep.iterations - int(d["gmres_iterations"])) <= 1, orth
+        assert rep.converged
+        res = np.linalg.norm(f.ravel() - cycle.fine_csr @ u) / np.linalg.norm(f)
+        assert res <= 1e-6, (orth, res)
+        assert rel(u, d["gmres_u"]) < 1e-5
+
+
+def test_c1_config_anchors():
+    """BASELINE configs[0]: |tgsp_apply(z)| and sampled entries vs the reference,
+    GMRES(20) iteration count vs the reference (9)."""
+    import paper_1412_0464_b200 as hb
+    from paper_1412_0464_b200.configs import config
+    a = c1_anchors()
+    p = config(0)
+    cycle, _ = hb.build_two_grid(p.mesh, p.model, smoother=hb.SmootherConfig(p.omega_jac, p.nu),
+                                 coarse="sweep",
+                                 sweep=hb.SweepOptions(p.w_dd, p.s_dd, "x",
+                                                       subdomains=p.subdomains))
+    rng = np.random.default_rng(0)
+    z = rng.standard_normal(p.mesh.unknowns) + 1j * rng.standard_normal(p.mesh.unknowns)
+    t = hb.tgsp_apply(cycle, z)
+    nrm = a["x"]["tgsp_norm"]
+    assert abs(np.linalg.norm(t) - nrm) <= 1e-10 * nrm
+    idx = np.array(a["x"]["tgsp_sample_idx"])
+    ref = np.array(a["x"]["tgsp_sample_re"]) + 1j * np.array(a["x"]["tgsp_sample_im"])
+    assert np.linalg.norm(t.ravel()[idx] - ref) <= 1e-10 * np.linalg.norm(ref)
+    u, rep = hb.gmres(cycle.fine_csr, cycle.as_preconditioner(), p.f[0].ravel(),
+                      hb.GmresConfig(p.tol, p.max_iter, p.restart))
+    assert abs(rep.iterations - a["x"]["iterations"]) <= 1 and rep.converged
+    res = np.linalg.norm(p.f[0].ravel() - cycle.fine_csr @ u) / np.linalg.norm(p.f[0])
+    assert res <= 1e-6
+
+
+def test_tgsp_vs_oracle_larger():
+    """C2 recipe at 1/4 size (wedge 256^2 + PML): GPU vs oracle, seeded input."""
+    import paper_1412_0464_b200 as hb
+    from paper_1412_0464_b200.configs import config
+    from oracle import tgsp_oracle as orc
+    p = config(1, scale=4)
+    hh = hb.build_hierarchy(p.mesh, p.model, None, hb.SmootherConfig(p.omega_jac, p.nu),
+                            hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains))
+    cycle, _ = hb.build_two_grid(p.mesh, p.model, smoother=hh.smoother, coarse="sweep",
+                                 sweep=hh.sweep)
+    tg = orc.from_hierarchy(hh)
+    z = crand(np.random.default_rng(5), p.mesh.unknowns)
+    assert rel(hb.tgsp_apply(cycle, z), tg.vcycle(z)) < 1e-10
+    # UD variant through the same kernels
+    assert rel(hb.prec_ud(hh.partition, z[:hh.coarse_op.shape[0], :hh.coarse_op.shape[1]]),
+               tg.part.prec_ud(z[:hh.coarse_op.shape[0], :hh.coarse_op.shape[1]])) < 1e-11
+
+
+def test_tgsp_linear_and_deterministic(rng):
+    import paper_1412_0464_b200 as hb
+    cycle = _build("wedge2d")
+    shape = cycle.fine_op.shape
+    f1, f2 = crand(rng, shape), crand(rng, shape)
+    lhs = hb.tgsp_apply(cycle, f1 + f2)
+    rhs = hb.tgsp_apply(cycle, f1) + hb.tgsp_apply(cycle, f2)
+    assert np.abs(lhs - rhs).max() < 1e-12 * np.abs(rhs).max()
+    assert np.array_equal(hb.tgsp_apply(cycle, f1), hb.tgsp_apply(cycle, f1))
+
+
+def test_torch_inputs_zero_copy():
+    import torch
+    import paper_1412_0464_b200 as hb
+    d = load_case("pml2d")
+    cycle = _build("pml2d")
+    z = torch.from_numpy(d["tgsp_z"]).cuda()
+    out = hb.tgsp_apply(cycle, z)
+    assert isinstance(out, torch.Tensor) and out.is_cuda
+    assert rel(out.cpu().numpy(), d["tgsp_out"]) < 1e-10
+
+
+def test_error_classes():
+    import paper_1412_0464_b200 as hb
+    op = hb.StencilOperator((3,), {(0,): np.array([1.0, 0.0, 1.0])})
+    with pytest.raises(ZeroDivisionError, match="1"):
+        hb.jacobi_smooth(op, np.zeros(3, complex), np.ones(3, complex), 0.8, 1)
+    # singular slab -> zero pivot at factorisation time
+    from paper_1412_0464_b200.device import DeviceStencil, DeviceSweep
+    coarse = DeviceStencil((8, 4), [(0, 0)], np.ones((1, 32)))
+    slabs = [DeviceStencil((4, 4), [(0, 0)], np.zeros((1, 16))) for _ in range(2)]
+    with pytest.raises(ZeroDivisionError, match="zero pivot"):
+        DeviceSweep(coarse, 2, [0, 4, 8], [0, 3, 8], [1, 5], [4, 8], slabs)
+    import types
+    with pytest.raises(ValueError, match="even"):
+        hb.SweepingPreconditioner(types.SimpleNamespace(J=3), "x")
+
+
+def test_gmres_small_known_answers(rng):
+    import paper_1412_0464_b200 as hb
+    b = rng.standard_normal(20) + 0j
+    u, rep = hb.gmres(lambda v: v, None, b, hb.GmresConfig(tol=1e-10))
+    assert rep.iterations == 1 and rep.converged and np.allclose(u, b)
+    dd = np.array([1.0] * 10 + [3.0] * 10, dtype=complex)
+    b = rng.standard_normal(20) + 1j * rng.standard_normal(20)
+    u, rep = hb.gmres(lambda v: v * __import__("torch").from_numpy(dd).to(v.device), None, b,
+                      hb.GmresConfig(tol=1e-12))
+    assert rep.iterations == 2 and rep.converged
+    _, rep = hb.gmres(lambda v: v, None, np.zeros(5, complex))
+    assert rep.iterations == 0 and rep.converged
+    with pytest.raises(FloatingPointError):
+        hb.gmres(lambda v: v * float("nan"), None, b)
