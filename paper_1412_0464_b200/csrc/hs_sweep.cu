@@ -39,6 +39,21 @@ namespace hs {
 
 namespace {
 
+// Per-block-size geometry.  TM = padded slab thickness (16 or 32 layers).
+template <int TM>
+struct Geo {
+  static constexpr int FREC = TM * TM + 3 * TM;   // Dinv (swizzled) + 3 L diagonals
+  static constexpr int BREC = TM * TM + 12;       // H (swizzled) + 12 transmission coefs
+  static constexpr int G = TM == 16 ? 4 : 2;      // chain steps per ring slot
+  static constexpr int NSLOT = 4;                 // ring depth in slots
+  static constexpr int NH = 32 / TM;              // lanes sharing one row
+  static constexpr int CPL = TM / NH;             // columns per lane
+  static constexpr int SLOT_BYTES = G * (FREC * 16 + TM * 16 + 2 * 32);
+  static constexpr int SMEM = NSLOT * SLOT_BYTES + 4 * TM * 16 + NSLOT * 8 + 64;
+  static_assert(G * (BREC * 16 + TM * 16) <= SLOT_BYTES, "slot too small");
+  static_assert(SMEM <= 227 * 1024, "ring does not fit shared memory");
+};
+
 // ---------------------------------------------------------------------------
 // setup kernels
 
@@ -48,21 +63,25 @@ struct SlabInfo {
   int slot[3][3];          // (o0+1, o1+1) -> coefficient slot or -1
 };
 
+template <int TM>
 __device__ __forceinline__ int swz(int r, int c) { return r * TM + (c ^ (r & 7)); }
 
-// One CTA (256 threads, thread = (r, c)) factorises one slab sequentially in y.
-__global__ void __launch_bounds__(256)
+// One CTA (TM*TM threads, thread = (r, c)) factorises one slab sequentially in y.
+template <int TM>
+__global__ void __launch_bounds__(TM * TM)
 k_slab_factor(const SlabInfo* __restrict__ slabs, int M, double2* __restrict__ fwd_rec,
               double2* __restrict__ bwd_rec, unsigned long long* __restrict__ err) {
+  using Gm = Geo<TM>;
   const int s = blockIdx.x;
   const SlabInfo si = slabs[s];
   const int tid = threadIdx.x;
-  const int r = tid >> 4, c = tid & 15;
+  const int r = tid / TM, c = tid % TM;
   const int T = si.T;
   const int64_t n = (int64_t)T * M;
-  __shared__ double2 A[TM][TM + 1];
-  __shared__ double2 Inv[TM][TM + 1];
-  __shared__ double2 Hs[TM][TM + 1];
+  extern __shared__ __align__(16) unsigned char fsm[];
+  double2(*A)[TM + 1] = reinterpret_cast<double2(*)[TM + 1]>(fsm);
+  double2(*Inv)[TM + 1] = A + TM;
+  double2(*Hs)[TM + 1] = Inv + TM;
   __shared__ int piv_row;
   __shared__ double piv_abs;
 
@@ -84,8 +103,7 @@ k_slab_factor(const SlabInfo* __restrict__ slabs, int M, double2* __restrict__ f
       if (y > 0) {
         for (int k = r - 1; k <= r + 1; ++k) {
           if (k < 0 || k >= T) continue;
-          const double2 l = coef(k - r, -1, r, y);
-          d = csub(d, cmul(l, Hs[k][c]));
+          d = csub(d, cmul(coef(k - r, -1, r, y), Hs[k][c]));
         }
       }
     } else {
@@ -114,17 +132,15 @@ k_slab_factor(const SlabInfo* __restrict__ slabs, int M, double2* __restrict__ f
               ((unsigned long long)s << 40) | ((unsigned long long)(p * M + y) & 0xffffffffffull);
           atomicMin(err, code);
         }
-        if (tid == p * TM + p) A[p][p] = make_double2(1.0, 0.0);
+        if (r == p && c == p) A[p][p] = make_double2(1.0, 0.0);
         __syncthreads();
       } else if (pr != p) {
-        // swap rows p and pr (threads of row p do it)
         if (r == p) {
           double2 t = A[p][c]; A[p][c] = A[pr][c]; A[pr][c] = t;
           t = Inv[p][c]; Inv[p][c] = Inv[pr][c]; Inv[pr][c] = t;
         }
         __syncthreads();
       }
-      // eliminate column p: read phase
       const double2 app = A[p][p];
       const double2 apc = A[p][c], ipc = Inv[p][c];
       const double2 arp = A[r][p];
@@ -143,9 +159,8 @@ k_slab_factor(const SlabInfo* __restrict__ slabs, int M, double2* __restrict__ f
       Inv[r][c] = irc;
       __syncthreads();
     }
-    // forward record: Dinv (swizzled) + L diagonals
-    double2* fr = fwd_rec + ((int64_t)s * M + y) * FREC;
-    fr[swz(r, c)] = Inv[r][c];
+    double2* fr = fwd_rec + ((int64_t)s * M + y) * Gm::FREC;
+    fr[swz<TM>(r, c)] = Inv[r][c];
     if (c < 3) fr[TM * TM + c * TM + r] = (r < T) ? coef(c - 1, -1, r, y) : czero();
     // H_y = Dinv_y U_y, U_y[k][c] = coupling (k, y) -> (c, y+1)
     double2 h = czero();
@@ -157,7 +172,7 @@ k_slab_factor(const SlabInfo* __restrict__ slabs, int M, double2* __restrict__ f
     }
     __syncthreads();
     Hs[r][c] = h;
-    bwd_rec[((int64_t)s * M + y) * BREC + swz(r, c)] = h;
+    bwd_rec[((int64_t)s * M + y) * Gm::BREC + swz<TM>(r, c)] = h;
     __syncthreads();
   }
 }
@@ -172,11 +187,12 @@ struct ToutArgs {
 };
 
 // Outgoing transmission coefficients per (slab, y) into the backward records.
+template <int TM>
 __global__ void k_tout(ToutArgs a, double2* __restrict__ bwd_rec) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)a.J * a.M) return;
   const int s = (int)(idx / a.M), y = (int)(idx % a.M);
-  double2* out = bwd_rec + idx * BREC + TM * TM;
+  double2* out = bwd_rec + idx * Geo<TM>::BREC + TM * TM;
   auto cc = [&](int o0, int o1, int row) -> double2 {
     const int sl = a.slot[o0 + 1][o1 + 1];
     if (sl < 0 || y + o1 < 0 || y + o1 >= a.M) return czero();
@@ -184,7 +200,7 @@ __global__ void k_tout(ToutArgs a, double2* __restrict__ bwd_rec) {
   };
   const int pf = a.fwd_point[s], pb = a.bwd_point[s];
   for (int o = -1; o <= 1; ++o) {
-    out[0 + o + 1] = pf > 0 ? cc(1, o, pf - 1) : czero();   // A[b, b+1] block row b = p
+    out[0 + o + 1] = pf > 0 ? cc(1, o, pf - 1) : czero();   // A[b, b+1], b = p
     out[3 + o + 1] = pf > 0 ? cc(-1, o, pf) : czero();      // A[b+1, b]
     out[6 + o + 1] = pb > 0 ? cc(1, o, pb - 1) : czero();
     out[9 + o + 1] = pb > 0 ? cc(-1, o, pb) : czero();
@@ -194,6 +210,7 @@ __global__ void k_tout(ToutArgs a, double2* __restrict__ bwd_rec) {
 // ---------------------------------------------------------------------------
 // apply kernels
 
+template <int TM>
 __global__ void k_gather(const SweepTask* __restrict__ tasks, int first, int M,
                          const double2* __restrict__ src, double2* __restrict__ fdpre) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -206,11 +223,10 @@ __global__ void k_gather(const SweepTask* __restrict__ tasks, int first, int M,
   fdpre[((int64_t)t.fdslot * M + y) * TM + x] = v;
 }
 
-constexpr int G = 4;       // chain steps per ring slot
-constexpr int NSLOT = 4;   // ring depth in slots
-constexpr int SLOT_BYTES = G * (FREC * 16 + TM * 16 + 2 * 32);   // forward is the larger
-static_assert(G * (BREC * 16 + TM * 16) <= SLOT_BYTES, "slot too small");
-constexpr int FRONT_SMEM = NSLOT * SLOT_BYTES + 4 * TM * 16 + NSLOT * 8 + 64;
+__global__ void k_combine(double2* __restrict__ u, const double2* __restrict__ u2, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) u[i] = cadd(u[i], __ldg(u2 + i));
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -256,16 +272,20 @@ struct FrontArgs {
   const double2* fdpre;
   double2* tin;
   double2* zs;
-  double2* u;
+  double2* u[2];
   int M;
 };
 
 // One warp = one sequential chain of slab solves (a "front" of the sweep).
+template <int TM>
 __global__ void __launch_bounds__(32, 1) k_front(FrontArgs a) {
+  using Gm = Geo<TM>;
+  constexpr int FREC = Gm::FREC, BREC = Gm::BREC, G = Gm::G, NSLOT = Gm::NSLOT;
+  constexpr int CPL = Gm::CPL, SLOT_BYTES = Gm::SLOT_BYTES;
   extern __shared__ __align__(128) unsigned char smem[];
   const int front = blockIdx.x;
   const int lane = threadIdx.x;
-  const int x = lane & 15, hh = lane >> 4;
+  const int x = lane % TM, hh = lane / TM;
   const int M = a.M;
   unsigned char* ring = smem;
   double2* zb = (double2*)(smem + NSLOT * SLOT_BYTES);   // [2][TM] chain vector (double buffer)
@@ -278,10 +298,14 @@ __global__ void __launch_bounds__(32, 1) k_front(FrontArgs a) {
   }
   __syncwarp();
   uint32_t phase_bits = 0;      // parity per slot
+  const int ffirst = front ? a.ffirst[1] : a.ffirst[0];
+  const int fcount = front ? a.fcount[1] : a.fcount[0];
   double2* zs = a.zs + (int64_t)front * M * TM;
+  // lanes that turn outgoing traces into the consumer's sources
+  const int tl = lane - (TM == 16 ? 16 : 0);
 
-  for (int ti = 0; ti < a.fcount[front]; ++ti) {
-    const SweepTask t = a.tasks[a.ffirst[front] + ti];
+  for (int ti = 0; ti < fcount; ++ti) {
+    const SweepTask t = a.tasks[ffirst + ti];
     const double2* frec = a.fwd_rec + (int64_t)t.slab * M * FREC;
     const double2* brec = a.bwd_rec + (int64_t)t.slab * M * BREC;
     const double2* fdp = a.fdpre + (int64_t)t.fdslot * M * TM;
@@ -307,7 +331,7 @@ __global__ void __launch_bounds__(32, 1) k_front(FrontArgs a) {
     };
     if (lane == 0)
       for (int g = 0; g < min(NSLOT, ngroups); ++g) issue_f(g);
-    if (lane < 2 * TM) zb[lane] = czero();
+    for (int i = lane; i < 2 * TM; i += 32) zb[i] = czero();
     __syncwarp();
     int cur = 0;
     for (int g = 0; g < ngroups; ++g) {
@@ -341,13 +365,13 @@ __global__ void __launch_bounds__(32, 1) k_front(FrontArgs a) {
         __syncwarp();
         double2 acc0 = czero(), acc1 = czero();
 #pragma unroll
-        for (int q = 0; q < 8; q += 2) {
-          const int c0 = 8 * hh + q;
-          acc0 = cfma(rec[swz(x, c0)], rb[c0], acc0);
-          acc1 = cfma(rec[swz(x, c0 + 1)], rb[c0 + 1], acc1);
+        for (int q = 0; q < CPL; q += 2) {
+          const int c0 = CPL * hh + q;
+          acc0 = cfma(rec[swz<TM>(x, c0)], rb[c0], acc0);
+          acc1 = cfma(rec[swz<TM>(x, c0 + 1)], rb[c0 + 1], acc1);
         }
         double2 acc = cadd(acc0, acc1);
-        acc = cadd(acc, shfl_xor_c(acc, 16));
+        if (TM == 16) acc = cadd(acc, shfl_xor_c(acc, 16));
         if (hh == 0) {
           zb[cur * TM + x] = acc;
           zs[(int64_t)y * TM + x] = acc;
@@ -377,10 +401,9 @@ __global__ void __launch_bounds__(32, 1) k_front(FrontArgs a) {
     };
     if (lane == 0)
       for (int g = 0; g < min(NSLOT, ngroups); ++g) issue_b(g);
-    if (lane < 2 * TM) zb[lane] = czero();
+    for (int i = lane; i < 2 * TM; i += 32) zb[i] = czero();
     __syncwarp();
-    // transmission-out lanes 16..19: (coef block, trace row, sign, out buffer, component)
-    const int tl = lane - 16;
+    // transmission-out lanes: (coef block, trace row, sign, out buffer, component)
     int trow = -1, tsgn = 0, tcb = 0;
     double2* tout = nullptr;
     if (tl >= 0 && tl < 4) {
@@ -412,19 +435,19 @@ __global__ void __launch_bounds__(32, 1) k_front(FrontArgs a) {
         const double2* xp = zb + (cur ^ 1) * TM;   // x_{y+1}
         double2 acc0 = czero(), acc1 = czero();
 #pragma unroll
-        for (int q = 0; q < 8; q += 2) {
-          const int c0 = 8 * hh + q;
-          acc0 = cfma(rec[swz(x, c0)], xp[c0], acc0);
-          acc1 = cfma(rec[swz(x, c0 + 1)], xp[c0 + 1], acc1);
+        for (int q = 0; q < CPL; q += 2) {
+          const int c0 = CPL * hh + q;
+          acc0 = cfma(rec[swz<TM>(x, c0)], xp[c0], acc0);
+          acc1 = cfma(rec[swz<TM>(x, c0 + 1)], xp[c0 + 1], acc1);
         }
         double2 acc = cadd(acc0, acc1);
-        acc = cadd(acc, shfl_xor_c(acc, 16));
+        if (TM == 16) acc = cadd(acc, shfl_xor_c(acc, 16));
         const double2 xv = csub(zv[x], acc);
         if (hh == 0) zb[cur * TM + x] = xv;
         __syncwarp();
         if (hh == 0 && x >= ur0 && x < ur1) {
-          double2* up = a.u + (int64_t)(x + t.lo - 1) * M + y;
-          *up = cadd(*up, xv);
+          // each row of u is produced by exactly one task per pass: plain store
+          a.u[t.dst][(int64_t)(x + t.lo - 1) * M + y] = xv;
         }
         if (tout) {
           const double2 tr = zb[cur * TM + trow];
@@ -492,10 +515,11 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   for (int j = 0; j < J; ++j) {
     const Stencil* op = slabs[j];
     const int T = (int)(hi[j] - lo[j] + 1);
-    if (T > TM) {
+    if (T > 32) {
       delete s;
-      return set_error(c, HS_E_SHAPE, "slab thicker than 16 layers: not supported by the sweep");
+      return set_error(c, HS_E_SHAPE, "slab thicker than 32 layers: not supported by the sweep");
     }
+    if (T > 16) s->tm = 32;
     if (op->dim != 2 || op->shape[0] != T || op->shape[1] != M) {
       delete s;
       return set_error(c, HS_E_SHAPE, "slab operator shape does not match the partition");
@@ -506,6 +530,9 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     if (j + 1 < J) fpt[j] = (int)beta[j + 1];   // out2 of slab j+1 (1-based) at beta_{j+1}
     if (j > 0) bpt[j] = (int)bt[j];             // out4 at beta~_{j}  (slab index j = (j+1)-1)
   }
+  const int TM = s->tm;
+  const int FREC = TM == 16 ? Geo<16>::FREC : Geo<32>::FREC;
+  const int BREC = TM == 16 ? Geo<16>::BREC : Geo<32>::BREC;
   const size_t frec_bytes = (size_t)J * M * FREC * sizeof(double2);
   const size_t brec_bytes = (size_t)J * M * BREC * sizeof(double2);
   s->factor_bytes = (long long)(frec_bytes + brec_bytes);
@@ -536,7 +563,18 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   HS_TRY(cudaMemcpyAsync(d_pts + J, bpt.data(), J * sizeof(int), cudaMemcpyHostToDevice,
                          c->stream), "upload");
   HS_TRY(cudaMemsetAsync(d_err, 0xff, sizeof(unsigned long long), c->stream), "memset");
-  k_slab_factor<<<J, 256, 0, c->stream>>>(d_info, M, s->fwd_rec, s->bwd_rec, d_err);
+  {
+    const int fsmem = 3 * TM * (TM + 1) * (int)sizeof(double2);
+    if (TM == 16) {
+      k_slab_factor<16><<<J, 256, fsmem, c->stream>>>(d_info, M, s->fwd_rec, s->bwd_rec, d_err);
+    } else {
+      HS_TRY(cudaFuncSetAttribute(k_slab_factor<32>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem),
+             "factor smem");
+      k_slab_factor<32><<<J, 1024, fsmem, c->stream>>>(d_info, M, s->fwd_rec, s->bwd_rec,
+                                                        d_err);
+    }
+  }
   c->launches++;
   HS_TRY(cudaGetLastError(), "slab factor kernel");
   ToutArgs ta{};
@@ -548,7 +586,10 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   ta.fwd_point = d_pts;
   ta.bwd_point = d_pts + J;
   const int64_t ntout = (int64_t)J * M;
-  k_tout<<<(unsigned)((ntout + 255) / 256), 256, 0, c->stream>>>(ta, s->bwd_rec);
+  if (TM == 16)
+    k_tout<16><<<(unsigned)((ntout + 255) / 256), 256, 0, c->stream>>>(ta, s->bwd_rec);
+  else
+    k_tout<32><<<(unsigned)((ntout + 255) / 256), 256, 0, c->stream>>>(ta, s->bwd_rec);
   c->launches++;
   HS_TRY(cudaGetLastError(), "tout kernel");
   unsigned long long err = 0;
@@ -656,6 +697,7 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
         const int f0 = (int)T.size();
         for (auto t : fr) {
           t.fdslot = slot++;
+          t.dst = src;
           T.push_back(t);
         }
         rs.push_back({f0, (int)fr.size()});
@@ -682,10 +724,10 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
         fl.nfront++;
         for (int i = r.first; i < r.first + r.second; ++i) {
           const SweepTask& t = T[i];
-          // records + rhs + z round trip + transmission streams + u read-modify-write
+          // records + rhs + z round trip + transmission streams + u stores
           double b = (double)M * 16.0 * (FREC + BREC + 3 * TM);
           b += (double)M * 32.0 * ((t.tin1 >= 0) + (t.tin3 >= 0) + (t.out2 >= 0) + (t.out4 >= 0));
-          b += (double)M * 32.0 * (t.tb - t.ta);
+          b += (double)M * 16.0 * (t.tb - t.ta);
           fl.bytes += b;
         }
       }
@@ -696,7 +738,6 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   // ---- UD: forward 1..J on f; g = f - A u; backward J..1 on g ----
   {
     std::vector<SweepLaunch>& plan = s->plan[HS_VARIANT_UD];
-    plan.push_back(SweepLaunch{SweepLaunch::kZero});
     std::vector<SweepTask> F, B;
     fwd_chain(1, J, F);
     clear_placeholders(F);
@@ -705,12 +746,12 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     emit_pass(plan, 0, {{F}});
     plan.push_back(SweepLaunch{SweepLaunch::kResidual});
     emit_pass(plan, 1, {{B}});
+    plan.push_back(SweepLaunch{SweepLaunch::kCombine});
     s->has_plan[HS_VARIANT_UD] = true;
   }
   // ---- X: simultaneous half sweeps meeting at jm = J/2 + 1 ----
   if (J % 2 == 0) {
     std::vector<SweepLaunch>& plan = s->plan[HS_VARIANT_X];
-    plan.push_back(SweepLaunch{SweepLaunch::kZero});
     const int jm = J / 2 + 1;
     std::vector<SweepTask> F, B, MI;
     fwd_chain(1, jm - 1, F);
@@ -735,6 +776,7 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     clear_placeholders(FF);
     MO.push_back(mo);
     emit_pass(plan, 1, {{MO}, {BB, FF}});
+    plan.push_back(SweepLaunch{SweepLaunch::kCombine});
     s->has_plan[HS_VARIANT_X] = true;
   }
 #undef HS_TRY
@@ -748,8 +790,12 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     e = cudaMalloc((void**)&s->tin, (size_t)std::max(1, ntin) * M * 2 * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->zs, (size_t)2 * M * TM * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->g, (size_t)s->n0 * M * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&s->u2, (size_t)s->n0 * M * sizeof(double2));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, FRONT_SMEM);
+    e = TM == 16 ? cudaFuncSetAttribute(k_front<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        Geo<16>::SMEM)
+                 : cudaFuncSetAttribute(k_front<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        Geo<32>::SMEM);
   if (e != cudaSuccess) {
     sweep_destroy(s);
     return check_cuda(c, e, "sweep buffers");
@@ -766,6 +812,7 @@ void sweep_destroy(Sweep* s) {
   cudaFree(s->tin);
   cudaFree(s->zs);
   cudaFree(s->g);
+  cudaFree(s->u2);
   cudaFree(s->d_tasks);
   delete s;
 }
@@ -776,17 +823,26 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u) {
                      variant == HS_VARIANT_X ? "X-sweep needs an even subdomain count"
                                              : "unknown sweep variant");
   const int M = s->M;
-  const size_t nbytes = (size_t)s->n0 * M * sizeof(double2);
+  const int TM = s->tm;
   for (const SweepLaunch& L : s->plan[variant]) {
     switch (L.kind) {
-      case SweepLaunch::kZero:
-        HS_CUDA(c, cudaMemsetAsync(u, 0, nbytes, c->stream), "zero u");
+      case SweepLaunch::kCombine: {
+        // u = u_pass1 + u_pass2 (the order of the reference's u[ta:tb] += ud)
+        const int64_t n = (int64_t)s->n0 * M;
+        ProfScope ps(c, K_SWEEP_GATHER, 48.0 * n);
+        k_combine<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(u, s->u2, n);
+        HS_LAUNCH_CHECK(c, "combine kernel");
         break;
+      }
       case SweepLaunch::kGather: {
         dim3 grid((unsigned)((M * TM + 255) / 256), (unsigned)L.count);
         ProfScope ps(c, K_SWEEP_GATHER, L.bytes);
-        k_gather<<<grid, 256, 0, c->stream>>>(s->d_tasks, L.first, M, L.src ? s->g : f,
-                                              s->fdpre);
+        if (TM == 16)
+          k_gather<16><<<grid, 256, 0, c->stream>>>(s->d_tasks, L.first, M, L.src ? s->g : f,
+                                                    s->fdpre);
+        else
+          k_gather<32><<<grid, 256, 0, c->stream>>>(s->d_tasks, L.first, M, L.src ? s->g : f,
+                                                    s->fdpre);
         HS_LAUNCH_CHECK(c, "gather kernel");
         break;
       }
@@ -807,10 +863,14 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u) {
         fa.fdpre = s->fdpre;
         fa.tin = s->tin;
         fa.zs = s->zs;
-        fa.u = u;
+        fa.u[0] = u;
+        fa.u[1] = s->u2;
         fa.M = M;
         ProfScope ps(c, K_SWEEP_FRONT, L.bytes);
-        k_front<<<L.nfront, 32, FRONT_SMEM, c->stream>>>(fa);
+        if (TM == 16)
+          k_front<16><<<L.nfront, 32, Geo<16>::SMEM, c->stream>>>(fa);
+        else
+          k_front<32><<<L.nfront, 32, Geo<32>::SMEM, c->stream>>>(fa);
         HS_LAUNCH_CHECK(c, "front kernel");
         break;
       }

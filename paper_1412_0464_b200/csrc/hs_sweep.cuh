@@ -4,10 +4,8 @@
 namespace hs {
 
 // Slab solve geometry: every slab is a block-tridiagonal system along the face
-// axis y (M blocks) whose blocks are TM x TM (thin sweep-axis layers, padded).
-constexpr int TM = 16;            // max slab thickness (layers along the sweep axis)
-constexpr int FREC = TM * TM + 3 * TM;   // forward record: Dinv (swizzled) + L diagonals
-constexpr int BREC = TM * TM + 12;       // backward record: H (swizzled) + transmission-out coefs
+// axis y (M blocks) whose blocks are tm x tm (thin sweep-axis layers padded to
+// tm = 16 or 32; see Geo<TM> in hs_sweep.cu for the record layouts).
 
 // One slab solve of a schedule (subdom_solve, sweepdd.py:236-268).
 struct SweepTask {
@@ -21,10 +19,11 @@ struct SweepTask {
   int tin3, row3;  // backward transmission in
   int out2, orow2; // forward trace out -> consumer's tin buffer, slab-local trace row
   int out4, orow4; // backward trace out
+  int dst;         // 0: pass-1 solution u, 1: pass-2 buffer u2 (summed at the end)
 };
 
 struct SweepLaunch {
-  enum Kind { kZero, kGather, kFront, kResidual } kind;
+  enum Kind { kCombine, kGather, kFront, kResidual } kind;
   int src;                  // gather: 0 = f, 1 = g
   int first, count;         // task range (gather: all tasks of the pass)
   int nfront;
@@ -34,13 +33,15 @@ struct SweepLaunch {
 
 struct Sweep {
   int J = 0, M = 0, n0 = 0;
+  int tm = 16;                  // padded block size (16 or 32)
   const Stencil* coarse = nullptr;
   double2* fwd_rec = nullptr;   // [J][M][FREC]
   double2* bwd_rec = nullptr;   // [J][M][BREC]
-  double2* fdpre = nullptr;     // [max pass tasks][M][TM]
+  double2* fdpre = nullptr;     // [max pass tasks][M][tm]
   double2* tin = nullptr;       // [ntin][M][2]
-  double2* zs = nullptr;        // [2][M][TM]
+  double2* zs = nullptr;        // [2][M][tm]
   double2* g = nullptr;         // [n0*M] mid-sweep residual
+  double2* u2 = nullptr;        // [n0*M] second-pass contributions
   SweepTask* d_tasks = nullptr;
   std::vector<SweepTask> tasks;
   std::vector<SweepLaunch> plan[2];   // by variant (UD, X)
