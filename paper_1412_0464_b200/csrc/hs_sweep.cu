@@ -287,7 +287,6 @@ struct SolveArgs {
   double2* trace;          // [ntrace][2][M]
   double2* u[2];
   unsigned long long* dbg;   // optional phase timestamps (HS_SWEEP_TRACE)
-  int flags;                 // experiment switches (HS_SWEEP_FLAGS)
 };
 
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
@@ -585,7 +584,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_bcr_solve(SolveArgs a) {
     if (m1) bulk_g2s(slot + TM2, m1, mb, bar);
     seq[sl] = i;
   };
-  if (threadIdx.x == 0 && !(a.flags & 32))
+  if (threadIdx.x == 0)
     for (int i = 0; i < total && i < NS; ++i) issue(i);
   if (L == 0 && rank == 0 && warp == 0 && lane == 0 && fcount) {
     // M == 1: the only block is the top; its Dinv is read directly
@@ -614,7 +613,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_bcr_solve(SolveArgs a) {
     stamp(ti, 0);
     const SweepTask t = a.tasks[ffirst + ti];
     if (threadIdx.x == 0 && ti + 1 < fcount)
-      if (!(a.flags & 1)) prefetch_slab<TM>(a, a.tasks[ffirst + ti + 1].slab, Y0, Y1);
+      prefetch_slab<TM>(a, slabs[ti + 1], Y0, Y1);
     // ---- right-hand side of the owned blocks (restriction + transmission)
     for (int yl = warp * YPW + hh; yl < nloc; yl += kWarps * YPW) {
       const int y = Y0 + yl;
@@ -643,7 +642,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_bcr_solve(SolveArgs a) {
       const int l = ph_level(p), s = 1 << l;
       const int f0 = ph_first(p), st = ph_step(p);
       const int cnt = pfx[p + 1] - pfx[p];
-      for (int j = warp; j < ((a.flags & 32) ? 0 : cnt); j += kWarps) {
+      for (int j = warp; j < cnt; j += kWarps) {
         const int y = f0 + j * st;
         const int i = base + pfx[p] + j;
         // a parity wait is only valid once the slot's previous use completed:
@@ -683,7 +682,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_bcr_solve(SolveArgs a) {
         __syncwarp();
         if (j == 0) stamp2(ti, p, 3);
         if (i + NS < total) {
-          if ((a.flags & 2) || i + NS < base + pfx[p + 1]) {   // needed within this phase: refill now
+          if (i + NS < base + pfx[p + 1]) {   // needed within this phase: refill now
             if (lane == 0) {
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
               issue(i + NS);
@@ -1146,7 +1145,8 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u) {
           cudaMemsetAsync(dbg, 0, 16 * 512 * sizeof(unsigned long long), c->stream);
         }
         a.dbg = dbg;
-        a.flags = getenv("HS_SWEEP_FLAGS") ? atoi(getenv("HS_SWEEP_FLAGS")) : 0;        ProfScope ps(c, K_SWEEP_FRONT, Lh.bytes);
+
+        ProfScope ps(c, K_SWEEP_FRONT, Lh.bytes);
         cudaError_t e = s->tm == 16 ? launch_solve<16>(a, Lh.nfront, c->stream)
                                     : launch_solve<32>(a, Lh.nfront, c->stream);
         if (e != cudaSuccess) return check_cuda(c, e, "sweep solve launch");
