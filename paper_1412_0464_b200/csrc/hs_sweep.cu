@@ -1,5 +1,6 @@
-// Coarse-level sweeping preconditioner on B200: slab solves by block cyclic
-// reduction (BCR) over the face axis, one thread-block cluster per sweep front.
+// Coarse-level sweeping preconditioner on B200: partitioned slab solves
+// (SPIKE with block cyclic reduction inside each partition), one thread-block
+// cluster per sweep front.
 //
 // Reference: build_partition + Factorization (sweepdd.py:192-218,
 // sparselin.py:40-68), subdom_solve (sweepdd.py:236-268), TransmissionMatrix
@@ -9,26 +10,33 @@
 // Slab system.  A slab of T <= 32 layers along the sweep axis and M face points
 // is block tridiagonal along the face: block y couples to y-1 (L_y), y (D_y),
 // y+1 (U_y), blocks tm x tm (tm = 16 or 32, T padded with identity rows).
-// SuperLU's sparse LU is a chain of ~2*M*T dependent rows per solve; a block
-// Thomas chain still has 2M dependent steps.  BCR has 2*ceil(log2 M)
-// dependent levels, each a batch of independent dense tm x tm mat-vecs:
-//   level l (stride s = 2^l): blocks y = odd multiples of s are eliminated,
-//     y_y = Dinv_y f_y;  kept blocks (even multiples) update
-//     f_y -= alpha_y f_{y-s} + gamma_y f_{y+s}   (alpha = L Dinv_{y-s}, gamma = U Dinv_{y+s})
-//   top: x_0 = Dinv_0 f_0
-//   back substitution, level L-1 .. 0: x_y = y_y - (Dinv L)_y x_{y-s} - (Dinv U)_y x_{y+s}.
-// Setup computes every level's Schur complements on the device, batched over
-// all slabs (k_bcr_elim / k_bcr_keep per level; Gauss-Jordan with partial
-// pivoting inside each block, no pivoting across blocks -- SURVEY H2).
+// SuperLU's sparse LU is a chain of ~2*M*T dependent rows per solve.  Here the
+// face is cut into C chunks, one per CTA of a cluster (C <= 16):
+//   A x = f  <=>  x_k = g_k - W_k x_{first(k)-1} - V_k x_{last(k)+1},
+//   g_k = A_k^{-1} f_k (chunk-local), W_k / V_k the chunk's spikes
+//   (A_k^{-1} applied to the couplings leaving the chunk).
+// 1. every CTA solves its chunk by block cyclic reduction (BCR): 2*ceil(log2 m)
+//    phases of independent tm x tm mat-vecs separated by __syncthreads only;
+// 2. the chunk-end values of g (the "tips") are pushed to every CTA (DSMEM
+//    stores) and one cluster barrier later each CTA applies its two rows of the
+//    precomputed inverse of the 2(C-1)-block interface system (R) to them;
+// 3. x_k = g_k - W_k alpha - V_k beta for every block (independent mat-vecs).
+// Two cluster barriers per slab instead of one per BCR level.
 //
-// Apply: one cluster of C CTAs per front (C <= 16, non-portable size), CTA k
-// owns face points [kM/C, (k+1)M/C); the right-hand side / solution blocks
-// live in shared memory and neighbours in other CTAs are read through DSMEM;
-// levels are separated by cluster barriers.  Dense blocks are stored
-// "lane-major" so each of a warp's 16-byte loads is one contiguous 512-byte
-// line.  Transmission (sweepdd.py:113-118) is applied by the consumer when it
-// builds its right-hand side, from the producer's two trace rows in global
-// memory and the global coarse operator's interface couplings.
+// Setup (all on the device, batched over slabs and chunks): chunk-local BCR
+// Schur complements (k_bcr_elim / k_bcr_keep per level, Gauss-Jordan with
+// partial pivoting inside each block, no pivoting across blocks -- SURVEY H2),
+// spikes by a block-Thomas pass per chunk (k_spikes), and R by block-Thomas
+// elimination of the interface system with identity right-hand sides
+// (k_reduced).
+//
+// Apply: every matrix a CTA needs (BCR records, R column blocks, spikes) is
+// streamed into a shared-memory ring by TMA bulk copies in consumption order,
+// up to NSLOT items ahead, also across slab solves; vectors stay in shared
+// memory.  Dense blocks are stored "lane-major" so a warp's 16-byte loads are
+// contiguous 512-byte lines.  Transmission (sweepdd.py:113-118) is applied by
+// the consumer when it builds its right-hand side, from the producer's two
+// trace rows in global memory and the global operator's interface couplings.
 
 #include "hs_common.cuh"
 #include "hs_sweep.cuh"
@@ -44,9 +52,11 @@ namespace hs {
 
 namespace {
 
-constexpr int kMaxLevels = 20;
-constexpr int kWarps = 16;
-constexpr int kMaxTasks = 1024;   // slab solves per front per launch
+constexpr int kMaxLevels = 16;     // local BCR levels: chunks up to 65536 points
+constexpr int kWarps = 16;        // 15 consumer warps + 1 TMA producer warp
+constexpr int kCW = kWarps - 1;
+constexpr int kMaxC = 16;
+constexpr int kMaxTasks = 1024;    // slab solves per front per launch
 
 template <int TM>
 struct Geo {
@@ -67,14 +77,26 @@ struct SlabInfo {
   int slot[3][3];          // (o0+1, o1+1) -> coefficient slot or -1
 };
 
-// ---------------------------------------------------------------------------
-// setup kernels (thread (r, c) of a tm x tm block; batched over slabs)
+// chunk geometry: chunk k covers face points [k M / C, (k+1) M / C)
+struct Chunks {
+  int M, C, L, kstride;
+  int koff[kMaxLevels];
+  __host__ __device__ int y0(int k) const { return (int)((int64_t)k * M / C); }
+  __host__ __device__ int len(int k) const { return y0(k + 1) - y0(k); }
+};
 
+// ---------------------------------------------------------------------------
+// setup kernels (thread (r, c) of a tm x tm block)
+
+// Dense D, L, U of every block; couplings that leave a chunk are moved to
+// EL / EU (the spikes' right-hand sides) and zeroed in L / U.
 template <int TM>
 __global__ void __launch_bounds__(TM * TM)
-k_bcr_init(const SlabInfo* __restrict__ slabs, int M, double2* __restrict__ D,
-           double2* __restrict__ Lc, double2* __restrict__ Uc) {
-  const int y = blockIdx.x, s = blockIdx.y;
+k_bcr_init(const SlabInfo* __restrict__ slabs, Chunks g, double2* __restrict__ D,
+           double2* __restrict__ Lc, double2* __restrict__ Uc, double2* __restrict__ EL,
+           double2* __restrict__ EU) {
+  constexpr int TM2 = Geo<TM>::TM2;
+  const int y = blockIdx.x, s = blockIdx.y, M = g.M;
   const SlabInfo si = slabs[s];
   const int r = threadIdx.x / TM, c = threadIdx.x % TM;
   const int T = si.T;
@@ -86,27 +108,42 @@ k_bcr_init(const SlabInfo* __restrict__ slabs, int M, double2* __restrict__ D,
     if (sl < 0 || r >= T || c >= T || y + o1 < 0 || y + o1 >= M) return czero();
     return si.coeffs[(int64_t)sl * n + (int64_t)r * M + y];
   };
-  const int64_t off = ((int64_t)s * M + y) * Geo<TM>::TM2 + r * TM + c;
+  const int64_t off = ((int64_t)s * M + y) * TM2 + r * TM + c;
   double2 d = coef(c - r, 0);
   if (r >= T || c >= T) d = make_double2(r == c ? 1.0 : 0.0, 0.0);
   D[off] = d;
-  Lc[off] = coef(c - r, -1);
-  Uc[off] = coef(c - r, 1);
+  double2 l = coef(c - r, -1), u = coef(c - r, 1);
+  const int k = (int)(((int64_t)(y + 1) * g.C - 1) / M);
+  if (y == g.y0(k)) {
+    EL[((int64_t)s * g.C + k) * TM2 + r * TM + c] = l;
+    l = czero();
+  }
+  if (y == g.y0(k + 1) - 1) {
+    EU[((int64_t)s * g.C + k) * TM2 + r * TM + c] = u;
+    u = czero();
+  }
+  Lc[off] = l;
+  Uc[off] = u;
 }
 
-// In-place Gauss-Jordan inversion with partial pivoting of A (smem, pitch TM+1)
-// into Inv.  All TM*TM threads participate.
-template <int TM>
-__device__ void gj_invert(double2 (*A)[TM + 1], double2 (*Inv)[TM + 1], int* piv_row,
+// In-place Gauss-Jordan inversion with partial pivoting of an N x N matrix A
+// (smem, pitch N+1) into Inv; any block size, threads loop over elements
+// (blockDim.x >= 256 assumed for the register staging below).
+template <int N>
+__device__ void gj_invert(double2 (*A)[N + 1], double2 (*Inv)[N + 1], int* piv_row,
                           double* piv_abs, unsigned long long* err, unsigned long long code) {
-  const int tid = threadIdx.x;
-  const int r = tid / TM, c = tid % TM;
-  Inv[r][c] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  constexpr int PER = (N * N + 255) / 256;
+  for (int e = tid; e < N * N; e += nt) Inv[e / N][e % N] = make_double2(e / N == e % N, 0.0);
   __syncthreads();
-  for (int p = 0; p < TM; ++p) {
+  for (int p = 0; p < N; ++p) {
     if (tid < 32) {
-      double v = (tid >= p && tid < TM) ? cabs2(A[tid][p]) : -1.0;
-      int idx = tid;
+      double v = -1.0;
+      int idx = 0;
+      for (int i = tid; i < N; i += 32) {
+        const double av = i >= p ? cabs2(A[i][p]) : -1.0;
+        if (av > v) { v = av; idx = i; }
+      }
       for (int m = 16; m > 0; m >>= 1) {
         const double ov = __shfl_xor_sync(0xffffffffu, v, m);
         const int oi = __shfl_xor_sync(0xffffffffu, idx, m);
@@ -117,32 +154,43 @@ __device__ void gj_invert(double2 (*A)[TM + 1], double2 (*Inv)[TM + 1], int* piv
     __syncthreads();
     const int pr = *piv_row;
     if (*piv_abs <= 0.0) {
-      if (tid == 0) atomicMin(err, code + (unsigned long long)p);
-      if (r == p && c == p) A[p][p] = make_double2(1.0, 0.0);
+      if (tid == 0) {
+        atomicMin(err, code + (unsigned long long)p);
+        A[p][p] = make_double2(1.0, 0.0);
+      }
       __syncthreads();
     } else if (pr != p) {
-      if (r == p) {
-        double2 t = A[p][c]; A[p][c] = A[pr][c]; A[pr][c] = t;
-        t = Inv[p][c]; Inv[p][c] = Inv[pr][c]; Inv[pr][c] = t;
+      for (int cc = tid; cc < N; cc += nt) {
+        double2 t = A[p][cc]; A[p][cc] = A[pr][cc]; A[pr][cc] = t;
+        t = Inv[p][cc]; Inv[p][cc] = Inv[pr][cc]; Inv[pr][cc] = t;
       }
       __syncthreads();
     }
-    const double2 app = A[p][p];
-    const double2 apc = A[p][c], ipc = Inv[p][c];
-    const double2 arp = A[r][p];
-    double2 arc = A[r][c], irc = Inv[r][c];
-    __syncthreads();
-    const double2 inv_p = cdiv(make_double2(1.0, 0.0), app);
-    const double2 np = cmul(apc, inv_p), ni = cmul(ipc, inv_p);
-    if (r == p) {
-      arc = np;
-      irc = ni;
-    } else {
-      arc = csub(arc, cmul(arp, np));
-      irc = csub(irc, cmul(arp, ni));
+    const double2 inv_p = cdiv(make_double2(1.0, 0.0), A[p][p]);
+    double2 na[PER], ni[PER];   // read phase
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = tid + q * nt;
+      if (e >= N * N) continue;
+      const int r = e / N, cc = e % N;
+      const double2 npc = cmul(A[p][cc], inv_p), nic = cmul(Inv[p][cc], inv_p);
+      if (r == p) {
+        na[q] = npc;
+        ni[q] = nic;
+      } else {
+        const double2 arp = A[r][p];
+        na[q] = csub(A[r][cc], cmul(arp, npc));
+        ni[q] = csub(Inv[r][cc], cmul(arp, nic));
+      }
     }
-    A[r][c] = arc;
-    Inv[r][c] = irc;
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {   // write phase
+      const int e = tid + q * nt;
+      if (e >= N * N) continue;
+      A[e / N][e % N] = na[q];
+      Inv[e / N][e % N] = ni[q];
+    }
     __syncthreads();
   }
 }
@@ -162,17 +210,21 @@ __device__ __forceinline__ double2 mm_rc(double2 (*A)[TM + 1], double2 (*B)[TM +
   return acc;
 }
 
-// Eliminated blocks of level l (odd multiples of s): Dinv, Dinv L, Dinv U.
-// D[y] is overwritten with Dinv (natural layout) for the keep kernel.
+// Eliminated blocks of level l in every chunk (local odd multiples of s):
+// Dinv, Dinv L, Dinv U.  D[y] is overwritten with Dinv for the keep kernel.
+// top != 0: the last block standing in each chunk (local 0).
 template <int TM>
 __global__ void __launch_bounds__(TM * TM)
-k_bcr_elim(int level, int M, int top, double2* __restrict__ D, const double2* __restrict__ Lc,
-           const double2* __restrict__ Uc, double2* __restrict__ ef, double2* __restrict__ eb,
+k_bcr_elim(int level, Chunks g, int top, double2* __restrict__ D,
+           const double2* __restrict__ Lc, const double2* __restrict__ Uc,
+           double2* __restrict__ ef, double2* __restrict__ eb,
            unsigned long long* __restrict__ err) {
   constexpr int TM2 = Geo<TM>::TM2;
   const int s_ = 1 << level;
-  const int y = top ? 0 : (2 * blockIdx.x + 1) * s_;
-  const int slab = blockIdx.y;
+  const int slab = blockIdx.y / g.C, k = blockIdx.y % g.C;
+  const int yl = top ? 0 : (2 * blockIdx.x + 1) * s_;
+  if (yl >= g.len(k)) return;
+  const int y = g.y0(k) + yl, M = g.M;
   extern __shared__ __align__(16) unsigned char smraw[];
   double2(*A)[TM + 1] = reinterpret_cast<double2(*)[TM + 1]>(smraw);
   double2(*Inv)[TM + 1] = A + TM;
@@ -198,19 +250,21 @@ k_bcr_elim(int level, int M, int top, double2* __restrict__ D, const double2* __
   eb[2 * base + TM2 + lm<TM>(r, c)] = mm_rc<TM>(Inv, B);
 }
 
-// Kept blocks of level l (multiples of 2s): alpha, gamma and the next level's
-// D, L, U (in place).
+// Kept blocks of level l (local multiples of 2s): alpha, gamma and the next
+// level's D, L, U (in place).
 template <int TM>
 __global__ void __launch_bounds__(TM * TM)
-k_bcr_keep(int level, int M, int koff, double2* __restrict__ D, double2* __restrict__ Lc,
-           double2* __restrict__ Uc, double2* __restrict__ kr, int ktot) {
+k_bcr_keep(int level, Chunks g, double2* __restrict__ D, double2* __restrict__ Lc,
+           double2* __restrict__ Uc, double2* __restrict__ kr) {
   constexpr int TM2 = Geo<TM>::TM2;
   const int s_ = 1 << level;
+  const int slab = blockIdx.y / g.C, k = blockIdx.y % g.C;
   const int j = blockIdx.x;
-  const int y = j * 2 * s_;
-  const int slab = blockIdx.y;
+  const int yl = j * 2 * s_, m = g.len(k);
+  if (yl >= m) return;
+  const int y = g.y0(k) + yl, M = g.M;
   const int left = y - s_, right = y + s_;
-  const bool hl = left >= 0, hr = right < M;
+  const bool hl = yl - s_ >= 0, hr = yl + s_ < m;
   extern __shared__ __align__(16) unsigned char smraw[];
   double2(*S0)[TM + 1] = reinterpret_cast<double2(*)[TM + 1]>(smraw);
   double2(*S1)[TM + 1] = S0 + TM;
@@ -218,8 +272,7 @@ k_bcr_keep(int level, int M, int koff, double2* __restrict__ D, double2* __restr
   double2(*Ga)[TM + 1] = Al + TM;
   const int r = threadIdx.x / TM, c = threadIdx.x % TM;
   auto at = [&](int yy) { return ((int64_t)slab * M + yy) * TM2; };
-  double2* kout = kr + ((int64_t)slab * ktot + koff + j) * 2 * TM2;
-  // alpha = L_y Dinv_left, gamma = U_y Dinv_right
+  double2* kout = kr + (((int64_t)slab * g.C + k) * g.kstride + g.koff[level] + j) * 2 * TM2;
   Al[r][c] = czero();
   Ga[r][c] = czero();
   if (hl) {
@@ -238,7 +291,6 @@ k_bcr_keep(int level, int M, int koff, double2* __restrict__ D, double2* __restr
   __syncthreads();
   kout[lm<TM>(r, c)] = Al[r][c];
   kout[TM2 + lm<TM>(r, c)] = Ga[r][c];
-  // D' = D - alpha U_left - gamma L_right
   double2 d = D[at(y) + r * TM + c];
   if (hl) {
     load_mat<TM>(S0, Uc + at(left));
@@ -253,7 +305,6 @@ k_bcr_keep(int level, int M, int koff, double2* __restrict__ D, double2* __restr
     __syncthreads();
   }
   D[at(y) + r * TM + c] = d;
-  // L' = -alpha L_left, U' = -gamma U_right
   double2 lnew = czero(), unew = czero();
   if (hl) {
     load_mat<TM>(S0, Lc + at(left));
@@ -269,74 +320,216 @@ k_bcr_keep(int level, int M, int koff, double2* __restrict__ D, double2* __restr
   Uc[at(y) + r * TM + c] = unew;
 }
 
+// Spikes of every chunk by one block-Thomas pass (one CTA per slab x chunk):
+//   W = A_k^{-1} [EL; 0 ...],  V = A_k^{-1} [... 0; EU]
+// stored lane-major per block (sp[y] = {W_y, V_y}) plus the four tips
+// (W_first, W_last, V_first, V_last; natural layout) for the interface system.
+// Uses pristine D, L, U (run before the BCR levels).  Hw / Zw: work [J][M][tm^2].
+template <int TM>
+__global__ void __launch_bounds__(TM * TM)
+k_spikes(Chunks g, const double2* __restrict__ D, const double2* __restrict__ Lc,
+         const double2* __restrict__ Uc, const double2* __restrict__ EL,
+         const double2* __restrict__ EU, double2* __restrict__ Hw, double2* __restrict__ Zw,
+         double2* __restrict__ sp, double2* __restrict__ tips,
+         unsigned long long* __restrict__ err) {
+  constexpr int TM2 = Geo<TM>::TM2;
+  const int slab = blockIdx.x / g.C, k = blockIdx.x % g.C, M = g.M;
+  const int Y0 = g.y0(k), Y1 = g.y0(k + 1);
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double2(*A)[TM + 1] = reinterpret_cast<double2(*)[TM + 1]>(smraw);
+  double2(*Inv)[TM + 1] = A + TM;
+  double2(*Hp)[TM + 1] = Inv + TM;   // H_{y-1}
+  double2(*Zp)[TM + 1] = Hp + TM;    // Z_{y-1} (W forward)
+  double2(*B)[TM + 1] = Zp + TM;
+  double2(*Wn)[TM + 1] = B + TM;     // W_{y+1}
+  double2(*Vn)[TM + 1] = Wn + TM;    // V_{y+1}
+  __shared__ int piv_row;
+  __shared__ double piv_abs;
+  const int r = threadIdx.x / TM, c = threadIdx.x % TM;
+  auto at = [&](int yy) { return ((int64_t)slab * M + yy) * TM2; };
+  const double2* el = EL + ((int64_t)slab * g.C + k) * TM2;
+  const double2* eu = EU + ((int64_t)slab * g.C + k) * TM2;
+  double2* tp = tips + ((int64_t)slab * g.C + k) * 4 * TM2;
+  Hp[r][c] = czero();
+  Zp[r][c] = czero();
+  double2 zv_last = czero();
+  for (int y = Y0; y < Y1; ++y) {
+    // D~ = D - L H_{y-1} (L zero at the chunk start)
+    load_mat<TM>(B, Lc + at(y));
+    __syncthreads();
+    double2 d = D[at(y) + r * TM + c];
+    d = csub(d, mm_rc<TM>(B, Hp));
+    A[r][c] = d;
+    __syncthreads();
+    const unsigned long long code =
+        ((unsigned long long)slab << 40) | ((unsigned long long)y * TM & 0xffffffffffull);
+    gj_invert<TM>(A, Inv, &piv_row, &piv_abs, err, code);
+    // Z_y = Inv (rhs_y - L Z_{y-1}); rhs = EL at the chunk start, else 0
+    double2 t = cscale(-1.0, mm_rc<TM>(B, Zp));
+    if (y == Y0) t = el[r * TM + c];
+    __syncthreads();
+    A[r][c] = t;
+    __syncthreads();
+    const double2 z = mm_rc<TM>(Inv, A);
+    __syncthreads();
+    // H_y = Inv U_y
+    load_mat<TM>(B, Uc + at(y));
+    __syncthreads();
+    const double2 h = mm_rc<TM>(Inv, B);
+    __syncthreads();
+    if (y == Y1 - 1) {   // V forward: nonzero only at the chunk end, Inv EU
+      load_mat<TM>(B, eu);
+      __syncthreads();
+      zv_last = mm_rc<TM>(Inv, B);
+    }
+    __syncthreads();
+    Hp[r][c] = h;
+    Zp[r][c] = z;
+    Hw[at(y) + r * TM + c] = h;
+    Zw[at(y) + r * TM + c] = z;
+    __syncthreads();
+  }
+  // backward: W_y = Z_y - H_y W_{y+1}, V_y = Zv_y - H_y V_{y+1}
+  Wn[r][c] = czero();
+  Vn[r][c] = czero();
+  __syncthreads();
+  for (int y = Y1 - 1; y >= Y0; --y) {
+    load_mat<TM>(A, Hw + at(y));
+    __syncthreads();
+    const double2 w = csub(Zw[at(y) + r * TM + c], mm_rc<TM>(A, Wn));
+    double2 v = cscale(-1.0, mm_rc<TM>(A, Vn));
+    if (y == Y1 - 1) v = zv_last;
+    __syncthreads();
+    Wn[r][c] = w;
+    Vn[r][c] = v;
+    sp[2 * at(y) + lm<TM>(r, c)] = w;
+    sp[2 * at(y) + TM2 + lm<TM>(r, c)] = v;
+    if (y == Y0) {
+      tp[0 * TM2 + r * TM + c] = w;
+      tp[2 * TM2 + r * TM + c] = v;
+    }
+    if (y == Y1 - 1) {
+      tp[1 * TM2 + r * TM + c] = w;
+      tp[3 * TM2 + r * TM + c] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// Inverse of the interface system (one CTA per slab).  Unknowns per boundary
+// b (between chunks b and b+1): xi_b = (alpha_b = x at the last point of chunk
+// b, beta_b = x at the first point of chunk b+1); right-hand side
+// tau_b = (g_b[last], g_{b+1}[first]):
+//   alpha_b + Vb[last] beta_b + Wb[last] alpha_{b-1}            = g_b[last]
+//   beta_b + W_{b+1}[first] alpha_b + V_{b+1}[first] beta_{b+1} = g_{b+1}[first]
+// Block Thomas over b with identity right-hand sides gives R = S^{-1}; CTA k
+// keeps rows alpha_{k-1} and beta_k, stored per column block q (tm columns) as
+// 2tm x tm with the row index fastest.
+template <int TM>
+__global__ void __launch_bounds__(1024)
+k_reduced(Chunks g, const double2* __restrict__ tips, double2* __restrict__ Gw,
+          double2* __restrict__ Zr, double2* __restrict__ rk,
+          unsigned long long* __restrict__ err) {
+  constexpr int TM2 = Geo<TM>::TM2;
+  constexpr int N = 2 * TM;
+  const int slab = blockIdx.x, C = g.C, B = C - 1, NR = B * N;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double2(*A)[N + 1] = reinterpret_cast<double2(*)[N + 1]>(smraw);
+  double2(*Inv)[N + 1] = A + N;
+  __shared__ int piv_row;
+  __shared__ double piv_abs;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const double2* tp = tips + (int64_t)slab * C * 4 * TM2;
+  auto tip = [&](int k, int which, int r, int c) -> double2 {   // 0 Wf 1 Wl 2 Vf 3 Vl
+    return tp[((int64_t)k * 4 + which) * TM2 + r * TM + c];
+  };
+  double2* G = Gw + (int64_t)slab * B * N * N;    // G_b = Dt_b^{-1} Up_b
+  double2* Z = Zr + (int64_t)slab * NR * NR;      // block row b: rows b*N.., all NR columns
+  for (int b = 0; b < B; ++b) {
+    // D~_b = D_b - Lo_b G_{b-1};  D_b = [[I, V_b[l]], [W_{b+1}[f], I]]; Lo_b = [[W_b[l], 0],[0,0]]
+    for (int e = tid; e < N * N; e += nt) {
+      const int r = e / N, c = e % N;
+      double2 d = make_double2(r == c ? 1.0 : 0.0, 0.0);
+      if (r < TM && c >= TM) d = tip(b, 3, r, c - TM);
+      if (r >= TM && c < TM) d = tip(b + 1, 0, r - TM, c);
+      if (b > 0 && r < TM) {
+        for (int q = 0; q < TM; ++q)
+          d = csub(d, cmul(tip(b, 1, r, q), G[((int64_t)(b - 1) * N + q) * N + c]));
+      }
+      A[r][c] = d;
+    }
+    __syncthreads();
+    gj_invert<N>(A, Inv, &piv_row, &piv_abs, err, ((unsigned long long)slab << 40));
+    // G_b = Inv Up_b, Up_b = [[0,0],[0, V_{b+1}[first]]] (coupling to beta_{b+1})
+    for (int e = tid; e < N * N; e += nt) {
+      const int r = e / N, c = e % N;
+      double2 acc = czero();
+      if (b + 1 < B && c >= TM)
+        for (int q = 0; q < TM; ++q) acc = cfma(Inv[r][TM + q], tip(b + 1, 2, q, c - TM), acc);
+      G[((int64_t)b * N + r) * N + c] = acc;
+    }
+    // Z_b = Inv (E_b - Lo_b Z_{b-1})
+    for (int e = tid; e < N * NR; e += nt) {
+      const int r = e / NR, col = e % NR;
+      double2 acc = czero();
+      for (int q = 0; q < N; ++q) {
+        double2 rhs = make_double2(col == b * N + q ? 1.0 : 0.0, 0.0);
+        if (b > 0 && q < TM)
+          for (int w = 0; w < TM; ++w)
+            rhs = csub(rhs, cmul(tip(b, 1, q, w), Z[((int64_t)(b - 1) * N + w) * NR + col]));
+        acc = cfma(Inv[r][q], rhs, acc);
+      }
+      Z[((int64_t)b * N + r) * NR + col] = acc;
+    }
+    __syncthreads();
+  }
+  // backward: X_b = Z_b - G_b X_{b+1}; X overwrites Z block rows
+  for (int b = B - 2; b >= 0; --b) {
+    for (int e = tid; e < N * NR; e += nt) {
+      const int r = e / NR, col = e % NR;
+      double2 acc = Z[((int64_t)b * N + r) * NR + col];
+      for (int q = TM; q < N; ++q)   // G_b has nonzero columns only in the beta half
+        acc = csub(acc, cmul(G[((int64_t)b * N + r) * N + q],
+                             Z[((int64_t)(b + 1) * N + q) * NR + col]));
+      Z[((int64_t)b * N + r) * NR + col] = acc;
+    }
+    __syncthreads();
+  }
+  // rows of CTA k: alpha_{k-1} (block k-1, rows 0..TM-1), beta_k (block k,
+  // rows TM..2TM-1); column block q of tm columns
+  for (int e = tid; e < C * N * NR; e += nt) {
+    const int k = e / (N * NR), rem = e % (N * NR);
+    const int r = rem / NR, col = rem % NR;
+    double2 v = czero();
+    if (r < TM && k > 0) v = Z[((int64_t)(k - 1) * N + r) * NR + col];
+    if (r >= TM && k < B) v = Z[((int64_t)k * N + r) * NR + col];
+    const int q = col / TM, cq = col % TM;
+    rk[(((int64_t)slab * C + k) * (2 * B) + q) * (2 * TM2) + cq * N + r] = v;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // apply
 
 struct SolveArgs {
   const SweepTask* tasks;
   int ffirst[2], fcount[2];
-  int C, M, L, ktot, nloc_max, nslot;
-  int koff[kMaxLevels];
+  Chunks g;
+  int nslot;
   const double2* ef;
   const double2* eb;
   const double2* kr;
+  const double2* sp;
+  const double2* rk;
   const double2* src;      // right-hand side field (n0 x M)
   const double2* coarse;   // global coarse operator [S][n0*M] (transmission couplings)
   int64_t ncoarse;
   int cslot[3][3];
   double2* trace;          // [ntrace][2][M]
   double2* u[2];
-  unsigned long long* dbg;   // optional phase timestamps (HS_SWEEP_TRACE)
+  unsigned long long* dbg; // optional per-phase timestamps (HS_SWEEP_TRACE)
 };
 
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-  // TMA bulk prefetch into L2 (sizes are multiples of 16 bytes here)
-  if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes)
-                          : "memory");
-}
-
-// Prefetch this CTA's share of slab `slab`'s BCR records into L2.
-template <int TM>
-__device__ void prefetch_slab(const SolveArgs& a, int slab, int Y0, int Y1) {
-  constexpr int TM2 = Geo<TM>::TM2;
-  const int M = a.M;
-  const uint32_t mb = TM2 * 16;
-  const double2* ef = a.ef + (int64_t)slab * M * TM2;
-  const double2* eb = a.eb + (int64_t)slab * M * 2 * TM2;
-  const double2* kr = a.kr + (int64_t)slab * a.ktot * 2 * TM2;
-  prefetch_l2(ef + (int64_t)Y0 * TM2, (uint32_t)(Y1 - Y0) * mb);
-  prefetch_l2(eb + (int64_t)Y0 * 2 * TM2, (uint32_t)(Y1 - Y0) * 2 * mb);
-  for (int l = 0; l < a.L; ++l) {
-    const int s2 = 2 << l;
-    const int j0 = (Y0 + s2 - 1) / s2, j1 = (Y1 - 1) / s2;
-    if (j1 >= j0)
-      prefetch_l2(kr + (int64_t)(a.koff[l] + j0) * 2 * TM2, (uint32_t)(j1 - j0 + 1) * 2 * mb);
-  }
-}
-
-// y = Mat v for a tm x tm lane-major block; every lane returns row (lane % tm)
-template <int TM>
-__device__ __forceinline__ double2 mv(const double2* __restrict__ mat, const double2* v,
-                                      int lane) {
-  constexpr int CPL = Geo<TM>::CPL;
-  const int hh = lane / TM;
-  double2 a0 = czero(), a1 = czero();
-#pragma unroll
-  for (int k = 0; k < CPL; k += 2) {
-    a0 = cfma(__ldg(mat + k * 32 + lane), v[CPL * hh + k], a0);
-    a1 = cfma(__ldg(mat + (k + 1) * 32 + lane), v[CPL * hh + k + 1], a1);
-  }
-  double2 acc = cadd(a0, a1);
-  if (TM == 16) acc = cadd(acc, shfl_xor_c(acc, 16));
-  return acc;
-}
-
-// Ring of shared-memory slots fed by TMA bulk copies: the BCR items (one
-// block's 1-2 matrices) of this CTA in consumption order, across phases and
-// tasks.  The warp that consumes item i refills its slot with item i+NSLOT, so
-// copies run up to NSLOT items ahead of the dependency chain and never sit on
-// a thread's scoreboard across a cluster barrier (a global load in flight
-// delays barrier.cluster completion; an async-proxy copy does not).
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -369,61 +562,31 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-
-// y = Mat v, Mat a lane-major tm x tm block in shared memory; every lane
-// returns row (lane % tm)
-template <int TM>
-__device__ __forceinline__ double2 mvs(const double2* mat, const double2* v, int lane) {
-  constexpr int CPL = Geo<TM>::CPL;
-  const int hh = lane / TM;
-  double2 vv[CPL];   // issue every operand load first (DSMEM round trips overlap)
-#pragma unroll
-  for (int k = 0; k < CPL; ++k) vv[k] = v[CPL * hh + k];
-  double2 a0 = czero(), a1 = czero();
-#pragma unroll
-  for (int k = 0; k < CPL; k += 2) {
-    a0 = cfma(mat[k * 32 + lane], vv[k], a0);
-    a1 = cfma(mat[(k + 1) * 32 + lane], vv[k + 1], a1);
-  }
-  double2 acc = cadd(a0, a1);
-  if (TM == 16) acc = cadd(acc, shfl_xor_c(acc, 16));
-  return acc;
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  if (bytes)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-// acc = A0 v0 + A1 v1 (either term may be absent); both operand vectors are
-// fetched before any arithmetic so remote (DSMEM) round trips overlap
+// acc = A0 v0 + A1 v1 (either term may be absent); A lane-major in shared
+// memory, v in shared memory; every lane returns row (lane % tm)
 template <int TM>
 __device__ __forceinline__ double2 mvs2(const double2* m0, const double2* v0, const double2* m1,
-                                        const double2* v1, int lane, double2* stage) {
+                                        const double2* v1, int lane) {
   constexpr int CPL = Geo<TM>::CPL;
   const int hh = lane / TM;
-  // one coalesced (possibly remote) read per operand element into this warp's
-  // staging area, then broadcast reads from local shared memory
-  if (lane < TM) {
-    if (v0) stage[lane] = v0[lane];
-    if (v1) stage[TM + lane] = v1[lane];
-  }
-  __syncwarp();
-  double2 va[CPL], vb[CPL];
-#pragma unroll
-  for (int k = 0; k < CPL; ++k) {
-    va[k] = v0 ? stage[CPL * hh + k] : czero();
-    vb[k] = v1 ? stage[TM + CPL * hh + k] : czero();
-  }
-  __syncwarp();
   double2 a0 = czero(), a1 = czero();
   if (v0) {
 #pragma unroll
     for (int k = 0; k < CPL; k += 2) {
-      a0 = cfma(m0[k * 32 + lane], va[k], a0);
-      a1 = cfma(m0[(k + 1) * 32 + lane], va[k + 1], a1);
+      a0 = cfma(m0[k * 32 + lane], v0[CPL * hh + k], a0);
+      a1 = cfma(m0[(k + 1) * 32 + lane], v0[CPL * hh + k + 1], a1);
     }
   }
   if (v1) {
 #pragma unroll
     for (int k = 0; k < CPL; k += 2) {
-      a0 = cfma(m1[k * 32 + lane], vb[k], a0);
-      a1 = cfma(m1[(k + 1) * 32 + lane], vb[k + 1], a1);
+      a0 = cfma(m1[k * 32 + lane], v1[CPL * hh + k], a0);
+      a1 = cfma(m1[(k + 1) * 32 + lane], v1[CPL * hh + k + 1], a1);
     }
   }
   double2 acc = cadd(a0, a1);
@@ -431,66 +594,63 @@ __device__ __forceinline__ double2 mvs2(const double2* m0, const double2* v0, co
   return acc;
 }
 
+// items of one chunk solve: <= 3m + 2L local, 2(C-1) R blocks, m spike blocks
+__host__ __device__ inline int itab_len(int mmax) { return 4 * mmax + 2 * kMaxLevels + 2 * kMaxC; }
+
+// Item copy descriptor: array (bits 29-31; 7 = none), double length (bit 28),
+// offset in double2 from the array's slab base (bits 0-27).
+enum ItemArray : uint32_t { kArrEf = 0, kArrEb = 1, kArrKr = 2, kArrRk = 3, kArrSp = 4 };
+__host__ __device__ constexpr uint32_t item_enc(uint32_t arr, int64_t off, bool dbl = false) {
+  return (arr << 29) | (dbl ? (1u << 28) : 0u) | (uint32_t)off;
+}
+constexpr uint32_t kItemNone = 0xffffffffu;
+
 template <int TM>
 struct Ring {
-  static constexpr int SLOT = 2 * Geo<TM>::TM2;   // double2 per slot (two matrices)
-  static int nslot(int nloc_max) {
-    const int vec = 2 * nloc_max * TM * 16;
-    const int avail = 225 * 1024 - vec - 1024 - kMaxTasks * 4 - kWarps * 2 * TM * 16;
-    return std::max(2, std::min(32, avail / (SLOT * 16 + 12)));
+  static constexpr int SLOT = 2 * Geo<TM>::TM2;   // double2 per slot (two blocks)
+  // F, Yv vectors + tau + R partials + bookkeeping, then the ring
+  static int fixed(int mmax) {
+    return 2 * (mmax + 1) * TM * 16 + 2 * kMaxC * TM * 16 + (kWarps + 1) * 2 * TM * 16 +
+           (64 + kMaxTasks) * 4 + itab_len(mmax) * 8 + 384;
   }
-  static int smem(int nloc_max) {
-    const int n = nslot(nloc_max);
-    return 2 * nloc_max * TM * 16 + n * SLOT * 16 + n * 12 + (64 + kMaxTasks) * 4 + 64 +
-           kWarps * 2 * TM * 16 + 16;
+  static int nslot(int mmax) {
+    const int avail = 225 * 1024 - fixed(mmax);
+    return std::max(2, std::min(48, avail / (SLOT * 16 + 16)));
   }
+  static int smem(int mmax) { return fixed(mmax) + nslot(mmax) * (SLOT * 16 + 16); }
 };
 
 template <int TM>
-__global__ void __launch_bounds__(kWarps * 32, 1) k_bcr_solve(SolveArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   constexpr int TM2 = Geo<TM>::TM2;
   constexpr int SLOT = Ring<TM>::SLOT;
   constexpr int YPW = 32 / TM;   // face points per warp pass in row-wise loops
+  constexpr int N2 = 2 * TM;     // interface unknowns per chunk (alpha, beta)
   cg::cluster_group cl = cg::this_cluster();
-  const int C = a.C, M = a.M, L = a.L;
+  const Chunks& g = a.g;
+  const int C = g.C, M = g.M, L = g.L, B = C - 1;
   const int rank = (int)cl.block_rank();
   const int front = blockIdx.x / C;
-  const int Y0 = (int)((int64_t)rank * M / C), Y1 = (int)((int64_t)(rank + 1) * M / C);
-  const int nloc = Y1 - Y0;
+  const int Y0 = g.y0(rank), Y1 = g.y0(rank + 1);
+  const int m = Y1 - Y0;
+  const int mmax = (M + C - 1) / C;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int x = lane % TM, hh = lane / TM;
   const int NS = a.nslot;
   extern __shared__ __align__(128) double2 sm[];
-  double2* F = sm;                          // [nloc_max][TM] right-hand side / reduced rhs
-  double2* Yv = sm + a.nloc_max * TM;       // [nloc_max][TM] Dinv f, then the solution
-  double2* ring = Yv + a.nloc_max * TM;     // [NS][SLOT]
-  uint64_t* bars = (uint64_t*)(ring + (int64_t)NS * SLOT);
-  volatile int* seq = (volatile int*)(bars + NS);   // [NS] item currently issued into a slot
-  int* pfx = (int*)(bars + NS) + NS;        // [2L+1] items before each phase
-  int* slabs = pfx + 64;                    // [fcount] slab of each task of this front
-  double2* stage = (double2*)(((uintptr_t)(slabs + kMaxTasks) + 15) & ~(uintptr_t)15) +
-                   warp * 2 * TM;             // [2][TM] per warp (16-byte aligned)
+  double2* F = sm;                                  // [mmax+1][TM] rhs / reduced rhs
+  double2* Yv = F + (mmax + 1) * TM;                // [mmax+1][TM] Dinv f, then x
+  double2* tau = Yv + (mmax + 1) * TM;              // [2 kMaxC][TM] interface rhs
+  double2* part = tau + 2 * kMaxC * TM;             // [kWarps][2TM] R partial sums
+  double2* ab = part + kWarps * N2;                 // [2TM] alpha_{k-1}, beta_k
+  uint64_t* bars = (uint64_t*)(ab + N2);            // [NS]
+  volatile int* seq = (volatile int*)(bars + NS);   // [NS] item issued into a slot
+  volatile int* done = seq + NS;                    // [NS] item consumed from a slot
+  int* pfx = (int*)(bars + NS) + 2 * NS;            // [2L+3] items before each phase
+  int* slabs = pfx + 64;                            // [fcount]
+  uint2* itab = (uint2*)(slabs + kMaxTasks);        // [ITEMS] copy descriptors
+  double2* ring = (double2*)(((uintptr_t)(itab + itab_len(mmax)) + 127) & ~(uintptr_t)127);
 
-  // owner CTA of face point y: local test first, else a search of the
-  // partition table (no 64-bit division on the chain)
-  auto owner = [&](int y, int& base) -> int {
-    if (y >= Y0 && y < Y1) { base = Y0; return rank; }
-    const int r = ((y + 1) * C - 1) / M;   // 32-bit: (y+1)*C < 2^31
-    base = r * M / C;
-    return r;
-  };
-  auto Fany = [&](int y) -> const double2* {
-    int base;
-    const int o = owner(y, base);
-    const double2* p = F + (y - base) * TM;
-    return o == rank ? p : cl.map_shared_rank(p, o);
-  };
-  auto Yany = [&](int y) -> const double2* {
-    int base;
-    const int o = owner(y, base);
-    const double2* p = Yv + (y - base) * TM;
-    return o == rank ? p : cl.map_shared_rank(p, o);
-  };
   auto cc = [&](int o0, int o1, int row, int y) -> double2 {
     const int sl = a.cslot[o0 + 1][o1 + 1];
     if (sl < 0 || y + o1 < 0 || y + o1 >= M) return czero();
@@ -498,7 +658,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_bcr_solve(SolveArgs a) {
   };
   // transmission source into slab row p-lo (which 0) / p+1-lo (which 1)
   auto trans = [&](int buf, int p, int sign, int which, int y) -> double2 {
-    const double2* B = a.trace + (int64_t)buf * 2 * M + (which == 0 ? M : 0);
+    const double2* Bt = a.trace + (int64_t)buf * 2 * M + (which == 0 ? M : 0);
     const int o0 = which == 0 ? 1 : -1;
     const int row = which == 0 ? p - 1 : p;
     double2 cv[3], bv[3];
@@ -506,7 +666,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_bcr_solve(SolveArgs a) {
     for (int o = -1; o <= 1; ++o) {   // all six loads in flight together
       const bool ok = y + o >= 0 && y + o < M;
       cv[o + 1] = ok ? cc(o0, o, row, y) : czero();
-      bv[o + 1] = ok ? B[y + o] : czero();
+      bv[o + 1] = ok ? Bt[y + o] : czero();
     }
     double2 acc = cmul(cv[0], bv[0]);
     acc = cfma(cv[1], bv[1], acc);
@@ -514,16 +674,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_bcr_solve(SolveArgs a) {
     return cscale(which == 0 ? (double)sign : (double)-sign, acc);
   };
 
-  // Phases of one slab solve: p < L forward level p, p >= L backward level
-  // 2L-1-p; items of a phase are this CTA's active blocks, item j -> warp j%16.
+  // Item streams of one slab solve of this CTA: local BCR phases
+  // (p < L forward level p, p >= L backward level 2L-1-p), then the 2B column
+  // blocks of R, then the m spike blocks.  Item j of a phase -> warp j % 16.
   const int NP = 2 * L;
   auto ph_level = [&](int p) { return p < L ? p : NP - 1 - p; };
-  auto ph_first = [&](int p) -> int {
-    const int s = 1 << ph_level(p);
-    int first = ((Y0 + s - 1) / s) * s;
-    if (p >= L && ((first / s) & 1) == 0) first += s;
-    return first;
-  };
+  auto ph_first = [&](int p) -> int { return p >= L ? (1 << ph_level(p)) : 0; };
   auto ph_step = [&](int p) { return (p < L ? 1 : 2) << ph_level(p); };
   const int ffirst = front ? a.ffirst[1] : a.ffirst[0];
   const int fcount = front ? a.fcount[1] : a.fcount[0];
@@ -532,67 +688,94 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_bcr_solve(SolveArgs a) {
     for (int p = 0; p < NP; ++p) {
       pfx[p] = acc;
       const int f = ph_first(p);
-      if (f < Y1) acc += (Y1 - 1 - f) / ph_step(p) + 1;
+      if (f < m) acc += (m - 1 - f) / ph_step(p) + 1;
     }
-    pfx[NP] = acc;
+    pfx[NP] = acc;                               // R column blocks
+    pfx[NP + 1] = acc + (B > 0 ? 2 * B : 0);     // spikes
+    pfx[NP + 2] = pfx[NP + 1] + (B > 0 ? m : 0);
     for (int i = 0; i < NS; ++i) {
       mbar_init(&bars[i], 1);
       seq[i] = -1;
+      done[i] = i - NS;   // slot i is free for item i
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = threadIdx.x; i < fcount; i += blockDim.x) slabs[i] = a.tasks[ffirst + i].slab;
   __syncthreads();
-  const int ITEMS = pfx[NP];
+  const int ITEMS = pfx[NP + 2];
   const int total = fcount * ITEMS;
+  const int64_t kbase = (int64_t)rank * g.kstride;
+  if (ITEMS > itab_len(mmax)) __trap();   // bound of the descriptor table (host-sized)
 
-  // matrices of item (task ti, phase p, y): up to two 16/32-square blocks
-  auto item_src = [&](int ti, int p, int y, const double2*& m0, const double2*& m1) {
-    const int slab = slabs[ti];
-    const int l = ph_level(p), s = 1 << l;
-    m0 = m1 = nullptr;
-    if (p < L) {
-      if ((y / s) & 1) {
-        m0 = a.ef + ((int64_t)slab * M + y) * TM2;
-      } else {
-        const double2* k2 =
-            a.kr + ((int64_t)slab * a.ktot + a.koff[l] + y / (2 * s)) * 2 * TM2;
-        if (y - s >= 0) m0 = k2;
-        if (y + s < M) m1 = k2 + TM2;
-        if (y == 0 && l == L - 1) m0 = a.ef + (int64_t)slab * M * TM2;   // top block Dinv
-      }
-    } else {
-      const double2* e2 = a.eb + ((int64_t)slab * M + y) * 2 * TM2;
-      if (y - s >= 0) m0 = e2;
-      if (y + s < M) m1 = e2 + TM2;
-    }
-  };
-  auto issue = [&](int i) {   // one lane
-    const int ti = i / ITEMS;
-    const int r = i - ti * ITEMS;
+  // Copy descriptors of one chunk solve (the same for every slab; offsets
+  // relative to the slab's base in each factor array), built once.
+  for (int r = threadIdx.x; r < ITEMS; r += blockDim.x) {
     int p = 0;
     while (pfx[p + 1] <= r) ++p;
-    const int y = ph_first(p) + (r - pfx[p]) * ph_step(p);
-    const double2 *m0, *m1;
-    item_src(ti, p, y, m0, m1);
-    const int sl = i % NS;
+    const int j = r - pfx[p];
+    uint2 e = make_uint2(kItemNone, kItemNone);
+    if (p < NP) {
+      const int l = ph_level(p), s = 1 << l;
+      const int yl = ph_first(p) + j * ph_step(p);
+      const int y = Y0 + yl;
+      if (p < L) {
+        if ((yl >> l) & 1) {
+          e.x = item_enc(kArrEf, (int64_t)y * TM2);
+        } else {
+          const int64_t k2 = (kbase + g.koff[l] + (yl >> (l + 1))) * 2 * TM2;
+          if (yl - s >= 0) e.x = item_enc(kArrKr, k2);
+          if (yl + s < m) e.y = item_enc(kArrKr, k2 + TM2);
+          if (yl == 0 && l == L - 1) e.x = item_enc(kArrEf, (int64_t)Y0 * TM2);   // top Dinv
+        }
+      } else {
+        const int64_t e2 = (int64_t)y * 2 * TM2;
+        if (yl - s >= 0) e.x = item_enc(kArrEb, e2);
+        if (yl + s < m) e.y = item_enc(kArrEb, e2 + TM2);
+      }
+    } else if (p == NP) {   // R column block j
+      e.x = item_enc(kArrRk, ((int64_t)rank * (2 * B) + j) * (2 * TM2), true);
+    } else {                // spikes of block j
+      e.x = item_enc(kArrSp, (int64_t)(Y0 + j) * 2 * TM2, true);
+    }
+    itab[r] = e;
+  }
+  __syncthreads();
+
+  // producer state: the current task's slab base of every factor array
+  const double2* sbase[5];
+  auto set_slab = [&](int slab) {
+    sbase[kArrEf] = a.ef + (int64_t)slab * M * TM2;
+    sbase[kArrEb] = a.eb + (int64_t)slab * M * 2 * TM2;
+    sbase[kArrKr] = a.kr + (int64_t)slab * C * g.kstride * 2 * TM2;
+    sbase[kArrRk] = a.rk + (int64_t)slab * C * (2 * B) * 2 * TM2;
+    sbase[kArrSp] = a.sp + (int64_t)slab * M * 2 * TM2;
+  };
+  auto src_of = [&](uint32_t e) -> const double2* {
+    const uint32_t arr = e >> 29;
+    const double2* b = arr == kArrEf ? sbase[0]
+                       : arr == kArrEb ? sbase[1]
+                       : arr == kArrKr ? sbase[2]
+                       : arr == kArrRk ? sbase[3]
+                                       : sbase[4];
+    return b + (e & 0x0fffffffu);
+  };
+  auto issue = [&](int r, int sl) {   // one lane: item r of the current task into slot sl
+    const uint2 e = itab[r];
     double2* slot = ring + sl * SLOT;
     uint64_t* bar = &bars[sl];
-    const uint32_t mb = TM2 * 16;
-    mbar_expect_tx(bar, (m0 ? mb : 0) + (m1 ? mb : 0));
-    if (m0) bulk_g2s(slot, m0, mb, bar);
-    if (m1) bulk_g2s(slot + TM2, m1, mb, bar);
-    seq[sl] = i;
+    constexpr uint32_t mb = TM2 * 16;
+    if (e.x != kItemNone && (e.x >> 28 & 1)) {
+      mbar_expect_tx(bar, 2 * mb);
+      bulk_g2s(slot, src_of(e.x), 2 * mb, bar);
+    } else {
+      mbar_expect_tx(bar, (e.x != kItemNone ? mb : 0) + (e.y != kItemNone ? mb : 0));
+      if (e.x != kItemNone) bulk_g2s(slot, src_of(e.x), mb, bar);
+      if (e.y != kItemNone) bulk_g2s(slot + TM2, src_of(e.y), mb, bar);
+    }
   };
-  if (threadIdx.x == 0)
-    for (int i = 0; i < total && i < NS; ++i) issue(i);
-  if (L == 0 && rank == 0 && warp == 0 && lane == 0 && fcount) {
-    // M == 1: the only block is the top; its Dinv is read directly
-  }
-
-  // optional instrumentation: timestamps of task 1 kept in shared memory (a
-  // global store would hold the next cluster-barrier arrive), dumped at exit
-  __shared__ unsigned long long tsm[512];
+  // optional instrumentation: task 1 timestamps kept in shared memory, dumped at exit
+  __shared__ unsigned long long tsm[128];
+  __shared__ unsigned long long tprod[128];   // producer: [spin start, issued] of task 1's first 64 items
   auto stamp = [&](int ti, int k) {
     if (a.dbg && threadIdx.x == 0 && ti == 1 && k < 64) {
       unsigned long long tt;
@@ -600,112 +783,229 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_bcr_solve(SolveArgs a) {
       tsm[k] = tt;
     }
   };
-  auto stamp2 = [&](int ti, int p, int k) {
-    if (a.dbg && threadIdx.x == 0 && ti == 1 && p < 56) {
+  if (a.dbg && threadIdx.x == 0)
+    for (int k = 0; k < 128; ++k) tsm[k] = tprod[k] = 0;
+  auto stamp2 = [&](int ti, int p, int j, int k) {
+    if (a.dbg && threadIdx.x == 0 && ti == 1 && j == 0 && p < 12) {
       unsigned long long tt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
-      tsm[64 + p * 8 + k] = tt;
+      tsm[64 + p * 5 + k] = tt;
     }
   };
-  if (a.dbg && threadIdx.x == 0)
-    for (int k = 0; k < 512; ++k) tsm[k] = 0;
+
+  // consume item i: wait until issued into its slot (a parity wait is valid
+  // only once the slot's previous occupant completed), then for the data
+  int dbg_ti = 0, dbg_p = 0, dbg_j = 0;
+  auto acquire = [&](int i) -> const double2* {
+    stamp2(dbg_ti, dbg_p, dbg_j, 0);
+    while (seq[i % NS] != i) {
+    }
+    stamp2(dbg_ti, dbg_p, dbg_j, 1);
+    mbar_wait(&bars[i % NS], (uint32_t)((i / NS) & 1));
+    stamp2(dbg_ti, dbg_p, dbg_j, 2);
+    return ring + (i % NS) * SLOT;
+  };
+  // The warp's reads of the slot have returned (their values are consumed
+  // before the __syncwarp), so the producer's async-proxy refill cannot race.
+  auto release = [&](int i) {   // whole consumer warp, after its last read of the slot
+    __syncwarp();
+    if (lane == 0) done[i % NS] = i;
+  };
+  auto csync = [&]() {   // consumer warps only (the producer never joins)
+    asm volatile("bar.sync 1, %0;" ::"r"(kCW * 32) : "memory");
+  };
+
+  if (warp == kCW) {
+    // ---- TMA producer warp: issues every item in consumption order as soon
+    // as its slot is free, prefetches the next slab into L2, and takes part in
+    // the cluster barriers (arriving early: it never holds data others read).
+    int nb = 0;                 // cluster barriers passed (arrived)
+    bool owe_wait = false;
+    const int per_task = B > 0 ? 2 : 1;
+    auto bar_pos = [&](int k) {   // first item consumed after barrier k
+      const int ti = k / per_task;
+      return (per_task == 2 && k % 2 == 0) ? ti * ITEMS + pfx[NP] : (ti + 1) * ITEMS;
+    };
+    const int nbar = fcount * per_task;
+    auto arrive_next = [&]() {
+      if (owe_wait) asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
+      asm volatile("barrier.cluster.arrive.release;" ::: "memory");
+      owe_wait = true;
+      ++nb;
+    };
+    int nextb = nbar > 0 ? bar_pos(0) : total;
+    const int BW = max(1, min(8, NS / 2));   // items issued per batch (one lane each)
+    int sl = 0;
+    for (int ti = 0; ti < fcount; ++ti) {
+      set_slab(slabs[ti]);
+      if (lane == 0 && ti + 1 < fcount) {   // next slab's matrices into L2
+        const int ns = slabs[ti + 1];
+        prefetch_l2(a.ef + ((int64_t)ns * M + Y0) * TM2, (uint32_t)m * TM2 * 16);
+        prefetch_l2(a.eb + ((int64_t)ns * M + Y0) * 2 * TM2, (uint32_t)m * 2 * TM2 * 16);
+        prefetch_l2(a.kr + (((int64_t)ns * C) * g.kstride + kbase) * 2 * TM2,
+                    (uint32_t)g.kstride * 2 * TM2 * 16);
+        if (B > 0) {
+          prefetch_l2(a.sp + ((int64_t)ns * M + Y0) * 2 * TM2, (uint32_t)m * 2 * TM2 * 16);
+          prefetch_l2(a.rk + (((int64_t)ns * C + rank) * (2 * B)) * (2 * TM2),
+                      (uint32_t)(2 * B) * 2 * TM2 * 16);
+        }
+      }
+      // batches of up to BW items, one lane each, never across a cluster barrier
+      const int base = ti * ITEMS;
+      for (int r0 = 0; r0 < ITEMS;) {
+        const int i0 = base + r0;
+        while (i0 == nextb) {
+          arrive_next();
+          nextb = nb < nbar ? bar_pos(nb) : total;
+        }
+        const int cnt = min(BW, min(ITEMS - r0, nextb - i0));
+        if (lane < cnt) {
+          const int i = i0 + lane;
+          int sl_l = sl + lane;
+          if (sl_l >= NS) sl_l -= NS;
+          const int k = i - ITEMS;
+          unsigned long long t0 = 0, t1 = 0;
+          if (a.dbg && k >= 0 && k < 64) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          while (done[sl_l] != i - NS) {
+          }
+          issue(r0 + lane, sl_l);
+          seq[sl_l] = i;
+          if (a.dbg && k >= 0 && k < 64) {
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            tprod[2 * k] = t0;
+            tprod[2 * k + 1] = t1;
+          }
+        }
+        sl += cnt;
+        if (sl >= NS) sl -= NS;
+        r0 += cnt;
+        __syncwarp();
+      }
+    }
+    while (nb < nbar) arrive_next();
+    if (owe_wait) asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
+    return;
+  }
+
   for (int ti = 0; ti < fcount; ++ti) {
-    stamp(ti, 0);
     const SweepTask t = a.tasks[ffirst + ti];
-    if (threadIdx.x == 0 && ti + 1 < fcount)
-      prefetch_slab<TM>(a, slabs[ti + 1], Y0, Y1);
+    const int base = ti * ITEMS;
+    stamp(ti, 0);
     // ---- right-hand side of the owned blocks (restriction + transmission)
-    for (int yl = warp * YPW + hh; yl < nloc; yl += kWarps * YPW) {
+    for (int yl = warp * YPW + hh; yl < m; yl += kCW * YPW) {
       const int y = Y0 + yl;
       double2 v = czero();
-      const int g = x + t.lo - 1;
-      if (x < t.T && g >= t.a && g < t.b) v = __ldg(a.src + (int64_t)g * M + y);
+      const int gr = x + t.lo - 1;
+      if (x < t.T && gr >= t.a && gr < t.b) v = __ldg(a.src + (int64_t)gr * M + y);
       if (t.tin1 >= 0 && (x == t.row1 || x == t.row1 + 1))
         v = cadd(v, trans(t.tin1, t.row1 + t.lo, 1, x - t.row1, y));
       if (t.tin3 >= 0 && (x == t.row3 || x == t.row3 + 1))
         v = cadd(v, trans(t.tin3, t.row3 + t.lo, -1, x - t.row3, y));
       F[yl * TM + x] = v;
     }
-    cl.sync();
+    csync();
     stamp(ti, 1);
-    if (L == 0) {   // M == 1: x_0 = Dinv_0 f_0
-      if (rank == 0 && warp == 0) {
-        const double2 r = mv<TM>(a.ef + (int64_t)t.slab * M * TM2, F, lane);
-        if (hh == 0) Yv[x] = r;
+    // ---- chunk-local BCR: forward reduction, top solve, back substitution
+    if (L == 0) {   // single-block chunk: x = Dinv f (Dinv via the global pointer)
+      if (warp == 0) {
+        const double2* e0 = a.ef + ((int64_t)slabs[ti] * M + Y0) * TM2;
+        double2 acc = czero();
+        for (int c = 0; c < TM; ++c) acc = cfma(__ldg(e0 + lm<TM>(x, c)), F[c], acc);
+        if (hh == 0) Yv[x] = acc;
       }
-      __syncthreads();
+      csync();
     }
-    // ---- forward reduction, top solve, back substitution
-    const int base = ti * ITEMS;
-    int defer0 = -1, defer = -1;
     for (int p = 0; p < NP; ++p) {
       const int l = ph_level(p), s = 1 << l;
       const int f0 = ph_first(p), st = ph_step(p);
       const int cnt = pfx[p + 1] - pfx[p];
-      for (int j = warp; j < cnt; j += kWarps) {
-        const int y = f0 + j * st;
+      for (int j = warp; j < cnt; j += kCW) {
+        const int yl = f0 + j * st;
         const int i = base + pfx[p] + j;
-        // a parity wait is only valid once the slot's previous use completed:
-        // wait until this item has been issued into the slot (which happens
-        // after its previous occupant was consumed)
-        if (j == 0) stamp2(ti, p, 0);
-        while (seq[i % NS] != (int)i) {
-        }
-        if (j == 0) stamp2(ti, p, 1);
-        mbar_wait(&bars[i % NS], (uint32_t)((i / NS) & 1));
-        if (j == 0) stamp2(ti, p, 2);
-        const double2* m0 = ring + (i % NS) * SLOT;
+        dbg_ti = ti; dbg_p = p; dbg_j = j;
+        const double2* m0 = acquire(i);
         const double2* m1 = m0 + TM2;
         if (p < L) {
-          if ((y / s) & 1) {   // eliminated at this level: y = Dinv f
-            const double2 r = mvs<TM>(m0, F + (y - Y0) * TM, lane);
-            if (hh == 0) Yv[(y - Y0) * TM + x] = r;
-          } else {             // kept: f -= alpha f_{y-s} + gamma f_{y+s}
-            double2 acc = czero();
-            acc = mvs2<TM>(y - s >= 0 ? m0 : nullptr, y - s >= 0 ? Fany(y - s) : nullptr,
-                           y + s < M ? m1 : nullptr, y + s < M ? Fany(y + s) : nullptr, lane,
-                           stage);
-            if (hh == 0) F[(y - Y0) * TM + x] = csub(F[(y - Y0) * TM + x], acc);
-            if (y == 0 && l == L - 1) {   // top of the reduction: x_0 = Dinv_0 f_0
+          if ((yl / s) & 1) {   // eliminated at this level: y = Dinv f
+            const double2 r = mvs2<TM>(m0, F + yl * TM, nullptr, nullptr, lane);
+            if (hh == 0) Yv[yl * TM + x] = r;
+          } else {              // kept: f -= alpha f_{y-s} + gamma f_{y+s}
+            const bool hl = yl - s >= 0, hr = yl + s < m;
+            const double2 acc = mvs2<TM>(hl ? m0 : nullptr, hl ? F + (yl - s) * TM : nullptr,
+                                         hr ? m1 : nullptr, hr ? F + (yl + s) * TM : nullptr,
+                                         lane);
+            if (hh == 0) F[yl * TM + x] = csub(F[yl * TM + x], acc);
+            if (yl == 0 && l == L - 1) {   // top of the reduction: x_0 = Dinv_0 f_0
               __syncwarp();
-              const double2 r = mvs<TM>(m0, F, lane);
+              const double2 r = mvs2<TM>(m0, F, nullptr, nullptr, lane);
               if (hh == 0) Yv[x] = r;
             }
           }
-        } else {               // x_y = Dinv f - (Dinv L) x_{y-s} - (Dinv U) x_{y+s}
-          double2 acc = czero();
-          acc = mvs2<TM>(y - s >= 0 ? m0 : nullptr, y - s >= 0 ? Yany(y - s) : nullptr,
-                         y + s < M ? m1 : nullptr, y + s < M ? Yany(y + s) : nullptr, lane,
-                         stage);
-          if (hh == 0) Yv[(y - Y0) * TM + x] = csub(Yv[(y - Y0) * TM + x], acc);
+        } else {                // x_y = Dinv f - (Dinv L) x_{y-s} - (Dinv U) x_{y+s}
+          const bool hl = yl - s >= 0, hr = yl + s < m;
+          const double2 acc = mvs2<TM>(hl ? m0 : nullptr, hl ? Yv + (yl - s) * TM : nullptr,
+                                       hr ? m1 : nullptr, hr ? Yv + (yl + s) * TM : nullptr,
+                                       lane);
+          if (hh == 0) Yv[yl * TM + x] = csub(Yv[yl * TM + x], acc);
         }
-        __syncwarp();
-        if (j == 0) stamp2(ti, p, 3);
-        if (i + NS < total) {
-          if (i + NS < base + pfx[p + 1]) {   // needed within this phase: refill now
-            if (lane == 0) {
-              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              issue(i + NS);
-            }
-          } else {
-            if (defer0 < 0) defer0 = i + NS;
-            defer = i + NS;   // refill after arriving at the barrier (off the chain)
-          }
-        }
-        if (j == 0) stamp2(ti, p, 4);
+        stamp2(ti, p, j, 3);
+        release(i);
+        stamp2(ti, p, j, 4);
+      }
+      csync();
+      stamp(ti, 2 + p);
+    }
+    if (B > 0) {
+      // ---- push this chunk's tips g[first], g[last] into every CTA's tau:
+      // tau block b = (g_b[last], g_{b+1}[first]) -> tm-slots 2b, 2b+1
+      for (int d = warp; d < C && lane < TM; d += kCW) {
+        double2* dst = cl.map_shared_rank(tau, d);
+        if (rank > 0) dst[(2 * (rank - 1) + 1) * TM + lane] = Yv[lane];
+        if (rank < B) dst[(2 * rank) * TM + lane] = Yv[(m - 1) * TM + lane];
       }
       asm volatile("barrier.cluster.arrive.release;" ::: "memory");
-      if (defer0 >= 0 && lane == 0) {   // refills deferred from this phase
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        for (int d = defer0; d <= defer; d += kWarps) issue(d);
-      }
-      defer0 = defer = -1;
       asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
-      stamp(ti, 2 + p);
+      stamp(ti, 40);
+      // ---- alpha_{k-1}, beta_k = (rows of R) tau: 2B column blocks over warps
+      double2 acc0 = czero(), acc1 = czero();   // rows lane (and lane+32 for tm = 32)
+      const int nq = 2 * B;
+      for (int j = warp; j < nq; j += kCW) {
+        const int i = base + pfx[NP] + j;
+        const double2* mq = acquire(i);   // 2tm x tm, row index fastest
+        const double2* tq = tau + j * TM;
+#pragma unroll 4
+        for (int c = 0; c < TM; ++c) {
+          const double2 tv = tq[c];
+          acc0 = cfma(mq[c * N2 + lane], tv, acc0);
+          if (TM == 32) acc1 = cfma(mq[c * N2 + lane + 32], tv, acc1);
+        }
+        release(i);
+      }
+      part[warp * N2 + lane] = acc0;
+      if (TM == 32) part[warp * N2 + lane + 32] = acc1;
+      csync();
+      if (threadIdx.x < N2) {
+        double2 sacc = czero();
+        for (int w = 0; w < kCW; ++w) sacc = cadd(sacc, part[w * N2 + threadIdx.x]);
+        ab[threadIdx.x] = sacc;
+      }
+      csync();
+      stamp(ti, 41);
+      // ---- x_y = g_y - W_y alpha_{k-1} - V_y beta_k
+      for (int j = warp; j < m; j += kCW) {
+        const int i = base + pfx[NP + 1] + j;
+        const double2* ms = acquire(i);
+        const double2 acc = mvs2<TM>(rank > 0 ? ms : nullptr, rank > 0 ? ab : nullptr,
+                                     rank < B ? ms + TM2 : nullptr, rank < B ? ab + TM : nullptr,
+                                     lane);
+        if (hh == 0) Yv[j * TM + x] = csub(Yv[j * TM + x], acc);
+        release(i);
+      }
+      csync();
     }
     // ---- outputs: solution rows into u (one producer per row and pass), traces
     const int ur0 = t.ta + 1 - t.lo, ur1 = t.tb + 1 - t.lo;
-    for (int yl = warp * YPW + hh; yl < nloc; yl += kWarps * YPW) {
+    for (int yl = warp * YPW + hh; yl < m; yl += kCW * YPW) {
       const int y = Y0 + yl;
       const double2 xv = Yv[yl * TM + x];
       if (x >= ur0 && x < ur1) a.u[t.dst][(int64_t)(x + t.lo - 1) * M + y] = xv;
@@ -714,13 +1014,16 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_bcr_solve(SolveArgs a) {
       if (t.out4 >= 0 && (x == t.orow4 || x == t.orow4 + 1))
         a.trace[((int64_t)t.out4 * 2 + (x - t.orow4)) * M + y] = xv;
     }
-    cl.sync();   // traces visible to the cluster; F / Yv free for the next task
+    // traces visible to the cluster (next right-hand side), tau free again
+    asm volatile("barrier.cluster.arrive.release;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
     stamp(ti, 63);
   }
   if (a.dbg && threadIdx.x == 0 && blockIdx.x < 16)
-    for (int k = 0; k < 512; ++k) a.dbg[blockIdx.x * 512 + k] = tsm[k];
-  {
-  }
+    for (int k = 0; k < 128; ++k) {
+      a.dbg[blockIdx.x * 256 + k] = tsm[k];
+      a.dbg[blockIdx.x * 256 + 128 + k] = tprod[k];
+    }
 }
 
 __global__ void k_combine(double2* __restrict__ u, const double2* __restrict__ u2, int64_t n) {
@@ -728,59 +1031,49 @@ __global__ void k_combine(double2* __restrict__ u, const double2* __restrict__ u
   if (i < n) u[i] = cadd(u[i], __ldg(u2 + i));
 }
 
-template <int TM>
-int solve_smem(int nloc_max) { return Ring<TM>::smem(nloc_max); }
-
-template <int TM>
-cudaError_t launch_solve(const SolveArgs& a, int nfront, cudaStream_t st) {
+cudaLaunchConfig_t solve_config(int C, int nfront, int smem, cudaStream_t st,
+                                cudaLaunchAttribute* attr) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nfront * a.C, 1, 1);
+  cfg.gridDim = dim3(nfront * C, 1, 1);
   cfg.blockDim = dim3(kWarps * 32, 1, 1);
-  cfg.dynamicSmemBytes = solve_smem<TM>(a.nloc_max);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = a.C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_bcr_solve<TM>, a);
-}
-
-template <int TM>
-cudaError_t prepare_solve(int C, int nloc_max, int* max_clusters) {
-  cudaError_t e = cudaFuncSetAttribute(k_bcr_solve<TM>,
-                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_bcr_solve<TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           std::max(solve_smem<TM>(nloc_max), 1024));
-  if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(C, 1, 1);
-  cfg.blockDim = dim3(kWarps * 32, 1, 1);
-  cfg.dynamicSmemBytes = solve_smem<TM>(nloc_max);
-  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaOccupancyMaxActiveClusters(max_clusters, k_bcr_solve<TM>, &cfg);
+  return cfg;
 }
 
 template <int TM>
-int factorize(Ctx* c, Sweep* s, const std::vector<SlabInfo>& info) {
+cudaError_t prepare_solve(int C, int mmax, int* max_clusters) {
+  cudaError_t e = cudaFuncSetAttribute(k_part_solve<TM>,
+                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  const int smem = Ring<TM>::smem(mmax);
+  e = cudaFuncSetAttribute(k_part_solve<TM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = solve_config(C, 1, smem, nullptr, attr);
+  return cudaOccupancyMaxActiveClusters(max_clusters, k_part_solve<TM>, &cfg);
+}
+
+template <int TM>
+int factorize(Ctx* c, Sweep* s, const std::vector<SlabInfo>& info, const Chunks& g) {
   constexpr int TM2 = Geo<TM>::TM2;
-  const int J = s->J, M = s->M, L = s->L;
+  const int J = s->J, M = s->M, L = s->L, C = s->C, B = C - 1;
   const size_t wbytes = (size_t)J * M * TM2 * sizeof(double2);
-  double2 *D = nullptr, *Lc = nullptr, *Uc = nullptr;
+  const size_t ebytes = (size_t)J * C * TM2 * sizeof(double2);
+  double2 *D = nullptr, *Lc = nullptr, *Uc = nullptr, *EL = nullptr, *EU = nullptr;
+  double2 *Hw = nullptr, *Zw = nullptr, *tips = nullptr, *Gw = nullptr, *Zr = nullptr;
   SlabInfo* d_info = nullptr;
   unsigned long long* d_err = nullptr;
   int rc = HS_OK;
   auto cleanup = [&]() {
-    cudaFree(D); cudaFree(Lc); cudaFree(Uc); cudaFree(d_info); cudaFree(d_err);
+    cudaFree(D); cudaFree(Lc); cudaFree(Uc); cudaFree(EL); cudaFree(EU); cudaFree(Hw);
+    cudaFree(Zw); cudaFree(tips); cudaFree(Gw); cudaFree(Zr); cudaFree(d_info); cudaFree(d_err);
   };
 #define HS_TRYF(call, what)                                            \
   do {                                                                 \
@@ -790,39 +1083,66 @@ int factorize(Ctx* c, Sweep* s, const std::vector<SlabInfo>& info) {
   HS_TRYF(cudaMalloc((void**)&D, wbytes), "bcr work alloc");
   HS_TRYF(cudaMalloc((void**)&Lc, wbytes), "bcr work alloc");
   HS_TRYF(cudaMalloc((void**)&Uc, wbytes), "bcr work alloc");
+  HS_TRYF(cudaMalloc((void**)&EL, ebytes), "alloc");
+  HS_TRYF(cudaMalloc((void**)&EU, ebytes), "alloc");
+  HS_TRYF(cudaMalloc((void**)&tips, 4 * ebytes), "alloc");
   HS_TRYF(cudaMalloc((void**)&d_info, J * sizeof(SlabInfo)), "alloc");
   HS_TRYF(cudaMalloc((void**)&d_err, sizeof(unsigned long long)), "alloc");
   HS_TRYF(cudaMemcpyAsync(d_info, info.data(), J * sizeof(SlabInfo), cudaMemcpyHostToDevice,
                           c->stream), "upload");
   HS_TRYF(cudaMemsetAsync(d_err, 0xff, sizeof(unsigned long long), c->stream), "memset");
-  HS_TRYF(cudaMemsetAsync(s->eb, 0, (size_t)J * M * 2 * TM2 * sizeof(double2), c->stream),
-          "memset");
+  HS_TRYF(cudaMemsetAsync(EL, 0, ebytes, c->stream), "memset");
+  HS_TRYF(cudaMemsetAsync(EU, 0, ebytes, c->stream), "memset");
+  HS_TRYF(cudaMemsetAsync(s->eb, 0, 2 * wbytes, c->stream), "memset");
+  HS_TRYF(cudaMemsetAsync(s->kr, 0, (size_t)J * C * g.kstride * 2 * TM2 * sizeof(double2),
+                          c->stream), "memset");
   const int smem3 = 3 * TM * (TM + 1) * (int)sizeof(double2);
   const int smem4 = 4 * TM * (TM + 1) * (int)sizeof(double2);
+  const int smem7 = 7 * TM * (TM + 1) * (int)sizeof(double2);
   HS_TRYF(cudaFuncSetAttribute(k_bcr_elim<TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem3), "attr");
   HS_TRYF(cudaFuncSetAttribute(k_bcr_keep<TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem4), "attr");
-  k_bcr_init<TM><<<dim3(M, J), TM * TM, 0, c->stream>>>(d_info, M, D, Lc, Uc);
+  HS_TRYF(cudaFuncSetAttribute(k_spikes<TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem7), "attr");
+  k_bcr_init<TM><<<dim3(M, J), TM * TM, 0, c->stream>>>(d_info, g, D, Lc, Uc, EL, EU);
   c->launches++;
   HS_TRYF(cudaGetLastError(), "bcr init");
-  std::vector<int> koff(L + 1, 0);
+  if (B > 0) {   // spikes from the pristine chunk operators
+    HS_TRYF(cudaMalloc((void**)&Hw, wbytes), "spike work alloc");
+    HS_TRYF(cudaMalloc((void**)&Zw, wbytes), "spike work alloc");
+    k_spikes<TM><<<J * C, TM * TM, smem7, c->stream>>>(g, D, Lc, Uc, EL, EU, Hw, Zw, s->sp,
+                                                       tips, d_err);
+    c->launches++;
+    HS_TRYF(cudaGetLastError(), "spikes");
+    constexpr int N = 2 * TM;
+    const int NR = B * N;
+    HS_TRYF(cudaMalloc((void**)&Gw, (size_t)J * B * N * N * sizeof(double2)), "alloc");
+    HS_TRYF(cudaMalloc((void**)&Zr, (size_t)J * NR * NR * sizeof(double2)), "alloc");
+    const int smemr = 2 * N * (N + 1) * (int)sizeof(double2);
+    HS_TRYF(cudaFuncSetAttribute(k_reduced<TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smemr), "attr");
+    k_reduced<TM><<<J, 1024, smemr, c->stream>>>(g, tips, Gw, Zr, s->rk, d_err);
+    c->launches++;
+    HS_TRYF(cudaGetLastError(), "reduced system");
+  }
+  const int mmax = s->mmax;
   for (int l = 0; l < L; ++l) {
     const int sl = 1 << l;
-    const int nel = (M - 1 - sl) / (2 * sl) + 1;   // odd multiples of s below M
-    const int nkeep = (M - 1) / (2 * sl) + 1;      // even multiples (incl. 0)
-    k_bcr_elim<TM><<<dim3(nel, J), TM * TM, smem3, c->stream>>>(l, M, 0, D, Lc, Uc, s->ef,
-                                                                   s->eb, d_err);
-    c->launches++;
-    HS_TRYF(cudaGetLastError(), "bcr elim");
-    k_bcr_keep<TM><<<dim3(nkeep, J), TM * TM, smem4, c->stream>>>(l, M, koff[l], D, Lc, Uc,
-                                                                     s->kr, s->ktot);
+    const int nel = mmax - 1 >= sl ? (mmax - 1 - sl) / (2 * sl) + 1 : 0;
+    const int nkeep = (mmax - 1) / (2 * sl) + 1;
+    if (nel) {
+      k_bcr_elim<TM><<<dim3(nel, J * C), TM * TM, smem3, c->stream>>>(l, g, 0, D, Lc, Uc,
+                                                                      s->ef, s->eb, d_err);
+      c->launches++;
+      HS_TRYF(cudaGetLastError(), "bcr elim");
+    }
+    k_bcr_keep<TM><<<dim3(nkeep, J * C), TM * TM, smem4, c->stream>>>(l, g, D, Lc, Uc, s->kr);
     c->launches++;
     HS_TRYF(cudaGetLastError(), "bcr keep");
-    koff[l + 1] = koff[l] + nkeep;
   }
-  k_bcr_elim<TM><<<dim3(1, J), TM * TM, smem3, c->stream>>>(L, M, 1, D, Lc, Uc, s->ef, s->eb,
-                                                              d_err);
+  k_bcr_elim<TM><<<dim3(1, J * C), TM * TM, smem3, c->stream>>>(L, g, 1, D, Lc, Uc, s->ef,
+                                                                  s->eb, d_err);
   c->launches++;
   HS_TRYF(cudaGetLastError(), "bcr top");
   unsigned long long err = 0;
@@ -851,6 +1171,20 @@ int slot_table(const Stencil* op, int slot[3][3], Ctx* c) {
   return HS_OK;
 }
 
+Chunks make_chunks(const Sweep* s) {
+  Chunks g{};
+  g.M = s->M;
+  g.C = s->C;
+  g.L = s->L;
+  int acc = 0;
+  for (int l = 0; l < s->L; ++l) {
+    g.koff[l] = acc;
+    acc += (s->mmax - 1) / (2 << l) + 1;
+  }
+  g.kstride = std::max(1, acc);
+  return g;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -862,6 +1196,7 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   if (coarse->dim != 2)
     return set_error(c, HS_E_SHAPE, "the device sweep supports 2-D levels (3-D: not yet)");
   if (J < 2) return set_error(c, HS_E_SHAPE, "the sweep needs at least 2 subdomains");
+  if (J > kMaxTasks) return set_error(c, HS_E_SHAPE, "too many subdomains for the sweep");
   Sweep* s = new Sweep();
   s->J = J;
   s->n0 = (int)coarse->shape[0];
@@ -886,17 +1221,12 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     if (int r = slot_table(op, info[j].slot, c)) { delete s; return r; }
   }
   const int TM = s->tm, TM2 = TM * TM;
-  s->L = 0;
-  while ((1 << s->L) < M) ++s->L;
-  if (s->L > kMaxLevels) { delete s; return set_error(c, HS_E_SHAPE, "face too long"); }
-  s->ktot = 0;
-  for (int l = 0; l < s->L; ++l) s->ktot += (M - 1) / (2 << l) + 1;
-  // cluster size: ~32 face points per CTA, at most 16 CTAs, schedulable twice
-  int C = std::min(16, std::max(1, (M + 31) / 32));
+  // chunks: ~32 face points per CTA, at most 16 CTAs, cluster schedulable twice
+  int C = std::min(kMaxC, std::max(1, (M + 31) / 32));
   for (;;) {
-    const int nloc = (M + C - 1) / C + 1;
+    const int mmax = (M + C - 1) / C;
     int maxc = 0;
-    cudaError_t e = TM == 16 ? prepare_solve<16>(C, nloc, &maxc) : prepare_solve<32>(C, nloc, &maxc);
+    cudaError_t e = TM == 16 ? prepare_solve<16>(C, mmax, &maxc) : prepare_solve<32>(C, mmax, &maxc);
     if (e == cudaSuccess && maxc >= 2) break;
     cudaGetLastError();
     if (C == 1) {
@@ -906,20 +1236,28 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     C = C > 8 ? 8 : C / 2;
   }
   s->C = C;
-  s->nloc_max = (M + C - 1) / C + 1;
+  s->mmax = (M + C - 1) / C;
+  s->L = 0;
+  while ((1 << s->L) < s->mmax) ++s->L;
+  if (s->L >= kMaxLevels) { delete s; return set_error(c, HS_E_SHAPE, "face too long"); }
+  const Chunks g = make_chunks(s);
+  s->kstride = g.kstride;
+  const int B = C - 1;
 
   const size_t efb = (size_t)J * M * TM2 * sizeof(double2);
-  const size_t ebb = 2 * efb;
-  const size_t krb = (size_t)J * s->ktot * 2 * TM2 * sizeof(double2);
-  s->factor_bytes = (long long)(efb + ebb + krb);
+  const size_t krb = (size_t)J * C * g.kstride * 2 * TM2 * sizeof(double2);
+  const size_t rkb = (size_t)J * C * std::max(1, 2 * B) * 2 * TM2 * sizeof(double2);
+  s->factor_bytes = (long long)(efb * 5 + krb + (B > 0 ? rkb : 0));
   cudaError_t e = cudaMalloc((void**)&s->ef, efb);
-  if (e == cudaSuccess) e = cudaMalloc((void**)&s->eb, ebb);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&s->eb, 2 * efb);
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->kr, krb);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&s->sp, 2 * efb);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&s->rk, rkb);
   if (e != cudaSuccess) {
     sweep_destroy(s);
     return check_cuda(c, e, "factor alloc");
   }
-  int r = TM == 16 ? factorize<16>(c, s, info) : factorize<32>(c, s, info);
+  int r = TM == 16 ? factorize<16>(c, s, info, g) : factorize<32>(c, s, info, g);
   if (r) {
     sweep_destroy(s);
     return r;
@@ -993,7 +1331,8 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
       if (t.out4 == -2) t.out4 = -1;
     }
   };
-  const double rec_bytes = (double)(3 * M + 2 * s->ktot) * TM2 * 16.0;
+  const double rec_bytes = (double)(5 * M + 2 * C * g.kstride) * TM2 * 16.0 +
+                           (B > 0 ? (double)C * 2 * B * 2 * TM2 * 16.0 : 0.0);
   // one solve launch per stage (up to two concurrent fronts)
   auto emit_pass = [&](std::vector<SweepLaunch>& plan, int src,
                        std::vector<std::vector<std::vector<SweepTask>>> stages) {
@@ -1020,14 +1359,14 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   // ---- UD: forward 1..J on f; g = f - A u; backward J..1 on g ----
   {
     std::vector<SweepLaunch>& plan = s->plan[HS_VARIANT_UD];
-    std::vector<SweepTask> F, B;
+    std::vector<SweepTask> F, Bk;
     fwd_chain(1, J, F);
     clear_placeholders(F);
-    bwd_chain(J, 1, B);
-    clear_placeholders(B);
+    bwd_chain(J, 1, Bk);
+    clear_placeholders(Bk);
     emit_pass(plan, 0, {{F}});
     plan.push_back(SweepLaunch{SweepLaunch::kResidual});
-    emit_pass(plan, 1, {{B}});
+    emit_pass(plan, 1, {{Bk}});
     plan.push_back(SweepLaunch{SweepLaunch::kCombine});
     s->has_plan[HS_VARIANT_UD] = true;
   }
@@ -1035,18 +1374,18 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   if (J % 2 == 0) {
     std::vector<SweepLaunch>& plan = s->plan[HS_VARIANT_X];
     const int jm = J / 2 + 1;
-    std::vector<SweepTask> F, B, MI;
+    std::vector<SweepTask> F, Bk, MI;
     fwd_chain(1, jm - 1, F);
-    bwd_chain(J, jm + 1, B);
+    bwd_chain(J, jm + 1, Bk);
     SweepTask mi = mk(jm, (int)beta[jm - 1], (int)bt[jm]);
     want1(mi, jm);
     want3(mi, jm);
     if (!F.empty() && F.back().out2 == -2) give2(F.back(), jm - 1, mi.tin1);
-    if (!B.empty() && B.back().out4 == -2) give4(B.back(), jm + 1, mi.tin3);
+    if (!Bk.empty() && Bk.back().out4 == -2) give4(Bk.back(), jm + 1, mi.tin3);
     clear_placeholders(F);
-    clear_placeholders(B);
+    clear_placeholders(Bk);
     MI.push_back(mi);
-    emit_pass(plan, 0, {{F, B}, {MI}});
+    emit_pass(plan, 0, {{F, Bk}, {MI}});
     plan.push_back(SweepLaunch{SweepLaunch::kResidual});
     std::vector<SweepTask> MO, BB, FF;
     SweepTask mo = mk(jm, (int)bt[jm - 1], (int)beta[jm]);
@@ -1081,6 +1420,8 @@ void sweep_destroy(Sweep* s) {
   cudaFree(s->ef);
   cudaFree(s->eb);
   cudaFree(s->kr);
+  cudaFree(s->sp);
+  cudaFree(s->rk);
   cudaFree(s->trace);
   cudaFree(s->g);
   cudaFree(s->u2);
@@ -1116,20 +1457,13 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u) {
           a.ffirst[i] = i < Lh.nfront ? Lh.ffirst[i] : 0;
           a.fcount[i] = i < Lh.nfront ? Lh.fcount[i] : 0;
         }
-        a.C = s->C;
-        a.M = M;
-        a.L = s->L;
-        a.ktot = s->ktot;
-        a.nloc_max = s->nloc_max;
-        a.nslot = s->tm == 16 ? Ring<16>::nslot(s->nloc_max) : Ring<32>::nslot(s->nloc_max);
-        int acc = 0;
-        for (int l = 0; l < s->L; ++l) {
-          a.koff[l] = acc;
-          acc += (M - 1) / (2 << l) + 1;
-        }
+        a.g = make_chunks(s);
+        a.nslot = s->tm == 16 ? Ring<16>::nslot(s->mmax) : Ring<32>::nslot(s->mmax);
         a.ef = s->ef;
         a.eb = s->eb;
         a.kr = s->kr;
+        a.sp = s->sp;
+        a.rk = s->rk;
         a.src = Lh.src ? s->g : f;
         a.coarse = s->coarse->d.coeffs;
         a.ncoarse = s->coarse->d.n;
@@ -1141,31 +1475,32 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u) {
         static bool traced = false;
         unsigned long long* dbg = nullptr;
         if (trace_path && !traced && Lh.nfront == 2) {
-          cudaMalloc((void**)&dbg, 16 * 512 * sizeof(unsigned long long));
-          cudaMemsetAsync(dbg, 0, 16 * 512 * sizeof(unsigned long long), c->stream);
+          cudaMalloc((void**)&dbg, 16 * 256 * sizeof(unsigned long long));
+          cudaMemsetAsync(dbg, 0, 16 * 256 * sizeof(unsigned long long), c->stream);
         }
         a.dbg = dbg;
-
+        const int smem = s->tm == 16 ? Ring<16>::smem(s->mmax) : Ring<32>::smem(s->mmax);
+        cudaLaunchAttribute attr[1];
+        cudaLaunchConfig_t cfg = solve_config(s->C, Lh.nfront, smem, c->stream, attr);
         ProfScope ps(c, K_SWEEP_FRONT, Lh.bytes);
-        cudaError_t e = s->tm == 16 ? launch_solve<16>(a, Lh.nfront, c->stream)
-                                    : launch_solve<32>(a, Lh.nfront, c->stream);
+        cudaError_t e = s->tm == 16 ? cudaLaunchKernelEx(&cfg, k_part_solve<16>, a)
+                                    : cudaLaunchKernelEx(&cfg, k_part_solve<32>, a);
         if (e != cudaSuccess) return check_cuda(c, e, "sweep solve launch");
         HS_LAUNCH_CHECK(c, "sweep solve kernel");
         if (dbg) {
-          std::vector<unsigned long long> h(16 * 512);
+          std::vector<unsigned long long> h(16 * 256);
           cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, c->stream);
           cudaStreamSynchronize(c->stream);
           cudaFree(dbg);
           traced = true;
           if (FILE* fp = fopen(trace_path, "w")) {
-            // per CTA of cluster 0: 512 stamps (task 1): [0] start, [1] after rhs barrier,
-            // [2+p] after phase p barrier, [63] end, [64+8p+k] item 0 of phase p:
-            // k = 0 start, 1 seq, 2 mbar, 3 compute, 4 refill   (ns, relative to CTA 0 [0])
+            // per CTA of cluster 0 (task 1): [0] start, [1] rhs, [2+p] local phase p,
+            // [40] tips barrier, [41] interface solve, [63] end (ns after CTA 0 start)
             fprintf(fp, "# C=%d M=%d L=%d\n", s->C, M, s->L);
             const unsigned long long t0 = h[0];
             for (int b = 0; b < std::min(16, s->C); ++b) {
-              for (int k = 0; k < 512; ++k)
-                fprintf(fp, "%lld ", h[b * 512 + k] ? (long long)(h[b * 512 + k] - t0) : -1LL);
+              for (int k = 0; k < 256; ++k)
+                fprintf(fp, "%lld ", h[b * 256 + k] ? (long long)(h[b * 256 + k] - t0) : -1LL);
               fprintf(fp, "\n");
             }
             fclose(fp);

@@ -25,19 +25,20 @@ struct SweepLaunch {
   double bytes;             // algorithmic HBM bytes of the launch (profiler)
 };
 
-// Block-cyclic-reduction factors of every slab (see hs_sweep.cu).
+// Partitioned slab factors of every slab (see hs_sweep.cu).
 struct Sweep {
   int J = 0, M = 0, n0 = 0;
   int tm = 16;                  // padded block size (16 or 32)
-  int C = 1;                    // CTAs per cluster (face partition)
-  int L = 0;                    // reduction levels: 2^L >= M
-  int nloc_max = 0;
+  int C = 1;                    // chunks of the face = CTAs per cluster
+  int L = 0;                    // local reduction levels: 2^L >= largest chunk
+  int mmax = 0;                 // largest chunk (face points)
+  int kstride = 0;              // kept-block records per chunk
   const Stencil* coarse = nullptr;
-  double2* ef = nullptr;        // [J][M][tm^2]     Dinv at each block's elimination level
-  double2* eb = nullptr;        // [J][M][2][tm^2]  Dinv L, Dinv U (back substitution)
-  double2* kr = nullptr;        // [J][Ktot][2][tm^2] alpha, gamma of kept blocks per level
-  int* d_koff = nullptr;        // [L] level offsets into kr
-  int ktot = 0;
+  double2* ef = nullptr;        // [J][M][tm^2]          Dinv at each block's elimination level
+  double2* eb = nullptr;        // [J][M][2][tm^2]       Dinv L, Dinv U (back substitution)
+  double2* kr = nullptr;        // [J][C][kstride][2][tm^2] alpha, gamma of kept blocks
+  double2* sp = nullptr;        // [J][M][2][tm^2]       spikes W, V of every block
+  double2* rk = nullptr;        // [J][C][2(C-1)][2 tm^2] rows of the reduced-system inverse
   double2* trace = nullptr;     // [ntrace][2][M] interface traces
   double2* g = nullptr;         // [n0*M] mid-sweep residual
   double2* u2 = nullptr;        // [n0*M] second-pass contributions
