@@ -78,7 +78,7 @@ def load_library(path: Path | str | None = None):
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        p = Path(path) if path else Path(os.environ.get("HS_LIB", LIB_PATH))
         if not p.exists():
             raise OSError(f"libhsweep.so not built at {p}: run "
                           "`python -m paper_1412_0464_b200.build` (nvcc, sm_100a)")

@@ -20,41 +20,49 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v
          "--expt-relaxed-constexpr", "-I", str(PKG.parent / "include")]
 
 
-def _compile(src: Path, obj: Path, verbose: bool):
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+def _compile(src: Path, obj: Path, verbose: bool, extra=()):
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", str(src), "-o", str(obj)]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src.name}:\n{p.stderr}")
     return src.name, p.stderr
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
+def build(verbose: bool = False, force: bool = False, defines=(), out: Path | None = None) -> Path:
+    """Compile every csrc/*.cu and link the library (``defines``/``out``:
+    experiment variants, e.g. ``("HS_SWEEP_PREFETCH=0",)`` into another file)."""
+    lib = Path(out) if out else LIB
+    extra = [f"-D{d}" for d in defines]
     sources = sorted(CSRC.glob("*.cu"))
     headers = list(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "hsweep.h"]
     newest = max(p.stat().st_mtime for p in sources + headers)
-    if LIB.exists() and not force and LIB.stat().st_mtime >= newest:
-        return LIB
-    objdir = PKG / "build"
-    objdir.mkdir(exist_ok=True)
+    if lib.exists() and not force and not defines and lib.stat().st_mtime >= newest:
+        return lib
+    objdir = PKG / "build" / (lib.stem if out else "")
+    objdir.mkdir(parents=True, exist_ok=True)
     objs = []
     with cf.ThreadPoolExecutor(max_workers=min(8, len(sources))) as ex:
         futs = []
         for src in sources:
             obj = objdir / (src.stem + ".o")
             objs.append(obj)
-            futs.append(ex.submit(_compile, src, obj, verbose))
+            futs.append(ex.submit(_compile, src, obj, verbose, extra))
         for f in futs:
             name, log = f.result()
             if verbose:
                 print(f"--- {name}\n{log}")
-    tmp = LIB.with_suffix(".so.tmp")
+    lib.parent.mkdir(parents=True, exist_ok=True)
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs)]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:
         raise RuntimeError(f"link failed:\n{p.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, defines=defs,
+                out=Path(outs[0]) if outs else None))

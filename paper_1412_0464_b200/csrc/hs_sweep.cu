@@ -55,6 +55,9 @@ namespace {
 constexpr int kMaxLevels = 16;     // local BCR levels: chunks up to 65536 points
 constexpr int kWarps = 16;        // 15 consumer warps + 1 TMA producer warp
 constexpr int kCW = kWarps - 1;
+#ifndef HS_SWEEP_PREFETCH
+#define HS_SWEEP_PREFETCH 0
+#endif
 constexpr int kMaxC = 16;
 constexpr int kMaxTasks = 1024;    // slab solves per front per launch
 
@@ -838,7 +841,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     int sl = 0;
     for (int ti = 0; ti < fcount; ++ti) {
       set_slab(slabs[ti]);
-      if (lane == 0 && ti + 1 < fcount) {   // next slab's matrices into L2
+      if (HS_SWEEP_PREFETCH && lane == 0 && ti + 1 < fcount) {   // next slab's matrices into L2
         const int ns = slabs[ti + 1];
         prefetch_l2(a.ef + ((int64_t)ns * M + Y0) * TM2, (uint32_t)m * TM2 * 16);
         prefetch_l2(a.eb + ((int64_t)ns * M + Y0) * 2 * TM2, (uint32_t)m * 2 * TM2 * 16);
@@ -1000,7 +1003,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
                                      lane);
         if (hh == 0) Yv[j * TM + x] = csub(Yv[j * TM + x], acc);
         release(i);
+        if (j < 15) stamp(ti, 44 + j / kCW);
       }
+      stamp(ti, 42);
       csync();
     }
     // ---- outputs: solution rows into u (one producer per row and pass), traces
@@ -1014,6 +1019,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       if (t.out4 >= 0 && (x == t.orow4 || x == t.orow4 + 1))
         a.trace[((int64_t)t.out4 * 2 + (x - t.orow4)) * M + y] = xv;
     }
+    stamp(ti, 43);
     // traces visible to the cluster (next right-hand side), tau free again
     asm volatile("barrier.cluster.arrive.release;" ::: "memory");
     asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
