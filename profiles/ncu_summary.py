@@ -27,7 +27,7 @@ METRICS = [
 SCALE = {"usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "nsecond": 1e-3, "ns": 1e-3, "byte": 1.0, "Kbyte": 1e3,
          "Mbyte": 1e6, "Gbyte": 1e9, "%": 1.0, "": 1.0, "register/thread": 1.0}
 
-CLASS = [("k_front", "sweep_front"), ("k_bcr", "sweep_front"), ("k_stencil<", None),
+CLASS = [("k_front", "sweep_front"), ("k_bcr", "sweep_front"), ("k_part_solve", "sweep_front"), ("k_stencil<", None),
          ("k_block_dot", "krylov_dot"), ("k_block_update", "krylov_update"),
          ("k_restrict", "restrict"), ("k_prolong", "prolong"), ("k_gather", "sweep_gather")]
 MODE = {"0": "stencil", "1": "residual", "2": "jacobi", "3": "jacobi2z"}
