@@ -565,6 +565,31 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  const uint32_t a = smem_u32(bar);
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ uint32_t map_rank(const void* p, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+// 16-B store into another CTA's shared memory, completing bytes on its mbarrier
+__device__ __forceinline__ void st_async_c(uint32_t dst, double2 v, uint32_t bar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+      ::"r"(dst), "d"(v.x), "d"(v.y), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   if (bytes)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
@@ -613,7 +638,7 @@ struct Ring {
   static constexpr int SLOT = 2 * Geo<TM>::TM2;   // double2 per slot (two blocks)
   // F, Yv vectors + tau + R partials + bookkeeping, then the ring
   static int fixed(int mmax) {
-    return 2 * (mmax + 1) * TM * 16 + 2 * kMaxC * TM * 16 + (kWarps + 1) * 2 * TM * 16 +
+    return 2 * (mmax + 1) * TM * 16 + 4 * kMaxC * TM * 16 + 4 * TM * 16 + (kWarps + 1) * 2 * TM * 16 + 32 +
            (64 + kMaxTasks) * 4 + itab_len(mmax) * 8 + 384;
   }
   static int nslot(int mmax) {
@@ -643,10 +668,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   extern __shared__ __align__(128) double2 sm[];
   double2* F = sm;                                  // [mmax+1][TM] rhs / reduced rhs
   double2* Yv = F + (mmax + 1) * TM;                // [mmax+1][TM] Dinv f, then x
-  double2* tau = Yv + (mmax + 1) * TM;              // [2 kMaxC][TM] interface rhs
-  double2* part = tau + 2 * kMaxC * TM;             // [kWarps][2TM] R partial sums
+  double2* tau2 = Yv + (mmax + 1) * TM;             // [2][2 kMaxC][TM] interface rhs (by task parity)
+  double2* halo2 = tau2 + 4 * kMaxC * TM;           // [2][2][TM] neighbours' edge blocks of x
+  double2* part = halo2 + 4 * TM;                   // [kWarps][2TM] R partial sums
   double2* ab = part + kWarps * N2;                 // [2TM] alpha_{k-1}, beta_k
-  uint64_t* bars = (uint64_t*)(ab + N2);            // [NS]
+  uint64_t* xbar = (uint64_t*)(ab + N2);            // [4] tips (2), halo (2) arrival barriers
+  uint64_t* bars = xbar + 4;                        // [NS]
   volatile int* seq = (volatile int*)(bars + NS);   // [NS] item issued into a slot
   volatile int* done = seq + NS;                    // [NS] item consumed from a slot
   int* pfx = (int*)(bars + NS) + 2 * NS;            // [2L+3] items before each phase
@@ -701,10 +728,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       seq[i] = -1;
       done[i] = i - NS;   // slot i is free for item i
     }
+    for (int i = 0; i < 4; ++i) mbar_init(&xbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = threadIdx.x; i < fcount; i += blockDim.x) slabs[i] = a.tasks[ffirst + i].slab;
-  __syncthreads();
+  cl.sync();   // every CTA's barriers initialised before any remote arrival
   const int ITEMS = pfx[NP + 2];
   const int total = fcount * ITEMS;
   const int64_t kbase = (int64_t)rank * g.kstride;
@@ -822,21 +850,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     // ---- TMA producer warp: issues every item in consumption order as soon
     // as its slot is free, prefetches the next slab into L2, and takes part in
     // the cluster barriers (arriving early: it never holds data others read).
-    int nb = 0;                 // cluster barriers passed (arrived)
-    bool owe_wait = false;
-    const int per_task = B > 0 ? 2 : 1;
-    auto bar_pos = [&](int k) {   // first item consumed after barrier k
-      const int ti = k / per_task;
-      return (per_task == 2 && k % 2 == 0) ? ti * ITEMS + pfx[NP] : (ti + 1) * ITEMS;
-    };
-    const int nbar = fcount * per_task;
-    auto arrive_next = [&]() {
-      if (owe_wait) asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
-      asm volatile("barrier.cluster.arrive.release;" ::: "memory");
-      owe_wait = true;
-      ++nb;
-    };
-    int nextb = nbar > 0 ? bar_pos(0) : total;
     const int BW = max(1, min(8, NS / 2));   // items issued per batch (one lane each)
     int sl = 0;
     for (int ti = 0; ti < fcount; ++ti) {
@@ -853,15 +866,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
                       (uint32_t)(2 * B) * 2 * TM2 * 16);
         }
       }
-      // batches of up to BW items, one lane each, never across a cluster barrier
+      // batches of up to BW items, one lane each
       const int base = ti * ITEMS;
       for (int r0 = 0; r0 < ITEMS;) {
         const int i0 = base + r0;
-        while (i0 == nextb) {
-          arrive_next();
-          nextb = nb < nbar ? bar_pos(nb) : total;
-        }
-        const int cnt = min(BW, min(ITEMS - r0, nextb - i0));
+        const int cnt = min(BW, ITEMS - r0);
         if (lane < cnt) {
           const int i = i0 + lane;
           int sl_l = sl + lane;
@@ -885,14 +894,43 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
         __syncwarp();
       }
     }
-    while (nb < nbar) arrive_next();
-    if (owe_wait) asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
+    cl.sync();   // matches the consumers' exit barrier
     return;
   }
 
+  // Transmission from the previous task of this front without a trip through
+  // global memory: its solution x is still in Yv (own face points) and the
+  // neighbours' edge blocks arrive in halo (st.async + mbarrier).
+  auto trans_local = [&](const double2* halo, int prow, int p, int sign, int which, int y) {
+    const int o0 = which == 0 ? 1 : -1;
+    const int row = which == 0 ? p - 1 : p;
+    const int xr = prow + (which == 0 ? 1 : 0);   // trace row 1 feeds which 0, row 0 which 1
+    double2 acc = czero();
+#pragma unroll
+    for (int o = -1; o <= 1; ++o) {
+      if (y + o < 0 || y + o >= M) continue;
+      const int yl = y + o - Y0;
+      const double2 bv = yl < 0 ? halo[xr] : yl >= m ? halo[TM + xr] : Yv[yl * TM + xr];
+      acc = cfma(cc(o0, o, row, y), bv, acc);
+    }
+    return cscale(which == 0 ? (double)sign : (double)-sign, acc);
+  };
+  const uint32_t halo_bytes = (rank > 0 ? TM * 16 : 0) + (rank < B ? TM * 16 : 0);
+
+  SweepTask prev{};
   for (int ti = 0; ti < fcount; ++ti) {
     const SweepTask t = a.tasks[ffirst + ti];
     const int base = ti * ITEMS;
+    const int par = ti & 1;
+    double2* tau = tau2 + par * 2 * kMaxC * TM;
+    const double2* halo = halo2 + par * 2 * TM;
+    // previous task's traces consumed here straight from shared memory
+    const bool loc1 = ti > 0 && t.tin1 >= 0 && prev.out2 == t.tin1;
+    const bool loc3 = ti > 0 && t.tin3 >= 0 && prev.out4 == t.tin3;
+    if (threadIdx.x == 0) {
+      if (ti > 0) mbar_expect_tx(&xbar[2 + par], halo_bytes);
+      if (B > 0) mbar_expect_tx(&xbar[par], 2 * B * TM * 16);
+    }
     stamp(ti, 0);
     // ---- right-hand side of the owned blocks (restriction + transmission)
     for (int yl = warp * YPW + hh; yl < m; yl += kCW * YPW) {
@@ -900,11 +938,23 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       double2 v = czero();
       const int gr = x + t.lo - 1;
       if (x < t.T && gr >= t.a && gr < t.b) v = __ldg(a.src + (int64_t)gr * M + y);
-      if (t.tin1 >= 0 && (x == t.row1 || x == t.row1 + 1))
+      if (!loc1 && t.tin1 >= 0 && (x == t.row1 || x == t.row1 + 1))
         v = cadd(v, trans(t.tin1, t.row1 + t.lo, 1, x - t.row1, y));
-      if (t.tin3 >= 0 && (x == t.row3 || x == t.row3 + 1))
+      if (!loc3 && t.tin3 >= 0 && (x == t.row3 || x == t.row3 + 1))
         v = cadd(v, trans(t.tin3, t.row3 + t.lo, -1, x - t.row3, y));
       F[yl * TM + x] = v;
+    }
+    if (loc1 || loc3) {
+      mbar_wait_cluster(&xbar[2 + par], (uint32_t)((ti - 1) >> 1) & 1);
+      for (int yl = warp * YPW + hh; yl < m; yl += kCW * YPW) {
+        const int y = Y0 + yl;
+        double2 v = czero();
+        if (loc1 && (x == t.row1 || x == t.row1 + 1))
+          v = cadd(v, trans_local(halo, prev.orow2, t.row1 + t.lo, 1, x - t.row1, y));
+        if (loc3 && (x == t.row3 || x == t.row3 + 1))
+          v = cadd(v, trans_local(halo, prev.orow4, t.row3 + t.lo, -1, x - t.row3, y));
+        F[yl * TM + x] = cadd(F[yl * TM + x], v);
+      }
     }
     csync();
     stamp(ti, 1);
@@ -962,12 +1012,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       // ---- push this chunk's tips g[first], g[last] into every CTA's tau:
       // tau block b = (g_b[last], g_{b+1}[first]) -> tm-slots 2b, 2b+1
       for (int d = warp; d < C && lane < TM; d += kCW) {
-        double2* dst = cl.map_shared_rank(tau, d);
-        if (rank > 0) dst[(2 * (rank - 1) + 1) * TM + lane] = Yv[lane];
-        if (rank < B) dst[(2 * rank) * TM + lane] = Yv[(m - 1) * TM + lane];
+        const uint32_t bar = map_rank(&xbar[par], d);
+        if (rank > 0) st_async_c(map_rank(&tau[(2 * (rank - 1) + 1) * TM + lane], d), Yv[lane], bar);
+        if (rank < B) st_async_c(map_rank(&tau[(2 * rank) * TM + lane], d), Yv[(m - 1) * TM + lane], bar);
       }
-      asm volatile("barrier.cluster.arrive.release;" ::: "memory");
-      asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
+      mbar_wait_cluster(&xbar[par], (uint32_t)(ti >> 1) & 1);
       stamp(ti, 40);
       // ---- alpha_{k-1}, beta_k = (rows of R) tau: 2B column blocks over warps
       double2 acc0 = czero(), acc1 = czero();   // rows lane (and lane+32 for tm = 32)
@@ -1008,6 +1057,16 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       stamp(ti, 42);
       csync();
     }
+    // ---- edge blocks of x to the neighbours (next task's transmission halo)
+    if (ti + 1 < fcount && lane < TM) {
+      const int nb = ((ti + 1) & 1) * 2 * TM;
+      if (warp == 0 && rank > 0)
+        st_async_c(map_rank(&halo2[nb + TM + lane], rank - 1), Yv[lane],
+                   map_rank(&xbar[2 + ((ti + 1) & 1)], rank - 1));
+      if (warp == 1 && rank < B)
+        st_async_c(map_rank(&halo2[nb + lane], rank + 1), Yv[(m - 1) * TM + lane],
+                   map_rank(&xbar[2 + ((ti + 1) & 1)], rank + 1));
+    }
     // ---- outputs: solution rows into u (one producer per row and pass), traces
     const int ur0 = t.ta + 1 - t.lo, ur1 = t.tb + 1 - t.lo;
     for (int yl = warp * YPW + hh; yl < m; yl += kCW * YPW) {
@@ -1020,11 +1079,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
         a.trace[((int64_t)t.out4 * 2 + (x - t.orow4)) * M + y] = xv;
     }
     stamp(ti, 43);
-    // traces visible to the cluster (next right-hand side), tau free again
-    asm volatile("barrier.cluster.arrive.release;" ::: "memory");
-    asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
+    prev = t;
     stamp(ti, 63);
   }
+  cl.sync();   // no CTA leaves while a peer may still write its shared memory
   if (a.dbg && threadIdx.x == 0 && blockIdx.x < 16)
     for (int k = 0; k < 128; ++k) {
       a.dbg[blockIdx.x * 256 + k] = tsm[k];
