@@ -58,6 +58,12 @@ constexpr int kCW = kWarps - 1;
 #ifndef HS_SWEEP_PREFETCH
 #define HS_SWEEP_PREFETCH 0
 #endif
+#ifndef HS_SWEEP_HALF      // tm 16: one ring item per half warp
+#define HS_SWEEP_HALF 0
+#endif
+#ifndef HS_SWEEP_L2NEXT    // producer prefetches each item of the next slab into L2
+#define HS_SWEEP_L2NEXT 0
+#endif
 constexpr int kMaxC = 16;
 constexpr int kMaxTasks = 1024;    // slab solves per front per launch
 
@@ -83,6 +89,7 @@ struct SlabInfo {
 // chunk geometry: chunk k covers face points [k M / C, (k+1) M / C)
 struct Chunks {
   int M, C, L, kstride;
+  int q;                   // dense top: blocks per chunk left after L levels
   int koff[kMaxLevels];
   __host__ __device__ int y0(int k) const { return (int)((int64_t)k * M / C); }
   __host__ __device__ int len(int k) const { return y0(k + 1) - y0(k); }
@@ -132,11 +139,11 @@ k_bcr_init(const SlabInfo* __restrict__ slabs, Chunks g, double2* __restrict__ D
 // In-place Gauss-Jordan inversion with partial pivoting of an N x N matrix A
 // (smem, pitch N+1) into Inv; any block size, threads loop over elements
 // (blockDim.x >= 256 assumed for the register staging below).
-template <int N>
+template <int N, int NT = 256>
 __device__ void gj_invert(double2 (*A)[N + 1], double2 (*Inv)[N + 1], int* piv_row,
                           double* piv_abs, unsigned long long* err, unsigned long long code) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  constexpr int PER = (N * N + 255) / 256;
+  const int tid = threadIdx.x, nt = blockDim.x;   // nt >= NT
+  constexpr int PER = (N * N + NT - 1) / NT;
   for (int e = tid; e < N * N; e += nt) Inv[e / N][e % N] = make_double2(e / N == e % N, 0.0);
   __syncthreads();
   for (int p = 0; p < N; ++p) {
@@ -321,6 +328,46 @@ k_bcr_keep(int level, Chunks g, double2* __restrict__ D, double2* __restrict__ L
   }
   Lc[at(y) + r * TM + c] = lnew;
   Uc[at(y) + r * TM + c] = unew;
+}
+
+// Dense top of every chunk (one CTA per slab x chunk): after L cyclic-reduction
+// levels the chunk's kept blocks (local multiples of S = 2^L, q_k of them)
+// form a block-tridiagonal system D, L, U; its inverse (padded to Q blocks
+// with identity) is stored lane-major per block: qd[slab][k][r][c].
+template <int TM, int Q>
+__global__ void __launch_bounds__(1024)
+k_dense_top(Chunks g, const double2* __restrict__ D, const double2* __restrict__ Lc,
+            const double2* __restrict__ Uc, double2* __restrict__ qd,
+            unsigned long long* __restrict__ err) {
+  constexpr int TM2 = Geo<TM>::TM2;
+  constexpr int N = Q * TM;
+  const int slab = blockIdx.x / g.C, k = blockIdx.x % g.C, M = g.M;
+  const int S = 1 << g.L, Y0 = g.y0(k);
+  const int qk = (g.len(k) - 1) / S + 1;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double2(*A)[N + 1] = reinterpret_cast<double2(*)[N + 1]>(smraw);
+  double2(*Inv)[N + 1] = A + N;
+  __shared__ int piv_row;
+  __shared__ double piv_abs;
+  for (int e = threadIdx.x; e < N * N; e += blockDim.x) {
+    const int R = e / N, Cc = e % N;
+    const int br = R / TM, bc = Cc / TM, r = R % TM, c = Cc % TM;
+    double2 v = make_double2(R == Cc ? 1.0 : 0.0, 0.0);
+    if (br < qk && bc < qk) {
+      const int64_t at = ((int64_t)slab * M + Y0 + br * S) * TM2 + r * TM + c;
+      v = bc == br ? D[at] : bc == br - 1 ? Lc[at] : bc == br + 1 ? Uc[at] : czero();
+    }
+    A[R][Cc] = v;
+  }
+  __syncthreads();
+  const unsigned long long code =
+      ((unsigned long long)slab << 40) | ((unsigned long long)Y0 * TM & 0xffffffffffull);
+  gj_invert<N, 1024>(A, Inv, &piv_row, &piv_abs, err, code);
+  double2* out = qd + ((int64_t)slab * g.C + k) * Q * Q * TM2;
+  for (int e = threadIdx.x; e < N * N; e += blockDim.x) {
+    const int R = e / N, Cc = e % N;
+    out[((R / TM) * Q + Cc / TM) * TM2 + lm<TM>(R % TM, Cc % TM)] = Inv[R][Cc];
+  }
 }
 
 // Spikes of every chunk by one block-Thomas pass (one CTA per slab x chunk):
@@ -524,6 +571,7 @@ struct SolveArgs {
   const double2* kr;
   const double2* sp;
   const double2* rk;
+  const double2* qd;
   const double2* src;      // right-hand side field (n0 x M)
   const double2* coarse;   // global coarse operator [S][n0*M] (transmission couplings)
   int64_t ncoarse;
@@ -623,15 +671,43 @@ __device__ __forceinline__ double2 mvs2(const double2* m0, const double2* v0, co
 }
 
 // items of one chunk solve: <= 3m + 2L local, 2(C-1) R blocks, m spike blocks
-__host__ __device__ inline int itab_len(int mmax) { return 4 * mmax + 2 * kMaxLevels + 2 * kMaxC; }
+__host__ __device__ inline int itab_len(int mmax) { return 4 * mmax + 2 * kMaxLevels + 2 * kMaxC + 16; }
 
 // Item copy descriptor: array (bits 29-31; 7 = none), double length (bit 28),
 // offset in double2 from the array's slab base (bits 0-27).
-enum ItemArray : uint32_t { kArrEf = 0, kArrEb = 1, kArrKr = 2, kArrRk = 3, kArrSp = 4 };
+enum ItemArray : uint32_t { kArrEf = 0, kArrEb = 1, kArrKr = 2, kArrRk = 3, kArrSp = 4, kArrQd = 5 };
 __host__ __device__ constexpr uint32_t item_enc(uint32_t arr, int64_t off, bool dbl = false) {
   return (arr << 29) | (dbl ? (1u << 28) : 0u) | (uint32_t)off;
 }
 constexpr uint32_t kItemNone = 0xffffffffu;
+
+// One item per half warp for tm = 16 (lane row x = lane % 16 of the half's
+// item, all 16 columns), the whole warp for tm = 32: row x of A0 v0 + A1 v1.
+template <int TM, int HW>
+__device__ __forceinline__ double2 mvx(const double2* m0, const double2* v0, const double2* m1,
+                                       const double2* v1, int lane) {
+  if constexpr (HW == 1) {
+    return mvs2<TM>(m0, v0, m1, v1, lane);
+  } else {
+    const int x = lane % 16;
+    double2 a0 = czero(), a1 = czero(), a2 = czero(), a3 = czero();
+    if (v0) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {   // lm<16>(x, c) = (c % 8) * 32 + (c / 8) * 16 + x
+        a0 = cfma(m0[k * 32 + x], v0[k], a0);
+        a1 = cfma(m0[k * 32 + 16 + x], v0[k + 8], a1);
+      }
+    }
+    if (v1) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        a2 = cfma(m1[k * 32 + x], v1[k], a2);
+        a3 = cfma(m1[k * 32 + 16 + x], v1[k + 8], a3);
+      }
+    }
+    return cadd(cadd(a0, a1), cadd(a2, a3));
+  }
+}
 
 template <int TM>
 struct Ring {
@@ -664,6 +740,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   const int mmax = (M + C - 1) / C;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int x = lane % TM, hh = lane / TM;
+  constexpr int HW = (TM == 16 && HS_SWEEP_HALF) ? 2 : 1;   // items per warp pass
+  const int sub = HW == 2 ? hh : 0;      // this lane's item within the pass
+  const bool wr = HW == 2 || hh == 0;    // lane owns the result row it computed
   const int NS = a.nslot;
   extern __shared__ __align__(128) double2 sm[];
   double2* F = sm;                                  // [mmax+1][TM] rhs / reduced rhs
@@ -704,13 +783,24 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     return cscale(which == 0 ? (double)sign : (double)-sign, acc);
   };
 
-  // Item streams of one slab solve of this CTA: local BCR phases
-  // (p < L forward level p, p >= L backward level 2L-1-p), then the 2B column
-  // blocks of R, then the m spike blocks.  Item j of a phase -> warp j % 16.
-  const int NP = 2 * L;
-  auto ph_level = [&](int p) { return p < L ? p : NP - 1 - p; };
-  auto ph_first = [&](int p) -> int { return p >= L ? (1 << ph_level(p)) : 0; };
+  // Item streams of one slab solve of this CTA: local phases (p < L forward
+  // cyclic-reduction level p; p == L the dense top, items (row r, column pair
+  // cp) of the level-L inverse; p > L back substitution of level 2L-p), then
+  // the 2B column blocks of R, then the m spike blocks.
+  const int NP = 2 * L + 1;
+  const int S = 1 << L;
+  const int qk = (m - 1) / S + 1;            // dense-top blocks of this chunk
+  const int QP = (qk + 1) / 2;               // their column pairs
+  auto ph_level = [&](int p) { return p <= L ? p : 2 * L - p; };
+  auto ph_first = [&](int p) -> int { return p > L ? (1 << ph_level(p)) : 0; };
   auto ph_step = [&](int p) { return (p < L ? 1 : 2) << ph_level(p); };
+  // face point of item j of a cyclic-reduction phase (forward phases list the
+  // eliminated points first, so neighbouring items share a branch)
+  auto item_yl = [&](int p, int j) -> int {
+    if (p > L) return ph_first(p) + j * ph_step(p);
+    const int ne = (pfx[p + 1] - pfx[p]) / 2;
+    return (j < ne ? 2 * j + 1 : 2 * (j - ne)) << p;
+  };
   const int ffirst = front ? a.ffirst[1] : a.ffirst[0];
   const int fcount = front ? a.fcount[1] : a.fcount[0];
   if (threadIdx.x == 0) {
@@ -718,7 +808,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     for (int p = 0; p < NP; ++p) {
       pfx[p] = acc;
       const int f = ph_first(p);
-      if (f < m) acc += (m - 1 - f) / ph_step(p) + 1;
+      if (p == L) acc += qk * QP;
+      else if (f < m) acc += (m - 1 - f) / ph_step(p) + 1;
     }
     pfx[NP] = acc;                               // R column blocks
     pfx[NP + 1] = acc + (B > 0 ? 2 * B : 0);     // spikes
@@ -745,9 +836,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     while (pfx[p + 1] <= r) ++p;
     const int j = r - pfx[p];
     uint2 e = make_uint2(kItemNone, kItemNone);
-    if (p < NP) {
+    if (p == L) {           // dense top: blocks (r, 2cp) and (r, 2cp + 1)
+      const int r = j / QP, c0 = 2 * (j % QP);
+      e.x = item_enc(kArrQd, (((int64_t)rank * g.q + r) * g.q + c0) * TM2, c0 + 1 < qk);
+    } else if (p < NP) {
       const int l = ph_level(p), s = 1 << l;
-      const int yl = ph_first(p) + j * ph_step(p);
+      const int yl = item_yl(p, j);
       const int y = Y0 + yl;
       if (p < L) {
         if ((yl >> l) & 1) {
@@ -756,7 +850,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
           const int64_t k2 = (kbase + g.koff[l] + (yl >> (l + 1))) * 2 * TM2;
           if (yl - s >= 0) e.x = item_enc(kArrKr, k2);
           if (yl + s < m) e.y = item_enc(kArrKr, k2 + TM2);
-          if (yl == 0 && l == L - 1) e.x = item_enc(kArrEf, (int64_t)Y0 * TM2);   // top Dinv
         }
       } else {
         const int64_t e2 = (int64_t)y * 2 * TM2;
@@ -773,25 +866,41 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   __syncthreads();
 
   // producer state: the current task's slab base of every factor array
-  const double2* sbase[5];
-  auto set_slab = [&](int slab) {
-    sbase[kArrEf] = a.ef + (int64_t)slab * M * TM2;
-    sbase[kArrEb] = a.eb + (int64_t)slab * M * 2 * TM2;
-    sbase[kArrKr] = a.kr + (int64_t)slab * C * g.kstride * 2 * TM2;
-    sbase[kArrRk] = a.rk + (int64_t)slab * C * (2 * B) * 2 * TM2;
-    sbase[kArrSp] = a.sp + (int64_t)slab * M * 2 * TM2;
+  const double2* sbase[6];
+  auto slab_bases = [&](int slab, const double2** sb) {
+    sb[kArrEf] = a.ef + (int64_t)slab * M * TM2;
+    sb[kArrEb] = a.eb + (int64_t)slab * M * 2 * TM2;
+    sb[kArrKr] = a.kr + (int64_t)slab * C * g.kstride * 2 * TM2;
+    sb[kArrRk] = a.rk + (int64_t)slab * C * (2 * B) * 2 * TM2;
+    sb[kArrSp] = a.sp + (int64_t)slab * M * 2 * TM2;
+    sb[kArrQd] = a.qd + (int64_t)slab * C * g.q * g.q * TM2;
   };
+  auto set_slab = [&](int slab) { slab_bases(slab, sbase); };
   auto src_of = [&](uint32_t e) -> const double2* {
     const uint32_t arr = e >> 29;
     const double2* b = arr == kArrEf ? sbase[0]
                        : arr == kArrEb ? sbase[1]
                        : arr == kArrKr ? sbase[2]
                        : arr == kArrRk ? sbase[3]
-                                       : sbase[4];
+                       : arr == kArrSp ? sbase[4]
+                                       : sbase[5];
     return b + (e & 0x0fffffffu);
   };
-  auto issue = [&](int r, int sl) {   // one lane: item r of the current task into slot sl
+  const double2* nbase[6];   // next task's slab bases (L2 prefetch)
+  auto issue = [&](int r, int sl, bool pf) {   // one lane: item r of the current task into slot sl
     const uint2 e = itab[r];
+    if (HS_SWEEP_L2NEXT && pf) {   // the same item of the next slab into L2
+      auto nsrc = [&](uint32_t q) {
+        const uint32_t arr = q >> 29;
+        const double2* b = arr == kArrEf ? nbase[0] : arr == kArrEb ? nbase[1]
+                         : arr == kArrKr ? nbase[2] : arr == kArrRk ? nbase[3]
+                         : arr == kArrSp ? nbase[4] : nbase[5];
+        return b + (q & 0x0fffffffu);
+      };
+      constexpr uint32_t mb1 = TM2 * 16;
+      if (e.x != kItemNone) prefetch_l2(nsrc(e.x), (e.x >> 28 & 1) ? 2 * mb1 : mb1);
+      if (e.y != kItemNone) prefetch_l2(nsrc(e.y), mb1);
+    }
     double2* slot = ring + sl * SLOT;
     uint64_t* bar = &bars[sl];
     constexpr uint32_t mb = TM2 * 16;
@@ -838,9 +947,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   };
   // The warp's reads of the slot have returned (their values are consumed
   // before the __syncwarp), so the producer's async-proxy refill cannot race.
-  auto release = [&](int i) {   // whole consumer warp, after its last read of the slot
+  auto release = [&](int i, bool has) {   // whole consumer warp, after its last read of the slot
     __syncwarp();
-    if (lane == 0) done[i % NS] = i;
+    if (has && lane % (32 / HW) == 0) done[i % NS] = i;
   };
   auto csync = [&]() {   // consumer warps only (the producer never joins)
     asm volatile("bar.sync 1, %0;" ::"r"(kCW * 32) : "memory");
@@ -854,6 +963,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     int sl = 0;
     for (int ti = 0; ti < fcount; ++ti) {
       set_slab(slabs[ti]);
+      const bool pf = ti + 1 < fcount;
+      if (pf) slab_bases(slabs[ti + 1], nbase);
       if (HS_SWEEP_PREFETCH && lane == 0 && ti + 1 < fcount) {   // next slab's matrices into L2
         const int ns = slabs[ti + 1];
         prefetch_l2(a.ef + ((int64_t)ns * M + Y0) * TM2, (uint32_t)m * TM2 * 16);
@@ -880,7 +991,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
           if (a.dbg && k >= 0 && k < 64) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
           while (done[sl_l] != i - NS) {
           }
-          issue(r0 + lane, sl_l);
+          issue(r0 + lane, sl_l, pf);
           seq[sl_l] = i;
           if (a.dbg && k >= 0 && k < 64) {
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
@@ -958,54 +1069,58 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     }
     csync();
     stamp(ti, 1);
-    // ---- chunk-local BCR: forward reduction, top solve, back substitution
-    if (L == 0) {   // single-block chunk: x = Dinv f (Dinv via the global pointer)
-      if (warp == 0) {
-        const double2* e0 = a.ef + ((int64_t)slabs[ti] * M + Y0) * TM2;
-        double2 acc = czero();
-        for (int c = 0; c < TM; ++c) acc = cfma(__ldg(e0 + lm<TM>(x, c)), F[c], acc);
-        if (hh == 0) Yv[x] = acc;
-      }
-      csync();
-    }
+    // ---- chunk-local solve: L cyclic-reduction levels, the dense top, back substitution
     for (int p = 0; p < NP; ++p) {
       const int l = ph_level(p), s = 1 << l;
-      const int f0 = ph_first(p), st = ph_step(p);
       const int cnt = pfx[p + 1] - pfx[p];
-      for (int j = warp; j < cnt; j += kCW) {
-        const int yl = f0 + j * st;
+      for (int jp = warp * HW; jp < cnt; jp += kCW * HW) {
+        const int j = jp + sub;
+        const bool has = j < cnt;
+        const int yl = has && p != L ? item_yl(p, j) : 0;
         const int i = base + pfx[p] + j;
         dbg_ti = ti; dbg_p = p; dbg_j = j;
-        const double2* m0 = acquire(i);
+        const double2* m0 = has ? acquire(i) : nullptr;
         const double2* m1 = m0 + TM2;
-        if (p < L) {
-          if ((yl / s) & 1) {   // eliminated at this level: y = Dinv f
-            const double2 r = mvs2<TM>(m0, F + yl * TM, nullptr, nullptr, lane);
-            if (hh == 0) Yv[yl * TM + x] = r;
-          } else {              // kept: f -= alpha f_{y-s} + gamma f_{y+s}
-            const bool hl = yl - s >= 0, hr = yl + s < m;
-            const double2 acc = mvs2<TM>(hl ? m0 : nullptr, hl ? F + (yl - s) * TM : nullptr,
-                                         hr ? m1 : nullptr, hr ? F + (yl + s) * TM : nullptr,
-                                         lane);
-            if (hh == 0) F[yl * TM + x] = csub(F[yl * TM + x], acc);
-            if (yl == 0 && l == L - 1) {   // top of the reduction: x_0 = Dinv_0 f_0
-              __syncwarp();
-              const double2 r = mvs2<TM>(m0, F, nullptr, nullptr, lane);
-              if (hh == 0) Yv[x] = r;
+        if (has) {
+          if (p == L) {            // partial x_r += Q[r][c0] f_c0 + Q[r][c0+1] f_c0+1
+            const int c0 = 2 * (j % QP);
+            const bool two = c0 + 1 < qk;
+            const double2 acc = mvx<TM, HW>(m0, F + c0 * S * TM, two ? m1 : nullptr,
+                                            two ? F + (c0 + 1) * S * TM : nullptr, lane);
+            if (wr) part[j * TM + x] = acc;
+          } else if (p < L) {
+            if ((yl >> l) & 1) {   // eliminated at this level: y = Dinv f
+              const double2 r = mvx<TM, HW>(m0, F + yl * TM, nullptr, nullptr, lane);
+              if (wr) Yv[yl * TM + x] = r;
+            } else {               // kept: f -= alpha f_{y-s} + gamma f_{y+s}
+              const bool hl = yl - s >= 0, hr = yl + s < m;
+              const double2 acc = mvx<TM, HW>(hl ? m0 : nullptr, hl ? F + (yl - s) * TM : nullptr,
+                                          hr ? m1 : nullptr, hr ? F + (yl + s) * TM : nullptr,
+                                          lane);
+              if (wr) F[yl * TM + x] = csub(F[yl * TM + x], acc);
             }
+          } else {                 // x_y = Dinv f - (Dinv L) x_{y-s} - (Dinv U) x_{y+s}
+            const bool hl = yl - s >= 0, hr = yl + s < m;
+            const double2 acc = mvx<TM, HW>(hl ? m0 : nullptr, hl ? Yv + (yl - s) * TM : nullptr,
+                                        hr ? m1 : nullptr, hr ? Yv + (yl + s) * TM : nullptr,
+                                        lane);
+            if (wr) Yv[yl * TM + x] = csub(Yv[yl * TM + x], acc);
           }
-        } else {                // x_y = Dinv f - (Dinv L) x_{y-s} - (Dinv U) x_{y+s}
-          const bool hl = yl - s >= 0, hr = yl + s < m;
-          const double2 acc = mvs2<TM>(hl ? m0 : nullptr, hl ? Yv + (yl - s) * TM : nullptr,
-                                       hr ? m1 : nullptr, hr ? Yv + (yl + s) * TM : nullptr,
-                                       lane);
-          if (hh == 0) Yv[yl * TM + x] = csub(Yv[yl * TM + x], acc);
         }
         stamp2(ti, p, j, 3);
-        release(i);
+        release(i, has);
         stamp2(ti, p, j, 4);
       }
       csync();
+      if (p == L) {   // x at the level-L points = sum of the column-pair partials
+        for (int t = threadIdx.x; t < qk * TM; t += kCW * 32) {
+          const int r = t / TM, xx = t % TM;
+          double2 acc = czero();
+          for (int cp = 0; cp < QP; ++cp) acc = cadd(acc, part[(r * QP + cp) * TM + xx]);
+          Yv[r * S * TM + xx] = acc;
+        }
+        csync();
+      }
       stamp(ti, 2 + p);
     }
     if (B > 0) {
@@ -1019,22 +1134,34 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       mbar_wait_cluster(&xbar[par], (uint32_t)(ti >> 1) & 1);
       stamp(ti, 40);
       // ---- alpha_{k-1}, beta_k = (rows of R) tau: 2B column blocks over warps
-      double2 acc0 = czero(), acc1 = czero();   // rows lane (and lane+32 for tm = 32)
+      // rows r0 = lane (tm 32) or x (tm 16, per half) and r0 + 32 / r0 + 16
+      double2 acc0 = czero(), acc1 = czero();
       const int nq = 2 * B;
-      for (int j = warp; j < nq; j += kCW) {
+      const int r0 = HW == 1 ? lane : x, r1 = r0 + (HW == 1 ? 32 : 16);   // r1 unused: tm 16, HW 1
+      for (int jp = warp * HW; jp < nq; jp += kCW * HW) {
+        const int j = jp + sub;
+        const bool has = j < nq;
         const int i = base + pfx[NP] + j;
-        const double2* mq = acquire(i);   // 2tm x tm, row index fastest
-        const double2* tq = tau + j * TM;
+        if (has) {
+          const double2* mq = acquire(i);   // 2tm x tm, row index fastest
+          const double2* tq = tau + j * TM;
 #pragma unroll 4
-        for (int c = 0; c < TM; ++c) {
-          const double2 tv = tq[c];
-          acc0 = cfma(mq[c * N2 + lane], tv, acc0);
-          if (TM == 32) acc1 = cfma(mq[c * N2 + lane + 32], tv, acc1);
+          for (int c = 0; c < TM; ++c) {
+            const double2 tv = tq[c];
+            acc0 = cfma(mq[c * N2 + r0], tv, acc0);
+            if (HW == 2 || TM == 32) acc1 = cfma(mq[c * N2 + r1], tv, acc1);
+          }
         }
-        release(i);
+        release(i, has);
       }
-      part[warp * N2 + lane] = acc0;
-      if (TM == 32) part[warp * N2 + lane + 32] = acc1;
+      if (HW == 2) {   // both halves' items hold rows x and x + 16
+        acc0 = cadd(acc0, shfl_xor_c(acc0, 16));
+        acc1 = cadd(acc1, shfl_xor_c(acc1, 16));
+      }
+      if (lane < 32 / HW) {
+        part[warp * N2 + r0] = acc0;
+        if (HW == 2 || TM == 32) part[warp * N2 + r1] = acc1;
+      }
       csync();
       if (threadIdx.x < N2) {
         double2 sacc = czero();
@@ -1044,15 +1171,18 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       csync();
       stamp(ti, 41);
       // ---- x_y = g_y - W_y alpha_{k-1} - V_y beta_k
-      for (int j = warp; j < m; j += kCW) {
+      for (int jp = warp * HW; jp < m; jp += kCW * HW) {
+        const int j = jp + sub;
+        const bool has = j < m;
         const int i = base + pfx[NP + 1] + j;
-        const double2* ms = acquire(i);
-        const double2 acc = mvs2<TM>(rank > 0 ? ms : nullptr, rank > 0 ? ab : nullptr,
-                                     rank < B ? ms + TM2 : nullptr, rank < B ? ab + TM : nullptr,
-                                     lane);
-        if (hh == 0) Yv[j * TM + x] = csub(Yv[j * TM + x], acc);
-        release(i);
-        if (j < 15) stamp(ti, 44 + j / kCW);
+        if (has) {
+          const double2* ms = acquire(i);
+          const double2 acc = mvx<TM, HW>(rank > 0 ? ms : nullptr, rank > 0 ? ab : nullptr,
+                                      rank < B ? ms + TM2 : nullptr, rank < B ? ab + TM : nullptr,
+                                      lane);
+          if (wr) Yv[j * TM + x] = csub(Yv[j * TM + x], acc);
+        }
+        release(i, has);
       }
       stamp(ti, 42);
       csync();
@@ -1122,6 +1252,39 @@ cudaError_t prepare_solve(int C, int mmax, int* max_clusters) {
   cudaLaunchAttribute attr[1];
   cudaLaunchConfig_t cfg = solve_config(C, 1, smem, nullptr, attr);
   return cudaOccupancyMaxActiveClusters(max_clusters, k_part_solve<TM>, &cfg);
+}
+
+template <int TM, int Q>
+cudaError_t launch_dense_top_q(Ctx* c, const Chunks& g, int J, const double2* D, const double2* Lc,
+                               const double2* Uc, double2* qd, unsigned long long* err) {
+  constexpr int N = Q * TM;
+  const int smem = 2 * N * (N + 1) * (int)sizeof(double2);
+  cudaError_t e = cudaFuncSetAttribute(k_dense_top<TM, Q>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k_dense_top<TM, Q><<<J * g.C, 1024, smem, c->stream>>>(g, D, Lc, Uc, qd, err);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+template <int TM>
+cudaError_t launch_dense_top(Ctx* c, const Chunks& g, int J, const double2* D, const double2* Lc,
+                             const double2* Uc, double2* qd, unsigned long long* err) {
+  if constexpr (TM == 16) {
+    switch (g.q) {
+      case 1: return launch_dense_top_q<16, 1>(c, g, J, D, Lc, Uc, qd, err);
+      case 2: return launch_dense_top_q<16, 2>(c, g, J, D, Lc, Uc, qd, err);
+      case 3: return launch_dense_top_q<16, 3>(c, g, J, D, Lc, Uc, qd, err);
+      case 4: return launch_dense_top_q<16, 4>(c, g, J, D, Lc, Uc, qd, err);
+      case 5: return launch_dense_top_q<16, 5>(c, g, J, D, Lc, Uc, qd, err);
+    }
+  } else {
+    switch (g.q) {
+      case 1: return launch_dense_top_q<32, 1>(c, g, J, D, Lc, Uc, qd, err);
+      case 2: return launch_dense_top_q<32, 2>(c, g, J, D, Lc, Uc, qd, err);
+    }
+  }
+  return cudaErrorInvalidValue;
 }
 
 template <int TM>
@@ -1205,10 +1368,7 @@ int factorize(Ctx* c, Sweep* s, const std::vector<SlabInfo>& info, const Chunks&
     c->launches++;
     HS_TRYF(cudaGetLastError(), "bcr keep");
   }
-  k_bcr_elim<TM><<<dim3(1, J * C), TM * TM, smem3, c->stream>>>(L, g, 1, D, Lc, Uc, s->ef,
-                                                                  s->eb, d_err);
-  c->launches++;
-  HS_TRYF(cudaGetLastError(), "bcr top");
+  HS_TRYF(launch_dense_top<TM>(c, g, J, D, Lc, Uc, s->qd, d_err), "dense top");
   unsigned long long err = 0;
   HS_TRYF(cudaMemcpyAsync(&err, d_err, sizeof err, cudaMemcpyDeviceToHost, c->stream), "err");
   HS_TRYF(cudaStreamSynchronize(c->stream), "factor sync");
@@ -1240,6 +1400,7 @@ Chunks make_chunks(const Sweep* s) {
   g.M = s->M;
   g.C = s->C;
   g.L = s->L;
+  g.q = s->q;
   int acc = 0;
   for (int l = 0; l < s->L; ++l) {
     g.koff[l] = acc;
@@ -1301,8 +1462,12 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   }
   s->C = C;
   s->mmax = (M + C - 1) / C;
+  // cyclic reduction until at most qmax blocks per chunk are left, then a
+  // dense inverse of that reduced system (qmax blocks fit the setup's smem)
+  const int qmax = TM == 16 ? 5 : 2;
   s->L = 0;
-  while ((1 << s->L) < s->mmax) ++s->L;
+  while ((s->mmax - 1) / (1 << s->L) + 1 > qmax) ++s->L;
+  s->q = (s->mmax - 1) / (1 << s->L) + 1;
   if (s->L >= kMaxLevels) { delete s; return set_error(c, HS_E_SHAPE, "face too long"); }
   const Chunks g = make_chunks(s);
   s->kstride = g.kstride;
@@ -1311,12 +1476,14 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   const size_t efb = (size_t)J * M * TM2 * sizeof(double2);
   const size_t krb = (size_t)J * C * g.kstride * 2 * TM2 * sizeof(double2);
   const size_t rkb = (size_t)J * C * std::max(1, 2 * B) * 2 * TM2 * sizeof(double2);
-  s->factor_bytes = (long long)(efb * 5 + krb + (B > 0 ? rkb : 0));
+  const size_t qdb = (size_t)J * C * s->q * s->q * TM2 * sizeof(double2);
+  s->factor_bytes = (long long)(efb * 5 + krb + qdb + (B > 0 ? rkb : 0));
   cudaError_t e = cudaMalloc((void**)&s->ef, efb);
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->eb, 2 * efb);
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->kr, krb);
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->sp, 2 * efb);
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->rk, rkb);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&s->qd, qdb);
   if (e != cudaSuccess) {
     sweep_destroy(s);
     return check_cuda(c, e, "factor alloc");
@@ -1395,8 +1562,22 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
       if (t.out4 == -2) t.out4 = -1;
     }
   };
-  const double rec_bytes = (double)(5 * M + 2 * C * g.kstride) * TM2 * 16.0 +
-                           (B > 0 ? (double)C * 2 * B * 2 * TM2 * 16.0 : 0.0);
+  // factor blocks streamed per slab solve (exactly the items of k_part_solve)
+  double rec_blocks = 0;
+  for (int k = 0; k < C; ++k) {
+    const int m = g.len(k), L = s->L;
+    for (int l = 0; l < L; ++l) {
+      const int sl = 1 << l;
+      for (int yl = 0; yl < m; yl += sl) {
+        if ((yl >> l) & 1) rec_blocks += 1 + 1 + (yl + sl < m);   // Dinv; back: Dinv L (+ Dinv U)
+        else rec_blocks += (yl > 0) + (yl + sl < m);              // alpha, gamma
+      }
+    }
+    const int qk = (m - 1) / (1 << L) + 1;
+    rec_blocks += (double)qk * qk;
+    if (B > 0) rec_blocks += 4.0 * B + 2.0 * m;                   // R rows, spikes
+  }
+  const double rec_bytes = rec_blocks * TM2 * 16.0;
   // one solve launch per stage (up to two concurrent fronts)
   auto emit_pass = [&](std::vector<SweepLaunch>& plan, int src,
                        std::vector<std::vector<std::vector<SweepTask>>> stages) {
@@ -1486,6 +1667,7 @@ void sweep_destroy(Sweep* s) {
   cudaFree(s->kr);
   cudaFree(s->sp);
   cudaFree(s->rk);
+  cudaFree(s->qd);
   cudaFree(s->trace);
   cudaFree(s->g);
   cudaFree(s->u2);
@@ -1528,6 +1710,7 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u) {
         a.kr = s->kr;
         a.sp = s->sp;
         a.rk = s->rk;
+        a.qd = s->qd;
         a.src = Lh.src ? s->g : f;
         a.coarse = s->coarse->d.coeffs;
         a.ncoarse = s->coarse->d.n;
@@ -1560,7 +1743,7 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u) {
           if (FILE* fp = fopen(trace_path, "w")) {
             // per CTA of cluster 0 (task 1): [0] start, [1] rhs, [2+p] local phase p,
             // [40] tips barrier, [41] interface solve, [63] end (ns after CTA 0 start)
-            fprintf(fp, "# C=%d M=%d L=%d\n", s->C, M, s->L);
+            fprintf(fp, "# C=%d M=%d L=%d q=%d\n", s->C, M, s->L, s->q);
             const unsigned long long t0 = h[0];
             for (int b = 0; b < std::min(16, s->C); ++b) {
               for (int k = 0; k < 256; ++k)

@@ -30,7 +30,8 @@ struct Sweep {
   int J = 0, M = 0, n0 = 0;
   int tm = 16;                  // padded block size (16 or 32)
   int C = 1;                    // chunks of the face = CTAs per cluster
-  int L = 0;                    // local reduction levels: 2^L >= largest chunk
+  int L = 0;                    // local cyclic-reduction levels before the dense top
+  int q = 1;                    // blocks left per chunk after L levels (dense inverse)
   int mmax = 0;                 // largest chunk (face points)
   int kstride = 0;              // kept-block records per chunk
   const Stencil* coarse = nullptr;
@@ -39,6 +40,7 @@ struct Sweep {
   double2* kr = nullptr;        // [J][C][kstride][2][tm^2] alpha, gamma of kept blocks
   double2* sp = nullptr;        // [J][M][2][tm^2]       spikes W, V of every block
   double2* rk = nullptr;        // [J][C][2(C-1)][2 tm^2] rows of the reduced-system inverse
+  double2* qd = nullptr;        // [J][C][q][q][tm^2]    inverse of the level-L reduced chunk system
   double2* trace = nullptr;     // [ntrace][2][M] interface traces
   double2* g = nullptr;         // [n0*M] mid-sweep residual
   double2* u2 = nullptr;        // [n0*M] second-pass contributions

@@ -2,13 +2,15 @@ import sys, numpy as np
 rows = [l.split() for l in open(sys.argv[1]) if not l.startswith('#')]
 A = np.array([[int(v) for v in r] for r in rows])
 hdr = open(sys.argv[1]).readline()
-L = int(hdr.split('L=')[1])
+import re
+L = int(re.search(r'L=(\d+)', hdr).group(1))
+NP = 2 * L + (1 if 'q=' in hdr else 0)
 a = A[0]
 print(hdr.strip())
-print("rhs", a[1]-a[0], " local phases:", [int(a[2+p]-(a[1+p] if p else a[1])) for p in range(2*L)])
-print("tips barrier", a[40]-a[1+2*L], " R gemv", a[41]-a[40], " correction+out+barrier", a[63]-a[41], " total", a[63]-a[0])
+print("rhs", a[1]-a[0], " local phases:", [int(a[2+p]-(a[1+p] if p else a[1])) for p in range(NP)])
+print("tips barrier", a[40]-a[1+NP], " R gemv", a[41]-a[40], " correction+out+barrier", a[63]-a[41], " total", a[63]-a[0])
 print("rank0 warp0 item j=0 per phase [start->seq, seq->mbar, mbar->done] and phase start offset:")
-for p in range(2*L):
+for p in range(NP):
     st = a[1+p] if p else a[1]
     it = a[64+5*p:64+5*p+5]
     if p < 12 and it[0] > 0:
