@@ -61,8 +61,11 @@ constexpr int kCW = kWarps - 1;
 #ifndef HS_SWEEP_HALF      // tm 16: one ring item per half warp
 #define HS_SWEEP_HALF 0
 #endif
-#ifndef HS_SWEEP_L2NEXT    // producer prefetches each item of the next slab into L2
+#ifndef HS_SWEEP_L2NEXT    // consumers prefetch the next slab's stream into L2
 #define HS_SWEEP_L2NEXT 0
+#endif
+#ifndef HS_SWEEP_G16       // tm 16: blocks per ring chunk (bulk copy)
+#define HS_SWEEP_G16 4
 #endif
 constexpr int kMaxC = 16;
 constexpr int kMaxTasks = 1024;    // slab solves per front per launch
@@ -565,13 +568,9 @@ struct SolveArgs {
   const SweepTask* tasks;
   int ffirst[2], fcount[2];
   Chunks g;
-  int nslot;
-  const double2* ef;
-  const double2* eb;
-  const double2* kr;
-  const double2* sp;
-  const double2* rk;
-  const double2* qd;
+  int nchunk;              // ring slots (16-KB chunks)
+  const double2* stream;   // [J][C][nbs] factor blocks in item order
+  int64_t nbs;
   const double2* src;      // right-hand side field (n0 x M)
   const double2* coarse;   // global coarse operator [S][n0*M] (transmission couplings)
   int64_t ncoarse;
@@ -626,6 +625,12 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase)
         : "memory");
   }
 }
+// 16-B global -> shared copy that does not block the thread (zero-fill when !ok)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(ok ? 16 : 0)
+               : "memory");
+}
 __device__ __forceinline__ uint32_t map_rank(const void* p, int rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
@@ -650,7 +655,7 @@ __device__ __forceinline__ double2 mvs2(const double2* m0, const double2* v0, co
                                         const double2* v1, int lane) {
   constexpr int CPL = Geo<TM>::CPL;
   const int hh = lane / TM;
-  double2 a0 = czero(), a1 = czero();
+  double2 a0 = czero(), a1 = czero(), a2 = czero(), a3 = czero();
   if (v0) {
 #pragma unroll
     for (int k = 0; k < CPL; k += 2) {
@@ -661,25 +666,174 @@ __device__ __forceinline__ double2 mvs2(const double2* m0, const double2* v0, co
   if (v1) {
 #pragma unroll
     for (int k = 0; k < CPL; k += 2) {
-      a0 = cfma(m1[k * 32 + lane], v1[CPL * hh + k], a0);
-      a1 = cfma(m1[(k + 1) * 32 + lane], v1[CPL * hh + k + 1], a1);
+      a2 = cfma(m1[k * 32 + lane], v1[CPL * hh + k], a2);
+      a3 = cfma(m1[(k + 1) * 32 + lane], v1[CPL * hh + k + 1], a3);
     }
   }
-  double2 acc = cadd(a0, a1);
+  double2 acc = cadd(cadd(a0, a1), cadd(a2, a3));
   if (TM == 16) acc = cadd(acc, shfl_xor_c(acc, 16));
   return acc;
 }
 
-// items of one chunk solve: <= 3m + 2L local, 2(C-1) R blocks, m spike blocks
+// ---------------------------------------------------------------------------
+// Item plan of one chunk solve, shared by the packing kernel (setup), the host
+// (stream sizes) and the solve kernel.  Phases: p < L forward cyclic-reduction
+// level p (eliminated points first, then kept ones); p == L the dense top,
+// items (row r, column pair cp); L < p < NP back substitution of level 2L-p;
+// then the 2B column blocks of R and the m spike blocks.
+struct ItemPlan {
+  int m, L, S, qk, QP, B, NP;
+  int pfx[2 * kMaxLevels + 4];   // items before each phase (NP + 2 = total)
+};
+
+__host__ __device__ inline int plan_level(const ItemPlan& P, int p) {
+  return p <= P.L ? p : 2 * P.L - p;
+}
+__host__ __device__ inline int plan_first(const ItemPlan& P, int p) {
+  return p > P.L ? (1 << plan_level(P, p)) : 0;
+}
+__host__ __device__ inline int plan_step(const ItemPlan& P, int p) {
+  return (p < P.L ? 1 : 2) << plan_level(P, p);
+}
+__host__ __device__ inline void plan_items(const Chunks& g, int rank, ItemPlan& P) {
+  P.m = g.len(rank);
+  P.L = g.L;
+  P.S = 1 << g.L;
+  P.qk = (P.m - 1) / P.S + 1;
+  P.QP = (P.qk + 1) / 2;
+  P.B = g.C - 1;
+  P.NP = 2 * P.L + 1;
+  int acc = 0;
+  for (int p = 0; p < P.NP; ++p) {
+    P.pfx[p] = acc;
+    const int f = plan_first(P, p);
+    if (p == P.L) acc += P.qk * P.QP;
+    else if (f < P.m) acc += (P.m - 1 - f) / plan_step(P, p) + 1;
+  }
+  P.pfx[P.NP] = acc;
+  P.pfx[P.NP + 1] = acc + (P.B > 0 ? 2 * P.B : 0);
+  P.pfx[P.NP + 2] = P.pfx[P.NP + 1] + (P.B > 0 ? P.m : 0);
+}
+// face point of item j of a cyclic-reduction phase
+__host__ __device__ inline int plan_yl(const ItemPlan& P, int p, int j) {
+  if (p > P.L) return plan_first(P, p) + j * plan_step(P, p);
+  const int ne = (P.pfx[p + 1] - P.pfx[p]) / 2;
+  return (j < ne ? 2 * j + 1 : 2 * (j - ne)) << p;
+}
+
+// Factor arrays of one slab before packing (setup only).
+enum ItemArray : uint32_t { kArrEf = 0, kArrEb = 1, kArrKr = 2, kArrRk = 3, kArrSp = 4, kArrQd = 5 };
+__host__ __device__ constexpr uint32_t item_enc(uint32_t arr, int64_t off) {
+  return (arr << 29) | (uint32_t)off;
+}
+
+// Source blocks of item r (array + offset from the slab base, in stream
+// order); *hasx: the first block is the item's "x" operand (alpha / Dinv L /
+// left), not only the right one.  Returns the block count (0..2).
+template <int TM>
+__host__ __device__ inline int item_sources(const Chunks& g, int rank, const ItemPlan& P, int r,
+                                            uint32_t src[2], bool* hasx) {
+  constexpr int TM2 = TM * TM;
+  int p = 0;
+  while (P.pfx[p + 1] <= r) ++p;
+  const int j = r - P.pfx[p];
+  const int Y0 = g.y0(rank), m = P.m;
+  int n = 0;
+  *hasx = true;
+  if (p == P.L) {            // dense top: Q[row][c0], Q[row][c0 + 1]
+    const int row = j / P.QP, c0 = 2 * (j % P.QP);
+    const int64_t o = (((int64_t)rank * g.q + row) * g.q + c0) * TM2;
+    src[n++] = item_enc(kArrQd, o);
+    if (c0 + 1 < P.qk) src[n++] = item_enc(kArrQd, o + TM2);
+  } else if (p < P.NP) {
+    const int l = plan_level(P, p), s = 1 << l;
+    const int yl = plan_yl(P, p, j);
+    const int64_t y = Y0 + yl;
+    if (p < P.L) {
+      if ((yl >> l) & 1) {
+        src[n++] = item_enc(kArrEf, y * TM2);
+      } else {
+        const int64_t k2 = ((int64_t)rank * g.kstride + g.koff[l] + (yl >> (l + 1))) * 2 * TM2;
+        *hasx = yl - s >= 0;
+        if (yl - s >= 0) src[n++] = item_enc(kArrKr, k2);
+        if (yl + s < m) src[n++] = item_enc(kArrKr, k2 + TM2);
+      }
+    } else {
+      if (yl - s >= 0) src[n++] = item_enc(kArrEb, y * 2 * TM2);
+      if (yl + s < m) src[n++] = item_enc(kArrEb, y * 2 * TM2 + TM2);
+    }
+  } else if (p == P.NP) {    // R column block j (2tm x tm, two blocks)
+    const int64_t o = ((int64_t)rank * (2 * P.B) + j) * (2 * TM2);
+    src[n++] = item_enc(kArrRk, o);
+    src[n++] = item_enc(kArrRk, o + TM2);
+  } else {                   // spikes W, V of block j
+    const int64_t o = (int64_t)(Y0 + j) * 2 * TM2;
+    src[n++] = item_enc(kArrSp, o);
+    src[n++] = item_enc(kArrSp, o + TM2);
+  }
+  return n;
+}
+
+constexpr int kMaxItems = 1024;   // items of one chunk solve (checked at sweep_create)
+
+// items of one chunk solve: <= 3m + 2L local, 15 dense, 2(C-1) R blocks, m spike blocks
 __host__ __device__ inline int itab_len(int mmax) { return 4 * mmax + 2 * kMaxLevels + 2 * kMaxC + 16; }
 
-// Item copy descriptor: array (bits 29-31; 7 = none), double length (bit 28),
-// offset in double2 from the array's slab base (bits 0-27).
-enum ItemArray : uint32_t { kArrEf = 0, kArrEb = 1, kArrKr = 2, kArrRk = 3, kArrSp = 4, kArrQd = 5 };
-__host__ __device__ constexpr uint32_t item_enc(uint32_t arr, int64_t off, bool dbl = false) {
-  return (arr << 29) | (dbl ? (1u << 28) : 0u) | (uint32_t)off;
+// blocks of one chunk's slab-solve stream
+template <int TM>
+__host__ __device__ inline int stream_blocks(const Chunks& g, int rank) {
+  ItemPlan P;
+  plan_items(g, rank, P);
+  int nb = 0;
+  uint32_t src[2];
+  bool hx;
+  for (int r = 0; r < P.pfx[P.NP + 2]; ++r) nb += item_sources<TM>(g, rank, P, r, src, &hx);
+  return nb;
 }
-constexpr uint32_t kItemNone = 0xffffffffu;
+
+struct FactorArrays {
+  const double2 *ef, *eb, *kr, *rk, *sp, *qd;
+};
+
+// Repack every slab's factors into per-chunk streams in item order (one CTA
+// per slab x chunk), so the solve kernel fetches 16-KB runs with single bulk
+// copies: stream[slab][k][nbs] blocks.
+template <int TM>
+__global__ void __launch_bounds__(256) k_pack(Chunks g, FactorArrays f, double2* __restrict__ stream,
+                                              int nbs) {
+  constexpr int TM2 = TM * TM;
+  const int slab = blockIdx.x / g.C, k = blockIdx.x % g.C, M = g.M, C = g.C;
+  __shared__ ItemPlan P;
+  __shared__ int boff[kMaxItems];
+  if (threadIdx.x == 0) {
+    plan_items(g, k, P);
+    int acc = 0;
+    uint32_t src[2];
+    bool hx;
+    for (int r = 0; r < P.pfx[P.NP + 2]; ++r) {
+      boff[r] = acc;
+      acc += item_sources<TM>(g, k, P, r, src, &hx);
+    }
+  }
+  __syncthreads();
+  const double2* base[6] = {
+      f.ef + (int64_t)slab * M * TM2,           f.eb + (int64_t)slab * M * 2 * TM2,
+      f.kr + (int64_t)slab * C * g.kstride * 2 * TM2,
+      f.rk + (int64_t)slab * C * (2 * (C - 1)) * 2 * TM2,
+      f.sp + (int64_t)slab * M * 2 * TM2,       f.qd + (int64_t)slab * C * g.q * g.q * TM2};
+  double2* out = stream + ((int64_t)slab * C + k) * nbs * TM2;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int r = warp; r < P.pfx[P.NP + 2]; r += 8) {
+    uint32_t src[2];
+    bool hx;
+    const int n = item_sources<TM>(g, k, P, r, src, &hx);
+    for (int b = 0; b < n; ++b) {
+      const double2* s = base[src[b] >> 29] + (src[b] & 0x1fffffffu);
+      double2* d = out + (int64_t)(boff[r] + b) * TM2;
+      for (int e = lane; e < TM2; e += 32) d[e] = s[e];
+    }
+  }
+}
 
 // One item per half warp for tm = 16 (lane row x = lane % 16 of the half's
 // item, all 16 columns), the whole warp for tm = 32: row x of A0 v0 + A1 v1.
@@ -709,30 +863,36 @@ __device__ __forceinline__ double2 mvx(const double2* m0, const double2* v0, con
   }
 }
 
+
+// Shared-memory ring of stream chunks: G blocks (16 KB) per bulk copy.
 template <int TM>
 struct Ring {
-  static constexpr int SLOT = 2 * Geo<TM>::TM2;   // double2 per slot (two blocks)
-  // F, Yv vectors + tau + R partials + bookkeeping, then the ring
+  static constexpr int TM2 = TM * TM;
+  static constexpr int G = TM == 16 ? HS_SWEEP_G16 : 2;   // blocks per chunk copy (>= 2: whole items)
+  static constexpr int CHUNK = G * TM2;            // double2 per chunk
+  // F, Yv vectors + tau + halo + R partials + couplings + bookkeeping, then the ring
   static int fixed(int mmax) {
-    return 2 * (mmax + 1) * TM * 16 + 4 * kMaxC * TM * 16 + 4 * TM * 16 + (kWarps + 1) * 2 * TM * 16 + 32 +
-           (64 + kMaxTasks) * 4 + itab_len(mmax) * 8 + 384;
+    return 2 * (mmax + 1) * TM * 16 + 4 * kMaxC * TM * 16 + 4 * TM * 16 +
+           (kWarps + 1) * 2 * TM * 16 + 12 * mmax * 16 + 64 + (int)sizeof(ItemPlan) +
+           kMaxTasks * 4 + itab_len(mmax) * 8 + 512;
   }
-  static int nslot(int mmax) {
+  static int nchunk(int mmax) {
     const int avail = 225 * 1024 - fixed(mmax);
-    return std::max(2, std::min(48, avail / (SLOT * 16 + 16)));
+    return std::max(2, std::min(64, avail / (CHUNK * 16 + 16)));
   }
-  static int smem(int mmax) { return fixed(mmax) + nslot(mmax) * (SLOT * 16 + 16); }
+  static int smem(int mmax) { return fixed(mmax) + nchunk(mmax) * (CHUNK * 16 + 16); }
 };
 
 template <int TM>
 __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   constexpr int TM2 = Geo<TM>::TM2;
-  constexpr int SLOT = Ring<TM>::SLOT;
+  constexpr int G = Ring<TM>::G;
+  constexpr int CHUNK = Ring<TM>::CHUNK;
   constexpr int YPW = 32 / TM;   // face points per warp pass in row-wise loops
   constexpr int N2 = 2 * TM;     // interface unknowns per chunk (alpha, beta)
   cg::cluster_group cl = cg::this_cluster();
   const Chunks& g = a.g;
-  const int C = g.C, M = g.M, L = g.L, B = C - 1;
+  const int C = g.C, M = g.M, B = C - 1;
   const int rank = (int)cl.block_rank();
   const int front = blockIdx.x / C;
   const int Y0 = g.y0(rank), Y1 = g.y0(rank + 1);
@@ -743,179 +903,69 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   constexpr int HW = (TM == 16 && HS_SWEEP_HALF) ? 2 : 1;   // items per warp pass
   const int sub = HW == 2 ? hh : 0;      // this lane's item within the pass
   const bool wr = HW == 2 || hh == 0;    // lane owns the result row it computed
-  const int NS = a.nslot;
+  const int NC = a.nchunk;
   extern __shared__ __align__(128) double2 sm[];
   double2* F = sm;                                  // [mmax+1][TM] rhs / reduced rhs
   double2* Yv = F + (mmax + 1) * TM;                // [mmax+1][TM] Dinv f, then x
   double2* tau2 = Yv + (mmax + 1) * TM;             // [2][2 kMaxC][TM] interface rhs (by task parity)
   double2* halo2 = tau2 + 4 * kMaxC * TM;           // [2][2][TM] neighbours' edge blocks of x
-  double2* part = halo2 + 4 * TM;                   // [kWarps][2TM] R partial sums
+  double2* part = halo2 + 4 * TM;                   // [kWarps][2TM] R / dense-top partial sums
   double2* ab = part + kWarps * N2;                 // [2TM] alpha_{k-1}, beta_k
-  uint64_t* xbar = (uint64_t*)(ab + N2);            // [4] tips (2), halo (2) arrival barriers
-  uint64_t* bars = xbar + 4;                        // [NS]
-  volatile int* seq = (volatile int*)(bars + NS);   // [NS] item issued into a slot
-  volatile int* done = seq + NS;                    // [NS] item consumed from a slot
-  int* pfx = (int*)(bars + NS) + 2 * NS;            // [2L+3] items before each phase
-  int* slabs = pfx + 64;                            // [fcount]
-  uint2* itab = (uint2*)(slabs + kMaxTasks);        // [ITEMS] copy descriptors
-  double2* ring = (double2*)(((uintptr_t)(itab + itab_len(mmax)) + 127) & ~(uintptr_t)127);
+  double2* stc = ab + N2;                           // [2 tin][2 rows][3 offsets][mmax] couplings
+  uint64_t* xbar = (uint64_t*)(stc + 12 * mmax);    // [4] tips (2), halo (2) arrival barriers
+  uint64_t* cbar = xbar + 4;                        // [NC] chunk arrival
+  volatile int* cseq = (volatile int*)(cbar + NC);  // [NC] chunk issued into a slot
+  int* ccnt = (int*)(cseq + NC);                    // [NC] blocks of the slot's chunk consumed
+  ItemPlan* Pp = (ItemPlan*)(ccnt + NC);
+  int* slabs = (int*)(Pp + 1);                      // [fcount]
+  uint32_t* ib = (uint32_t*)(slabs + kMaxTasks);    // [ITEMS] chunk | offset in chunk | nblk | hasx
+  uint32_t* ctab = ib + itab_len(mmax);             // [<= ITEMS] chunk: first block | blocks
+  int* nchk = (int*)(ctab + itab_len(mmax));        // chunks per slab solve
+  // (offset from sm keeps the shared-space provenance: LDS, not generic loads)
+  double2* ring = sm + ((((char*)(nchk + 1) - (char*)sm) + 127) & ~(ptrdiff_t)127) / 16;
+  const ItemPlan& P = *Pp;
 
-  auto cc = [&](int o0, int o1, int row, int y) -> double2 {
-    const int sl = a.cslot[o0 + 1][o1 + 1];
-    if (sl < 0 || y + o1 < 0 || y + o1 >= M) return czero();
-    return __ldg(a.coarse + (int64_t)sl * a.ncoarse + (int64_t)row * M + y);
-  };
-  // transmission source into slab row p-lo (which 0) / p+1-lo (which 1)
-  auto trans = [&](int buf, int p, int sign, int which, int y) -> double2 {
-    const double2* Bt = a.trace + (int64_t)buf * 2 * M + (which == 0 ? M : 0);
-    const int o0 = which == 0 ? 1 : -1;
-    const int row = which == 0 ? p - 1 : p;
-    double2 cv[3], bv[3];
-#pragma unroll
-    for (int o = -1; o <= 1; ++o) {   // all six loads in flight together
-      const bool ok = y + o >= 0 && y + o < M;
-      cv[o + 1] = ok ? cc(o0, o, row, y) : czero();
-      bv[o + 1] = ok ? Bt[y + o] : czero();
-    }
-    double2 acc = cmul(cv[0], bv[0]);
-    acc = cfma(cv[1], bv[1], acc);
-    acc = cfma(cv[2], bv[2], acc);
-    return cscale(which == 0 ? (double)sign : (double)-sign, acc);
-  };
-
-  // Item streams of one slab solve of this CTA: local phases (p < L forward
-  // cyclic-reduction level p; p == L the dense top, items (row r, column pair
-  // cp) of the level-L inverse; p > L back substitution of level 2L-p), then
-  // the 2B column blocks of R, then the m spike blocks.
-  const int NP = 2 * L + 1;
-  const int S = 1 << L;
-  const int qk = (m - 1) / S + 1;            // dense-top blocks of this chunk
-  const int QP = (qk + 1) / 2;               // their column pairs
-  auto ph_level = [&](int p) { return p <= L ? p : 2 * L - p; };
-  auto ph_first = [&](int p) -> int { return p > L ? (1 << ph_level(p)) : 0; };
-  auto ph_step = [&](int p) { return (p < L ? 1 : 2) << ph_level(p); };
-  // face point of item j of a cyclic-reduction phase (forward phases list the
-  // eliminated points first, so neighbouring items share a branch)
-  auto item_yl = [&](int p, int j) -> int {
-    if (p > L) return ph_first(p) + j * ph_step(p);
-    const int ne = (pfx[p + 1] - pfx[p]) / 2;
-    return (j < ne ? 2 * j + 1 : 2 * (j - ne)) << p;
-  };
   const int ffirst = front ? a.ffirst[1] : a.ffirst[0];
   const int fcount = front ? a.fcount[1] : a.fcount[0];
   if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int p = 0; p < NP; ++p) {
-      pfx[p] = acc;
-      const int f = ph_first(p);
-      if (p == L) acc += qk * QP;
-      else if (f < m) acc += (m - 1 - f) / ph_step(p) + 1;
+    plan_items(g, rank, *Pp);
+    // Chunks: runs of whole items of one phase, up to G blocks (one bulk copy
+    // each); a slot is released as soon as its items are consumed, so a chunk
+    // never waits for a later phase.
+    int acc = 0, nc = -1, cfill = G, ph = 0;
+    uint32_t src[2];
+    bool hx;
+    for (int r = 0; r < Pp->pfx[Pp->NP + 2]; ++r) {   // stream offsets (k_pack's order)
+      const int n = item_sources<TM>(g, rank, *Pp, r, src, &hx);
+      bool new_phase = false;
+      while (Pp->pfx[ph + 1] <= r) { ++ph; new_phase = true; }
+      if (new_phase || cfill + n > G) {
+        ++nc;
+        ctab[nc] = (uint32_t)acc << 8;
+        cfill = 0;
+      }
+      ib[r] = (uint32_t)nc << 12 | (uint32_t)cfill << 3 | (uint32_t)n << 1 | (hx ? 1u : 0u);
+      ctab[nc] += (uint32_t)n;
+      cfill += n;
+      acc += n;
     }
-    pfx[NP] = acc;                               // R column blocks
-    pfx[NP + 1] = acc + (B > 0 ? 2 * B : 0);     // spikes
-    pfx[NP + 2] = pfx[NP + 1] + (B > 0 ? m : 0);
-    for (int i = 0; i < NS; ++i) {
-      mbar_init(&bars[i], 1);
-      seq[i] = -1;
-      done[i] = i - NS;   // slot i is free for item i
+    *nchk = nc + 1;
+    for (int i = 0; i < NC; ++i) {
+      mbar_init(&cbar[i], 1);
+      cseq[i] = -1;
+      ccnt[i] = 0;
     }
     for (int i = 0; i < 4; ++i) mbar_init(&xbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = threadIdx.x; i < fcount; i += blockDim.x) slabs[i] = a.tasks[ffirst + i].slab;
   cl.sync();   // every CTA's barriers initialised before any remote arrival
-  const int ITEMS = pfx[NP + 2];
-  const int total = fcount * ITEMS;
-  const int64_t kbase = (int64_t)rank * g.kstride;
-  if (ITEMS > itab_len(mmax)) __trap();   // bound of the descriptor table (host-sized)
+  const int NP = P.NP, L = P.L, S = P.S, qk = P.qk, QP = P.QP;
+  const int ITEMS = P.pfx[NP + 2];
+  const int CPT = *nchk;   // chunk copies per slab solve
 
-  // Copy descriptors of one chunk solve (the same for every slab; offsets
-  // relative to the slab's base in each factor array), built once.
-  for (int r = threadIdx.x; r < ITEMS; r += blockDim.x) {
-    int p = 0;
-    while (pfx[p + 1] <= r) ++p;
-    const int j = r - pfx[p];
-    uint2 e = make_uint2(kItemNone, kItemNone);
-    if (p == L) {           // dense top: blocks (r, 2cp) and (r, 2cp + 1)
-      const int r = j / QP, c0 = 2 * (j % QP);
-      e.x = item_enc(kArrQd, (((int64_t)rank * g.q + r) * g.q + c0) * TM2, c0 + 1 < qk);
-    } else if (p < NP) {
-      const int l = ph_level(p), s = 1 << l;
-      const int yl = item_yl(p, j);
-      const int y = Y0 + yl;
-      if (p < L) {
-        if ((yl >> l) & 1) {
-          e.x = item_enc(kArrEf, (int64_t)y * TM2);
-        } else {
-          const int64_t k2 = (kbase + g.koff[l] + (yl >> (l + 1))) * 2 * TM2;
-          if (yl - s >= 0) e.x = item_enc(kArrKr, k2);
-          if (yl + s < m) e.y = item_enc(kArrKr, k2 + TM2);
-        }
-      } else {
-        const int64_t e2 = (int64_t)y * 2 * TM2;
-        if (yl - s >= 0) e.x = item_enc(kArrEb, e2);
-        if (yl + s < m) e.y = item_enc(kArrEb, e2 + TM2);
-      }
-    } else if (p == NP) {   // R column block j
-      e.x = item_enc(kArrRk, ((int64_t)rank * (2 * B) + j) * (2 * TM2), true);
-    } else {                // spikes of block j
-      e.x = item_enc(kArrSp, (int64_t)(Y0 + j) * 2 * TM2, true);
-    }
-    itab[r] = e;
-  }
-  __syncthreads();
-
-  // producer state: the current task's slab base of every factor array
-  const double2* sbase[6];
-  auto slab_bases = [&](int slab, const double2** sb) {
-    sb[kArrEf] = a.ef + (int64_t)slab * M * TM2;
-    sb[kArrEb] = a.eb + (int64_t)slab * M * 2 * TM2;
-    sb[kArrKr] = a.kr + (int64_t)slab * C * g.kstride * 2 * TM2;
-    sb[kArrRk] = a.rk + (int64_t)slab * C * (2 * B) * 2 * TM2;
-    sb[kArrSp] = a.sp + (int64_t)slab * M * 2 * TM2;
-    sb[kArrQd] = a.qd + (int64_t)slab * C * g.q * g.q * TM2;
-  };
-  auto set_slab = [&](int slab) { slab_bases(slab, sbase); };
-  auto src_of = [&](uint32_t e) -> const double2* {
-    const uint32_t arr = e >> 29;
-    const double2* b = arr == kArrEf ? sbase[0]
-                       : arr == kArrEb ? sbase[1]
-                       : arr == kArrKr ? sbase[2]
-                       : arr == kArrRk ? sbase[3]
-                       : arr == kArrSp ? sbase[4]
-                                       : sbase[5];
-    return b + (e & 0x0fffffffu);
-  };
-  const double2* nbase[6];   // next task's slab bases (L2 prefetch)
-  auto issue = [&](int r, int sl, bool pf) {   // one lane: item r of the current task into slot sl
-    const uint2 e = itab[r];
-    if (HS_SWEEP_L2NEXT && pf) {   // the same item of the next slab into L2
-      auto nsrc = [&](uint32_t q) {
-        const uint32_t arr = q >> 29;
-        const double2* b = arr == kArrEf ? nbase[0] : arr == kArrEb ? nbase[1]
-                         : arr == kArrKr ? nbase[2] : arr == kArrRk ? nbase[3]
-                         : arr == kArrSp ? nbase[4] : nbase[5];
-        return b + (q & 0x0fffffffu);
-      };
-      constexpr uint32_t mb1 = TM2 * 16;
-      if (e.x != kItemNone) prefetch_l2(nsrc(e.x), (e.x >> 28 & 1) ? 2 * mb1 : mb1);
-      if (e.y != kItemNone) prefetch_l2(nsrc(e.y), mb1);
-    }
-    double2* slot = ring + sl * SLOT;
-    uint64_t* bar = &bars[sl];
-    constexpr uint32_t mb = TM2 * 16;
-    if (e.x != kItemNone && (e.x >> 28 & 1)) {
-      mbar_expect_tx(bar, 2 * mb);
-      bulk_g2s(slot, src_of(e.x), 2 * mb, bar);
-    } else {
-      mbar_expect_tx(bar, (e.x != kItemNone ? mb : 0) + (e.y != kItemNone ? mb : 0));
-      if (e.x != kItemNone) bulk_g2s(slot, src_of(e.x), mb, bar);
-      if (e.y != kItemNone) bulk_g2s(slot + TM2, src_of(e.y), mb, bar);
-    }
-  };
   // optional instrumentation: task 1 timestamps kept in shared memory, dumped at exit
   __shared__ unsigned long long tsm[128];
-  __shared__ unsigned long long tprod[128];   // producer: [spin start, issued] of task 1's first 64 items
   auto stamp = [&](int ti, int k) {
     if (a.dbg && threadIdx.x == 0 && ti == 1 && k < 64) {
       unsigned long long tt;
@@ -924,114 +974,136 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     }
   };
   if (a.dbg && threadIdx.x == 0)
-    for (int k = 0; k < 128; ++k) tsm[k] = tprod[k] = 0;
-  auto stamp2 = [&](int ti, int p, int j, int k) {
-    if (a.dbg && threadIdx.x == 0 && ti == 1 && j == 0 && p < 12) {
+    for (int k = 0; k < 128; ++k) tsm[k] = 0;
+  // per-item timestamps of task 1 (cluster 0): chunk issue, item data ready, item consumed
+  auto istamp = [&](int r, int k) {
+    if (a.dbg && blockIdx.x < 16 && r >= 0 && r < 256) {
       unsigned long long tt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
-      tsm[64 + p * 5 + k] = tt;
+      a.dbg[blockIdx.x * 1024 + 256 + 3 * r + k] = tt;
     }
-  };
-
-  // consume item i: wait until issued into its slot (a parity wait is valid
-  // only once the slot's previous occupant completed), then for the data
-  int dbg_ti = 0, dbg_p = 0, dbg_j = 0;
-  auto acquire = [&](int i) -> const double2* {
-    stamp2(dbg_ti, dbg_p, dbg_j, 0);
-    while (seq[i % NS] != i) {
-    }
-    stamp2(dbg_ti, dbg_p, dbg_j, 1);
-    mbar_wait(&bars[i % NS], (uint32_t)((i / NS) & 1));
-    stamp2(dbg_ti, dbg_p, dbg_j, 2);
-    return ring + (i % NS) * SLOT;
-  };
-  // The warp's reads of the slot have returned (their values are consumed
-  // before the __syncwarp), so the producer's async-proxy refill cannot race.
-  auto release = [&](int i, bool has) {   // whole consumer warp, after its last read of the slot
-    __syncwarp();
-    if (has && lane % (32 / HW) == 0) done[i % NS] = i;
   };
   auto csync = [&]() {   // consumer warps only (the producer never joins)
     asm volatile("bar.sync 1, %0;" ::"r"(kCW * 32) : "memory");
   };
 
   if (warp == kCW) {
-    // ---- TMA producer warp: issues every item in consumption order as soon
-    // as its slot is free, prefetches the next slab into L2, and takes part in
-    // the cluster barriers (arriving early: it never holds data others read).
-    const int BW = max(1, min(8, NS / 2));   // items issued per batch (one lane each)
-    int sl = 0;
+    // ---- TMA producer warp: streams each slab solve's blocks in 16-KB chunk
+    // copies (one lane per chunk, up to BW in flight per batch) as soon as the
+    // chunk's ring slot has been fully consumed.
+    const int BW = max(1, min(4, NC / 2));
+    int cs0 = 0;
     for (int ti = 0; ti < fcount; ++ti) {
-      set_slab(slabs[ti]);
-      const bool pf = ti + 1 < fcount;
-      if (pf) slab_bases(slabs[ti + 1], nbase);
-      if (HS_SWEEP_PREFETCH && lane == 0 && ti + 1 < fcount) {   // next slab's matrices into L2
-        const int ns = slabs[ti + 1];
-        prefetch_l2(a.ef + ((int64_t)ns * M + Y0) * TM2, (uint32_t)m * TM2 * 16);
-        prefetch_l2(a.eb + ((int64_t)ns * M + Y0) * 2 * TM2, (uint32_t)m * 2 * TM2 * 16);
-        prefetch_l2(a.kr + (((int64_t)ns * C) * g.kstride + kbase) * 2 * TM2,
-                    (uint32_t)g.kstride * 2 * TM2 * 16);
-        if (B > 0) {
-          prefetch_l2(a.sp + ((int64_t)ns * M + Y0) * 2 * TM2, (uint32_t)m * 2 * TM2 * 16);
-          prefetch_l2(a.rk + (((int64_t)ns * C + rank) * (2 * B)) * (2 * TM2),
-                      (uint32_t)(2 * B) * 2 * TM2 * 16);
-        }
-      }
-      // batches of up to BW items, one lane each
-      const int base = ti * ITEMS;
-      for (int r0 = 0; r0 < ITEMS;) {
-        const int i0 = base + r0;
-        const int cnt = min(BW, ITEMS - r0);
-        if (lane < cnt) {
-          const int i = i0 + lane;
-          int sl_l = sl + lane;
-          if (sl_l >= NS) sl_l -= NS;
-          const int k = i - ITEMS;
-          unsigned long long t0 = 0, t1 = 0;
-          if (a.dbg && k >= 0 && k < 64) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-          while (done[sl_l] != i - NS) {
+      const double2* sbase = a.stream + ((int64_t)slabs[ti] * C + rank) * a.nbs * TM2;
+      for (int c0 = 0; c0 < CPT; c0 += BW) {
+        const int c = c0 + lane;
+        if (lane < BW && c < CPT) {
+          const int cs = cs0 + c;
+          const int sl = cs % NC;
+          const uint32_t ce = ctab[c];
+          const int nbk = (int)(ce & 0xff);
+          // the slot's previous chunk (cs - NC) fully consumed: its block count
+          if (cs >= NC) {
+            const int prev_n = (int)(ctab[(cs - NC) % CPT] & 0xff);
+            while (*(volatile int*)&ccnt[sl] != prev_n) {
+            }
           }
-          issue(r0 + lane, sl_l, pf);
-          seq[sl_l] = i;
-          if (a.dbg && k >= 0 && k < 64) {
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-            tprod[2 * k] = t0;
-            tprod[2 * k + 1] = t1;
-          }
+          ccnt[sl] = 0;
+          __threadfence_block();
+          mbar_expect_tx(&cbar[sl], (uint32_t)nbk * TM2 * 16);
+          bulk_g2s(ring + (int64_t)sl * CHUNK, sbase + (int64_t)(ce >> 8) * TM2,
+                   (uint32_t)nbk * TM2 * 16, &cbar[sl]);
+          cseq[sl] = cs;
+          if (ti == 1) istamp(c, 0);
         }
-        sl += cnt;
-        if (sl >= NS) sl -= NS;
-        r0 += cnt;
         __syncwarp();
       }
+      cs0 += CPT;
     }
     cl.sync();   // matches the consumers' exit barrier
     return;
   }
 
-  // Transmission from the previous task of this front without a trip through
-  // global memory: its solution x is still in Yv (own face points) and the
-  // neighbours' edge blocks arrive in halo (st.async + mbarrier).
-  auto trans_local = [&](const double2* halo, int prow, int p, int sign, int which, int y) {
-    const int o0 = which == 0 ? 1 : -1;
-    const int row = which == 0 ? p - 1 : p;
+  // ---- consumers: item r of task ti -> its (one or two) blocks in the ring
+  auto wait_chunk = [&](int cs) {
+    const int sl = cs % NC;
+    while (cseq[sl] != cs) {
+    }
+    mbar_wait(&cbar[sl], (uint32_t)((cs / NC) & 1));
+  };
+  struct Item { const double2* m0; const double2* m1; };
+  auto acquire = [&](int ti, int r) -> Item {
+    const uint32_t e = ib[r];
+    const int cs = ti * CPT + (int)(e >> 12);
+    const bool hx = e & 1;
+    wait_chunk(cs);
+    if (ti == 1 && lane % (32 / HW) == 0) istamp(r, 1);
+    const double2* p0 = ring + (int64_t)(cs % NC) * CHUNK + (int)((e >> 3) & 0x1ff) * TM2;
+    return hx ? Item{p0, p0 + TM2} : Item{nullptr, p0};
+  };
+  // The warp's reads of the blocks have returned (their values are consumed
+  // before the __syncwarp), so the producer's async-proxy refill cannot race.
+  auto release = [&](int ti, int r, bool has) {
+    __syncwarp();
+    if (has && lane % (32 / HW) == 0) {
+      const uint32_t e = ib[r];
+      atomicAdd(&ccnt[(ti * CPT + (int)(e >> 12)) % NC], (int)((e >> 1) & 3));
+      if (ti == 1) istamp(r, 2);
+    }
+  };
+  // Right-hand-side inputs of task tn, copied asynchronously while the
+  // previous task finishes: restriction rows straight into F (free after the
+  // previous task's dense top) and the transmission couplings into stc.
+  auto prefetch_rhs = [&](const SweepTask& t) {
+    for (int yl = warp * YPW + hh; yl < m; yl += kCW * YPW) {
+      const int y = Y0 + yl;
+      const int gr = x + t.lo - 1;
+      const bool ok = x < t.T && gr >= t.a && gr < t.b;
+      cp_async16(&F[yl * TM + x], a.src + (ok ? (int64_t)gr * M + y : 0), ok);
+#pragma unroll
+      for (int tn_i = 0; tn_i < 2; ++tn_i) {
+        const int tin = tn_i ? t.tin3 : t.tin1, row = tn_i ? t.row3 : t.row1;
+        if (tin < 0 || (x != row && x != row + 1)) continue;
+        const int which = x - row, p = row + t.lo;
+        const int o0 = which == 0 ? 1 : -1, crow = which == 0 ? p - 1 : p;
+#pragma unroll
+        for (int o = -1; o <= 1; ++o) {
+          const int sl = a.cslot[o0 + 1][o + 1];
+          const bool okc = sl >= 0 && y + o >= 0 && y + o < M;
+          cp_async16(&stc[((tn_i * 2 + which) * 3 + o + 1) * mmax + yl],
+                     a.coarse + (okc ? (int64_t)sl * a.ncoarse + (int64_t)crow * M + y : 0), okc);
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  // Transmission into slab row `which` of an incoming trace: from the previous
+  // task of this front without a trip through global memory (its x is still in
+  // Yv, the neighbours' edge blocks arrive in halo by st.async), else from the
+  // trace buffer written by an earlier launch.
+  auto transx = [&](int tn_i, bool local, const double2* halo, int buf, int prow, int sign,
+                    int which, int yl) -> double2 {
+    const int y = Y0 + yl;
     const int xr = prow + (which == 0 ? 1 : 0);   // trace row 1 feeds which 0, row 0 which 1
+    const double2* Bt = a.trace + (int64_t)buf * 2 * M + (which == 0 ? M : 0);
     double2 acc = czero();
 #pragma unroll
     for (int o = -1; o <= 1; ++o) {
       if (y + o < 0 || y + o >= M) continue;
-      const int yl = y + o - Y0;
-      const double2 bv = yl < 0 ? halo[xr] : yl >= m ? halo[TM + xr] : Yv[yl * TM + xr];
-      acc = cfma(cc(o0, o, row, y), bv, acc);
+      const int q = yl + o;
+      const double2 bv = !local ? Bt[y + o]
+                         : q < 0 ? halo[xr] : q >= m ? halo[TM + xr] : Yv[q * TM + xr];
+      acc = cfma(stc[((tn_i * 2 + which) * 3 + o + 1) * mmax + yl], bv, acc);
     }
     return cscale(which == 0 ? (double)sign : (double)-sign, acc);
   };
   const uint32_t halo_bytes = (rank > 0 ? TM * 16 : 0) + (rank < B ? TM * 16 : 0);
 
-  SweepTask prev{};
+  SweepTask prev{}, t = fcount > 0 ? a.tasks[ffirst] : SweepTask{};
+  if (fcount > 0) prefetch_rhs(t);
   for (int ti = 0; ti < fcount; ++ti) {
-    const SweepTask t = a.tasks[ffirst + ti];
-    const int base = ti * ITEMS;
+    if (ti > 0) t = a.tasks[ffirst + ti];
+    const SweepTask tn = ti + 1 < fcount ? a.tasks[ffirst + ti + 1] : t;   // in flight early
     const int par = ti & 1;
     double2* tau = tau2 + par * 2 * kMaxC * TM;
     const double2* halo = halo2 + par * 2 * TM;
@@ -1043,44 +1115,40 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       if (B > 0) mbar_expect_tx(&xbar[par], 2 * B * TM * 16);
     }
     stamp(ti, 0);
-    // ---- right-hand side of the owned blocks (restriction + transmission)
-    for (int yl = warp * YPW + hh; yl < m; yl += kCW * YPW) {
-      const int y = Y0 + yl;
-      double2 v = czero();
-      const int gr = x + t.lo - 1;
-      if (x < t.T && gr >= t.a && gr < t.b) v = __ldg(a.src + (int64_t)gr * M + y);
-      if (!loc1 && t.tin1 >= 0 && (x == t.row1 || x == t.row1 + 1))
-        v = cadd(v, trans(t.tin1, t.row1 + t.lo, 1, x - t.row1, y));
-      if (!loc3 && t.tin3 >= 0 && (x == t.row3 || x == t.row3 + 1))
-        v = cadd(v, trans(t.tin3, t.row3 + t.lo, -1, x - t.row3, y));
-      F[yl * TM + x] = v;
+    if (HS_SWEEP_L2NEXT && ti + 1 < fcount) {   // next slab's stream into L2 (LSU path, not TMA)
+      const char* nb = (const char*)(a.stream + ((int64_t)slabs[ti + 1] * C + rank) * a.nbs * TM2);
+      const int64_t bytes = (int64_t)((ctab[CPT - 1] >> 8) + (ctab[CPT - 1] & 0xff)) * TM2 * 16;
+      for (int64_t o = (int64_t)threadIdx.x * 128; o < bytes; o += kCW * 32 * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(nb + o));
     }
-    if (loc1 || loc3) {
-      mbar_wait_cluster(&xbar[2 + par], (uint32_t)((ti - 1) >> 1) & 1);
-      for (int yl = warp * YPW + hh; yl < m; yl += kCW * YPW) {
-        const int y = Y0 + yl;
-        double2 v = czero();
-        if (loc1 && (x == t.row1 || x == t.row1 + 1))
-          v = cadd(v, trans_local(halo, prev.orow2, t.row1 + t.lo, 1, x - t.row1, y));
-        if (loc3 && (x == t.row3 || x == t.row3 + 1))
-          v = cadd(v, trans_local(halo, prev.orow4, t.row3 + t.lo, -1, x - t.row3, y));
-        F[yl * TM + x] = cadd(F[yl * TM + x], v);
-      }
+    // ---- right-hand side of the owned blocks: restriction rows (already in
+    // F) plus the transmission terms of the incoming traces
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    if (loc1 || loc3) mbar_wait(&xbar[2 + par], (uint32_t)((ti - 1) >> 1) & 1);
+    csync();
+    for (int yl = warp * YPW + hh; yl < m; yl += kCW * YPW) {
+      const bool r1 = t.tin1 >= 0 && (x == t.row1 || x == t.row1 + 1);
+      const bool r3 = t.tin3 >= 0 && (x == t.row3 || x == t.row3 + 1);
+      if (!r1 && !r3) continue;
+      double2 v = F[yl * TM + x];
+      if (r1) v = cadd(v, transx(0, loc1, halo, t.tin1, prev.orow2, 1, x - t.row1, yl));
+      if (r3) v = cadd(v, transx(1, loc3, halo, t.tin3, prev.orow4, -1, x - t.row3, yl));
+      F[yl * TM + x] = v;
     }
     csync();
     stamp(ti, 1);
     // ---- chunk-local solve: L cyclic-reduction levels, the dense top, back substitution
     for (int p = 0; p < NP; ++p) {
-      const int l = ph_level(p), s = 1 << l;
-      const int cnt = pfx[p + 1] - pfx[p];
+      const int l = plan_level(P, p), s = 1 << l;
+      const int cnt = P.pfx[p + 1] - P.pfx[p];
       for (int jp = warp * HW; jp < cnt; jp += kCW * HW) {
         const int j = jp + sub;
         const bool has = j < cnt;
-        const int yl = has && p != L ? item_yl(p, j) : 0;
-        const int i = base + pfx[p] + j;
-        dbg_ti = ti; dbg_p = p; dbg_j = j;
-        const double2* m0 = has ? acquire(i) : nullptr;
-        const double2* m1 = m0 + TM2;
+        const int yl = has && p != L ? plan_yl(P, p, j) : 0;
+        const int r = P.pfx[p] + j;
+        const Item it = has ? acquire(ti, r) : Item{nullptr, nullptr};
+        const double2* m0 = it.m0;
+        const double2* m1 = it.m1;
         if (has) {
           if (p == L) {            // partial x_r += Q[r][c0] f_c0 + Q[r][c0+1] f_c0+1
             const int c0 = 2 * (j % QP);
@@ -1107,9 +1175,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
             if (wr) Yv[yl * TM + x] = csub(Yv[yl * TM + x], acc);
           }
         }
-        stamp2(ti, p, j, 3);
-        release(i, has);
-        stamp2(ti, p, j, 4);
+        release(ti, r, has);
       }
       csync();
       if (p == L) {   // x at the level-L points = sum of the column-pair partials
@@ -1120,6 +1186,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
           Yv[r * S * TM + xx] = acc;
         }
         csync();
+        if (ti + 1 < fcount) prefetch_rhs(tn);   // F is free from here on
       }
       stamp(ti, 2 + p);
     }
@@ -1131,7 +1198,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
         if (rank > 0) st_async_c(map_rank(&tau[(2 * (rank - 1) + 1) * TM + lane], d), Yv[lane], bar);
         if (rank < B) st_async_c(map_rank(&tau[(2 * rank) * TM + lane], d), Yv[(m - 1) * TM + lane], bar);
       }
-      mbar_wait_cluster(&xbar[par], (uint32_t)(ti >> 1) & 1);
+      mbar_wait(&xbar[par], (uint32_t)(ti >> 1) & 1);
       stamp(ti, 40);
       // ---- alpha_{k-1}, beta_k = (rows of R) tau: 2B column blocks over warps
       // rows r0 = lane (tm 32) or x (tm 16, per half) and r0 + 32 / r0 + 16
@@ -1141,18 +1208,24 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       for (int jp = warp * HW; jp < nq; jp += kCW * HW) {
         const int j = jp + sub;
         const bool has = j < nq;
-        const int i = base + pfx[NP] + j;
+        const int r = P.pfx[NP] + j;
         if (has) {
-          const double2* mq = acquire(i);   // 2tm x tm, row index fastest
+          const Item it = acquire(ti, r);   // 2tm x tm, row index fastest, over two blocks
           const double2* tq = tau + j * TM;
 #pragma unroll 4
-          for (int c = 0; c < TM; ++c) {
+          for (int c = 0; c < TM / 2; ++c) {
             const double2 tv = tq[c];
-            acc0 = cfma(mq[c * N2 + r0], tv, acc0);
-            if (HW == 2 || TM == 32) acc1 = cfma(mq[c * N2 + r1], tv, acc1);
+            acc0 = cfma(it.m0[c * N2 + r0], tv, acc0);
+            if (HW == 2 || TM == 32) acc1 = cfma(it.m0[c * N2 + r1], tv, acc1);
+          }
+#pragma unroll 4
+          for (int c = 0; c < TM / 2; ++c) {
+            const double2 tv = tq[TM / 2 + c];
+            acc0 = cfma(it.m1[c * N2 + r0], tv, acc0);
+            if (HW == 2 || TM == 32) acc1 = cfma(it.m1[c * N2 + r1], tv, acc1);
           }
         }
-        release(i, has);
+        release(ti, r, has);
       }
       if (HW == 2) {   // both halves' items hold rows x and x + 16
         acc0 = cadd(acc0, shfl_xor_c(acc0, 16));
@@ -1174,15 +1247,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       for (int jp = warp * HW; jp < m; jp += kCW * HW) {
         const int j = jp + sub;
         const bool has = j < m;
-        const int i = base + pfx[NP + 1] + j;
+        const int r = P.pfx[NP + 1] + j;
         if (has) {
-          const double2* ms = acquire(i);
-          const double2 acc = mvx<TM, HW>(rank > 0 ? ms : nullptr, rank > 0 ? ab : nullptr,
-                                      rank < B ? ms + TM2 : nullptr, rank < B ? ab + TM : nullptr,
+          const Item it = acquire(ti, r);   // W_j, V_j
+          const double2 acc = mvx<TM, HW>(rank > 0 ? it.m0 : nullptr, rank > 0 ? ab : nullptr,
+                                      rank < B ? it.m1 : nullptr, rank < B ? ab + TM : nullptr,
                                       lane);
           if (wr) Yv[j * TM + x] = csub(Yv[j * TM + x], acc);
         }
-        release(i, has);
+        release(ti, r, has);
       }
       stamp(ti, 42);
       csync();
@@ -1215,8 +1288,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   cl.sync();   // no CTA leaves while a peer may still write its shared memory
   if (a.dbg && threadIdx.x == 0 && blockIdx.x < 16)
     for (int k = 0; k < 128; ++k) {
-      a.dbg[blockIdx.x * 256 + k] = tsm[k];
-      a.dbg[blockIdx.x * 256 + 128 + k] = tprod[k];
+      a.dbg[blockIdx.x * 1024 + k] = tsm[k];
     }
 }
 
@@ -1369,11 +1441,26 @@ int factorize(Ctx* c, Sweep* s, const std::vector<SlabInfo>& info, const Chunks&
     HS_TRYF(cudaGetLastError(), "bcr keep");
   }
   HS_TRYF(launch_dense_top<TM>(c, g, J, D, Lc, Uc, s->qd, d_err), "dense top");
+  // repack into per-(slab, chunk) streams in the solve kernel's item order
+  long long nbs = 1;
+  for (int k = 0; k < C; ++k) nbs = std::max<long long>(nbs, stream_blocks<TM>(g, k));
+  s->nbs = nbs;
+  HS_TRYF(cudaMalloc((void**)&s->stream, (size_t)J * C * nbs * TM2 * sizeof(double2)),
+          "stream alloc");
+  k_pack<TM><<<J * C, 256, 0, c->stream>>>(g, FactorArrays{s->ef, s->eb, s->kr, s->rk, s->sp, s->qd},
+                                            s->stream, (int)nbs);
+  c->launches++;
+  HS_TRYF(cudaGetLastError(), "pack");
   unsigned long long err = 0;
   HS_TRYF(cudaMemcpyAsync(&err, d_err, sizeof err, cudaMemcpyDeviceToHost, c->stream), "err");
   HS_TRYF(cudaStreamSynchronize(c->stream), "factor sync");
 #undef HS_TRYF
   cleanup();
+  for (double2** p : {&s->ef, &s->eb, &s->kr, &s->sp, &s->rk, &s->qd}) {
+    cudaFree(*p);
+    *p = nullptr;
+  }
+  s->factor_bytes = (long long)J * C * nbs * TM2 * (long long)sizeof(double2);
   if (err != ~0ull) {
     const int slab = (int)(err >> 40);
     const long long row = (long long)(err & 0xffffffffffull);
@@ -1468,7 +1555,10 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   s->L = 0;
   while ((s->mmax - 1) / (1 << s->L) + 1 > qmax) ++s->L;
   s->q = (s->mmax - 1) / (1 << s->L) + 1;
-  if (s->L >= kMaxLevels) { delete s; return set_error(c, HS_E_SHAPE, "face too long"); }
+  if (s->L >= kMaxLevels || itab_len(s->mmax) > kMaxItems) {
+    delete s;
+    return set_error(c, HS_E_SHAPE, "face too long for the sweep's chunking");
+  }
   const Chunks g = make_chunks(s);
   s->kstride = g.kstride;
   const int B = C - 1;
@@ -1564,19 +1654,8 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   };
   // factor blocks streamed per slab solve (exactly the items of k_part_solve)
   double rec_blocks = 0;
-  for (int k = 0; k < C; ++k) {
-    const int m = g.len(k), L = s->L;
-    for (int l = 0; l < L; ++l) {
-      const int sl = 1 << l;
-      for (int yl = 0; yl < m; yl += sl) {
-        if ((yl >> l) & 1) rec_blocks += 1 + 1 + (yl + sl < m);   // Dinv; back: Dinv L (+ Dinv U)
-        else rec_blocks += (yl > 0) + (yl + sl < m);              // alpha, gamma
-      }
-    }
-    const int qk = (m - 1) / (1 << L) + 1;
-    rec_blocks += (double)qk * qk;
-    if (B > 0) rec_blocks += 4.0 * B + 2.0 * m;                   // R rows, spikes
-  }
+  for (int k = 0; k < C; ++k)
+    rec_blocks += TM == 16 ? stream_blocks<16>(g, k) : stream_blocks<32>(g, k);
   const double rec_bytes = rec_blocks * TM2 * 16.0;
   // one solve launch per stage (up to two concurrent fronts)
   auto emit_pass = [&](std::vector<SweepLaunch>& plan, int src,
@@ -1668,6 +1747,7 @@ void sweep_destroy(Sweep* s) {
   cudaFree(s->sp);
   cudaFree(s->rk);
   cudaFree(s->qd);
+  cudaFree(s->stream);
   cudaFree(s->trace);
   cudaFree(s->g);
   cudaFree(s->u2);
@@ -1704,13 +1784,9 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u) {
           a.fcount[i] = i < Lh.nfront ? Lh.fcount[i] : 0;
         }
         a.g = make_chunks(s);
-        a.nslot = s->tm == 16 ? Ring<16>::nslot(s->mmax) : Ring<32>::nslot(s->mmax);
-        a.ef = s->ef;
-        a.eb = s->eb;
-        a.kr = s->kr;
-        a.sp = s->sp;
-        a.rk = s->rk;
-        a.qd = s->qd;
+        a.nchunk = s->tm == 16 ? Ring<16>::nchunk(s->mmax) : Ring<32>::nchunk(s->mmax);
+        a.stream = s->stream;
+        a.nbs = s->nbs;
         a.src = Lh.src ? s->g : f;
         a.coarse = s->coarse->d.coeffs;
         a.ncoarse = s->coarse->d.n;
@@ -1722,8 +1798,8 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u) {
         static bool traced = false;
         unsigned long long* dbg = nullptr;
         if (trace_path && !traced && Lh.nfront == 2) {
-          cudaMalloc((void**)&dbg, 16 * 256 * sizeof(unsigned long long));
-          cudaMemsetAsync(dbg, 0, 16 * 256 * sizeof(unsigned long long), c->stream);
+          cudaMalloc((void**)&dbg, 16 * 1024 * sizeof(unsigned long long));
+          cudaMemsetAsync(dbg, 0, 16 * 1024 * sizeof(unsigned long long), c->stream);
         }
         a.dbg = dbg;
         const int smem = s->tm == 16 ? Ring<16>::smem(s->mmax) : Ring<32>::smem(s->mmax);
@@ -1735,7 +1811,7 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u) {
         if (e != cudaSuccess) return check_cuda(c, e, "sweep solve launch");
         HS_LAUNCH_CHECK(c, "sweep solve kernel");
         if (dbg) {
-          std::vector<unsigned long long> h(16 * 256);
+          std::vector<unsigned long long> h(16 * 1024);
           cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, c->stream);
           cudaStreamSynchronize(c->stream);
           cudaFree(dbg);
@@ -1746,8 +1822,8 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u) {
             fprintf(fp, "# C=%d M=%d L=%d q=%d\n", s->C, M, s->L, s->q);
             const unsigned long long t0 = h[0];
             for (int b = 0; b < std::min(16, s->C); ++b) {
-              for (int k = 0; k < 256; ++k)
-                fprintf(fp, "%lld ", h[b * 256 + k] ? (long long)(h[b * 256 + k] - t0) : -1LL);
+              for (int k = 0; k < 1024; ++k)
+                fprintf(fp, "%lld ", h[b * 1024 + k] ? (long long)(h[b * 1024 + k] - t0) : -1LL);
               fprintf(fp, "\n");
             }
             fclose(fp);
