@@ -1098,6 +1098,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     return cscale(which == 0 ? (double)sign : (double)-sign, acc);
   };
   const uint32_t halo_bytes = (rank > 0 ? TM * 16 : 0) + (rank < B ? TM * 16 : 0);
+  // tips g[first], g[last] of this chunk go to every CTA's tau:
+  // tau block b = (g_b[last], g_{b+1}[first]) -> tm-slots 2b, 2b+1
+  auto push_tip = [&](double2* tau, int par, int slot, const double2* v) {   // lanes < TM
+    const double2 val = v[lane];
+    for (int d = warp - (kCW - 8); d < C; d += 8)
+      st_async_c(map_rank(&tau[slot + lane], d), val, map_rank(&xbar[par], d));
+  };
+  // phase after which g[m-1] is final: the dense top or its back-substitution level
+  const int p_last = (m - 1) % S == 0 ? L : 2 * L - __ffs(m - 1) + 1;
 
   SweepTask prev{}, t = fcount > 0 ? a.tasks[ffirst] : SweepTask{};
   if (fcount > 0) prefetch_rhs(t);
@@ -1124,7 +1133,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     // ---- right-hand side of the owned blocks: restriction rows (already in
     // F) plus the transmission terms of the incoming traces
     asm volatile("cp.async.wait_all;" ::: "memory");
-    if (loc1 || loc3) mbar_wait(&xbar[2 + par], (uint32_t)((ti - 1) >> 1) & 1);
+    // (always: the neighbours' previous task is then complete, which also
+    // orders the double-buffered tau/halo reuse across the cluster)
+    if (ti > 0) mbar_wait(&xbar[2 + par], (uint32_t)((ti - 1) >> 1) & 1);
     csync();
     for (int yl = warp * YPW + hh; yl < m; yl += kCW * YPW) {
       const bool r1 = t.tin1 >= 0 && (x == t.row1 || x == t.row1 + 1);
@@ -1188,16 +1199,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
         csync();
         if (ti + 1 < fcount) prefetch_rhs(tn);   // F is free from here on
       }
+      // a tip is final once its level is done: send it right away
+      if (B > 0 && lane < TM && warp >= kCW - 8) {   // high warps: idle in small phases
+        if (p == L && rank > 0) push_tip(tau, par, (2 * (rank - 1) + 1) * TM, Yv);
+        if (p == p_last && rank < B) push_tip(tau, par, 2 * rank * TM, Yv + (m - 1) * TM);
+      }
       stamp(ti, 2 + p);
     }
     if (B > 0) {
-      // ---- push this chunk's tips g[first], g[last] into every CTA's tau:
-      // tau block b = (g_b[last], g_{b+1}[first]) -> tm-slots 2b, 2b+1
-      for (int d = warp; d < C && lane < TM; d += kCW) {
-        const uint32_t bar = map_rank(&xbar[par], d);
-        if (rank > 0) st_async_c(map_rank(&tau[(2 * (rank - 1) + 1) * TM + lane], d), Yv[lane], bar);
-        if (rank < B) st_async_c(map_rank(&tau[(2 * rank) * TM + lane], d), Yv[(m - 1) * TM + lane], bar);
-      }
+      // ---- every chunk's tips (pushed as soon as final) are in tau
       mbar_wait(&xbar[par], (uint32_t)(ti >> 1) & 1);
       stamp(ti, 40);
       // ---- alpha_{k-1}, beta_k = (rows of R) tau: 2B column blocks over warps
