@@ -61,6 +61,29 @@ def dist_info():
     return world, rank, local
 
 
+def assign_rhs(nrhs: int, world: int, rank: int) -> list[int]:
+    """Right-hand sides solved by ``rank``: round-robin over ranks; with fewer
+    right-hand sides than ranks every rank solves a replica of one."""
+    return [r for r in range(nrhs) if r % world == rank] or [rank % nrhs]
+
+
+def reduce_over_ranks(x: float, world: int, op: str = "max", device=None) -> float:
+    """max / sum of a per-rank scalar over the process group (identity for
+    world == 1); ``device``: "cuda" under NCCL, "cpu" under gloo."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device or "cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def job_value(n_fine: int, solves_all_ranks: float, ms_max: float) -> float:
+    """Whole-job throughput: fine DOF of every solve on every rank / slowest rank's time."""
+    return n_fine * solves_all_ranks / (ms_max / 1e3)
+
+
 def peaks():
     f = ROOT / "MEASURED_PEAKS.json"
     if f.exists():
@@ -212,7 +235,7 @@ def run_ours(args):
     setup_s = time.perf_counter() - t0
     ctx = context()
     nrhs_total = p.f.shape[0]
-    mine = [r for r in range(nrhs_total) if r % world == rank] or [rank % nrhs_total]
+    mine = assign_rhs(nrhs_total, world, rank)
     f_dev = [torch.from_numpy(p.f[r].ravel()).cuda() for r in mine]
     cfg = hb.GmresConfig(p.tol, p.max_iter, p.restart)
     prec = cycle.as_preconditioner()
@@ -248,13 +271,9 @@ def run_ours(args):
     if world > 1:
         torch.distributed.barrier()
     ms_local = ev0.elapsed_time(ev1)
-    ms = ms_local
-    if world > 1:
-        t = torch.tensor([ms_local], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    solves = args.steps * len(f_dev) * world
-    value = p.n_fine * solves / (ms / 1e3)
+    ms = reduce_over_ranks(ms_local, world, "max")
+    solves = reduce_over_ranks(args.steps * len(f_dev), world, "sum")
+    value = job_value(p.n_fine, solves, ms)
     its = [r.iterations for r in reports]
     # true residual of the last solve
     u_h = u.cpu().numpy()
@@ -271,12 +290,8 @@ def run_ours(args):
             u_out, _ = hb.gmres(cycle.fine_csr, prec, fh, cfg, orth=args.orth)
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = p.n_fine * solves / (e2e_ms / 1e3)
+    e2e_ms = reduce_over_ranks(e0.elapsed_time(e1), world, "max")
+    e2e_value = job_value(p.n_fine, solves, e2e_ms)
 
     # ---- roofline of the dominant kernel class (profiler events over the timed region)
     peak, peak_kind = peaks()

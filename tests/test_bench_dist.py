@@ -1,0 +1,59 @@
+"""Multi-rank host logic of bench.py (rank partitioning of right-hand sides,
+max-over-ranks timing, whole-job value) on a world_size-2 gloo group (CPU)."""
+
+import json
+import os
+import socket
+import sys
+from pathlib import Path
+
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out_dir):
+    sys.path.insert(0, str(ROOT))
+    import torch.distributed as dist
+    import bench
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = bench.assign_rhs(8, world, rank)
+    replica = bench.assign_rhs(1, world, rank)
+    ms = bench.reduce_over_ranks(10.0 + 5.0 * rank, world, "max", device="cpu")
+    solves = bench.reduce_over_ranks(3 * len(mine), world, "sum", device="cpu")
+    value = bench.job_value(1000, solves, ms)
+    dist.barrier()
+    dist.destroy_process_group()
+    Path(out_dir, f"r{rank}.json").write_text(json.dumps(
+        {"mine": mine, "replica": replica, "ms": ms, "solves": solves, "value": value}))
+
+
+def test_bench_rank_logic_gloo(tmp_path):
+    world = 2
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    res = [json.loads((tmp_path / f"r{r}.json").read_text()) for r in range(world)]
+    # right-hand sides: disjoint, complete cover; single rhs -> replicas
+    assert sorted(res[0]["mine"] + res[1]["mine"]) == list(range(8))
+    assert not set(res[0]["mine"]) & set(res[1]["mine"])
+    assert res[0]["replica"] == res[1]["replica"] == [0]
+    for r in res:
+        assert r["ms"] == 15.0                      # max over ranks (slowest rank)
+        assert r["solves"] == 24                    # 3 steps x 8 rhs over both ranks
+        assert r["value"] == pytest.approx(1000 * 24 / 0.015)
+
+
+def test_bench_single_rank_identity():
+    sys.path.insert(0, str(ROOT))
+    import bench
+    assert bench.reduce_over_ranks(3.5, 1) == 3.5
+    assert bench.assign_rhs(1, 1, 0) == [0]
+    assert bench.assign_rhs(4, 1, 0) == [0, 1, 2, 3]
