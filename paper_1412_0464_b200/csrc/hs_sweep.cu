@@ -571,6 +571,7 @@ struct SolveArgs {
   int nchunk;              // ring slots (16-KB chunks)
   const double2* stream;   // [J][C][nbs] factor blocks in item order
   int64_t nbs;
+  const uint32_t* plan;    // [C][plan_words] item / chunk tables (chunk_plan)
   const double2* src;      // right-hand side field (n0 x M)
   const double2* coarse;   // global coarse operator [S][n0*M] (transmission couplings)
   int64_t ncoarse;
@@ -791,6 +792,49 @@ __host__ __device__ inline int stream_blocks(const Chunks& g, int rank) {
   return nb;
 }
 
+template <int TM>
+__host__ __device__ constexpr int ring_g() { return TM == 16 ? HS_SWEEP_G16 : 2; }
+
+// Words of one rank's solve plan: ItemPlan, ib[itab_len], ctab[itab_len], nchk.
+__host__ __device__ inline int plan_words(int mmax) {
+  return (int)(sizeof(ItemPlan) / 4) + 2 * itab_len(mmax) + 1;
+}
+// The solve kernel's item and chunk tables of one rank (built on the host
+// once per sweep).  Chunks: runs of whole items of one phase, up to G blocks
+// (one bulk copy each); a ring slot is released as soon as its items are
+// consumed, so a chunk never waits for a later phase.
+//   ib[r]   = chunk << 12 | offset in chunk << 3 | blocks << 1 | hasx
+//   ctab[c] = first stream block << 8 | blocks
+template <int TM>
+__host__ __device__ inline void chunk_plan(const Chunks& g, int rank, int mmax, uint32_t* w) {
+  constexpr int G = ring_g<TM>();
+  ItemPlan& P = *(ItemPlan*)w;
+  uint32_t* ib = w + sizeof(ItemPlan) / 4;
+  uint32_t* ctab = ib + itab_len(mmax);
+  plan_items(g, rank, P);
+  int acc = 0, nc = -1, cfill = G, ph = 0;
+  uint32_t src[2];
+  bool hx;
+  for (int r = 0; r < P.pfx[P.NP + 2]; ++r) {   // stream order (k_pack's)
+    const int n = item_sources<TM>(g, rank, P, r, src, &hx);
+    bool new_phase = false;
+    while (P.pfx[ph + 1] <= r) {
+      ++ph;
+      new_phase = true;
+    }
+    if (new_phase || cfill + n > G) {
+      ++nc;
+      ctab[nc] = (uint32_t)acc << 8;
+      cfill = 0;
+    }
+    ib[r] = (uint32_t)nc << 12 | (uint32_t)cfill << 3 | (uint32_t)n << 1 | (hx ? 1u : 0u);
+    ctab[nc] += (uint32_t)n;
+    cfill += n;
+    acc += n;
+  }
+  ctab[itab_len(mmax)] = (uint32_t)(nc + 1);   // nchk
+}
+
 struct FactorArrays {
   const double2 *ef, *eb, *kr, *rk, *sp, *qd;
 };
@@ -868,7 +912,7 @@ __device__ __forceinline__ double2 mvx(const double2* m0, const double2* v0, con
 template <int TM>
 struct Ring {
   static constexpr int TM2 = TM * TM;
-  static constexpr int G = TM == 16 ? HS_SWEEP_G16 : 2;   // blocks per chunk copy (>= 2: whole items)
+  static constexpr int G = ring_g<TM>();           // blocks per chunk copy (>= 2: whole items)
   static constexpr int CHUNK = G * TM2;            // double2 per chunk
   // F, Yv vectors + tau + halo + R partials + couplings + bookkeeping, then the ring
   static int fixed(int mmax) {
@@ -916,40 +960,24 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   uint64_t* cbar = xbar + 4;                        // [NC] chunk arrival
   volatile int* cseq = (volatile int*)(cbar + NC);  // [NC] chunk issued into a slot
   int* ccnt = (int*)(cseq + NC);                    // [NC] blocks of the slot's chunk consumed
-  ItemPlan* Pp = (ItemPlan*)(ccnt + NC);
-  int* slabs = (int*)(Pp + 1);                      // [fcount]
-  uint32_t* ib = (uint32_t*)(slabs + kMaxTasks);    // [ITEMS] chunk | offset in chunk | nblk | hasx
+  uint32_t* plan = (uint32_t*)(ccnt + NC);          // this rank's plan (chunk_plan layout)
+  ItemPlan* Pp = (ItemPlan*)plan;
+  uint32_t* ib = plan + sizeof(ItemPlan) / 4;       // [ITEMS] chunk | offset in chunk | nblk | hasx
   uint32_t* ctab = ib + itab_len(mmax);             // [<= ITEMS] chunk: first block | blocks
   int* nchk = (int*)(ctab + itab_len(mmax));        // chunks per slab solve
+  int* slabs = nchk + 1;                            // [fcount]
   // (offset from sm keeps the shared-space provenance: LDS, not generic loads)
-  double2* ring = sm + ((((char*)(nchk + 1) - (char*)sm) + 127) & ~(ptrdiff_t)127) / 16;
+  double2* ring = sm + ((((char*)(slabs + kMaxTasks) - (char*)sm) + 127) & ~(ptrdiff_t)127) / 16;
   const ItemPlan& P = *Pp;
 
   const int ffirst = front ? a.ffirst[1] : a.ffirst[0];
   const int fcount = front ? a.fcount[1] : a.fcount[0];
+  {
+    const int pw = plan_words(mmax);
+    const uint32_t* src = a.plan + (int64_t)rank * pw;
+    for (int i = threadIdx.x; i < pw; i += blockDim.x) plan[i] = __ldg(src + i);
+  }
   if (threadIdx.x == 0) {
-    plan_items(g, rank, *Pp);
-    // Chunks: runs of whole items of one phase, up to G blocks (one bulk copy
-    // each); a slot is released as soon as its items are consumed, so a chunk
-    // never waits for a later phase.
-    int acc = 0, nc = -1, cfill = G, ph = 0;
-    uint32_t src[2];
-    bool hx;
-    for (int r = 0; r < Pp->pfx[Pp->NP + 2]; ++r) {   // stream offsets (k_pack's order)
-      const int n = item_sources<TM>(g, rank, *Pp, r, src, &hx);
-      bool new_phase = false;
-      while (Pp->pfx[ph + 1] <= r) { ++ph; new_phase = true; }
-      if (new_phase || cfill + n > G) {
-        ++nc;
-        ctab[nc] = (uint32_t)acc << 8;
-        cfill = 0;
-      }
-      ib[r] = (uint32_t)nc << 12 | (uint32_t)cfill << 3 | (uint32_t)n << 1 | (hx ? 1u : 0u);
-      ctab[nc] += (uint32_t)n;
-      cfill += n;
-      acc += n;
-    }
-    *nchk = nc + 1;
     for (int i = 0; i < NC; ++i) {
       mbar_init(&cbar[i], 1);
       cseq[i] = -1;
@@ -1085,13 +1113,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
                     int which, int yl) -> double2 {
     const int y = Y0 + yl;
     const int xr = prow + (which == 0 ? 1 : 0);   // trace row 1 feeds which 0, row 0 which 1
-    const double2* Bt = a.trace + (int64_t)buf * 2 * M + (which == 0 ? M : 0);
+    const double2* Bt = a.trace + (int64_t)buf * 2 * M + (which == 0 ? M : 0);   // L2 reads (__ldcg)
     double2 acc = czero();
 #pragma unroll
     for (int o = -1; o <= 1; ++o) {
       if (y + o < 0 || y + o >= M) continue;
       const int q = yl + o;
-      const double2 bv = !local ? Bt[y + o]
+      const double2 bv = !local ? __ldcg(Bt + y + o)
                          : q < 0 ? halo[xr] : q >= m ? halo[TM + xr] : Yv[q * TM + xr];
       acc = cfma(stc[((tn_i * 2 + which) * 3 + o + 1) * mmax + yl], bv, acc);
     }
@@ -1593,6 +1621,21 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     sweep_destroy(s);
     return r;
   }
+  {   // the solve kernel's per-rank item / chunk tables
+    const int pw = plan_words(s->mmax);
+    std::vector<uint32_t> hp((size_t)C * pw, 0u);
+    for (int k = 0; k < C; ++k) {
+      if (TM == 16) chunk_plan<16>(g, k, s->mmax, hp.data() + (size_t)k * pw);
+      else chunk_plan<32>(g, k, s->mmax, hp.data() + (size_t)k * pw);
+    }
+    e = cudaMalloc((void**)&s->ptab, hp.size() * sizeof(uint32_t));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(s->ptab, hp.data(), hp.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      sweep_destroy(s);
+      return check_cuda(c, e, "plan upload");
+    }
+  }
 
   // ---- schedules (task lists) ----
   int ntin = 0;
@@ -1721,7 +1764,7 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     MI.push_back(mi);
     emit_pass(plan, 0, {{F, Bk}, {MI}});
     plan.push_back(SweepLaunch{SweepLaunch::kResidual});
-    std::vector<SweepTask> MO, BB, FF;
+    std::vector<SweepTask> BB, FF;
     SweepTask mo = mk(jm, (int)bt[jm - 1], (int)beta[jm]);
     bwd_chain(jm - 1, 1, BB);
     fwd_chain(jm + 1, J, FF);
@@ -1729,8 +1772,11 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     if (!BB.empty()) give4(mo, jm, BB.front().tin3);
     clear_placeholders(BB);
     clear_placeholders(FF);
-    MO.push_back(mo);
-    emit_pass(plan, 1, {{MO}, {BB, FF}});
+    // the middle solve opens both outward fronts (computed by both clusters,
+    // identical results), so pass 2 is one launch with in-cluster handoffs
+    BB.insert(BB.begin(), mo);
+    FF.insert(FF.begin(), mo);
+    emit_pass(plan, 1, {{BB, FF}});
     plan.push_back(SweepLaunch{SweepLaunch::kCombine});
     s->has_plan[HS_VARIANT_X] = true;
   }
@@ -1758,6 +1804,7 @@ void sweep_destroy(Sweep* s) {
   cudaFree(s->rk);
   cudaFree(s->qd);
   cudaFree(s->stream);
+  cudaFree(s->ptab);
   cudaFree(s->trace);
   cudaFree(s->g);
   cudaFree(s->u2);
@@ -1797,6 +1844,7 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u) {
         a.nchunk = s->tm == 16 ? Ring<16>::nchunk(s->mmax) : Ring<32>::nchunk(s->mmax);
         a.stream = s->stream;
         a.nbs = s->nbs;
+        a.plan = s->ptab;
         a.src = Lh.src ? s->g : f;
         a.coarse = s->coarse->d.coeffs;
         a.ncoarse = s->coarse->d.n;

@@ -43,6 +43,7 @@ struct Sweep {
   double2* qd = nullptr;        // [J][C][q][q][tm^2]    inverse of the level-L reduced chunk system
   double2* stream = nullptr;    // [J][C][nbs][tm^2]     all of the above in solve order (setup frees the rest)
   long long nbs = 0;            // blocks per (slab, chunk) stream
+  uint32_t* ptab = nullptr;     // [C][plan words] solve-kernel item / chunk tables
   double2* trace = nullptr;     // [ntrace][2][M] interface traces
   double2* g = nullptr;         // [n0*M] mid-sweep residual
   double2* u2 = nullptr;        // [n0*M] second-pass contributions
