@@ -64,10 +64,17 @@ constexpr int kCW = kWarps - 1;
 #ifndef HS_SWEEP_L2NEXT    // consumers prefetch the next slab's stream into L2
 #define HS_SWEEP_L2NEXT 0
 #endif
+#ifndef HS_SWEEP_EXP       // timing experiments: 1 no item arithmetic, 2 no factor copies
+#define HS_SWEEP_EXP 0
+#endif
+#ifndef HS_SWEEP_DIRECT    // experiment: consumers read factor blocks straight from global memory
+#define HS_SWEEP_DIRECT 0
+#endif
 #ifndef HS_SWEEP_G16       // tm 16: blocks per ring chunk (bulk copy)
 #define HS_SWEEP_G16 4
 #endif
 constexpr int kMaxC = 16;
+constexpr int kNR = 8;             // rows of a restricted (last-level / spike) update
 constexpr int kMaxTasks = 1024;    // slab solves per front per launch
 
 template <int TM>
@@ -93,6 +100,7 @@ struct SlabInfo {
 struct Chunks {
   int M, C, L, kstride;
   int q;                   // dense top: blocks per chunk left after L levels
+  int nr;                  // restricted level-0 / spike updates (kNR rows) or 0
   int koff[kMaxLevels];
   __host__ __device__ int y0(int k) const { return (int)((int64_t)k * M / C); }
   __host__ __device__ int len(int k) const { return y0(k + 1) - y0(k); }
@@ -572,6 +580,7 @@ struct SolveArgs {
   const double2* stream;   // [J][C][nbs] factor blocks in item order
   int64_t nbs;
   const uint32_t* plan;    // [C][plan_words] item / chunk tables (chunk_plan)
+  const int* rows;         // [J][kNR] rows of the restricted updates (g.nr != 0)
   const double2* src;      // right-hand side field (n0 x M)
   const double2* coarse;   // global coarse operator [S][n0*M] (transmission couplings)
   int64_t ncoarse;
@@ -654,6 +663,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 template <int TM>
 __device__ __forceinline__ double2 mvs2(const double2* m0, const double2* v0, const double2* m1,
                                         const double2* v1, int lane) {
+  if (HS_SWEEP_EXP & 1) return czero();
   constexpr int CPL = Geo<TM>::CPL;
   const int hh = lane / TM;
   double2 a0 = czero(), a1 = czero(), a2 = czero(), a3 = czero();
@@ -723,7 +733,9 @@ __host__ __device__ inline int plan_yl(const ItemPlan& P, int p, int j) {
 }
 
 // Factor arrays of one slab before packing (setup only).
-enum ItemArray : uint32_t { kArrEf = 0, kArrEb = 1, kArrKr = 2, kArrRk = 3, kArrSp = 4, kArrQd = 5 };
+enum ItemArray : uint32_t {
+  kArrEf = 0, kArrEb = 1, kArrKr = 2, kArrRk = 3, kArrSp = 4, kArrQd = 5, kArrEbr = 6, kArrSpr = 7
+};
 __host__ __device__ constexpr uint32_t item_enc(uint32_t arr, int64_t off) {
   return (arr << 29) | (uint32_t)off;
 }
@@ -759,6 +771,8 @@ __host__ __device__ inline int item_sources(const Chunks& g, int rank, const Ite
         if (yl - s >= 0) src[n++] = item_enc(kArrKr, k2);
         if (yl + s < m) src[n++] = item_enc(kArrKr, k2 + TM2);
       }
+    } else if (g.nr && l == 0 && yl != m - 1) {   // restricted level-0 update (one block)
+      src[n++] = item_enc(kArrEbr, y * TM2);
     } else {
       if (yl - s >= 0) src[n++] = item_enc(kArrEb, y * 2 * TM2);
       if (yl + s < m) src[n++] = item_enc(kArrEb, y * 2 * TM2 + TM2);
@@ -767,6 +781,8 @@ __host__ __device__ inline int item_sources(const Chunks& g, int rank, const Ite
     const int64_t o = ((int64_t)rank * (2 * P.B) + j) * (2 * TM2);
     src[n++] = item_enc(kArrRk, o);
     src[n++] = item_enc(kArrRk, o + TM2);
+  } else if (g.nr) {         // spikes W, V of block j, restricted to the kNR rows
+    src[n++] = item_enc(kArrSpr, (int64_t)(Y0 + j) * TM2);
   } else {                   // spikes W, V of block j
     const int64_t o = (int64_t)(Y0 + j) * 2 * TM2;
     src[n++] = item_enc(kArrSp, o);
@@ -836,8 +852,28 @@ __host__ __device__ inline void chunk_plan(const Chunks& g, int rank, int mmax, 
 }
 
 struct FactorArrays {
-  const double2 *ef, *eb, *kr, *rk, *sp, *qd;
+  const double2 *ef, *eb, *kr, *rk, *sp, *qd, *ebr, *spr;
 };
+
+// Restricted updates (setup): for the kNR rows R of each slab, one block per
+// face point holding [A0[R, :] | A1[R, :]] laid out for a 32-lane GEMV:
+// element (k, q, r) at k*32 + q*8 + r, q = 2*matrix + column half,
+// column = k + (q & 1) * tm/2.  ebr: (Dinv L, Dinv U); spr: (W, V).
+template <int TM>
+__global__ void __launch_bounds__(256) k_rows(Chunks g, const int* __restrict__ rows,
+                                              const double2* __restrict__ eb,
+                                              const double2* __restrict__ sp,
+                                              double2* __restrict__ ebr, double2* __restrict__ spr) {
+  constexpr int TM2 = TM * TM, H = TM / 2;
+  const int y = blockIdx.x, slab = blockIdx.y, M = g.M;
+  const int64_t b = ((int64_t)slab * M + y);
+  for (int e = threadIdx.x; e < H * 32; e += blockDim.x) {
+    const int k = e / 32, q = (e % 32) / 8, r = e % 8;
+    const int row = rows[slab * kNR + r], col = k + (q & 1) * H, mat = q >> 1;
+    ebr[b * TM2 + e] = eb[(b * 2 + mat) * TM2 + lm<TM>(row, col)];
+    spr[b * TM2 + e] = sp[(b * 2 + mat) * TM2 + lm<TM>(row, col)];
+  }
+}
 
 // Repack every slab's factors into per-chunk streams in item order (one CTA
 // per slab x chunk), so the solve kernel fetches 16-KB runs with single bulk
@@ -860,11 +896,13 @@ __global__ void __launch_bounds__(256) k_pack(Chunks g, FactorArrays f, double2*
     }
   }
   __syncthreads();
-  const double2* base[6] = {
+  const double2* base[8] = {
       f.ef + (int64_t)slab * M * TM2,           f.eb + (int64_t)slab * M * 2 * TM2,
       f.kr + (int64_t)slab * C * g.kstride * 2 * TM2,
       f.rk + (int64_t)slab * C * (2 * (C - 1)) * 2 * TM2,
-      f.sp + (int64_t)slab * M * 2 * TM2,       f.qd + (int64_t)slab * C * g.q * g.q * TM2};
+      f.sp + (int64_t)slab * M * 2 * TM2,       f.qd + (int64_t)slab * C * g.q * g.q * TM2,
+      f.ebr ? f.ebr + (int64_t)slab * M * TM2 : nullptr,
+      f.spr ? f.spr + (int64_t)slab * M * TM2 : nullptr};
   double2* out = stream + ((int64_t)slab * C + k) * nbs * TM2;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   for (int r = warp; r < P.pfx[P.NP + 2]; r += 8) {
@@ -909,6 +947,29 @@ __device__ __forceinline__ double2 mvx(const double2* m0, const double2* v0, con
 
 
 // Shared-memory ring of stream chunks: G blocks (16 KB) per bulk copy.
+// Restricted update (k_rows layout): lanes 0..7 return row r = lane of
+// A0[R, :] v0 + A1[R, :] v1 (a term with a null vector is skipped).
+template <int TM>
+__device__ __forceinline__ double2 mvr(const double2* blk, const double2* v0, const double2* v1,
+                                       int lane) {
+  if (HS_SWEEP_EXP & 1) return czero();
+  constexpr int H = TM / 2;
+  const int q = lane / 8;
+  const double2* v = q < 2 ? v0 : v1;
+  double2 a0 = czero(), a1 = czero();
+  if (v) {
+    v += (q & 1) * H;
+#pragma unroll
+    for (int k = 0; k < H; k += 2) {
+      a0 = cfma(blk[k * 32 + lane], v[k], a0);
+      a1 = cfma(blk[(k + 1) * 32 + lane], v[k + 1], a1);
+    }
+  }
+  double2 acc = cadd(a0, a1);
+  acc = cadd(acc, shfl_xor_c(acc, 8));
+  return cadd(acc, shfl_xor_c(acc, 16));
+}
+
 template <int TM>
 struct Ring {
   static constexpr int TM2 = TM * TM;
@@ -922,7 +983,7 @@ struct Ring {
   }
   static int nchunk(int mmax) {
     const int avail = 225 * 1024 - fixed(mmax);
-    return std::max(2, std::min(64, avail / (CHUNK * 16 + 16)));
+    return std::max(2, std::min(32, avail / (CHUNK * 16 + 16)));   // one producer lane per slot
   }
   static int smem(int mmax) { return fixed(mmax) + nchunk(mmax) * (CHUNK * 16 + 16); }
 };
@@ -992,6 +1053,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   const int ITEMS = P.pfx[NP + 2];
   const int CPT = *nchk;   // chunk copies per slab solve
 
+  __shared__ int rr[kNR];   // the current task's restricted-update rows
   // optional instrumentation: task 1 timestamps kept in shared memory, dumped at exit
   __shared__ unsigned long long tsm[128];
   auto stamp = [&](int ti, int k) {
@@ -1016,38 +1078,34 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   };
 
   if (warp == kCW) {
-    // ---- TMA producer warp: streams each slab solve's blocks in 16-KB chunk
-    // copies (one lane per chunk, up to BW in flight per batch) as soon as the
-    // chunk's ring slot has been fully consumed.
-    const int BW = max(1, min(4, NC / 2));
-    int cs0 = 0;
-    for (int ti = 0; ti < fcount; ++ti) {
-      const double2* sbase = a.stream + ((int64_t)slabs[ti] * C + rank) * a.nbs * TM2;
-      for (int c0 = 0; c0 < CPT; c0 += BW) {
-        const int c = c0 + lane;
-        if (lane < BW && c < CPT) {
-          const int cs = cs0 + c;
-          const int sl = cs % NC;
-          const uint32_t ce = ctab[c];
-          const int nbk = (int)(ce & 0xff);
-          // the slot's previous chunk (cs - NC) fully consumed: its block count
-          if (cs >= NC) {
-            const int prev_n = (int)(ctab[(cs - NC) % CPT] & 0xff);
-            while (*(volatile int*)&ccnt[sl] != prev_n) {
-            }
+    // ---- TMA producer warp: lane l owns ring slot l (l < NC) and streams
+    // chunks cs = l, l + NC, l + 2 NC, ... of the launch's slab solves, each as
+    // soon as the slot's previous chunk has been fully consumed.  Lanes run
+    // independently (no batch lockstep).
+    if (lane < NC && !HS_SWEEP_DIRECT) {
+      const int sl = lane;
+      const int total = fcount * CPT;
+      int prev_n = -1;
+      for (int cs = sl; cs < total; cs += NC) {
+        const int ti = cs / CPT, c = cs - ti * CPT;
+        const uint32_t ce = ctab[c];
+        const int nbk = (int)(ce & 0xff);
+        if (prev_n >= 0) {   // the slot's previous chunk (cs - NC) fully consumed
+          while (*(volatile int*)&ccnt[sl] != prev_n) {
           }
-          ccnt[sl] = 0;
-          __threadfence_block();
-          mbar_expect_tx(&cbar[sl], (uint32_t)nbk * TM2 * 16);
+        }
+        prev_n = nbk;
+        *(volatile int*)&ccnt[sl] = 0;   // ordered before cseq (same thread, volatile)
+        const double2* sbase = a.stream + ((int64_t)slabs[ti] * C + rank) * a.nbs * TM2;
+        mbar_expect_tx(&cbar[sl], (HS_SWEEP_EXP & 2) ? 0u : (uint32_t)nbk * TM2 * 16);
+        if (!(HS_SWEEP_EXP & 2))
           bulk_g2s(ring + (int64_t)sl * CHUNK, sbase + (int64_t)(ce >> 8) * TM2,
                    (uint32_t)nbk * TM2 * 16, &cbar[sl]);
-          cseq[sl] = cs;
-          if (ti == 1) istamp(c, 0);
-        }
-        __syncwarp();
+        cseq[sl] = cs;
+        if (ti == 1) istamp(c, 0);
       }
-      cs0 += CPT;
     }
+    __syncwarp();
     cl.sync();   // matches the consumers' exit barrier
     return;
   }
@@ -1064,6 +1122,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     const uint32_t e = ib[r];
     const int cs = ti * CPT + (int)(e >> 12);
     const bool hx = e & 1;
+    if (HS_SWEEP_DIRECT) {
+      const double2* p0 = a.stream + (((int64_t)slabs[ti] * C + rank) * a.nbs +
+                                      (ctab[e >> 12] >> 8) + ((e >> 3) & 0x1ff)) * TM2;
+      return hx ? Item{p0, p0 + TM2} : Item{nullptr, p0};
+    }
     wait_chunk(cs);
     if (ti == 1 && lane % (32 / HW) == 0) istamp(r, 1);
     const double2* p0 = ring + (int64_t)(cs % NC) * CHUNK + (int)((e >> 3) & 0x1ff) * TM2;
@@ -1073,7 +1136,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   // before the __syncwarp), so the producer's async-proxy refill cannot race.
   auto release = [&](int ti, int r, bool has) {
     __syncwarp();
-    if (has && lane % (32 / HW) == 0) {
+    if (!HS_SWEEP_DIRECT && has && lane % (32 / HW) == 0) {
       const uint32_t e = ib[r];
       atomicAdd(&ccnt[(ti * CPT + (int)(e >> 12)) % NC], (int)((e >> 1) & 3));
       if (ti == 1) istamp(r, 2);
@@ -1158,6 +1221,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       for (int64_t o = (int64_t)threadIdx.x * 128; o < bytes; o += kCW * 32 * 128)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(nb + o));
     }
+    if (g.nr && threadIdx.x < kNR) rr[threadIdx.x] = a.rows[t.slab * kNR + threadIdx.x];
     // ---- right-hand side of the owned blocks: restriction rows (already in
     // F) plus the transmission terms of the incoming traces
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -1206,6 +1270,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
                                           lane);
               if (wr) F[yl * TM + x] = csub(F[yl * TM + x], acc);
             }
+          } else if (g.nr && l == 0 && yl != m - 1) {   // level 0: only the rows read later
+            const double2 acc = mvr<TM>(m0, Yv + (yl - 1) * TM, Yv + (yl + 1) * TM, lane);
+            if (lane < kNR) Yv[yl * TM + rr[lane]] = csub(Yv[yl * TM + rr[lane]], acc);
           } else {                 // x_y = Dinv f - (Dinv L) x_{y-s} - (Dinv U) x_{y+s}
             const bool hl = yl - s >= 0, hr = yl + s < m;
             const double2 acc = mvx<TM, HW>(hl ? m0 : nullptr, hl ? Yv + (yl - s) * TM : nullptr,
@@ -1288,10 +1355,16 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
         const int r = P.pfx[NP + 1] + j;
         if (has) {
           const Item it = acquire(ti, r);   // W_j, V_j
-          const double2 acc = mvx<TM, HW>(rank > 0 ? it.m0 : nullptr, rank > 0 ? ab : nullptr,
-                                      rank < B ? it.m1 : nullptr, rank < B ? ab + TM : nullptr,
-                                      lane);
-          if (wr) Yv[j * TM + x] = csub(Yv[j * TM + x], acc);
+          if (g.nr) {                       // only the rows read later
+            const double2 acc = mvr<TM>(it.m0, rank > 0 ? ab : nullptr, rank < B ? ab + TM : nullptr,
+                                        lane);
+            if (lane < kNR) Yv[j * TM + rr[lane]] = csub(Yv[j * TM + rr[lane]], acc);
+          } else {
+            const double2 acc = mvx<TM, HW>(rank > 0 ? it.m0 : nullptr, rank > 0 ? ab : nullptr,
+                                        rank < B ? it.m1 : nullptr, rank < B ? ab + TM : nullptr,
+                                        lane);
+            if (wr) Yv[j * TM + x] = csub(Yv[j * TM + x], acc);
+          }
         }
         release(ti, r, has);
       }
@@ -1479,14 +1552,21 @@ int factorize(Ctx* c, Sweep* s, const std::vector<SlabInfo>& info, const Chunks&
     HS_TRYF(cudaGetLastError(), "bcr keep");
   }
   HS_TRYF(launch_dense_top<TM>(c, g, J, D, Lc, Uc, s->qd, d_err), "dense top");
+  if (g.nr) {   // restricted level-0 / spike updates
+    HS_TRYF(cudaMalloc((void**)&s->ebr, (size_t)J * M * TM2 * sizeof(double2)), "alloc");
+    HS_TRYF(cudaMalloc((void**)&s->spr, (size_t)J * M * TM2 * sizeof(double2)), "alloc");
+    k_rows<TM><<<dim3(M, J), 256, 0, c->stream>>>(g, s->rows, s->eb, s->sp, s->ebr, s->spr);
+    c->launches++;
+    HS_TRYF(cudaGetLastError(), "rows");
+  }
   // repack into per-(slab, chunk) streams in the solve kernel's item order
   long long nbs = 1;
   for (int k = 0; k < C; ++k) nbs = std::max<long long>(nbs, stream_blocks<TM>(g, k));
   s->nbs = nbs;
   HS_TRYF(cudaMalloc((void**)&s->stream, (size_t)J * C * nbs * TM2 * sizeof(double2)),
           "stream alloc");
-  k_pack<TM><<<J * C, 256, 0, c->stream>>>(g, FactorArrays{s->ef, s->eb, s->kr, s->rk, s->sp, s->qd},
-                                            s->stream, (int)nbs);
+  k_pack<TM><<<J * C, 256, 0, c->stream>>>(
+      g, FactorArrays{s->ef, s->eb, s->kr, s->rk, s->sp, s->qd, s->ebr, s->spr}, s->stream, (int)nbs);
   c->launches++;
   HS_TRYF(cudaGetLastError(), "pack");
   unsigned long long err = 0;
@@ -1494,7 +1574,7 @@ int factorize(Ctx* c, Sweep* s, const std::vector<SlabInfo>& info, const Chunks&
   HS_TRYF(cudaStreamSynchronize(c->stream), "factor sync");
 #undef HS_TRYF
   cleanup();
-  for (double2** p : {&s->ef, &s->eb, &s->kr, &s->sp, &s->rk, &s->qd}) {
+  for (double2** p : {&s->ef, &s->eb, &s->kr, &s->sp, &s->rk, &s->qd, &s->ebr, &s->spr}) {
     cudaFree(*p);
     *p = nullptr;
   }
@@ -1526,6 +1606,7 @@ Chunks make_chunks(const Sweep* s) {
   g.C = s->C;
   g.L = s->L;
   g.q = s->q;
+  g.nr = s->nr;
   int acc = 0;
   for (int l = 0; l < s->L; ++l) {
     g.koff[l] = acc;
@@ -1597,45 +1678,10 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     delete s;
     return set_error(c, HS_E_SHAPE, "face too long for the sweep's chunking");
   }
-  const Chunks g = make_chunks(s);
+  Chunks g = make_chunks(s);
   s->kstride = g.kstride;
   const int B = C - 1;
-
-  const size_t efb = (size_t)J * M * TM2 * sizeof(double2);
-  const size_t krb = (size_t)J * C * g.kstride * 2 * TM2 * sizeof(double2);
-  const size_t rkb = (size_t)J * C * std::max(1, 2 * B) * 2 * TM2 * sizeof(double2);
-  const size_t qdb = (size_t)J * C * s->q * s->q * TM2 * sizeof(double2);
-  s->factor_bytes = (long long)(efb * 5 + krb + qdb + (B > 0 ? rkb : 0));
-  cudaError_t e = cudaMalloc((void**)&s->ef, efb);
-  if (e == cudaSuccess) e = cudaMalloc((void**)&s->eb, 2 * efb);
-  if (e == cudaSuccess) e = cudaMalloc((void**)&s->kr, krb);
-  if (e == cudaSuccess) e = cudaMalloc((void**)&s->sp, 2 * efb);
-  if (e == cudaSuccess) e = cudaMalloc((void**)&s->rk, rkb);
-  if (e == cudaSuccess) e = cudaMalloc((void**)&s->qd, qdb);
-  if (e != cudaSuccess) {
-    sweep_destroy(s);
-    return check_cuda(c, e, "factor alloc");
-  }
-  int r = TM == 16 ? factorize<16>(c, s, info, g) : factorize<32>(c, s, info, g);
-  if (r) {
-    sweep_destroy(s);
-    return r;
-  }
-  {   // the solve kernel's per-rank item / chunk tables
-    const int pw = plan_words(s->mmax);
-    std::vector<uint32_t> hp((size_t)C * pw, 0u);
-    for (int k = 0; k < C; ++k) {
-      if (TM == 16) chunk_plan<16>(g, k, s->mmax, hp.data() + (size_t)k * pw);
-      else chunk_plan<32>(g, k, s->mmax, hp.data() + (size_t)k * pw);
-    }
-    e = cudaMalloc((void**)&s->ptab, hp.size() * sizeof(uint32_t));
-    if (e == cudaSuccess)
-      e = cudaMemcpy(s->ptab, hp.data(), hp.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) {
-      sweep_destroy(s);
-      return check_cuda(c, e, "plan upload");
-    }
-  }
+  cudaError_t e = cudaSuccess;
 
   // ---- schedules (task lists) ----
   int ntin = 0;
@@ -1705,11 +1751,6 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
       if (t.out4 == -2) t.out4 = -1;
     }
   };
-  // factor blocks streamed per slab solve (exactly the items of k_part_solve)
-  double rec_blocks = 0;
-  for (int k = 0; k < C; ++k)
-    rec_blocks += TM == 16 ? stream_blocks<16>(g, k) : stream_blocks<32>(g, k);
-  const double rec_bytes = rec_blocks * TM2 * 16.0;
   // one solve launch per stage (up to two concurrent fronts)
   auto emit_pass = [&](std::vector<SweepLaunch>& plan, int src,
                        std::vector<std::vector<std::vector<SweepTask>>> stages) {
@@ -1724,9 +1765,6 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
         fl.nfront++;
         for (auto t : fr) {
           t.dst = src;
-          double b = rec_bytes + (double)M * 16.0 * ((t.b - t.a) + (t.tb - t.ta));
-          b += (double)M * 32.0 * ((t.tin1 >= 0) + (t.tin3 >= 0) + (t.out2 >= 0) + (t.out4 >= 0));
-          fl.bytes += b;
           T.push_back(t);
         }
       }
@@ -1780,6 +1818,93 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     plan.push_back(SweepLaunch{SweepLaunch::kCombine});
     s->has_plan[HS_VARIANT_X] = true;
   }
+  // ---- rows of each slab's solution the chain ever reads (outputs, traces):
+  // the last back-substitution level and the spike correction only update
+  // those (<= kNR rows; otherwise the slab keeps the full update)
+  {
+    std::vector<std::vector<int>> rows(J);
+    for (const SweepTask& t : T) {
+      auto& rs = rows[t.slab];
+      for (int x = t.ta + 1 - t.lo; x < t.tb + 1 - t.lo; ++x) rs.push_back(x);
+      if (t.out2 >= 0) { rs.push_back(t.orow2); rs.push_back(t.orow2 + 1); }
+      if (t.out4 >= 0) { rs.push_back(t.orow4); rs.push_back(t.orow4 + 1); }
+    }
+    bool fits = TM == 16 && HS_SWEEP_HALF == 0;
+    std::vector<int> rr((size_t)J * kNR, 0);
+    for (int j = 0; j < J && fits; ++j) {
+      auto& rs = rows[j];
+      std::sort(rs.begin(), rs.end());
+      rs.erase(std::unique(rs.begin(), rs.end()), rs.end());
+      if (rs.empty()) rs.push_back(0);
+      if ((int)rs.size() > kNR) fits = false;
+      for (int i = 0; i < kNR; ++i) rr[(size_t)j * kNR + i] = rs[std::min(i, (int)rs.size() - 1)];
+    }
+    s->nr = fits ? kNR : 0;
+    g.nr = s->nr;
+    if (fits) {
+      e = cudaMalloc((void**)&s->rows, rr.size() * sizeof(int));
+      if (e == cudaSuccess)
+        e = cudaMemcpy(s->rows, rr.data(), rr.size() * sizeof(int), cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) {
+        sweep_destroy(s);
+        return check_cuda(c, e, "row sets");
+      }
+    }
+  }
+  {   // algorithmic bytes of every solve launch (profiler): exactly the streamed blocks
+    double rec_blocks = 0;
+    for (int k = 0; k < C; ++k)
+      rec_blocks += TM == 16 ? stream_blocks<16>(g, k) : stream_blocks<32>(g, k);
+    const double rec_bytes = rec_blocks * TM2 * 16.0;
+    for (auto& plan : s->plan)
+      for (auto& fl : plan) {
+        if (fl.kind != SweepLaunch::kSolve) continue;
+        for (int f = 0; f < fl.nfront; ++f)
+          for (int i = fl.ffirst[f]; i < fl.ffirst[f] + fl.fcount[f]; ++i) {
+            const SweepTask& t = T[i];
+            double b = rec_bytes + (double)M * 16.0 * ((t.b - t.a) + (t.tb - t.ta));
+            b += (double)M * 32.0 * ((t.tin1 >= 0) + (t.tin3 >= 0) + (t.out2 >= 0) + (t.out4 >= 0));
+            fl.bytes += b;
+          }
+      }
+  }
+
+  const size_t efb = (size_t)J * M * TM2 * sizeof(double2);
+  const size_t krb = (size_t)J * C * g.kstride * 2 * TM2 * sizeof(double2);
+  const size_t rkb = (size_t)J * C * std::max(1, 2 * B) * 2 * TM2 * sizeof(double2);
+  const size_t qdb = (size_t)J * C * s->q * s->q * TM2 * sizeof(double2);
+  s->factor_bytes = (long long)(efb * 5 + krb + qdb + (B > 0 ? rkb : 0));
+  e = cudaMalloc((void**)&s->ef, efb);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&s->eb, 2 * efb);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&s->kr, krb);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&s->sp, 2 * efb);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&s->rk, rkb);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&s->qd, qdb);
+  if (e != cudaSuccess) {
+    sweep_destroy(s);
+    return check_cuda(c, e, "factor alloc");
+  }
+  int r = TM == 16 ? factorize<16>(c, s, info, g) : factorize<32>(c, s, info, g);
+  if (r) {
+    sweep_destroy(s);
+    return r;
+  }
+  {   // the solve kernel's per-rank item / chunk tables
+    const int pw = plan_words(s->mmax);
+    std::vector<uint32_t> hp((size_t)C * pw, 0u);
+    for (int k = 0; k < C; ++k) {
+      if (TM == 16) chunk_plan<16>(g, k, s->mmax, hp.data() + (size_t)k * pw);
+      else chunk_plan<32>(g, k, s->mmax, hp.data() + (size_t)k * pw);
+    }
+    e = cudaMalloc((void**)&s->ptab, hp.size() * sizeof(uint32_t));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(s->ptab, hp.data(), hp.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      sweep_destroy(s);
+      return check_cuda(c, e, "plan upload");
+    }
+  }
+
   const size_t tb = T.size() * sizeof(SweepTask);
   e = cudaMalloc((void**)&s->d_tasks, tb);
   if (e == cudaSuccess) e = cudaMemcpy(s->d_tasks, T.data(), tb, cudaMemcpyHostToDevice);
@@ -1805,6 +1930,9 @@ void sweep_destroy(Sweep* s) {
   cudaFree(s->qd);
   cudaFree(s->stream);
   cudaFree(s->ptab);
+  cudaFree(s->rows);
+  cudaFree(s->ebr);
+  cudaFree(s->spr);
   cudaFree(s->trace);
   cudaFree(s->g);
   cudaFree(s->u2);
@@ -1845,6 +1973,7 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u) {
         a.stream = s->stream;
         a.nbs = s->nbs;
         a.plan = s->ptab;
+        a.rows = s->rows;
         a.src = Lh.src ? s->g : f;
         a.coarse = s->coarse->d.coeffs;
         a.ncoarse = s->coarse->d.n;

@@ -44,6 +44,10 @@ struct Sweep {
   double2* stream = nullptr;    // [J][C][nbs][tm^2]     all of the above in solve order (setup frees the rest)
   long long nbs = 0;            // blocks per (slab, chunk) stream
   uint32_t* ptab = nullptr;     // [C][plan words] solve-kernel item / chunk tables
+  int nr = 0;                   // rows per restricted update (0: full updates)
+  int* rows = nullptr;          // [J][nr] solution rows the chain reads (outputs, traces)
+  double2* ebr = nullptr;       // [J][M][tm^2] Dinv L, Dinv U restricted to those rows (packing only)
+  double2* spr = nullptr;       // [J][M][tm^2] W, V restricted to those rows (packing only)
   double2* trace = nullptr;     // [ntrace][2][M] interface traces
   double2* g = nullptr;         // [n0*M] mid-sweep residual
   double2* u2 = nullptr;        // [n0*M] second-pass contributions
