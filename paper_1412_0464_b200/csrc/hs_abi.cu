@@ -3,6 +3,7 @@
 // device pointers; all work is ordered on the context stream.
 
 #include "hs_common.cuh"
+#include <vector>
 #include "hs_sweep.cuh"
 #include "hs_transfer.cuh"
 
@@ -248,6 +249,26 @@ int hs_stencil_create(hs_ctx* c, int dim, const int64_t* shape, int S, const int
     return check_cuda(c, e, "stencil upload");
   }
   op->d.coeffs = op->coeffs;
+  op->d.invd = nullptr;
+  if (op->d.diag >= 0 && !op->has_zero_diag) {   // 1/diag for the smoother (products, no divisions)
+    const double* dg = coeffs + (size_t)2 * n * op->d.diag;
+    std::vector<double> inv((size_t)2 * n);
+    for (int64_t i = 0; i < n; ++i) {
+      const double re = dg[2 * i], im = dg[2 * i + 1], d = 1.0 / (re * re + im * im);
+      inv[2 * i] = re * d;
+      inv[2 * i + 1] = -im * d;
+    }
+    e = cudaMalloc((void**)&op->invd, (size_t)n * sizeof(double2));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(op->invd, inv.data(), (size_t)n * sizeof(double2), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaFree(op->coeffs);
+      cudaFree(op->invd);
+      delete op;
+      return check_cuda(c, e, "stencil upload");
+    }
+    op->d.invd = op->invd;
+  }
   *out = op;
   return HS_OK;
 }
@@ -256,6 +277,7 @@ int hs_stencil_destroy(hs_ctx* c, hs_stencil* op) {
   (void)c;
   if (!op) return HS_OK;
   cudaFree(op->coeffs);
+  cudaFree(op->invd);
   delete op;
   return HS_OK;
 }

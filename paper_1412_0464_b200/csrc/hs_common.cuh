@@ -141,6 +141,7 @@ struct StencilDesc {
   int diag;                       // slot of the (0,0,0) offset or -1
   int8_t off[kMaxOffsets][3];     // canonical offsets
   const double2* coeffs;          // [S][n]
+  const double2* invd;            // [n] 1 / diagonal (smoother), or null
 };
 
 struct Stencil {
@@ -148,6 +149,7 @@ struct Stencil {
   int64_t shape[3] = {1, 1, 1};   // user-facing shape
   StencilDesc d{};
   double2* coeffs = nullptr;      // owned device copy
+  double2* invd = nullptr;        // owned 1 / diagonal
   int has_zero_diag = 0;
   long long zero_diag_node = -1;
 };

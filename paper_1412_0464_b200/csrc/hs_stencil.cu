@@ -13,6 +13,8 @@
 
 #include "hs_common.cuh"
 
+#include <algorithm>
+
 namespace hs {
 
 namespace {
@@ -26,71 +28,90 @@ enum Mode : int {
   kJacobi2Z = 3,   // y = two Jacobi steps from x = 0 (x unused)
 };
 
+// Persistent grid-stride form: one wave of resident blocks (no tail), flat
+// 32-bit point index decomposed per point; blockIdx.y = right-hand side.
 template <int S, int MODE>
 __global__ void __launch_bounds__(kThreads)
 k_stencil(StencilDesc d, const double2* __restrict__ x, const double2* __restrict__ f,
           double2* __restrict__ y, double omega) {
-  const int64_t i2 = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  if (i2 >= d.n2) return;
-  const int64_t row = blockIdx.y;            // i0 * n1 + i1
-  const int64_t i1 = row % d.n1;
-  const int64_t i0 = row / d.n1;
-  const int64_t i = row * d.n2 + i2;
-  const int64_t rhs = (int64_t)blockIdx.z * d.n;
+  const uint32_t n = (uint32_t)d.n, n1 = (uint32_t)d.n1, n2 = (uint32_t)d.n2;
+  const int64_t rhs = (int64_t)blockIdx.y * d.n;
   const double2* __restrict__ C = d.coeffs;
-
-  double2 acc = czero();
-  double2 diag = make_double2(1.0, 0.0);
+  int64_t delta[S];
 #pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const int o0 = d.off[s][0], o1 = d.off[s][1], o2 = d.off[s][2];
-    const bool ok = (uint64_t)(i0 + o0) < (uint64_t)d.n0 && (uint64_t)(i1 + o1) < (uint64_t)d.n1 &&
-                    (uint64_t)(i2 + o2) < (uint64_t)d.n2;
-    const double2 c = __ldg(C + (int64_t)s * d.n + i);
-    if (MODE >= kJacobi && s == d.diag) diag = c;
-    if (ok) {
-      const int64_t j = i + ((int64_t)o0 * d.n1 + o1) * d.n2 + o2;
-      double2 xv;
-      if (MODE == kJacobi2Z) {
-        // first pre-smoothing step from zero, evaluated at the neighbour:
-        // u1[j] = w f[j] / diag[j]
-        const double2 dj = __ldg(C + (int64_t)d.diag * d.n + j);
-        xv = cscale(omega, cdiv(__ldg(f + rhs + j), dj));
-      } else {
-        xv = __ldg(x + rhs + j);
+  for (int s = 0; s < S; ++s)
+    delta[s] = ((int64_t)d.off[s][0] * d.n1 + d.off[s][1]) * d.n2 + d.off[s][2];
+  for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < n; i += gridDim.x * kThreads) {
+    const uint32_t row = i / n2, i2 = i - row * n2;
+    const uint32_t i0 = row / n1, i1 = row - i0 * n1;
+    double2 acc = czero();
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int o0 = d.off[s][0], o1 = d.off[s][1], o2 = d.off[s][2];
+      const bool ok = (uint32_t)(i0 + o0) < (uint32_t)d.n0 && (uint32_t)(i1 + o1) < n1 &&
+                      (uint32_t)(i2 + o2) < n2;
+      const double2 c = __ldg(C + (int64_t)s * d.n + i);
+      if (ok) {
+        const int64_t j = (int64_t)i + delta[s];
+        double2 xv;
+        if (MODE == kJacobi2Z) {
+          // first pre-smoothing step from zero, evaluated at the neighbour:
+          // u1[j] = w f[j] / diag[j]
+          xv = cscale(omega, cmul(__ldg(f + rhs + j), __ldg(d.invd + j)));
+        } else {
+          xv = __ldg(x + rhs + j);
+        }
+        acc = cfma(c, xv, acc);
       }
-      acc = cfma(c, xv, acc);
+    }
+    if (MODE == kApply) {
+      y[rhs + i] = acc;
+    } else if (MODE == kResidual) {
+      y[rhs + i] = csub(__ldg(f + rhs + i), acc);
+    } else {
+      const double2 fi = __ldg(f + rhs + i);
+      const double2 inv = __ldg(d.invd + i);
+      double2 ui;
+      if (MODE == kJacobi2Z) ui = cscale(omega, cmul(fi, inv));
+      else ui = __ldg(x + rhs + i);
+      const double2 corr = cmul(cscale(omega, csub(fi, acc)), inv);
+      y[rhs + i] = cadd(ui, corr);
     }
   }
-  if (MODE == kApply) {
-    y[rhs + i] = acc;
-  } else if (MODE == kResidual) {
-    y[rhs + i] = csub(__ldg(f + rhs + i), acc);
-  } else {
-    const double2 fi = __ldg(f + rhs + i);
-    double2 ui;
-    if (MODE == kJacobi2Z) ui = cscale(omega, cdiv(fi, diag));
-    else ui = __ldg(x + rhs + i);
-    const double2 corr = cdiv(cscale(omega, csub(fi, acc)), diag);
-    y[rhs + i] = cadd(ui, corr);
+}
+
+// one wave of resident blocks of this kernel (grid-stride loop, no tail)
+template <int S, int MODE>
+int wave_of() {
+  static int wave = 0;
+  if (!wave) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_stencil<S, MODE>, kThreads, 0);
+    wave = std::max(1, sms * std::max(1, per));
   }
+  return wave;
 }
 
 template <int MODE>
 int launch_mode(Ctx* c, const Stencil* op, const double2* x, const double2* f, double2* y,
                 double omega, int nrhs) {
   const StencilDesc& d = op->d;
-  dim3 grid((unsigned)((d.n2 + kThreads - 1) / kThreads), (unsigned)(d.n0 * d.n1),
-            (unsigned)nrhs);
-  if (d.n0 * d.n1 > 65535) return set_error(c, HS_E_SHAPE, "stencil grid too large");
+  if (d.n >= (int64_t)1 << 31) return set_error(c, HS_E_SHAPE, "stencil grid too large");
+  const int64_t need = (d.n + kThreads - 1) / kThreads;
   const int cls = MODE == kApply ? K_STENCIL
                   : MODE == kResidual ? K_RESIDUAL
                   : MODE == kJacobi ? K_JACOBI : K_JACOBI2Z;
   const double nb = (double)d.n * nrhs * 16.0;
   ProfScope ps(c, cls, nb * (d.S + ((MODE == kApply || MODE == kJacobi2Z) ? 2 : 3)));
   switch (d.S) {
-#define HS_CASE(SS) \
-  case SS: k_stencil<SS, MODE><<<grid, kThreads, 0, c->stream>>>(d, x, f, y, omega); break;
+#define HS_CASE(SS)                                                                    \
+  case SS: {                                                                           \
+    dim3 grid((unsigned)std::min<int64_t>(need, wave_of<SS, MODE>()), (unsigned)nrhs); \
+    k_stencil<SS, MODE><<<grid, kThreads, 0, c->stream>>>(d, x, f, y, omega);          \
+    break;                                                                             \
+  }
     HS_CASE(1) HS_CASE(2) HS_CASE(3) HS_CASE(4) HS_CASE(5) HS_CASE(6) HS_CASE(7) HS_CASE(8)
     HS_CASE(9) HS_CASE(10) HS_CASE(11) HS_CASE(12) HS_CASE(13) HS_CASE(14) HS_CASE(15)
     HS_CASE(16) HS_CASE(17) HS_CASE(18) HS_CASE(19) HS_CASE(20) HS_CASE(21) HS_CASE(22)
