@@ -1201,9 +1201,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
 
   SweepTask prev{}, t = fcount > 0 ? a.tasks[ffirst] : SweepTask{};
   if (fcount > 0) prefetch_rhs(t);
+  SweepTask tn = t;
   for (int ti = 0; ti < fcount; ++ti) {
-    if (ti > 0) t = a.tasks[ffirst + ti];
-    const SweepTask tn = ti + 1 < fcount ? a.tasks[ffirst + ti + 1] : t;   // in flight early
+    if (ti > 0) t = tn;   // loaded during the previous task
+    if (ti + 1 < fcount) tn = a.tasks[ffirst + ti + 1];   // in flight early
     const int par = ti & 1;
     double2* tau = tau2 + par * 2 * kMaxC * TM;
     const double2* halo = halo2 + par * 2 * TM;
