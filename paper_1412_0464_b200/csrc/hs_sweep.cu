@@ -55,6 +55,8 @@ namespace {
 constexpr int kMaxLevels = 16;     // local BCR levels: chunks up to 65536 points
 constexpr int kWarps = 16;        // 15 consumer warps + 1 TMA producer warp
 constexpr int kCW = kWarps - 1;
+constexpr int kNA = 8;             // consumer warps of the back substitution while the rest
+                                   // run the interface GEMV (group B = kCW - kNA warps)
 #ifndef HS_SWEEP_PREFETCH
 #define HS_SWEEP_PREFETCH 0
 #endif
@@ -102,8 +104,15 @@ struct Chunks {
   int q;                   // dense top: blocks per chunk left after L levels
   int nr;                  // restricted level-0 / spike updates (kNR rows) or 0
   int koff[kMaxLevels];
-  __host__ __device__ int y0(int k) const { return (int)((int64_t)k * M / C); }
-  __host__ __device__ int len(int k) const { return y0(k + 1) - y0(k); }
+  int y0s[kMaxC + 1];      // chunk k covers face points [y0s[k], y0s[k+1])
+  int mmax;                // longest chunk
+  __host__ __device__ int y0(int k) const { return y0s[k]; }
+  __host__ __device__ int len(int k) const { return y0s[k + 1] - y0s[k]; }
+  __host__ __device__ int chunk_of(int y) const {
+    int k = 0;
+    while (y >= y0s[k + 1]) ++k;
+    return k;
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -134,7 +143,7 @@ k_bcr_init(const SlabInfo* __restrict__ slabs, Chunks g, double2* __restrict__ D
   if (r >= T || c >= T) d = make_double2(r == c ? 1.0 : 0.0, 0.0);
   D[off] = d;
   double2 l = coef(c - r, -1), u = coef(c - r, 1);
-  const int k = (int)(((int64_t)(y + 1) * g.C - 1) / M);
+  const int k = g.chunk_of(y);
   if (y == g.y0(k)) {
     EL[((int64_t)s * g.C + k) * TM2 + r * TM + c] = l;
     l = czero();
@@ -694,6 +703,7 @@ __device__ __forceinline__ double2 mvs2(const double2* m0, const double2* v0, co
 // then the 2B column blocks of R and the m spike blocks.
 struct ItemPlan {
   int m, L, S, qk, QP, B, NP;
+  int plast;                     // phase after which the right tip g[m-1] is final
   int pfx[2 * kMaxLevels + 4];   // items before each phase (NP + 2 = total)
 };
 
@@ -724,6 +734,44 @@ __host__ __device__ inline void plan_items(const Chunks& g, int rank, ItemPlan& 
   P.pfx[P.NP] = acc;
   P.pfx[P.NP + 1] = acc + (P.B > 0 ? 2 * P.B : 0);
   P.pfx[P.NP + 2] = P.pfx[P.NP + 1] + (P.B > 0 ? P.m : 0);
+  // the dense top, or the back-substitution level of m-1 (its lowest set bit)
+  int tz = 0;
+  while (P.m > 1 && (((P.m - 1) >> tz) & 1) == 0) ++tz;
+  P.plast = (P.m == 1 || (P.m - 1) % P.S == 0) ? P.L : 2 * P.L - tz;
+}
+__host__ __device__ inline int plan_phase(const ItemPlan& P, int r) {
+  int p = 0;
+  while (P.pfx[p + 1] <= r) ++p;
+  return p;
+}
+
+// Stream (= ring) order of one chunk solve's items, as (item, segment); a new
+// segment starts a new copy chunk.  Phases up to the dense top in order; then
+// the back substitution (warp group A) and the interface GEMV (group B) in
+// interleaved runs -- the first A run holds every level the right tip needs,
+// so group B's data never blocks it -- then the spikes.
+constexpr int kRunA = 4, kRunB = 4;
+template <class Fn>
+__host__ __device__ inline void for_stream(const ItemPlan& P, Fn&& fn) {
+  const int L = P.L, NP = P.NP;
+  for (int r = 0; r < P.pfx[L + 1]; ++r) fn(r, plan_phase(P, r));
+  int a = P.pfx[L + 1], b = P.pfx[NP];
+  const int a_end = P.pfx[NP], b_end = P.pfx[NP + 1];
+  const int first = P.pfx[(P.plast > L + 1 ? P.plast : L + 1) + 1];
+  for (; a < first && a < a_end; ++a) fn(a, 64 + plan_phase(P, a));
+  int seg = 128;
+  bool turn_b = true;
+  while (a < a_end || b < b_end) {
+    if (turn_b && b < b_end) {
+      for (int k = 0; k < kRunB && b < b_end; ++k) fn(b++, seg);
+    } else if (a < a_end) {
+      const int ph = plan_phase(P, a);
+      for (int k = 0; k < kRunA && a < a_end && plan_phase(P, a) == ph; ++k) fn(a++, seg);
+    }
+    ++seg;
+    turn_b = !turn_b;
+  }
+  for (int r = P.pfx[NP + 1]; r < P.pfx[NP + 2]; ++r) fn(r, 1 << 20);
 }
 // face point of item j of a cyclic-reduction phase
 __host__ __device__ inline int plan_yl(const ItemPlan& P, int p, int j) {
@@ -828,26 +876,22 @@ __host__ __device__ inline void chunk_plan(const Chunks& g, int rank, int mmax, 
   uint32_t* ib = w + sizeof(ItemPlan) / 4;
   uint32_t* ctab = ib + itab_len(mmax);
   plan_items(g, rank, P);
-  int acc = 0, nc = -1, cfill = G, ph = 0;
-  uint32_t src[2];
-  bool hx;
-  for (int r = 0; r < P.pfx[P.NP + 2]; ++r) {   // stream order (k_pack's)
+  int acc = 0, nc = -1, cfill = G, last_seg = -1;
+  for_stream(P, [&](int r, int seg) {   // stream order (k_pack's)
+    uint32_t src[2];
+    bool hx;
     const int n = item_sources<TM>(g, rank, P, r, src, &hx);
-    bool new_phase = false;
-    while (P.pfx[ph + 1] <= r) {
-      ++ph;
-      new_phase = true;
-    }
-    if (new_phase || cfill + n > G) {
+    if (seg != last_seg || cfill + n > G) {
       ++nc;
       ctab[nc] = (uint32_t)acc << 8;
       cfill = 0;
+      last_seg = seg;
     }
     ib[r] = (uint32_t)nc << 12 | (uint32_t)cfill << 3 | (uint32_t)n << 1 | (hx ? 1u : 0u);
     ctab[nc] += (uint32_t)n;
     cfill += n;
     acc += n;
-  }
+  });
   ctab[itab_len(mmax)] = (uint32_t)(nc + 1);   // nchk
 }
 
@@ -888,12 +932,12 @@ __global__ void __launch_bounds__(256) k_pack(Chunks g, FactorArrays f, double2*
   if (threadIdx.x == 0) {
     plan_items(g, k, P);
     int acc = 0;
-    uint32_t src[2];
-    bool hx;
-    for (int r = 0; r < P.pfx[P.NP + 2]; ++r) {
+    for_stream(P, [&](int r, int) {
+      uint32_t src[2];
+      bool hx;
       boff[r] = acc;
       acc += item_sources<TM>(g, k, P, r, src, &hx);
-    }
+    });
   }
   __syncthreads();
   const double2* base[8] = {
@@ -1002,7 +1046,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   const int front = blockIdx.x / C;
   const int Y0 = g.y0(rank), Y1 = g.y0(rank + 1);
   const int m = Y1 - Y0;
-  const int mmax = (M + C - 1) / C;
+  const int mmax = g.mmax;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int x = lane % TM, hh = lane / TM;
   constexpr int HW = (TM == 16 && HS_SWEEP_HALF) ? 2 : 1;   // items per warp pass
@@ -1191,13 +1235,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   const uint32_t halo_bytes = (rank > 0 ? TM * 16 : 0) + (rank < B ? TM * 16 : 0);
   // tips g[first], g[last] of this chunk go to every CTA's tau:
   // tau block b = (g_b[last], g_{b+1}[first]) -> tm-slots 2b, 2b+1
-  auto push_tip = [&](double2* tau, int par, int slot, const double2* v) {   // lanes < TM
-    const double2 val = v[lane];
-    for (int d = warp - (kCW - 8); d < C; d += 8)
+  auto push_tip = [&](double2* tau, int par, int slot, const double2* v, int w, int nw) {
+    const double2 val = v[lane];   // lanes < TM; warp w of nw pushing warps
+    for (int d = w; d < C; d += nw)
       st_async_c(map_rank(&tau[slot + lane], d), val, map_rank(&xbar[par], d));
   };
-  // phase after which g[m-1] is final: the dense top or its back-substitution level
-  const int p_last = (m - 1) % S == 0 ? L : 2 * L - __ffs(m - 1) + 1;
 
   SweepTask prev{}, t = fcount > 0 ? a.tasks[ffirst] : SweepTask{};
   if (fcount > 0) prefetch_rhs(t);
@@ -1242,76 +1284,92 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     csync();
     stamp(ti, 1);
     // ---- chunk-local solve: L cyclic-reduction levels, the dense top, back substitution
-    for (int p = 0; p < NP; ++p) {
+    // item j of phase p (warp-uniform `has`)
+    auto do_item = [&](int p, int j, bool has) {
       const int l = plan_level(P, p), s = 1 << l;
-      const int cnt = P.pfx[p + 1] - P.pfx[p];
-      for (int jp = warp * HW; jp < cnt; jp += kCW * HW) {
-        const int j = jp + sub;
-        const bool has = j < cnt;
-        const int yl = has && p != L ? plan_yl(P, p, j) : 0;
-        const int r = P.pfx[p] + j;
-        const Item it = has ? acquire(ti, r) : Item{nullptr, nullptr};
-        const double2* m0 = it.m0;
-        const double2* m1 = it.m1;
-        if (has) {
-          if (p == L) {            // partial x_r += Q[r][c0] f_c0 + Q[r][c0+1] f_c0+1
-            const int c0 = 2 * (j % QP);
-            const bool two = c0 + 1 < qk;
-            const double2 acc = mvx<TM, HW>(m0, F + c0 * S * TM, two ? m1 : nullptr,
-                                            two ? F + (c0 + 1) * S * TM : nullptr, lane);
-            if (wr) part[j * TM + x] = acc;
-          } else if (p < L) {
-            if ((yl >> l) & 1) {   // eliminated at this level: y = Dinv f
-              const double2 r = mvx<TM, HW>(m0, F + yl * TM, nullptr, nullptr, lane);
-              if (wr) Yv[yl * TM + x] = r;
-            } else {               // kept: f -= alpha f_{y-s} + gamma f_{y+s}
-              const bool hl = yl - s >= 0, hr = yl + s < m;
-              const double2 acc = mvx<TM, HW>(hl ? m0 : nullptr, hl ? F + (yl - s) * TM : nullptr,
-                                          hr ? m1 : nullptr, hr ? F + (yl + s) * TM : nullptr,
-                                          lane);
-              if (wr) F[yl * TM + x] = csub(F[yl * TM + x], acc);
-            }
-          } else if (g.nr && l == 0 && yl != m - 1) {   // level 0: only the rows read later
-            const double2 acc = mvr<TM>(m0, Yv + (yl - 1) * TM, Yv + (yl + 1) * TM, lane);
-            if (lane < kNR) Yv[yl * TM + rr[lane]] = csub(Yv[yl * TM + rr[lane]], acc);
-          } else {                 // x_y = Dinv f - (Dinv L) x_{y-s} - (Dinv U) x_{y+s}
+      const int yl = has && p != L ? plan_yl(P, p, j) : 0;
+      const int r = P.pfx[p] + j;
+      const Item it = has ? acquire(ti, r) : Item{nullptr, nullptr};
+      const double2* m0 = it.m0;
+      const double2* m1 = it.m1;
+      if (has) {
+        if (p == L) {            // partial x_r += Q[r][c0] f_c0 + Q[r][c0+1] f_c0+1
+          const int c0 = 2 * (j % QP);
+          const bool two = c0 + 1 < qk;
+          const double2 acc = mvx<TM, HW>(m0, F + c0 * S * TM, two ? m1 : nullptr,
+                                          two ? F + (c0 + 1) * S * TM : nullptr, lane);
+          if (wr) part[j * TM + x] = acc;
+        } else if (p < L) {
+          if ((yl >> l) & 1) {   // eliminated at this level: y = Dinv f
+            const double2 r = mvx<TM, HW>(m0, F + yl * TM, nullptr, nullptr, lane);
+            if (wr) Yv[yl * TM + x] = r;
+          } else {               // kept: f -= alpha f_{y-s} + gamma f_{y+s}
             const bool hl = yl - s >= 0, hr = yl + s < m;
-            const double2 acc = mvx<TM, HW>(hl ? m0 : nullptr, hl ? Yv + (yl - s) * TM : nullptr,
-                                        hr ? m1 : nullptr, hr ? Yv + (yl + s) * TM : nullptr,
+            const double2 acc = mvx<TM, HW>(hl ? m0 : nullptr, hl ? F + (yl - s) * TM : nullptr,
+                                        hr ? m1 : nullptr, hr ? F + (yl + s) * TM : nullptr,
                                         lane);
-            if (wr) Yv[yl * TM + x] = csub(Yv[yl * TM + x], acc);
+            if (wr) F[yl * TM + x] = csub(F[yl * TM + x], acc);
           }
+        } else if (g.nr && l == 0 && yl != m - 1) {   // level 0: only the rows read later
+          const double2 acc = mvr<TM>(m0, Yv + (yl - 1) * TM, Yv + (yl + 1) * TM, lane);
+          if (lane < kNR) Yv[yl * TM + rr[lane]] = csub(Yv[yl * TM + rr[lane]], acc);
+        } else {                 // x_y = Dinv f - (Dinv L) x_{y-s} - (Dinv U) x_{y+s}
+          const bool hl = yl - s >= 0, hr = yl + s < m;
+          const double2 acc = mvx<TM, HW>(hl ? m0 : nullptr, hl ? Yv + (yl - s) * TM : nullptr,
+                                      hr ? m1 : nullptr, hr ? Yv + (yl + s) * TM : nullptr,
+                                      lane);
+          if (wr) Yv[yl * TM + x] = csub(Yv[yl * TM + x], acc);
         }
-        release(ti, r, has);
       }
+      release(ti, r, has);
+    };
+    // phase p over warps [w0, w0 + nw)
+    auto run_phase = [&](int p, int w0, int nw) {
+      const int cnt = P.pfx[p + 1] - P.pfx[p];
+      for (int jp = (warp - w0) * HW; jp < cnt; jp += nw * HW) do_item(p, jp + sub, jp + sub < cnt);
+    };
+    for (int p = 0; p <= L; ++p) {   // forward levels and the dense top: all warps
+      run_phase(p, 0, kCW);
       csync();
-      if (p == L) {   // x at the level-L points = sum of the column-pair partials
-        for (int t = threadIdx.x; t < qk * TM; t += kCW * 32) {
-          const int r = t / TM, xx = t % TM;
-          double2 acc = czero();
-          for (int cp = 0; cp < QP; ++cp) acc = cadd(acc, part[(r * QP + cp) * TM + xx]);
-          Yv[r * S * TM + xx] = acc;
-        }
-        csync();
-        if (ti + 1 < fcount) prefetch_rhs(tn);   // F is free from here on
-      }
-      // a tip is final once its level is done: send it right away
-      if (B > 0 && lane < TM && warp >= kCW - 8) {   // high warps: idle in small phases
-        if (p == L && rank > 0) push_tip(tau, par, (2 * (rank - 1) + 1) * TM, Yv);
-        if (p == p_last && rank < B) push_tip(tau, par, 2 * rank * TM, Yv + (m - 1) * TM);
-      }
       stamp(ti, 2 + p);
     }
-    if (B > 0) {
-      // ---- every chunk's tips (pushed as soon as final) are in tau
+    {   // x at the level-L points = sum of the column-pair partials
+      for (int t = threadIdx.x; t < qk * TM; t += kCW * 32) {
+        const int r = t / TM, xx = t % TM;
+        double2 acc = czero();
+        for (int cp = 0; cp < QP; ++cp) acc = cadd(acc, part[(r * QP + cp) * TM + xx]);
+        Yv[r * S * TM + xx] = acc;
+      }
+      csync();
+      if (ti + 1 < fcount) prefetch_rhs(tn);   // F is free from here on
+    }
+    // tips are pushed to every CTA as soon as final
+    if (B > 0 && lane < TM && warp >= kCW - 8) {
+      if (rank > 0) push_tip(tau, par, (2 * (rank - 1) + 1) * TM, Yv, warp - (kCW - 8), 8);
+      if (P.plast == L && rank < B) push_tip(tau, par, 2 * rank * TM, Yv + (m - 1) * TM, warp - (kCW - 8), 8);
+    }
+    if (B == 0) {
+      for (int p = L + 1; p < NP; ++p) {
+        run_phase(p, 0, kCW);
+        csync();
+      }
+    } else if (warp < kNA) {
+      // ---- group A: back substitution (its own named barrier)
+      for (int p = L + 1; p < NP; ++p) {
+        run_phase(p, 0, kNA);
+        asm volatile("bar.sync 2, %0;" ::"r"(kNA * 32) : "memory");
+        if (p == P.plast && rank < B && lane < TM)
+          push_tip(tau, par, 2 * rank * TM, Yv + (m - 1) * TM, warp, kNA);
+      }
+    } else {
+      // ---- group B: alpha_{k-1}, beta_k = (rows of R) tau once every tip is in
       mbar_wait(&xbar[par], (uint32_t)(ti >> 1) & 1);
       stamp(ti, 40);
-      // ---- alpha_{k-1}, beta_k = (rows of R) tau: 2B column blocks over warps
       // rows r0 = lane (tm 32) or x (tm 16, per half) and r0 + 32 / r0 + 16
       double2 acc0 = czero(), acc1 = czero();
       const int nq = 2 * B;
       const int r0 = HW == 1 ? lane : x, r1 = r0 + (HW == 1 ? 32 : 16);   // r1 unused: tm 16, HW 1
-      for (int jp = warp * HW; jp < nq; jp += kCW * HW) {
+      for (int jp = (warp - kNA) * HW; jp < nq; jp += (kCW - kNA) * HW) {
         const int j = jp + sub;
         const bool has = j < nq;
         const int r = P.pfx[NP] + j;
@@ -1341,14 +1399,17 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
         part[warp * N2 + r0] = acc0;
         if (HW == 2 || TM == 32) part[warp * N2 + r1] = acc1;
       }
-      csync();
-      if (threadIdx.x < N2) {
+      asm volatile("bar.sync 3, %0;" ::"r"((kCW - kNA) * 32) : "memory");
+      if (threadIdx.x - kNA * 32 < (unsigned)N2) {
+        const int t = threadIdx.x - kNA * 32;
         double2 sacc = czero();
-        for (int w = 0; w < kCW; ++w) sacc = cadd(sacc, part[w * N2 + threadIdx.x]);
-        ab[threadIdx.x] = sacc;
+        for (int w = kNA; w < kCW; ++w) sacc = cadd(sacc, part[w * N2 + t]);
+        ab[t] = sacc;
       }
-      csync();
       stamp(ti, 41);
+    }
+    if (B > 0) {
+      csync();   // back substitution and alpha, beta both done
       // ---- x_y = g_y - W_y alpha_{k-1} - V_y beta_k
       for (int jp = warp * HW; jp < m; jp += kCW * HW) {
         const int j = jp + sub;
@@ -1608,6 +1669,8 @@ Chunks make_chunks(const Sweep* s) {
   g.L = s->L;
   g.q = s->q;
   g.nr = s->nr;
+  for (int k = 0; k <= s->C; ++k) g.y0s[k] = s->y0s[k];
+  g.mmax = s->mmax;
   int acc = 0;
   for (int l = 0; l < s->L; ++l) {
     g.koff[l] = acc;
@@ -1674,6 +1737,42 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   const int qmax = TM == 16 ? 5 : 2;
   s->L = 0;
   while ((s->mmax - 1) / (1 << s->L) + 1 > qmax) ++s->L;
+  {
+    // Chunk sizes m = 1 (mod S/2) for every chunk but the last, so each right
+    // tip is final after the dense top or the first back-substitution level
+    // and the interface solve overlaps the rest of the back substitution.
+    const int S = 1 << s->L, h = std::max(1, S / 2), cap = S * qmax;
+    std::vector<int> mk(C, 0);
+    const double mean = (double)M / C;
+    const int base = std::max(1, 1 + h * (int)std::lround((mean - 1.0) / h));
+    int rem = M;
+    for (int k = 0; k + 1 < C; ++k) { mk[k] = base; rem -= base; }
+    for (int k = 0; k + 1 < C && rem > mean + h / 2.0; k = (k + 1) % (C - 1)) {
+      if (mk[k] + h > cap) break;
+      mk[k] += h; rem -= h;
+    }
+    for (int k = 0; k + 1 < C && rem < std::max(1.0, mean - h); k = (k + 1) % (C - 1)) {
+      if (mk[k] - h < 1) break;
+      mk[k] -= h; rem += h;
+    }
+    mk[C - 1] = rem;
+    bool ok = true;
+    for (int k = 0; k < C; ++k) ok = ok && mk[k] >= 1 && mk[k] <= cap;
+    s->y0s[0] = 0;
+    for (int k = 0; k < C; ++k)
+      s->y0s[k + 1] = ok ? s->y0s[k] + mk[k] : (int)((int64_t)(k + 1) * M / C);
+    s->mmax = 0;
+    for (int k = 0; k < C; ++k) s->mmax = std::max(s->mmax, s->y0s[k + 1] - s->y0s[k]);
+    while ((s->mmax - 1) / (1 << s->L) + 1 > qmax) ++s->L;   // (uniform fallback only)
+    int maxc = 0;   // the kernel's shared memory follows the final chunk length
+    cudaError_t e0 = TM == 16 ? prepare_solve<16>(C, s->mmax, &maxc)
+                              : prepare_solve<32>(C, s->mmax, &maxc);
+    if (e0 != cudaSuccess || maxc < 2) {
+      cudaGetLastError();
+      delete s;
+      return set_error(c, HS_E_CUDA, "no schedulable cluster for the sweep kernel");
+    }
+  }
   s->q = (s->mmax - 1) / (1 << s->L) + 1;
   if (s->L >= kMaxLevels || itab_len(s->mmax) > kMaxItems) {
     delete s;

@@ -33,6 +33,7 @@ struct Sweep {
   int L = 0;                    // local cyclic-reduction levels before the dense top
   int q = 1;                    // blocks left per chunk after L levels (dense inverse)
   int mmax = 0;                 // largest chunk (face points)
+  int y0s[17] = {};             // chunk boundaries (C + 1 entries)
   int kstride = 0;              // kept-block records per chunk
   const Stencil* coarse = nullptr;
   double2* ef = nullptr;        // [J][M][tm^2]          Dinv at each block's elimination level
