@@ -1685,104 +1685,11 @@ Chunks make_chunks(const Sweep* s) {
 // ---------------------------------------------------------------------------
 // host side
 
-int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, const int64_t* bt,
-                 const int64_t* lo, const int64_t* hi, const Stencil* const* slabs,
-                 Sweep** out) {
-  if (coarse->dim != 2)
-    return set_error(c, HS_E_SHAPE, "the device sweep supports 2-D levels (3-D: not yet)");
-  if (J < 2) return set_error(c, HS_E_SHAPE, "the sweep needs at least 2 subdomains");
-  if (J > kMaxTasks) return set_error(c, HS_E_SHAPE, "too many subdomains for the sweep");
-  Sweep* s = new Sweep();
-  s->J = J;
-  s->n0 = (int)coarse->shape[0];
-  s->M = (int)coarse->shape[1];
-  s->coarse = coarse;
-  const int M = s->M;
-  std::vector<SlabInfo> info(J);
-  for (int j = 0; j < J; ++j) {
-    const Stencil* op = slabs[j];
-    const int T = (int)(hi[j] - lo[j] + 1);
-    if (T > 32) {
-      delete s;
-      return set_error(c, HS_E_SHAPE, "slab thicker than 32 layers: not supported by the sweep");
-    }
-    if (T > 16) s->tm = 32;
-    if (op->dim != 2 || op->shape[0] != T || op->shape[1] != M) {
-      delete s;
-      return set_error(c, HS_E_SHAPE, "slab operator shape does not match the partition");
-    }
-    info[j].coeffs = op->d.coeffs;
-    info[j].T = T;
-    if (int r = slot_table(op, info[j].slot, c)) { delete s; return r; }
-  }
-  const int TM = s->tm, TM2 = TM * TM;
-  // chunks: ~32 face points per CTA, at most 16 CTAs, cluster schedulable twice
-  int C = std::min(kMaxC, std::max(1, (M + 31) / 32));
-  for (;;) {
-    const int mmax = (M + C - 1) / C;
-    int maxc = 0;
-    cudaError_t e = TM == 16 ? prepare_solve<16>(C, mmax, &maxc) : prepare_solve<32>(C, mmax, &maxc);
-    if (e == cudaSuccess && maxc >= 2) break;
-    cudaGetLastError();
-    if (C == 1) {
-      delete s;
-      return set_error(c, HS_E_CUDA, "no schedulable cluster for the sweep kernel");
-    }
-    C = C > 8 ? 8 : C / 2;
-  }
-  s->C = C;
-  s->mmax = (M + C - 1) / C;
-  // cyclic reduction until at most qmax blocks per chunk are left, then a
-  // dense inverse of that reduced system (qmax blocks fit the setup's smem)
-  const int qmax = TM == 16 ? 5 : 2;
-  s->L = 0;
-  while ((s->mmax - 1) / (1 << s->L) + 1 > qmax) ++s->L;
-  {
-    // Chunk sizes m = 1 (mod S/2) for every chunk but the last, so each right
-    // tip is final after the dense top or the first back-substitution level
-    // and the interface solve overlaps the rest of the back substitution.
-    const int S = 1 << s->L, h = std::max(1, S / 2), cap = S * qmax;
-    std::vector<int> mk(C, 0);
-    const double mean = (double)M / C;
-    const int base = std::max(1, 1 + h * (int)std::lround((mean - 1.0) / h));
-    int rem = M;
-    for (int k = 0; k + 1 < C; ++k) { mk[k] = base; rem -= base; }
-    for (int k = 0; k + 1 < C && rem > mean + h / 2.0; k = (k + 1) % (C - 1)) {
-      if (mk[k] + h > cap) break;
-      mk[k] += h; rem -= h;
-    }
-    for (int k = 0; k + 1 < C && rem < std::max(1.0, mean - h); k = (k + 1) % (C - 1)) {
-      if (mk[k] - h < 1) break;
-      mk[k] -= h; rem += h;
-    }
-    mk[C - 1] = rem;
-    bool ok = true;
-    for (int k = 0; k < C; ++k) ok = ok && mk[k] >= 1 && mk[k] <= cap;
-    s->y0s[0] = 0;
-    for (int k = 0; k < C; ++k)
-      s->y0s[k + 1] = ok ? s->y0s[k] + mk[k] : (int)((int64_t)(k + 1) * M / C);
-    s->mmax = 0;
-    for (int k = 0; k < C; ++k) s->mmax = std::max(s->mmax, s->y0s[k + 1] - s->y0s[k]);
-    while ((s->mmax - 1) / (1 << s->L) + 1 > qmax) ++s->L;   // (uniform fallback only)
-    int maxc = 0;   // the kernel's shared memory follows the final chunk length
-    cudaError_t e0 = TM == 16 ? prepare_solve<16>(C, s->mmax, &maxc)
-                              : prepare_solve<32>(C, s->mmax, &maxc);
-    if (e0 != cudaSuccess || maxc < 2) {
-      cudaGetLastError();
-      delete s;
-      return set_error(c, HS_E_CUDA, "no schedulable cluster for the sweep kernel");
-    }
-  }
-  s->q = (s->mmax - 1) / (1 << s->L) + 1;
-  if (s->L >= kMaxLevels || itab_len(s->mmax) > kMaxItems) {
-    delete s;
-    return set_error(c, HS_E_SHAPE, "face too long for the sweep's chunking");
-  }
-  Chunks g = make_chunks(s);
-  s->kstride = g.kstride;
-  const int B = C - 1;
-  cudaError_t e = cudaSuccess;
-
+// Task lists and launch plans of the UD and X schedules (prec_ud / prec_x,
+// sweepdd.py:312-359), shared by the 2-D and 3-D sweeps.  Returns the number
+// of trace buffers.
+static int build_schedule(Sweep* s, int J, const int64_t* beta, const int64_t* bt,
+                          const int64_t* lo, const int64_t* hi) {
   // ---- schedules (task lists) ----
   int ntin = 0;
   auto mk = [&](int j, int a_, int b_) {
@@ -1918,6 +1825,142 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     plan.push_back(SweepLaunch{SweepLaunch::kCombine});
     s->has_plan[HS_VARIANT_X] = true;
   }
+  return ntin;
+}
+
+int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, const int64_t* bt,
+                 const int64_t* lo, const int64_t* hi, const Stencil* const* slabs,
+                 Sweep** out) {
+  if (coarse->dim != 2 && coarse->dim != 3)
+    return set_error(c, HS_E_SHAPE, "the device sweep needs a 2-D or 3-D level");
+  if (J < 2) return set_error(c, HS_E_SHAPE, "the sweep needs at least 2 subdomains");
+  if (J > kMaxTasks) return set_error(c, HS_E_SHAPE, "too many subdomains for the sweep");
+  auto buffers = [&](Sweep* s, int ntin) -> int {   // traces, mid-sweep residual, pass-2 u
+    cudaError_t e = cudaMalloc((void**)&s->trace, (size_t)std::max(1, ntin) * 2 * s->M * sizeof(double2));
+    if (e == cudaSuccess) e = cudaMalloc((void**)&s->g, (size_t)s->n0 * s->M * sizeof(double2));
+    if (e == cudaSuccess) e = cudaMalloc((void**)&s->u2, (size_t)s->n0 * s->M * sizeof(double2));
+    return e == cudaSuccess ? HS_OK : check_cuda(c, e, "sweep buffers");
+  };
+  if (coarse->dim == 3) {   // block-LU slabs along face axis 1 (hs_sweep3.cu)
+    Sweep* s = new Sweep();
+    s->J = J;
+    s->n0 = (int)coarse->shape[0];
+    s->M = (int)(coarse->shape[1] * coarse->shape[2]);
+    s->coarse = coarse;
+    const int ntin = build_schedule(s, J, beta, bt, lo, hi);
+    int r = sweep3_create(c, s, coarse, slabs, lo, hi);
+    if (!r) r = buffers(s, ntin);
+    if (!r)   // algorithmic bytes per launch: both factor blocks of every plane + rhs/u/traces
+      for (auto& plan : s->plan)
+        for (auto& fl : plan)
+          for (int f = 0; f < fl.nfront; ++f)
+            for (int i = fl.ffirst[f]; i < fl.ffirst[f] + fl.fcount[f]; ++i) {
+              const SweepTask& t = s->tasks[i];
+              const double NB = (double)t.T * coarse->shape[2];
+              fl.bytes += (2.0 * coarse->shape[1] - 1.0) * NB * NB * 16.0 +
+                          (double)s->M * 16.0 * ((t.b - t.a) + (t.tb - t.ta));
+            }
+    if (r) {
+      sweep_destroy(s);
+      return r;
+    }
+    *out = s;
+    return HS_OK;
+  }
+  Sweep* s = new Sweep();
+  s->J = J;
+  s->n0 = (int)coarse->shape[0];
+  s->M = (int)coarse->shape[1];
+  s->coarse = coarse;
+  const int M = s->M;
+  std::vector<SlabInfo> info(J);
+  for (int j = 0; j < J; ++j) {
+    const Stencil* op = slabs[j];
+    const int T = (int)(hi[j] - lo[j] + 1);
+    if (T > 32) {
+      delete s;
+      return set_error(c, HS_E_SHAPE, "slab thicker than 32 layers: not supported by the sweep");
+    }
+    if (T > 16) s->tm = 32;
+    if (op->dim != 2 || op->shape[0] != T || op->shape[1] != M) {
+      delete s;
+      return set_error(c, HS_E_SHAPE, "slab operator shape does not match the partition");
+    }
+    info[j].coeffs = op->d.coeffs;
+    info[j].T = T;
+    if (int r = slot_table(op, info[j].slot, c)) { delete s; return r; }
+  }
+  const int TM = s->tm, TM2 = TM * TM;
+  // chunks: ~32 face points per CTA, at most 16 CTAs, cluster schedulable twice
+  int C = std::min(kMaxC, std::max(1, (M + 31) / 32));
+  for (;;) {
+    const int mmax = (M + C - 1) / C;
+    int maxc = 0;
+    cudaError_t e = TM == 16 ? prepare_solve<16>(C, mmax, &maxc) : prepare_solve<32>(C, mmax, &maxc);
+    if (e == cudaSuccess && maxc >= 2) break;
+    cudaGetLastError();
+    if (C == 1) {
+      delete s;
+      return set_error(c, HS_E_CUDA, "no schedulable cluster for the sweep kernel");
+    }
+    C = C > 8 ? 8 : C / 2;
+  }
+  s->C = C;
+  s->mmax = (M + C - 1) / C;
+  // cyclic reduction until at most qmax blocks per chunk are left, then a
+  // dense inverse of that reduced system (qmax blocks fit the setup's smem)
+  const int qmax = TM == 16 ? 5 : 2;
+  s->L = 0;
+  while ((s->mmax - 1) / (1 << s->L) + 1 > qmax) ++s->L;
+  {
+    // Chunk sizes m = 1 (mod S/2) for every chunk but the last, so each right
+    // tip is final after the dense top or the first back-substitution level
+    // and the interface solve overlaps the rest of the back substitution.
+    const int S = 1 << s->L, h = std::max(1, S / 2), cap = S * qmax;
+    std::vector<int> mk(C, 0);
+    const double mean = (double)M / C;
+    const int base = std::max(1, 1 + h * (int)std::lround((mean - 1.0) / h));
+    int rem = M;
+    for (int k = 0; k + 1 < C; ++k) { mk[k] = base; rem -= base; }
+    for (int k = 0; k + 1 < C && rem > mean + h / 2.0; k = (k + 1) % (C - 1)) {
+      if (mk[k] + h > cap) break;
+      mk[k] += h; rem -= h;
+    }
+    for (int k = 0; k + 1 < C && rem < std::max(1.0, mean - h); k = (k + 1) % (C - 1)) {
+      if (mk[k] - h < 1) break;
+      mk[k] -= h; rem += h;
+    }
+    mk[C - 1] = rem;
+    bool ok = true;
+    for (int k = 0; k < C; ++k) ok = ok && mk[k] >= 1 && mk[k] <= cap;
+    s->y0s[0] = 0;
+    for (int k = 0; k < C; ++k)
+      s->y0s[k + 1] = ok ? s->y0s[k] + mk[k] : (int)((int64_t)(k + 1) * M / C);
+    s->mmax = 0;
+    for (int k = 0; k < C; ++k) s->mmax = std::max(s->mmax, s->y0s[k + 1] - s->y0s[k]);
+    while ((s->mmax - 1) / (1 << s->L) + 1 > qmax) ++s->L;   // (uniform fallback only)
+    int maxc = 0;   // the kernel's shared memory follows the final chunk length
+    cudaError_t e0 = TM == 16 ? prepare_solve<16>(C, s->mmax, &maxc)
+                              : prepare_solve<32>(C, s->mmax, &maxc);
+    if (e0 != cudaSuccess || maxc < 2) {
+      cudaGetLastError();
+      delete s;
+      return set_error(c, HS_E_CUDA, "no schedulable cluster for the sweep kernel");
+    }
+  }
+  s->q = (s->mmax - 1) / (1 << s->L) + 1;
+  if (s->L >= kMaxLevels || itab_len(s->mmax) > kMaxItems) {
+    delete s;
+    return set_error(c, HS_E_SHAPE, "face too long for the sweep's chunking");
+  }
+  Chunks g = make_chunks(s);
+  s->kstride = g.kstride;
+  const int B = C - 1;
+  cudaError_t e = cudaSuccess;
+
+  const int ntin = build_schedule(s, J, beta, bt, lo, hi);
+  std::vector<SweepTask>& T = s->tasks;
+
   // ---- rows of each slab's solution the chain ever reads (outputs, traces):
   // the last back-substitution level and the spike correction only update
   // those (<= kNR rows; otherwise the slab keeps the full update)
@@ -2021,6 +2064,7 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
 }
 
 void sweep_destroy(Sweep* s) {
+  if (s) sweep3_destroy(s->s3);
   if (!s) return;
   cudaFree(s->ef);
   cudaFree(s->eb);
@@ -2062,6 +2106,16 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u) {
         break;
       }
       case SweepLaunch::kSolve: {
+        if (s->s3) {   // 3-D: the fronts' slab solves in order (host-driven block LU)
+          ProfScope ps(c, K_SWEEP_FRONT, Lh.bytes);
+          double2* us[2] = {u, s->u2};
+          for (int fr = 0; fr < Lh.nfront; ++fr)
+            for (int i = Lh.ffirst[fr]; i < Lh.ffirst[fr] + Lh.fcount[fr]; ++i)
+              if (int r = sweep3_task(c, s, s->tasks[i], Lh.src ? s->g : f, us,
+                                      s->coarse->d.coeffs, s->coarse->d.n))
+                return r;
+          break;
+        }
         SolveArgs a{};
         a.tasks = s->d_tasks;
         for (int i = 0; i < 2; ++i) {

@@ -25,6 +25,8 @@ struct SweepLaunch {
   double bytes;             // algorithmic HBM bytes of the launch (profiler)
 };
 
+struct Sweep3;   // 3-D levels (hs_sweep3.cu)
+
 // Partitioned slab factors of every slab (see hs_sweep.cu).
 struct Sweep {
   int J = 0, M = 0, n0 = 0;
@@ -57,11 +59,18 @@ struct Sweep {
   std::vector<SweepLaunch> plan[2];   // by variant (UD, X)
   bool has_plan[2] = {false, false};
   long long factor_bytes = 0;
+  Sweep3* s3 = nullptr;         // 3-D level: block LU slabs, host-driven tasks
 };
 
 int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, const int64_t* bt,
                  const int64_t* lo, const int64_t* hi, const Stencil* const* slabs, Sweep** out);
 void sweep_destroy(Sweep* s);
 int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u);
+
+int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const* slabs,
+                  const int64_t* lo, const int64_t* hi);
+int sweep3_task(Ctx* c, Sweep* s, const SweepTask& t, const double2* src, double2* const* u,
+                const double2* coarse_coeffs, int64_t coarse_n);
+void sweep3_destroy(Sweep3* s3);
 
 }  // namespace hs

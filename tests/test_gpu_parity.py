@@ -18,8 +18,6 @@ pytestmark = pytest.mark.gpu
 def _build(name):
     import paper_1412_0464_b200 as hb
     mesh, model, fine_op, sm, sw = case(name)
-    if mesh.dim == 3:
-        return None
     cycle, clevel = hb.build_two_grid(mesh, model, fine_op=fine_op, smoother=sm,
                                       coarse="sweep", sweep=sw)
     return cycle
@@ -76,8 +74,6 @@ def test_transfers(golden):
 
 def test_sweeps(golden):
     name, d = golden
-    if len(d["fine_shape"]) == 3:
-        pytest.skip("3-D sweep: not on the device yet (DESIGN.md)")
     import paper_1412_0464_b200 as hb
     hh = hierarchy(name, device=True)
     part = hh.partition
@@ -89,8 +85,6 @@ def test_sweeps(golden):
 def test_tgsp_apply(golden):
     name, d = golden
     cycle = _build(name)
-    if cycle is None:
-        pytest.skip("3-D sweep: not on the device yet")
     import paper_1412_0464_b200 as hb
     out = hb.tgsp_apply(cycle, d["tgsp_z"])
     assert rel(out, d["tgsp_out"]) < 1e-10
