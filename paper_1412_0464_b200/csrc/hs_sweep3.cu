@@ -24,18 +24,24 @@
 #include <array>
 #include <vector>
 
+#ifndef HS_S3_EXP   // timing experiments: 1 no GEMV, 2 no rhs stencil, 4 no grid barrier
+#define HS_S3_EXP 0
+#endif
+
 namespace hs {
 
 struct Sweep3 {
   int n1 = 0, n2 = 0;
   std::vector<int> T;                  // slab thickness
-  std::vector<double2*> dinv, xf;      // per slab: [n1][NB^2], [n1-1][NB^2] (column-major)
+  std::vector<double2*> dinv, xf;      // per slab: [n1][NB^2], [n1-1][NB^2] (row-major)
   std::vector<double2*> coef;          // per slab: stencil coefficients [S][T n1 n2] (owned copy)
   std::vector<std::array<int, 27>> slot;   // per slab: (o0+1)*9 + (o1+1)*3 + (o2+1) -> slot
   std::array<int, 27> cslot{};         // coarse operator slots
   cublasHandle_t blas = nullptr;
-  double2* F = nullptr;                // [n1][NBmax] right-hand side / forward solution
-  double2* W = nullptr;                // [NBmax] work
+  double2* F = nullptr;                // [n1][NBmax] right-hand side
+  double2* Y = nullptr;                // [n1][NBmax] forward solution, then x
+  unsigned* gbar = nullptr;            // grid barrier counter of the solve kernel
+  int grid = 0;                        // CTAs of the solve kernel (one per SM)
   long long bytes = 0;
 };
 
@@ -105,27 +111,6 @@ __global__ void k3_rhs(SweepTask t, int n0, int n1, int n2, const double2* __res
   F[(int64_t)i1 * NB + r] = v;
 }
 
-// W = F_i1 - L_i1 y_{i1-1}   (L from the stencil's o1 = -1 offsets)
-__global__ void k3_lsub(const double2* __restrict__ coef, Slots sl, int T, int n1, int n2, int i1,
-                        const double2* __restrict__ Fi, const double2* __restrict__ yprev,
-                        double2* __restrict__ W) {
-  const int NB = T * n2;
-  const int r = blockIdx.x * kT3 + threadIdx.x;
-  if (r >= NB) return;
-  const int t = r / n2, i2 = r - t * n2;
-  const int64_t n = (int64_t)T * n1 * n2;
-  double2 acc = Fi[r];
-  if (i1 > 0)
-    for (int o0 = -1; o0 <= 1; ++o0)
-      for (int o2 = -1; o2 <= 1; ++o2) {
-        const int s = sl.s[oid(o0, -1, o2)];
-        if (s < 0 || t + o0 < 0 || t + o0 >= T || i2 + o2 < 0 || i2 + o2 >= n2) continue;
-        const double2 c = coef[(int64_t)s * n + ((int64_t)t * n1 + i1) * n2 + i2];
-        acc = csub(acc, cmul(c, yprev[(t + o0) * n2 + (i2 + o2)]));
-      }
-  W[r] = acc;
-}
-
 // u rows [ta, tb) and the outgoing traces (subdom_solve steps 4-5)
 __global__ void k3_out(SweepTask t, int n1, int n2, const double2* __restrict__ X,
                        double2* __restrict__ u, double2* __restrict__ trace) {
@@ -141,6 +126,129 @@ __global__ void k3_out(SweepTask t, int n1, int n2, const double2* __restrict__ 
     trace[((int64_t)t.out2 * 2 + (x - t.orow2)) * M + f] = v;
   if (t.out4 >= 0 && (x == t.orow4 || x == t.orow4 + 1))
     trace[((int64_t)t.out4 * 2 + (x - t.orow4)) * M + f] = v;
+}
+
+// ---- the whole block recursion of one slab solve in one cooperative launch:
+// every CTA rebuilds the step's right-hand vector in shared memory, owns rows
+// (one warp per row, coalesced row-major blocks), and a grid barrier orders
+// the planes.  F: the rhs (read by every CTA while Y fills), Y: y, then x.
+constexpr int kW3 = 16;   // warps per CTA
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (HS_S3_EXP & 4) return;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar));
+    } while ((int)(v - target) < 0);
+  }
+  __syncthreads();
+}
+
+// This CTA's rows r = blockIdx.x + k * gridDim.x of A v (A row-major NB x NB,
+// v in shared memory): a row is split over wpr warps (4 loads in flight per
+// lane); partial sums land in acc[k][part] (summed in a fixed order by the
+// caller: bitwise reproducible).
+__device__ __forceinline__ int rows_wpr(int NB) {
+  const int rows = blockIdx.x < NB ? (NB - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  return max(1, kW3 / max(1, rows));
+}
+__device__ __forceinline__ void cta_rows(const double2* __restrict__ A, const double2* v, int NB,
+                                         double2* acc) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int b = blockIdx.x, g = gridDim.x;
+  const int rows = b < NB ? (NB - 1 - b) / g + 1 : 0;
+  if (rows == 0 || (HS_S3_EXP & 1)) return;
+  const int wpr = max(1, kW3 / rows);           // warps per row
+  const int seg = (NB + wpr - 1) / wpr;
+  for (int k = warp / wpr; k < rows && warp / wpr < kW3 / wpr; k += kW3 / wpr) {
+    const int r = b + k * g, part = warp % wpr;
+    const int c0 = part * seg, c1 = min(NB, c0 + seg);
+    const double2* row = A + (int64_t)r * NB;
+    double2 a0 = czero(), a1 = czero(), a2 = czero(), a3 = czero();
+    int c = c0 + lane;
+    for (; c + 96 < c1; c += 128) {
+      const double2 m0 = __ldg(row + c), m1 = __ldg(row + c + 32), m2 = __ldg(row + c + 64),
+                    m3 = __ldg(row + c + 96);
+      a0 = cfma(m0, v[c], a0);
+      a1 = cfma(m1, v[c + 32], a1);
+      a2 = cfma(m2, v[c + 64], a2);
+      a3 = cfma(m3, v[c + 96], a3);
+    }
+    for (; c < c1; c += 32) a0 = cfma(__ldg(row + c), v[c], a0);
+    double2 t = cadd(cadd(a0, a1), cadd(a2, a3));
+    for (int m = 16; m > 0; m >>= 1) t = cadd(t, shfl_xor_c(t, m));
+    if (lane == 0) acc[k * wpr + part] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kW3 * 32, 1)
+k3_solve(const double2* __restrict__ coef, Slots sl, int T, int n1, int n2,
+         const double2* __restrict__ dinvT, const double2* __restrict__ xT,
+         const double2* __restrict__ F, double2* Y, unsigned* bar) {
+  extern __shared__ double2 v3[];   // [NB] step vector, then [2 * rows] row sums
+  const int NB = T * n2;
+  const int64_t nb2 = (int64_t)NB * NB, n = (int64_t)T * n1 * n2;
+  const int nrow = blockIdx.x < NB ? (NB - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  double2* yp = v3 + NB;               // [NB] previous plane's y
+  double2* racc = yp + NB;             // [rows][warps per row] partial row sums
+  const int wpr = rows_wpr(NB);
+  auto row_sum = [&](int k) {
+    double2 a = czero();
+    for (int p = 0; p < wpr; ++p) a = cadd(a, racc[k * wpr + p]);
+    return a;
+  };
+  unsigned epoch = 0;
+  for (int i1 = 0; i1 < n1; ++i1) {   // y_i = Dinv_i (f_i - L_i y_{i-1})
+    const double2* Fi = F + (int64_t)i1 * NB;
+    double2* Yi = Y + (int64_t)i1 * NB;
+    if (i1 > 0 && !(HS_S3_EXP & 2)) {   // y_{i-1} into shared memory once (L2 reads)
+      for (int r = threadIdx.x; r < NB; r += blockDim.x) yp[r] = __ldcg(Yi - NB + r);
+      __syncthreads();
+    }
+    for (int r = threadIdx.x; r < NB; r += blockDim.x) {
+      const int t = r / n2, i2 = r - t * n2;
+      double2 acc = __ldg(Fi + r);
+      if (i1 > 0 && !(HS_S3_EXP & 2)) {
+        double2 cv[9], yv[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {   // all loads first (predicated), then the sum
+          const int o0 = k / 3 - 1, o2 = k % 3 - 1;
+          const int s = sl.s[oid(o0, -1, o2)];
+          const bool ok = s >= 0 && t + o0 >= 0 && t + o0 < T && i2 + o2 >= 0 && i2 + o2 < n2;
+          cv[k] = ok ? __ldg(coef + (int64_t)s * n + ((int64_t)t * n1 + i1) * n2 + i2) : czero();
+          yv[k] = ok ? yp[(t + o0) * n2 + (i2 + o2)] : czero();
+        }
+#pragma unroll
+        for (int k = 0; k < 9; ++k) acc = csub(acc, cmul(cv[k], yv[k]));
+      }
+      v3[r] = acc;
+    }
+    __syncthreads();
+    cta_rows(dinvT + i1 * nb2, v3, NB, racc);
+    __syncthreads();
+    for (int k = threadIdx.x; k < nrow; k += blockDim.x) Yi[blockIdx.x + k * gridDim.x] = row_sum(k);
+    grid_barrier(bar, (++epoch) * gridDim.x);
+  }
+  for (int i1 = n1 - 2; i1 >= 0; --i1) {   // x_i = y_i - X_i x_{i+1}
+    double2* Yi = Y + (int64_t)i1 * NB;
+    for (int r = threadIdx.x; r < NB; r += blockDim.x) v3[r] = __ldcg(Yi + NB + r);
+    __syncthreads();
+    cta_rows(xT + i1 * nb2, v3, NB, racc);
+    __syncthreads();
+    for (int k = threadIdx.x; k < nrow; k += blockDim.x) {
+      const int r = blockIdx.x + k * gridDim.x;
+      Yi[r] = csub(__ldcg(Yi + r), row_sum(k));
+    }
+    grid_barrier(bar, (++epoch) * gridDim.x);
+  }
+}
+
+size_t k3_smem(int NB, int grid) {
+  return (size_t)2 * NB * sizeof(double2) + (size_t)(kW3 + (NB + grid - 1) / grid) * sizeof(double2);
 }
 
 Slots to_slots(const std::array<int, 27>& a) {
@@ -178,7 +286,8 @@ void sweep3_destroy(Sweep3* s3) {
   for (auto* p : s3->xf) cudaFree(p);
   for (auto* p : s3->coef) cudaFree(p);
   cudaFree(s3->F);
-  cudaFree(s3->W);
+  cudaFree(s3->Y);
+  cudaFree(s3->gbar);
   if (s3->blas) cublasDestroy(s3->blas);
   delete s3;
 }
@@ -202,20 +311,23 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
   cusolverDnSetStream(sol, c->stream);
   int NBmax = 0;
   for (int j = 0; j < J; ++j) NBmax = std::max(NBmax, (int)(hi[j] - lo[j] + 1) * n2);
-  double2 *D = nullptr, *Lb = nullptr, *U = nullptr, *work = nullptr;
+  double2 *D = nullptr, *Lb = nullptr, *U = nullptr, *work = nullptr, *Di = nullptr, *Xc = nullptr;
   int *ipiv = nullptr, *info = nullptr;
   const size_t blk = (size_t)NBmax * NBmax * sizeof(double2);
   int lwork = 0;
   auto done = [&](int rc) {
     cudaFree(D); cudaFree(Lb); cudaFree(U); cudaFree(work); cudaFree(ipiv); cudaFree(info);
+    cudaFree(Di); cudaFree(Xc);
     if (sol) cusolverDnDestroy(sol);
     return rc;
   };
   if (cudaMalloc((void**)&D, blk) || cudaMalloc((void**)&Lb, blk) || cudaMalloc((void**)&U, blk) ||
+      cudaMalloc((void**)&Di, blk) || cudaMalloc((void**)&Xc, blk) ||
+      cudaMalloc((void**)&s3->gbar, sizeof(unsigned)) ||
       cudaMalloc((void**)&ipiv, NBmax * sizeof(int)) ||
       cudaMalloc((void**)&info, (size_t)n1 * J * sizeof(int)) ||
       cudaMalloc((void**)&s3->F, (size_t)n1 * NBmax * sizeof(double2)) ||
-      cudaMalloc((void**)&s3->W, (size_t)NBmax * sizeof(double2)))
+      cudaMalloc((void**)&s3->Y, (size_t)n1 * NBmax * sizeof(double2)))
     return done(set_error(c, HS_E_CUDA, "3-D sweep work allocation failed"));
   if (cusolverDnZgetrf_bufferSize(sol, NBmax, NBmax, (cuDoubleComplex*)D, NBmax, &lwork) != 0 ||
       cudaMalloc((void**)&work, (size_t)std::max(1, lwork) * sizeof(double2)))
@@ -248,7 +360,6 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
     const Slots sl = to_slots(s3->slot[j]);
     const unsigned gb = (unsigned)((NB + kT3 - 1) / kT3);
     for (int i1 = 0; i1 < n1; ++i1) {
-      double2* Di = dv + i1 * nb2;
       S3_TRY(cudaMemsetAsync(D, 0, nb2 * sizeof(double2), c->stream), "memset");
       k3_block<<<gb, kT3, 0, c->stream>>>(cf, sl, T, n1, n2, i1, 0, D);
       c->launches++;
@@ -257,7 +368,7 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
         k3_block<<<gb, kT3, 0, c->stream>>>(cf, sl, T, n1, n2, i1, -1, Lb);
         c->launches++;
         S3_BLAS(cublasZgemm(s3->blas, CUBLAS_OP_N, CUBLAS_OP_N, NB, NB, NB, &mone,
-                            (cuDoubleComplex*)Lb, NB, (cuDoubleComplex*)(xv + (i1 - 1) * nb2), NB,
+                            (cuDoubleComplex*)Lb, NB, (cuDoubleComplex*)Xc, NB,
                             &one, (cuDoubleComplex*)D, NB), "zgemm");
       }
       // Dinv = D'^{-1} (partial pivoting inside the block)
@@ -267,13 +378,20 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
       c->launches++;
       S3_BLAS(cusolverDnZgetrs(sol, CUBLAS_OP_N, NB, NB, (cuDoubleComplex*)D, NB, ipiv,
                                (cuDoubleComplex*)Di, NB, info + j * n1 + i1), "getrs");
+      // stored row-major (= the column-major transpose) for the solve kernel's rows
+      S3_BLAS(cublasZgeam(s3->blas, CUBLAS_OP_T, CUBLAS_OP_N, NB, NB, &one, (cuDoubleComplex*)Di,
+                          NB, &zero, (cuDoubleComplex*)Di, NB, (cuDoubleComplex*)(dv + i1 * nb2),
+                          NB), "geam");
       if (i1 + 1 < n1) {   // X_i = Dinv_i U_i
         S3_TRY(cudaMemsetAsync(U, 0, nb2 * sizeof(double2), c->stream), "memset");
         k3_block<<<gb, kT3, 0, c->stream>>>(cf, sl, T, n1, n2, i1, 1, U);
         c->launches++;
         S3_BLAS(cublasZgemm(s3->blas, CUBLAS_OP_N, CUBLAS_OP_N, NB, NB, NB, &one,
                             (cuDoubleComplex*)Di, NB, (cuDoubleComplex*)U, NB, &zero,
-                            (cuDoubleComplex*)(xv + i1 * nb2), NB), "zgemm");
+                            (cuDoubleComplex*)Xc, NB), "zgemm");
+        S3_BLAS(cublasZgeam(s3->blas, CUBLAS_OP_T, CUBLAS_OP_N, NB, NB, &one,
+                            (cuDoubleComplex*)Xc, NB, &zero, (cuDoubleComplex*)Xc, NB,
+                            (cuDoubleComplex*)(xv + i1 * nb2), NB), "geam");
       }
     }
     S3_TRY(cudaGetLastError(), "3-D factor kernels");
@@ -291,6 +409,15 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
         return done(set_error(c, HS_E_ZERO_PIVOT, buf, row));
       }
   s->factor_bytes = s3->bytes;
+  {   // the solve kernel: one CTA per SM, co-resident (cooperative launch)
+    s3->grid = c->num_sms;
+    const int smem = (int)k3_smem(NBmax, s3->grid);
+    S3_TRY(cudaFuncSetAttribute(k3_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "attr");
+    int per = 0;
+    S3_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k3_solve, kW3 * 32, smem), "occ");
+    if (per < 1) return done(set_error(c, HS_E_CUDA, "3-D solve kernel does not fit an SM"));
+    s3->grid = c->num_sms;
+  }
   return done(HS_OK);
 }
 
@@ -306,28 +433,24 @@ int sweep3_task(Ctx* c, Sweep* s, const SweepTask& t, const double2* src, double
   k3_rhs<<<(unsigned)((tot + kT3 - 1) / kT3), kT3, 0, c->stream>>>(
       t, s->n0, n1, n2, src, coarse_coeffs, coarse_n, to_slots(s3->cslot), s->trace, s3->F);
   HS_LAUNCH_CHECK(c, "3-D rhs");
-  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), mone = make_cuDoubleComplex(-1.0, 0.0),
-                        zero = make_cuDoubleComplex(0.0, 0.0);
-  const unsigned gb = (unsigned)((NB + kT3 - 1) / kT3);
-  for (int i1 = 0; i1 < n1; ++i1) {   // y_i = Dinv_i (f_i - L_i y_{i-1})
-    double2* Fi = s3->F + (int64_t)i1 * NB;
-    k3_lsub<<<gb, kT3, 0, c->stream>>>(s3->coef[j], sl, T, n1, n2, i1, Fi,
-                                        i1 ? Fi - NB : nullptr, s3->W);
-    HS_LAUNCH_CHECK(c, "3-D forward");
-    S3_BLAS(cublasZgemv(s3->blas, CUBLAS_OP_N, NB, NB, &one,
-                        (const cuDoubleComplex*)(s3->dinv[j] + i1 * nb2), NB,
-                        (const cuDoubleComplex*)s3->W, 1, &zero, (cuDoubleComplex*)Fi, 1), "zgemv");
-    c->launches++;
+  {   // block recursion: one cooperative launch
+    S3_TRY(cudaMemsetAsync(s3->gbar, 0, sizeof(unsigned), c->stream), "memset");
+    const double2* cf = s3->coef[j];
+    const double2* dv = s3->dinv[j];
+    const double2* xv = s3->xf[j];
+    const double2* Fp = s3->F;
+    double2* Yp = s3->Y;
+    unsigned* gb = s3->gbar;
+    int T_ = T, n1_ = n1, n2_ = n2;
+    Slots sl_ = sl;
+    void* args[] = {(void*)&cf, (void*)&sl_, (void*)&T_, (void*)&n1_, (void*)&n2_,
+                    (void*)&dv, (void*)&xv, (void*)&Fp, (void*)&Yp, (void*)&gb};
+    S3_TRY(cudaLaunchCooperativeKernel((const void*)k3_solve, dim3(s3->grid), dim3(kW3 * 32), args,
+                                       k3_smem(NB, s3->grid), c->stream),
+           "3-D solve launch");
+    HS_LAUNCH_CHECK(c, "3-D solve kernel");
   }
-  for (int i1 = n1 - 2; i1 >= 0; --i1) {   // x_i = y_i - X_i x_{i+1}
-    double2* Fi = s3->F + (int64_t)i1 * NB;
-    S3_BLAS(cublasZgemv(s3->blas, CUBLAS_OP_N, NB, NB, &mone,
-                        (const cuDoubleComplex*)(s3->xf[j] + i1 * nb2), NB,
-                        (const cuDoubleComplex*)(Fi + NB), 1, &one, (cuDoubleComplex*)Fi, 1),
-            "zgemv");
-    c->launches++;
-  }
-  k3_out<<<(unsigned)((tot + kT3 - 1) / kT3), kT3, 0, c->stream>>>(t, n1, n2, s3->F, u[t.dst],
+  k3_out<<<(unsigned)((tot + kT3 - 1) / kT3), kT3, 0, c->stream>>>(t, n1, n2, s3->Y, u[t.dst],
                                                                    s->trace);
   HS_LAUNCH_CHECK(c, "3-D outputs");
   return HS_OK;

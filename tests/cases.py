@@ -50,6 +50,10 @@ def case(name):
         mesh, model = constant_case(3, 8, AbsorbingLayerSpec(PML, 3, 15.0), 6.0)
         return mesh, model, None, hb.SmootherConfig(0.6, 2), hb.SweepOptions(3, 15.0, "x",
                                                                              subdomains=2)
+    if name == "pml3d_s":
+        mesh, model = constant_case(3, 16, AbsorbingLayerSpec(PML, 3, 15.0), 8.0)
+        return mesh, model, None, hb.SmootherConfig(0.6, 2), hb.SweepOptions(3, 15.0, "x",
+                                                                             subdomains=4)
     raise KeyError(name)
 
 

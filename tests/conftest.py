@@ -10,8 +10,8 @@ GOLDEN = ROOT / "tests" / "golden"
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
 
-CASES = ["pml2d", "wedge2d", "sponge2d", "fe9_2d", "pml3d"]
-SOLVED = ["pml2d", "wedge2d", "sponge2d"]
+CASES = ["pml2d", "wedge2d", "sponge2d", "fe9_2d", "pml3d", "pml3d_s"]
+SOLVED = ["pml2d", "wedge2d", "sponge2d", "pml3d_s"]
 
 
 def pytest_configure(config):

@@ -214,6 +214,9 @@ def main():
     mesh, model = constant_case(3, 8, AbsorbingLayerSpec(PML, 3, 15.0), 6.0)
     case_fixture("pml3d", mesh, model, SmootherConfig(0.6, 2),
                  SweepOptions(3, 15.0, "x", subdomains=2), solve=False)
+    mesh, model = constant_case(3, 16, AbsorbingLayerSpec(PML, 3, 15.0), 8.0)
+    case_fixture("pml3d_s", mesh, model, SmootherConfig(0.6, 2),
+                 SweepOptions(3, 15.0, "x", subdomains=4))
     known_answers()
     c1_anchors()
 

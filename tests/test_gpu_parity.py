@@ -151,9 +151,10 @@ def test_tgsp_vs_oracle_larger():
                tg.part.prec_ud(z[:hh.coarse_op.shape[0], :hh.coarse_op.shape[1]])) < 1e-11
 
 
-def test_tgsp_linear_and_deterministic(rng):
+@pytest.mark.parametrize("name", ["wedge2d", "pml3d"])
+def test_tgsp_linear_and_deterministic(rng, name):
     import paper_1412_0464_b200 as hb
-    cycle = _build("wedge2d")
+    cycle = _build(name)
     shape = cycle.fine_op.shape
     f1, f2 = crand(rng, shape), crand(rng, shape)
     lhs = hb.tgsp_apply(cycle, f1 + f2)
