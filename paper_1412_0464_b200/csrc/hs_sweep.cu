@@ -1121,6 +1121,22 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     asm volatile("bar.sync 1, %0;" ::"r"(kCW * 32) : "memory");
   };
 
+  const int total_chunks = fcount * CPT;
+  // issue chunk cs into its ring slot (the slot's previous chunk is consumed)
+  auto fill = [&](int cs) {
+    const int sl = cs % NC;
+    const int ti = cs / CPT, c = cs - ti * CPT;
+    const uint32_t ce = ctab[c];
+    const int nbk = (int)(ce & 0xff);
+    *(volatile int*)&ccnt[sl] = 0;   // ordered before cseq (same thread, volatile)
+    const double2* sbase = a.stream + ((int64_t)slabs[ti] * C + rank) * a.nbs * TM2;
+    mbar_expect_tx(&cbar[sl], (HS_SWEEP_EXP & 2) ? 0u : (uint32_t)nbk * TM2 * 16);
+    if (!(HS_SWEEP_EXP & 2))
+      bulk_g2s(ring + (int64_t)sl * CHUNK, sbase + (int64_t)(ce >> 8) * TM2,
+               (uint32_t)nbk * TM2 * 16, &cbar[sl]);
+    cseq[sl] = cs;
+    if (ti == 1) istamp(c, 0);
+  };
   if (warp == kCW) {
     // ---- TMA producer warp: lane l owns ring slot l (l < NC) and streams
     // chunks cs = l, l + NC, l + 2 NC, ... of the launch's slab solves, each as
@@ -1128,25 +1144,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     // independently (no batch lockstep).
     if (lane < NC && !HS_SWEEP_DIRECT) {
       const int sl = lane;
-      const int total = fcount * CPT;
       int prev_n = -1;
-      for (int cs = sl; cs < total; cs += NC) {
-        const int ti = cs / CPT, c = cs - ti * CPT;
-        const uint32_t ce = ctab[c];
-        const int nbk = (int)(ce & 0xff);
+      for (int cs = sl; cs < total_chunks; cs += NC) {
         if (prev_n >= 0) {   // the slot's previous chunk (cs - NC) fully consumed
           while (*(volatile int*)&ccnt[sl] != prev_n) {
           }
         }
-        prev_n = nbk;
-        *(volatile int*)&ccnt[sl] = 0;   // ordered before cseq (same thread, volatile)
-        const double2* sbase = a.stream + ((int64_t)slabs[ti] * C + rank) * a.nbs * TM2;
-        mbar_expect_tx(&cbar[sl], (HS_SWEEP_EXP & 2) ? 0u : (uint32_t)nbk * TM2 * 16);
-        if (!(HS_SWEEP_EXP & 2))
-          bulk_g2s(ring + (int64_t)sl * CHUNK, sbase + (int64_t)(ce >> 8) * TM2,
-                   (uint32_t)nbk * TM2 * 16, &cbar[sl]);
-        cseq[sl] = cs;
-        if (ti == 1) istamp(c, 0);
+        prev_n = (int)(ctab[cs % CPT] & 0xff);
+        fill(cs);
       }
     }
     __syncwarp();
@@ -1182,7 +1187,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     __syncwarp();
     if (!HS_SWEEP_DIRECT && has && lane % (32 / HW) == 0) {
       const uint32_t e = ib[r];
-      atomicAdd(&ccnt[(ti * CPT + (int)(e >> 12)) % NC], (int)((e >> 1) & 3));
+      const int cs = ti * CPT + (int)(e >> 12), n = (int)((e >> 1) & 3);
+      atomicAdd(&ccnt[cs % NC], n);
       if (ti == 1) istamp(r, 2);
     }
   };
