@@ -69,6 +69,9 @@ constexpr int kNA = 8;             // consumer warps of the back substitution wh
 #ifndef HS_SWEEP_EXP       // timing experiments: 1 no item arithmetic, 2 no factor copies
 #define HS_SWEEP_EXP 0
 #endif
+#if (HS_SWEEP_EXP & 8) && !(HS_SWEEP_EXP & 2)
+#error "HS_SWEEP_EXP bit 8 (no ring reuse wait) needs bit 2 (no copies)"
+#endif
 #ifndef HS_SWEEP_DIRECT    // experiment: consumers read factor blocks straight from global memory
 #define HS_SWEEP_DIRECT 0
 #endif
@@ -1023,7 +1026,7 @@ struct Ring {
   static int fixed(int mmax) {
     return 2 * (mmax + 1) * TM * 16 + 4 * kMaxC * TM * 16 + 4 * TM * 16 +
            (kWarps + 1) * 2 * TM * 16 + 12 * mmax * 16 + 64 + (int)sizeof(ItemPlan) +
-           kMaxTasks * 4 + itab_len(mmax) * 8 + 512;
+           kMaxTasks * 4 + itab_len(mmax) * 12 + 512;
   }
   static int nchunk(int mmax) {
     const int avail = 225 * 1024 - fixed(mmax);
@@ -1071,8 +1074,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   uint32_t* ctab = ib + itab_len(mmax);             // [<= ITEMS] chunk: first block | blocks
   int* nchk = (int*)(ctab + itab_len(mmax));        // chunks per slab solve
   int* slabs = nchk + 1;                            // [fcount]
+  uint32_t* cmq = (uint32_t*)(slabs + kMaxTasks);   // [chunks] c % NC | (c / NC) << 16
   // (offset from sm keeps the shared-space provenance: LDS, not generic loads)
-  double2* ring = sm + ((((char*)(slabs + kMaxTasks) - (char*)sm) + 127) & ~(ptrdiff_t)127) / 16;
+  double2* ring = sm + ((((char*)(cmq + itab_len(mmax)) - (char*)sm) + 127) & ~(ptrdiff_t)127) / 16;
   const ItemPlan& P = *Pp;
 
   const int ffirst = front ? a.ffirst[1] : a.ffirst[0];
@@ -1096,6 +1100,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   const int NP = P.NP, L = P.L, S = P.S, qk = P.qk, QP = P.QP;
   const int ITEMS = P.pfx[NP + 2];
   const int CPT = *nchk;   // chunk copies per slab solve
+  for (int c = threadIdx.x; c < CPT; c += blockDim.x) cmq[c] = (uint32_t)(c % NC) | (uint32_t)(c / NC) << 16;
+  __syncthreads();
+  // ring position of the current task's chunk 0 (set per task: no divisions per item)
+  int task_q = 0, task_r = 0;
+  bool trace_task = false;   // HS_SWEEP_TRACE: per-item stamps of task 1
 
   __shared__ int rr[kNR];   // the current task's restricted-update rows
   // optional instrumentation: task 1 timestamps kept in shared memory, dumped at exit
@@ -1146,7 +1155,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       const int sl = lane;
       int prev_n = -1;
       for (int cs = sl; cs < total_chunks; cs += NC) {
-        if (prev_n >= 0) {   // the slot's previous chunk (cs - NC) fully consumed
+        if (prev_n >= 0 && !(HS_SWEEP_EXP & 8)) {   // the slot's previous chunk fully consumed
           while (*(volatile int*)&ccnt[sl] != prev_n) {
           }
         }
@@ -1160,36 +1169,48 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   }
 
   // ---- consumers: item r of task ti -> its (one or two) blocks in the ring
-  auto wait_chunk = [&](int cs) {
-    const int sl = cs % NC;
+  auto wait_chunk = [&](int cs, int sl, int q) {
+    if (HS_SWEEP_EXP & 8) {   // experiment: no slot reuse hazard (no data), only issue order
+      while ((int)(cseq[sl] - cs) < 0) {
+      }
+      return;
+    }
     while (cseq[sl] != cs) {
     }
-    mbar_wait(&cbar[sl], (uint32_t)((cs / NC) & 1));
+    mbar_wait(&cbar[sl], (uint32_t)(q & 1));
   };
-  struct Item { const double2* m0; const double2* m1; };
+  struct Item { const double2* m0; const double2* m1; int sl, n, r; };
+  // slot and phase parity of chunk c of the current task
+  auto slot_of = [&](int c, int& sl, int& q) {
+    const uint32_t t = cmq[c];
+    sl = task_r + (int)(t & 0xffff);
+    q = task_q + (int)(t >> 16);
+    if (sl >= NC) { sl -= NC; ++q; }
+  };
   auto acquire = [&](int ti, int r) -> Item {
     const uint32_t e = ib[r];
     const int cs = ti * CPT + (int)(e >> 12);
     const bool hx = e & 1;
+    const int n = (int)((e >> 1) & 3);
     if (HS_SWEEP_DIRECT) {
       const double2* p0 = a.stream + (((int64_t)slabs[ti] * C + rank) * a.nbs +
                                       (ctab[e >> 12] >> 8) + ((e >> 3) & 0x1ff)) * TM2;
-      return hx ? Item{p0, p0 + TM2} : Item{nullptr, p0};
+      return hx ? Item{p0, p0 + TM2, 0, n, r} : Item{nullptr, p0, 0, n, r};
     }
-    wait_chunk(cs);
+    int sl, q;
+    slot_of((int)(e >> 12), sl, q);
+    wait_chunk(cs, sl, q);
     if (ti == 1 && lane % (32 / HW) == 0) istamp(r, 1);
-    const double2* p0 = ring + (int64_t)(cs % NC) * CHUNK + (int)((e >> 3) & 0x1ff) * TM2;
-    return hx ? Item{p0, p0 + TM2} : Item{nullptr, p0};
+    const double2* p0 = ring + (int64_t)sl * CHUNK + (int)((e >> 3) & 0x1ff) * TM2;
+    return hx ? Item{p0, p0 + TM2, sl, n, r} : Item{nullptr, p0, sl, n, r};
   };
   // The warp's reads of the blocks have returned (their values are consumed
   // before the __syncwarp), so the producer's async-proxy refill cannot race.
-  auto release = [&](int ti, int r, bool has) {
+  auto release = [&](const Item& it, bool has) {
     __syncwarp();
     if (!HS_SWEEP_DIRECT && has && lane % (32 / HW) == 0) {
-      const uint32_t e = ib[r];
-      const int cs = ti * CPT + (int)(e >> 12), n = (int)((e >> 1) & 3);
-      atomicAdd(&ccnt[cs % NC], n);
-      if (ti == 1) istamp(r, 2);
+      atomicAdd(&ccnt[it.sl], it.n);
+      if (trace_task) istamp(it.r, 2);
     }
   };
   // Right-hand-side inputs of task tn, copied asynchronously while the
@@ -1252,6 +1273,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   SweepTask tn = t;
   for (int ti = 0; ti < fcount; ++ti) {
     if (ti > 0) t = tn;   // loaded during the previous task
+    trace_task = a.dbg != nullptr && ti == 1;
+    task_q = ti * CPT / NC;
+    task_r = ti * CPT - task_q * NC;
     if (ti + 1 < fcount) tn = a.tasks[ffirst + ti + 1];   // in flight early
     const int par = ti & 1;
     double2* tau = tau2 + par * 2 * kMaxC * TM;
@@ -1291,10 +1315,27 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     stamp(ti, 1);
     // ---- chunk-local solve: L cyclic-reduction levels, the dense top, back substitution
     // item j of phase p (warp-uniform `has`)
-    auto do_item = [&](int p, int j, bool has) {
-      const int l = plan_level(P, p), s = 1 << l;
-      const int yl = has && p != L ? plan_yl(P, p, j) : 0;
-      const int r = P.pfx[p] + j;
+    // phase constants in registers (P lives in shared memory and the ring's
+    // waits are memory clobbers: per-item reloads would be on the critical path)
+    struct Ph { int p, l, s, pf0, cnt, ne, first, step; };
+    auto phase = [&](int p) {
+      Ph h;
+      h.p = p;
+      h.l = plan_level(P, p);
+      h.s = 1 << h.l;
+      h.pf0 = P.pfx[p];
+      h.cnt = P.pfx[p + 1] - h.pf0;
+      h.ne = h.cnt / 2;
+      h.first = plan_first(P, p);
+      h.step = plan_step(P, p);
+      return h;
+    };
+    auto do_item = [&](const Ph& h, int j, bool has) {
+      const int p = h.p, l = h.l, s = h.s;
+      const int yl = !has || p == L ? 0
+                     : p > L        ? h.first + j * h.step
+                                    : (j < h.ne ? 2 * j + 1 : 2 * (j - h.ne)) << p;
+      const int r = h.pf0 + j;
       const Item it = has ? acquire(ti, r) : Item{nullptr, nullptr};
       const double2* m0 = it.m0;
       const double2* m1 = it.m1;
@@ -1327,12 +1368,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
           if (wr) Yv[yl * TM + x] = csub(Yv[yl * TM + x], acc);
         }
       }
-      release(ti, r, has);
+      release(it, has);
     };
     // phase p over warps [w0, w0 + nw)
     auto run_phase = [&](int p, int w0, int nw) {
-      const int cnt = P.pfx[p + 1] - P.pfx[p];
-      for (int jp = (warp - w0) * HW; jp < cnt; jp += nw * HW) do_item(p, jp + sub, jp + sub < cnt);
+      const Ph h = phase(p);
+      for (int jp = (warp - w0) * HW; jp < h.cnt; jp += nw * HW) do_item(h, jp + sub, jp + sub < h.cnt);
     };
     for (int p = 0; p <= L; ++p) {   // forward levels and the dense top: all warps
       run_phase(p, 0, kCW);
@@ -1379,8 +1420,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
         const int j = jp + sub;
         const bool has = j < nq;
         const int r = P.pfx[NP] + j;
+        Item it{};
         if (has) {
-          const Item it = acquire(ti, r);   // 2tm x tm, row index fastest, over two blocks
+          it = acquire(ti, r);   // 2tm x tm, row index fastest, over two blocks
           const double2* tq = tau + j * TM;
 #pragma unroll 4
           for (int c = 0; c < TM / 2; ++c) {
@@ -1395,7 +1437,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
             if (HW == 2 || TM == 32) acc1 = cfma(it.m1[c * N2 + r1], tv, acc1);
           }
         }
-        release(ti, r, has);
+        release(it, has);
       }
       if (HW == 2) {   // both halves' items hold rows x and x + 16
         acc0 = cadd(acc0, shfl_xor_c(acc0, 16));
@@ -1421,8 +1463,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
         const int j = jp + sub;
         const bool has = j < m;
         const int r = P.pfx[NP + 1] + j;
+        Item it{};
         if (has) {
-          const Item it = acquire(ti, r);   // W_j, V_j
+          it = acquire(ti, r);   // W_j, V_j
           if (g.nr) {                       // only the rows read later
             const double2 acc = mvr<TM>(it.m0, rank > 0 ? ab : nullptr, rank < B ? ab + TM : nullptr,
                                         lane);
@@ -1434,7 +1477,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
             if (wr) Yv[j * TM + x] = csub(Yv[j * TM + x], acc);
           }
         }
-        release(ti, r, has);
+        release(it, has);
       }
       stamp(ti, 42);
       csync();
