@@ -1216,8 +1216,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   // Right-hand-side inputs of task tn, copied asynchronously while the
   // previous task finishes: restriction rows straight into F (free after the
   // previous task's dense top) and the transmission couplings into stc.
-  auto prefetch_rhs = [&](const SweepTask& t) {
-    for (int yl = warp * YPW + hh; yl < m; yl += kCW * YPW) {
+  auto prefetch_rhs = [&](const SweepTask& t, int w0, int nw) {   // warps [w0, w0 + nw)
+    for (int yl = (warp - w0) * YPW + hh; yl < m; yl += nw * YPW) {
       const int y = Y0 + yl;
       const int gr = x + t.lo - 1;
       const bool ok = x < t.T && gr >= t.a && gr < t.b;
@@ -1269,7 +1269,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   };
 
   SweepTask prev{}, t = fcount > 0 ? a.tasks[ffirst] : SweepTask{};
-  if (fcount > 0) prefetch_rhs(t);
+  if (fcount > 0) prefetch_rhs(t, 0, kCW);
   SweepTask tn = t;
   for (int ti = 0; ti < fcount; ++ti) {
     if (ti > 0) t = tn;   // loaded during the previous task
@@ -1388,14 +1388,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
         Yv[r * S * TM + xx] = acc;
       }
       csync();
-      if (ti + 1 < fcount) prefetch_rhs(tn);   // F is free from here on
-    }
-    // tips are pushed to every CTA as soon as final
-    if (B > 0 && lane < TM && warp >= kCW - 8) {
-      if (rank > 0) push_tip(tau, par, (2 * (rank - 1) + 1) * TM, Yv, warp - (kCW - 8), 8);
-      if (P.plast == L && rank < B) push_tip(tau, par, 2 * rank * TM, Yv + (m - 1) * TM, warp - (kCW - 8), 8);
     }
     if (B == 0) {
+      if (ti + 1 < fcount) prefetch_rhs(tn, 0, kCW);   // F is free from here on
       for (int p = L + 1; p < NP; ++p) {
         run_phase(p, 0, kCW);
         csync();
@@ -1409,7 +1404,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
           push_tip(tau, par, 2 * rank * TM, Yv + (m - 1) * TM, warp, kNA);
       }
     } else {
-      // ---- group B: alpha_{k-1}, beta_k = (rows of R) tau once every tip is in
+      // ---- group B: tips out (as soon as final), the next task's rhs inputs
+      // (F is free from here on), then alpha_{k-1}, beta_k = (rows of R) tau
+      if (lane < TM) {
+        if (rank > 0) push_tip(tau, par, (2 * (rank - 1) + 1) * TM, Yv, warp - kNA, kCW - kNA);
+        if (P.plast == L && rank < B)
+          push_tip(tau, par, 2 * rank * TM, Yv + (m - 1) * TM, warp - kNA, kCW - kNA);
+      }
+      if (ti + 1 < fcount) prefetch_rhs(tn, kNA, kCW - kNA);
       mbar_wait(&xbar[par], (uint32_t)(ti >> 1) & 1);
       stamp(ti, 40);
       // rows r0 = lane (tm 32) or x (tm 16, per half) and r0 + 32 / r0 + 16
