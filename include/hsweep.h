@@ -127,6 +127,14 @@ int hs_cycle_destroy(hs_ctx* ctx, hs_cycle* c);
 int hs_vcycle(hs_ctx* ctx, hs_cycle* c, const void* f, void* u);
 /* w = A M f (the GMRES operator, krylov.py:125-126) */
 int hs_vcycle_apply_a(hs_ctx* ctx, hs_cycle* c, const void* f, void* w);
+/* The same operator in two halves, so a host pipelining the Arnoldi loop can
+ * queue the pre-coarse part of the next iteration before it reads the
+ * current Hessenberg column: begin = pre-smoothing, residual, restriction
+ * (twogrid.py:152-154); end = sweep, prolongation, post-smoothing and the
+ * fine matvec (twogrid.py:155-159, krylov.py:126).  One begin/end pair per
+ * cycle handle may be in flight. */
+int hs_vcycle_apply_a_begin(hs_ctx* ctx, hs_cycle* c, const void* f);
+int hs_vcycle_apply_a_end(hs_ctx* ctx, hs_cycle* c, const void* f, void* w);
 
 /* ---- GMRES vector kernels (krylov.py:46-102) ------------------------------
  * V: device basis, k vectors of length n with leading dimension ldv (elements).
@@ -137,6 +145,19 @@ int hs_block_dot(hs_ctx* ctx, const void* V, int64_t ldv, int k, const void* w, 
 /* w -= sum_i h[i] V_i (i < k); nrm2[0] = (||w||^2, 0) */
 int hs_block_update(hs_ctx* ctx, const void* V, int64_t ldv, int k, const void* h, void* w,
                     int64_t n, void* nrm2);
+/* Second (DGKS) Gram-Schmidt pass gated on the device, krylov.py:67-70 with
+ * re-orthogonalisation: runs only when g_after[0].re < thresh * g_before[0].re
+ * (||w||^2 after / before the first pass); a closed gate leaves h untouched
+ * and copies g_after[0] into nrm2[0]. */
+int hs_block_dot_gated(hs_ctx* ctx, const void* V, int64_t ldv, int k, const void* w,
+                       int64_t n, void* h, const void* g_after, const void* g_before,
+                       double thresh);
+int hs_block_update_gated(hs_ctx* ctx, const void* V, int64_t ldv, int k, const void* h,
+                          void* w, int64_t n, void* nrm2, const void* g_after,
+                          const void* g_before, double thresh);
+/* x *= 1 / sqrt(max(s[0].re, 0)): the Arnoldi normalisation v_{k+1} = w / H[k+1,k]
+ * (krylov.py:70-72) with the norm read on the device */
+int hs_scale_inv_sqrt(hs_ctx* ctx, void* x, int64_t n, const void* s);
 /* out = sum_i y[i] V_i  (y: device, k complex) */
 int hs_lincomb(hs_ctx* ctx, const void* V, int64_t ldv, int k, const void* y, void* out,
                int64_t n);

@@ -69,9 +69,11 @@ static int prof_collect(Ctx* c) {
 }
 
 // declared in the kernel translation units
-int krylov_block_dot(Ctx*, const double2*, int64_t, int, const double2*, int64_t, double2*);
+int krylov_block_dot(Ctx*, const double2*, int64_t, int, const double2*, int64_t, double2*,
+                     const double2*, const double2*, double);
 int krylov_block_update(Ctx*, const double2*, int64_t, int, const double2*, double2*, int64_t,
-                        double2*);
+                        double2*, const double2*, const double2*, double);
+int krylov_scale_inv_sqrt(Ctx*, double2*, int64_t, const double2*);
 int krylov_lincomb(Ctx*, const double2*, int64_t, int, const double2*, double2*, int64_t);
 int krylov_scale(Ctx*, double2*, int64_t, double2);
 int krylov_axpby(Ctx*, double2, const double2*, double2, double2*, int64_t);
@@ -93,7 +95,9 @@ struct Cycle {
   double2* tmp = nullptr;  // fine M f for apply_a
 };
 
-static int vcycle(Ctx* c, Cycle* cy, const double2* f, double2* u) {
+// First half of the cycle: pre-smoothing from zero, residual, restriction
+// (everything before the coarse solve).
+static int vcycle_begin(Ctx* c, Cycle* cy, const double2* f, double2* u) {
   const int64_t nf = cy->fine->d.n;
   int r;
   if (cy->nu > 0) {
@@ -104,11 +108,21 @@ static int vcycle(Ctx* c, Cycle* cy, const double2* f, double2* u) {
   }
   if (r) return r;
   if ((r = stencil_apply(c, cy->fine, u, cy->r, 1, f))) return r;              // r = f - A u
-  if ((r = transfer_restrict(c, cy->t, cy->r, cy->rc, cy->scale, 1))) return r; // h^d P^T r
+  return transfer_restrict(c, cy->t, cy->r, cy->rc, cy->scale, 1);             // h^d P^T r
+}
+
+// Second half: coarse sweep, prolongation + correction, post-smoothing.
+static int vcycle_end(Ctx* c, Cycle* cy, const double2* f, double2* u) {
+  int r;
   if ((r = sweep_apply(c, cy->sweep, cy->variant, cy->rc, cy->uc))) return r;   // coarse solve
   if ((r = transfer_prolong(c, cy->t, cy->uc, u, 1, 1))) return r;             // u += P uc
   if (cy->nu > 0) r = stencil_jacobi(c, cy->fine, u, f, cy->omega, cy->nu, 0, 1);
   return r;
+}
+
+static int vcycle(Ctx* c, Cycle* cy, const double2* f, double2* u) {
+  int r = vcycle_begin(c, cy, f, u);
+  return r ? r : vcycle_end(c, cy, f, u);
 }
 
 }  // namespace hs
@@ -430,18 +444,52 @@ int hs_vcycle_apply_a(hs_ctx* c, hs_cycle* cy, const void* f, void* w) {
   return stencil_apply(c, cy->fine, cy->tmp, (double2*)w, 1, nullptr);
 }
 
+int hs_vcycle_apply_a_begin(hs_ctx* c, hs_cycle* cy, const void* f) {
+  if (!c || !cy || !f) return HS_E_ARG;
+  return vcycle_begin(c, cy, (const double2*)f, cy->tmp);
+}
+
+int hs_vcycle_apply_a_end(hs_ctx* c, hs_cycle* cy, const void* f, void* w) {
+  if (!c || !cy || !f || !w) return HS_E_ARG;
+  int r = vcycle_end(c, cy, (const double2*)f, cy->tmp);
+  if (r) return r;
+  return stencil_apply(c, cy->fine, cy->tmp, (double2*)w, 1, nullptr);
+}
+
 // ---------------------------------------------------------------------------
 int hs_block_dot(hs_ctx* c, const void* V, int64_t ldv, int k, const void* w, int64_t n,
                  void* h) {
   if (!c || (!V && k > 0) || !w || !h) return HS_E_ARG;
-  return krylov_block_dot(c, (const double2*)V, ldv, k, (const double2*)w, n, (double2*)h);
+  return krylov_block_dot(c, (const double2*)V, ldv, k, (const double2*)w, n, (double2*)h,
+                          nullptr, nullptr, 0.0);
 }
 
 int hs_block_update(hs_ctx* c, const void* V, int64_t ldv, int k, const void* h, void* w,
                     int64_t n, void* nrm2) {
   if (!c || (!V && k > 0) || !h || !w || !nrm2) return HS_E_ARG;
   return krylov_block_update(c, (const double2*)V, ldv, k, (const double2*)h, (double2*)w, n,
-                             (double2*)nrm2);
+                             (double2*)nrm2, nullptr, nullptr, 0.0);
+}
+
+int hs_block_dot_gated(hs_ctx* c, const void* V, int64_t ldv, int k, const void* w, int64_t n,
+                       void* h, const void* g_after, const void* g_before, double thresh) {
+  if (!c || (!V && k > 0) || !w || !h || !g_after || !g_before) return HS_E_ARG;
+  return krylov_block_dot(c, (const double2*)V, ldv, k, (const double2*)w, n, (double2*)h,
+                          (const double2*)g_after, (const double2*)g_before, thresh);
+}
+
+int hs_block_update_gated(hs_ctx* c, const void* V, int64_t ldv, int k, const void* h, void* w,
+                          int64_t n, void* nrm2, const void* g_after, const void* g_before,
+                          double thresh) {
+  if (!c || (!V && k > 0) || !h || !w || !nrm2 || !g_after || !g_before) return HS_E_ARG;
+  return krylov_block_update(c, (const double2*)V, ldv, k, (const double2*)h, (double2*)w, n,
+                             (double2*)nrm2, (const double2*)g_after,
+                             (const double2*)g_before, thresh);
+}
+
+int hs_scale_inv_sqrt(hs_ctx* c, void* x, int64_t n, const void* s) {
+  if (!c || !x || !s) return HS_E_ARG;
+  return krylov_scale_inv_sqrt(c, (double2*)x, n, (const double2*)s);
 }
 
 int hs_lincomb(hs_ctx* c, const void* V, int64_t ldv, int k, const void* y, void* out,

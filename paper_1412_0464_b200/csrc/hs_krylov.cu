@@ -33,10 +33,24 @@ __device__ __forceinline__ double2 block_sum(double2 v, double2* sh) {
   return s;
 }
 
+// DGKS gate of the second Gram-Schmidt pass, evaluated on the device so the
+// host never has to read the first pass before issuing the second:
+// run = ||w_after||^2 < thresh * ||w_before||^2 (the host's test, same double ops).
+struct Gate {
+  const double2* after;    // null: always run
+  const double2* before;
+  double thresh;
+};
+
+__device__ __forceinline__ bool gate_open(const Gate& g) {
+  return g.after == nullptr || g.after->x < g.thresh * g.before->x;
+}
+
 template <int K>
 __global__ void __launch_bounds__(kThreads)
 k_block_dot(const double2* __restrict__ V, int64_t ldv, const double2* __restrict__ w,
-            int64_t n, double2* __restrict__ part) {
+            int64_t n, double2* __restrict__ part, Gate gate) {
+  if (!gate_open(gate)) return;
   double2 acc[K + 1];
 #pragma unroll
   for (int i = 0; i <= K; ++i) acc[i] = czero();
@@ -58,7 +72,8 @@ k_block_dot(const double2* __restrict__ V, int64_t ldv, const double2* __restric
 template <int K>
 __global__ void __launch_bounds__(kThreads)
 k_block_update(const double2* __restrict__ V, int64_t ldv, const double2* __restrict__ h,
-               double2* __restrict__ w, int64_t n, double2* __restrict__ part) {
+               double2* __restrict__ w, int64_t n, double2* __restrict__ part, Gate gate) {
+  if (!gate_open(gate)) return;
   double2 hv[K > 0 ? K : 1];
 #pragma unroll
   for (int i = 0; i < K; ++i) hv[i] = h[i];
@@ -95,9 +110,15 @@ k_lincomb(const double2* __restrict__ V, int64_t ldv, const double2* __restrict_
   }
 }
 
-// second stage: out[i] = sum_b part[b][i], fixed order
+// second stage: out[i] = sum_b part[b][i], fixed order.  A closed gate
+// leaves `out` alone, or (pass_through) copies the gate's norm into out[0]
+// so the caller always finds the final ||w||^2 in the same slot.
 __global__ void k_reduce_parts(const double2* __restrict__ part, int nblk, int width,
-                               double2* __restrict__ out) {
+                               double2* __restrict__ out, Gate gate, int pass_through) {
+  if (!gate_open(gate)) {
+    if (pass_through && threadIdx.x == 0) out[0] = *gate.after;
+    return;
+  }
   __shared__ double2 sh[kThreads / 32];
   for (int i = 0; i < width; ++i) {
     double2 acc = czero();
@@ -108,6 +129,15 @@ __global__ void k_reduce_parts(const double2* __restrict__ part, int nblk, int w
 }
 
 __global__ void k_scale(double2* x, int64_t n, double2 a) {
+  for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * kThreads)
+    x[j] = cmul(a, x[j]);
+}
+
+// x *= 1 / sqrt(max(s.re, 0)): the Arnoldi normalisation with the norm read
+// on the device (the host computes the same value for H[k+1,k]).
+__global__ void k_scale_inv_sqrt(double2* x, int64_t n, const double2* __restrict__ s) {
+  const double2 a = make_double2(1.0 / sqrt(fmax(s->x, 0.0)), 0.0);
   for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * kThreads)
     x[j] = cmul(a, x[j]);
@@ -142,7 +172,9 @@ int grid_for(Ctx* c, int64_t n) {
 }  // namespace
 
 int krylov_block_dot(Ctx* c, const double2* V, int64_t ldv, int k, const double2* w, int64_t n,
-                     double2* h) {
+                     double2* h, const double2* g_after, const double2* g_before,
+                     double thresh) {
+  const Gate gate{g_after, g_before, thresh};
   if (k < 0 || k > kMaxK) return set_error(c, HS_E_ARG, "block_dot: k out of range");
   const int nb = grid_for(c, n);
   double2* part = (double2*)scratch(c, (size_t)nb * (k + 1) * sizeof(double2), 2);
@@ -150,7 +182,7 @@ int krylov_block_dot(Ctx* c, const double2* V, int64_t ldv, int k, const double2
   ProfScope ps(c, K_KRYLOV_DOT, 16.0 * (k + 1) * (double)n);
   switch (k) {
 #define HS_CASE(KK) \
-  case KK: k_block_dot<KK><<<nb, kThreads, 0, c->stream>>>(V, ldv, w, n, part); break;
+  case KK: k_block_dot<KK><<<nb, kThreads, 0, c->stream>>>(V, ldv, w, n, part, gate); break;
     HS_CASE(0) HS_CASE(1) HS_CASE(2) HS_CASE(3) HS_CASE(4) HS_CASE(5) HS_CASE(6) HS_CASE(7)
     HS_CASE(8) HS_CASE(9) HS_CASE(10) HS_CASE(11) HS_CASE(12) HS_CASE(13) HS_CASE(14)
     HS_CASE(15) HS_CASE(16) HS_CASE(17) HS_CASE(18) HS_CASE(19) HS_CASE(20) HS_CASE(21)
@@ -159,13 +191,15 @@ int krylov_block_dot(Ctx* c, const double2* V, int64_t ldv, int k, const double2
 #undef HS_CASE
   }
   HS_LAUNCH_CHECK(c, "block_dot");
-  k_reduce_parts<<<1, kThreads, 0, c->stream>>>(part, nb, k + 1, h);
+  k_reduce_parts<<<1, kThreads, 0, c->stream>>>(part, nb, k + 1, h, gate, 0);
   HS_LAUNCH_CHECK(c, "reduce");
   return HS_OK;
 }
 
 int krylov_block_update(Ctx* c, const double2* V, int64_t ldv, int k, const double2* h,
-                        double2* w, int64_t n, double2* nrm2) {
+                        double2* w, int64_t n, double2* nrm2, const double2* g_after,
+                        const double2* g_before, double thresh) {
+  const Gate gate{g_after, g_before, thresh};
   if (k < 0 || k > kMaxK) return set_error(c, HS_E_ARG, "block_update: k out of range");
   const int nb = grid_for(c, n);
   double2* part = (double2*)scratch(c, (size_t)nb * sizeof(double2), 2);
@@ -173,7 +207,8 @@ int krylov_block_update(Ctx* c, const double2* V, int64_t ldv, int k, const doub
   ProfScope ps(c, K_KRYLOV_UPDATE, 16.0 * (k + 2) * (double)n);
   switch (k) {
 #define HS_CASE(KK) \
-  case KK: k_block_update<KK><<<nb, kThreads, 0, c->stream>>>(V, ldv, h, w, n, part); break;
+  case KK: k_block_update<KK><<<nb, kThreads, 0, c->stream>>>(V, ldv, h, w, n, part, gate); \
+    break;
     HS_CASE(0) HS_CASE(1) HS_CASE(2) HS_CASE(3) HS_CASE(4) HS_CASE(5) HS_CASE(6) HS_CASE(7)
     HS_CASE(8) HS_CASE(9) HS_CASE(10) HS_CASE(11) HS_CASE(12) HS_CASE(13) HS_CASE(14)
     HS_CASE(15) HS_CASE(16) HS_CASE(17) HS_CASE(18) HS_CASE(19) HS_CASE(20) HS_CASE(21)
@@ -182,7 +217,7 @@ int krylov_block_update(Ctx* c, const double2* V, int64_t ldv, int k, const doub
 #undef HS_CASE
   }
   HS_LAUNCH_CHECK(c, "block_update");
-  k_reduce_parts<<<1, kThreads, 0, c->stream>>>(part, nb, 1, nrm2);
+  k_reduce_parts<<<1, kThreads, 0, c->stream>>>(part, nb, 1, nrm2, gate, 1);
   HS_LAUNCH_CHECK(c, "reduce");
   return HS_OK;
 }
@@ -213,6 +248,13 @@ int krylov_scale(Ctx* c, double2* x, int64_t n, double2 a) {
   return HS_OK;
 }
 
+int krylov_scale_inv_sqrt(Ctx* c, double2* x, int64_t n, const double2* s) {
+  ProfScope ps(c, K_KRYLOV_OTHER, 32.0 * (double)n);
+  k_scale_inv_sqrt<<<grid_for(c, n), kThreads, 0, c->stream>>>(x, n, s);
+  HS_LAUNCH_CHECK(c, "scale_inv_sqrt");
+  return HS_OK;
+}
+
 int krylov_axpby(Ctx* c, double2 a, const double2* x, double2 b, double2* y, int64_t n) {
   ProfScope ps(c, K_KRYLOV_OTHER, 48.0 * (double)n);
   k_axpby<<<grid_for(c, n), kThreads, 0, c->stream>>>(a, x, b, y, n);
@@ -227,7 +269,7 @@ int krylov_norm2(Ctx* c, const double2* x, int64_t n, double2* out) {
   ProfScope ps(c, K_KRYLOV_OTHER, 16.0 * (double)n);
   k_norm2<<<nb, kThreads, 0, c->stream>>>(x, n, part);
   HS_LAUNCH_CHECK(c, "norm2");
-  k_reduce_parts<<<1, kThreads, 0, c->stream>>>(part, nb, 1, out);
+  k_reduce_parts<<<1, kThreads, 0, c->stream>>>(part, nb, 1, out, Gate{nullptr, nullptr, 0.0}, 0);
   HS_LAUNCH_CHECK(c, "reduce");
   return HS_OK;
 }

@@ -212,6 +212,15 @@ class DeviceCycle(_Handle):
         self.ctx.call("hs_vcycle", self.h, ptr(f_dev), ptr(u))
         return u
 
+    def apply_a_begin(self, f_dev):
+        """First half of w = A M f (pre-smoothing, residual, restriction)."""
+        self.ctx.call("hs_vcycle_apply_a_begin", self.h, ptr(f_dev))
+
+    def apply_a_end(self, f_dev, w):
+        """Second half (sweep, prolongation, post-smoothing, fine matvec) into w."""
+        self.ctx.call("hs_vcycle_apply_a_end", self.h, ptr(f_dev), ptr(w))
+        return w
+
     def apply_a_dev(self, f_dev, out=None):
         w = out if out is not None else empty(self.n, self.ctx)
         self.ctx.call("hs_vcycle_apply_a", self.h, ptr(f_dev), ptr(w))

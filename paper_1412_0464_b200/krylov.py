@@ -135,30 +135,158 @@ class _Basis:
         return self.V[i]
 
 
-def _dot_pass(ctx, basis, k, w, n, hbuf):
-    """hbuf[0:k] = V[0:k]^H w ; returns ||w||^2 slot index (written at hbuf[k])."""
+def _dot_pass(ctx, basis, k, w, n, hbuf, gate=None):
+    """hbuf[0:k] = V[0:k]^H w, ||w||^2 at hbuf[k].  ``gate = (after, before)``:
+    run only when after.re < DGKS^2 * before.re (decided on the device)."""
     lda = basis.V.stride(0)
     done = 0
     while True:
         kk = min(_KCHUNK, k - done)
         # the chunk writes kk dots then ||w||^2 at hbuf[done + kk]
-        ctx.call("hs_block_dot", ptr(basis.V[done]) if kk else ptr(w), lda, kk, ptr(w), n,
-                 ptr(hbuf[done:]))
+        vp = ptr(basis.V[done]) if kk else ptr(w)
+        if gate is None:
+            ctx.call("hs_block_dot", vp, lda, kk, ptr(w), n, ptr(hbuf[done:]))
+        else:
+            ctx.call("hs_block_dot_gated", vp, lda, kk, ptr(w), n, ptr(hbuf[done:]),
+                     ptr(gate[0]), ptr(gate[1]), _DGKS ** 2)
         done += kk
         if done >= k:
             return
 
 
-def _update_pass(ctx, basis, k, h, w, n, nbuf):
+def _update_pass(ctx, basis, k, h, w, n, nbuf, gate=None):
+    """w -= V[0:k] h, ||w||^2 into nbuf[0] (a closed gate copies gate[0] there)."""
     lda = basis.V.stride(0)
     done = 0
     while True:
         kk = min(_KCHUNK, k - done)
-        ctx.call("hs_block_update", ptr(basis.V[done]) if kk else ptr(w), lda, kk,
-                 ptr(h[done:]), ptr(w), n, ptr(nbuf))
+        vp = ptr(basis.V[done]) if kk else ptr(w)
+        if gate is None:
+            ctx.call("hs_block_update", vp, lda, kk, ptr(h[done:]), ptr(w), n, ptr(nbuf))
+        else:
+            ctx.call("hs_block_update_gated", vp, lda, kk, ptr(h[done:]), ptr(w), n, ptr(nbuf),
+                     ptr(gate[0]), ptr(gate[1]), _DGKS ** 2)
         done += kk
         if done >= k:
             return
+
+
+def _givens_column(hess, cs, sn, g, k):
+    """Apply the previous rotations to column k, form rotation k, update g
+    (krylov.py:74-88)."""
+    for i in range(k):
+        t = cs[i] * hess[i, k] + sn[i] * hess[i + 1, k]
+        hess[i + 1, k] = -np.conj(sn[i]) * hess[i, k] + np.conj(cs[i]) * hess[i + 1, k]
+        hess[i, k] = t
+    denom = np.sqrt(abs(hess[k, k]) ** 2 + abs(hess[k + 1, k]) ** 2)
+    if denom == 0.0:
+        cs[k], sn[k] = 1.0, 0.0
+    else:
+        cs[k] = np.conj(hess[k, k]) / denom
+        sn[k] = np.conj(hess[k + 1, k]) / denom
+    hess[k, k] = cs[k] * hess[k, k] + sn[k] * hess[k + 1, k]
+    hess[k + 1, k] = 0.0
+    g[k + 1] = -np.conj(sn[k]) * g[k]
+    g[k] = cs[k] * g[k]
+
+
+def _basis_update(ctx, basis, hess, g, k, n, dev):
+    """dv = sum_i y_i v_i with y = H[:k,:k]^-1 g[:k] (krylov.py:96-101)."""
+    import torch
+    y = np.linalg.solve(hess[:k, :k], g[:k])
+    yd = torch.from_numpy(np.ascontiguousarray(y)).to(dev)
+    upd = empty(n, ctx)
+    done = 0
+    while done < k:
+        kk = min(_KCHUNK, k - done)
+        part = upd if done == 0 else empty(n, ctx)
+        ctx.call("hs_lincomb", ptr(basis.row(done)), basis.V.stride(0), kk, ptr(yd[done:]),
+                 ptr(part), n)
+        if done:
+            ctx.call("hs_axpby", 1.0, 0.0, ptr(part), 1.0, 0.0, ptr(upd), n)
+        done += kk
+    return upd
+
+
+def _gmres_cycle_pipelined(ops: _Ops, basis: _Basis, r0, r0_norm, bnorm, tol, max_steps,
+                           history):
+    """CGS2 Arnoldi cycle for this package's TGSP operator with the host one
+    step behind the device.  Everything the next step needs is decided on the
+    device (the DGKS second pass is gated there, v_{k+1} = w / ||w|| is scaled
+    there), so while the host reads Hessenberg column k and applies the
+    Givens rotations, the first half of A M v_{k+1} is already queued.  The
+    arithmetic is the synchronous cycle's, operation for operation; a
+    converged cycle discards one queued half V-cycle."""
+    import torch
+    ctx, n = ops.ctx, ops.n
+    cyc = ops.cycle
+    dev = torch.device(f"cuda:{ctx.device}")
+    hess = np.zeros((max_steps + 1, max_steps), dtype=complex)
+    cs = np.zeros(max_steps, dtype=complex)
+    sn = np.zeros(max_steps, dtype=complex)
+    beta = r0_norm
+    basis.ensure(max_steps + 1)
+    v0 = basis.row(0)
+    v0.copy_(r0)
+    ctx.call("hs_scale", ptr(v0), n, 1.0 / beta, 0.0)
+    g = np.zeros(max_steps + 1, dtype=complex)
+    g[0] = beta
+    W = max_steps + 2
+    col = torch.zeros(2 * W + 2, dtype=torch.complex128, device=dev)
+    hb, h2b, nb = col[:W], col[W:2 * W], col[2 * W:]
+    pin = torch.empty((max_steps, 2 * W + 2), dtype=torch.complex128, pin_memory=True)
+    stream = torch.cuda.current_stream(dev)
+    events = [torch.cuda.Event() for _ in range(max_steps)]
+
+    def orthonormalise(k):
+        w = basis.row(k + 1)
+        _dot_pass(ctx, basis, k + 1, w, n, hb)
+        _update_pass(ctx, basis, k + 1, hb, w, n, nb[0:])
+        gate = (nb[0:], hb[k + 1:])
+        _dot_pass(ctx, basis, k + 1, w, n, h2b, gate)
+        _update_pass(ctx, basis, k + 1, h2b, w, n, nb[1:], gate)
+        ctx.call("hs_scale_inv_sqrt", ptr(w), n, ptr(nb[1:]))
+        pin[k].copy_(col, non_blocking=True)
+        events[k].record(stream)
+
+    cyc.apply_a_begin(basis.row(0))
+    cyc.apply_a_end(basis.row(0), basis.row(1))
+    orthonormalise(0)
+    k = 0
+    converged = False
+    for k in range(max_steps):
+        ahead = k + 1 < max_steps
+        if ahead:
+            cyc.apply_a_begin(basis.row(k + 1))
+        events[k].synchronize()
+        host = pin[k].numpy()
+        hcol, w_norm0, nrm1 = host[:k + 1].copy(), host[k + 1].real, host[2 * W].real
+        if not math.isfinite(w_norm0):
+            raise FloatingPointError("operator produced non-finite values "
+                                     f"at iteration {len(history)}")
+        if nrm1 < (_DGKS ** 2) * w_norm0:          # the device ran the DGKS pass
+            hcol = hcol + host[W:W + k + 1]
+        nrm2 = host[2 * W + 1].real
+        if not (math.isfinite(nrm2) and np.all(np.isfinite(hcol))):
+            raise FloatingPointError("operator produced non-finite values "
+                                     f"at iteration {len(history)}")
+        hess[:k + 1, k] = hcol
+        hess[k + 1, k] = math.sqrt(max(nrm2, 0.0))
+        happy = hess[k + 1, k].real <= 1e-14 * beta
+        _givens_column(hess, cs, sn, g, k)
+        history.append(abs(g[k + 1]) / bnorm)
+        if history[-1] <= tol or happy:
+            converged = True
+            k += 1
+            break
+        if ahead:
+            cyc.apply_a_end(basis.row(k + 1), basis.row(k + 2))
+            orthonormalise(k + 1)
+    else:
+        k += 1
+    if k == 0:
+        return None, converged
+    return _basis_update(ctx, basis, hess, g, k, n, dev), converged
 
 
 def _gmres_cycle(ops: _Ops, basis: _Basis, r0, r0_norm, bnorm, tol, max_steps, history, orth):
@@ -215,20 +343,7 @@ def _gmres_cycle(ops: _Ops, basis: _Basis, r0, r0_norm, bnorm, tol, max_steps, h
         happy = hess[k + 1, k].real <= 1e-14 * beta
         if not happy:
             ctx.call("hs_scale", ptr(w), n, 1.0 / hess[k + 1, k].real, 0.0)
-        for i in range(k):
-            t = cs[i] * hess[i, k] + sn[i] * hess[i + 1, k]
-            hess[i + 1, k] = -np.conj(sn[i]) * hess[i, k] + np.conj(cs[i]) * hess[i + 1, k]
-            hess[i, k] = t
-        denom = np.sqrt(abs(hess[k, k]) ** 2 + abs(hess[k + 1, k]) ** 2)
-        if denom == 0.0:
-            cs[k], sn[k] = 1.0, 0.0
-        else:
-            cs[k] = np.conj(hess[k, k]) / denom
-            sn[k] = np.conj(hess[k + 1, k]) / denom
-        hess[k, k] = cs[k] * hess[k, k] + sn[k] * hess[k + 1, k]
-        hess[k + 1, k] = 0.0
-        g[k + 1] = -np.conj(sn[k]) * g[k]
-        g[k] = cs[k] * g[k]
+        _givens_column(hess, cs, sn, g, k)
         history.append(abs(g[k + 1]) / bnorm)
         if history[-1] <= tol or happy:
             converged = True
@@ -238,19 +353,7 @@ def _gmres_cycle(ops: _Ops, basis: _Basis, r0, r0_norm, bnorm, tol, max_steps, h
         k += 1
     if k == 0:
         return None, converged
-    y = np.linalg.solve(hess[:k, :k], g[:k])
-    yd = torch.from_numpy(np.ascontiguousarray(y)).to(dev)
-    upd = empty(n, ctx)
-    done = 0
-    while done < k:
-        kk = min(_KCHUNK, k - done)
-        part = upd if done == 0 else empty(n, ctx)
-        ctx.call("hs_lincomb", ptr(basis.row(done)), basis.V.stride(0), kk, ptr(yd[done:]),
-                 ptr(part), n)
-        if done:
-            ctx.call("hs_axpby", 1.0, 0.0, ptr(part), 1.0, 0.0, ptr(upd), n)
-        done += kk
-    return upd, converged
+    return _basis_update(ctx, basis, hess, g, k, n, dev), converged
 
 
 def _norm(ctx, x, n):
@@ -261,11 +364,14 @@ def _norm(ctx, x, n):
     return math.sqrt(max(v.real, 0.0)), v.imag
 
 
-def gmres(apply_a, apply_m, f, config: GmresConfig | None = None, orth: str = "cgs2"):
+def gmres(apply_a, apply_m, f, config: GmresConfig | None = None, orth: str = "cgs2",
+          pipelined: bool = True):
     """Solve A u = f with right preconditioning (GMRES on A M v = f, u = M v).
 
     ``f`` numpy -> ``u`` numpy; ``f`` torch CUDA -> ``u`` torch.  Stops on
     the true relative residual between restarts, like the reference.
+    ``pipelined`` (CGS2 with this package's TGSP operator): the host trails
+    the device by one Arnoldi step; same arithmetic as the synchronous loop.
     """
     if config is None:
         config = GmresConfig()
@@ -294,8 +400,12 @@ def gmres(apply_a, apply_m, f, config: GmresConfig | None = None, orth: str = "c
         steps = config.max_iter - (len(history) - 1)
         if config.restart is not None:
             steps = min(steps, config.restart)
-        dv, converged = _gmres_cycle(ops, basis, res, res_norm, bnorm, config.tol, steps,
-                                     history, orth)
+        if pipelined and orth == "cgs2" and ops.cycle is not None:
+            dv, converged = _gmres_cycle_pipelined(ops, basis, res, res_norm, bnorm,
+                                                   config.tol, steps, history)
+        else:
+            dv, converged = _gmres_cycle(ops, basis, res, res_norm, bnorm, config.tol, steps,
+                                         history, orth)
         if dv is not None:
             mdv = ops.apply_m(dv)
             ctx.call("hs_axpby", 1.0, 0.0, ptr(mdv), 1.0, 0.0, ptr(u), n)

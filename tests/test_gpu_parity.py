@@ -204,3 +204,20 @@ def test_gmres_small_known_answers(rng):
     assert rep.iterations == 0 and rep.converged
     with pytest.raises(FloatingPointError):
         hb.gmres(lambda v: v * float("nan"), None, b)
+
+
+@pytest.mark.parametrize("name", ["wedge2d", "pml3d"])
+def test_gmres_pipelined_matches_synchronous(name):
+    """The pipelined Arnoldi loop (device-gated DGKS pass, device-side
+    normalisation, host one step behind) does the synchronous loop's
+    arithmetic: identical histories and bitwise-identical solutions, across
+    restarts (restart 5) and with the final-step discard."""
+    import paper_1412_0464_b200 as hb
+    cycle = _build(name)
+    f = point_rhs(case(name)[0]).ravel()
+    cfg = hb.GmresConfig(tol=1e-6, max_iter=200, restart=5)
+    u1, r1 = hb.gmres(cycle.fine_csr, cycle.as_preconditioner(), f, cfg, pipelined=True)
+    u0, r0 = hb.gmres(cycle.fine_csr, cycle.as_preconditioner(), f, cfg, pipelined=False)
+    assert r1.iterations == r0.iterations and r1.converged
+    assert np.array_equal(r1.residual_history, r0.residual_history)
+    assert np.array_equal(u1, u0)
