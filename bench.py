@@ -50,6 +50,11 @@ def parse():
                    help="GMRES iterations in the bounded CPU-oracle sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--orth", default="cgs2")
+    p.add_argument("--shard", action="store_true",
+                   help="one solve sharded along the sweep axis over the ranks (strong "
+                        "scaling; halos P2P, dots all-reduced, coarse level replicated)")
+    p.add_argument("--local-shards", type=int, default=0,
+                   help="with --shard on one process: G logical shards on one GPU")
     p.add_argument("--no-pipeline", action="store_true",
                    help="synchronous Arnoldi loop (A/B against the pipelined default)")
     return p.parse_args()
@@ -377,10 +382,85 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def run_sharded(args):
+    """--shard: the single right-hand side solve decomposed along the sweep
+    axis (paper_1412_0464_b200/shards.py).  Each rank owns a slab of fine
+    rows; value = fine DOF / max-over-ranks solve time (strong scaling)."""
+    import torch
+    world, rank, local = dist_info()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    import paper_1412_0464_b200 as hb
+    from paper_1412_0464_b200.configs import config
+    from paper_1412_0464_b200.shards import (CudaShardBackend, DistComm, LocalComm,
+                                             ShardedTGSP, plan_shards, scatter_rows)
+    p = config(args.config, args.scale)
+    t0 = time.perf_counter()
+    hh = hb.build_hierarchy(p.mesh, p.model, None, hb.SmootherConfig(p.omega_jac, p.nu),
+                            hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains),
+                            keep_slab_ops=False)
+    G = world if world > 1 else max(1, args.local_shards)
+    plans = plan_shards(hh.fine_op.shape, hh.cmap, G)
+    comm = DistComm(plans, rank) if world > 1 else LocalComm(plans)
+    be = CudaShardBackend(hh, plans, comm.local)
+    st = ShardedTGSP(plans, be, comm)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    fh = p.f[0]
+    f = {g: be.upload(g, scatter_rows(plans[g], fh)) for g in comm.local}
+    cfg = hb.GmresConfig(p.tol, p.max_iter, p.restart)
+    for _ in range(args.warmup):
+        st.gmres(f, cfg)
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = be.ctx.launches
+    reps = []
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            u, rep = st.gmres(f, cfg)
+            reps.append(rep)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = be.ctx.launches - launches0
+    ms = reduce_over_ranks(ev0.elapsed_time(ev1), world, "max")
+    # true residual of the sharded solution (owned rows gathered on rank 0)
+    resid = {g: be.zeros(g) for g in comm.local}
+    comm.exchange(u)
+    for g in comm.local:
+        be.residual(g, f[g], u[g], resid[g])
+    true_res = st.norm(resid) / st.norm(f)
+    if rank == 0:
+        line = {
+            "metric": "TGSP-GMRES fine DOF/s (solve to 1e-6 rel-res)",
+            "value": p.n_fine * args.steps / (ms / 1e3), "unit": "DOF/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "c128", "data": "synthetic",
+            "config": {"workload": workload_name(p), "fine_dof": p.n_fine,
+                       "parallelism": f"sweep-axis shards x{G}"
+                                      + (" (logical, one GPU)" if world == 1 else ""),
+                       "l2": "working set > L2; no flush"},
+            "iterations": int(np.median([r.iterations for r in reps])),
+            "true_residual": true_res, "setup_s": setup_s, "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.shard:
+        run_sharded(args)
     else:
         run_ours(args)
 

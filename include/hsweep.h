@@ -89,6 +89,16 @@ int hs_jacobi(hs_ctx* ctx, const hs_stencil* op, void* u, const void* f, double 
  * fp_len[dim]); refined_concat: per-axis refined_cell (length fp_len[a]-1). */
 int hs_transfer_create(hs_ctx* ctx, int dim, const int64_t* fp_len, const int64_t* fp_concat,
                        const uint8_t* refined_concat, hs_transfer** out);
+/* The same maps for one shard of an x-slab (sweep-axis) decomposition
+ * (SURVEY 8(e)): window = {fw_lo, fw_hi, cr_lo, cr_hi, fr_lo, fr_hi}, global
+ * 0-based indices on the sweep axis.  The fine buffers hold rows [fw_lo,
+ * fw_hi) (owned rows plus halo planes); hs_restrict computes coarse rows
+ * [cr_lo, cr_hi) into a full-size coarse vector (other rows untouched);
+ * hs_prolong_add computes fine rows [fr_lo, fr_hi) from a full-size coarse
+ * vector.  HS_E_SHAPE if a computed coarse row reads outside the window. */
+int hs_transfer_create_window(hs_ctx* ctx, int dim, const int64_t* fp_len,
+                              const int64_t* fp_concat, const uint8_t* refined_concat,
+                              const int64_t* window, hs_transfer** out);
 int hs_transfer_destroy(hs_ctx* ctx, hs_transfer* t);
 /* rc = scale * P^T r                         twogrid.py:154 (restrict: 89-93 with scale 1) */
 int hs_restrict(hs_ctx* ctx, const hs_transfer* t, const void* r_fine, void* rc, double scale,

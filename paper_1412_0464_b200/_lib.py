@@ -45,6 +45,8 @@ SIGNATURES = {
     "hs_jacobi": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, C.c_int, C.c_int, C.c_int]),
     "hs_transfer_create": (C.c_int, [_vp, C.c_int, _i64p, _i64p, C.POINTER(C.c_uint8),
                                      C.POINTER(_vp)]),
+    "hs_transfer_create_window": (C.c_int, [_vp, C.c_int, _i64p, _i64p, C.POINTER(C.c_uint8),
+                                            _i64p, C.POINTER(_vp)]),
     "hs_transfer_destroy": (C.c_int, [_vp, _vp]),
     "hs_restrict": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, C.c_int]),
     "hs_restrict_residual": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, C.c_double, C.c_int]),

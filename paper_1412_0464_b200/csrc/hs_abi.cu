@@ -327,6 +327,20 @@ int hs_transfer_create(hs_ctx* c, int dim, const int64_t* fp_len, const int64_t*
   return HS_OK;
 }
 
+int hs_transfer_create_window(hs_ctx* c, int dim, const int64_t* fp_len,
+                              const int64_t* fp_concat, const uint8_t* refined_concat,
+                              const int64_t* window, hs_transfer** out) {
+  if (!c || !out || !fp_len || !fp_concat || !refined_concat || !window) return HS_E_ARG;
+  Transfer* t = nullptr;
+  int r = transfer_create(c, dim, fp_len, fp_concat, refined_concat, &t, window);
+  if (r) return r;
+  hs_transfer* h = new hs_transfer();
+  static_cast<Transfer&>(*h) = *t;
+  delete t;
+  *out = h;
+  return HS_OK;
+}
+
 int hs_transfer_destroy(hs_ctx* c, hs_transfer* t) {
   (void)c;
   if (!t) return HS_OK;

@@ -22,15 +22,18 @@ constexpr int kThreads = 256;
 
 __global__ void k_restrict(TransferDesc t, const double2* __restrict__ r,
                            double2* __restrict__ rc, double scale) {
-  const int64_t I2 = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  if (I2 >= t.nc[2]) return;
+  const int64_t L2 = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (L2 >= t.cr_cnt[2]) return;
   const int64_t row = blockIdx.y;
-  const int64_t I1 = row % t.nc[1];
-  const int64_t I0 = row / t.nc[1];
-  const int64_t nf = t.nf[0] * t.nf[1] * t.nf[2];
+  const int64_t I0 = t.cr_lo[0] + row / t.cr_cnt[1];
+  const int64_t I1 = t.cr_lo[1] + row % t.cr_cnt[1];
+  const int64_t I2 = t.cr_lo[2] + L2;
+  const int64_t nf = t.fw_cnt[0] * t.fw_cnt[1] * t.fw_cnt[2];
   const int64_t ncn = t.nc[0] * t.nc[1] * t.nc[2];
   r += (int64_t)blockIdx.z * nf;
-  const int c0 = t.ctr[0][I0], c1 = t.ctr[1][I1], c2 = t.ctr[2][I2];
+  // fine centres, local to the window
+  const int64_t c0 = t.ctr[0][I0] - t.fw_lo[0], c1 = t.ctr[1][I1] - t.fw_lo[1],
+                c2 = t.ctr[2][I2] - t.fw_lo[2];
   double w0[3] = {t.wl[0][I0], 1.0, t.wr[0][I0]};
   double w1[3] = {t.wl[1][I1], 1.0, t.wr[1][I1]};
   double w2[3] = {t.wl[2][I2], 1.0, t.wr[2][I2]};
@@ -44,7 +47,7 @@ __global__ void k_restrict(TransferDesc t, const double2* __restrict__ r,
       if (w1[b] == 0.0) continue;
       const int64_t f1 = c1 + b - 1;
       const double w01 = w0[a] * w1[b];
-      const double2* rrow = r + (f0 * t.nf[1] + f1) * t.nf[2];
+      const double2* rrow = r + (f0 * t.fw_cnt[1] + f1) * t.fw_cnt[2];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         if (w2[c] == 0.0) continue;
@@ -60,15 +63,18 @@ __global__ void k_restrict(TransferDesc t, const double2* __restrict__ r,
 
 __global__ void k_prolong(TransferDesc t, const double2* __restrict__ uc,
                           double2* __restrict__ u, int accumulate) {
-  const int64_t f2 = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  if (f2 >= t.nf[2]) return;
+  const int64_t l2 = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (l2 >= t.fr_cnt[2]) return;
   const int64_t row = blockIdx.y;
-  const int64_t f1 = row % t.nf[1];
-  const int64_t f0 = row / t.nf[1];
-  const int64_t nf = t.nf[0] * t.nf[1] * t.nf[2];
+  const int64_t f0 = t.fr_lo[0] + row / t.fr_cnt[1];     // global fine indices
+  const int64_t f1 = t.fr_lo[1] + row % t.fr_cnt[1];
+  const int64_t f2 = t.fr_lo[2] + l2;
+  const int64_t nf = t.fw_cnt[0] * t.fw_cnt[1] * t.fw_cnt[2];
   const int64_t ncn = t.nc[0] * t.nc[1] * t.nc[2];
   uc += (int64_t)blockIdx.z * ncn;
-  const int64_t i = (int64_t)blockIdx.z * nf + (f0 * t.nf[1] + f1) * t.nf[2] + f2;
+  const int64_t i = (int64_t)blockIdx.z * nf +
+                    ((f0 - t.fw_lo[0]) * t.fw_cnt[1] + (f1 - t.fw_lo[1])) * t.fw_cnt[2] +
+                    (f2 - t.fw_lo[2]);
   double2 acc = czero();
 #pragma unroll
   for (int a = 0; a < 2; ++a) {
@@ -99,10 +105,14 @@ __global__ void k_prolong(TransferDesc t, const double2* __restrict__ uc,
 int transfer_restrict(Ctx* c, const Transfer* t, const double2* r, double2* rc, double scale,
                       int nrhs) {
   const TransferDesc& d = t->d;
-  dim3 grid((unsigned)((d.nc[2] + kThreads - 1) / kThreads), (unsigned)(d.nc[0] * d.nc[1]),
+  const int64_t rows = d.cr_cnt[0] * d.cr_cnt[1];
+  if (rows == 0 || d.cr_cnt[2] == 0) return HS_OK;
+  dim3 grid((unsigned)((d.cr_cnt[2] + kThreads - 1) / kThreads), (unsigned)rows,
             (unsigned)nrhs);
-  ProfScope ps(c, K_RESTRICT,
-               16.0 * nrhs * (double)(d.nf[0] * d.nf[1] * d.nf[2] + d.nc[0] * d.nc[1] * d.nc[2]));
+  const double ncomp = (double)rows * d.cr_cnt[2];
+  ProfScope ps(c, K_RESTRICT, 16.0 * nrhs * (double)(d.nf[0] * d.nf[1] * d.nf[2]) *
+                                  (ncomp / (double)(d.nc[0] * d.nc[1] * d.nc[2])) +
+                                  16.0 * nrhs * ncomp);
   k_restrict<<<grid, kThreads, 0, c->stream>>>(d, r, rc, scale);
   HS_LAUNCH_CHECK(c, "restrict kernel");
   return HS_OK;
@@ -111,11 +121,15 @@ int transfer_restrict(Ctx* c, const Transfer* t, const double2* r, double2* rc, 
 int transfer_prolong(Ctx* c, const Transfer* t, const double2* uc, double2* u, int accumulate,
                      int nrhs) {
   const TransferDesc& d = t->d;
-  dim3 grid((unsigned)((d.nf[2] + kThreads - 1) / kThreads), (unsigned)(d.nf[0] * d.nf[1]),
+  const int64_t rows = d.fr_cnt[0] * d.fr_cnt[1];
+  if (rows == 0 || d.fr_cnt[2] == 0) return HS_OK;
+  dim3 grid((unsigned)((d.fr_cnt[2] + kThreads - 1) / kThreads), (unsigned)rows,
             (unsigned)nrhs);
+  const double ncomp = (double)rows * d.fr_cnt[2];
   ProfScope ps(c, K_PROLONG,
-               16.0 * nrhs * (double)((accumulate ? 2 : 1) * d.nf[0] * d.nf[1] * d.nf[2] +
-                                      d.nc[0] * d.nc[1] * d.nc[2]));
+               16.0 * nrhs * ((accumulate ? 2 : 1) * ncomp +
+                              (double)(d.nc[0] * d.nc[1] * d.nc[2]) *
+                                  (ncomp / (double)(d.nf[0] * d.nf[1] * d.nf[2]))));
   k_prolong<<<grid, kThreads, 0, c->stream>>>(d, uc, u, accumulate);
   HS_LAUNCH_CHECK(c, "prolong kernel");
   return HS_OK;
@@ -123,7 +137,7 @@ int transfer_prolong(Ctx* c, const Transfer* t, const double2* uc, double2* u, i
 
 // Build the per-axis tables on the host and upload them in one buffer.
 int transfer_create(Ctx* c, int dim, const int64_t* fp_len, const int64_t* fp_concat,
-                    const uint8_t* refined_concat, Transfer** out) {
+                    const uint8_t* refined_concat, Transfer** out, const int64_t* window) {
   if (dim < 1 || dim > 3) return set_error(c, HS_E_SHAPE, "transfer dim must be 1..3");
   Transfer* t = new Transfer();
   t->dim = dim;
@@ -180,6 +194,36 @@ int transfer_create(Ctx* c, int dim, const int64_t* fp_len, const int64_t* fp_co
     }
     fpp += L;
     rp += L - 1;
+  }
+  // identity window, or the shard window on the sweep axis
+  for (int ca = 0; ca < 3; ++ca) {
+    t->d.fw_lo[ca] = t->d.cr_lo[ca] = t->d.fr_lo[ca] = 0;
+    t->d.fw_cnt[ca] = t->d.fr_cnt[ca] = t->d.nf[ca];
+    t->d.cr_cnt[ca] = t->d.nc[ca];
+  }
+  if (window) {
+    const int wa = 3 - dim;
+    const int64_t fw_lo = window[0], fw_hi = window[1], cr_lo = window[2], cr_hi = window[3],
+                  fr_lo = window[4], fr_hi = window[5];
+    const int64_t nf = t->d.nf[wa], nc = t->d.nc[wa];
+    bool ok = 0 <= fw_lo && fw_lo <= fw_hi && fw_hi <= nf && 0 <= cr_lo && cr_lo <= cr_hi &&
+              cr_hi <= nc && fw_lo <= fr_lo && fr_lo <= fr_hi && fr_hi <= fw_hi;
+    // every fine row a computed coarse row reads must lie inside the window
+    for (int64_t I = cr_lo; ok && I < cr_hi; ++I) {
+      const int64_t lo = ctr[wa][I] - (wl[wa][I] != 0.0), hi = ctr[wa][I] + (wr[wa][I] != 0.0);
+      ok = lo >= fw_lo && hi < fw_hi;
+    }
+    if (!ok) {
+      delete t;
+      return set_error(c, HS_E_SHAPE, "transfer window does not cover the restriction stencil "
+                                      "of its coarse rows (shard map)");
+    }
+    t->d.fw_lo[wa] = fw_lo;
+    t->d.fw_cnt[wa] = fw_hi - fw_lo;
+    t->d.cr_lo[wa] = cr_lo;
+    t->d.cr_cnt[wa] = cr_hi - cr_lo;
+    t->d.fr_lo[wa] = fr_lo;
+    t->d.fr_cnt[wa] = fr_hi - fr_lo;
   }
   // pack: ints then doubles
   size_t ni = 0, nd = 0;

@@ -126,7 +126,9 @@ class DeviceTransfer(_Handle):
 
     _destroy = "hs_transfer_destroy"
 
-    def __init__(self, cmap, ctx=None):
+    def __init__(self, cmap, ctx=None, window=None):
+        """``window``: (fw_lo, fw_hi, cr_lo, cr_hi, fr_lo, fr_hi) on axis 0 for
+        one shard of a sweep-axis decomposition (hs_transfer_create_window)."""
         self.ctx = ctx or context()
         fps = [np.asarray(f, dtype=np.int64) for f in cmap.fine_point_of_coarse]
         refs = [np.asarray(r, dtype=np.uint8) for r in cmap.refined_cell]
@@ -138,8 +140,13 @@ class DeviceTransfer(_Handle):
         cat, pcat = i64(np.concatenate(fps))
         rc = np.ascontiguousarray(np.concatenate(refs), dtype=np.uint8)
         h = C.c_void_p()
-        self.ctx.call("hs_transfer_create", len(fps), plen, pcat,
-                      rc.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(h))
+        if window is None:
+            self.ctx.call("hs_transfer_create", len(fps), plen, pcat,
+                          rc.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(h))
+        else:
+            win, pwin = i64(window)
+            self.ctx.call("hs_transfer_create_window", len(fps), plen, pcat,
+                          rc.ctypes.data_as(C.POINTER(C.c_uint8)), pwin, C.byref(h))
         self.h = h
 
     def restrict(self, r, scale=1.0):
