@@ -55,6 +55,8 @@ def parse():
                         "scaling; halos P2P, dots all-reduced, coarse level replicated)")
     p.add_argument("--local-shards", type=int, default=0,
                    help="with --shard on one process: G logical shards on one GPU")
+    p.add_argument("--lanes", type=int, default=4,
+                   help="multi-RHS configs (C4): right-hand sides in flight at once per GPU")
     p.add_argument("--no-pipeline", action="store_true",
                    help="synchronous Arnoldi loop (A/B against the pipelined default)")
     return p.parse_args()
@@ -263,11 +265,20 @@ def run_ours(args):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     launches0 = ctx.launches
+    multi = len(f_dev) > 1 and args.lanes > 1
+
+    def step(fs):
+        if multi:
+            return hb.solve_many(cycle, fs, cfg, lanes=args.lanes, orth=args.orth)
+        return [solve(fd) for fd in fs]
+
+    if multi:
+        for _ in range(args.warmup):
+            step(f_dev)
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            for fd in f_dev:
-                u, rep = solve(fd)
+            for u, rep in step(f_dev):
                 reports.append(rep)
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -300,6 +311,9 @@ def run_ours(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
+        if multi:
+            step(f_host)
+            continue
         for fh in f_host:
             u_out, _ = hb.gmres(cycle.fine_csr, prec, fh, cfg, orth=args.orth,
                                 pipelined=not args.no_pipeline)
@@ -360,6 +374,7 @@ def run_ours(args):
             "config": {"workload": workload_name(p), "fine_dof": p.n_fine,
                        "coarse_dof": int(np.prod(cycle.coarse_op.shape)),
                        "subdomains": p.subdomains, "rhs_per_rank": len(f_dev),
+                       "rhs_in_flight": min(args.lanes, len(f_dev)) if multi else 1,
                        "parallelism": "replicas" if world > 1 else "single",
                        "l2": f"working set > L2 (slab factors {fac_gb:.2f} GB + basis + operators "
                              f"stream every step); no flush"},

@@ -132,6 +132,12 @@ long long hs_sweep_factor_bytes(hs_sweep* s);
 int hs_cycle_create(hs_ctx* ctx, const hs_stencil* fine, const hs_transfer* t,
                     const hs_stencil* coarse, hs_sweep* sweep, double omega_jac, int nu,
                     double restrict_scale, int variant, hs_cycle** out);
+/* A lane of `base`: the same operators, transfer maps and factorised sweep,
+ * with private cycle and sweep scratch, so applications of the two cycles on
+ * two contexts / streams run concurrently (several right-hand sides in
+ * flight on one GPU; each 2-D sweep front occupies one 16-SM cluster).
+ * 2-D levels only (the 3-D slab solve is a cooperative all-SM kernel). */
+int hs_cycle_create_lane(hs_ctx* ctx, const hs_cycle* base, hs_cycle** out);
 int hs_cycle_destroy(hs_ctx* ctx, hs_cycle* c);
 /* u = M f : vcycle / tgsp_apply / as_preconditioner   twogrid.py:150-176 */
 int hs_vcycle(hs_ctx* ctx, hs_cycle* c, const void* f, void* u);

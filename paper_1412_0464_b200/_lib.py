@@ -58,6 +58,7 @@ SIGNATURES = {
     "hs_sweep_factor_bytes": (C.c_longlong, [_vp]),
     "hs_cycle_create": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_double, C.c_int, C.c_double,
                                   C.c_int, C.POINTER(_vp)]),
+    "hs_cycle_create_lane": (C.c_int, [_vp, _vp, C.POINTER(_vp)]),
     "hs_cycle_destroy": (C.c_int, [_vp, _vp]),
     "hs_vcycle": (C.c_int, [_vp, _vp, _vp, _vp]),
     "hs_vcycle_apply_a": (C.c_int, [_vp, _vp, _vp, _vp]),

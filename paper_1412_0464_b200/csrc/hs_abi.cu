@@ -93,6 +93,8 @@ struct Cycle {
   double2* uc = nullptr;   // coarse solution
   double2* r = nullptr;    // fine residual scratch
   double2* tmp = nullptr;  // fine M f for apply_a
+  SweepWork work{};        // lane-private sweep scratch (null: the sweep's own)
+  bool lane = false;
 };
 
 // First half of the cycle: pre-smoothing from zero, residual, restriction
@@ -114,7 +116,9 @@ static int vcycle_begin(Ctx* c, Cycle* cy, const double2* f, double2* u) {
 // Second half: coarse sweep, prolongation + correction, post-smoothing.
 static int vcycle_end(Ctx* c, Cycle* cy, const double2* f, double2* u) {
   int r;
-  if ((r = sweep_apply(c, cy->sweep, cy->variant, cy->rc, cy->uc))) return r;   // coarse solve
+  if ((r = sweep_apply(c, cy->sweep, cy->variant, cy->rc, cy->uc,
+                       cy->lane ? &cy->work : nullptr)))
+    return r;                                                                    // coarse solve
   if ((r = transfer_prolong(c, cy->t, cy->uc, u, 1, 1))) return r;             // u += P uc
   if (cy->nu > 0) r = stencil_jacobi(c, cy->fine, u, f, cy->omega, cy->nu, 0, 1);
   return r;
@@ -438,10 +442,41 @@ int hs_cycle_create(hs_ctx* c, const hs_stencil* fine, const hs_transfer* t,
   return HS_OK;
 }
 
+int hs_cycle_create_lane(hs_ctx* c, const hs_cycle* base, hs_cycle** out) {
+  if (!c || !base || !out) return HS_E_ARG;
+  hs_cycle* cy = new hs_cycle();
+  cy->fine = base->fine;
+  cy->t = base->t;
+  cy->coarse = base->coarse;
+  cy->sweep = base->sweep;
+  cy->omega = base->omega;
+  cy->nu = base->nu;
+  cy->scale = base->scale;
+  cy->variant = base->variant;
+  cy->lane = true;
+  if (int r = sweep_work_create(c, cy->sweep, &cy->work)) {
+    delete cy;
+    return r;
+  }
+  cudaError_t e = cudaMalloc((void**)&cy->rc, cy->coarse->d.n * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&cy->uc, cy->coarse->d.n * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&cy->r, cy->fine->d.n * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&cy->tmp, cy->fine->d.n * sizeof(double2));
+  if (e != cudaSuccess) {
+    cudaFree(cy->rc); cudaFree(cy->uc); cudaFree(cy->r); cudaFree(cy->tmp);
+    sweep_work_destroy(&cy->work);
+    delete cy;
+    return check_cuda(c, e, "cycle lane buffers");
+  }
+  *out = cy;
+  return HS_OK;
+}
+
 int hs_cycle_destroy(hs_ctx* c, hs_cycle* cy) {
   (void)c;
   if (!cy) return HS_OK;
   cudaFree(cy->rc); cudaFree(cy->uc); cudaFree(cy->r); cudaFree(cy->tmp);
+  if (cy->lane) sweep_work_destroy(&cy->work);
   delete cy;
   return HS_OK;
 }

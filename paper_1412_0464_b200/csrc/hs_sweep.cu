@@ -1899,6 +1899,8 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     s->M = (int)(coarse->shape[1] * coarse->shape[2]);
     s->coarse = coarse;
     const int ntin = build_schedule(s, J, beta, bt, lo, hi);
+    s->ntrace = ntin;
+  s->ntrace = ntin;
     int r = sweep3_create(c, s, coarse, slabs, lo, hi);
     if (!r) r = buffers(s, ntin);
     if (!r)   // algorithmic bytes per launch: both factor blocks of every plane + rhs/u/traces
@@ -2010,6 +2012,7 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   cudaError_t e = cudaSuccess;
 
   const int ntin = build_schedule(s, J, beta, bt, lo, hi);
+  s->ntrace = ntin;
   std::vector<SweepTask>& T = s->tasks;
 
   // ---- rows of each slab's solution the chain ever reads (outputs, traces):
@@ -2135,7 +2138,31 @@ void sweep_destroy(Sweep* s) {
   delete s;
 }
 
-int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u) {
+int sweep_work_create(Ctx* c, const Sweep* s, SweepWork* w) {
+  if (s->s3) return set_error(c, HS_E_ARG, "sweep lanes need a 2-D level (the 3-D solve uses every SM)");
+  *w = SweepWork{};
+  const size_t nf = (size_t)s->n0 * s->M * sizeof(double2);
+  cudaError_t e = cudaMalloc((void**)&w->trace, (size_t)std::max(1, s->ntrace) * 2 * s->M * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&w->g, nf);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&w->u2, nf);
+  if (e != cudaSuccess) {
+    sweep_work_destroy(w);
+    return check_cuda(c, e, "sweep work buffers");
+  }
+  return HS_OK;
+}
+
+void sweep_work_destroy(SweepWork* w) {
+  cudaFree(w->trace);
+  cudaFree(w->g);
+  cudaFree(w->u2);
+  *w = SweepWork{};
+}
+
+int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
+                const SweepWork* w) {
+  const SweepWork own{s->trace, s->g, s->u2};
+  if (!w) w = &own;
   if (variant < 0 || variant > 1 || !s->has_plan[variant])
     return set_error(c, HS_E_ARG,
                      variant == HS_VARIANT_X ? "X-sweep needs an even subdomain count"
@@ -2147,18 +2174,19 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u) {
         // u = u_pass1 + u_pass2 (the order of the reference's u[ta:tb] += ud)
         const int64_t n = (int64_t)s->n0 * M;
         ProfScope ps(c, K_SWEEP_GATHER, 48.0 * n);
-        k_combine<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(u, s->u2, n);
+        k_combine<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(u, w->u2, n);
         HS_LAUNCH_CHECK(c, "combine kernel");
         break;
       }
       case SweepLaunch::kResidual: {
-        int r = stencil_apply(c, s->coarse, u, s->g, 1, f);
+        int r = stencil_apply(c, s->coarse, u, w->g, 1, f);
         if (r) return r;
         break;
       }
       case SweepLaunch::kSolve: {
         if (s->s3) {   // 3-D: the fronts' slab solves in order (host-driven block LU)
           ProfScope ps(c, K_SWEEP_FRONT, Lh.bytes);
+          if (w->g != s->g) return set_error(c, HS_E_ARG, "sweep lanes need a 2-D level");
           double2* us[2] = {u, s->u2};
           for (int fr = 0; fr < Lh.nfront; ++fr)
             for (int i = Lh.ffirst[fr]; i < Lh.ffirst[fr] + Lh.fcount[fr]; ++i)
@@ -2179,13 +2207,13 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u) {
         a.nbs = s->nbs;
         a.plan = s->ptab;
         a.rows = s->rows;
-        a.src = Lh.src ? s->g : f;
+        a.src = Lh.src ? w->g : f;
         a.coarse = s->coarse->d.coeffs;
         a.ncoarse = s->coarse->d.n;
         if (int r = slot_table(s->coarse, a.cslot, c)) return r;
-        a.trace = s->trace;
+        a.trace = w->trace;
         a.u[0] = u;
-        a.u[1] = s->u2;
+        a.u[1] = w->u2;
         static const char* trace_path = getenv("HS_SWEEP_TRACE");
         static bool traced = false;
         unsigned long long* dbg = nullptr;

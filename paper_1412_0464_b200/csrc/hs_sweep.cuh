@@ -27,6 +27,15 @@ struct SweepLaunch {
 
 struct Sweep3;   // 3-D levels (hs_sweep3.cu)
 
+// Per-application scratch of a sweep: traces, mid-sweep residual, pass-2
+// contributions.  The Sweep owns one; a cycle lane owns another so that
+// applications on different streams can run concurrently (2-D levels).
+struct SweepWork {
+  double2* trace = nullptr;     // [ntrace][2][M]
+  double2* g = nullptr;         // [n0*M]
+  double2* u2 = nullptr;        // [n0*M]
+};
+
 // Partitioned slab factors of every slab (see hs_sweep.cu).
 struct Sweep {
   int J = 0, M = 0, n0 = 0;
@@ -59,13 +68,18 @@ struct Sweep {
   std::vector<SweepLaunch> plan[2];   // by variant (UD, X)
   bool has_plan[2] = {false, false};
   long long factor_bytes = 0;
+  int ntrace = 0;               // trace buffers of the schedules
   Sweep3* s3 = nullptr;         // 3-D level: block LU slabs, host-driven tasks
 };
 
 int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, const int64_t* bt,
                  const int64_t* lo, const int64_t* hi, const Stencil* const* slabs, Sweep** out);
 void sweep_destroy(Sweep* s);
-int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u);
+int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
+                const SweepWork* w = nullptr);
+// allocate / free a SweepWork sized for s (2-D levels only)
+int sweep_work_create(Ctx* c, const Sweep* s, SweepWork* w);
+void sweep_work_destroy(SweepWork* w);
 
 int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const* slabs,
                   const int64_t* lo, const int64_t* hi);

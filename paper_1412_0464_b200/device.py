@@ -214,6 +214,20 @@ class DeviceCycle(_Handle):
                       float(omega_jac), int(nu), float(restrict_scale), v, C.byref(h))
         self.h = h
 
+    def lane(self, ctx):
+        """A lane of this cycle on another context (hs_cycle_create_lane):
+        shared operators and factors, private scratch."""
+        ln = DeviceCycle.__new__(DeviceCycle)
+        ln.ctx = ctx
+        ln.fine, ln.transfer, ln.coarse, ln.sweep = self.fine, self.transfer, self.coarse, \
+            self.sweep
+        ln.base = self            # keeps the shared handles alive
+        ln.n = self.n
+        h = C.c_void_p()
+        ctx.call("hs_cycle_create_lane", self.h, C.byref(h))
+        ln.h = h
+        return ln
+
     def vcycle_dev(self, f_dev, out=None):
         u = out if out is not None else empty(self.n, self.ctx)
         self.ctx.call("hs_vcycle", self.h, ptr(f_dev), ptr(u))

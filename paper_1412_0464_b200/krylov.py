@@ -71,8 +71,9 @@ class _Ops:
         if isinstance(apply_a, FineOperator):
             self.fine = apply_a.op.device()
         cyc = getattr(apply_m, "cycle", None)
+        lane = getattr(apply_m, "lane", None)
         if cyc is not None and self.fine is not None and cyc.fine_op is apply_a.op:
-            self.cycle = cyc.device()
+            self.cycle = lane.dev if lane is not None else cyc.device()
 
     def _call(self, fn, v):
         out = fn(v)
@@ -377,7 +378,8 @@ def gmres(apply_a, apply_m, f, config: GmresConfig | None = None, orth: str = "c
         config = GmresConfig()
     if orth not in ("cgs2", "mgs"):
         raise ValueError(f"orth must be 'cgs2' or 'mgs', got {orth!r}")
-    ctx = context()
+    lane = getattr(apply_m, "lane", None)
+    ctx = lane.ctx if lane is not None else context()
     t0 = time.perf_counter()
     ft, was_np = to_device(f, None, ctx)
     n = ft.numel()

@@ -189,17 +189,90 @@ class TwoGridCycle:
             return from_device(u, True, self.fine_op.shape)
         return u.reshape(f.shape)
 
-    def as_preconditioner(self):
+    def as_preconditioner(self, lane=None):
+        """The flat-vector preconditioner callable (twogrid.py:161-164);
+        ``lane``: run on a :class:`Lane` (its own context and stream)."""
         dev_cycle = self
+        the_lane = lane
 
         class _Prec:
             cycle = dev_cycle
+            lane = the_lane
 
             def __call__(self, v):
                 out = dev_cycle.vcycle(v)
                 return out.reshape(-1)
 
         return _Prec()
+
+    def lanes(self, n: int):
+        """``n`` lanes of this cycle for right-hand sides in flight at once on
+        one GPU (2-D levels): each has its own library context, CUDA stream
+        and cycle/sweep scratch and shares the operators and slab factors."""
+        return [Lane(self) for _ in range(n)]
+
+
+class Lane:
+    """One right-hand side in flight: a private libhsweep context bound to its
+    own CUDA stream and a lane of the cycle's device handle."""
+
+    def __init__(self, cycle: TwoGridCycle):
+        import torch
+        from ._lib import Context
+        base = cycle.device()
+        self.cycle = cycle
+        self.stream = torch.cuda.Stream(device=base.ctx.device)
+        self.ctx = Context(base.ctx.device)
+        with torch.cuda.stream(self.stream):
+            self.ctx.bind_stream()
+            self.dev = base.lane(self.ctx)
+
+    def preconditioner(self):
+        return self.cycle.as_preconditioner(lane=self)
+
+
+def solve_many(cycle: TwoGridCycle, rhs, config=None, lanes: int = 4, orth: str = "cgs2"):
+    """Independent GMRES solves of several right-hand sides (C4's sources),
+    ``lanes`` of them in flight at once on one GPU (one host thread and one
+    CUDA stream per lane; the sweeps of different lanes run on disjoint
+    clusters).  Stream-ordered with the caller: the lanes start after the
+    caller's current stream and the caller's stream waits for all of them.
+    Returns [(u, SolveReport)] in input order."""
+    import concurrent.futures as cf
+    import threading
+    import torch
+    from .krylov import gmres
+    rhs = list(rhs)
+    if not rhs:
+        return []
+    pool = getattr(cycle, "_lanes", [])
+    want = max(1, min(lanes, len(rhs)))
+    if len(pool) < want:
+        pool = pool + cycle.lanes(want - len(pool))
+        cycle._lanes = pool
+    pool = pool[:want]
+    main = torch.cuda.current_stream(pool[0].ctx.device)
+    start = torch.cuda.Event()
+    start.record(main)
+    free = list(pool)
+    lock = threading.Lock()
+
+    def one(f):
+        with lock:
+            ln = free.pop()
+        try:
+            with torch.cuda.stream(ln.stream):
+                ln.stream.wait_event(start)
+                return gmres(cycle.fine_csr, ln.preconditioner(), f, config, orth=orth)
+        finally:
+            with lock:
+                free.append(ln)
+
+    with cf.ThreadPoolExecutor(max_workers=len(pool)) as ex:
+        out = list(ex.map(one, rhs))
+    for ln in pool:
+        main.wait_stream(ln.stream)
+    return out
 
 
 def vcycle(cycle: TwoGridCycle, f):
