@@ -57,6 +57,7 @@ def parse():
                    help="with --shard on one process: G logical shards on one GPU")
     p.add_argument("--lanes", type=int, default=4,
                    help="multi-RHS configs (C4): right-hand sides in flight at once per GPU")
+    p.add_argument("--clock-sampler", choices=["smi", "nvml", "none"], default="smi")
     p.add_argument("--no-pipeline", action="store_true",
                    help="synchronous Arnoldi loop (A/B against the pipelined default)")
     return p.parse_args()
@@ -105,24 +106,49 @@ def peaks():
 
 
 class ClockSampler:
-    """Samples SM clocks and throttle reasons (NVML) while the timed region runs."""
+    """SM clocks and throttle reasons sampled DURING the timed region by a
+    separate ``nvidia-smi -lms 200`` process (the profiling recipe's clocks
+    line).  In-process NVML polling was measured to stall the launching
+    thread (driver lock) and is only the fallback; ``mode="none"`` skips."""
 
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
     REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
                0x2: "applications_clocks_setting", 0x10: "sync_boost"}
 
-    def __init__(self, device_index):
+    def __init__(self, device_index, mode="smi"):
+        self.idx, self.mode = device_index, mode
         self.samples, self.reasons = [], set()
         self.max_mhz = None
+        self.proc = None
+        self.nv = None
         self._stop = threading.Event()
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-        except Exception:
-            self.nv = None
+
+    def __enter__(self):
+        import shutil
+        import subprocess
+        import tempfile
+        if self.mode == "smi" and shutil.which("nvidia-smi"):
+            self.out = tempfile.TemporaryFile(mode="w+")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.out, stderr=subprocess.DEVNULL)
+        elif self.mode in ("smi", "nvml"):
+            try:
+                import pynvml
+                pynvml.nvmlInit()
+                self.nv = pynvml
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+                self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+                self.t = threading.Thread(target=self._run, daemon=True)
+                self.t.start()
+            except Exception:
+                self.nv = None
+        return self
 
     def _run(self):
         while not self._stop.is_set():
@@ -134,24 +160,36 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            self._stop.wait(0.1)
-
-    def __enter__(self):
-        if self.nv:
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
-        return self
+            self._stop.wait(0.2)
 
     def __exit__(self, *a):
         self._stop.set()
         if self.nv:
             self.t.join()
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+            self.out.seek(0)
+            for line in self.out.read().splitlines():
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 6:
+                    continue
+                try:
+                    self.samples.append(float(f[0]))
+                    self.max_mhz = float(f[1])
+                except ValueError:
+                    continue
+                for name, v in zip(self.NAMES, f[2:6]):
+                    if v.lower() == "active":
+                        self.reasons.add(name)
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz,
+                    "reasons": ["unavailable" if self.mode != "none" else "not sampled"]}
         return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "sampler": "nvidia-smi -lms 200" if self.proc is not None else "nvml"}
 
 
 def workload_name(p):
@@ -275,7 +313,7 @@ def run_ours(args):
     if multi:
         for _ in range(args.warmup):
             step(f_dev)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, args.clock_sampler) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
             for u, rep in step(f_dev):
@@ -435,7 +473,7 @@ def run_sharded(args):
     torch.cuda.synchronize()
     launches0 = be.ctx.launches
     reps = []
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, args.clock_sampler) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
             u, rep = st.gmres(f, cfg)

@@ -72,6 +72,39 @@ int hs_profile_read(hs_ctx* ctx, int nclass, double* ms, double* bytes, long lon
 int hs_stencil_create(hs_ctx* ctx, int dim, const int64_t* shape, int S,
                       const int8_t* offsets, const double* coeffs, hs_stencil** out);
 int hs_stencil_destroy(hs_ctx* ctx, hs_stencil* op);
+/* copy the S x prod(shape) coefficients back to host memory (synchronises) */
+int hs_stencil_download(hs_ctx* ctx, const hs_stencil* op, double* coeffs);
+
+/* ---- operator assembly on the device -----------------
+ * The per-axis 1-D arrays come from the host (numpy, the reference's own
+ * expressions); every per-node product runs on the device in numpy's
+ * operation order and lands in the [S][n] layout, 1/diagonal included.
+ * Complex arrays are interleaved (re, im) doubles, per-axis arrays
+ * concatenated over the axes.
+ *
+ * Fine FD operator, _fd_operator / assemble_fine / assemble_sponge
+ * (discretize.py:191-253): a_half[a] (N_a = shape[a]+1 complex, alpha at cell
+ * midpoints), a_node[a] (N_a - 1 complex, alpha at the unknowns),
+ * gamma_nodes[a] (N_a - 1 real sponge damping, or NULL for (k + 0i)^2),
+ * k_dev: device float64 wavenumbers at the unknowns.  2*dim+1 offsets. */
+int hs_assemble_fd(hs_ctx* ctx, int dim, const int64_t* shape, double h, const double* a_half,
+                   const double* a_node, const double* gamma_nodes, const void* k_dev,
+                   hs_stencil** out);
+/* FE operator with the optimized-table weights, _fe_operator with per-cell
+ * wavenumbers (discretize.py:413-506; coarse level :514-537, slabs :685-723):
+ * per axis (N_a = shape[a]+1 cells) woa = widths/alpha, aow = alpha/widths,
+ * cw = widths*(1/alpha) (complex), gamma_cells (real, or NULL).  k_nodes_dev /
+ * k_cells_dev: the GLOBAL level's float64 fields, rows of kn_ld / kc_ld
+ * elements; rowmap = {nrow0, nlo, nhi, crow0, clo, chi}: local sweep-axis row
+ * r reads global node row clamp(nrow0 + r, nlo, nhi) and cell row
+ * clamp(crow0 + r, clo, chi) (a slab's replicated edge rows).  Table:
+ * ntab abscissae (1/G) and ntab x ncoef weights; h_ref the table's spacing.
+ * 3^dim offsets in itertools.product order. */
+int hs_assemble_fe(hs_ctx* ctx, int dim, const int64_t* shape, const double* woa,
+                   const double* aow, const double* cw, const double* gamma_cells,
+                   const void* k_nodes_dev, int64_t kn_ld, const void* k_cells_dev,
+                   int64_t kc_ld, const int32_t* rowmap, double h_ref, int ntab, int ncoef,
+                   const double* tab_x, const double* tab_c, hs_stencil** out);
 /* y = A x            stencil_apply / fine_csr @ v   discretize.py:110-117, twogrid.py:140-141 */
 int hs_stencil_apply(hs_ctx* ctx, const hs_stencil* op, const void* x, void* y, int nrhs);
 /* r = f - A u        the residual lines twogrid.py:153, sweepdd.py:343 */
@@ -151,6 +184,10 @@ int hs_vcycle_apply_a(hs_ctx* ctx, hs_cycle* c, const void* f, void* w);
  * cycle handle may be in flight. */
 int hs_vcycle_apply_a_begin(hs_ctx* ctx, hs_cycle* c, const void* f);
 int hs_vcycle_apply_a_end(hs_ctx* ctx, hs_cycle* c, const void* f, void* w);
+/* Finer split for a deeper host pipeline: part 0 = begin; part 1 = the
+ * sweep's first launch (X: both pass-1 fronts, prec_x sweepdd.py:331-341);
+ * part 2 = the rest of end (w written here).  0, 1, 2 in order == begin+end. */
+int hs_vcycle_apply_a_part(hs_ctx* ctx, hs_cycle* c, const void* f, void* w, int part);
 
 /* ---- GMRES vector kernels (krylov.py:46-102) ------------------------------
  * V: device basis, k vectors of length n with leading dimension ldv (elements).

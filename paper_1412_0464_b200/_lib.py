@@ -40,6 +40,15 @@ SIGNATURES = {
     "hs_stencil_create": (C.c_int, [_vp, C.c_int, _i64p, C.c_int, C.POINTER(C.c_int8),
                                     C.POINTER(C.c_double), C.POINTER(_vp)]),
     "hs_stencil_destroy": (C.c_int, [_vp, _vp]),
+    "hs_stencil_download": (C.c_int, [_vp, _vp, C.POINTER(C.c_double)]),
+    "hs_assemble_fd": (C.c_int, [_vp, C.c_int, _i64p, C.c_double, C.POINTER(C.c_double),
+                                 C.POINTER(C.c_double), C.POINTER(C.c_double), _vp,
+                                 C.POINTER(_vp)]),
+    "hs_assemble_fe": (C.c_int, [_vp, C.c_int, _i64p, C.POINTER(C.c_double),
+                                 C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                 C.POINTER(C.c_double), _vp, C.c_int64, _vp, C.c_int64,
+                                 C.POINTER(C.c_int32), C.c_double, C.c_int, C.c_int,
+                                 C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(_vp)]),
     "hs_stencil_apply": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int]),
     "hs_stencil_residual": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int]),
     "hs_jacobi": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, C.c_int, C.c_int, C.c_int]),
@@ -64,6 +73,7 @@ SIGNATURES = {
     "hs_vcycle_apply_a": (C.c_int, [_vp, _vp, _vp, _vp]),
     "hs_vcycle_apply_a_begin": (C.c_int, [_vp, _vp, _vp]),
     "hs_vcycle_apply_a_end": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "hs_vcycle_apply_a_part": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int]),
     "hs_block_dot": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, _vp, C.c_int64, _vp]),
     "hs_block_dot_gated": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, _vp, C.c_int64, _vp, _vp,
                                      _vp, C.c_double]),

@@ -113,11 +113,12 @@ static int vcycle_begin(Ctx* c, Cycle* cy, const double2* f, double2* u) {
   return transfer_restrict(c, cy->t, cy->r, cy->rc, cy->scale, 1);             // h^d P^T r
 }
 
-// Second half: coarse sweep, prolongation + correction, post-smoothing.
-static int vcycle_end(Ctx* c, Cycle* cy, const double2* f, double2* u) {
+// Second half: coarse sweep (plan launches [sweep_first, end)), prolongation
+// + correction, post-smoothing.
+static int vcycle_end(Ctx* c, Cycle* cy, const double2* f, double2* u, int sweep_first = 0) {
   int r;
   if ((r = sweep_apply(c, cy->sweep, cy->variant, cy->rc, cy->uc,
-                       cy->lane ? &cy->work : nullptr)))
+                       cy->lane ? &cy->work : nullptr, sweep_first)))
     return r;                                                                    // coarse solve
   if ((r = transfer_prolong(c, cy->t, cy->uc, u, 1, 1))) return r;             // u += P uc
   if (cy->nu > 0) r = stencil_jacobi(c, cy->fine, u, f, cy->omega, cy->nu, 0, 1);
@@ -129,12 +130,45 @@ static int vcycle(Ctx* c, Cycle* cy, const double2* f, double2* u) {
   return r ? r : vcycle_end(c, cy, f, u);
 }
 
+// Stencil descriptor from (dim, shape, offsets); coefficients not touched.
+int stencil_init_desc(Ctx* c, int dim, const int64_t* shape, int S, const int8_t* offsets,
+                      Stencil* op) {
+  if (dim < 1 || dim > 3) return set_error(c, HS_E_SHAPE, "stencil dim must be 1, 2 or 3");
+  if (S < 1 || S > kMaxOffsets) return set_error(c, HS_E_SHAPE, "stencil needs 1..27 offsets");
+  op->dim = dim;
+  int64_t n = 1;
+  for (int a = 0; a < dim; ++a) {
+    if (shape[a] < 1) return set_error(c, HS_E_SHAPE, "empty stencil shape");
+    op->shape[a] = shape[a];
+    n *= shape[a];
+  }
+  int64_t cs[3] = {1, 1, 1};
+  for (int a = 0; a < dim; ++a) cs[3 - dim + a] = shape[a];
+  op->d.n0 = cs[0];
+  op->d.n1 = cs[1];
+  op->d.n2 = cs[2];
+  op->d.n = n;
+  op->d.S = S;
+  op->d.diag = -1;
+  for (int s = 0; s < S; ++s) {
+    int8_t o[3] = {0, 0, 0};
+    bool zero = true;
+    for (int a = 0; a < dim; ++a) {
+      const int8_t v = offsets[s * dim + a];
+      if (v < -1 || v > 1) return set_error(c, HS_E_SHAPE, "offset breaks the compact-stencil contract");
+      o[3 - dim + a] = v;
+      zero = zero && v == 0;
+    }
+    for (int a = 0; a < 3; ++a) op->d.off[s][a] = o[a];
+    if (zero) op->d.diag = s;
+  }
+  return HS_OK;
+}
+
 }  // namespace hs
 
 using namespace hs;
 
-struct hs_ctx : Ctx {};
-struct hs_stencil : Stencil {};
 struct hs_transfer : Transfer {};
 struct hs_sweep : Sweep {};
 struct hs_cycle : Cycle {};
@@ -216,37 +250,12 @@ int hs_synchronize(hs_ctx* c) {
 int hs_stencil_create(hs_ctx* c, int dim, const int64_t* shape, int S, const int8_t* offsets,
                       const double* coeffs, hs_stencil** out) {
   if (!c || !out || !shape || !offsets || !coeffs) return HS_E_ARG;
-  if (dim < 1 || dim > 3) return set_error(c, HS_E_SHAPE, "stencil dim must be 1, 2 or 3");
-  if (S < 1 || S > kMaxOffsets)
-    return set_error(c, HS_E_SHAPE, "stencil needs 1..27 offsets");
   hs_stencil* op = new hs_stencil();
-  op->dim = dim;
-  int64_t n = 1;
-  for (int a = 0; a < dim; ++a) {
-    if (shape[a] < 1) { delete op; return set_error(c, HS_E_SHAPE, "empty stencil shape"); }
-    op->shape[a] = shape[a];
-    n *= shape[a];
+  if (int r = stencil_init_desc(c, dim, shape, S, offsets, op)) {
+    delete op;
+    return r;
   }
-  int64_t cs[3] = {1, 1, 1};
-  for (int a = 0; a < dim; ++a) cs[3 - dim + a] = shape[a];
-  op->d.n0 = cs[0];
-  op->d.n1 = cs[1];
-  op->d.n2 = cs[2];
-  op->d.n = n;
-  op->d.S = S;
-  op->d.diag = -1;
-  for (int s = 0; s < S; ++s) {
-    int8_t o[3] = {0, 0, 0};
-    bool zero = true;
-    for (int a = 0; a < dim; ++a) {
-      const int8_t v = offsets[s * dim + a];
-      if (v < -1 || v > 1) { delete op; return set_error(c, HS_E_SHAPE, "offset breaks the compact-stencil contract"); }
-      o[3 - dim + a] = v;
-      zero = zero && v == 0;
-    }
-    for (int a = 0; a < 3; ++a) op->d.off[s][a] = o[a];
-    if (zero) op->d.diag = s;
-  }
+  const int64_t n = op->d.n;
   // zero-diagonal scan (jacobi_smooth's ZeroDivisionError, twogrid.py:43-46)
   if (op->d.diag >= 0) {
     const double* dg = coeffs + (size_t)2 * n * op->d.diag;
@@ -288,6 +297,14 @@ int hs_stencil_create(hs_ctx* c, int dim, const int64_t* shape, int S, const int
     op->d.invd = op->invd;
   }
   *out = op;
+  return HS_OK;
+}
+
+int hs_stencil_download(hs_ctx* c, const hs_stencil* op, double* coeffs) {
+  if (!c || !op || !coeffs) return HS_E_ARG;
+  HS_CUDA(c, cudaStreamSynchronize(c->stream), "download sync");
+  HS_CUDA(c, cudaMemcpy(coeffs, op->coeffs, (size_t)op->d.S * op->d.n * sizeof(double2),
+                        cudaMemcpyDeviceToHost), "stencil download");
   return HS_OK;
 }
 
@@ -496,6 +513,24 @@ int hs_vcycle_apply_a(hs_ctx* c, hs_cycle* cy, const void* f, void* w) {
 int hs_vcycle_apply_a_begin(hs_ctx* c, hs_cycle* cy, const void* f) {
   if (!c || !cy || !f) return HS_E_ARG;
   return vcycle_begin(c, cy, (const double2*)f, cy->tmp);
+}
+
+int hs_vcycle_apply_a_part(hs_ctx* c, hs_cycle* cy, const void* f, void* w, int part) {
+  if (!c || !cy || !f || (part == 2 && !w)) return HS_E_ARG;
+  switch (part) {
+    case 0:
+      return vcycle_begin(c, cy, (const double2*)f, cy->tmp);
+    case 1:   // the sweep's first launch (X: both pass-1 fronts)
+      return sweep_apply(c, cy->sweep, cy->variant, cy->rc, cy->uc,
+                         cy->lane ? &cy->work : nullptr, 0, 1);
+    case 2: {
+      int r = vcycle_end(c, cy, (const double2*)f, cy->tmp, 1);
+      if (r) return r;
+      return stencil_apply(c, cy->fine, cy->tmp, (double2*)w, 1, nullptr);
+    }
+    default:
+      return set_error(c, HS_E_ARG, "apply_a part must be 0, 1 or 2");
+  }
 }
 
 int hs_vcycle_apply_a_end(hs_ctx* c, hs_cycle* cy, const void* f, void* w) {

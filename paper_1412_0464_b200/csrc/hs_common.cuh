@@ -154,6 +154,13 @@ struct Stencil {
   long long zero_diag_node = -1;
 };
 
+// descriptor from shape / offsets (hs_abi.cu); coefficients untouched
+int stencil_init_desc(Ctx* c, int dim, const int64_t* shape, int S, const int8_t* offsets,
+                      Stencil* op);
+// device-side completion of an operator whose coefficients were assembled on
+// the device: 1/diagonal and the first zero-diagonal node (hs_assemble.cu)
+int stencil_finish_device(Ctx* c, Stencil* op);
+
 // kernels (hs_stencil.cu)
 int stencil_apply(Ctx* c, const Stencil* op, const double2* x, double2* y, int nrhs,
                   const double2* f_minus /*if non-null: y = f - A x*/);
@@ -161,3 +168,8 @@ int stencil_jacobi(Ctx* c, const Stencil* op, double2* u, const double2* f, doub
                    int steps, int u_is_zero, int nrhs);
 
 }  // namespace hs
+
+// opaque C-ABI handle types of the context and of stencil operators (the
+// other handles are declared where their implementation lives)
+struct hs_ctx : hs::Ctx {};
+struct hs_stencil : hs::Stencil {};

@@ -1138,7 +1138,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     const uint32_t ce = ctab[c];
     const int nbk = (int)(ce & 0xff);
     *(volatile int*)&ccnt[sl] = 0;   // ordered before cseq (same thread, volatile)
-    const double2* sbase = a.stream + ((int64_t)slabs[ti] * C + rank) * a.nbs * TM2;
+    // (timing experiment bit 16: every task streams slab 0's data -> L2-resident)
+    const double2* sbase = a.stream + ((int64_t)((HS_SWEEP_EXP & 16) ? 0 : slabs[ti]) * C + rank) *
+                                          a.nbs * TM2;
     mbar_expect_tx(&cbar[sl], (HS_SWEEP_EXP & 2) ? 0u : (uint32_t)nbk * TM2 * 16);
     if (!(HS_SWEEP_EXP & 2))
       bulk_g2s(ring + (int64_t)sl * CHUNK, sbase + (int64_t)(ce >> 8) * TM2,
@@ -2160,7 +2162,7 @@ void sweep_work_destroy(SweepWork* w) {
 }
 
 int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
-                const SweepWork* w) {
+                const SweepWork* w, int first, int last) {
   const SweepWork own{s->trace, s->g, s->u2};
   if (!w) w = &own;
   if (variant < 0 || variant > 1 || !s->has_plan[variant])
@@ -2168,7 +2170,10 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
                      variant == HS_VARIANT_X ? "X-sweep needs an even subdomain count"
                                              : "unknown sweep variant");
   const int M = s->M;
-  for (const SweepLaunch& Lh : s->plan[variant]) {
+  const int np_ = (int)s->plan[variant].size();
+  if (last < 0 || last > np_) last = np_;
+  for (int li = std::max(0, first); li < last; ++li) {
+    const SweepLaunch& Lh = s->plan[variant][li];
     switch (Lh.kind) {
       case SweepLaunch::kCombine: {
         // u = u_pass1 + u_pass2 (the order of the reference's u[ta:tb] += ud)

@@ -75,8 +75,9 @@ struct Sweep {
 int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, const int64_t* bt,
                  const int64_t* lo, const int64_t* hi, const Stencil* const* slabs, Sweep** out);
 void sweep_destroy(Sweep* s);
+// launches [first, last) of the variant's plan (last < 0: to the end)
 int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
-                const SweepWork* w = nullptr);
+                const SweepWork* w = nullptr, int first = 0, int last = -1);
 // allocate / free a SweepWork sized for s (2-D levels only)
 int sweep_work_create(Ctx* c, const Sweep* s, SweepWork* w);
 void sweep_work_destroy(SweepWork* w);

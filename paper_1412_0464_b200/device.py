@@ -90,6 +90,24 @@ class DeviceStencil(_Handle):
         self.h = h
 
     @classmethod
+    def adopt(cls, h, shape, offsets, ctx):
+        """Wrap a handle created on the device (hs_assemble_*)."""
+        self = cls.__new__(cls)
+        self.ctx = ctx
+        self.shape = tuple(int(s) for s in shape)
+        self.n = int(np.prod(self.shape))
+        self.offsets = [tuple(int(v) for v in o) for o in offsets]
+        self.h = h
+        return self
+
+    def download(self) -> np.ndarray:
+        """[S][n] complex128 coefficients back on the host (synchronises)."""
+        out = np.empty((len(self.offsets), self.n), dtype=complex)
+        self.ctx.call("hs_stencil_download", self.h,
+                      out.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)))
+        return out
+
+    @classmethod
     def from_host(cls, op, ctx=None):
         offs = sorted(op.coeffs)
         return cls(op.shape, offs, np.stack([op.coeffs[o].reshape(-1) for o in offs]), ctx)
@@ -236,6 +254,12 @@ class DeviceCycle(_Handle):
     def apply_a_begin(self, f_dev):
         """First half of w = A M f (pre-smoothing, residual, restriction)."""
         self.ctx.call("hs_vcycle_apply_a_begin", self.h, ptr(f_dev))
+
+    def apply_a_part(self, f_dev, w, part):
+        """hs_vcycle_apply_a_part: 0 begin, 1 the sweep's first launch, 2 the rest (-> w)."""
+        self.ctx.call("hs_vcycle_apply_a_part", self.h, ptr(f_dev), ptr(w) if w is not None
+                      else None, int(part))
+        return w
 
     def apply_a_end(self, f_dev, w):
         """Second half (sweep, prolongation, post-smoothing, fine matvec) into w."""

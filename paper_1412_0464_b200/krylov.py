@@ -215,9 +215,10 @@ def _gmres_cycle_pipelined(ops: _Ops, basis: _Basis, r0, r0_norm, bnorm, tol, ma
     step behind the device.  Everything the next step needs is decided on the
     device (the DGKS second pass is gated there, v_{k+1} = w / ||w|| is scaled
     there), so while the host reads Hessenberg column k and applies the
-    Givens rotations, the first half of A M v_{k+1} is already queued.  The
-    arithmetic is the synchronous cycle's, operation for operation; a
-    converged cycle discards one queued half V-cycle."""
+    Givens rotations, A M v_{k+1} up to and including the sweep's first launch
+    (~1 ms of device work) is already queued.  The arithmetic is the
+    synchronous cycle's, operation for operation; a converged cycle discards
+    that queued part."""
     import torch
     ctx, n = ops.ctx, ops.n
     cyc = ops.cycle
@@ -257,8 +258,9 @@ def _gmres_cycle_pipelined(ops: _Ops, basis: _Basis, r0, r0_norm, bnorm, tol, ma
     converged = False
     for k in range(max_steps):
         ahead = k + 1 < max_steps
-        if ahead:
-            cyc.apply_a_begin(basis.row(k + 1))
+        if ahead:   # ~1 ms of the next step queued while the host trails
+            cyc.apply_a_part(basis.row(k + 1), None, 0)
+            cyc.apply_a_part(basis.row(k + 1), None, 1)
         events[k].synchronize()
         host = pin[k].numpy()
         hcol, w_norm0, nrm1 = host[:k + 1].copy(), host[k + 1].real, host[2 * W].real
@@ -281,7 +283,7 @@ def _gmres_cycle_pipelined(ops: _Ops, basis: _Basis, r0, r0_norm, bnorm, tol, ma
             k += 1
             break
         if ahead:
-            cyc.apply_a_end(basis.row(k + 1), basis.row(k + 2))
+            cyc.apply_a_part(basis.row(k + 1), basis.row(k + 2), 2)
             orthonormalise(k + 1)
     else:
         k += 1

@@ -37,7 +37,14 @@ class HelmholtzLevel:
     k_cells: np.ndarray | None = None
     table: object = None
 
+    fields: object = None   # device wavenumbers (assembly.CoarseFields): slabs assembled on the GPU
+
     def subdomain_operator(self, core_lo, core_hi, w_dd, s_dd, open_left, open_right):
+        if self.kind == "fe" and self.fields is not None and self.k_cells is not None:
+            from .assembly import subdomain_fe_operator_device
+            return subdomain_fe_operator_device(self.mesh, self.model, self.k_cells, self.table,
+                                                core_lo, core_hi, w_dd, s_dd, open_left,
+                                                open_right, self.fields)
         if self.kind == "fd":
             return subdomain_fd_operator(self.mesh, self.model, core_lo, core_hi, w_dd, s_dd,
                                          open_left, open_right)
@@ -169,8 +176,10 @@ class Partition:
         """Factorise every slab on the device (once) and return the handle."""
         if self._device is None:
             from .device import DeviceStencil, DeviceSweep
+            from .assembly import DeviceOperator
             coarse = self.level.op.device()
-            slab_ops = [DeviceStencil.from_host(sd.op, coarse.ctx) for sd in self.subs]
+            slab_ops = [sd.op.device() if isinstance(sd.op, DeviceOperator)
+                        else DeviceStencil.from_host(sd.op, coarse.ctx) for sd in self.subs]
             self._device = DeviceSweep(coarse, self.J, self.beta, self.beta_tilde,
                                        [sd.pt_lo for sd in self.subs],
                                        [sd.pt_hi for sd in self.subs], slab_ops, coarse.ctx)
@@ -179,6 +188,13 @@ class Partition:
 
     def apply_global(self, u):
         return self.level.op.apply(u)
+
+    @property
+    def csr(self):
+        """The level operator as ``apply_a`` (reference ``part.csr @ v``,
+        cli.py:248): a device matvec object, not a host CSR matrix."""
+        from .twogrid import FineOperator
+        return FineOperator(self.level.op)
 
 
 def partition_geometry(n1: int, J: int, tilde_right: bool = False):

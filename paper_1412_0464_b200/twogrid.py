@@ -313,13 +313,36 @@ class HostHierarchy:
 
 
 def build_hierarchy(mesh: Mesh, model: WaveModel, fine_op=None, smoother=None, sweep=None,
-                    table=None, device=True, keep_slab_ops=True) -> HostHierarchy:
-    """Host assembly of the TGSP hierarchy (reference twogrid.py:196-229)."""
+                    table=None, device=True, keep_slab_ops=True,
+                    assembly: str | None = None) -> HostHierarchy:
+    """Assembly of the TGSP hierarchy (reference twogrid.py:196-229).
+
+    ``assembly="device"`` (the default when ``device``): the fine FD operator,
+    the PML coarse FE operator and every slab operator are formed on the GPU
+    (:mod:`.assembly`); ``"host"``: numpy assembly (the oracle's inputs).  The
+    wavenumber transfers and the per-axis profiles stay on the host."""
+    if assembly is None:
+        assembly = "device" if device else "host"
+    if assembly not in ("device", "host"):
+        raise ValueError(f"assembly must be 'device' or 'host', got {assembly!r}")
+    on_gpu = assembly == "device"
+    if on_gpu and fine_op is None:
+        from .assembly import assemble_fine_device
+        fine_op = assemble_fine_device(mesh, model)
     flevel = fine_level(mesh, model, fine_op)
     mesh_c, cmap = coarsen_mesh(mesh)
     model_c = WaveModel(model.omega, coarsen_wavenumber(model.k, cmap))
     k_cells = wavenumber_cell_midpoints(model.k, cmap)
-    clevel = coarse_level(mesh_c, cmap, model_c, k_cells=k_cells, table=table)
+    has_pml = any(s.kind == "pml" for pair in mesh_c.layers for s in pair)
+    coarse_op, fields = None, None
+    if on_gpu and has_pml:
+        from .assembly import CoarseFields, assemble_fe_pml_coarse_device
+        from ._lib import context
+        fields = CoarseFields(model_c, k_cells, context())
+        coarse_op = assemble_fe_pml_coarse_device(mesh_c, cmap, model_c, k_cells, table,
+                                                  fields=fields)
+    clevel = coarse_level(mesh_c, cmap, model_c, op=coarse_op, k_cells=k_cells, table=table)
+    clevel.fields = fields
     if smoother is None:
         smoother = SmootherConfig(omega_jac=0.8 if mesh.dim == 2 else 0.6, nu=3)
     sweep = sweep or SweepOptions()
@@ -332,7 +355,8 @@ def build_hierarchy(mesh: Mesh, model: WaveModel, fine_op=None, smoother=None, s
 
 def build_two_grid(mesh: Mesh, model: WaveModel, fine_op: StencilOperator | None = None,
                    smoother: SmootherConfig | None = None, coarse: str = "exact",
-                   sweep: SweepOptions | None = None, table=None, keep_slab_ops=True):
+                   sweep: SweepOptions | None = None, table=None, keep_slab_ops=True,
+                   assembly: str = "device"):
     """Assemble the two-grid hierarchy; returns (cycle, coarse level).
 
     ``coarse="sweep"`` is the TGSP path (device).  ``coarse="exact"`` (a
@@ -346,7 +370,7 @@ def build_two_grid(mesh: Mesh, model: WaveModel, fine_op: StencilOperator | None
     if sweep.variant not in ("ud", "x"):
         raise ValueError(f"sweep variant {sweep.variant!r} is not implemented on the device")
     hh = build_hierarchy(mesh, model, fine_op, smoother, sweep, table,
-                         keep_slab_ops=keep_slab_ops)
+                         keep_slab_ops=keep_slab_ops, assembly=assembly)
     prec = SweepingPreconditioner(hh.partition, sweep.variant, parallel=sweep.parallel)
     cycle = TwoGridCycle(hh.fine_op, hh.coarse_op, hh.cmap, hh.smoother,
                          SweepCoarseSolver(prec), restrict_scale=hh.restrict_scale,

@@ -244,3 +244,52 @@ def test_solve_many_lanes_match_sequential():
         assert np.array_equal(u1, u0)
     with pytest.raises(ValueError, match="2-D"):
         _build("pml3d").lanes(1)
+
+
+def test_sweep_only_fine_level():
+    """The reference's sweep-only preconditioner (cli.py:245-252: fine_level ->
+    build_partition -> SweepingPreconditioner, GMRES on part.csr): 5-point FD
+    slabs with added PML through the same device sweep, vs the oracle."""
+    import paper_1412_0464_b200 as hb
+    from oracle import tgsp_oracle as orc
+    mesh, model = case("pml2d")[:2]
+    level = hb.fine_level(mesh, model)
+    part = hb.build_partition(level, 3, 15.0, J=8)
+    opart = orc.Partition(orc.Op.from_dict(level.op.coeffs), part.beta, part.beta_tilde,
+                          [orc.Slab(sd.pt_lo, sd.pt_hi, orc.Op.from_dict(sd.op.coeffs))
+                           for sd in part.subs])
+    z = crand(np.random.default_rng(3), level.op.shape)
+    assert rel(hb.prec_x(part, z), opart.prec_x(z)) < 1e-11
+    assert rel(hb.prec_ud(part, z), opart.prec_ud(z)) < 1e-11
+    f = point_rhs(mesh).ravel()
+    prec = hb.SweepingPreconditioner(part, "x")
+    u, rep = hb.gmres(part.csr, prec, f, hb.GmresConfig(1e-6, 200, 20))
+    _, its, _, _, _ = orc.gmres(lambda v: opart.op.csr @ v,
+                                lambda v: opart.prec_x(v.reshape(level.op.shape)).ravel(), f,
+                                tol=1e-6, max_iter=200, restart=20)
+    assert rep.converged and abs(rep.iterations - its) <= 1
+    assert np.linalg.norm(f - opart.op.csr @ u) / np.linalg.norm(f) <= 1e-6
+
+
+@pytest.mark.parametrize("name", ["pml2d", "wedge2d", "sponge2d", "pml3d", "pml3d_s"])
+def test_device_assembly_matches_host(name):
+    """GPU assembly (fine FD / sponge, PML coarse FE, every added-PML slab) vs
+    the host numpy assembly the oracle is pinned on: same offsets, coefficients
+    within 2 ulp-scale (1e-15 of the operator's largest entry)."""
+    import paper_1412_0464_b200 as hb
+    mesh, model, fine_op, sm, sw = case(name)
+    host = hb.build_hierarchy(mesh, model, fine_op, sm, sw, device=False)
+    dev = hb.build_hierarchy(mesh, model, fine_op, sm, sw, device=True, assembly="device")
+
+    def close(a, b):
+        assert sorted(a.coeffs) == sorted(b.coeffs)
+        scale = max(np.abs(c).max() for c in b.coeffs.values())
+        for o in b.coeffs:
+            assert np.abs(a.coeffs[o] - b.coeffs[o]).max() <= 1e-15 * scale, o
+
+    close(dev.fine_op, host.fine_op)
+    close(dev.coarse_op, host.coarse_op)
+    assert len(dev.slabs) == len(host.slabs)
+    for (lo, hi, op), (lo2, hi2, op2) in zip(dev.slabs, host.slabs):
+        assert (lo, hi) == (lo2, hi2)
+        close(op, op2)
