@@ -42,7 +42,13 @@ def to_device(x, n: int | None = None, ctx=None):
 
 def from_device(t, was_numpy: bool, shape=None):
     if was_numpy:
-        a = t.detach().cpu().numpy()
+        # DMA into pinned host memory (the numpy result keeps the buffer
+        # alive): a pageable .cpu() would stage through a bounce buffer
+        torch = _torch()
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t.detach(), non_blocking=True)
+        torch.cuda.current_stream(t.device).synchronize()
+        a = h.numpy()
         return a.reshape(shape) if shape is not None else a
     return t.reshape(shape) if shape is not None else t
 
