@@ -129,17 +129,42 @@ __global__ void k3_out(SweepTask t, int n1, int n2, const double2* __restrict__ 
 }
 
 // ---- the whole block recursion of one slab solve in one cooperative launch:
-// every CTA rebuilds the step's right-hand vector in shared memory, owns rows
-// (one warp per row, coalesced row-major blocks), and a grid barrier orders
-// the planes.  F: the rhs (read by every CTA while Y fills), Y: y, then x.
+// every CTA rebuilds the step's right-hand vector in shared memory and owns
+// rows r = blockIdx.x + k * gridDim.x of every plane's dense block.  Those
+// rows do not depend on the chain, so they are staged by TMA bulk copies
+// (one per row, completing on an mbarrier) into shared memory one plane
+// ahead: the copy of plane i+1's rows is issued as soon as plane i's GEMV
+// has read its buffer and lands while the CTA writes its rows, crosses the
+// grid barrier and rebuilds the next right-hand vector.  The GEMV then reads
+// shared memory only.  Grid barrier split into arrive / wait.
 constexpr int kW3 = 16;   // warps per CTA
 
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+__device__ __forceinline__ uint32_t s3_smem(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void s3_mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(s3_smem(bar)), "r"(phase)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void barrier_arrive(unsigned* bar) {
   __syncthreads();
   if (HS_S3_EXP & 4) return;
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(bar, 1u);
+  }
+}
+__device__ __forceinline__ void barrier_wait(unsigned* bar, unsigned target) {
+  if (!(HS_S3_EXP & 4) && threadIdx.x == 0) {
     unsigned v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar));
@@ -148,37 +173,45 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
   __syncthreads();
 }
 
-// This CTA's rows r = blockIdx.x + k * gridDim.x of A v (A row-major NB x NB,
-// v in shared memory): a row is split over wpr warps (4 loads in flight per
-// lane); partial sums land in acc[k][part] (summed in a fixed order by the
-// caller: bitwise reproducible).
-__device__ __forceinline__ int rows_wpr(int NB) {
-  const int rows = blockIdx.x < NB ? (NB - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  return max(1, kW3 / max(1, rows));
+// this CTA's rows of a plane matrix -> shared memory (thread 0; one bulk copy per row)
+__device__ __forceinline__ void stage_rows(const double2* __restrict__ A, int NB, int nrow,
+                                           double2* dst, uint64_t* bar) {
+  const uint32_t bytes = (uint32_t)NB * 16u;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s3_smem(bar)),
+               "r"(bytes * (uint32_t)nrow)
+               : "memory");
+  for (int k = 0; k < nrow; ++k) {
+    const double2* src = A + (int64_t)(blockIdx.x + k * gridDim.x) * NB;
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(s3_smem(dst + (int64_t)k * NB)), "l"(src), "r"(bytes), "r"(s3_smem(bar))
+        : "memory");
+  }
 }
-__device__ __forceinline__ void cta_rows(const double2* __restrict__ A, const double2* v, int NB,
+
+// rows k < nrow of (staged rows) x v: a row is split over wpr warps (4
+// independent partial sums per lane); partial sums land in acc[k][part],
+// summed in a fixed order by the caller: bitwise reproducible.
+__device__ __forceinline__ int rows_wpr(int nrow) { return max(1, kW3 / max(1, nrow)); }
+__device__ __forceinline__ void cta_rows(const double2* A, const double2* v, int NB, int nrow,
                                          double2* acc) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int b = blockIdx.x, g = gridDim.x;
-  const int rows = b < NB ? (NB - 1 - b) / g + 1 : 0;
-  if (rows == 0 || (HS_S3_EXP & 1)) return;
-  const int wpr = max(1, kW3 / rows);           // warps per row
+  if (nrow == 0 || (HS_S3_EXP & 1)) return;
+  const int wpr = rows_wpr(nrow);               // warps per row
   const int seg = (NB + wpr - 1) / wpr;
-  for (int k = warp / wpr; k < rows && warp / wpr < kW3 / wpr; k += kW3 / wpr) {
-    const int r = b + k * g, part = warp % wpr;
+  for (int k = warp / wpr; k < nrow && warp / wpr < kW3 / wpr; k += kW3 / wpr) {
+    const int part = warp % wpr;
     const int c0 = part * seg, c1 = min(NB, c0 + seg);
-    const double2* row = A + (int64_t)r * NB;
+    const double2* row = A + (int64_t)k * NB;
     double2 a0 = czero(), a1 = czero(), a2 = czero(), a3 = czero();
     int c = c0 + lane;
     for (; c + 96 < c1; c += 128) {
-      const double2 m0 = __ldg(row + c), m1 = __ldg(row + c + 32), m2 = __ldg(row + c + 64),
-                    m3 = __ldg(row + c + 96);
-      a0 = cfma(m0, v[c], a0);
-      a1 = cfma(m1, v[c + 32], a1);
-      a2 = cfma(m2, v[c + 64], a2);
-      a3 = cfma(m3, v[c + 96], a3);
+      a0 = cfma(row[c], v[c], a0);
+      a1 = cfma(row[c + 32], v[c + 32], a1);
+      a2 = cfma(row[c + 64], v[c + 64], a2);
+      a3 = cfma(row[c + 96], v[c + 96], a3);
     }
-    for (; c < c1; c += 32) a0 = cfma(__ldg(row + c), v[c], a0);
+    for (; c < c1; c += 32) a0 = cfma(row[c], v[c], a0);
     double2 t = cadd(cadd(a0, a1), cadd(a2, a3));
     for (int m = 16; m > 0; m >>= 1) t = cadd(t, shfl_xor_c(t, m));
     if (lane == 0) acc[k * wpr + part] = t;
@@ -189,22 +222,33 @@ __global__ void __launch_bounds__(kW3 * 32, 1)
 k3_solve(const double2* __restrict__ coef, Slots sl, int T, int n1, int n2,
          const double2* __restrict__ dinvT, const double2* __restrict__ xT,
          const double2* __restrict__ F, double2* Y, unsigned* bar) {
-  extern __shared__ double2 v3[];   // [NB] step vector, then [2 * rows] row sums
+  extern __shared__ __align__(128) double2 v3[];   // [NB] vector | [NB] y_{i-1} | rows | sums
   const int NB = T * n2;
   const int64_t nb2 = (int64_t)NB * NB, n = (int64_t)T * n1 * n2;
   const int nrow = blockIdx.x < NB ? (NB - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  double2* yp = v3 + NB;               // [NB] previous plane's y
-  double2* racc = yp + NB;             // [rows][warps per row] partial row sums
-  const int wpr = rows_wpr(NB);
+  const int rmax = (NB + gridDim.x - 1) / gridDim.x;
+  double2* yp = v3 + NB;                    // [NB] previous plane's y
+  double2* rows = yp + NB;                  // [rmax][NB] staged rows of the current plane
+  double2* racc = rows + (int64_t)rmax * NB;   // [rows][warps per row] partial row sums
+  uint64_t* rbar = (uint64_t*)(racc + rmax * kW3);
+  const int wpr = rows_wpr(nrow);
   auto row_sum = [&](int k) {
     double2 a = czero();
     for (int p = 0; p < wpr; ++p) a = cadd(a, racc[k * wpr + p]);
     return a;
   };
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s3_smem(rbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && nrow > 0) stage_rows(dinvT, NB, nrow, rows, rbar);
+  uint32_t ph = 0;
   unsigned epoch = 0;
   for (int i1 = 0; i1 < n1; ++i1) {   // y_i = Dinv_i (f_i - L_i y_{i-1})
     const double2* Fi = F + (int64_t)i1 * NB;
     double2* Yi = Y + (int64_t)i1 * NB;
+    if (i1 > 0) barrier_wait(bar, epoch * gridDim.x);
     if (i1 > 0 && !(HS_S3_EXP & 2)) {   // y_{i-1} into shared memory once (L2 reads)
       for (int r = threadIdx.x; r < NB; r += blockDim.x) yp[r] = __ldcg(Yi - NB + r);
       __syncthreads();
@@ -228,27 +272,40 @@ k3_solve(const double2* __restrict__ coef, Slots sl, int T, int n1, int n2,
       v3[r] = acc;
     }
     __syncthreads();
-    cta_rows(dinvT + i1 * nb2, v3, NB, racc);
-    __syncthreads();
+    if (nrow > 0) s3_mbar_wait(rbar, ph);
+    ph ^= 1;
+    cta_rows(rows, v3, NB, nrow, racc);
+    __syncthreads();   // staged rows consumed: refill with the next plane's
+    if (threadIdx.x == 0 && nrow > 0) {
+      if (i1 + 1 < n1) stage_rows(dinvT + (i1 + 1) * nb2, NB, nrow, rows, rbar);
+      else if (n1 >= 2) stage_rows(xT + (n1 - 2) * nb2, NB, nrow, rows, rbar);
+    }
     for (int k = threadIdx.x; k < nrow; k += blockDim.x) Yi[blockIdx.x + k * gridDim.x] = row_sum(k);
-    grid_barrier(bar, (++epoch) * gridDim.x);
+    barrier_arrive(bar);
+    ++epoch;
   }
   for (int i1 = n1 - 2; i1 >= 0; --i1) {   // x_i = y_i - X_i x_{i+1}
     double2* Yi = Y + (int64_t)i1 * NB;
+    barrier_wait(bar, epoch * gridDim.x);
     for (int r = threadIdx.x; r < NB; r += blockDim.x) v3[r] = __ldcg(Yi + NB + r);
     __syncthreads();
-    cta_rows(xT + i1 * nb2, v3, NB, racc);
+    if (nrow > 0) s3_mbar_wait(rbar, ph);
+    ph ^= 1;
+    cta_rows(rows, v3, NB, nrow, racc);
     __syncthreads();
+    if (threadIdx.x == 0 && nrow > 0 && i1 > 0) stage_rows(xT + (i1 - 1) * nb2, NB, nrow, rows, rbar);
     for (int k = threadIdx.x; k < nrow; k += blockDim.x) {
       const int r = blockIdx.x + k * gridDim.x;
       Yi[r] = csub(__ldcg(Yi + r), row_sum(k));
     }
-    grid_barrier(bar, (++epoch) * gridDim.x);
+    barrier_arrive(bar);
+    ++epoch;
   }
 }
 
 size_t k3_smem(int NB, int grid) {
-  return (size_t)2 * NB * sizeof(double2) + (size_t)(kW3 + (NB + grid - 1) / grid) * sizeof(double2);
+  const int rmax = (NB + grid - 1) / grid;
+  return (size_t)(2 * NB + (size_t)rmax * NB + (size_t)rmax * kW3) * sizeof(double2) + 16;
 }
 
 Slots to_slots(const std::array<int, 27>& a) {
