@@ -7,9 +7,11 @@
 // pivot blocks, cuBLAS ZGEMM for the Schur updates):
 //   D'_0 = D_0,  D'_i = D_i - L_i X_{i-1},  Dinv_i = D'_i^{-1},  X_i = Dinv_i U_i,
 // so a slab solve (subdom_solve's LU_j^{-1}, sweepdd.py:236-268) is
-//   y_i = Dinv_i (f_i - L_i y_{i-1})   (L_i applied from the stencil coefficients)
+//   y_i = Dinv_i (f_i - L_i y_{i-1}) = w_i - G_i y_{i-1},  w_i = Dinv_i f_i,  G_i = Dinv_i L_i
 //   x_i = y_i - X_i x_{i+1}.
-// Storage: 2 dense blocks per plane (C5: ~2.5 GB per slab, 71 GB in all).
+// w for every plane is one batched GEMV ahead of the chain (independent of
+// it); the chain is then one dense GEMV per plane in both directions.
+// Storage: 3 dense blocks per plane (C5: ~3 GB per slab, 86 GB in all).
 // Right-hand side (restriction rows + the 9-offset transmission terms of
 // TransmissionMatrix.apply, sweepdd.py:98-141) and the output scatter are
 // small kernels; the schedules (tasks, traces) are shared with the 2-D sweep.
@@ -33,7 +35,8 @@ namespace hs {
 struct Sweep3 {
   int n1 = 0, n2 = 0;
   std::vector<int> T;                  // slab thickness
-  std::vector<double2*> dinv, xf;      // per slab: [n1][NB^2], [n1-1][NB^2] (row-major)
+  std::vector<double2*> dinv, xf, gf;  // per slab: [n1][NB^2], [n1-1][NB^2], [n1][NB^2] (row-major;
+                                       // gf[0] unused: G_i = Dinv_i L_i for i >= 1)
   std::vector<double2*> coef;          // per slab: stencil coefficients [S][T n1 n2] (owned copy)
   std::vector<std::array<int, 27>> slot;   // per slab: (o0+1)*9 + (o1+1)*3 + (o2+1) -> slot
   std::array<int, 27> cslot{};         // coarse operator slots
@@ -42,6 +45,7 @@ struct Sweep3 {
   double2* Y = nullptr;                // [n1][NBmax] forward solution, then x
   unsigned* gbar = nullptr;            // grid barrier counter of the solve kernel
   int grid = 0;                        // CTAs of the solve kernel (one per SM)
+  int nbuf = 1;                        // staging buffers of the solve kernel
   long long bytes = 0;
 };
 
@@ -155,12 +159,19 @@ __device__ __forceinline__ void s3_mbar_wait(uint64_t* bar, uint32_t phase) {
   }
 }
 
+#ifndef HS_S3_RED
+#define HS_S3_RED 1
+#endif
 __device__ __forceinline__ void barrier_arrive(unsigned* bar) {
   __syncthreads();
   if (HS_S3_EXP & 4) return;
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
+    if (HS_S3_RED) {   // release-add: orders the CTA's writes (bar.sync + cumulativity)
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    } else {
+      __threadfence();
+      atomicAdd(bar, 1u);
+    }
   }
 }
 __device__ __forceinline__ void barrier_wait(unsigned* bar, unsigned target) {
@@ -189,9 +200,18 @@ __device__ __forceinline__ void stage_rows(const double2* __restrict__ A, int NB
   }
 }
 
+// rows k < nrow of (staged rows) x v: warp w owns the column segment
+// [w seg, (w+1) seg) of every row, so it reads its slice of v once (two
+// entries per lane, registers) and each staged row element once; partial
+// sums land in acc[k][w] and are summed in a fixed order by the caller
+// (bitwise reproducible).
+constexpr int kR3 = 8;   // rows per CTA at most (NB <= 8 * grid)
+
 // rows k < nrow of (staged rows) x v: a row is split over wpr warps (4
 // independent partial sums per lane); partial sums land in acc[k][part],
-// summed in a fixed order by the caller: bitwise reproducible.
+// summed in a fixed order by the caller: bitwise reproducible.  (A
+// column-segment variant -- each warp all rows of a slice of v -- measured
+// 12% slower at C5.)
 __device__ __forceinline__ int rows_wpr(int nrow) { return max(1, kW3 / max(1, nrow)); }
 __device__ __forceinline__ void cta_rows(const double2* A, const double2* v, int NB, int nrow,
                                          double2* acc) {
@@ -219,93 +239,64 @@ __device__ __forceinline__ void cta_rows(const double2* A, const double2* v, int
 }
 
 __global__ void __launch_bounds__(kW3 * 32, 1)
-k3_solve(const double2* __restrict__ coef, Slots sl, int T, int n1, int n2,
-         const double2* __restrict__ dinvT, const double2* __restrict__ xT,
-         const double2* __restrict__ F, double2* Y, unsigned* bar) {
-  extern __shared__ __align__(128) double2 v3[];   // [NB] vector | [NB] y_{i-1} | rows | sums
+k3_solve(int T, int n1, int n2, const double2* __restrict__ gT, const double2* __restrict__ xT,
+         double2* Y, unsigned* bar, int nbuf) {
+  extern __shared__ __align__(128) double2 v3[];   // [NB] vector | [nbuf][rmax][NB] rows | sums
   const int NB = T * n2;
-  const int64_t nb2 = (int64_t)NB * NB, n = (int64_t)T * n1 * n2;
+  const int64_t nb2 = (int64_t)NB * NB;
   const int nrow = blockIdx.x < NB ? (NB - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int rmax = (NB + gridDim.x - 1) / gridDim.x;
-  double2* yp = v3 + NB;                    // [NB] previous plane's y
-  double2* rows = yp + NB;                  // [rmax][NB] staged rows of the current plane
-  double2* racc = rows + (int64_t)rmax * NB;   // [rows][warps per row] partial row sums
-  uint64_t* rbar = (uint64_t*)(racc + rmax * kW3);
+  double2* rows = v3 + NB;                          // nbuf (1 or 2) staging buffers
+  double2* racc = rows + nbuf * (int64_t)rmax * NB; // [rows][warps per row] partial row sums
+  uint64_t* rbar = (uint64_t*)(racc + rmax * kW3);  // [2] staging barriers
   const int wpr = rows_wpr(nrow);
   auto row_sum = [&](int k) {
     double2 a = czero();
     for (int p = 0; p < wpr; ++p) a = cadd(a, racc[k * wpr + p]);
     return a;
   };
+  // step s: forward plane i = s + 1 (y_i = w_i - G_i y_{i-1}, Y_i holds w_i), then
+  // back substitution plane i = 2 n1 - 3 - s (x_i = y_i - X_i x_{i+1})
+  const int nsteps = 2 * (n1 - 1);
+  auto mat = [&](int st) {
+    return st < n1 - 1 ? gT + (int64_t)(st + 1) * nb2 : xT + (int64_t)(2 * n1 - 3 - st) * nb2;
+  };
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s3_smem(rbar)) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s3_smem(rbar + 1)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (threadIdx.x == 0 && nrow > 0) stage_rows(dinvT, NB, nrow, rows, rbar);
-  uint32_t ph = 0;
-  unsigned epoch = 0;
-  for (int i1 = 0; i1 < n1; ++i1) {   // y_i = Dinv_i (f_i - L_i y_{i-1})
-    const double2* Fi = F + (int64_t)i1 * NB;
+  if (threadIdx.x == 0 && nrow > 0)   // nbuf steps ahead
+    for (int st = 0; st < nbuf && st < nsteps; ++st)
+      stage_rows(mat(st), NB, nrow, rows + (int64_t)st * rmax * NB, rbar + st);
+  for (int st = 0; st < nsteps; ++st) {
+    const bool fwd = st < n1 - 1;
+    const int i1 = fwd ? st + 1 : 2 * n1 - 3 - st;
     double2* Yi = Y + (int64_t)i1 * NB;
-    if (i1 > 0) barrier_wait(bar, epoch * gridDim.x);
-    if (i1 > 0 && !(HS_S3_EXP & 2)) {   // y_{i-1} into shared memory once (L2 reads)
-      for (int r = threadIdx.x; r < NB; r += blockDim.x) yp[r] = __ldcg(Yi - NB + r);
-      __syncthreads();
-    }
-    for (int r = threadIdx.x; r < NB; r += blockDim.x) {
-      const int t = r / n2, i2 = r - t * n2;
-      double2 acc = __ldg(Fi + r);
-      if (i1 > 0 && !(HS_S3_EXP & 2)) {
-        double2 cv[9], yv[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) {   // all loads first (predicated), then the sum
-          const int o0 = k / 3 - 1, o2 = k % 3 - 1;
-          const int s = sl.s[oid(o0, -1, o2)];
-          const bool ok = s >= 0 && t + o0 >= 0 && t + o0 < T && i2 + o2 >= 0 && i2 + o2 < n2;
-          cv[k] = ok ? __ldg(coef + (int64_t)s * n + ((int64_t)t * n1 + i1) * n2 + i2) : czero();
-          yv[k] = ok ? yp[(t + o0) * n2 + (i2 + o2)] : czero();
-        }
-#pragma unroll
-        for (int k = 0; k < 9; ++k) acc = csub(acc, cmul(cv[k], yv[k]));
-      }
-      v3[r] = acc;
-    }
+    const double2* Yin = fwd ? Yi - NB : Yi + NB;
+    if (st > 0) barrier_wait(bar, (unsigned)st * gridDim.x);
+    if (!(HS_S3_EXP & 2))
+      for (int r = threadIdx.x; r < NB; r += blockDim.x) v3[r] = __ldcg(Yin + r);
     __syncthreads();
-    if (nrow > 0) s3_mbar_wait(rbar, ph);
-    ph ^= 1;
-    cta_rows(rows, v3, NB, nrow, racc);
-    __syncthreads();   // staged rows consumed: refill with the next plane's
-    if (threadIdx.x == 0 && nrow > 0) {
-      if (i1 + 1 < n1) stage_rows(dinvT + (i1 + 1) * nb2, NB, nrow, rows, rbar);
-      else if (n1 >= 2) stage_rows(xT + (n1 - 2) * nb2, NB, nrow, rows, rbar);
-    }
-    for (int k = threadIdx.x; k < nrow; k += blockDim.x) Yi[blockIdx.x + k * gridDim.x] = row_sum(k);
-    barrier_arrive(bar);
-    ++epoch;
-  }
-  for (int i1 = n1 - 2; i1 >= 0; --i1) {   // x_i = y_i - X_i x_{i+1}
-    double2* Yi = Y + (int64_t)i1 * NB;
-    barrier_wait(bar, epoch * gridDim.x);
-    for (int r = threadIdx.x; r < NB; r += blockDim.x) v3[r] = __ldcg(Yi + NB + r);
-    __syncthreads();
-    if (nrow > 0) s3_mbar_wait(rbar, ph);
-    ph ^= 1;
-    cta_rows(rows, v3, NB, nrow, racc);
-    __syncthreads();
-    if (threadIdx.x == 0 && nrow > 0 && i1 > 0) stage_rows(xT + (i1 - 1) * nb2, NB, nrow, rows, rbar);
+    const int b = nbuf == 2 ? (st & 1) : 0;
+    double2* buf = rows + (int64_t)b * rmax * NB;
+    if (nrow > 0) s3_mbar_wait(rbar + b, (uint32_t)(st / nbuf) & 1);
+    cta_rows(buf, v3, NB, nrow, racc);
+    __syncthreads();   // this buffer is consumed: stage the step after next into it
+    if (threadIdx.x == 0 && nrow > 0 && st + nbuf < nsteps)
+      stage_rows(mat(st + nbuf), NB, nrow, buf, rbar + b);
     for (int k = threadIdx.x; k < nrow; k += blockDim.x) {
       const int r = blockIdx.x + k * gridDim.x;
       Yi[r] = csub(__ldcg(Yi + r), row_sum(k));
     }
     barrier_arrive(bar);
-    ++epoch;
   }
 }
 
-size_t k3_smem(int NB, int grid) {
+size_t k3_smem(int NB, int grid, int nbuf) {
   const int rmax = (NB + grid - 1) / grid;
-  return (size_t)(2 * NB + (size_t)rmax * NB + (size_t)rmax * kW3) * sizeof(double2) + 16;
+  return (size_t)(NB + nbuf * (size_t)rmax * NB + (size_t)rmax * kW3) * sizeof(double2) + 16;
 }
 
 Slots to_slots(const std::array<int, 27>& a) {
@@ -341,6 +332,7 @@ void sweep3_destroy(Sweep3* s3) {
   if (!s3) return;
   for (auto* p : s3->dinv) cudaFree(p);
   for (auto* p : s3->xf) cudaFree(p);
+  for (auto* p : s3->gf) cudaFree(p);
   for (auto* p : s3->coef) cudaFree(p);
   cudaFree(s3->F);
   cudaFree(s3->Y);
@@ -413,7 +405,10 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
     S3_TRY(cudaMalloc((void**)&xv, std::max(1, n1 - 1) * nb2 * sizeof(double2)),
            "3-D slab factors (X)");
     s3->xf.push_back(xv);
-    s3->bytes += (long long)(2 * n1 - 1) * nb2 * sizeof(double2);
+    double2* gv = nullptr;
+    S3_TRY(cudaMalloc((void**)&gv, n1 * nb2 * sizeof(double2)), "3-D slab factors (G)");
+    s3->gf.push_back(gv);
+    s3->bytes += (long long)(3 * n1 - 2) * nb2 * sizeof(double2);
     const Slots sl = to_slots(s3->slot[j]);
     const unsigned gb = (unsigned)((NB + kT3 - 1) / kT3);
     for (int i1 = 0; i1 < n1; ++i1) {
@@ -439,6 +434,14 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
       S3_BLAS(cublasZgeam(s3->blas, CUBLAS_OP_T, CUBLAS_OP_N, NB, NB, &one, (cuDoubleComplex*)Di,
                           NB, &zero, (cuDoubleComplex*)Di, NB, (cuDoubleComplex*)(dv + i1 * nb2),
                           NB), "geam");
+      if (i1 > 0) {   // G_i = Dinv_i L_i (the forward chain's coupling), row-major
+        S3_BLAS(cublasZgemm(s3->blas, CUBLAS_OP_N, CUBLAS_OP_N, NB, NB, NB, &one,
+                            (cuDoubleComplex*)Di, NB, (cuDoubleComplex*)Lb, NB, &zero,
+                            (cuDoubleComplex*)U, NB), "zgemm");
+        S3_BLAS(cublasZgeam(s3->blas, CUBLAS_OP_T, CUBLAS_OP_N, NB, NB, &one,
+                            (cuDoubleComplex*)U, NB, &zero, (cuDoubleComplex*)U, NB,
+                            (cuDoubleComplex*)(gv + i1 * nb2), NB), "geam");
+      }
       if (i1 + 1 < n1) {   // X_i = Dinv_i U_i
         S3_TRY(cudaMemsetAsync(U, 0, nb2 * sizeof(double2), c->stream), "memset");
         k3_block<<<gb, kT3, 0, c->stream>>>(cf, sl, T, n1, n2, i1, 1, U);
@@ -466,14 +469,21 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
         return done(set_error(c, HS_E_ZERO_PIVOT, buf, row));
       }
   s->factor_bytes = s3->bytes;
-  {   // the solve kernel: one CTA per SM, co-resident (cooperative launch)
+  {   // the solve kernel: one CTA per SM, co-resident (cooperative launch); the
+      // staged rows double-buffered when two planes' rows fit shared memory
     s3->grid = c->num_sms;
-    const int smem = (int)k3_smem(NBmax, s3->grid);
+    int optin = 0;
+    S3_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device),
+           "smem attr");
+    if ((NBmax + s3->grid - 1) / s3->grid > kR3)
+      return done(set_error(c, HS_E_SHAPE, "3-D slab planes too large for the solve kernel"));
+    s3->nbuf = k3_smem(NBmax, s3->grid, 2) <= (size_t)optin ? 2 : 1;
+    const int smem = (int)k3_smem(NBmax, s3->grid, s3->nbuf);
+    if (smem > optin) return done(set_error(c, HS_E_SHAPE, "3-D slab planes too large for the solve kernel"));
     S3_TRY(cudaFuncSetAttribute(k3_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "attr");
     int per = 0;
     S3_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k3_solve, kW3 * 32, smem), "occ");
     if (per < 1) return done(set_error(c, HS_E_CUDA, "3-D solve kernel does not fit an SM"));
-    s3->grid = c->num_sms;
   }
   return done(HS_OK);
 }
@@ -490,20 +500,29 @@ int sweep3_task(Ctx* c, Sweep* s, const SweepTask& t, const double2* src, double
   k3_rhs<<<(unsigned)((tot + kT3 - 1) / kT3), kT3, 0, c->stream>>>(
       t, s->n0, n1, n2, src, coarse_coeffs, coarse_n, to_slots(s3->cslot), s->trace, s3->F);
   HS_LAUNCH_CHECK(c, "3-D rhs");
-  {   // block recursion: one cooperative launch
+  {   // w_i = Dinv_i f_i for every plane: one batched GEMV (Dinv stored row-major
+      // = column-major transpose), written into Y where the chain updates it
+    const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+    ProfScope ps(c, K_SWEEP_GATHER, (double)n1 * nb2 * 16.0);
+    if (cublasZgemvStridedBatched(s3->blas, CUBLAS_OP_T, NB, NB, &one,
+                                  (const cuDoubleComplex*)s3->dinv[j], NB, (long long)nb2,
+                                  (const cuDoubleComplex*)s3->F, 1, NB, &zero,
+                                  (cuDoubleComplex*)s3->Y, 1, NB, n1) != CUBLAS_STATUS_SUCCESS)
+      return set_error(c, HS_E_CUDA, "3-D batched GEMV failed");
+    c->launches++;
+  }
+  {   // the chain: one cooperative launch
     S3_TRY(cudaMemsetAsync(s3->gbar, 0, sizeof(unsigned), c->stream), "memset");
-    const double2* cf = s3->coef[j];
-    const double2* dv = s3->dinv[j];
+    const double2* gv = s3->gf[j];
     const double2* xv = s3->xf[j];
-    const double2* Fp = s3->F;
     double2* Yp = s3->Y;
     unsigned* gb = s3->gbar;
     int T_ = T, n1_ = n1, n2_ = n2;
-    Slots sl_ = sl;
-    void* args[] = {(void*)&cf, (void*)&sl_, (void*)&T_, (void*)&n1_, (void*)&n2_,
-                    (void*)&dv, (void*)&xv, (void*)&Fp, (void*)&Yp, (void*)&gb};
+    int nb_ = s3->nbuf;
+    void* args[] = {(void*)&T_, (void*)&n1_, (void*)&n2_, (void*)&gv, (void*)&xv, (void*)&Yp,
+                    (void*)&gb, (void*)&nb_};
     S3_TRY(cudaLaunchCooperativeKernel((const void*)k3_solve, dim3(s3->grid), dim3(kW3 * 32), args,
-                                       k3_smem(NB, s3->grid), c->stream),
+                                       k3_smem(NB, s3->grid, s3->nbuf), c->stream),
            "3-D solve launch");
     HS_LAUNCH_CHECK(c, "3-D solve kernel");
   }
