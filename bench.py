@@ -137,6 +137,12 @@ class ClockSampler:
                 ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=self.out, stderr=subprocess.DEVNULL)
+            # nvidia-smi's start-up (NVML init) was measured to stall this
+            # process's launches for ~20 ms: start timing only after its
+            # first sample is written
+            t_end = time.perf_counter() + 5.0
+            while time.perf_counter() < t_end and os.fstat(self.out.fileno()).st_size == 0:
+                time.sleep(0.01)
         elif self.mode in ("smi", "nvml"):
             try:
                 import pynvml
@@ -314,16 +320,20 @@ def run_ours(args):
         for _ in range(args.warmup):
             step(f_dev)
     with ClockSampler(local, args.clock_sampler) as clk:
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         ev0.record(stream)
-        for _ in range(args.steps):
+        evs[0].record(stream)
+        for s in range(args.steps):
             for u, rep in step(f_dev):
                 reports.append(rep)
+            evs[s + 1].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = ctx.launches - launches0
     if world > 1:
         torch.distributed.barrier()
     ms_local = ev0.elapsed_time(ev1)
+    ms_steps = [evs[s].elapsed_time(evs[s + 1]) for s in range(args.steps)]
     # kernel-class attribution: the same K steps again with the library's
     # event profiler on (events bracket every launch, so this pass is not
     # the timed one; its per-kernel durations feed roofline/kernel_shares)
@@ -352,17 +362,21 @@ def run_ours(args):
             hb.gmres(cycle.fine_csr, prec, fh, cfg, orth=args.orth, pipelined=not args.no_pipeline)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    eevs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0.record(stream)
-    for _ in range(args.steps):
+    eevs[0].record(stream)
+    for s_ in range(args.steps):
         if multi:
             step(f_host)
-            continue
-        for fh in f_host:
-            u_out, _ = hb.gmres(cycle.fine_csr, prec, fh, cfg, orth=args.orth,
-                                pipelined=not args.no_pipeline)
+        else:
+            for fh in f_host:
+                u_out, _ = hb.gmres(cycle.fine_csr, prec, fh, cfg, orth=args.orth,
+                                    pipelined=not args.no_pipeline)
+        eevs[s_ + 1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = reduce_over_ranks(e0.elapsed_time(e1), world, "max")
+    e2e_steps = [eevs[i].elapsed_time(eevs[i + 1]) for i in range(args.steps)]
     e2e_value = job_value(p.n_fine, solves, e2e_ms)
 
     # ---- roofline of the dominant kernel class (profiler events over the timed region)
@@ -412,6 +426,7 @@ def run_ours(args):
             "metric": "TGSP-GMRES fine DOF/s (solve to 1e-6 rel-res)",
             "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "ms_steps_rank0": ms_steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "c128", "data": "synthetic",
             "config": {"workload": workload_name(p), "fine_dof": p.n_fine,
@@ -427,7 +442,8 @@ def run_ours(args):
             "true_residual": true_res,
             "e2e": {"value": e2e_value, "unit": "DOF/s",
                     "h2d_bytes_per_step": 16 * p.n_fine * len(f_dev),
-                    "d2h_bytes_per_step": 16 * p.n_fine * len(f_dev)},
+                    "d2h_bytes_per_step": 16 * p.n_fine * len(f_dev),
+                    "ms_steps_rank0": e2e_steps},
             "gpu_launches": launches,
             "roofline": roofline,
             "roofline_stencil": stencil_roof,

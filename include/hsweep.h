@@ -35,7 +35,7 @@ enum {
   HS_E_BUFFER = 7
 };
 
-enum { HS_VARIANT_UD = 0, HS_VARIANT_X = 1 };
+enum { HS_VARIANT_UD = 0, HS_VARIANT_X = 1 };   /* NX plans get ids >= 2 (hs_sweep_plan_nx) */
 
 typedef struct hs_ctx hs_ctx;
 typedef struct hs_stencil hs_stencil;
@@ -157,6 +157,23 @@ int hs_sweep_destroy(hs_ctx* ctx, hs_sweep* s);
 /* u = Sweep(f); variant HS_VARIANT_X (prec_x, sweepdd.py:322-359) or
  * HS_VARIANT_UD (prec_ud, sweepdd.py:312-319).  f and u: device, coarse shape. */
 int hs_sweep_apply(hs_ctx* ctx, hs_sweep* s, int variant, const void* f, void* u);
+/* NX sweep (prec_nx, sweepdd.py:403-437; NxCells / make_nx_cells :362-401):
+ * registers the launch plan of one cell grouping -- j_cell: ncell + 1 cell
+ * boundaries with sentinels -1 and J + 1, j_mid: the slab where each cell's
+ * sweeps meet -- and returns its variant id (>= 2) for hs_sweep_apply and
+ * hs_cycle_create.  The groups' fronts run concurrently (one cluster each).
+ * Fails with HS_E_SHAPE on an invalid grouping (NxCells.validate). */
+int hs_sweep_plan_nx(hs_ctx* ctx, hs_sweep* s, int ncell, const int64_t* j_cell,
+                     const int64_t* j_mid, int* variant);
+/* Exact solve of a whole stencil operator: factorize / Factorization.solve
+ * (sparselin.py:40-68) and ExactCoarseSolver (twogrid.py:99-105).  Block LU
+ * along the operator's second axis with dense planes of the first (x third)
+ * axis -- NB = n0 (2-D) or n0*n2 (3-D) unknowns per block, at most
+ * 8 * (SM count); factors: (3 n1 - 2) NB^2 complex128 in HBM.  The handle is
+ * an hs_sweep: apply it with hs_sweep_apply(HS_VARIANT_UD), or pass it to
+ * hs_cycle_create with HS_VARIANT_UD for a two-grid cycle with an exact
+ * coarse solve.  Fails with HS_E_ZERO_PIVOT on a singular pivot block. */
+int hs_exact_create(hs_ctx* ctx, const hs_stencil* op, hs_sweep** out);
 /* bytes of device memory held by the slab factors (diagnostic) */
 long long hs_sweep_factor_bytes(hs_sweep* s);
 

@@ -256,8 +256,61 @@ class Partition:
         self.forward(u, g, jm + 1, self.J, B2)
         return u
 
-    def apply(self, f, variant="x"):
+    def mid_in(self, u, f, j, B1, B3):
+        """midsolve_in (sweepdd.py:297-300)."""
+        self.solve(u, f, j, self.beta[j - 1], self.bt[j], self.beta[j - 1], self.bt[j],
+                   B1=B1, B3=B3)
+
+    def mid_out(self, u, f, j):
+        """midsolve_out (sweepdd.py:303-306): returns (out2, out4)."""
+        return self.solve(u, f, j, self.bt[j - 1], self.beta[j], self.bt[j - 1], self.beta[j],
+                          out2=True, out4=True)
+
+    def prec_nx(self, f, j_cell, j_mid):
+        """NX sweep over cell groups (sweepdd.py:403-434): j_cell has the -1 / J+1
+        sentinels; buffer k of the reference is buf[k] here."""
+        f = np.asarray(f, complex).reshape(self.shape)
+        u = np.zeros(self.shape, complex)
+        jc, jm = list(j_cell), list(j_mid)
+        nc = len(jm)
+        buf = {i: None for i in range(1, 2 * nc + 2)}
+        for m in range(1, nc + 1):
+            if m < nc:
+                bf, bb = self.mid_out(u, f, jc[m])
+                buf[2 * m + 1], buf[2 * m] = bf, bb
+            buf[2 * m - 1] = self.forward(u, f, jc[m - 1] + 1, jm[m - 1] - 1, buf[2 * m - 1])
+            buf[2 * m] = self.backward(u, f, jc[m] - 1, jm[m - 1] + 1, buf[2 * m])
+            self.mid_in(u, f, jm[m - 1], buf[2 * m - 1], buf[2 * m])
+        g = self.residual(u, f)
+        for m in range(1, nc + 1):
+            bf, bb = self.mid_out(u, g, jm[m - 1])
+            buf[2 * m], buf[2 * m - 1] = bf, bb
+            buf[2 * m - 1] = self.backward(u, g, jm[m - 1] - 1, jc[m - 1] + 1, buf[2 * m - 1])
+            buf[2 * m] = self.forward(u, g, jm[m - 1] + 1, jc[m] - 1, buf[2 * m])
+            if m > 1:
+                self.mid_in(u, g, jc[m - 1], buf[2 * m - 2], buf[2 * m - 1])
+        return u
+
+    def apply(self, f, variant="x", cells=None):
+        if variant == "nx":
+            return self.prec_nx(f, *cells)
         return self.prec_x(f) if variant == "x" else self.prec_ud(f)
+
+
+class Exact:
+    """ExactCoarseSolver (twogrid.py:99-105): SuperLU of the whole operator
+    (sparselin.py:40-62), as a stand-in for a partition in TwoGrid."""
+
+    def __init__(self, op: Op):
+        self.op = op
+        self.shape = op.shape
+        self.lu = spla.splu(sp.csc_matrix(op.csr))
+
+    def solve(self, b):
+        return self.lu.solve(np.asarray(b, complex).ravel())
+
+    def apply(self, f, variant=None, cells=None):
+        return self.solve(f).reshape(self.shape)
 
 
 # ---------------------------------------------------------------------------
@@ -265,8 +318,9 @@ class Partition:
 
 class TwoGrid:
     def __init__(self, fine: Op, p_matrix, partition: Partition, omega_jac, nu,
-                 restrict_scale, variant="x"):
+                 restrict_scale, variant="x", cells=None):
         self.fine, self.p, self.part = fine, p_matrix, partition
+        self.cells = cells          # NX: (j_cell, j_mid)
         self.omega_jac, self.nu = float(omega_jac), int(nu)
         self.restrict_scale = float(restrict_scale)
         self.variant = variant
@@ -283,7 +337,7 @@ class TwoGrid:
         u = self._smooth(np.zeros_like(f), f) if self.nu else np.zeros_like(f)
         r = f - (self.fine.csr @ u.ravel()).reshape(f.shape)
         rc = self.restrict_scale * (self.p.T @ r.ravel())
-        uc = self.part.apply(rc.reshape(self.part.shape), self.variant)
+        uc = self.part.apply(rc.reshape(self.part.shape), self.variant, self.cells)
         u = u + (self.p @ uc.ravel()).reshape(f.shape)
         if self.nu:
             u = self._smooth(u, f)
@@ -393,7 +447,17 @@ def from_fixture(d, variant=None):
     dim = len(d["fine_shape"])
     p = prolongation([d[f"fp{a}"] for a in range(dim)], [d[f"refined{a}"] for a in range(dim)])
     v = variant or str(d["variant"])
-    return TwoGrid(fine, p, part, d["omega_jac"], d["nu"], d["restrict_scale"], v)
+    cells = (d["nx2_cells"], d["nx2_mid"]) if v == "nx" else None   # the nx2d case's NX(2)
+    return TwoGrid(fine, p, part, d["omega_jac"], d["nu"], d["restrict_scale"], v, cells)
+
+
+def from_exact_fixture(d):
+    """Two-grid cycle with the exact coarse solve from tests/golden/exact2d.npz."""
+    fine = Op(d["fine_offsets"], d["fine_coeffs"])
+    coarse = Op(d["coarse_offsets"], d["coarse_coeffs"])
+    dim = len(d["fine_shape"])
+    p = prolongation([d[f"fp{a}"] for a in range(dim)], [d[f"refined{a}"] for a in range(dim)])
+    return TwoGrid(fine, p, Exact(coarse), d["omega_jac"], d["nu"], d["restrict_scale"], "exact")
 
 
 def from_hierarchy(h):
@@ -404,5 +468,18 @@ def from_hierarchy(h):
     slabs = [Slab(lo, hi, Op.from_dict(op.coeffs)) for (lo, hi, op) in h.slabs]
     part = Partition(coarse, h.beta, h.beta_tilde, slabs)
     p = prolongation(h.cmap.fine_point_of_coarse, h.cmap.refined_cell)
+    cells = None
+    if h.sweep.variant == "nx":
+        c = h.sweep.n_cell
+        cells = (list(c.j_cell), list(c.j_mid)) if hasattr(c, "j_cell") else \
+            _nx_cells(h.partition.J, int(c))
     return TwoGrid(fine, p, part, h.smoother.omega_jac, h.smoother.nu, h.restrict_scale,
-                   h.sweep.variant)
+                   h.sweep.variant, cells)
+
+
+def _nx_cells(J, n_cell):
+    """make_nx_cells (sweepdd.py:392-401) as (j_cell, j_mid)."""
+    bounds = [-1] + [round(m * J / n_cell) for m in range(1, n_cell)] + [J + 1]
+    mids = [(max(1, bounds[m - 1] + 1) + min(J, bounds[m] - 1) + 1) // 2
+            for m in range(1, n_cell + 1)]
+    return bounds, mids

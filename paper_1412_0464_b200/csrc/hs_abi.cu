@@ -407,6 +407,15 @@ int hs_sweep_create(hs_ctx* c, const hs_stencil* coarse, int J, const int64_t* b
   return HS_OK;
 }
 
+int hs_exact_create(hs_ctx* c, const hs_stencil* op, hs_sweep** out) {
+  if (!c || !op || !out) return HS_E_ARG;
+  Sweep* s = nullptr;
+  int r = exact_create(c, op, &s);
+  if (r) return r;
+  *out = reinterpret_cast<hs_sweep*>(s);
+  return HS_OK;
+}
+
 int hs_sweep_destroy(hs_ctx* c, hs_sweep* s) {
   (void)c;
   sweep_destroy(s);
@@ -418,6 +427,12 @@ int hs_sweep_apply(hs_ctx* c, hs_sweep* s, int variant, const void* f, void* u) 
   return sweep_apply(c, s, variant, (const double2*)f, (double2*)u);
 }
 
+int hs_sweep_plan_nx(hs_ctx* c, hs_sweep* s, int ncell, const int64_t* j_cell,
+                     const int64_t* j_mid, int* variant) {
+  if (!c || !s || !j_cell || !j_mid || !variant) return HS_E_ARG;
+  return sweep_plan_nx(c, s, ncell, j_cell, j_mid, variant);
+}
+
 long long hs_sweep_factor_bytes(hs_sweep* s) { return s ? s->factor_bytes : 0; }
 
 // ---------------------------------------------------------------------------
@@ -425,10 +440,9 @@ int hs_cycle_create(hs_ctx* c, const hs_stencil* fine, const hs_transfer* t,
                     const hs_stencil* coarse, hs_sweep* sweep, double omega_jac, int nu,
                     double restrict_scale, int variant, hs_cycle** out) {
   if (!c || !fine || !t || !coarse || !sweep || !out || nu < 0) return HS_E_ARG;
-  if (variant != HS_VARIANT_X && variant != HS_VARIANT_UD)
-    return set_error(c, HS_E_ARG, "unknown sweep variant");
-  if (!sweep->has_plan[variant])
-    return set_error(c, HS_E_ARG, "X-sweep needs an even subdomain count");
+  if (!sweep->has_plan(variant))
+    return set_error(c, HS_E_ARG, variant == HS_VARIANT_X ? "X-sweep needs an even subdomain count"
+                                                          : "unknown sweep variant");
   if (t->d.nf[0] * t->d.nf[1] * t->d.nf[2] != fine->d.n ||
       t->d.nc[0] * t->d.nc[1] * t->d.nc[2] != coarse->d.n)
     return set_error(c, HS_E_SHAPE, "coarsening map does not match the operators");

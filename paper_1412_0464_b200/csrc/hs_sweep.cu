@@ -586,7 +586,7 @@ k_reduced(Chunks g, const double2* __restrict__ tips, double2* __restrict__ Gw,
 
 struct SolveArgs {
   const SweepTask* tasks;
-  int ffirst[2], fcount[2];
+  int ffirst[kMaxFront], fcount[kMaxFront];
   Chunks g;
   int nchunk;              // ring slots (16-KB chunks)
   const double2* stream;   // [J][C][nbs] factor blocks in item order
@@ -1079,8 +1079,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   double2* ring = sm + ((((char*)(cmq + itab_len(mmax)) - (char*)sm) + 127) & ~(ptrdiff_t)127) / 16;
   const ItemPlan& P = *Pp;
 
-  const int ffirst = front ? a.ffirst[1] : a.ffirst[0];
-  const int fcount = front ? a.fcount[1] : a.fcount[0];
+  const int ffirst = a.ffirst[front];
+  const int fcount = a.fcount[front];
   {
     const int pw = plan_words(mmax);
     const uint32_t* src = a.plan + (int64_t)rank * pw;
@@ -1738,14 +1738,20 @@ Chunks make_chunks(const Sweep* s) {
 // ---------------------------------------------------------------------------
 // host side
 
-// Task lists and launch plans of the UD and X schedules (prec_ud / prec_x,
-// sweepdd.py:312-359), shared by the 2-D and 3-D sweeps.  Returns the number
-// of trace buffers.
-static int build_schedule(Sweep* s, int J, const int64_t* beta, const int64_t* bt,
-                          const int64_t* lo, const int64_t* hi) {
-  // ---- schedules (task lists) ----
-  int ntin = 0;
-  auto mk = [&](int j, int a_, int b_) {
+// Task lists and launch plans of the sweep schedules (prec_ud / prec_x /
+// prec_nx, sweepdd.py:312-437), shared by the 2-D and 3-D sweeps.  A front
+// is a chain of slab solves run in order by one cluster (2-D) with the
+// traces of consecutive tasks handed over on chip; fronts of one launch are
+// independent.  A trace consumed by two fronts comes from a task placed at
+// the head of both (computed twice, identical results).
+namespace {
+struct SchedBuilder {
+  Sweep* s;
+  int J;
+  const int64_t *beta, *bt, *lo, *hi;
+  int ntin = 0;   // trace buffers handed out
+
+  SweepTask mk(int j, int a_, int b_) const {
     SweepTask t{};
     t.slab = j - 1;
     t.lo = (int)lo[j - 1];
@@ -1757,128 +1763,239 @@ static int build_schedule(Sweep* s, int J, const int64_t* beta, const int64_t* b
     t.tin1 = t.tin3 = t.out2 = t.out4 = -1;
     t.row1 = t.row3 = t.orow2 = t.orow4 = -1;
     return t;
-  };
-  auto want1 = [&](SweepTask& t, int j) {   // tau1 (forward in), gated j > 1
+  }
+  int want1(SweepTask& t) {   // tau1 (forward in), gated j > 1
+    const int j = t.slab + 1;
     if (j <= 1) return -1;
     t.tin1 = ntin++;
     t.row1 = (int)beta[j - 1] - t.lo;
     return t.tin1;
-  };
-  auto want3 = [&](SweepTask& t, int j) {   // tau3 (backward in), gated j < J
+  }
+  int want3(SweepTask& t) {   // tau3 (backward in), gated j < J
+    const int j = t.slab + 1;
     if (j >= J) return -1;
     t.tin3 = ntin++;
     t.row3 = (int)bt[j] - t.lo;
     return t.tin3;
-  };
-  auto give2 = [&](SweepTask& t, int j, int buf) {   // tau2 (forward out), gated j < J
+  }
+  void give2(SweepTask& t, int buf) const {   // tau2 (forward out), gated j < J
+    const int j = t.slab + 1;
     if (j >= J || buf < 0) return;
     t.out2 = buf;
     t.orow2 = (int)beta[j] - t.lo;
-  };
-  auto give4 = [&](SweepTask& t, int j, int buf) {   // tau4 (backward out), gated j > 1
+  }
+  void give4(SweepTask& t, int buf) const {   // tau4 (backward out), gated j > 1
+    const int j = t.slab + 1;
     if (j <= 1 || buf < 0) return;
     t.out4 = buf;
     t.orow4 = (int)bt[j - 1] - t.lo;
-  };
-  auto fwd_task = [&](int j) { return mk(j, (int)beta[j - 1], (int)beta[j]); };
-  auto bwd_task = [&](int j) { return mk(j, (int)bt[j - 1], (int)bt[j]); };
-  std::vector<SweepTask>& T = s->tasks;
-  auto fwd_chain = [&](int j0, int j1, std::vector<SweepTask>& pass) {
+  }
+  SweepTask fwd_task(int j) const { return mk(j, (int)beta[j - 1], (int)beta[j]); }
+  SweepTask bwd_task(int j) const { return mk(j, (int)bt[j - 1], (int)bt[j]); }
+  SweepTask mid_in(int j) const { return mk(j, (int)beta[j - 1], (int)bt[j]); }    // midsolve_in
+  SweepTask mid_out(int j) const { return mk(j, (int)bt[j - 1], (int)beta[j]); }   // midsolve_out
+  // forward_sweep j0..j1 (out-of-range slabs skipped), chained through traces
+  std::vector<SweepTask> fwd_chain(int j0, int j1) {
+    std::vector<SweepTask> v;
     for (int j = j0; j <= j1; ++j) {
       if (j < 1 || j > J) continue;
       SweepTask t = fwd_task(j);
-      want1(t, j);
-      if (!pass.empty() && j > 1 && pass.back().slab == j - 2 && pass.back().out2 == -2)
-        give2(pass.back(), j - 1, t.tin1);
-      if (j < J) t.out2 = -2;   // placeholder until a consumer appears
-      pass.push_back(t);
+      const int in = want1(t);
+      if (!v.empty()) give2(v.back(), in);
+      v.push_back(t);
     }
-  };
-  auto bwd_chain = [&](int j0, int j1, std::vector<SweepTask>& pass) {
+    return v;
+  }
+  std::vector<SweepTask> bwd_chain(int j0, int j1) {
+    std::vector<SweepTask> v;
     for (int j = j0; j >= j1; --j) {
       if (j < 1 || j > J) continue;
       SweepTask t = bwd_task(j);
-      want3(t, j);
-      if (!pass.empty() && j < J && pass.back().slab == j && pass.back().out4 == -2)
-        give4(pass.back(), j + 1, t.tin3);
-      if (j > 1) t.out4 = -2;
-      pass.push_back(t);
+      const int in = want3(t);
+      if (!v.empty()) give4(v.back(), in);
+      v.push_back(t);
     }
-  };
-  auto clear_placeholders = [&](std::vector<SweepTask>& v) {
-    for (auto& t : v) {
-      if (t.out2 == -2) t.out2 = -1;
-      if (t.out4 == -2) t.out4 = -1;
-    }
-  };
-  // one solve launch per stage (up to two concurrent fronts)
-  auto emit_pass = [&](std::vector<SweepLaunch>& plan, int src,
-                       std::vector<std::vector<std::vector<SweepTask>>> stages) {
-    for (auto& st : stages) {
+    return v;
+  }
+  // one solve launch per stage; a stage with more than kMaxFront fronts is
+  // split into several launches (its fronts are independent)
+  void emit(std::vector<SweepLaunch>& plan, int src,
+            const std::vector<std::vector<std::vector<SweepTask>>>& stages) {
+    std::vector<SweepTask>& T = s->tasks;
+    for (const auto& st : stages) {
       SweepLaunch fl{};
       fl.kind = SweepLaunch::kSolve;
       fl.src = src;
-      for (auto& fr : st) {
+      for (const auto& fr : st) {
         if (fr.empty()) continue;
+        if (fl.nfront == kMaxFront) {
+          plan.push_back(fl);
+          fl = SweepLaunch{};
+          fl.kind = SweepLaunch::kSolve;
+          fl.src = src;
+        }
         fl.ffirst[fl.nfront] = (int)T.size();
         fl.fcount[fl.nfront] = (int)fr.size();
         fl.nfront++;
-        for (auto t : fr) {
+        for (SweepTask t : fr) {
           t.dst = src;
           T.push_back(t);
         }
       }
       if (fl.nfront) plan.push_back(fl);
     }
-  };
+  }
+};
+
+std::vector<SweepTask> cat(const std::vector<SweepTask>& head, const std::vector<SweepTask>& v) {
+  std::vector<SweepTask> r(head);
+  r.insert(r.end(), v.begin(), v.end());
+  return r;
+}
+}  // namespace
+
+// UD and X plans; returns the number of trace buffers
+static int build_schedule(Sweep* s, int J, const int64_t* beta, const int64_t* bt,
+                          const int64_t* lo, const int64_t* hi) {
+  s->hbeta.assign(beta, beta + J + 1);
+  s->hbt.assign(bt, bt + J + 1);
+  s->hlo.assign(lo, lo + J);
+  s->hhi.assign(hi, hi + J);
+  SchedBuilder b{s, J, beta, bt, lo, hi};
   // ---- UD: forward 1..J on f; g = f - A u; backward J..1 on g ----
   {
     std::vector<SweepLaunch>& plan = s->plan[HS_VARIANT_UD];
-    std::vector<SweepTask> F, Bk;
-    fwd_chain(1, J, F);
-    clear_placeholders(F);
-    bwd_chain(J, 1, Bk);
-    clear_placeholders(Bk);
-    emit_pass(plan, 0, {{F}});
+    b.emit(plan, 0, {{b.fwd_chain(1, J)}});
     plan.push_back(SweepLaunch{SweepLaunch::kResidual});
-    emit_pass(plan, 1, {{Bk}});
+    b.emit(plan, 1, {{b.bwd_chain(J, 1)}});
     plan.push_back(SweepLaunch{SweepLaunch::kCombine});
-    s->has_plan[HS_VARIANT_UD] = true;
   }
   // ---- X: simultaneous half sweeps meeting at jm = J/2 + 1 ----
   if (J % 2 == 0) {
     std::vector<SweepLaunch>& plan = s->plan[HS_VARIANT_X];
     const int jm = J / 2 + 1;
-    std::vector<SweepTask> F, Bk, MI;
-    fwd_chain(1, jm - 1, F);
-    bwd_chain(J, jm + 1, Bk);
-    SweepTask mi = mk(jm, (int)beta[jm - 1], (int)bt[jm]);
-    want1(mi, jm);
-    want3(mi, jm);
-    if (!F.empty() && F.back().out2 == -2) give2(F.back(), jm - 1, mi.tin1);
-    if (!Bk.empty() && Bk.back().out4 == -2) give4(Bk.back(), jm + 1, mi.tin3);
-    clear_placeholders(F);
-    clear_placeholders(Bk);
-    MI.push_back(mi);
-    emit_pass(plan, 0, {{F, Bk}, {MI}});
+    std::vector<SweepTask> F = b.fwd_chain(1, jm - 1), Bk = b.bwd_chain(J, jm + 1);
+    SweepTask mi = b.mid_in(jm);
+    const int in1 = b.want1(mi), in3 = b.want3(mi);
+    if (!F.empty()) b.give2(F.back(), in1);
+    if (!Bk.empty()) b.give4(Bk.back(), in3);
+    b.emit(plan, 0, {{F, Bk}, {{mi}}});
     plan.push_back(SweepLaunch{SweepLaunch::kResidual});
-    std::vector<SweepTask> BB, FF;
-    SweepTask mo = mk(jm, (int)bt[jm - 1], (int)beta[jm]);
-    bwd_chain(jm - 1, 1, BB);
-    fwd_chain(jm + 1, J, FF);
-    if (!FF.empty()) give2(mo, jm, FF.front().tin1);
-    if (!BB.empty()) give4(mo, jm, BB.front().tin3);
-    clear_placeholders(BB);
-    clear_placeholders(FF);
+    SweepTask mo = b.mid_out(jm);
+    std::vector<SweepTask> BB = b.bwd_chain(jm - 1, 1), FF = b.fwd_chain(jm + 1, J);
+    if (!FF.empty()) b.give2(mo, FF.front().tin1);
+    if (!BB.empty()) b.give4(mo, BB.front().tin3);
     // the middle solve opens both outward fronts (computed by both clusters,
     // identical results), so pass 2 is one launch with in-cluster handoffs
-    BB.insert(BB.begin(), mo);
-    FF.insert(FF.begin(), mo);
-    emit_pass(plan, 1, {{BB, FF}});
+    b.emit(plan, 1, {{cat({mo}, BB), cat({mo}, FF)}});
     plan.push_back(SweepLaunch{SweepLaunch::kCombine});
-    s->has_plan[HS_VARIANT_X] = true;
   }
-  return ntin;
+  return b.ntin;
+}
+
+// NX: ncell groups, each an X sweep over its cell; the group-boundary input
+// solve of pass 2 runs once both of its traces exist (prec_nx's note,
+// sweepdd.py:403-437).  Pass 1: every cell's forward and backward fronts in
+// one launch -- the boundary output solve mid_out(jc[m]) heads both fronts
+// that read its traces -- then the cells' meeting solves mid_in(jm[m]).
+// Pass 2: mid_out(jm[m]) heads both outward fronts of cell m, then the
+// boundary input solves mid_in(jc[m]).
+static std::vector<SweepLaunch> build_nx(Sweep* s, int ncell, const int64_t* jc,
+                                         const int64_t* jmid, int* ntin) {
+  const int J = s->J;
+  SchedBuilder b{s, J, s->hbeta.data(), s->hbt.data(), s->hlo.data(), s->hhi.data()};
+  std::vector<SweepLaunch> plan;
+  const int nc = ncell;
+  // a chain's head task hands its trace to the chain's first task, or, for an
+  // empty chain, to the solve after it (forward_sweep returns B unchanged)
+  {   // ---- pass 1 ----
+    std::vector<std::vector<SweepTask>> F(nc + 1), Bk(nc + 1);
+    std::vector<SweepTask> MI(nc + 1), MO(nc + 1);
+    for (int m = 1; m <= nc; ++m) {
+      F[m] = b.fwd_chain((int)jc[m - 1] + 1, (int)jmid[m - 1] - 1);
+      Bk[m] = b.bwd_chain((int)jc[m] - 1, (int)jmid[m - 1] + 1);
+      MI[m] = b.mid_in((int)jmid[m - 1]);
+      const int in1 = b.want1(MI[m]), in3 = b.want3(MI[m]);
+      if (!F[m].empty()) b.give2(F[m].back(), in1);
+      if (!Bk[m].empty()) b.give4(Bk[m].back(), in3);
+    }
+    for (int m = 1; m < nc; ++m) {   // mid_out(jc[m]) feeds F[m+1] and Bk[m]
+      MO[m] = b.mid_out((int)jc[m]);
+      b.give2(MO[m], F[m + 1].empty() ? MI[m + 1].tin1 : F[m + 1].front().tin1);
+      b.give4(MO[m], Bk[m].empty() ? MI[m].tin3 : Bk[m].front().tin3);
+    }
+    std::vector<std::vector<SweepTask>> fronts, mids;
+    for (int m = 1; m <= nc; ++m) {
+      fronts.push_back(m > 1 && !F[m].empty() ? cat({MO[m - 1]}, F[m]) : F[m]);
+      if (m < nc) {
+        if (!Bk[m].empty()) fronts.push_back(cat({MO[m]}, Bk[m]));
+        else if (F[m + 1].empty()) fronts.push_back({MO[m]});   // computed once
+      } else {
+        fronts.push_back(Bk[m]);
+      }
+      mids.push_back({MI[m]});
+    }
+    b.emit(plan, 0, {fronts, mids});
+  }
+  plan.push_back(SweepLaunch{SweepLaunch::kResidual});
+  {   // ---- pass 2 ----
+    std::vector<std::vector<SweepTask>> BB(nc + 1), FF(nc + 1);
+    std::vector<SweepTask> MO(nc + 1), MI(nc + 1);
+    for (int m = 1; m <= nc; ++m) {
+      BB[m] = b.bwd_chain((int)jmid[m - 1] - 1, (int)jc[m - 1] + 1);
+      FF[m] = b.fwd_chain((int)jmid[m - 1] + 1, (int)jc[m] - 1);
+      MO[m] = b.mid_out((int)jmid[m - 1]);
+    }
+    for (int m = 2; m <= nc; ++m) {   // mid_in(jc[m-1]) after cells m-1 and m
+      MI[m] = b.mid_in((int)jc[m - 1]);
+      const int in1 = b.want1(MI[m]), in3 = b.want3(MI[m]);
+      if (!FF[m - 1].empty()) b.give2(FF[m - 1].back(), in1);
+      else b.give2(MO[m - 1], in1);
+      if (!BB[m].empty()) b.give4(BB[m].back(), in3);
+      else b.give4(MO[m], in3);
+    }
+    for (int m = 1; m <= nc; ++m) {
+      if (!FF[m].empty()) b.give2(MO[m], FF[m].front().tin1);
+      if (!BB[m].empty()) b.give4(MO[m], BB[m].front().tin3);
+    }
+    std::vector<std::vector<SweepTask>> fronts, mids;
+    for (int m = 1; m <= nc; ++m) {
+      if (BB[m].empty() && FF[m].empty()) {
+        fronts.push_back({MO[m]});
+      } else {
+        if (!BB[m].empty()) fronts.push_back(cat({MO[m]}, BB[m]));
+        if (!FF[m].empty()) fronts.push_back(cat({MO[m]}, FF[m]));
+      }
+      if (m > 1) mids.push_back({MI[m]});
+    }
+    b.emit(plan, 1, {fronts, mids});
+  }
+  plan.push_back(SweepLaunch{SweepLaunch::kCombine});
+  *ntin = b.ntin;
+  return plan;
+}
+
+// algorithmic HBM bytes of every solve launch of a plan (profiler): 2-D --
+// exactly the streamed factor blocks + rhs/u/trace rows; 3-D -- both factor
+// blocks of every plane + rhs/u rows
+static void plan_bytes(const Sweep* s, std::vector<SweepLaunch>& plan) {
+  const double M = (double)s->M;
+  for (auto& fl : plan) {
+    if (fl.kind != SweepLaunch::kSolve) continue;
+    fl.bytes = 0;
+    for (int f = 0; f < fl.nfront; ++f)
+      for (int i = fl.ffirst[f]; i < fl.ffirst[f] + fl.fcount[f]; ++i) {
+        const SweepTask& t = s->tasks[i];
+        if (s->s3) {
+          const double NB = (double)t.T * s->coarse->shape[2];
+          fl.bytes += (2.0 * s->coarse->shape[1] - 1.0) * NB * NB * 16.0 +
+                      M * 16.0 * ((t.b - t.a) + (t.tb - t.ta));
+        } else {
+          fl.bytes += s->rec_bytes + M * 16.0 * ((t.b - t.a) + (t.tb - t.ta)) +
+                      M * 32.0 * ((t.tin1 >= 0) + (t.tin3 >= 0) + (t.out2 >= 0) + (t.out4 >= 0));
+        }
+      }
+  }
 }
 
 int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, const int64_t* bt,
@@ -1905,16 +2022,8 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   s->ntrace = ntin;
     int r = sweep3_create(c, s, coarse, slabs, lo, hi);
     if (!r) r = buffers(s, ntin);
-    if (!r)   // algorithmic bytes per launch: both factor blocks of every plane + rhs/u/traces
-      for (auto& plan : s->plan)
-        for (auto& fl : plan)
-          for (int f = 0; f < fl.nfront; ++f)
-            for (int i = fl.ffirst[f]; i < fl.ffirst[f] + fl.fcount[f]; ++i) {
-              const SweepTask& t = s->tasks[i];
-              const double NB = (double)t.T * coarse->shape[2];
-              fl.bytes += (2.0 * coarse->shape[1] - 1.0) * NB * NB * 16.0 +
-                          (double)s->M * 16.0 * ((t.b - t.a) + (t.tb - t.ta));
-            }
+    if (!r)
+      for (auto& plan : s->plan) plan_bytes(s, plan);
     if (r) {
       sweep_destroy(s);
       return r;
@@ -2040,6 +2149,7 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     }
     s->nr = fits ? kNR : 0;
     g.nr = s->nr;
+    if (fits) s->hrows = rr;
     if (fits) {
       e = cudaMalloc((void**)&s->rows, rr.size() * sizeof(int));
       if (e == cudaSuccess)
@@ -2055,17 +2165,8 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     for (int k = 0; k < C; ++k)
       rec_blocks += TM == 16 ? stream_blocks<16>(g, k) : stream_blocks<32>(g, k);
     const double rec_bytes = rec_blocks * TM2 * 16.0;
-    for (auto& plan : s->plan)
-      for (auto& fl : plan) {
-        if (fl.kind != SweepLaunch::kSolve) continue;
-        for (int f = 0; f < fl.nfront; ++f)
-          for (int i = fl.ffirst[f]; i < fl.ffirst[f] + fl.fcount[f]; ++i) {
-            const SweepTask& t = T[i];
-            double b = rec_bytes + (double)M * 16.0 * ((t.b - t.a) + (t.tb - t.ta));
-            b += (double)M * 32.0 * ((t.tin1 >= 0) + (t.tin3 >= 0) + (t.out2 >= 0) + (t.out4 >= 0));
-            fl.bytes += b;
-          }
-      }
+    s->rec_bytes = rec_bytes;
+    for (auto& plan : s->plan) plan_bytes(s, plan);
   }
 
   const size_t efb = (size_t)J * M * TM2 * sizeof(double2);
@@ -2119,9 +2220,69 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   return HS_OK;
 }
 
+int sweep_plan_nx(Ctx* c, Sweep* s, int ncell, const int64_t* jc, const int64_t* jm,
+                  int* variant) {
+  const int J = s->J;
+  // NxCells.validate (sweepdd.py:376-390)
+  if (ncell < 1 || jc[0] != -1 || jc[ncell] != J + 1)
+    return set_error(c, HS_E_SHAPE, "cell boundaries must start at -1 and end at J+1");
+  for (int i = 0; i < ncell; ++i)
+    if (jc[i] >= jc[i + 1]) return set_error(c, HS_E_SHAPE, "cell boundaries must be strictly increasing");
+  for (int m = 1; m <= ncell; ++m) {
+    const int64_t lo = std::max<int64_t>(1, jc[m - 1] + 1), hi = std::min<int64_t>(J, jc[m] - 1);
+    if (jm[m - 1] < lo || jm[m - 1] > hi) {
+      char buf[128];
+      snprintf(buf, sizeof buf, "cell %d: meeting slab %lld outside [%lld,%lld]", m,
+               (long long)jm[m - 1], (long long)lo, (long long)hi);
+      return set_error(c, HS_E_SHAPE, buf);
+    }
+  }
+  const size_t t0 = s->tasks.size();
+  int ntin = 0;
+  std::vector<SweepLaunch> plan = build_nx(s, ncell, jc, jm, &ntin);
+  auto undo = [&](int rc) {
+    s->tasks.resize(t0);
+    return rc;
+  };
+  if (ntin > std::max(1, s->ntrace))
+    return undo(set_error(c, HS_E_SHAPE, "NX cells need more trace buffers than the sweep has"));
+  if (!s->s3 && s->nr) {   // every row the NX tasks read must be in the slab's restricted set
+    for (size_t i = t0; i < s->tasks.size(); ++i) {
+      const SweepTask& t = s->tasks[i];
+      const int* rs = s->hrows.data() + (size_t)t.slab * kNR;
+      auto has = [&](int x) { return std::find(rs, rs + kNR, x) != rs + kNR; };
+      bool ok = true;
+      for (int x = t.ta + 1 - t.lo; x < t.tb + 1 - t.lo; ++x) ok = ok && has(x);
+      if (t.out2 >= 0) ok = ok && has(t.orow2) && has(t.orow2 + 1);
+      if (t.out4 >= 0) ok = ok && has(t.orow4) && has(t.orow4 + 1);
+      if (!ok) return undo(set_error(c, HS_E_SHAPE, "NX cells read slab rows outside the sweep's row sets"));
+    }
+  }
+  if (s->tasks.size() > (size_t)kMaxTasks * 64)
+    return undo(set_error(c, HS_E_SHAPE, "too many NX plans on one sweep"));
+  plan_bytes(s, plan);
+  if (!s->s3) {   // re-upload the task list (the plan indexes it)
+    SweepTask* d = nullptr;
+    const size_t tb = s->tasks.size() * sizeof(SweepTask);
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&d, tb);
+    if (e == cudaSuccess) e = cudaMemcpy(d, s->tasks.data(), tb, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaFree(d);
+      return undo(check_cuda(c, e, "NX task upload"));
+    }
+    cudaFree(s->d_tasks);
+    s->d_tasks = d;
+  }
+  s->plan.push_back(std::move(plan));
+  *variant = (int)s->plan.size() - 1;
+  return HS_OK;
+}
+
 void sweep_destroy(Sweep* s) {
   if (s) sweep3_destroy(s->s3);
   if (!s) return;
+  delete s->view;
   cudaFree(s->ef);
   cudaFree(s->eb);
   cudaFree(s->kr);
@@ -2165,7 +2326,7 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
                 const SweepWork* w, int first, int last) {
   const SweepWork own{s->trace, s->g, s->u2};
   if (!w) w = &own;
-  if (variant < 0 || variant > 1 || !s->has_plan[variant])
+  if (!s->has_plan(variant))
     return set_error(c, HS_E_ARG,
                      variant == HS_VARIANT_X ? "X-sweep needs an even subdomain count"
                                              : "unknown sweep variant");
@@ -2202,7 +2363,7 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
         }
         SolveArgs a{};
         a.tasks = s->d_tasks;
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kMaxFront; ++i) {
           a.ffirst[i] = i < Lh.nfront ? Lh.ffirst[i] : 0;
           a.fcount[i] = i < Lh.nfront ? Lh.fcount[i] : 0;
         }

@@ -17,11 +17,13 @@ struct SweepTask {
   int dst;         // 0: pass-1 solution u, 1: pass-2 buffer u2 (summed at the end)
 };
 
+constexpr int kMaxFront = 16;   // concurrent fronts (clusters) of one solve launch
+
 struct SweepLaunch {
   enum Kind { kCombine, kSolve, kResidual } kind;
   int src;                  // solve: right-hand side 0 = f, 1 = g (mid-sweep residual)
   int nfront;
-  int ffirst[2], fcount[2]; // front task ranges (global task indices)
+  int ffirst[kMaxFront], fcount[kMaxFront];   // front task ranges (global task indices)
   double bytes;             // algorithmic HBM bytes of the launch (profiler)
 };
 
@@ -65,11 +67,18 @@ struct Sweep {
   double2* u2 = nullptr;        // [n0*M] second-pass contributions
   SweepTask* d_tasks = nullptr;
   std::vector<SweepTask> tasks;
-  std::vector<SweepLaunch> plan[2];   // by variant (UD, X)
-  bool has_plan[2] = {false, false};
+  // launch plans by variant id: HS_VARIANT_UD, HS_VARIANT_X, then one per NX
+  // cell grouping (sweep_plan_nx); an empty plan = variant not available
+  std::vector<std::vector<SweepLaunch>> plan = std::vector<std::vector<SweepLaunch>>(2);
+  bool has_plan(int v) const { return v >= 0 && v < (int)plan.size() && !plan[v].empty(); }
+  // host copies of the partition geometry (NX plans are built after setup)
+  std::vector<int64_t> hbeta, hbt, hlo, hhi;
+  std::vector<int> hrows;       // [J][kNR] restricted-update rows (nr != 0)
+  double rec_bytes = 0;         // streamed factor bytes per 2-D slab solve (profiler)
   long long factor_bytes = 0;
   int ntrace = 0;               // trace buffers of the schedules
   Sweep3* s3 = nullptr;         // 3-D level: block LU slabs, host-driven tasks
+  Stencil* view = nullptr;      // exact solver: owned 3-axis view of the operator
 };
 
 int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, const int64_t* bt,
@@ -79,6 +88,11 @@ void sweep_destroy(Sweep* s);
 int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
                 const SweepWork* w = nullptr, int first = 0, int last = -1);
 // allocate / free a SweepWork sized for s (2-D levels only)
+// NX schedule (prec_nx, sweepdd.py:403-437) for one cell grouping: j_cell
+// (ncell + 1 entries, sentinels -1 and J + 1) and j_mid (ncell entries);
+// returns the plan's variant id in *variant
+int sweep_plan_nx(Ctx* c, Sweep* s, int ncell, const int64_t* j_cell, const int64_t* j_mid,
+                  int* variant);
 int sweep_work_create(Ctx* c, const Sweep* s, SweepWork* w);
 void sweep_work_destroy(SweepWork* w);
 
@@ -87,5 +101,10 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
 int sweep3_task(Ctx* c, Sweep* s, const SweepTask& t, const double2* src, double2* const* u,
                 const double2* coarse_coeffs, int64_t coarse_n);
 void sweep3_destroy(Sweep3* s3);
+// Exact solver of a whole operator (ExactCoarseSolver / factorize,
+// twogrid.py:99-105, sparselin.py:40-68): the operator as ONE block-LU slab
+// (hs_sweep3.cu) behind the sweep interface -- plan HS_VARIANT_UD is a single
+// slab solve over every row.
+int exact_create(Ctx* c, const Stencil* op, Sweep** out);
 
 }  // namespace hs

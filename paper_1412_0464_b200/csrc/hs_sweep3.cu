@@ -374,7 +374,7 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
       cudaMalloc((void**)&Di, blk) || cudaMalloc((void**)&Xc, blk) ||
       cudaMalloc((void**)&s3->gbar, sizeof(unsigned)) ||
       cudaMalloc((void**)&ipiv, NBmax * sizeof(int)) ||
-      cudaMalloc((void**)&info, (size_t)n1 * J * sizeof(int)) ||
+      cudaMalloc((void**)&info, ((size_t)n1 * J + 1) * sizeof(int)) ||
       cudaMalloc((void**)&s3->F, (size_t)n1 * NBmax * sizeof(double2)) ||
       cudaMalloc((void**)&s3->Y, (size_t)n1 * NBmax * sizeof(double2)))
     return done(set_error(c, HS_E_CUDA, "3-D sweep work allocation failed"));
@@ -428,8 +428,10 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
                                info + j * n1 + i1), "getrf");
       k3_eye<<<(unsigned)((nb2 + kT3 - 1) / kT3), kT3, 0, c->stream>>>(Di, NB);
       c->launches++;
+      // (getrs reports argument errors only: its own slot, so that getrf's
+      // singular-pivot code survives for the check below)
       S3_BLAS(cusolverDnZgetrs(sol, CUBLAS_OP_N, NB, NB, (cuDoubleComplex*)D, NB, ipiv,
-                               (cuDoubleComplex*)Di, NB, info + j * n1 + i1), "getrs");
+                               (cuDoubleComplex*)Di, NB, info + (size_t)n1 * J), "getrs");
       // stored row-major (= the column-major transpose) for the solve kernel's rows
       S3_BLAS(cublasZgeam(s3->blas, CUBLAS_OP_T, CUBLAS_OP_N, NB, NB, &one, (cuDoubleComplex*)Di,
                           NB, &zero, (cuDoubleComplex*)Di, NB, (cuDoubleComplex*)(dv + i1 * nb2),
@@ -529,6 +531,73 @@ int sweep3_task(Ctx* c, Sweep* s, const SweepTask& t, const double2* src, double
   k3_out<<<(unsigned)((tot + kT3 - 1) / kT3), kT3, 0, c->stream>>>(t, n1, n2, s3->Y, u[t.dst],
                                                                    s->trace);
   HS_LAUNCH_CHECK(c, "3-D outputs");
+  return HS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// exact solver: the operator viewed as a single slab.  Canonical shapes are
+// (1, a, b) for 2-D and (1, 1, a) for 1-D; the view puts the user's first
+// axis on the slab's layer axis so that the blocks are planes of the
+// second axis: 2-D (a, b) -> (T = a, n1 = b, n2 = 1), NB = a; 3-D keeps
+// (a, b, c), NB = a c; 1-D (a) -> (1, a, 1).  Same memory layout in every
+// case (only the axis bookkeeping changes).
+int exact_create(Ctx* c, const Stencil* op, Sweep** out) {
+  Stencil* v = new Stencil(*op);
+  v->coeffs = nullptr;   // borrowed: the operator owns its coefficients
+  v->invd = nullptr;
+  v->dim = 3;
+  const StencilDesc& d = op->d;
+  int64_t sh[3];
+  if (op->dim == 3) {
+    sh[0] = d.n0; sh[1] = d.n1; sh[2] = d.n2;
+  } else if (op->dim == 2) {
+    sh[0] = d.n1; sh[1] = d.n2; sh[2] = 1;
+  } else {
+    sh[0] = 1; sh[1] = d.n2; sh[2] = 1;
+  }
+  for (int s_ = 0; s_ < d.S; ++s_) {
+    int8_t o[3] = {d.off[s_][0], d.off[s_][1], d.off[s_][2]};
+    if (op->dim == 2) { o[0] = d.off[s_][1]; o[1] = d.off[s_][2]; o[2] = 0; }
+    if (op->dim == 1) { o[0] = 0; o[1] = d.off[s_][2]; o[2] = 0; }
+    for (int k = 0; k < 3; ++k) v->d.off[s_][k] = o[k];
+  }
+  for (int k = 0; k < 3; ++k) v->shape[k] = sh[k];
+  v->d.n0 = sh[0]; v->d.n1 = sh[1]; v->d.n2 = sh[2];
+  Sweep* s = new Sweep();
+  s->view = v;
+  s->J = 1;
+  s->n0 = (int)sh[0];
+  s->M = (int)(sh[1] * sh[2]);
+  s->coarse = v;
+  const int64_t lo = 1, hi = sh[0];
+  SweepTask t{};
+  t.slab = 0;
+  t.lo = 1;
+  t.T = (int)sh[0];
+  t.a = 0;
+  t.b = (int)sh[0];
+  t.ta = 0;
+  t.tb = (int)sh[0];
+  t.tin1 = t.tin3 = t.out2 = t.out4 = -1;
+  t.row1 = t.row3 = t.orow2 = t.orow4 = -1;
+  t.dst = 0;
+  s->tasks.push_back(t);
+  SweepLaunch fl{};
+  fl.kind = SweepLaunch::kSolve;
+  fl.src = 0;
+  fl.nfront = 1;
+  fl.ffirst[0] = 0;
+  fl.fcount[0] = 1;
+  const Stencil* slabs[1] = {v};
+  int r = sweep3_create(c, s, v, slabs, &lo, &hi);
+  if (r) {
+    sweep_destroy(s);
+    return r;
+  }
+  fl.bytes = (2.0 * sh[1] - 1.0) * (double)sh[0] * sh[2] * (double)sh[0] * sh[2] * 16.0 +
+             32.0 * (double)sh[0] * sh[1] * sh[2];
+  s->plan[HS_VARIANT_UD].push_back(fl);
+  *out = s;
   return HS_OK;
 }
 

@@ -214,11 +214,59 @@ class DeviceSweep(_Handle):
     def factor_bytes(self) -> int:
         return int(self.ctx.lib.hs_sweep_factor_bytes(self.h))
 
-    def apply(self, f, variant="x"):
-        v = _lib.HS_VARIANT_X if variant == "x" else _lib.HS_VARIANT_UD
+    def variant_id(self, variant="x", cells=None) -> int:
+        """C-ABI variant id: HS_VARIANT_X / HS_VARIANT_UD, or the plan of an
+        NX cell grouping (registered once per grouping, hs_sweep_plan_nx)."""
+        if variant == "x":
+            return _lib.HS_VARIANT_X
+        if variant == "ud":
+            return _lib.HS_VARIANT_UD
+        if variant != "nx" or cells is None:
+            raise ValueError(f"unknown sweep variant {variant!r}")
+        key = (tuple(int(v) for v in cells.j_cell), tuple(int(v) for v in cells.j_mid))
+        plans = self.__dict__.setdefault("_nx_plans", {})
+        if key not in plans:
+            jc, pjc = i64(key[0])
+            jm, pjm = i64(key[1])
+            v = C.c_int()
+            self.ctx.call("hs_sweep_plan_nx", self.h, len(key[1]), pjc, pjm, C.byref(v))
+            plans[key] = int(v.value)
+        return plans[key]
+
+    def apply(self, f, variant="x", cells=None):
+        v = self.variant_id(variant, cells)
         ft, was_np = to_device(f, self.n, self.ctx)
         u = empty(self.n, self.ctx)
         self.ctx.call("hs_sweep_apply", self.h, v, ptr(ft), ptr(u))
+        return u, was_np
+
+
+class DeviceExact(_Handle):
+    """Exact solver of a whole stencil operator (hs_exact_create): one block-LU
+    slab behind the sweep interface (variant HS_VARIANT_UD)."""
+
+    _destroy = "hs_sweep_destroy"
+
+    def __init__(self, op: DeviceStencil):
+        self.ctx = op.ctx
+        self.op = op              # the factors copy the coefficients; kept for shape
+        self.n = op.n
+        self.shape = op.shape
+        h = C.c_void_p()
+        self.ctx.call("hs_exact_create", op.h, C.byref(h))
+        self.h = h
+
+    @property
+    def factor_bytes(self) -> int:
+        return int(self.ctx.lib.hs_sweep_factor_bytes(self.h))
+
+    def variant_id(self, variant="ud", cells=None) -> int:
+        return _lib.HS_VARIANT_UD
+
+    def apply(self, f, variant="ud", cells=None):
+        ft, was_np = to_device(f, self.n, self.ctx)
+        u = empty(self.n, self.ctx)
+        self.ctx.call("hs_sweep_apply", self.h, _lib.HS_VARIANT_UD, ptr(ft), ptr(u))
         return u, was_np
 
 
@@ -228,11 +276,13 @@ class DeviceCycle(_Handle):
     _destroy = "hs_cycle_destroy"
 
     def __init__(self, fine: DeviceStencil, transfer: DeviceTransfer, coarse: DeviceStencil,
-                 sweep: DeviceSweep, omega_jac, nu, restrict_scale, variant, ctx=None):
+                 sweep, omega_jac, nu, restrict_scale, variant, ctx=None, cells=None):
+        """``sweep``: a DeviceSweep or DeviceExact; ``variant``: a C-ABI
+        variant id, or "x" / "ud" / "nx" (with ``cells``)."""
         self.ctx = ctx or context()
         self.fine, self.transfer, self.coarse, self.sweep = fine, transfer, coarse, sweep
         self.n = fine.n
-        v = _lib.HS_VARIANT_X if variant == "x" else _lib.HS_VARIANT_UD
+        v = variant if isinstance(variant, int) else sweep.variant_id(variant, cells)
         h = C.c_void_p()
         self.ctx.call("hs_cycle_create", fine.h, transfer.h, coarse.h, sweep.h,
                       float(omega_jac), int(nu), float(restrict_scale), v, C.byref(h))

@@ -246,7 +246,11 @@ class CudaShardBackend:
             self.fine[g] = DeviceStencil(shape, offs, co, self.ctx)
             self.transfer[g] = DeviceTransfer(hh.cmap, self.ctx, window=p.window)
         self.sweep = hh.partition.device()
-        self.variant = 1 if hh.sweep.variant == "x" else 0
+        cells = hh.sweep.n_cell
+        if hh.sweep.variant == "nx" and isinstance(cells, (int, np.integer)):
+            from .sweepdd import make_nx_cells
+            cells = make_nx_cells(hh.partition.J, int(cells))
+        self.variant = self.sweep.variant_id(hh.sweep.variant, cells)
         self.nc = int(np.prod(hh.coarse_op.shape))
         self.omega = float(hh.smoother.omega_jac)
         self.nu = int(hh.smoother.nu)

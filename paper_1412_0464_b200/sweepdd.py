@@ -8,6 +8,7 @@ Drop-in names of reference ``sweepdd.py``:
 * ``spaced_interfaces``, ``default_subdomain_count``    :179-189
 * ``build_partition``                                    :192-218
 * ``prec_ud``, ``prec_x``, ``SweepingPreconditioner``    :312-359, :437-467
+* ``NxCells``, ``make_nx_cells``, ``prec_nx``           :362-434
 
 Setup (geometry, slab operator assembly) runs on the host; the slabs are
 factorised on the device at ``build_partition`` time and every application
@@ -247,10 +248,10 @@ def extract_transmission(part: Partition, j: int, direction: str) -> Transmissio
 # ---------------------------------------------------------------------------
 # applications (device)
 
-def _apply(part: Partition, f, variant: str):
+def _apply(part: Partition, f, variant: str, cells=None):
     from .device import from_device
     shape = part.shape
-    u, was_np = part.device().apply(f, variant)
+    u, was_np = part.device().apply(f, variant, cells)
     if was_np:
         return from_device(u, True, shape)
     return u.reshape(f.shape) if hasattr(f, "shape") else u
@@ -268,6 +269,57 @@ def prec_x(part: Partition, f, parallel: bool = False):
     return _apply(part, f, "x")
 
 
+@dataclass(frozen=True)
+class NxCells:
+    """Grouping for partial intersecting sweeps (reference sweepdd.py:362-390):
+    cell boundaries with -1 and J+1 sentinels and each cell's meeting slab."""
+
+    j_cell: tuple
+    j_mid: tuple
+
+    @property
+    def n_cell(self):
+        return len(self.j_cell) - 1
+
+    def validate(self, J):
+        jc, jm = self.j_cell, self.j_mid
+        if jc[0] != -1 or jc[-1] != J + 1:
+            raise ValueError("cell boundaries must start at -1 and end at J+1")
+        if len(jm) != self.n_cell:
+            raise ValueError("one meeting slab per cell required")
+        if any(jc[i] >= jc[i + 1] for i in range(len(jc) - 1)):
+            raise ValueError("cell boundaries must be strictly increasing")
+        for m in range(1, self.n_cell + 1):
+            lo = max(1, jc[m - 1] + 1)
+            hi = min(J, jc[m] - 1)
+            if not lo <= jm[m - 1] <= hi:
+                raise ValueError(f"cell {m}: meeting slab {jm[m - 1]} outside [{lo},{hi}]")
+
+
+def make_nx_cells(J: int, n_cell: int) -> NxCells:
+    """Evenly spaced cells, each meeting at its middle slab (sweepdd.py:392-401)."""
+    if not 1 <= n_cell <= J // 2:
+        raise ValueError(f"need 1 <= n_cell <= J/2, got {n_cell} for J={J}")
+    bounds = [-1] + [round(m * J / n_cell) for m in range(1, n_cell)] + [J + 1]
+    mids = []
+    for m in range(1, n_cell + 1):
+        lo = max(1, bounds[m - 1] + 1)
+        hi = min(J, bounds[m] - 1)
+        mids.append((lo + hi + 1) // 2)
+    cells = NxCells(tuple(bounds), tuple(mids))
+    cells.validate(J)
+    return cells
+
+
+def prec_nx(part: Partition, f, cells: NxCells):
+    """NX sweep: partial intersecting X sweeps over slab groups (sweepdd.py:
+    403-434).  Every cell's fronts run concurrently on the device (one
+    cluster per front); the group-boundary input solve runs after both
+    neighbouring cells, as in the reference."""
+    cells.validate(part.J)
+    return _apply(part, f, "nx", cells)
+
+
 @dataclass
 class SweepingPreconditioner:
     part: Partition
@@ -281,10 +333,18 @@ class SweepingPreconditioner:
         if self.variant == "x" and self.part.J % 2 != 0:
             raise ValueError(f"X-sweep needs an even subdomain count, got {self.part.J}")
         if self.variant == "nx":
-            raise ValueError("NX sweep is not implemented on the device (out of scope, "
-                             "SURVEY 8(f))")
+            if isinstance(self.cells, (int, np.integer)):
+                self.cells = make_nx_cells(self.part.J, int(self.cells))
+            if self.cells is None:
+                raise ValueError("NX-sweep needs its cell grouping")
+            self.cells.validate(self.part.J)
 
     def __call__(self, f):
         flat = np.ndim(f) == 1 if not hasattr(f, "dim") else f.dim() == 1
-        u = prec_x(self.part, f) if self.variant == "x" else prec_ud(self.part, f)
+        if self.variant == "x":
+            u = prec_x(self.part, f)
+        elif self.variant == "ud":
+            u = prec_ud(self.part, f)
+        else:
+            u = prec_nx(self.part, f, self.cells)
         return u.reshape(-1) if flat else u

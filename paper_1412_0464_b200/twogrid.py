@@ -117,6 +117,24 @@ def restrict(cmap: CoarseningMap, r_fine):
 # ---------------------------------------------------------------------------
 # coarse solvers
 
+class ExactCoarseSolver:
+    """Exact coarse solve (twogrid.py:99-105): device block-LU factors of the
+    coarse operator (:class:`.sparselin.Factorization`)."""
+
+    def __init__(self, factor, shape):
+        self.factor = factor
+        self.shape = tuple(shape)
+
+    def solve(self, rc):
+        out = self.factor.solve(rc.reshape(-1) if hasattr(rc, "reshape") else rc)
+        return out.reshape(self.shape)
+
+    def device_plan(self):
+        """(device solver handle, C-ABI variant id) for hs_cycle_create."""
+        dev = self.factor.device
+        return dev, dev.variant_id()
+
+
 class SweepCoarseSolver:
     """One sweep application, never iterated."""
 
@@ -126,6 +144,10 @@ class SweepCoarseSolver:
 
     def solve(self, rc):
         return self.prec(rc.reshape(self.shape) if hasattr(rc, "reshape") else rc)
+
+    def device_plan(self):
+        sw = self.prec.part.device()
+        return sw, sw.variant_id(self.prec.variant, self.prec.cells)
 
 
 class FineOperator:
@@ -172,12 +194,10 @@ class TwoGridCycle:
         if self._dev is None:
             from .device import DeviceCycle, DeviceTransfer
             fine = self.fine_op.device()
-            part = self.coarse_solver.prec.part
-            sweep = part.device()
+            solver, vid = self.coarse_solver.device_plan()
             self._dev = DeviceCycle(fine, DeviceTransfer(self.cmap, fine.ctx),
-                                    self.coarse_op.device(), sweep, self.smoother.omega_jac,
-                                    self.smoother.nu, self.restrict_scale, self.variant,
-                                    fine.ctx)
+                                    self.coarse_op.device(), solver, self.smoother.omega_jac,
+                                    self.smoother.nu, self.restrict_scale, vid, fine.ctx)
         return self._dev
 
     def vcycle(self, f):
@@ -314,7 +334,7 @@ class HostHierarchy:
 
 def build_hierarchy(mesh: Mesh, model: WaveModel, fine_op=None, smoother=None, sweep=None,
                     table=None, device=True, keep_slab_ops=True,
-                    assembly: str | None = None) -> HostHierarchy:
+                    assembly: str | None = None, coarse: str = "sweep") -> HostHierarchy:
     """Assembly of the TGSP hierarchy (reference twogrid.py:196-229).
 
     ``assembly="device"`` (the default when ``device``): the fine FD operator,
@@ -346,8 +366,10 @@ def build_hierarchy(mesh: Mesh, model: WaveModel, fine_op=None, smoother=None, s
     if smoother is None:
         smoother = SmootherConfig(omega_jac=0.8 if mesh.dim == 2 else 0.6, nu=3)
     sweep = sweep or SweepOptions()
-    part = build_partition(clevel, sweep.w_dd, sweep.s_dd, J=sweep.subdomains, device=device,
-                           keep_slab_ops=keep_slab_ops)
+    part = None
+    if coarse == "sweep":
+        part = build_partition(clevel, sweep.w_dd, sweep.s_dd, J=sweep.subdomains,
+                               device=device, keep_slab_ops=keep_slab_ops)
     h = float(mesh.spacing[0][0])
     return HostHierarchy(mesh, flevel.op, clevel.op, cmap, clevel, part, smoother, sweep,
                          h ** mesh.dim)
@@ -357,23 +379,30 @@ def build_two_grid(mesh: Mesh, model: WaveModel, fine_op: StencilOperator | None
                    smoother: SmootherConfig | None = None, coarse: str = "exact",
                    sweep: SweepOptions | None = None, table=None, keep_slab_ops=True,
                    assembly: str = "device"):
-    """Assemble the two-grid hierarchy; returns (cycle, coarse level).
+    """Assemble the two-grid hierarchy; returns (cycle, coarse level)
+    (twogrid.py:196-229).
 
-    ``coarse="sweep"`` is the TGSP path (device).  ``coarse="exact"`` (a
-    sparse direct coarse solve) is out of this build's scope.
+    ``coarse="sweep"``: the TGSP path (one sweep application per cycle).
+    ``coarse="exact"``: the coarse operator factorised on the device (block
+    LU, :mod:`.sparselin`) and solved exactly in every cycle.
     """
-    if coarse == "exact":
-        raise ValueError("coarse solver 'exact' is outside the GPU path; use coarse='sweep'")
-    if coarse != "sweep":
+    if coarse not in ("exact", "sweep"):
         raise ValueError(f"coarse solver must be 'exact' or 'sweep', got {coarse!r}")
     sweep = sweep or SweepOptions()
-    if sweep.variant not in ("ud", "x"):
-        raise ValueError(f"sweep variant {sweep.variant!r} is not implemented on the device")
+    if sweep.variant not in ("ud", "x", "nx"):
+        raise ValueError(f"unknown sweep variant {sweep.variant!r}")
     hh = build_hierarchy(mesh, model, fine_op, smoother, sweep, table,
-                         keep_slab_ops=keep_slab_ops, assembly=assembly)
-    prec = SweepingPreconditioner(hh.partition, sweep.variant, parallel=sweep.parallel)
-    cycle = TwoGridCycle(hh.fine_op, hh.coarse_op, hh.cmap, hh.smoother,
-                         SweepCoarseSolver(prec), restrict_scale=hh.restrict_scale,
-                         variant=sweep.variant)
+                         keep_slab_ops=keep_slab_ops, assembly=assembly, coarse=coarse)
+    if coarse == "exact":
+        from .sparselin import factorize
+        solver = ExactCoarseSolver(factorize(hh.coarse_op), hh.coarse_op.shape)
+        variant = "exact"
+    else:
+        prec = SweepingPreconditioner(hh.partition, sweep.variant, cells=sweep.n_cell,
+                                      parallel=sweep.parallel)
+        solver = SweepCoarseSolver(prec)
+        variant = sweep.variant
+    cycle = TwoGridCycle(hh.fine_op, hh.coarse_op, hh.cmap, hh.smoother, solver,
+                         restrict_scale=hh.restrict_scale, variant=variant)
     cycle.hierarchy = hh
     return cycle, hh.clevel

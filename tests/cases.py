@@ -54,6 +54,10 @@ def case(name):
         mesh, model = constant_case(3, 16, AbsorbingLayerSpec(PML, 3, 15.0), 8.0)
         return mesh, model, None, hb.SmootherConfig(0.6, 2), hb.SweepOptions(3, 15.0, "x",
                                                                              subdomains=4)
+    if name == "nx2d":
+        mesh, model = hetero_case(64, 8, 8.0, seed=5)
+        return mesh, model, None, hb.SmootherConfig(0.8, 2), hb.SweepOptions(
+            5, 25.0, "nx", n_cell=2, subdomains=8)
     raise KeyError(name)
 
 

@@ -10,8 +10,10 @@ GOLDEN = ROOT / "tests" / "golden"
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
 
-CASES = ["pml2d", "wedge2d", "sponge2d", "fe9_2d", "pml3d", "pml3d_s"]
-SOLVED = ["pml2d", "wedge2d", "sponge2d", "pml3d_s"]
+CASES = ["pml2d", "wedge2d", "sponge2d", "fe9_2d", "pml3d", "pml3d_s", "nx2d"]
+SOLVED = ["pml2d", "wedge2d", "sponge2d", "pml3d_s", "nx2d"]
+# NX groupings stored in nx2d.npz: make_nx_cells(8, n) for n = 1..4 and a hand grouping
+NX_KEYS = ["nx1", "nx2", "nx3", "nx4", "nxc"]
 
 
 def pytest_configure(config):

@@ -199,7 +199,96 @@ def known_answers():
     np.savez_compressed(OUT / "known_answers.npz", **out)
 
 
+NX_CUSTOM = ((-1, 3, 6, 9), (1, 5, 7))   # J = 8: empty forward / backward chains in both passes
+
+
+def nx_fixture():
+    """NX sweep (prec_nx, sweepdd.py:403-434) on a J = 8 wedge case: the TGSP
+    cycle with NX(2) coarse sweeps plus raw prec_nx outputs for n_cell 1..4
+    and a hand grouping whose cells have empty chains."""
+    mesh, model = hetero_case(64, 8, 8.0, seed=5)
+    case_fixture("nx2d", mesh, model, SmootherConfig(0.8, 2),
+                 SweepOptions(5, 25.0, "nx", n_cell=2, subdomains=8))
+    path = OUT / "nx2d.npz"
+    d = dict(np.load(path))
+    cycle, clevel = hs.build_two_grid(mesh, model, smoother=SmootherConfig(0.8, 2),
+                                      coarse="sweep",
+                                      sweep=SweepOptions(5, 25.0, "nx", n_cell=2, subdomains=8))
+    part = cycle.coarse_solver.prec.part
+    xc = d["probe_xc"]
+    for nc in (1, 2, 3, 4):
+        cells = hs.sweepdd.make_nx_cells(part.J, nc)
+        d[f"nx{nc}_cells"] = np.array(cells.j_cell)
+        d[f"nx{nc}_mid"] = np.array(cells.j_mid)
+        d[f"sweep_nx{nc}"] = hs.sweepdd.prec_nx(part, xc, cells)
+    cells = hs.sweepdd.NxCells(*NX_CUSTOM)
+    d["nxc_cells"] = np.array(cells.j_cell)
+    d["nxc_mid"] = np.array(cells.j_mid)
+    d["sweep_nxc"] = hs.sweepdd.prec_nx(part, xc, cells)
+    np.savez_compressed(path, **d)
+    print("nx2d: n_cell 1..4 + custom grouping")
+
+
+def exact_fixture():
+    """Exact coarse solve (ExactCoarseSolver, factorize / SuperLU): a 2-D
+    two-grid cycle with coarse="exact" (vcycle + GMRES) and factorize().solve
+    on the 2-D and 3-D coarse operators and a 1-D operator."""
+    out = {}
+    rng = np.random.default_rng(11)
+    mesh, model = constant_case(2, 32, AbsorbingLayerSpec(PML, 4, 20.0), 10.0)
+    cycle, clevel = hs.build_two_grid(mesh, model, smoother=SmootherConfig(0.8, 2),
+                                      coarse="exact")
+    pack_op("fine_", cycle.fine_op, out)
+    pack_op("coarse_", clevel.op, out)
+    out["fine_shape"] = np.array(cycle.fine_op.shape)
+    out["coarse_shape"] = np.array(clevel.op.shape)
+    _, cmap = hs.coarsen_mesh(mesh)
+    for a in range(mesh.dim):
+        out[f"fp{a}"] = cmap.fine_point_of_coarse[a]
+        out[f"refined{a}"] = cmap.refined_cell[a]
+    out["restrict_scale"] = np.array(cycle.restrict_scale)
+    out["omega_jac"] = np.array(cycle.smoother.omega_jac)
+    out["nu"] = np.array(cycle.smoother.nu)
+    z = crand(np.random.default_rng(0), cycle.fine_op.shape)
+    out["vcycle_z"] = z
+    out["vcycle_out"] = cycle.vcycle(z)
+    b = crand(rng, clevel.op.n)
+    out["coarse_b"] = b
+    out["coarse_x"] = hs.factorize(clevel.op).solve(b)
+    f = point_rhs(mesh)
+    out["rhs"] = f
+    u, rep = hs.gmres(lambda v: cycle.fine_csr @ v, cycle.as_preconditioner(), f.ravel(),
+                      hs.GmresConfig(tol=1e-6, max_iter=200, restart=20))
+    out["gmres_u"] = u.reshape(mesh.unknowns)
+    out["gmres_history"] = rep.residual_history
+    out["gmres_iterations"] = np.array(rep.iterations)
+    # 3-D coarse operator (pml3d recipe) and a 1-D PML operator
+    mesh3, model3 = constant_case(3, 8, AbsorbingLayerSpec(PML, 3, 15.0), 6.0)
+    _, cl3 = hs.build_two_grid(mesh3, model3, smoother=SmootherConfig(0.6, 2), coarse="exact")
+    pack_op("c3_", cl3.op, out)
+    out["c3_shape"] = np.array(cl3.op.shape)
+    b3 = crand(rng, cl3.op.n)
+    out["c3_b"] = b3
+    out["c3_x"] = hs.factorize(cl3.op).solve(b3)
+    mesh1 = hs.build_mesh(1, 64, 1.0 / 64, AbsorbingLayerSpec(PML, 8, 20.0))
+    op1 = hs.assemble_fine(mesh1, hs.WaveModel.constant(mesh1, 2 * np.pi * 64 / 10.0))
+    pack_op("l1_", op1, out)
+    out["l1_shape"] = np.array(op1.shape)
+    b1 = crand(rng, op1.n)
+    out["l1_b"] = b1
+    out["l1_x"] = hs.factorize(op1).solve(b1)
+    np.savez_compressed(OUT / "exact2d.npz", **out)
+    print(f"exact2d: coarse {clevel.op.shape} its={rep.iterations}; 3-D coarse {cl3.op.shape}; "
+          f"1-D {op1.shape}")
+
+
 def main():
+    if sys.argv[1:] == ["nx"]:
+        nx_fixture()
+        return
+    if sys.argv[1:] == ["exact"]:
+        exact_fixture()
+        return
     sm2 = SmootherConfig(0.8, 2)
     mesh, model = constant_case(2, 32, AbsorbingLayerSpec(PML, 4, 20.0), 10.0)
     case_fixture("pml2d", mesh, model, sm2, SweepOptions(3, 15.0, "x", subdomains=4))
@@ -219,6 +308,8 @@ def main():
                  SweepOptions(3, 15.0, "x", subdomains=4))
     known_answers()
     c1_anchors()
+    nx_fixture()
+    exact_fixture()
 
 
 if __name__ == "__main__":

@@ -9,7 +9,7 @@ GMRES iteration count +-1 and final true relative residual <= 1e-6.
 import numpy as np
 import pytest
 
-from conftest import CASES, SOLVED, c1_anchors, crand, load_case, rel
+from conftest import CASES, NX_KEYS, SOLVED, c1_anchors, crand, load_case, rel
 from cases import case, hierarchy, point_rhs
 
 pytestmark = pytest.mark.gpu
@@ -80,6 +80,37 @@ def test_sweeps(golden):
     if part.J % 2 == 0:
         assert rel(hb.prec_x(part, d["probe_xc"]), d["sweep_x"]) < 1e-11
     assert rel(hb.prec_ud(part, d["probe_xc"]), d["sweep_ud"]) < 1e-11
+    for k in NX_KEYS:   # NX groupings (nx2d): every cell's fronts in one launch
+        if f"sweep_{k}" in d:
+            cells = hb.NxCells(tuple(int(v) for v in d[f"{k}_cells"]),
+                               tuple(int(v) for v in d[f"{k}_mid"]))
+            assert rel(hb.prec_nx(part, d["probe_xc"], cells), d[f"sweep_{k}"]) < 1e-11, k
+            prec = hb.SweepingPreconditioner(part, "nx", cells=cells)
+            assert rel(prec(d["probe_xc"].ravel()), d[f"sweep_{k}"]) < 1e-11, k
+
+
+def test_nx_sweep_3d_matches_oracle(rng):
+    """NX on a 3-D level (host-driven block-LU slab solves) vs the oracle."""
+    import paper_1412_0464_b200 as hb
+    from oracle import tgsp_oracle as orc
+    hh = hierarchy("pml3d_s", device=True)
+    part = hh.partition
+    tg = orc.from_hierarchy(hierarchy("pml3d_s"))
+    f = crand(rng, part.shape)
+    cells = hb.make_nx_cells(part.J, 2)
+    ref = tg.part.prec_nx(f, cells.j_cell, cells.j_mid)
+    assert rel(hb.prec_nx(part, f, cells), ref) < 1e-11
+
+
+def test_nx_cell_validation():
+    """test_sweepdd.py:249-255: invalid groupings raise ValueError."""
+    import paper_1412_0464_b200 as hb
+    hh = hierarchy("nx2d", device=True)
+    bad = hb.NxCells((-1, 4, 9), (2, 9))
+    with pytest.raises(ValueError):
+        hb.prec_nx(hh.partition, np.zeros(hh.partition.shape, complex), bad)
+    with pytest.raises(ValueError):
+        hb.make_nx_cells(8, 5)
 
 
 def test_tgsp_apply(golden):
@@ -293,3 +324,65 @@ def test_device_assembly_matches_host(name):
     for (lo, hi, op), (lo2, hi2, op2) in zip(dev.slabs, host.slabs):
         assert (lo, hi) == (lo2, hi2)
         close(op, op2)
+
+
+def _op(d, p):
+    import paper_1412_0464_b200 as hb
+    return hb.StencilOperator(tuple(int(v) for v in d[f"{p}_shape"]),
+                              {tuple(int(o) for o in off): c
+                               for off, c in zip(d[f"{p}_offsets"], d[f"{p}_coeffs"])})
+
+
+def test_factorize_matches_reference():
+    """factorize(op).solve (device block LU) vs the reference's SuperLU solve on
+    2-D / 3-D coarse operators and a 1-D PML operator."""
+    import paper_1412_0464_b200 as hb
+    d = load_case("exact2d")
+    for p, b, x in (("coarse", "coarse_b", "coarse_x"), ("c3", "c3_b", "c3_x"),
+                    ("l1", "l1_b", "l1_x")):
+        fac = hb.factorize(_op(d, p))
+        assert rel(fac.solve(d[b]), d[x]) < 1e-10, p
+    # several right-hand sides equal sequential solves (test_sparselin.py:66-72)
+    fac = hb.factorize(_op(d, "coarse"))
+    rng = np.random.default_rng(3)
+    B = crand(rng, (fac.n, 3))
+    X = fac.solve(B)
+    for j in range(3):
+        assert np.array_equal(X[:, j], fac.solve(B[:, j]))
+    with pytest.raises(ValueError):
+        fac.solve(np.zeros(fac.n + 1, complex))
+
+
+def test_factorize_known_answers():
+    """test_sparselin.py:39-47 and :58-63: scalar / tridiagonal hand solves and
+    the zero-pivot error class."""
+    import paper_1412_0464_b200 as hb
+    ka = load_case("known_answers")
+    two, one = np.full(3, 2.0, complex), np.full(3, -1.0, complex)
+    op = hb.StencilOperator((3,), {(0,): two, (-1,): one, (1,): one})
+    assert rel(hb.factorize(op).solve(np.ones(3, complex)), ka["tridiag_solve"]) < 1e-14
+    op = hb.StencilOperator((1,), {(0,): np.array([2.0 + 0j])})
+    assert abs(hb.factorize(op).solve(np.array([1.0 + 0j]))[0] - 0.5) < 1e-15
+    sing = hb.StencilOperator((4, 4), {(0, 0): np.zeros((4, 4), complex),
+                                       (1, 0): np.ones((4, 4), complex)})
+    with pytest.raises(ZeroDivisionError, match="zero pivot"):
+        hb.factorize(sing)
+
+
+def test_exact_coarse_cycle_and_gmres():
+    """build_two_grid(coarse="exact"): V-cycle vs the reference (1e-10), GMRES
+    iterations +-1, and tgsp_apply refuses a cycle without a sweep."""
+    import paper_1412_0464_b200 as hb
+    from cases import constant_case
+    from paper_1412_0464_b200.mesh import PML, AbsorbingLayerSpec
+    d = load_case("exact2d")
+    mesh, model = constant_case(2, 32, AbsorbingLayerSpec(PML, 4, 20.0), 10.0)
+    cycle, _ = hb.build_two_grid(mesh, model, smoother=hb.SmootherConfig(0.8, 2),
+                                 coarse="exact")
+    assert rel(cycle.vcycle(d["vcycle_z"]), d["vcycle_out"]) < 1e-10
+    u, rep = hb.gmres(cycle.fine_csr, cycle.as_preconditioner(), d["rhs"].ravel(),
+                      hb.GmresConfig(tol=1e-6, max_iter=200, restart=20))
+    assert abs(rep.iterations - int(d["gmres_iterations"])) <= 1 and rep.converged
+    assert rel(u, d["gmres_u"]) < 1e-5
+    with pytest.raises(ValueError):
+        hb.tgsp_apply(cycle, d["vcycle_z"])

@@ -5,7 +5,7 @@ known-answer tests.  Runs on CPU."""
 import numpy as np
 import pytest
 
-from conftest import CASES, SOLVED, c1_anchors, load_case, rel
+from conftest import CASES, NX_KEYS, SOLVED, c1_anchors, load_case, rel
 from oracle import tgsp_oracle as orc
 
 
@@ -41,6 +41,19 @@ def test_sweeps(case):
     if tg.part.J % 2 == 0:
         assert rel(tg.part.prec_x(d["probe_xc"]), d["sweep_x"]) < 1e-12
     assert rel(tg.part.prec_ud(d["probe_xc"]), d["sweep_ud"]) < 1e-12
+    for k in NX_KEYS:
+        if f"sweep_{k}" in d:
+            out = tg.part.prec_nx(d["probe_xc"], d[f"{k}_cells"], d[f"{k}_mid"])
+            assert rel(out, d[f"sweep_{k}"]) < 1e-12, k
+
+
+def test_nx_one_cell_is_x():
+    """test_sweepdd.py:231-236: NX with one cell equals the X sweep."""
+    d = load_case("nx2d")
+    assert rel(d["sweep_nx1"], d["sweep_x"]) < 1e-14
+    assert orc._nx_cells(8, 1) == (list(d["nx1_cells"]), list(d["nx1_mid"]))
+    for n in (2, 3, 4):
+        assert orc._nx_cells(8, n) == (list(d[f"nx{n}_cells"]), list(d[f"nx{n}_mid"]))
 
 
 def test_tgsp_apply(case):
@@ -123,3 +136,18 @@ def test_c1_anchor_oracle():
                                       p.f[0].ravel(), tol=1e-6, max_iter=400, restart=20)
     assert its == a["x"]["iterations"] and conv
     assert np.allclose(hist, a["x"]["history"], rtol=1e-8, atol=1e-14)
+
+
+def test_exact_coarse_oracle():
+    """Exact coarse solve (ExactCoarseSolver / factorize) vs the reference."""
+    d = load_case("exact2d")
+    tg = orc.from_exact_fixture(d)
+    assert rel(tg.vcycle(d["vcycle_z"]), d["vcycle_out"]) < 1e-12
+    assert rel(tg.part.solve(d["coarse_b"]), d["coarse_x"]) < 1e-12
+    for p in ("c3", "l1"):
+        ex = orc.Exact(orc.Op(d[f"{p}_offsets"], d[f"{p}_coeffs"]))
+        assert rel(ex.solve(d[f"{p}_b"]), d[f"{p}_x"]) < 1e-12, p
+    u, its, hist, conv, _ = orc.gmres(lambda v: tg.fine.csr @ v, tg.as_preconditioner(),
+                                      d["rhs"].ravel(), tol=1e-6, max_iter=200, restart=20)
+    assert its == int(d["gmres_iterations"]) and conv
+    assert np.allclose(hist, d["gmres_history"], rtol=1e-8, atol=1e-14)
