@@ -18,6 +18,7 @@ preconditioner, ``A M v`` runs as one fused device call.
 
 from __future__ import annotations
 
+import gc
 import math
 import time
 from dataclasses import dataclass
@@ -369,6 +370,21 @@ def _norm(ctx, x, n):
 
 def gmres(apply_a, apply_m, f, config: GmresConfig | None = None, orth: str = "cgs2",
           pipelined: bool = True):
+    """Solve A u = f with right preconditioning (see :func:`_gmres`).  The
+    cyclic garbage collector is paused for the solve: a generation-2 pass
+    over torch's object graph was measured to stall the launching thread for
+    30-50 ms in one of ~6 solves (C2, 157 ms each)."""
+    was = gc.isenabled()
+    gc.disable()
+    try:
+        return _gmres(apply_a, apply_m, f, config, orth, pipelined)
+    finally:
+        if was:
+            gc.enable()
+
+
+def _gmres(apply_a, apply_m, f, config: GmresConfig | None = None, orth: str = "cgs2",
+           pipelined: bool = True):
     """Solve A u = f with right preconditioning (GMRES on A M v = f, u = M v).
 
     ``f`` numpy -> ``u`` numpy; ``f`` torch CUDA -> ``u`` torch.  Stops on

@@ -282,7 +282,39 @@ def exact_fixture():
           f"1-D {op1.shape}")
 
 
+def harness_fixture():
+    """Reference file formats (cli.py:83-143): bytes of save_field, a velocity
+    file read by load_model, and a results CSV written by write_rows."""
+    import tempfile
+    from helmsweep import cli
+    out = {}
+    rng = np.random.default_rng(21)
+    u = crand(rng, (5, 4, 3))
+    out["field_u"] = u
+    with tempfile.TemporaryDirectory() as td:
+        p = Path(td) / "u.bin"
+        cli.save_field(p, u)
+        out["field_bytes"] = np.frombuffer(p.read_bytes(), dtype=np.uint8)
+        vel = (1.0 + rng.random(6 * 7)).astype("<f4")
+        vp = Path(td) / "v.bin"
+        vel.tofile(vp)
+        out["model_raw"] = np.frombuffer(vp.read_bytes(), dtype=np.uint8)
+        out["model_loaded"] = cli.load_model(vp, (6, 7))
+        rows = [cli.ResultRow("k1", "constant", 2, 64, 6.4, "pml", "tg-sweep", "x", 5, 6, "",
+                              12, True, 7.5e-7, 0.1234567890123, 1.0 / 3.0, "k1.csv"),
+                cli.ResultRow("k2", "wedge", 3, 32, 3.2, "sponge", "sweep-only", "nx", 3, 4, 7,
+                              40, False, 2.5e-3, 10.0, 2.0 ** -40, "k2.csv")]
+        cp = Path(td) / "r.csv"
+        cli.write_rows(cp, rows)
+        out["csv_bytes"] = np.frombuffer(cp.read_bytes(), dtype=np.uint8)
+    np.savez_compressed(OUT / "harness.npz", **out)
+    print("harness: field / model / csv bytes")
+
+
 def main():
+    if sys.argv[1:] == ["harness"]:
+        harness_fixture()
+        return
     if sys.argv[1:] == ["nx"]:
         nx_fixture()
         return
@@ -310,6 +342,7 @@ def main():
     c1_anchors()
     nx_fixture()
     exact_fixture()
+    harness_fixture()
 
 
 if __name__ == "__main__":

@@ -1,0 +1,61 @@
+"""Harness file formats (reference cli.py:83-143) against bytes the reference
+itself wrote (tests/golden/harness.npz): field dumps, velocity ingestion,
+results CSV."""
+
+import numpy as np
+import pytest
+
+from conftest import load_case
+
+from paper_1412_0464_b200 import harness as hz
+
+
+def test_save_field_bytes_match_reference(tmp_path):
+    d = load_case("harness")
+    p = tmp_path / "u.bin"
+    hz.save_field(p, d["field_u"])
+    assert p.read_bytes() == d["field_bytes"].tobytes()
+    back = hz.load_field(p, d["field_u"].shape)
+    assert np.array_equal(back, d["field_u"])          # bit-exact round trip
+    with pytest.raises(ValueError, match="wrong size"):
+        hz.load_field(p, (5, 4, 4))
+
+
+def test_load_model_matches_reference(tmp_path):
+    d = load_case("harness")
+    p = tmp_path / "v.bin"
+    p.write_bytes(d["model_raw"].tobytes())
+    v = hz.load_model(p, (6, 7))
+    assert v.dtype == np.float64 and np.array_equal(v, d["model_loaded"])
+    with pytest.raises(ValueError, match="samples"):
+        hz.load_model(p, (6, 8))
+    bad = np.frombuffer(d["model_raw"].tobytes(), dtype="<f4").copy()
+    bad[5] = 0.0
+    bad.tofile(p)
+    with pytest.raises(ValueError, match="nonpositive velocity at flat index 5"):
+        hz.load_model(p, (6, 7))
+
+
+def test_results_csv_matches_reference(tmp_path):
+    d = load_case("harness")
+    rows = [hz.ResultRow("k1", "constant", 2, 64, 6.4, "pml", "tg-sweep", "x", 5, 6, "",
+                         12, True, 7.5e-7, 0.1234567890123, 1.0 / 3.0, "k1.csv"),
+            hz.ResultRow("k2", "wedge", 3, 32, 3.2, "sponge", "sweep-only", "nx", 3, 4, 7,
+                         40, False, 2.5e-3, 10.0, 2.0 ** -40, "k2.csv")]
+    p = tmp_path / "r.csv"
+    hz.write_rows(p, rows)
+    assert p.read_bytes() == d["csv_bytes"].tobytes()
+    recs = hz.read_rows(p)
+    assert recs[0]["iterations"] == 12 and recs[0]["converged"] is True
+    assert recs[1]["solve_time"] == 2.0 ** -40 and recs[1]["converged"] is False
+    hz.write_rows(p, rows[:1], append=True)
+    assert len(hz.read_rows(p)) == 3
+
+
+@pytest.mark.gpu
+def test_save_field_from_device(tmp_path):
+    import torch
+    d = load_case("harness")
+    p = tmp_path / "u.bin"
+    hz.save_field(p, torch.from_numpy(d["field_u"]).cuda())
+    assert p.read_bytes() == d["field_bytes"].tobytes()
