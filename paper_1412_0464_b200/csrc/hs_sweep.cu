@@ -2354,11 +2354,42 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
           ProfScope ps(c, K_SWEEP_FRONT, Lh.bytes);
           if (w->g != s->g) return set_error(c, HS_E_ARG, "sweep lanes need a 2-D level");
           double2* us[2] = {u, s->u2};
-          for (int fr = 0; fr < Lh.nfront; ++fr)
-            for (int i = Lh.ffirst[fr]; i < Lh.ffirst[fr] + Lh.fcount[fr]; ++i)
-              if (int r = sweep3_task(c, s, s->tasks[i], Lh.src ? s->g : f, us,
-                                      s->coarse->d.coeffs, s->coarse->d.n))
-                return r;
+          // fronts zipped in pairs (two chains per launch); a task identical
+          // to one already run in this launch (a solve heading two fronts)
+          // is not repeated -- its outputs are already in place
+          std::vector<const SweepTask*> done;
+          auto ran = [&](const SweepTask* t, size_t upto) {
+            for (size_t k = 0; k < upto; ++k)
+              if (!memcmp(done[k], t, sizeof(SweepTask))) return true;
+            return false;
+          };
+          for (int fr = 0; fr < Lh.nfront; fr += 2) {
+            std::vector<const SweepTask*> q[2];
+            for (int h = 0; h < 2 && fr + h < Lh.nfront; ++h)
+              for (int i = Lh.ffirst[fr + h]; i < Lh.ffirst[fr + h] + Lh.fcount[fr + h]; ++i)
+                q[h].push_back(&s->tasks[i]);
+            size_t p0 = 0, p1 = 0;
+            while (p0 < q[0].size() || p1 < q[1].size()) {
+              const size_t before = done.size();
+              const SweepTask* ts[2];
+              int nt = 0;
+              while (p0 < q[0].size() && ran(q[0][p0], before)) ++p0;
+              while (p1 < q[1].size() && ran(q[1][p1], before)) ++p1;
+              if (p0 < q[0].size()) ts[nt++] = q[0][p0++];
+              if (p1 < q[1].size()) {
+                // the same solve heading both fronts runs once; the second
+                // front's next task depends on it, so it waits a launch
+                if (nt && !memcmp(ts[0], q[1][p1], sizeof(SweepTask))) ++p1;
+                else ts[nt++] = q[1][p1++];
+              }
+              for (int k = 0; k < nt; ++k) done.push_back(ts[k]);
+              if (nt) {
+                const int r2 = sweep3_tasks(c, s, ts, nt, Lh.src ? s->g : f, us,
+                                            s->coarse->d.coeffs, s->coarse->d.n);
+                if (r2) return r2;
+              }
+            }
+          }
           break;
         }
         SolveArgs a{};

@@ -100,6 +100,9 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
                   const int64_t* lo, const int64_t* hi);
 int sweep3_task(Ctx* c, Sweep* s, const SweepTask& t, const double2* src, double2* const* u,
                 const double2* coarse_coeffs, int64_t coarse_n);
+// one or two independent slab solves (two sweep fronts) in one chain launch
+int sweep3_tasks(Ctx* c, Sweep* s, const SweepTask* const* ts, int nt, const double2* src,
+                 double2* const* u, const double2* coarse_coeffs, int64_t coarse_n);
 void sweep3_destroy(Sweep3* s3);
 // Exact solver of a whole operator (ExactCoarseSolver / factorize,
 // twogrid.py:99-105, sparselin.py:40-68): the operator as ONE block-LU slab

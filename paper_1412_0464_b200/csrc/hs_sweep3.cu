@@ -41,9 +41,10 @@ struct Sweep3 {
   std::vector<std::array<int, 27>> slot;   // per slab: (o0+1)*9 + (o1+1)*3 + (o2+1) -> slot
   std::array<int, 27> cslot{};         // coarse operator slots
   cublasHandle_t blas = nullptr;
-  double2* F = nullptr;                // [n1][NBmax] right-hand side
-  double2* Y = nullptr;                // [n1][NBmax] forward solution, then x
-  unsigned* gbar = nullptr;            // grid barrier counter of the solve kernel
+  double2* F[2] = {nullptr, nullptr};  // per concurrent chain: [n1][NBmax] right-hand side
+  double2* Y[2] = {nullptr, nullptr};  // [n1][NBmax] forward solution, then x
+  unsigned* gbar = nullptr;            // [2] grid barrier counters of the solve kernel
+  int optin = 0;                       // opt-in shared memory per block
   int grid = 0;                        // CTAs of the solve kernel (one per SM)
   int nbuf = 1;                        // staging buffers of the solve kernel
   long long bytes = 0;
@@ -186,13 +187,13 @@ __device__ __forceinline__ void barrier_wait(unsigned* bar, unsigned target) {
 
 // this CTA's rows of a plane matrix -> shared memory (thread 0; one bulk copy per row)
 __device__ __forceinline__ void stage_rows(const double2* __restrict__ A, int NB, int nrow,
-                                           double2* dst, uint64_t* bar) {
+                                           double2* dst, uint64_t* bar, int lb, int G) {
   const uint32_t bytes = (uint32_t)NB * 16u;
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s3_smem(bar)),
                "r"(bytes * (uint32_t)nrow)
                : "memory");
   for (int k = 0; k < nrow; ++k) {
-    const double2* src = A + (int64_t)(blockIdx.x + k * gridDim.x) * NB;
+    const double2* src = A + (int64_t)(lb + k * G) * NB;
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
         ::"r"(s3_smem(dst + (int64_t)k * NB)), "l"(src), "r"(bytes), "r"(s3_smem(bar))
@@ -200,12 +201,7 @@ __device__ __forceinline__ void stage_rows(const double2* __restrict__ A, int NB
   }
 }
 
-// rows k < nrow of (staged rows) x v: warp w owns the column segment
-// [w seg, (w+1) seg) of every row, so it reads its slice of v once (two
-// entries per lane, registers) and each staged row element once; partial
-// sums land in acc[k][w] and are summed in a fixed order by the caller
-// (bitwise reproducible).
-constexpr int kR3 = 8;   // rows per CTA at most (NB <= 8 * grid)
+constexpr int kR3 = 16;  // rows per CTA at most (NB <= 16 * CTAs of the task)
 
 // rows k < nrow of (staged rows) x v: a row is split over wpr warps (4
 // independent partial sums per lane); partial sums land in acc[k][part],
@@ -238,14 +234,36 @@ __device__ __forceinline__ void cta_rows(const double2* A, const double2* v, int
   }
 }
 
+// One chain of a slab solve: its slab thickness, factors, vector and grid
+// barrier.  A launch runs one chain on every CTA or two independent chains
+// (the two sweep fronts' slabs) on disjoint CTA groups [0, g0) and
+// [g0, grid), each with its own barrier: the per-step latency (barrier,
+// vector load) is paid once for both.
+struct K3Chain {
+  int T;
+  const double2* gT;
+  const double2* xT;
+  double2* Y;
+  unsigned* bar;
+  int nbuf;
+};
+
 __global__ void __launch_bounds__(kW3 * 32, 1)
-k3_solve(int T, int n1, int n2, const double2* __restrict__ gT, const double2* __restrict__ xT,
-         double2* Y, unsigned* bar, int nbuf) {
+k3_solve(K3Chain c0, K3Chain c1, int g0, int n1, int n2) {
   extern __shared__ __align__(128) double2 v3[];   // [NB] vector | [nbuf][rmax][NB] rows | sums
+  const bool second = (int)blockIdx.x >= g0;
+  const K3Chain& ch = second ? c1 : c0;
+  const int lb = second ? (int)blockIdx.x - g0 : (int)blockIdx.x;   // CTA within the chain
+  const int G = second ? (int)gridDim.x - g0 : g0;                 // CTAs of the chain
+  const int T = ch.T, nbuf = ch.nbuf;
+  const double2* __restrict__ gT = ch.gT;
+  const double2* __restrict__ xT = ch.xT;
+  double2* Y = ch.Y;
+  unsigned* bar = ch.bar;
   const int NB = T * n2;
   const int64_t nb2 = (int64_t)NB * NB;
-  const int nrow = blockIdx.x < NB ? (NB - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int rmax = (NB + gridDim.x - 1) / gridDim.x;
+  const int nrow = lb < NB ? (NB - 1 - lb) / G + 1 : 0;
+  const int rmax = (NB + G - 1) / G;
   double2* rows = v3 + NB;                          // nbuf (1 or 2) staging buffers
   double2* racc = rows + nbuf * (int64_t)rmax * NB; // [rows][warps per row] partial row sums
   uint64_t* rbar = (uint64_t*)(racc + rmax * kW3);  // [2] staging barriers
@@ -269,13 +287,13 @@ k3_solve(int T, int n1, int n2, const double2* __restrict__ gT, const double2* _
   __syncthreads();
   if (threadIdx.x == 0 && nrow > 0)   // nbuf steps ahead
     for (int st = 0; st < nbuf && st < nsteps; ++st)
-      stage_rows(mat(st), NB, nrow, rows + (int64_t)st * rmax * NB, rbar + st);
+      stage_rows(mat(st), NB, nrow, rows + (int64_t)st * rmax * NB, rbar + st, lb, G);
   for (int st = 0; st < nsteps; ++st) {
     const bool fwd = st < n1 - 1;
     const int i1 = fwd ? st + 1 : 2 * n1 - 3 - st;
     double2* Yi = Y + (int64_t)i1 * NB;
     const double2* Yin = fwd ? Yi - NB : Yi + NB;
-    if (st > 0) barrier_wait(bar, (unsigned)st * gridDim.x);
+    if (st > 0) barrier_wait(bar, (unsigned)st * G);
     if (!(HS_S3_EXP & 2))
       for (int r = threadIdx.x; r < NB; r += blockDim.x) v3[r] = __ldcg(Yin + r);
     __syncthreads();
@@ -285,9 +303,9 @@ k3_solve(int T, int n1, int n2, const double2* __restrict__ gT, const double2* _
     cta_rows(buf, v3, NB, nrow, racc);
     __syncthreads();   // this buffer is consumed: stage the step after next into it
     if (threadIdx.x == 0 && nrow > 0 && st + nbuf < nsteps)
-      stage_rows(mat(st + nbuf), NB, nrow, buf, rbar + b);
+      stage_rows(mat(st + nbuf), NB, nrow, buf, rbar + b, lb, G);
     for (int k = threadIdx.x; k < nrow; k += blockDim.x) {
-      const int r = blockIdx.x + k * gridDim.x;
+      const int r = lb + k * G;
       Yi[r] = csub(__ldcg(Yi + r), row_sum(k));
     }
     barrier_arrive(bar);
@@ -334,8 +352,10 @@ void sweep3_destroy(Sweep3* s3) {
   for (auto* p : s3->xf) cudaFree(p);
   for (auto* p : s3->gf) cudaFree(p);
   for (auto* p : s3->coef) cudaFree(p);
-  cudaFree(s3->F);
-  cudaFree(s3->Y);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(s3->F[i]);
+    cudaFree(s3->Y[i]);
+  }
   cudaFree(s3->gbar);
   if (s3->blas) cublasDestroy(s3->blas);
   delete s3;
@@ -372,11 +392,13 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
   };
   if (cudaMalloc((void**)&D, blk) || cudaMalloc((void**)&Lb, blk) || cudaMalloc((void**)&U, blk) ||
       cudaMalloc((void**)&Di, blk) || cudaMalloc((void**)&Xc, blk) ||
-      cudaMalloc((void**)&s3->gbar, sizeof(unsigned)) ||
+      cudaMalloc((void**)&s3->gbar, 2 * sizeof(unsigned)) ||
       cudaMalloc((void**)&ipiv, NBmax * sizeof(int)) ||
       cudaMalloc((void**)&info, ((size_t)n1 * J + 1) * sizeof(int)) ||
-      cudaMalloc((void**)&s3->F, (size_t)n1 * NBmax * sizeof(double2)) ||
-      cudaMalloc((void**)&s3->Y, (size_t)n1 * NBmax * sizeof(double2)))
+      cudaMalloc((void**)&s3->F[0], (size_t)n1 * NBmax * sizeof(double2)) ||
+      cudaMalloc((void**)&s3->Y[0], (size_t)n1 * NBmax * sizeof(double2)) ||
+      cudaMalloc((void**)&s3->F[1], (size_t)n1 * NBmax * sizeof(double2)) ||
+      cudaMalloc((void**)&s3->Y[1], (size_t)n1 * NBmax * sizeof(double2)))
     return done(set_error(c, HS_E_CUDA, "3-D sweep work allocation failed"));
   if (cusolverDnZgetrf_bufferSize(sol, NBmax, NBmax, (cuDoubleComplex*)D, NBmax, &lwork) != 0 ||
       cudaMalloc((void**)&work, (size_t)std::max(1, lwork) * sizeof(double2)))
@@ -482,56 +504,92 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
     s3->nbuf = k3_smem(NBmax, s3->grid, 2) <= (size_t)optin ? 2 : 1;
     const int smem = (int)k3_smem(NBmax, s3->grid, s3->nbuf);
     if (smem > optin) return done(set_error(c, HS_E_SHAPE, "3-D slab planes too large for the solve kernel"));
-    S3_TRY(cudaFuncSetAttribute(k3_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "attr");
+    s3->optin = optin;
+    S3_TRY(cudaFuncSetAttribute(k3_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, optin), "attr");
     int per = 0;
-    S3_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k3_solve, kW3 * 32, smem), "occ");
+    S3_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k3_solve, kW3 * 32, optin), "occ");
     if (per < 1) return done(set_error(c, HS_E_CUDA, "3-D solve kernel does not fit an SM"));
   }
   return done(HS_OK);
 }
 
 // One slab solve of the schedule (subdom_solve, sweepdd.py:236-268).
-int sweep3_task(Ctx* c, Sweep* s, const SweepTask& t, const double2* src, double2* const* u,
-                const double2* coarse_coeffs, int64_t coarse_n) {
+// Slab solves of one or two independent tasks (two sweep fronts): right-hand
+// sides, the batched w = Dinv f GEMVs, then ONE cooperative chain launch --
+// two chains on disjoint CTA groups when both fit the group's shared memory
+// (CTAs split by NB^2, the per-step bytes) -- and the outputs.
+int sweep3_tasks(Ctx* c, Sweep* s, const SweepTask* const* ts, int nt, const double2* src,
+                 double2* const* u, const double2* coarse_coeffs, int64_t coarse_n) {
   Sweep3* s3 = s->s3;
-  const int n1 = s3->n1, n2 = s3->n2, j = t.slab, T = s3->T[j], NB = T * n2;
-  const size_t nb2 = (size_t)NB * NB;
-  cublasSetStream(s3->blas, c->stream);
-  const Slots sl = to_slots(s3->slot[j]);
-  const int64_t tot = (int64_t)n1 * NB;
-  k3_rhs<<<(unsigned)((tot + kT3 - 1) / kT3), kT3, 0, c->stream>>>(
-      t, s->n0, n1, n2, src, coarse_coeffs, coarse_n, to_slots(s3->cslot), s->trace, s3->F);
-  HS_LAUNCH_CHECK(c, "3-D rhs");
-  {   // w_i = Dinv_i f_i for every plane: one batched GEMV (Dinv stored row-major
-      // = column-major transpose), written into Y where the chain updates it
-    const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
-    ProfScope ps(c, K_SWEEP_GATHER, (double)n1 * nb2 * 16.0);
-    if (cublasZgemvStridedBatched(s3->blas, CUBLAS_OP_T, NB, NB, &one,
-                                  (const cuDoubleComplex*)s3->dinv[j], NB, (long long)nb2,
-                                  (const cuDoubleComplex*)s3->F, 1, NB, &zero,
-                                  (cuDoubleComplex*)s3->Y, 1, NB, n1) != CUBLAS_STATUS_SUCCESS)
-      return set_error(c, HS_E_CUDA, "3-D batched GEMV failed");
-    c->launches++;
+  const int n1 = s3->n1, n2 = s3->n2;
+  const int G = s3->grid;
+  int NB[2] = {0, 0}, g0 = G, nbuf[2] = {1, 1};
+  for (int k = 0; k < nt; ++k) NB[k] = s3->T[ts[k]->slab] * n2;
+  if (nt == 2) {   // CTA split by per-step bytes; both groups must fit
+    const double a = (double)NB[0] * NB[0], b = (double)NB[1] * NB[1];
+    g0 = std::min(G - 1, std::max(1, (int)std::lround(G * a / (a + b))));
+    bool ok = true;
+    for (int k = 0; k < 2; ++k) {
+      const int gk = k ? G - g0 : g0;
+      nbuf[k] = k3_smem(NB[k], gk, 2) <= (size_t)s3->optin ? 2 : 1;
+      ok = ok && (NB[k] + gk - 1) / gk <= kR3 && k3_smem(NB[k], gk, nbuf[k]) <= (size_t)s3->optin;
+    }
+    if (!ok) {   // one chain at a time
+      for (int k = 0; k < 2; ++k)
+        if (int r = sweep3_tasks(c, s, ts + k, 1, src, u, coarse_coeffs, coarse_n)) return r;
+      return HS_OK;
+    }
+  } else {
+    nbuf[0] = s3->nbuf;
   }
-  {   // the chain: one cooperative launch
-    S3_TRY(cudaMemsetAsync(s3->gbar, 0, sizeof(unsigned), c->stream), "memset");
-    const double2* gv = s3->gf[j];
-    const double2* xv = s3->xf[j];
-    double2* Yp = s3->Y;
-    unsigned* gb = s3->gbar;
-    int T_ = T, n1_ = n1, n2_ = n2;
-    int nb_ = s3->nbuf;
-    void* args[] = {(void*)&T_, (void*)&n1_, (void*)&n2_, (void*)&gv, (void*)&xv, (void*)&Yp,
-                    (void*)&gb, (void*)&nb_};
-    S3_TRY(cudaLaunchCooperativeKernel((const void*)k3_solve, dim3(s3->grid), dim3(kW3 * 32), args,
-                                       k3_smem(NB, s3->grid, s3->nbuf), c->stream),
+  cublasSetStream(s3->blas, c->stream);
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+  size_t smem = 0;
+  K3Chain ch[2] = {};
+  for (int k = 0; k < nt; ++k) {
+    const SweepTask& t = *ts[k];
+    const int j = t.slab, nb = NB[k];
+    const size_t nb2 = (size_t)nb * nb;
+    const int64_t tot = (int64_t)n1 * nb;
+    k3_rhs<<<(unsigned)((tot + kT3 - 1) / kT3), kT3, 0, c->stream>>>(
+        t, s->n0, n1, n2, src, coarse_coeffs, coarse_n, to_slots(s3->cslot), s->trace, s3->F[k]);
+    HS_LAUNCH_CHECK(c, "3-D rhs");
+    {   // w_i = Dinv_i f_i for every plane: one batched GEMV (Dinv stored row-major
+      ProfScope ps(c, K_SWEEP_GATHER, (double)n1 * nb2 * 16.0);
+      if (cublasZgemvStridedBatched(s3->blas, CUBLAS_OP_T, nb, nb, &one,
+                                    (const cuDoubleComplex*)s3->dinv[j], nb, (long long)nb2,
+                                    (const cuDoubleComplex*)s3->F[k], 1, nb, &zero,
+                                    (cuDoubleComplex*)s3->Y[k], 1, nb, n1) != CUBLAS_STATUS_SUCCESS)
+        return set_error(c, HS_E_CUDA, "3-D batched GEMV failed");
+      c->launches++;
+    }
+    ch[k] = K3Chain{s3->T[j], s3->gf[j], s3->xf[j], s3->Y[k], s3->gbar + k, nbuf[k]};
+    smem = std::max(smem, k3_smem(nb, nt == 2 ? (k ? G - g0 : g0) : G, nbuf[k]));
+  }
+  if (nt == 1) ch[1] = ch[0];
+  {   // the chains: one cooperative launch
+    S3_TRY(cudaMemsetAsync(s3->gbar, 0, 2 * sizeof(unsigned), c->stream), "memset");
+    int g0_ = g0, n1_ = n1, n2_ = n2;
+    void* args[] = {(void*)&ch[0], (void*)&ch[1], (void*)&g0_, (void*)&n1_, (void*)&n2_};
+    S3_TRY(cudaLaunchCooperativeKernel((const void*)k3_solve, dim3(G), dim3(kW3 * 32), args, smem,
+                                       c->stream),
            "3-D solve launch");
     HS_LAUNCH_CHECK(c, "3-D solve kernel");
   }
-  k3_out<<<(unsigned)((tot + kT3 - 1) / kT3), kT3, 0, c->stream>>>(t, n1, n2, s3->Y, u[t.dst],
-                                                                   s->trace);
-  HS_LAUNCH_CHECK(c, "3-D outputs");
+  for (int k = 0; k < nt; ++k) {
+    const SweepTask& t = *ts[k];
+    const int64_t tot = (int64_t)n1 * NB[k];
+    k3_out<<<(unsigned)((tot + kT3 - 1) / kT3), kT3, 0, c->stream>>>(t, n1, n2, s3->Y[k],
+                                                                     u[t.dst], s->trace);
+    HS_LAUNCH_CHECK(c, "3-D outputs");
+  }
   return HS_OK;
+}
+
+int sweep3_task(Ctx* c, Sweep* s, const SweepTask& t, const double2* src, double2* const* u,
+                const double2* coarse_coeffs, int64_t coarse_n) {
+  const SweepTask* ts[1] = {&t};
+  return sweep3_tasks(c, s, ts, 1, src, u, coarse_coeffs, coarse_n);
 }
 
 // ---------------------------------------------------------------------------
