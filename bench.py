@@ -111,9 +111,7 @@ class ClockSampler:
     line).  In-process NVML polling was measured to stall the launching
     thread (driver lock) and is only the fallback; ``mode="none"`` skips."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    FIELDS = os.environ.get("HS_SMI_FIELDS", "clocks.sm,clocks.max.sm,clocks_event_reasons.active")
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
     REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
@@ -182,16 +180,25 @@ class ClockSampler:
             self.out.seek(0)
             for line in self.out.read().splitlines():
                 f = [x.strip() for x in line.split(",")]
-                if len(f) < 6:
+                if len(f) < 3:
                     continue
                 try:
                     self.samples.append(float(f[0]))
                     self.max_mhz = float(f[1])
                 except ValueError:
                     continue
-                for name, v in zip(self.NAMES, f[2:6]):
-                    if v.lower() == "active":
-                        self.reasons.add(name)
+                if len(f) == 3:   # clocks_event_reasons.active: the NVML bit mask
+                    try:
+                        mask = int(f[2], 16) if f[2].lower().startswith("0x") else int(f[2])
+                    except ValueError:
+                        mask = 0
+                    for bit, name in self.REASONS.items():
+                        if mask & bit:
+                            self.reasons.add(name)
+                else:
+                    for name, v in zip(self.NAMES, f[2:6]):
+                        if v.lower() == "active":
+                            self.reasons.add(name)
 
     def summary(self):
         if not self.samples:

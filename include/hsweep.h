@@ -215,6 +215,12 @@ int hs_block_dot(hs_ctx* ctx, const void* V, int64_t ldv, int k, const void* w, 
 /* w -= sum_i h[i] V_i (i < k); nrm2[0] = (||w||^2, 0) */
 int hs_block_update(hs_ctx* ctx, const void* V, int64_t ldv, int k, const void* h, void* w,
                     int64_t n, void* nrm2);
+/* CGS2 step fused (the first pass's update with the second pass's dots,
+ * one read of V): w -= sum_i h[i] V_i; h2[i] = vdot(V_i, w) (i < k),
+ * h2[k] = nrm2[0] = (||w||^2, 0).  Bitwise equal to hs_block_update followed
+ * by hs_block_dot.  1 <= k <= 32. */
+int hs_block_update_dot(hs_ctx* ctx, const void* V, int64_t ldv, int k, const void* h, void* w,
+                        int64_t n, void* nrm2, void* h2);
 /* Second (DGKS) Gram-Schmidt pass gated on the device, krylov.py:67-70 with
  * re-orthogonalisation: runs only when g_after[0].re < thresh * g_before[0].re
  * (||w||^2 after / before the first pass); a closed gate leaves h untouched

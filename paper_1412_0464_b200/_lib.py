@@ -82,6 +82,7 @@ SIGNATURES = {
     "hs_block_update_gated": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, _vp, _vp, C.c_int64,
                                         _vp, _vp, _vp, C.c_double]),
     "hs_scale_inv_sqrt": (C.c_int, [_vp, _vp, C.c_int64, _vp]),
+    "hs_block_update_dot": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, _vp, _vp, C.c_int64, _vp, _vp]),
     "hs_block_update": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, _vp, _vp, C.c_int64, _vp]),
     "hs_lincomb": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, _vp, _vp, C.c_int64]),
     "hs_scale": (C.c_int, [_vp, _vp, C.c_int64, C.c_double, C.c_double]),

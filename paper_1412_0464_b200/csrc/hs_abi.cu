@@ -71,6 +71,8 @@ static int prof_collect(Ctx* c) {
 // declared in the kernel translation units
 int krylov_block_dot(Ctx*, const double2*, int64_t, int, const double2*, int64_t, double2*,
                      const double2*, const double2*, double);
+int krylov_block_update_dot(Ctx*, const double2*, int64_t, int, const double2*, double2*, int64_t,
+                            double2*, double2*);
 int krylov_block_update(Ctx*, const double2*, int64_t, int, const double2*, double2*, int64_t,
                         double2*, const double2*, const double2*, double);
 int krylov_scale_inv_sqrt(Ctx*, double2*, int64_t, const double2*);
@@ -567,6 +569,13 @@ int hs_block_update(hs_ctx* c, const void* V, int64_t ldv, int k, const void* h,
   if (!c || (!V && k > 0) || !h || !w || !nrm2) return HS_E_ARG;
   return krylov_block_update(c, (const double2*)V, ldv, k, (const double2*)h, (double2*)w, n,
                              (double2*)nrm2, nullptr, nullptr, 0.0);
+}
+
+int hs_block_update_dot(hs_ctx* c, const void* V, int64_t ldv, int k, const void* h, void* w,
+                        int64_t n, void* nrm2, void* h2) {
+  if (!c || !V || !h || !w || !nrm2 || !h2) return HS_E_ARG;
+  return krylov_block_update_dot(c, (const double2*)V, ldv, k, (const double2*)h, (double2*)w, n,
+                                 (double2*)nrm2, (double2*)h2);
 }
 
 int hs_block_dot_gated(hs_ctx* c, const void* V, int64_t ldv, int k, const void* w, int64_t n,

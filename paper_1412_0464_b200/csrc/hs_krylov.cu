@@ -17,22 +17,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kMaxK = 32;
 
-__device__ __forceinline__ double2 block_sum(double2 v, double2* sh) {
-  // sum over the block; result valid in thread 0
-  for (int m = 16; m > 0; m >>= 1) {
-    v.x += __shfl_xor_sync(0xffffffffu, v.x, m);
-    v.y += __shfl_xor_sync(0xffffffffu, v.y, m);
-  }
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) sh[w] = v;
-  __syncthreads();
-  double2 s = czero();
-  if (threadIdx.x == 0)
-    for (int i = 0; i < kThreads / 32; ++i) s = cadd(s, sh[i]);
-  return s;
-}
-
 // DGKS gate of the second Gram-Schmidt pass, evaluated on the device so the
 // host never has to read the first pass before issuing the second:
 // run = ||w_after||^2 < thresh * ||w_before||^2 (the host's test, same double ops).
@@ -44,6 +28,29 @@ struct Gate {
 
 __device__ __forceinline__ bool gate_open(const Gate& g) {
   return g.after == nullptr || g.after->x < g.thresh * g.before->x;
+}
+
+// per-block sums of acc[0..W) (fixed order: warp shuffles, then the block's
+// warps in order) -> part[blockIdx.x * W + i]; one __syncthreads
+template <int W>
+__device__ __forceinline__ void block_sums(double2 (&acc)[W], double2* __restrict__ part) {
+  __shared__ double2 sh[kThreads / 32][W];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    double2 v = acc[i];
+    for (int m = 16; m > 0; m >>= 1) {
+      v.x += __shfl_xor_sync(0xffffffffu, v.x, m);
+      v.y += __shfl_xor_sync(0xffffffffu, v.y, m);
+    }
+    if (l == 0) sh[w][i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < W) {
+    double2 s = czero();
+    for (int q = 0; q < kThreads / 32; ++q) s = cadd(s, sh[q][threadIdx.x]);
+    part[(int64_t)blockIdx.x * W + threadIdx.x] = s;
+  }
 }
 
 template <int K>
@@ -61,12 +68,35 @@ k_block_dot(const double2* __restrict__ V, int64_t ldv, const double2* __restric
     for (int i = 0; i < K; ++i) acc[i] = cfma_conj(__ldg(V + i * ldv + j), wj, acc[i]);
     acc[K].x = fma(wj.x, wj.x, fma(wj.y, wj.y, acc[K].x));
   }
-  __shared__ double2 sh[kThreads / 32];
+  block_sums<K + 1>(acc, part);
+}
+
+// First Gram-Schmidt update fused with the second pass's dots: w' = w - V h
+// and, from the same reads of V, the partials of V^H w' and ||w'||^2.  Per
+// element the arithmetic (and the grid-stride / reduction order) is that of
+// k_block_update followed by k_block_dot: bitwise the same results.
+template <int K>
+__global__ void __launch_bounds__(kThreads)
+k_block_update_dot(const double2* __restrict__ V, int64_t ldv, const double2* __restrict__ h,
+                   double2* __restrict__ w, int64_t n, double2* __restrict__ part) {
+  __shared__ double2 hv[K];   // broadcast reads (keeps the accumulators in registers)
+  if (threadIdx.x < K) hv[threadIdx.x] = h[threadIdx.x];
+  __syncthreads();
+  double2 acc[K + 1];
 #pragma unroll
-  for (int i = 0; i <= K; ++i) {
-    const double2 s = block_sum(acc[i], sh);
-    if (threadIdx.x == 0) part[(int64_t)blockIdx.x * (K + 1) + i] = s;
+  for (int i = 0; i <= K; ++i) acc[i] = czero();
+  for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * kThreads) {
+    double2 wj = w[j];
+#pragma unroll
+    for (int i = 0; i < K; ++i) wj = csub(wj, cmul(hv[i], __ldg(V + i * ldv + j)));
+    w[j] = wj;
+#pragma unroll
+    for (int i = 0; i < K; ++i)   // second read of V_ij: an L1 hit
+      acc[i] = cfma_conj(__ldg(V + i * ldv + j), wj, acc[i]);
+    acc[K].x = fma(wj.x, wj.x, fma(wj.y, wj.y, acc[K].x));
   }
+  block_sums<K + 1>(acc, part);
 }
 
 template <int K>
@@ -89,9 +119,8 @@ k_block_update(const double2* __restrict__ V, int64_t ldv, const double2* __rest
     w[j] = wj;
     nrm = fma(wj.x, wj.x, fma(wj.y, wj.y, nrm));
   }
-  __shared__ double2 sh[kThreads / 32];
-  const double2 s = block_sum(make_double2(nrm, 0.0), sh);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
+  double2 acc[1] = {make_double2(nrm, 0.0)};
+  block_sums<1>(acc, part);
 }
 
 template <int K>
@@ -119,12 +148,16 @@ __global__ void k_reduce_parts(const double2* __restrict__ part, int nblk, int w
     if (pass_through && threadIdx.x == 0) out[0] = *gate.after;
     return;
   }
-  __shared__ double2 sh[kThreads / 32];
-  for (int i = 0; i < width; ++i) {
+  // one warp per output column, lanes over the blocks in fixed order
+  const int wp = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int i = wp; i < width; i += kThreads / 32) {
     double2 acc = czero();
-    for (int b = threadIdx.x; b < nblk; b += kThreads) acc = cadd(acc, part[(int64_t)b * width + i]);
-    const double2 s = block_sum(acc, sh);
-    if (threadIdx.x == 0) out[i] = s;
+    for (int b = l; b < nblk; b += 32) acc = cadd(acc, part[(int64_t)b * width + i]);
+    for (int m = 16; m > 0; m >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, m);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, m);
+    }
+    if (l == 0) out[i] = acc;
   }
 }
 
@@ -158,9 +191,8 @@ __global__ void k_norm2(const double2* __restrict__ x, int64_t n, double2* part)
     if (!isfinite(v.x) || !isfinite(v.y)) bad += 1.0;
     s = fma(v.x, v.x, fma(v.y, v.y, s));
   }
-  __shared__ double2 sh[kThreads / 32];
-  const double2 r = block_sum(make_double2(s, bad), sh);
-  if (threadIdx.x == 0) part[blockIdx.x] = r;
+  double2 acc[1] = {make_double2(s, bad)};
+  block_sums<1>(acc, part);
 }
 
 int grid_for(Ctx* c, int64_t n) {
@@ -219,6 +251,31 @@ int krylov_block_update(Ctx* c, const double2* V, int64_t ldv, int k, const doub
   HS_LAUNCH_CHECK(c, "block_update");
   k_reduce_parts<<<1, kThreads, 0, c->stream>>>(part, nb, 1, nrm2, gate, 1);
   HS_LAUNCH_CHECK(c, "reduce");
+  return HS_OK;
+}
+
+int krylov_block_update_dot(Ctx* c, const double2* V, int64_t ldv, int k, const double2* h,
+                            double2* w, int64_t n, double2* nrm2, double2* h2) {
+  if (k < 1 || k > kMaxK) return set_error(c, HS_E_ARG, "block_update_dot: k out of range");
+  const int nb = grid_for(c, n);
+  double2* part = (double2*)scratch(c, (size_t)nb * (k + 1) * sizeof(double2), 2);
+  if (!part) return set_error(c, HS_E_CUDA, "scratch allocation failed");
+  ProfScope ps(c, K_KRYLOV_UPDATE, 16.0 * (k + 2) * (double)n);
+  switch (k) {
+#define HS_CASE(KK) \
+  case KK: k_block_update_dot<KK><<<nb, kThreads, 0, c->stream>>>(V, ldv, h, w, n, part); break;
+    HS_CASE(1) HS_CASE(2) HS_CASE(3) HS_CASE(4) HS_CASE(5) HS_CASE(6) HS_CASE(7)
+    HS_CASE(8) HS_CASE(9) HS_CASE(10) HS_CASE(11) HS_CASE(12) HS_CASE(13) HS_CASE(14)
+    HS_CASE(15) HS_CASE(16) HS_CASE(17) HS_CASE(18) HS_CASE(19) HS_CASE(20) HS_CASE(21)
+    HS_CASE(22) HS_CASE(23) HS_CASE(24) HS_CASE(25) HS_CASE(26) HS_CASE(27) HS_CASE(28)
+    HS_CASE(29) HS_CASE(30) HS_CASE(31) HS_CASE(32)
+#undef HS_CASE
+  }
+  HS_LAUNCH_CHECK(c, "block_update_dot");
+  // second-pass dots (and ||w'||^2 at h2[k]), then ||w'||^2 into nrm2 as well
+  k_reduce_parts<<<1, kThreads, 0, c->stream>>>(part, nb, k + 1, h2, Gate{nullptr, nullptr, 0.0}, 0);
+  HS_LAUNCH_CHECK(c, "reduce");
+  cudaMemcpyAsync(nrm2, h2 + k, sizeof(double2), cudaMemcpyDeviceToDevice, c->stream);
   return HS_OK;
 }
 

@@ -173,6 +173,18 @@ def _update_pass(ctx, basis, k, h, w, n, nbuf, gate=None):
             return
 
 
+def _update_dot_pass(ctx, basis, k, h, w, n, nbuf, h2):
+    """First-pass update fused with the second pass's dots (one read of the
+    basis; bitwise the update then the dot pass): w -= V[0:k] h, h2[0:k] =
+    V[0:k]^H w, ||w||^2 into nbuf[0] and h2[k].  False when k exceeds one
+    kernel chunk (the caller then runs the two passes)."""
+    if k > _KCHUNK:
+        return False
+    ctx.call("hs_block_update_dot", ptr(basis.V[0]), basis.V.stride(0), k, ptr(h), ptr(w), n,
+             ptr(nbuf), ptr(h2))
+    return True
+
+
 def _givens_column(hess, cs, sn, g, k):
     """Apply the previous rotations to column k, form rotation k, update g
     (krylov.py:74-88)."""
@@ -244,9 +256,10 @@ def _gmres_cycle_pipelined(ops: _Ops, basis: _Basis, r0, r0_norm, bnorm, tol, ma
     def orthonormalise(k):
         w = basis.row(k + 1)
         _dot_pass(ctx, basis, k + 1, w, n, hb)
-        _update_pass(ctx, basis, k + 1, hb, w, n, nb[0:])
         gate = (nb[0:], hb[k + 1:])
-        _dot_pass(ctx, basis, k + 1, w, n, h2b, gate)
+        if not _update_dot_pass(ctx, basis, k + 1, hb, w, n, nb[0:], h2b):
+            _update_pass(ctx, basis, k + 1, hb, w, n, nb[0:])
+            _dot_pass(ctx, basis, k + 1, w, n, h2b, gate)
         _update_pass(ctx, basis, k + 1, h2b, w, n, nb[1:], gate)
         ctx.call("hs_scale_inv_sqrt", ptr(w), n, ptr(nb[1:]))
         pin[k].copy_(col, non_blocking=True)
@@ -327,14 +340,17 @@ def _gmres_cycle(ops: _Ops, basis: _Basis, r0, r0_norm, bnorm, tol, max_steps, h
             w_norm0 = None
         else:
             _dot_pass(ctx, basis, k + 1, w, n, hbuf)
-            _update_pass(ctx, basis, k + 1, hbuf, w, n, nbuf)
+            fused = _update_dot_pass(ctx, basis, k + 1, hbuf, w, n, nbuf, h2buf)
+            if not fused:
+                _update_pass(ctx, basis, k + 1, hbuf, w, n, nbuf)
             host = torch.cat([hbuf[:k + 2], nbuf[:1]]).cpu().numpy()
             hcol, w_norm0, nrm2 = host[:k + 1], host[k + 1].real, host[k + 2].real
             if not math.isfinite(w_norm0):
                 raise FloatingPointError("operator produced non-finite values "
                                          f"at iteration {len(history)}")
             if nrm2 < (_DGKS ** 2) * w_norm0:      # DGKS: re-orthogonalise once
-                _dot_pass(ctx, basis, k + 1, w, n, h2buf)
+                if not fused:
+                    _dot_pass(ctx, basis, k + 1, w, n, h2buf)
                 _update_pass(ctx, basis, k + 1, h2buf, w, n, nbuf)
                 host2 = torch.cat([h2buf[:k + 1], nbuf[:1]]).cpu().numpy()
                 hcol = hcol + host2[:k + 1]
