@@ -422,6 +422,7 @@ def run_ours(args):
     roofline["kernel"] = dom
     roofline["traffic"] = traffic
     stencil_roof = roof(["stencil", "residual", "jacobi", "jacobi2z"])
+    fused_roof = roof(["pre_fused", "post_fused"])
     shares = {k: {"share": v["ms"] / total_ms, "ms": v["ms"], "launches": v["launches"],
                   "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None}
               for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
@@ -463,6 +464,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "roofline": roofline,
             "roofline_stencil": stencil_roof,
+            "roofline_vcycle_fused": fused_roof,
             "kernel_shares": shares,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),

@@ -177,7 +177,7 @@ class Context:
     # built-in per-kernel-class event profiler
     KERNEL_CLASSES = ("stencil", "residual", "jacobi", "jacobi2z", "restrict", "prolong",
                       "sweep_gather", "sweep_front", "krylov_dot", "krylov_update",
-                      "krylov_other", "setup")
+                      "krylov_other", "setup", "pre_fused", "post_fused")
 
     def profile(self, on: bool):
         raise_for(self.lib.hs_profile_enable(self.h, int(on)), self.h)

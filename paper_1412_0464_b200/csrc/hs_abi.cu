@@ -97,13 +97,24 @@ struct Cycle {
   double2* tmp = nullptr;  // fine M f for apply_a
   SweepWork work{};        // lane-private sweep scratch (null: the sweep's own)
   bool lane = false;
+  bool fused = false;      // 2-D, nu = 2: fused pre / post kernels (u2 holds the pre-smoothed u)
+  double2* u2 = nullptr;
 };
+
+static bool want_fused(const Stencil* fine, const Transfer* t, int nu) {
+  static const bool off = getenv("HS_NO_FUSE") != nullptr;   // A/B switch
+  return !off && fused2d_ok(fine, t, nu);
+}
 
 // First half of the cycle: pre-smoothing from zero, residual, restriction
 // (everything before the coarse solve).
 static int vcycle_begin(Ctx* c, Cycle* cy, const double2* f, double2* u) {
   const int64_t nf = cy->fine->d.n;
   int r;
+  if (cy->fused) {   // u2 = S_pre(0), r = f - A u2 in one pass; then h^d P^T r
+    if ((r = stencil_pre2d(c, cy->fine, f, cy->u2, cy->r, cy->omega))) return r;
+    return transfer_restrict(c, cy->t, cy->r, cy->rc, cy->scale, 1);
+  }
   if (cy->nu > 0) {
     r = stencil_jacobi(c, cy->fine, u, f, cy->omega, cy->nu, 1, 1);
   } else {
@@ -122,6 +133,8 @@ static int vcycle_end(Ctx* c, Cycle* cy, const double2* f, double2* u, int sweep
   if ((r = sweep_apply(c, cy->sweep, cy->variant, cy->rc, cy->uc,
                        cy->lane ? &cy->work : nullptr, sweep_first)))
     return r;                                                                    // coarse solve
+  if (cy->fused)   // u = S_post(u2 + P uc) in one pass
+    return stencil_post2d(c, cy->fine, cy->t, cy->uc, f, cy->u2, u, cy->omega);
   if ((r = transfer_prolong(c, cy->t, cy->uc, u, 1, 1))) return r;             // u += P uc
   if (cy->nu > 0) r = stencil_jacobi(c, cy->fine, u, f, cy->omega, cy->nu, 0, 1);
   return r;
@@ -462,12 +475,14 @@ int hs_cycle_create(hs_ctx* c, const hs_stencil* fine, const hs_transfer* t,
   cy->nu = nu;
   cy->scale = restrict_scale;
   cy->variant = variant;
+  cy->fused = want_fused(fine, t, nu);
   cudaError_t e = cudaMalloc((void**)&cy->rc, coarse->d.n * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc((void**)&cy->uc, coarse->d.n * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc((void**)&cy->r, fine->d.n * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc((void**)&cy->tmp, fine->d.n * sizeof(double2));
+  if (e == cudaSuccess && cy->fused) e = cudaMalloc((void**)&cy->u2, fine->d.n * sizeof(double2));
   if (e != cudaSuccess) {
-    cudaFree(cy->rc); cudaFree(cy->uc); cudaFree(cy->r); cudaFree(cy->tmp);
+    cudaFree(cy->rc); cudaFree(cy->uc); cudaFree(cy->r); cudaFree(cy->tmp); cudaFree(cy->u2);
     delete cy;
     return check_cuda(c, e, "cycle buffers");
   }
@@ -491,12 +506,14 @@ int hs_cycle_create_lane(hs_ctx* c, const hs_cycle* base, hs_cycle** out) {
     delete cy;
     return r;
   }
+  cy->fused = base->fused;
   cudaError_t e = cudaMalloc((void**)&cy->rc, cy->coarse->d.n * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc((void**)&cy->uc, cy->coarse->d.n * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc((void**)&cy->r, cy->fine->d.n * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc((void**)&cy->tmp, cy->fine->d.n * sizeof(double2));
+  if (e == cudaSuccess && cy->fused) e = cudaMalloc((void**)&cy->u2, cy->fine->d.n * sizeof(double2));
   if (e != cudaSuccess) {
-    cudaFree(cy->rc); cudaFree(cy->uc); cudaFree(cy->r); cudaFree(cy->tmp);
+    cudaFree(cy->rc); cudaFree(cy->uc); cudaFree(cy->r); cudaFree(cy->tmp); cudaFree(cy->u2);
     sweep_work_destroy(&cy->work);
     delete cy;
     return check_cuda(c, e, "cycle lane buffers");
@@ -508,7 +525,7 @@ int hs_cycle_create_lane(hs_ctx* c, const hs_cycle* base, hs_cycle** out) {
 int hs_cycle_destroy(hs_ctx* c, hs_cycle* cy) {
   (void)c;
   if (!cy) return HS_OK;
-  cudaFree(cy->rc); cudaFree(cy->uc); cudaFree(cy->r); cudaFree(cy->tmp);
+  cudaFree(cy->rc); cudaFree(cy->uc); cudaFree(cy->r); cudaFree(cy->tmp); cudaFree(cy->u2);
   if (cy->lane) sweep_work_destroy(&cy->work);
   delete cy;
   return HS_OK;

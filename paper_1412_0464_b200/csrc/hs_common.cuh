@@ -63,7 +63,8 @@ __device__ __forceinline__ double2 shfl_xor_c(double2 v, int m) {
 // Kernel classes for the built-in event profiler (hs_profile_*).
 enum KernelClass : int {
   K_STENCIL = 0, K_RESIDUAL, K_JACOBI, K_JACOBI2Z, K_RESTRICT, K_PROLONG, K_SWEEP_GATHER,
-  K_SWEEP_FRONT, K_KRYLOV_DOT, K_KRYLOV_UPDATE, K_KRYLOV_OTHER, K_SETUP, K_NCLASS
+  K_SWEEP_FRONT, K_KRYLOV_DOT, K_KRYLOV_UPDATE, K_KRYLOV_OTHER, K_SETUP, K_PRE_FUSED,
+  K_POST_FUSED, K_NCLASS
 };
 
 struct ProfRec {
@@ -164,6 +165,15 @@ int stencil_finish_device(Ctx* c, Stencil* op);
 // kernels (hs_stencil.cu)
 int stencil_apply(Ctx* c, const Stencil* op, const double2* x, double2* y, int nrhs,
                   const double2* f_minus /*if non-null: y = f - A x*/);
+// fused 2-D V-cycle halves (nu = 2; hs_stencil.cu): pre = two Jacobi steps
+// from zero + residual (-> u2, r); post = prolongation-correction + two
+// Jacobi steps (u2, uc -> u)
+struct Transfer;
+bool fused2d_ok(const Stencil* op, const Transfer* t, int nu);
+int stencil_pre2d(Ctx* c, const Stencil* op, const double2* f, double2* u2, double2* r,
+                  double omega);
+int stencil_post2d(Ctx* c, const Stencil* op, const Transfer* t, const double2* uc,
+                   const double2* f, const double2* u2, double2* u, double omega);
 int stencil_jacobi(Ctx* c, const Stencil* op, double2* u, const double2* f, double omega,
                    int steps, int u_is_zero, int nrhs);
 

@@ -148,11 +148,22 @@ __global__ void k_reduce_parts(const double2* __restrict__ part, int nblk, int w
     if (pass_through && threadIdx.x == 0) out[0] = *gate.after;
     return;
   }
-  // one warp per output column, lanes over the blocks in fixed order
+  // one warp per output column, lanes over the blocks in fixed order; a
+  // lane's loads are issued together (independent), then summed in order
   const int wp = threadIdx.x >> 5, l = threadIdx.x & 31;
+  constexpr int kQ = 8;
   for (int i = wp; i < width; i += kThreads / 32) {
     double2 acc = czero();
-    for (int b = l; b < nblk; b += 32) acc = cadd(acc, part[(int64_t)b * width + i]);
+    for (int b0 = l; b0 < nblk; b0 += 32 * kQ) {
+      double2 v[kQ];
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int b = b0 + 32 * q;
+        v[q] = b < nblk ? __ldcg(part + (int64_t)b * width + i) : czero();
+      }
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) acc = cadd(acc, v[q]);
+    }
     for (int m = 16; m > 0; m >>= 1) {
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, m);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, m);

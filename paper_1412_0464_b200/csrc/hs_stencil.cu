@@ -186,3 +186,205 @@ int stencil_jacobi(Ctx* c, const Stencil* op, double2* u, const double2* f, doub
 }
 
 }  // namespace hs
+
+// ---------------------------------------------------------------------------
+// Fused fine-level halves of the V-cycle on 2-D levels (twogrid.py:150-159
+// with nu = 2): temporal blocking over a BY x BX tile with a two-point halo,
+// the intermediate smoother iterates in shared memory.
+//   pre:  u1 = w f / d (ring 2), u2 = u1 + w (f - A u1) / d (ring 1),
+//         r = f - A u2 (tile)                    -> u2, r
+//   post: u3 = u2 + P uc (ring 2), u4 = Jacobi(u3) (ring 1),
+//         u5 = Jacobi(u4) (tile)                 -> u5
+// Per point the arithmetic is that of the unfused kernels (k_stencil modes,
+// k_prolong), in the same order: the results are bitwise the same.  HBM
+// bytes per DOF (5-point): pre 16 f + 8 d + 80 A + 32 out = 136 (vs 256
+// unfused); post 16 u2 + 4 uc + 16 f + 8 d + 80 A + 16 out = 140 (vs 288);
+// halo re-reads hit L2.
+
+#include "hs_transfer.cuh"
+
+namespace hs {
+namespace {
+
+constexpr int kBX = 32, kBY = 16;              // tile (fastest axis x rows)
+constexpr int kR2X = kBX + 4, kR2Y = kBY + 4;  // tile + 2-point ring
+constexpr int kR1X = kBX + 2, kR1Y = kBY + 2;  // tile + 1-point ring
+
+// A x at global (g1, g2) = flat i from a shared-memory field V (row length
+// W, the point at (vy, vx)); couplings leaving the box are dropped.  The
+// coefficients are re-read per stage (L1/L2 hits for the tile's second
+// stage: keeping them in registers was measured slower -- occupancy).
+template <int S>
+__device__ __forceinline__ double2 apply_at(const StencilDesc& d, int64_t i, int g1, int g2,
+                                            const double2* V, int W, int vy, int vx) {
+  double2 acc = czero();
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int o1 = d.off[s][1], o2 = d.off[s][2];
+    const bool ok = (uint32_t)(g1 + o1) < (uint32_t)d.n1 && (uint32_t)(g2 + o2) < (uint32_t)d.n2;
+    const double2 c = __ldg(d.coeffs + (int64_t)s * d.n + i);
+    if (ok) acc = cfma(c, V[(vy + o1) * W + vx + o2], acc);
+  }
+  return acc;
+}
+
+template <int S>
+__global__ void __launch_bounds__(256)
+k_pre2d(StencilDesc d, const double2* __restrict__ f, double2* __restrict__ u2,
+        double2* __restrict__ r, double omega) {
+  __shared__ double2 U1[kR2Y * kR2X];
+  __shared__ double2 U2[kR1Y * kR1X];
+  const int n1 = (int)d.n1, n2 = (int)d.n2;
+  const int t1 = blockIdx.y * kBY, t2 = blockIdx.x * kBX;
+  for (int k = threadIdx.x; k < kR2Y * kR2X; k += blockDim.x) {   // u1 = w f / d, ring 2
+    const int ly = k / kR2X, lx = k - ly * kR2X;
+    const int g1 = t1 + ly - 2, g2 = t2 + lx - 2;
+    double2 v = czero();
+    if ((unsigned)g1 < (unsigned)n1 && (unsigned)g2 < (unsigned)n2) {
+      const int64_t j = (int64_t)g1 * n2 + g2;
+      v = cscale(omega, cmul(__ldg(f + j), __ldg(d.invd + j)));
+    }
+    U1[k] = v;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < kR1Y * kR1X; k += blockDim.x) {   // u2, ring 1
+    const int ly = k / kR1X, lx = k - ly * kR1X;
+    const int g1 = t1 + ly - 1, g2 = t2 + lx - 1;
+    double2 v = czero();
+    if ((unsigned)g1 < (unsigned)n1 && (unsigned)g2 < (unsigned)n2) {
+      const int64_t i = (int64_t)g1 * n2 + g2;
+      const double2 acc = apply_at<S>(d, i, g1, g2, U1, kR2X, ly + 1, lx + 1);
+      const double2 fi = __ldg(f + i), inv = __ldg(d.invd + i);
+      const double2 ui = cscale(omega, cmul(fi, inv));
+      v = cadd(ui, cmul(cscale(omega, csub(fi, acc)), inv));
+    }
+    U2[k] = v;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < kBY * kBX; k += blockDim.x) {   // r = f - A u2, tile
+    const int ly = k / kBX, lx = k - ly * kBX;
+    const int g1 = t1 + ly, g2 = t2 + lx;
+    if (g1 >= n1 || g2 >= n2) continue;
+    const int64_t i = (int64_t)g1 * n2 + g2;
+    const double2 acc = apply_at<S>(d, i, g1, g2, U2, kR1X, ly + 1, lx + 1);
+    u2[i] = U2[(ly + 1) * kR1X + lx + 1];
+    r[i] = csub(__ldg(f + i), acc);
+  }
+}
+
+// (P uc)[g1, g2] on a 2-D level: k_prolong's gather (axis 0 of the canonical
+// shape is the singleton)
+__device__ __forceinline__ double2 prolong_at(const TransferDesc& t, const double2* uc, int g1,
+                                              int g2) {
+  double2 acc = czero();
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const int p0 = t.par[0][a];
+    if (p0 < 0) continue;
+    const double w0 = t.pw[0][a];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int p1 = t.par[1][2 * g1 + b];
+      if (p1 < 0) continue;
+      const double w01 = w0 * t.pw[1][2 * g1 + b];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int p2 = t.par[2][2 * g2 + c];
+        if (p2 < 0) continue;
+        const double w = w01 * t.pw[2][2 * g2 + c];
+        const double2 v = __ldg(uc + ((int64_t)p0 * t.nc[1] + p1) * t.nc[2] + p2);
+        acc.x = fma(w, v.x, acc.x);
+        acc.y = fma(w, v.y, acc.y);
+      }
+    }
+  }
+  return acc;
+}
+
+template <int S>
+__global__ void __launch_bounds__(256)
+k_post2d(StencilDesc d, TransferDesc t, const double2* __restrict__ uc,
+         const double2* __restrict__ f, const double2* __restrict__ u2,
+         double2* __restrict__ u, double omega) {
+  __shared__ double2 U3[kR2Y * kR2X];
+  __shared__ double2 U4[kR1Y * kR1X];
+  const int n1 = (int)d.n1, n2 = (int)d.n2;
+  const int t1 = blockIdx.y * kBY, t2 = blockIdx.x * kBX;
+  for (int k = threadIdx.x; k < kR2Y * kR2X; k += blockDim.x) {   // u3 = u2 + P uc, ring 2
+    const int ly = k / kR2X, lx = k - ly * kR2X;
+    const int g1 = t1 + ly - 2, g2 = t2 + lx - 2;
+    double2 v = czero();
+    if ((unsigned)g1 < (unsigned)n1 && (unsigned)g2 < (unsigned)n2)
+      v = cadd(__ldg(u2 + (int64_t)g1 * n2 + g2), prolong_at(t, uc, g1, g2));
+    U3[k] = v;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < kR1Y * kR1X; k += blockDim.x) {   // u4, ring 1
+    const int ly = k / kR1X, lx = k - ly * kR1X;
+    const int g1 = t1 + ly - 1, g2 = t2 + lx - 1;
+    double2 v = czero();
+    if ((unsigned)g1 < (unsigned)n1 && (unsigned)g2 < (unsigned)n2) {
+      const int64_t i = (int64_t)g1 * n2 + g2;
+      const double2 acc = apply_at<S>(d, i, g1, g2, U3, kR2X, ly + 1, lx + 1);
+      const double2 fi = __ldg(f + i), inv = __ldg(d.invd + i);
+      v = cadd(U3[(ly + 1) * kR2X + lx + 1], cmul(cscale(omega, csub(fi, acc)), inv));
+    }
+    U4[k] = v;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < kBY * kBX; k += blockDim.x) {   // u5, tile
+    const int ly = k / kBX, lx = k - ly * kBX;
+    const int g1 = t1 + ly, g2 = t2 + lx;
+    if (g1 >= n1 || g2 >= n2) continue;
+    const int64_t i = (int64_t)g1 * n2 + g2;
+    const double2 acc = apply_at<S>(d, i, g1, g2, U4, kR1X, ly + 1, lx + 1);
+    const double2 fi = __ldg(f + i), inv = __ldg(d.invd + i);
+    u[i] = cadd(U4[(ly + 1) * kR1X + lx + 1], cmul(cscale(omega, csub(fi, acc)), inv));
+  }
+}
+
+}  // namespace
+
+bool fused2d_ok(const Stencil* op, const Transfer* t, int nu) {
+  const StencilDesc& d = op->d;
+  if (nu != 2 || op->dim != 2 || d.n0 != 1 || d.diag < 0 || op->has_zero_diag || !d.invd) return false;
+  if (d.S != 5 && d.S != 9) return false;
+  for (int s = 0; s < d.S; ++s)
+    if (d.off[s][0] != 0) return false;
+  if (d.n >= ((int64_t)1 << 31)) return false;
+  if (t) {
+    const TransferDesc& q = t->d;
+    for (int a = 0; a < 3; ++a)
+      if (q.fw_lo[a] != 0 || q.fw_cnt[a] != q.nf[a] || q.fr_lo[a] != 0 || q.fr_cnt[a] != q.nf[a])
+        return false;
+    if (q.nf[0] != 1 || q.nf[1] != d.n1 || q.nf[2] != d.n2) return false;
+  }
+  return true;
+}
+
+int stencil_pre2d(Ctx* c, const Stencil* op, const double2* f, double2* u2, double2* r,
+                  double omega) {
+  const StencilDesc& d = op->d;
+  dim3 grid((unsigned)((d.n2 + kBX - 1) / kBX), (unsigned)((d.n1 + kBY - 1) / kBY));
+  // algorithmic bytes: f, 1/d, coefficients once; u2 and r written
+  ProfScope ps(c, K_PRE_FUSED, (double)d.n * (16.0 * d.S + 16.0 + 8.0 + 32.0));
+  if (d.S == 5) k_pre2d<5><<<grid, 256, 0, c->stream>>>(d, f, u2, r, omega);
+  else k_pre2d<9><<<grid, 256, 0, c->stream>>>(d, f, u2, r, omega);
+  HS_LAUNCH_CHECK(c, "fused pre-smoothing kernel");
+  return HS_OK;
+}
+
+int stencil_post2d(Ctx* c, const Stencil* op, const Transfer* t, const double2* uc,
+                   const double2* f, const double2* u2, double2* u, double omega) {
+  const StencilDesc& d = op->d;
+  dim3 grid((unsigned)((d.n2 + kBX - 1) / kBX), (unsigned)((d.n1 + kBY - 1) / kBY));
+  const double nc = (double)(t->d.nc[0] * t->d.nc[1] * t->d.nc[2]);
+  // algorithmic bytes: u2, f, 1/d, coefficients, uc once; u written
+  ProfScope ps(c, K_POST_FUSED, (double)d.n * (16.0 * d.S + 16.0 + 16.0 + 8.0 + 16.0) + 16.0 * nc);
+  if (d.S == 5) k_post2d<5><<<grid, 256, 0, c->stream>>>(d, t->d, uc, f, u2, u, omega);
+  else k_post2d<9><<<grid, 256, 0, c->stream>>>(d, t->d, uc, f, u2, u, omega);
+  HS_LAUNCH_CHECK(c, "fused post-smoothing kernel");
+  return HS_OK;
+}
+
+}  // namespace hs

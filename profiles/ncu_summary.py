@@ -29,7 +29,8 @@ SCALE = {"usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "nsecond": 1e-3, 
 
 CLASS = [("k_front", "sweep_front"), ("k_bcr", "sweep_front"), ("k_part_solve", "sweep_front"), ("k_stencil<", None),
          ("k_block_dot", "krylov_dot"), ("k_block_update", "krylov_update"),
-         ("k_restrict", "restrict"), ("k_prolong", "prolong"), ("k_gather", "sweep_gather")]
+         ("k_restrict", "restrict"), ("k_prolong", "prolong"), ("k_gather", "sweep_gather"),
+         ("k_pre2d", "pre_fused"), ("k_post2d", "post_fused"), ("k3_solve", "sweep_front")]
 MODE = {"0": "stencil", "1": "residual", "2": "jacobi", "3": "jacobi2z"}
 
 

@@ -386,3 +386,42 @@ def test_exact_coarse_cycle_and_gmres():
     assert rel(u, d["gmres_u"]) < 1e-5
     with pytest.raises(ValueError):
         hb.tgsp_apply(cycle, d["vcycle_z"])
+
+
+_UNFUSED = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+sys.path.insert(0, sys.argv[1] + "/tests")
+from cases import case
+import paper_1412_0464_b200 as hb
+for name in ("wedge2d", "fe9_2d"):
+    mesh, model, fine_op, sm, sw = case(name)
+    cyc, _ = hb.build_two_grid(mesh, model, fine_op=fine_op, smoother=sm, coarse="sweep", sweep=sw)
+    z = np.load(sys.argv[2])[name]
+    np.save(sys.argv[2].replace(".npz", f"_{name}.npy"), cyc.vcycle(z))
+'''
+
+
+def test_fused_vcycle_bitwise_equals_unfused(tmp_path):
+    """The fused 2-D pre/post kernels (nu = 2) give bitwise the V-cycle of the
+    separate smoother / residual / prolongation kernels (HS_NO_FUSE=1 in a
+    subprocess), for a 5-point and a 9-point fine operator."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    rng = np.random.default_rng(5)
+    zs = {}
+    for name in ("wedge2d", "fe9_2d"):
+        zs[name] = crand(rng, case(name)[0].unknowns)
+    zp = tmp_path / "z.npz"
+    np.savez(zp, **zs)
+    script = tmp_path / "unfused.py"
+    script.write_text(_UNFUSED)
+    env = dict(os.environ, HS_NO_FUSE="1")
+    subprocess.run([sys.executable, str(script), str(ROOT), str(zp)], check=True, env=env,
+                   timeout=600)
+    for name in ("wedge2d", "fe9_2d"):
+        ref = np.load(tmp_path / f"z_{name}.npy")
+        out = _build(name).vcycle(zs[name])
+        assert np.array_equal(out, ref), name
