@@ -165,6 +165,17 @@ int hs_sweep_apply(hs_ctx* ctx, hs_sweep* s, int variant, const void* f, void* u
  * Fails with HS_E_SHAPE on an invalid grouping (NxCells.validate). */
 int hs_sweep_plan_nx(hs_ctx* ctx, hs_sweep* s, int ncell, const int64_t* j_cell,
                      const int64_t* j_mid, int* variant);
+/* One slab solve outside a schedule: subdom_solve (sweepdd.py:236-268).
+ * Slab j (1-based) with right-hand side rows [a, b) of f (global rows,
+ * 0-based) plus the transmission of the input traces B1 (forward, used when
+ * j > 1) and B3 (backward, j < J) -- each 2 x face, device, or NULL; the
+ * solution rows [ta, tb) are ADDED into u (u[ta:tb] += ud); out2 (j < J) /
+ * out4 (j > 1), when non-NULL, receive the outgoing 2 x face traces.  On a
+ * 2-D level the requested rows must be rows the sweep's schedules read
+ * (HS_E_SHAPE otherwise: the device slab solve updates those rows only). */
+int hs_sweep_solve_one(hs_ctx* ctx, hs_sweep* s, int j, int64_t a, int64_t b, int64_t ta,
+                       int64_t tb, const void* B1, const void* B3, void* out2, void* out4,
+                       const void* f, void* u);
 /* Exact solve of a whole stencil operator: factorize / Factorization.solve
  * (sparselin.py:40-68) and ExactCoarseSolver (twogrid.py:99-105).  Block LU
  * along the operator's second axis with dense planes of the first (x third)

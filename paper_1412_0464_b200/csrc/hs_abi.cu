@@ -422,6 +422,14 @@ int hs_sweep_create(hs_ctx* c, const hs_stencil* coarse, int J, const int64_t* b
   return HS_OK;
 }
 
+int hs_sweep_solve_one(hs_ctx* c, hs_sweep* s, int j, int64_t a, int64_t b, int64_t ta,
+                       int64_t tb, const void* B1, const void* B3, void* out2, void* out4,
+                       const void* f, void* u) {
+  if (!c || !s || !f || !u) return HS_E_ARG;
+  return sweep_solve_one(c, s, j, a, b, ta, tb, (const double2*)B1, (const double2*)B3,
+                         (double2*)out2, (double2*)out4, (const double2*)f, (double2*)u);
+}
+
 int hs_exact_create(hs_ctx* c, const hs_stencil* op, hs_sweep** out) {
   if (!c || !op || !out) return HS_E_ARG;
   Sweep* s = nullptr;

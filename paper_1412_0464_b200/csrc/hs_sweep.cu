@@ -2017,9 +2017,8 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     s->n0 = (int)coarse->shape[0];
     s->M = (int)(coarse->shape[1] * coarse->shape[2]);
     s->coarse = coarse;
-    const int ntin = build_schedule(s, J, beta, bt, lo, hi);
+    const int ntin = std::max(4, build_schedule(s, J, beta, bt, lo, hi));
     s->ntrace = ntin;
-  s->ntrace = ntin;
     int r = sweep3_create(c, s, coarse, slabs, lo, hi);
     if (!r) r = buffers(s, ntin);
     if (!r)
@@ -2122,7 +2121,7 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   const int B = C - 1;
   cudaError_t e = cudaSuccess;
 
-  const int ntin = build_schedule(s, J, beta, bt, lo, hi);
+  const int ntin = std::max(4, build_schedule(s, J, beta, bt, lo, hi));   // >= 4: sweep_solve_one
   s->ntrace = ntin;
   std::vector<SweepTask>& T = s->tasks;
 
@@ -2299,6 +2298,115 @@ void sweep_destroy(Sweep* s) {
   cudaFree(s->u2);
   cudaFree(s->d_tasks);
   delete s;
+}
+
+__global__ void k_add_rows(double2* __restrict__ u, const double2* __restrict__ v, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) u[i] = cadd(u[i], __ldg(v + i));
+}
+
+// One slab solve outside a schedule (subdom_solve, sweepdd.py:236-268):
+// right-hand side rows [a, b) of f plus the transmission of the given input
+// traces, solution rows [ta, tb) ADDED into u, outgoing traces on request.
+int sweep_solve_one(Ctx* c, Sweep* s, int j, int64_t a, int64_t b, int64_t ta, int64_t tb,
+                    const double2* B1, const double2* B3, double2* out2, double2* out4,
+                    const double2* f, double2* u) {
+  const int J = s->J, M = s->M;
+  if (j < 1 || j > J) return set_error(c, HS_E_SHAPE, "slab index out of range");
+  const int64_t lo = s->hlo[j - 1], hi = s->hhi[j - 1];
+  // rows must lie inside the slab's layers lo..hi (1-based points -> rows lo-1..hi-1)
+  if (a < lo - 1 || b > hi || a > b || ta < lo - 1 || tb > hi || ta > tb)
+    return set_error(c, HS_E_SHAPE, "rows outside the slab");
+  SweepTask t{};
+  t.slab = j - 1;
+  t.lo = (int)lo;
+  t.T = (int)(hi - lo + 1);
+  t.a = (int)a;
+  t.b = (int)b;
+  t.ta = (int)ta;
+  t.tb = (int)tb;
+  t.tin1 = t.tin3 = t.out2 = t.out4 = -1;
+  t.row1 = t.row3 = t.orow2 = t.orow4 = -1;
+  t.dst = 1;
+  const size_t tr = (size_t)2 * M * sizeof(double2);
+  if (B1 && j > 1) {
+    t.tin1 = 0;
+    t.row1 = (int)s->hbeta[j - 1] - t.lo;
+    HS_CUDA(c, cudaMemcpyAsync(s->trace, B1, tr, cudaMemcpyDeviceToDevice, c->stream), "trace in");
+  }
+  if (B3 && j < J) {
+    t.tin3 = 1;
+    t.row3 = (int)s->hbt[j] - t.lo;
+    HS_CUDA(c, cudaMemcpyAsync(s->trace + 2 * M, B3, tr, cudaMemcpyDeviceToDevice, c->stream),
+            "trace in");
+  }
+  if (out2 && j < J) {
+    t.out2 = 2;
+    t.orow2 = (int)s->hbeta[j] - t.lo;
+  }
+  if (out4 && j > 1) {
+    t.out4 = 3;
+    t.orow4 = (int)s->hbt[j - 1] - t.lo;
+  }
+  if (!s->s3 && s->nr) {   // the restricted updates compute the chain's rows only
+    const int* rs = s->hrows.data() + (size_t)t.slab * kNR;
+    auto has = [&](int x) { return std::find(rs, rs + kNR, x) != rs + kNR; };
+    bool ok = true;
+    for (int x = t.ta + 1 - t.lo; x < t.tb + 1 - t.lo; ++x) ok = ok && has(x);
+    if (t.out2 >= 0) ok = ok && has(t.orow2) && has(t.orow2 + 1);
+    if (t.out4 >= 0) ok = ok && has(t.orow4) && has(t.orow4 + 1);
+    if (!ok)
+      return set_error(c, HS_E_SHAPE,
+                       "solution rows outside the sweep's row sets (the device slab solve "
+                       "computes the rows its schedules read)");
+  }
+  if (s->s3) {
+    const SweepTask* ts[1] = {&t};
+    double2* us[2] = {s->u2, s->u2};
+    if (int r = sweep3_tasks(c, s, ts, 1, f, us, s->coarse->d.coeffs, s->coarse->d.n)) return r;
+  } else {
+    SweepTask* dt = (SweepTask*)scratch(c, sizeof(SweepTask), 3);
+    if (!dt) return set_error(c, HS_E_CUDA, "scratch allocation failed");
+    HS_CUDA(c, cudaMemcpyAsync(dt, &t, sizeof(SweepTask), cudaMemcpyHostToDevice, c->stream),
+            "task upload");
+    SolveArgs g{};
+    g.tasks = dt;
+    g.ffirst[0] = 0;
+    g.fcount[0] = 1;
+    g.g = make_chunks(s);
+    g.nchunk = s->tm == 16 ? Ring<16>::nchunk(s->mmax) : Ring<32>::nchunk(s->mmax);
+    g.stream = s->stream;
+    g.nbs = s->nbs;
+    g.plan = s->ptab;
+    g.rows = s->rows;
+    g.src = f;
+    g.coarse = s->coarse->d.coeffs;
+    g.ncoarse = s->coarse->d.n;
+    if (int r = slot_table(s->coarse, g.cslot, c)) return r;
+    g.trace = s->trace;
+    g.u[0] = s->u2;
+    g.u[1] = s->u2;
+    const int smem = s->tm == 16 ? Ring<16>::smem(s->mmax) : Ring<32>::smem(s->mmax);
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = solve_config(s->C, 1, smem, c->stream, attr);
+    ProfScope ps(c, K_SWEEP_FRONT, s->rec_bytes);
+    cudaError_t e = s->tm == 16 ? cudaLaunchKernelEx(&cfg, k_part_solve<16>, g)
+                                : cudaLaunchKernelEx(&cfg, k_part_solve<32>, g);
+    if (e != cudaSuccess) return check_cuda(c, e, "slab solve launch");
+    HS_LAUNCH_CHECK(c, "slab solve kernel");
+  }
+  const int64_t n = (tb - ta) * (int64_t)M;
+  if (n > 0) {
+    k_add_rows<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(u + ta * M, s->u2 + ta * M, n);
+    HS_LAUNCH_CHECK(c, "row scatter");
+  }
+  if (t.out2 >= 0)
+    HS_CUDA(c, cudaMemcpyAsync(out2, s->trace + 4 * M, tr, cudaMemcpyDeviceToDevice, c->stream),
+            "trace out");
+  if (t.out4 >= 0)
+    HS_CUDA(c, cudaMemcpyAsync(out4, s->trace + 6 * M, tr, cudaMemcpyDeviceToDevice, c->stream),
+            "trace out");
+  return HS_OK;
 }
 
 int sweep_work_create(Ctx* c, const Sweep* s, SweepWork* w) {

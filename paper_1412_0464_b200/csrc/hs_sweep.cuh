@@ -93,6 +93,10 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
 // returns the plan's variant id in *variant
 int sweep_plan_nx(Ctx* c, Sweep* s, int ncell, const int64_t* j_cell, const int64_t* j_mid,
                   int* variant);
+// one slab solve outside a schedule (subdom_solve); u rows [ta, tb) accumulated
+int sweep_solve_one(Ctx* c, Sweep* s, int j, int64_t a, int64_t b, int64_t ta, int64_t tb,
+                    const double2* B1, const double2* B3, double2* out2, double2* out4,
+                    const double2* f, double2* u);
 int sweep_work_create(Ctx* c, const Sweep* s, SweepWork* w);
 void sweep_work_destroy(SweepWork* w);
 

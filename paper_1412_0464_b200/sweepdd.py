@@ -9,6 +9,8 @@ Drop-in names of reference ``sweepdd.py``:
 * ``build_partition``                                    :192-218
 * ``prec_ud``, ``prec_x``, ``SweepingPreconditioner``    :312-359, :437-467
 * ``NxCells``, ``make_nx_cells``, ``prec_nx``           :362-434
+* ``subdom_solve``, ``forward_sweep``, ``backward_sweep``,
+  ``midsolve_in``, ``midsolve_out``                      :236-306
 
 Setup (geometry, slab operator assembly) runs on the host; the slabs are
 factorised on the device at ``build_partition`` time and every application
@@ -247,6 +249,98 @@ def extract_transmission(part: Partition, j: int, direction: str) -> Transmissio
 
 # ---------------------------------------------------------------------------
 # applications (device)
+
+def subdom_solve(part: Partition, u, f, j, a, b, ta, tb, tau1=False, B1=None, tau2=False,
+                 tau3=False, B3=None, tau4=False):
+    """One slab solve (sweepdd.py:236-268) on the device (hs_sweep_solve_one):
+    right-hand side rows a..b-1 of f plus the transmission sources of the
+    incoming traces, u[ta:tb] += the solution rows (u updated in place: a
+    numpy array or a torch CUDA tensor), returns the outgoing traces (out2,
+    out4) that were asked for (2 x face arrays) or None."""
+    import ctypes as C
+    import torch
+    from .device import ptr, to_device
+    J = part.J
+    if tau1 and j > 1 and B1 is None:
+        raise RuntimeError(f"forward transmission buffer for slab {j} not populated")
+    if tau3 and j < J and B3 is None:
+        raise RuntimeError(f"backward transmission buffer for slab {j} not populated")
+    sw = part.device()
+    ctx = sw.ctx
+    shape = part.shape
+    face = int(np.prod(shape[1:]))
+    ft, _ = to_device(f, sw.n, ctx)
+    is_np = not isinstance(u, torch.Tensor)
+    ut, _ = to_device(u, sw.n, ctx)
+    if not is_np and ut.data_ptr() != u.data_ptr():
+        raise ValueError("u must be a contiguous complex128 CUDA tensor (updated in place)")
+    ut = ut.clone() if is_np else ut
+
+    def trace_in(B, used):
+        if not used or B is None:
+            return None
+        return to_device(np.asarray(B) if not isinstance(B, torch.Tensor) else B, 2 * face,
+                         ctx)[0]
+    b1 = trace_in(B1, tau1 and j > 1)
+    b3 = trace_in(B3, tau3 and j < J)
+    o2 = torch.empty(2 * face, dtype=torch.complex128, device=ut.device) \
+        if tau2 and j < J else None
+    o4 = torch.empty(2 * face, dtype=torch.complex128, device=ut.device) \
+        if tau4 and j > 1 else None
+    nul = C.c_void_p(None)
+    ctx.call("hs_sweep_solve_one", sw.h, int(j), int(a), int(b), int(ta), int(tb),
+             ptr(b1) if b1 is not None else nul, ptr(b3) if b3 is not None else nul,
+             ptr(o2) if o2 is not None else nul, ptr(o4) if o4 is not None else nul,
+             ptr(ft), ptr(ut))
+    if is_np:
+        u[...] = ut.cpu().numpy().reshape(np.shape(u))
+    tshape = (2,) + tuple(shape[1:])
+
+    def out(t):
+        if t is None:
+            return None
+        return t.cpu().numpy().reshape(tshape) if is_np else t.reshape(tshape)
+    return out(o2), out(o4)
+
+
+def forward_sweep(part, u, f, j0, j1, B=None):
+    """Slab solves j0..j1 ascending with forward transmission; out-of-range
+    slab numbers are skipped (sweepdd.py:271-282)."""
+    for j in range(j0, j1 + 1):
+        if j < 1 or j > part.J:
+            continue
+        out, _ = subdom_solve(part, u, f, j, part.beta[j - 1], part.beta[j],
+                              part.beta[j - 1], part.beta[j],
+                              tau1=j > 1, B1=B, tau2=j < part.J)
+        if out is not None:
+            B = out
+    return B
+
+
+def backward_sweep(part, u, f, j0, j1, B=None):
+    """Slab solves j0..j1 descending with backward transmission (sweepdd.py:285-294)."""
+    for j in range(j0, j1 - 1, -1):
+        if j < 1 or j > part.J:
+            continue
+        _, out = subdom_solve(part, u, f, j, part.beta_tilde[j - 1], part.beta_tilde[j],
+                              part.beta_tilde[j - 1], part.beta_tilde[j],
+                              tau3=j < part.J, B3=B, tau4=j > 1)
+        if out is not None:
+            B = out
+    return B
+
+
+def midsolve_in(part, u, f, j, B1, B3):
+    """sweepdd.py:297-300."""
+    subdom_solve(part, u, f, j, part.beta[j - 1], part.beta_tilde[j],
+                 part.beta[j - 1], part.beta_tilde[j], tau1=True, B1=B1, tau3=True, B3=B3)
+
+
+def midsolve_out(part, u, f, j):
+    """sweepdd.py:303-306: returns (out2, out4)."""
+    return subdom_solve(part, u, f, j, part.beta_tilde[j - 1], part.beta[j],
+                        part.beta_tilde[j - 1], part.beta[j], tau2=True, tau4=True)
+
 
 def _apply(part: Partition, f, variant: str, cells=None):
     from .device import from_device

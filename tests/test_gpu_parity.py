@@ -425,3 +425,43 @@ def test_fused_vcycle_bitwise_equals_unfused(tmp_path):
         ref = np.load(tmp_path / f"z_{name}.npy")
         out = _build(name).vcycle(zs[name])
         assert np.array_equal(out, ref), name
+
+
+@pytest.mark.parametrize("name", ["wedge2d", "pml3d_s"])
+def test_subdom_solve_loops_reproduce_x_sweep(name):
+    """The reference's public slab-level functions (subdom_solve,
+    forward_sweep, backward_sweep, midsolve_in/out, sweepdd.py:236-306),
+    composed as prec_x does (sweepdd.py:322-359), give the reference's X sweep."""
+    import paper_1412_0464_b200 as hb
+    d = load_case(name)
+    part = hierarchy(name, device=True).partition
+    f = d["probe_xc"]
+    u = np.zeros(part.shape, complex)
+    J, jm = part.J, part.J // 2 + 1
+    B1 = hb.forward_sweep(part, u, f, 1, jm - 1)
+    B2 = hb.backward_sweep(part, u, f, J, jm + 1)
+    hb.midsolve_in(part, u, f, jm, B1, B2)
+    g = f - part.apply_global(u)
+    B2, B1 = hb.midsolve_out(part, u, g, jm)
+    hb.backward_sweep(part, u, g, jm - 1, 1, B1)
+    hb.forward_sweep(part, u, g, jm + 1, J, B2)
+    assert rel(u, d["sweep_x"]) < 1e-11
+
+
+def test_subdom_solve_semantics():
+    """test_sweepdd.py:99-130: zero input leaves u alone, rows outside
+    [ta, tb) untouched, an unpopulated transmission buffer raises."""
+    import paper_1412_0464_b200 as hb
+    part = hierarchy("wedge2d", device=True).partition
+    u = np.zeros(part.shape, complex)
+    f = np.zeros(part.shape, complex)
+    hb.subdom_solve(part, u, f, 2, part.beta[1], part.beta[2], part.beta[1], part.beta[2])
+    assert not u.any()
+    f[int(part.beta[1]) + 1] = 1.0
+    out, _ = hb.subdom_solve(part, u, f, 2, part.beta[1], part.beta[2], part.beta[1],
+                             part.beta[2], tau2=True)
+    assert u[part.beta[1]:part.beta[2]].any() and out is not None and out.shape[0] == 2
+    assert not u[:part.beta[1]].any() and not u[part.beta[2]:].any()
+    with pytest.raises(RuntimeError, match="buffer"):
+        hb.subdom_solve(part, u, f, 2, part.beta[1], part.beta[2], part.beta[1], part.beta[2],
+                        tau1=True)
