@@ -206,6 +206,12 @@ int stencil_jacobi(Ctx* c, const Stencil* op, double2* u, const double2* f, doub
 namespace hs {
 namespace {
 
+#ifndef HS_FUSED_MINB
+#define HS_FUSED_MINB 6   // 40 registers: 6 blocks per SM (measured best of 1 / 6 / 8)
+#endif
+#ifndef HS_FUSED_UNROLL
+#define HS_FUSED_UNROLL _Pragma("unroll")
+#endif
 constexpr int kBX = 32, kBY = 16;              // tile (fastest axis x rows)
 constexpr int kR2X = kBX + 4, kR2Y = kBY + 4;  // tile + 2-point ring
 constexpr int kR1X = kBX + 2, kR1Y = kBY + 2;  // tile + 1-point ring
@@ -229,14 +235,15 @@ __device__ __forceinline__ double2 apply_at(const StencilDesc& d, int64_t i, int
 }
 
 template <int S>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, HS_FUSED_MINB)
 k_pre2d(StencilDesc d, const double2* __restrict__ f, double2* __restrict__ u2,
         double2* __restrict__ r, double omega) {
   __shared__ double2 U1[kR2Y * kR2X];
   __shared__ double2 U2[kR1Y * kR1X];
   const int n1 = (int)d.n1, n2 = (int)d.n2;
   const int t1 = blockIdx.y * kBY, t2 = blockIdx.x * kBX;
-  for (int k = threadIdx.x; k < kR2Y * kR2X; k += blockDim.x) {   // u1 = w f / d, ring 2
+  HS_FUSED_UNROLL
+  for (int k = threadIdx.x; k < kR2Y * kR2X; k += 256) {   // u1 = w f / d, ring 2
     const int ly = k / kR2X, lx = k - ly * kR2X;
     const int g1 = t1 + ly - 2, g2 = t2 + lx - 2;
     double2 v = czero();
@@ -247,7 +254,8 @@ k_pre2d(StencilDesc d, const double2* __restrict__ f, double2* __restrict__ u2,
     U1[k] = v;
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < kR1Y * kR1X; k += blockDim.x) {   // u2, ring 1
+  HS_FUSED_UNROLL
+  for (int k = threadIdx.x; k < kR1Y * kR1X; k += 256) {   // u2, ring 1
     const int ly = k / kR1X, lx = k - ly * kR1X;
     const int g1 = t1 + ly - 1, g2 = t2 + lx - 1;
     double2 v = czero();
@@ -261,7 +269,8 @@ k_pre2d(StencilDesc d, const double2* __restrict__ f, double2* __restrict__ u2,
     U2[k] = v;
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < kBY * kBX; k += blockDim.x) {   // r = f - A u2, tile
+  HS_FUSED_UNROLL
+  for (int k = threadIdx.x; k < kBY * kBX; k += 256) {   // r = f - A u2, tile
     const int ly = k / kBX, lx = k - ly * kBX;
     const int g1 = t1 + ly, g2 = t2 + lx;
     if (g1 >= n1 || g2 >= n2) continue;
@@ -302,7 +311,7 @@ __device__ __forceinline__ double2 prolong_at(const TransferDesc& t, const doubl
 }
 
 template <int S>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, HS_FUSED_MINB)
 k_post2d(StencilDesc d, TransferDesc t, const double2* __restrict__ uc,
          const double2* __restrict__ f, const double2* __restrict__ u2,
          double2* __restrict__ u, double omega) {
@@ -310,7 +319,8 @@ k_post2d(StencilDesc d, TransferDesc t, const double2* __restrict__ uc,
   __shared__ double2 U4[kR1Y * kR1X];
   const int n1 = (int)d.n1, n2 = (int)d.n2;
   const int t1 = blockIdx.y * kBY, t2 = blockIdx.x * kBX;
-  for (int k = threadIdx.x; k < kR2Y * kR2X; k += blockDim.x) {   // u3 = u2 + P uc, ring 2
+  HS_FUSED_UNROLL
+  for (int k = threadIdx.x; k < kR2Y * kR2X; k += 256) {   // u3 = u2 + P uc, ring 2
     const int ly = k / kR2X, lx = k - ly * kR2X;
     const int g1 = t1 + ly - 2, g2 = t2 + lx - 2;
     double2 v = czero();
@@ -319,7 +329,8 @@ k_post2d(StencilDesc d, TransferDesc t, const double2* __restrict__ uc,
     U3[k] = v;
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < kR1Y * kR1X; k += blockDim.x) {   // u4, ring 1
+  HS_FUSED_UNROLL
+  for (int k = threadIdx.x; k < kR1Y * kR1X; k += 256) {   // u4, ring 1
     const int ly = k / kR1X, lx = k - ly * kR1X;
     const int g1 = t1 + ly - 1, g2 = t2 + lx - 1;
     double2 v = czero();
@@ -332,7 +343,8 @@ k_post2d(StencilDesc d, TransferDesc t, const double2* __restrict__ uc,
     U4[k] = v;
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < kBY * kBX; k += blockDim.x) {   // u5, tile
+  HS_FUSED_UNROLL
+  for (int k = threadIdx.x; k < kBY * kBX; k += 256) {   // u5, tile
     const int ly = k / kBX, lx = k - ly * kBX;
     const int g1 = t1 + ly, g2 = t2 + lx;
     if (g1 >= n1 || g2 >= n2) continue;
