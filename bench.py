@@ -209,6 +209,16 @@ class ClockSampler:
                 "sampler": "nvidia-smi -lms 200" if self.proc is not None else "nvml"}
 
 
+def fine_operator(p):
+    """The config's fine operator: None = the 5-point FD default (SURVEY F2
+    (ii)); "fe9" / "fe27" = the literal compact FE-opt operator (C5's
+    27-point stencil, BASELINE configs[4])."""
+    if p.fine == "fd5":
+        return None
+    from paper_1412_0464_b200.configs import fe_fine_operator
+    return fe_fine_operator(p.mesh, p.model)
+
+
 def workload_name(p):
     op = {"fd5": "5-point fine op (SURVEY F2 ii)", "fe9": "9-point compact fine op",
           "fe27": "27-point compact fine op"}[p.fine]
@@ -245,7 +255,7 @@ def run_reference(args):
     import paper_1412_0464_b200 as hb
     from paper_1412_0464_b200.configs import config
     p = config(args.config, args.scale)
-    hh = hb.build_hierarchy(p.mesh, p.model, None, hb.SmootherConfig(p.omega_jac, p.nu),
+    hh = hb.build_hierarchy(p.mesh, p.model, fine_operator(p), hb.SmootherConfig(p.omega_jac, p.nu),
                             hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains),
                             device=False)
     its_target = {0: 9, 1: 48}.get(args.config, 50) if args.scale == 1 else 30
@@ -289,7 +299,8 @@ def run_ours(args):
     p = config(args.config, args.scale)
     t0 = time.perf_counter()
     keep = (rank == 0 and world == 1 and not args.no_cpu_baseline)
-    cycle, _ = hb.build_two_grid(p.mesh, p.model, smoother=hb.SmootherConfig(p.omega_jac, p.nu),
+    cycle, _ = hb.build_two_grid(p.mesh, p.model, fine_op=fine_operator(p),
+                                 smoother=hb.SmootherConfig(p.omega_jac, p.nu),
                                  coarse="sweep",
                                  sweep=hb.SweepOptions(p.w_dd, p.s_dd, "x",
                                                        subdomains=p.subdomains),
@@ -490,7 +501,7 @@ def run_sharded(args):
                                              ShardedTGSP, plan_shards, scatter_rows)
     p = config(args.config, args.scale)
     t0 = time.perf_counter()
-    hh = hb.build_hierarchy(p.mesh, p.model, None, hb.SmootherConfig(p.omega_jac, p.nu),
+    hh = hb.build_hierarchy(p.mesh, p.model, fine_operator(p), hb.SmootherConfig(p.omega_jac, p.nu),
                             hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains),
                             keep_slab_ops=False)
     G = world if world > 1 else max(1, args.local_shards)

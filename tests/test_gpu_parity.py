@@ -465,3 +465,45 @@ def test_subdom_solve_semantics():
     with pytest.raises(RuntimeError, match="buffer"):
         hb.subdom_solve(part, u, f, 2, part.beta[1], part.beta[2], part.beta[1], part.beta[2],
                         tau1=True)
+
+
+def _large_anchors():
+    import json
+    from conftest import GOLDEN
+    f = GOLDEN / "large_anchors.json"
+    return json.loads(f.read_text()) if f.exists() else {}
+
+
+@pytest.mark.parametrize("name", ["C2", "C4_rhs0", "C3_half", "C5_half"])
+def test_baseline_config_matches_reference_solve(name):
+    """BASELINE configs at full (C2, C4 right-hand side 0) or half size (C3,
+    C5), solved by the reference itself (tests/golden/make_large_anchors.py):
+    the same GMRES iteration count +-1, residual histories within 1e-6
+    relative over the common iterations, true residual <= 1e-6 and the
+    solution within 1e-5 relative at the sampled unknowns."""
+    import paper_1412_0464_b200 as hb
+    from paper_1412_0464_b200.configs import config, fe_fine_operator
+    a = _large_anchors().get(name)
+    if a is None:
+        pytest.skip(f"no reference anchor for {name}")
+    p = config(a["config"], a["scale"])
+    fine = fe_fine_operator(p.mesh, p.model) if a.get("fine_operator", "fd5") != "fd5" else None
+    cycle, _ = hb.build_two_grid(p.mesh, p.model, fine_op=fine,
+                                 smoother=hb.SmootherConfig(p.omega_jac, p.nu), coarse="sweep",
+                                 sweep=hb.SweepOptions(p.w_dd, p.s_dd, "x",
+                                                       subdomains=p.subdomains),
+                                 keep_slab_ops=False)
+    assert cycle.hierarchy.partition.J == a["subdomains"]
+    f = p.f[a["rhs"]].ravel()
+    u, rep = hb.gmres(cycle.fine_csr, cycle.as_preconditioner(), f,
+                      hb.GmresConfig(p.tol, p.max_iter, p.restart))
+    assert abs(rep.iterations - a["iterations"]) <= 1, (rep.iterations, a["iterations"])
+    k = min(len(rep.residual_history), len(a["history"]))
+    h_ref = np.asarray(a["history"][:k])
+    assert np.all(np.abs(rep.residual_history[:k] - h_ref) <= 1e-6 * h_ref + 1e-14)
+    res = np.linalg.norm(f - cycle.fine_csr @ u) / np.linalg.norm(f)
+    assert rep.converged and res <= 1e-6
+    idx = np.asarray(a["u_sample_idx"])
+    ref = np.asarray(a["u_sample_re"]) + 1j * np.asarray(a["u_sample_im"])
+    assert np.linalg.norm(u[idx] - ref) <= 1e-5 * np.linalg.norm(ref)
+    assert abs(np.linalg.norm(u) - a["u_norm"]) <= 1e-5 * a["u_norm"]
