@@ -265,6 +265,11 @@ def solve_many(cycle: TwoGridCycle, rhs, config=None, lanes: int = 4, orth: str 
     rhs = list(rhs)
     if not rhs:
         return []
+    if lanes <= 1 or not _lane_capable(cycle):
+        # 3-D levels and the exact coarse solve run one cooperative all-SM
+        # chain per slab solve: no concurrent lanes, solves in order
+        prec = cycle.as_preconditioner()
+        return [gmres(cycle.fine_csr, prec, f, config, orth=orth) for f in rhs]
     pool = getattr(cycle, "_lanes", [])
     want = max(1, min(lanes, len(rhs)))
     if len(pool) < want:
@@ -293,6 +298,11 @@ def solve_many(cycle: TwoGridCycle, rhs, config=None, lanes: int = 4, orth: str 
     for ln in pool:
         main.wait_stream(ln.stream)
     return out
+
+
+def _lane_capable(cycle: TwoGridCycle) -> bool:
+    """Lanes need a 2-D sweep coarse solver (private sweep scratch per lane)."""
+    return isinstance(cycle.coarse_solver, SweepCoarseSolver) and cycle.coarse_op.dim == 2
 
 
 def vcycle(cycle: TwoGridCycle, f):

@@ -507,3 +507,21 @@ def test_baseline_config_matches_reference_solve(name):
     ref = np.asarray(a["u_sample_re"]) + 1j * np.asarray(a["u_sample_im"])
     assert np.linalg.norm(u[idx] - ref) <= 1e-5 * np.linalg.norm(ref)
     assert abs(np.linalg.norm(u) - a["u_norm"]) <= 1e-5 * a["u_norm"]
+
+
+def test_solve_many_without_lanes_for_exact_and_3d():
+    """solve_many falls back to in-order solves where lanes do not apply
+    (exact coarse solve, 3-D levels); results equal separate gmres calls."""
+    import paper_1412_0464_b200 as hb
+    from cases import constant_case
+    from paper_1412_0464_b200.mesh import PML, AbsorbingLayerSpec
+    mesh, model = constant_case(2, 32, AbsorbingLayerSpec(PML, 4, 20.0), 10.0)
+    cycle, _ = hb.build_two_grid(mesh, model, smoother=hb.SmootherConfig(0.8, 2),
+                                 coarse="exact")
+    rng = np.random.default_rng(9)
+    fs = [crand(rng, mesh.unknowns).ravel() for _ in range(3)]
+    cfg = hb.GmresConfig(1e-6, 100, 20)
+    many = hb.solve_many(cycle, fs, cfg, lanes=4)
+    for f, (u, rep) in zip(fs, many):
+        u1, rep1 = hb.gmres(cycle.fine_csr, cycle.as_preconditioner(), f, cfg)
+        assert rep.iterations == rep1.iterations and np.array_equal(u, u1)
