@@ -414,7 +414,9 @@ def run_ours(args):
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(dom)
+            tj = json.loads(tf.read_text())
+            # ncu traffic was captured on one config (C2): not another config's
+            traffic = tj.get(dom) if tj.get("config", 1) == args.config and args.scale == 1 else None
         except Exception:
             traffic = None
 

@@ -2458,8 +2458,8 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
         break;
       }
       case SweepLaunch::kSolve: {
-        if (s->s3) {   // 3-D: the fronts' slab solves in order (host-driven block LU)
-          ProfScope ps(c, K_SWEEP_FRONT, Lh.bytes);
+        if (s->s3) {   // 3-D: the fronts' slab solves in order (host-driven block LU;
+                       // sweep3_tasks attributes the GEMV and chain kernels itself)
           if (w->g != s->g) return set_error(c, HS_E_ARG, "sweep lanes need a 2-D level");
           double2* us[2] = {u, s->u2};
           // fronts zipped in pairs (two chains per launch); a task identical

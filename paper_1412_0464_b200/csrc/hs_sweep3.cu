@@ -567,6 +567,12 @@ int sweep3_tasks(Ctx* c, Sweep* s, const SweepTask* const* ts, int nt, const dou
     smem = std::max(smem, k3_smem(nb, nt == 2 ? (k ? G - g0 : g0) : G, nbuf[k]));
   }
   if (nt == 1) ch[1] = ch[0];
+  // profiler: the chain kernel (and the output scatter) as sweep_front, with
+  // its algorithmic bytes -- both factor planes of every step + Y in/out
+  double chain_bytes = 0;
+  for (int k = 0; k < nt; ++k)
+    chain_bytes += (2.0 * (n1 - 1)) * (double)NB[k] * NB[k] * 16.0 + 48.0 * n1 * (double)NB[k];
+  ProfScope pf(c, K_SWEEP_FRONT, chain_bytes);
   {   // the chains: one cooperative launch
     S3_TRY(cudaMemsetAsync(s3->gbar, 0, 2 * sizeof(unsigned), c->stream), "memset");
     int g0_ = g0, n1_ = n1, n2_ = n2;

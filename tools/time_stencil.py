@@ -7,7 +7,9 @@ from paper_1412_0464_b200.configs import config
 from paper_1412_0464_b200.device import to_device, empty, ptr
 idx = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 p = config(idx)
-cycle, _ = hb.build_two_grid(p.mesh, p.model, smoother=hb.SmootherConfig(p.omega_jac, p.nu), coarse="sweep",
+from paper_1412_0464_b200.configs import fe_fine_operator
+fine = fe_fine_operator(p.mesh, p.model) if p.fine != "fd5" else None
+cycle, _ = hb.build_two_grid(p.mesh, p.model, fine_op=fine, smoother=hb.SmootherConfig(p.omega_jac, p.nu), coarse="sweep",
                              sweep=hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains), keep_slab_ops=False)
 dev = cycle.device()
 op = dev.fine
