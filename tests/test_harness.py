@@ -59,3 +59,25 @@ def test_save_field_from_device(tmp_path):
     p = tmp_path / "u.bin"
     hz.save_field(p, torch.from_numpy(d["field_u"]).cuda())
     assert p.read_bytes() == d["field_bytes"].tobytes()
+
+
+def test_nx_cells_host_logic():
+    """make_nx_cells / NxCells.validate (sweepdd.py:362-401) against the
+    groupings the reference produced (nx2d.npz) and its error cases."""
+    from conftest import NX_KEYS
+    from paper_1412_0464_b200.sweepdd import NxCells, make_nx_cells
+    d = load_case("nx2d")
+    for n in (1, 2, 3, 4):
+        c = make_nx_cells(8, n)
+        assert list(c.j_cell) == list(d[f"nx{n}_cells"]) and list(c.j_mid) == list(d[f"nx{n}_mid"])
+        assert c.n_cell == n
+    NxCells(tuple(int(v) for v in d["nxc_cells"]), tuple(int(v) for v in d["nxc_mid"])).validate(8)
+    assert "nxc" in NX_KEYS
+    with pytest.raises(ValueError):
+        make_nx_cells(8, 5)
+    with pytest.raises(ValueError, match="sentinel|start at -1"):
+        NxCells((0, 4, 9), (2, 6)).validate(8)
+    with pytest.raises(ValueError, match="strictly increasing"):
+        NxCells((-1, 4, 4, 9), (2, 3, 6)).validate(8)
+    with pytest.raises(ValueError, match="meeting slab"):
+        NxCells((-1, 4, 9), (5, 6)).validate(8)
