@@ -525,3 +525,26 @@ def test_solve_many_without_lanes_for_exact_and_3d():
     for f, (u, rep) in zip(fs, many):
         u1, rep1 = hb.gmres(cycle.fine_csr, cycle.as_preconditioner(), f, cfg)
         assert rep.iterations == rep1.iterations and np.array_equal(u, u1)
+
+
+def test_nx_many_cells_split_launches(rng):
+    """NX with more fronts than one launch holds (C1's J = 38, 10 and 19
+    cells: 20 / 38 fronts per pass, several launches per stage) against the
+    oracle's prec_nx (sweepdd.py:403-434)."""
+    import paper_1412_0464_b200 as hb
+    from oracle import tgsp_oracle as orc
+    from paper_1412_0464_b200.configs import config
+    p = config(0)
+    kw = dict(device=True)
+    hh = hb.build_hierarchy(p.mesh, p.model, None, hb.SmootherConfig(p.omega_jac, p.nu),
+                            hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains), **kw)
+    hh_host = hb.build_hierarchy(p.mesh, p.model, None, hb.SmootherConfig(p.omega_jac, p.nu),
+                                 hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains),
+                                 device=False)
+    tg = orc.from_hierarchy(hh_host)
+    part = hh.partition
+    f = crand(rng, part.shape)
+    for nc in (10, part.J // 2):
+        cells = hb.make_nx_cells(part.J, nc)
+        ref = tg.part.prec_nx(f, cells.j_cell, cells.j_mid)
+        assert rel(hb.prec_nx(part, f, cells), ref) < 1e-11, nc
