@@ -138,16 +138,17 @@ def test_gmres_iterations(name):
         assert rel(u, d["gmres_u"]) < 1e-5
 
 
-def test_c1_config_anchors():
-    """BASELINE configs[0]: |tgsp_apply(z)| and sampled entries vs the reference,
-    GMRES(20) iteration count vs the reference (9)."""
+@pytest.mark.parametrize("variant", ["x", "ud"])
+def test_c1_config_anchors(variant):
+    """BASELINE configs[0] with the X and UD sweeps: |tgsp_apply(z)| and sampled
+    entries vs the reference, GMRES(20) iteration count vs the reference (9)."""
     import paper_1412_0464_b200 as hb
     from paper_1412_0464_b200.configs import config
-    a = c1_anchors()
+    a = {"x": c1_anchors()[variant]}
     p = config(0)
     cycle, _ = hb.build_two_grid(p.mesh, p.model, smoother=hb.SmootherConfig(p.omega_jac, p.nu),
                                  coarse="sweep",
-                                 sweep=hb.SweepOptions(p.w_dd, p.s_dd, "x",
+                                 sweep=hb.SweepOptions(p.w_dd, p.s_dd, variant,
                                                        subdomains=p.subdomains))
     rng = np.random.default_rng(0)
     z = rng.standard_normal(p.mesh.unknowns) + 1j * rng.standard_normal(p.mesh.unknowns)
@@ -548,3 +549,18 @@ def test_nx_many_cells_split_launches(rng):
         cells = hb.make_nx_cells(part.J, nc)
         ref = tg.part.prec_nx(f, cells.j_cell, cells.j_mid)
         assert rel(hb.prec_nx(part, f, cells), ref) < 1e-11, nc
+
+
+def test_exact_coarse_cycle_3d_vs_oracle(rng):
+    """3-D V-cycle with the exact coarse solve (device block LU over the whole
+    coarse operator) vs the oracle's SuperLU coarse solve."""
+    import paper_1412_0464_b200 as hb
+    from oracle import tgsp_oracle as orc
+    mesh, model, _, sm, _ = case("pml3d")
+    cycle, _ = hb.build_two_grid(mesh, model, smoother=sm, coarse="exact")
+    tg = orc.TwoGrid(orc.Op.from_dict(cycle.fine_op.coeffs),
+                     orc.prolongation(cycle.cmap.fine_point_of_coarse, cycle.cmap.refined_cell),
+                     orc.Exact(orc.Op.from_dict(cycle.coarse_op.coeffs)), sm.omega_jac, sm.nu,
+                     cycle.restrict_scale, "exact")
+    z = crand(rng, mesh.unknowns)
+    assert rel(cycle.vcycle(z), tg.vcycle(z)) < 1e-10
