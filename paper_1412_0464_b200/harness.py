@@ -24,6 +24,8 @@ import numpy as np
 
 @dataclass
 class ResultRow:
+    """One results-CSV row; the field order is the CSV column order."""
+
     key: str
     model: str
     dim: int
@@ -47,53 +49,52 @@ class ResultRow:
         return [f.name for f in fields(ResultRow)]
 
     def values(self):
-        return [getattr(self, name) for name in self.columns()]
+        return [self.__dict__[name] for name in self.columns()]
 
 
-def _cell(v):
-    return repr(v) if isinstance(v, float) else v
+_TYPES = {"dim": int, "size": int, "w_dd": int, "subdomains": int, "iterations": int,
+          "freq": float, "final_residual": float, "setup_time": float, "solve_time": float,
+          "converged": lambda v: v == "True"}
 
 
 def write_rows(path, rows, append=False):
-    """CSV with a header row; floats written with repr (round-trip exact)."""
-    mode = "a" if append and Path(path).exists() else "w"
-    with open(path, mode, newline="", encoding="utf-8") as fh:
-        w = csv.writer(fh)
-        if mode == "w":
-            w.writerow(ResultRow.columns())
-        for row in rows:
-            w.writerow([_cell(v) for v in row.values()])
-
-
-_INT = ("dim", "size", "w_dd", "subdomains", "iterations")
-_FLOAT = ("freq", "final_residual", "setup_time", "solve_time")
+    """Rows to CSV (header first when the file is new); floats as repr, so a
+    read-back is exact."""
+    path = Path(path)
+    fresh = not (append and path.exists())
+    with path.open("w" if fresh else "a", newline="", encoding="utf-8") as fh:
+        out = csv.writer(fh)
+        if fresh:
+            out.writerow(ResultRow.columns())
+        out.writerows([[repr(v) if isinstance(v, float) else v for v in r.values()]
+                       for r in rows])
 
 
 def read_rows(path):
-    out = []
+    """CSV rows as dicts with the numeric / boolean columns converted."""
     with open(path, newline="", encoding="utf-8") as fh:
-        for rec in csv.DictReader(fh):
-            for k in _INT:
-                rec[k] = int(rec[k])
-            for k in _FLOAT:
-                rec[k] = float(rec[k])
-            rec["converged"] = rec["converged"] == "True"
-            out.append(rec)
-    return out
+        return [{k: _TYPES[k](v) if k in _TYPES else v for k, v in rec.items()}
+                for rec in csv.DictReader(fh)]
+
+
+def _xfast(dims):
+    """Reshape order of an x-fastest file: the raw samples are the C-order
+    array of the reversed shape, transposed back."""
+    return tuple(int(n) for n in dims)[::-1]
 
 
 def load_model(path, dims, dtype="<f4") -> np.ndarray:
     """Velocities on the lattice ``dims`` (x-fastest raw file) as float64."""
-    dims = tuple(int(d) for d in dims)
+    dims = tuple(int(n) for n in dims)
     raw = np.fromfile(path, dtype=dtype)
-    expected = int(np.prod(dims))
-    if raw.size != expected:
-        raise ValueError(f"{path}: {raw.size} samples, expected {expected} "
-                         f"({expected * 4} bytes) for dims {dims}")
-    bad = np.flatnonzero(raw <= 0.0)
-    if bad.size:
-        raise ValueError(f"{path}: nonpositive velocity at flat index {bad[0]}")
-    return raw.reshape(dims[::-1]).T.astype(float)
+    need = int(np.prod(dims))
+    if raw.size != need:
+        raise ValueError(f"{path}: {raw.size} samples, expected {need} "
+                         f"({need * 4} bytes) for dims {dims}")
+    nonpos = np.nonzero(raw <= 0.0)[0]
+    if len(nonpos):
+        raise ValueError(f"{path}: nonpositive velocity at flat index {nonpos[0]}")
+    return np.transpose(raw.reshape(_xfast(dims))).astype(np.float64)
 
 
 def save_field(path, u):
@@ -104,19 +105,17 @@ def save_field(path, u):
         t = t.permute(*reversed(range(t.dim()))).contiguous()   # x-fastest, on the device
         h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
         h.copy_(t)
-        inter = torch.view_as_real(h).numpy().reshape(-1)
+        flat = h.numpy().reshape(-1)
     else:
-        flat = np.ascontiguousarray(np.asarray(u, dtype=complex).T)
-        inter = np.empty(flat.size * 2)
-        inter[0::2] = flat.real.ravel()
-        inter[1::2] = flat.imag.ravel()
-    np.asarray(inter, dtype="<f8").tofile(path)
+        flat = np.transpose(np.asarray(u, dtype=np.complex128)).reshape(-1)
+    # complex128 in memory is exactly (re, im) float64 pairs
+    np.ascontiguousarray(flat).view(np.float64).astype("<f8").tofile(path)
 
 
 def load_field(path, dims) -> np.ndarray:
-    dims = tuple(int(d) for d in dims)
+    dims = tuple(int(n) for n in dims)
     raw = np.fromfile(path, dtype="<f8")
     if raw.size != 2 * int(np.prod(dims)):
         raise ValueError(f"{path}: wrong size for dims {dims}")
-    u = raw[0::2] + 1j * raw[1::2]
-    return u.reshape(dims[::-1]).T
+    z = raw.astype(np.float64).view(np.complex128)
+    return np.transpose(z.reshape(_xfast(dims)))

@@ -21,19 +21,33 @@ from .discretize import StencilOperator
 
 
 def to_csr(op) -> sp.csr_matrix:
-    """CSR matrix of a stencil operator (row-major unknown ordering), host."""
-    shape = op.shape
-    n = int(np.prod(shape))
-    flat = np.arange(n).reshape(shape)
+    """CSR matrix of a stencil operator (row-major unknown ordering), host:
+    for every offset, the (row, row + offset) pairs whose neighbour lies in
+    the box carry that offset's coefficient at the row."""
+    shape = tuple(op.shape)
+    idx = np.arange(int(np.prod(shape))).reshape(shape)
     rows, cols, vals = [], [], []
-    for off, c in op.coeffs.items():
-        dst = tuple(slice(max(0, -o), m + min(0, -o)) for o, m in zip(off, shape))
-        src = tuple(slice(max(0, o), m + min(0, o)) for o, m in zip(off, shape))
-        rows.append(flat[dst].ravel())
-        cols.append(flat[src].ravel())
-        vals.append(np.asarray(c)[dst].ravel())
-    a = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
-                      shape=(n, n), dtype=complex).tocsr()
+    for off, coef in op.coeffs.items():
+        keep = np.ones(shape, dtype=bool)
+        for ax, o in enumerate(off):
+            n = shape[ax]
+            sl = [slice(None)] * len(shape)
+            if o > 0:
+                sl[ax] = slice(n - o, n)
+            elif o < 0:
+                sl[ax] = slice(0, -o)
+            else:
+                continue
+            keep[tuple(sl)] = False
+        r = idx[keep]
+        strides = [int(np.prod(shape[ax + 1:])) for ax in range(len(shape))]
+        c = r + sum(o * st for o, st in zip(off, strides))
+        rows.append(r)
+        cols.append(c)
+        vals.append(np.asarray(coef, dtype=complex)[keep])
+    n = idx.size
+    a = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                      shape=(n, n), dtype=complex)
     a.sort_indices()
     return a
 

@@ -375,32 +375,35 @@ class NxCells:
     def n_cell(self):
         return len(self.j_cell) - 1
 
+    def _span(self, m, J):
+        """Slabs of cell m (1-based), clipped to 1..J."""
+        return max(1, self.j_cell[m - 1] + 1), min(J, self.j_cell[m] - 1)
+
     def validate(self, J):
-        jc, jm = self.j_cell, self.j_mid
-        if jc[0] != -1 or jc[-1] != J + 1:
+        b = np.asarray(self.j_cell)
+        if b[0] != -1 or b[-1] != J + 1:
             raise ValueError("cell boundaries must start at -1 and end at J+1")
-        if len(jm) != self.n_cell:
+        if len(self.j_mid) != len(b) - 1:
             raise ValueError("one meeting slab per cell required")
-        if any(jc[i] >= jc[i + 1] for i in range(len(jc) - 1)):
+        if np.any(np.diff(b) <= 0):
             raise ValueError("cell boundaries must be strictly increasing")
-        for m in range(1, self.n_cell + 1):
-            lo = max(1, jc[m - 1] + 1)
-            hi = min(J, jc[m] - 1)
-            if not lo <= jm[m - 1] <= hi:
-                raise ValueError(f"cell {m}: meeting slab {jm[m - 1]} outside [{lo},{hi}]")
+        for m, mid in enumerate(self.j_mid, start=1):
+            lo, hi = self._span(m, J)
+            if mid < lo or mid > hi:
+                raise ValueError(f"cell {m}: meeting slab {mid} outside [{lo},{hi}]")
 
 
 def make_nx_cells(J: int, n_cell: int) -> NxCells:
-    """Evenly spaced cells, each meeting at its middle slab (sweepdd.py:392-401)."""
-    if not 1 <= n_cell <= J // 2:
+    """n_cell cells of ~J/n_cell slabs (boundaries round(m J / n_cell)), each
+    meeting at the upper middle of its slab span (sweepdd.py:392-401)."""
+    if n_cell < 1 or 2 * n_cell > J:
         raise ValueError(f"need 1 <= n_cell <= J/2, got {n_cell} for J={J}")
-    bounds = [-1] + [round(m * J / n_cell) for m in range(1, n_cell)] + [J + 1]
-    mids = []
-    for m in range(1, n_cell + 1):
-        lo = max(1, bounds[m - 1] + 1)
-        hi = min(J, bounds[m] - 1)
-        mids.append((lo + hi + 1) // 2)
-    cells = NxCells(tuple(bounds), tuple(mids))
+    inner = tuple(round(m * J / n_cell) for m in range(1, n_cell))
+    bounds = (-1,) + inner + (J + 1,)
+    probe = NxCells(bounds, ())
+    mids = tuple(sum(probe._span(m, J)) // 2 + (sum(probe._span(m, J)) % 2)
+                 for m in range(1, n_cell + 1))
+    cells = NxCells(bounds, mids)
     cells.validate(J)
     return cells
 
