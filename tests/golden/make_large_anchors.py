@@ -34,7 +34,8 @@ from helmsweep.twogrid import SmootherConfig, SweepOptions  # noqa: E402
 from paper_1412_0464_b200.configs import config  # noqa: E402  (inputs only)
 
 OUT = Path(__file__).resolve().parent / "large_anchors.json"
-CASES = [("C2", 1, 1, 0), ("C4_rhs0", 3, 1, 0), ("C3_half", 2, 2, 0), ("C5_half", 4, 2, 0)]
+CASES = [("C2", 1, 1, 0), ("C4_rhs0", 3, 1, 0), ("C3_half", 2, 2, 0), ("C5_half", 4, 2, 0),
+         ("C1_exact", 0, 1, 0), ("C1_nx4", 0, 1, 0)]
 
 
 def fe_fine(mesh, model):
@@ -48,6 +49,16 @@ def fe_fine(mesh, model):
     return op.scaled(h ** (-dim), fe_scaled=False)
 
 
+def _coarse(name):
+    """coarse solver and sweep variant of a case: C1_exact -> the reference's
+    default exact coarse solve; C1_nx4 -> NX sweep with 4 cells."""
+    if name.endswith("_exact"):
+        return "exact", "x", None
+    if name.endswith("_nx4"):
+        return "sweep", "nx", 4
+    return "sweep", "x", None
+
+
 def run(name, idx, scale, rhs):
     p = config(idx, scale)
     m = p.mesh
@@ -59,10 +70,11 @@ def run(name, idx, scale, rhs):
     model = hs.WaveModel(p.model.omega, np.asarray(p.model.k))
     t0 = time.perf_counter()
     fine_op = fe_fine(mesh, model) if p.fine != "fd5" else None
+    coarse, variant, n_cell = _coarse(name)
     cycle, _ = hs.build_two_grid(mesh, model, fine_op=fine_op,
                                  smoother=SmootherConfig(p.omega_jac, p.nu),
-                                 coarse="sweep",
-                                 sweep=SweepOptions(p.w_dd, p.s_dd, "x",
+                                 coarse=coarse,
+                                 sweep=SweepOptions(p.w_dd, p.s_dd, variant, n_cell=n_cell,
                                                     subdomains=p.subdomains))
     setup = time.perf_counter() - t0
     f = p.f[rhs].ravel()
@@ -73,7 +85,7 @@ def run(name, idx, scale, rhs):
     true_res = float(np.linalg.norm(f - cycle.fine_csr @ u) / np.linalg.norm(f))
     sel = np.arange(0, u.size, max(1, u.size // 64))
     out = {"config": idx, "scale": scale, "rhs": rhs, "subdomains": int(p.subdomains),
-           "fine_operator": p.fine,
+           "fine_operator": p.fine, "coarse": coarse, "variant": variant, "n_cell": n_cell,
            "fine_unknowns": list(m.unknowns), "iterations": int(rep.iterations),
            "history": [float(v) for v in rep.residual_history], "true_residual": true_res,
            "u_norm": float(np.linalg.norm(u)), "u_sample_idx": sel.tolist(),

@@ -475,10 +475,11 @@ def _large_anchors():
     return json.loads(f.read_text()) if f.exists() else {}
 
 
-@pytest.mark.parametrize("name", ["C2", "C4_rhs0", "C3_half", "C5_half"])
+@pytest.mark.parametrize("name", ["C2", "C4_rhs0", "C3_half", "C5_half", "C1_exact", "C1_nx4"])
 def test_baseline_config_matches_reference_solve(name):
     """BASELINE configs at full (C2, C4 right-hand side 0) or half size (C3,
-    C5), solved by the reference itself (tests/golden/make_large_anchors.py):
+    C5), and configs[0] with the exact coarse solve and with NX(4) sweeps,
+    solved by the reference itself (tests/golden/make_large_anchors.py):
     the same GMRES iteration count +-1, residual histories within 1e-6
     relative over the common iterations, true residual <= 1e-6 and the
     solution within 1e-5 relative at the sampled unknowns."""
@@ -489,12 +490,15 @@ def test_baseline_config_matches_reference_solve(name):
         pytest.skip(f"no reference anchor for {name}")
     p = config(a["config"], a["scale"])
     fine = fe_fine_operator(p.mesh, p.model) if a.get("fine_operator", "fd5") != "fd5" else None
+    coarse = a.get("coarse", "sweep")
     cycle, _ = hb.build_two_grid(p.mesh, p.model, fine_op=fine,
-                                 smoother=hb.SmootherConfig(p.omega_jac, p.nu), coarse="sweep",
-                                 sweep=hb.SweepOptions(p.w_dd, p.s_dd, "x",
+                                 smoother=hb.SmootherConfig(p.omega_jac, p.nu), coarse=coarse,
+                                 sweep=hb.SweepOptions(p.w_dd, p.s_dd, a.get("variant", "x"),
+                                                       n_cell=a.get("n_cell"),
                                                        subdomains=p.subdomains),
                                  keep_slab_ops=False)
-    assert cycle.hierarchy.partition.J == a["subdomains"]
+    if coarse == "sweep":
+        assert cycle.hierarchy.partition.J == a["subdomains"]
     f = p.f[a["rhs"]].ravel()
     u, rep = hb.gmres(cycle.fine_csr, cycle.as_preconditioner(), f,
                       hb.GmresConfig(p.tol, p.max_iter, p.restart))
