@@ -568,3 +568,15 @@ def test_exact_coarse_cycle_3d_vs_oracle(rng):
                      cycle.restrict_scale, "exact")
     z = crand(rng, mesh.unknowns)
     assert rel(cycle.vcycle(z), tg.vcycle(z)) < 1e-10
+
+
+def test_factorize_too_large_block_raises():
+    """Planes wider than the chain kernel supports (NB > 8 * SMs) fail with
+    ValueError (HS_E_SHAPE), not a wrong answer."""
+    import paper_1412_0464_b200 as hb
+    shape = (40, 3, 40)   # NB = 40 * 40 = 1600 rows per block
+    op = hb.StencilOperator(shape, {(0, 0, 0): np.full(shape, 4.0 + 0j),
+                                    (0, 1, 0): np.full(shape, -1.0 + 0j),
+                                    (0, -1, 0): np.full(shape, -1.0 + 0j)})
+    with pytest.raises(ValueError, match="too large"):
+        hb.factorize(op)
