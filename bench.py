@@ -133,7 +133,7 @@ class ClockSampler:
             self.out = tempfile.TemporaryFile(mode="w+")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", os.environ.get("HS_SMI_LMS", "200")],
                 stdout=self.out, stderr=subprocess.DEVNULL)
             # nvidia-smi's start-up and its first periodic query were measured
             # to stall this process's launches (20-55 ms, once): start timing
@@ -319,11 +319,14 @@ def run_ours(args):
         return hb.gmres(cycle.fine_csr, prec, fd, cfg, orth=args.orth,
                         pipelined=not args.no_pipeline)
 
-    # warm-up
+    # warm-up, holding each step's solutions like the timed loop does: the
+    # caching allocator then already owns the second solution buffer (a
+    # fresh cudaMalloc inside the 2nd timed step was measured to stall it)
     reports = []
+    held = None
     for _ in range(args.warmup):
-        for fd in f_dev:
-            solve(fd)
+        held = [solve(fd) for fd in f_dev]
+    held = None
     # ---- timed region: K steps (each step solves this rank's right-hand sides)
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
