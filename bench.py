@@ -341,9 +341,10 @@ def run_ours(args):
             return hb.solve_many(cycle, fs, cfg, lanes=args.lanes, orth=args.orth)
         return [solve(fd) for fd in fs]
 
-    if multi:
+    if multi:   # (lanes) same holding pattern as the timed loop
         for _ in range(args.warmup):
-            step(f_dev)
+            held = step(f_dev)
+        held = None
     with ClockSampler(local, args.clock_sampler) as clk:
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         ev0.record(stream)
