@@ -386,7 +386,7 @@ def run_ours(args):
     # (a fresh 18-MB cudaHostAlloc costs ~14 ms)
     for _ in range(2):
         if multi:
-            step(f_host)
+            outs = step(f_host)
         else:
             outs = [hb.gmres(cycle.fine_csr, prec, fh, cfg, orth=args.orth,
                              pipelined=not args.no_pipeline) for fh in f_host]
