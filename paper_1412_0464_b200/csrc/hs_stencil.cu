@@ -80,6 +80,79 @@ k_stencil(StencilDesc d, const double2* __restrict__ x, const double2* __restric
   }
 }
 
+// 3-D compact 27-point operators (2.5-D blocking): a block owns a TY x TX
+// tile of the (i1, i2) plane and marches over a run of i0 planes, keeping
+// three planes of the input (with a one-point ring) in shared memory, so each
+// x value is loaded once per run instead of 27 times per point; the 27
+// coefficient streams are read once.  Per point the arithmetic is
+// k_stencil's, in the same order (bitwise the same).
+constexpr int k3TX = 32, k3TY = 8, k3Run = 16;
+
+template <int MODE>
+__global__ void __launch_bounds__(256)
+k_stencil27(StencilDesc d, const double2* __restrict__ x, const double2* __restrict__ f,
+            double2* __restrict__ y, double omega) {
+  constexpr int W = k3TX + 2, H = k3TY + 2;
+  __shared__ double2 P[3][H * W];
+  const int n0 = (int)d.n0, n1 = (int)d.n1, n2 = (int)d.n2;
+  const int t1 = blockIdx.y * k3TY, t2 = blockIdx.x * k3TX;
+  const int p0 = blockIdx.z * k3Run, p1 = min(n0, p0 + k3Run);
+  const int tx = threadIdx.x % k3TX, ty = threadIdx.x / k3TX;
+  const int g1 = t1 + ty, g2 = t2 + tx;
+  const bool mine = g1 < n1 && g2 < n2;
+  const int64_t plane = (int64_t)n1 * n2;
+  // neighbour value at flat index j (x, or the first smoothing step from zero)
+  auto val = [&](int64_t j) {
+    if (MODE == kJacobi2Z) return cscale(omega, cmul(__ldg(f + j), __ldg(d.invd + j)));
+    return __ldg(x + j);
+  };
+  auto load_plane = [&](int i0, double2* dst) {
+    for (int k = threadIdx.x; k < H * W; k += 256) {
+      const int ly = k / W, lx = k - ly * W;
+      const int a = t1 + ly - 1, b = t2 + lx - 1;
+      double2 v = czero();
+      if (i0 >= 0 && i0 < n0 && (unsigned)a < (unsigned)n1 && (unsigned)b < (unsigned)n2)
+        v = val((int64_t)i0 * plane + (int64_t)a * n2 + b);
+      dst[k] = v;
+    }
+  };
+  load_plane(p0 - 1, P[0]);
+  load_plane(p0, P[1]);
+  for (int i0 = p0; i0 < p1; ++i0) {
+    const int cur = (i0 - p0 + 1) % 3, nxt = (i0 - p0 + 2) % 3, prv = (i0 - p0) % 3;
+    load_plane(i0 + 1, P[nxt]);
+    __syncthreads();
+    if (mine) {
+      const int64_t i = (int64_t)i0 * plane + (int64_t)g1 * n2 + g2;
+      double2 acc = czero();
+#pragma unroll
+      for (int s = 0; s < 27; ++s) {
+        const int o0 = d.off[s][0], o1 = d.off[s][1], o2 = d.off[s][2];
+        const bool ok = (unsigned)(i0 + o0) < (unsigned)n0 && (unsigned)(g1 + o1) < (unsigned)n1 &&
+                        (unsigned)(g2 + o2) < (unsigned)n2;
+        const double2 c = __ldg(d.coeffs + (int64_t)s * d.n + i);
+        if (ok) {
+          const double2* pl = P[o0 < 0 ? prv : o0 > 0 ? nxt : cur];
+          acc = cfma(c, pl[(ty + 1 + o1) * W + tx + 1 + o2], acc);
+        }
+      }
+      if (MODE == kApply) {
+        y[i] = acc;
+      } else if (MODE == kResidual) {
+        y[i] = csub(__ldg(f + i), acc);
+      } else {
+        const double2 fi = __ldg(f + i);
+        const double2 inv = __ldg(d.invd + i);
+        double2 ui;
+        if (MODE == kJacobi2Z) ui = cscale(omega, cmul(fi, inv));
+        else ui = __ldg(x + i);
+        y[i] = cadd(ui, cmul(cscale(omega, csub(fi, acc)), inv));
+      }
+    }
+    __syncthreads();   // plane `prv` is overwritten by the next iteration's load
+  }
+}
+
 // one wave of resident blocks of this kernel (grid-stride loop, no tail)
 template <int S, int MODE>
 int wave_of() {
@@ -105,6 +178,14 @@ int launch_mode(Ctx* c, const Stencil* op, const double2* x, const double2* f, d
                   : MODE == kJacobi ? K_JACOBI : K_JACOBI2Z;
   const double nb = (double)d.n * nrhs * 16.0;
   ProfScope ps(c, cls, nb * (d.S + ((MODE == kApply || MODE == kJacobi2Z) ? 2 : 3)));
+  static const bool flat27 = getenv("HS_STENCIL27_FLAT") != nullptr;   // A/B switch
+  if (d.S == 27 && d.n0 > 1 && nrhs == 1 && !flat27) {   // 3-D compact: 2.5-D blocking
+    dim3 grid((unsigned)((d.n2 + k3TX - 1) / k3TX), (unsigned)((d.n1 + k3TY - 1) / k3TY),
+              (unsigned)((d.n0 + k3Run - 1) / k3Run));
+    k_stencil27<MODE><<<grid, 256, 0, c->stream>>>(d, x, f, y, omega);
+    HS_LAUNCH_CHECK(c, "stencil kernel");
+    return HS_OK;
+  }
   switch (d.S) {
 #define HS_CASE(SS)                                                                    \
   case SS: {                                                                           \
