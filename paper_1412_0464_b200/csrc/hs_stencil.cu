@@ -87,9 +87,10 @@ k_stencil(StencilDesc d, const double2* __restrict__ x, const double2* __restric
 // coefficient streams are read once.  Per point the arithmetic is
 // k_stencil's, in the same order (bitwise the same).
 constexpr int k3TX = 32, k3TY = 8, k3Run = 16;
-
+// residency: the matvec keeps its 27 coefficient loads in flight with 2
+// blocks per SM; the smoother / residual modes run best at 3 (measured)
 template <int MODE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, MODE == kApply ? 2 : 3)
 k_stencil27(StencilDesc d, const double2* __restrict__ x, const double2* __restrict__ f,
             double2* __restrict__ y, double omega) {
   constexpr int W = k3TX + 2, H = k3TY + 2;
