@@ -1,21 +1,27 @@
 #!/usr/bin/env python
-"""Benchmark: TGSP-GMRES solve on BASELINE configs[1] (C2) on B200.
+"""Benchmark: TGSP-GMRES solve on BASELINE configs[2] (C3) on B200.
 
 A "step" = one full right-preconditioned GMRES(20) solve to 1e-6 with the
 two-grid sweeping preconditioner (the north_star hot path), inputs resident
-in HBM.  ``value`` = fine DOF/s summed over ranks (n_fine * solves / time,
-time = max over ranks of CUDA-event time).  ``e2e`` = the same metric
-through the public API with the right-hand side in host memory and the
-solution copied back (H2D + D2H inside the timed region).
+in HBM.  The default workload is C3 (4095^2 smooth random medium, 17.2 M
+fine DOF), the largest BASELINE config on one GPU.  ``value`` = fine DOF/s
+(n_fine * distinct solves / time, time = max over ranks of CUDA-event
+time).  ``e2e`` = the same metric through the public API with the
+right-hand side in host memory and the solution copied back (H2D + D2H
+inside the timed region).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 1] [--scale 1]
+                    [--config 2] [--scale 1]
 
 ``--impl reference`` times the CPU oracle port of the reference algorithm
-(oracle/, numpy + scipy SuperLU exactly like the reference) on a bounded
-sample of the same workload.  N>1: one process per GPU (torchrun); the
-path's sweep is a sequential chain, so ranks run independent replicas of the
-solve (weak scaling, no data-path collective) -- see DESIGN.md.
+(oracle/, numpy + scipy SuperLU exactly like the reference, 1 core) on the
+same config: each step is a bounded sample of whole GMRES iterations,
+projected to a full solve with the reference's own iteration count
+(tests/golden/large_anchors.json, made by running the reference).
+N>1 (torchrun, one process per GPU): a single-right-hand-side config is
+solved ONCE, sharded along the sweep axis (strong scaling, shards.py); a
+multi-right-hand-side config (C4) spreads its right-hand sides over the
+ranks (each solve counted once).  See DESIGN.md section 7.
 """
 
 from __future__ import annotations
@@ -44,10 +50,10 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", type=int, default=1, help="BASELINE configs index (0-based)")
+    p.add_argument("--config", type=int, default=2, help="BASELINE configs index (0-based)")
     p.add_argument("--scale", type=int, default=1, help="divide the grid size (debug)")
-    p.add_argument("--cpu-iters", type=int, default=3,
-                   help="GMRES iterations in the bounded CPU-oracle sample")
+    p.add_argument("--cpu-iters", type=int, default=1,
+                   help="GMRES iterations in each bounded CPU-oracle sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--orth", default="cgs2")
     p.add_argument("--shard", action="store_true",
@@ -72,9 +78,10 @@ def dist_info():
 
 
 def assign_rhs(nrhs: int, world: int, rank: int) -> list[int]:
-    """Right-hand sides solved by ``rank``: round-robin over ranks; with fewer
-    right-hand sides than ranks every rank solves a replica of one."""
-    return [r for r in range(nrhs) if r % world == rank] or [rank % nrhs]
+    """Right-hand sides solved by ``rank``: round-robin over ranks.  A rank
+    left without one gets none (no replicas: every solve counted is a
+    distinct right-hand side; single-RHS configs shard instead, --shard)."""
+    return [r for r in range(nrhs) if r % world == rank]
 
 
 def reduce_over_ranks(x: float, world: int, op: str = "max", device=None) -> float:
@@ -219,6 +226,34 @@ def fine_operator(p):
     return fe_fine_operator(p.mesh, p.model)
 
 
+def reference_iterations(p, args):
+    """GMRES iterations of the REFERENCE solver on this config (committed
+    anchors, tests/golden/large_anchors.json), or None."""
+    if args.scale != 1:
+        return None
+    f = ROOT / "tests" / "golden" / "large_anchors.json"
+    try:
+        d = json.loads(f.read_text())
+    except Exception:
+        return None
+    key = {0: "C1_x", 1: "C2", 2: "C3", 3: "C4_rhs0", 4: "C5"}.get(args.config)
+    a = d.get(key)
+    return None if a is None else int(a["iterations"])
+
+
+def bench_config(p, args, world):
+    """The ``config`` object of both arms (identical keys and values)."""
+    nrhs = int(p.f.shape[0])
+    if world > 1:
+        par = f"rhs across {world} ranks" if nrhs > 1 else f"sweep-axis shards x{world}"
+    else:
+        par = "single GPU" + (f", {nrhs} rhs" if nrhs > 1 else "")
+    return {"workload": workload_name(p), "fine_dof": p.n_fine, "rhs": nrhs,
+            "subdomains": int(p.subdomains), "parallelism": par,
+            "l2": "working set > L2 (slab factors + GMRES basis + operators stream every "
+                  "step); no flush"}
+
+
 def workload_name(p):
     op = {"fd5": "5-point fine op (SURVEY F2 ii)", "fe9": "9-point compact fine op",
           "fe27": "27-point compact fine op"}[p.fine]
@@ -227,15 +262,23 @@ def workload_name(p):
 
 
 # ---------------------------------------------------------------------------
-def cpu_sample(problem, hh, its_target, iters):
-    """Bounded sample of the CPU oracle (reference algorithm, SuperLU slabs):
-    ``iters`` GMRES iterations on the same problem, extrapolated by
-    per-iteration time to the full solve of ``its_target`` iterations."""
+def cpu_oracle(hh):
+    """The CPU oracle (numpy/scipy restatement of the reference, SuperLU slab
+    factorisations) built from the host hierarchy; setup is not timed."""
     from oracle import tgsp_oracle as orc
     t0 = time.perf_counter()
     tg = orc.from_hierarchy(hh)
     tg.fine.csr, tg.part.op.csr        # assemble the CSR matrices outside the sample
-    setup = time.perf_counter() - t0
+    return tg, time.perf_counter() - t0
+
+
+def cpu_sample(problem, tg, its_target, iters):
+    """Bounded sample of the CPU oracle (reference algorithm, 1 core):
+    ``iters`` whole GMRES(restart) iterations on the config's right-hand
+    side (each = one A M v + orthogonalisation) plus the solve's closing
+    M dv and residual, timed, then projected per iteration to a solve of
+    ``its_target`` iterations (the reference's own count)."""
+    from oracle import tgsp_oracle as orc
     f = problem.f[0].ravel()
     t0 = time.perf_counter()
     _, its, _, _, _ = orc.gmres(lambda v: tg.fine.csr @ v, tg.as_preconditioner(), f,
@@ -244,8 +287,15 @@ def cpu_sample(problem, hh, its_target, iters):
     per_it = dt / (its + 1)           # its x (A M v + orth) + final (M dv, f - A u)
     projected = per_it * (its_target + 1)
     return {"value": problem.n_fine / projected, "projected_solve_s": projected,
-            "per_iteration_s": per_it, "sample_s": dt, "oracle_setup_s": setup,
-            "sample_iterations": its}
+            "per_iteration_s": per_it, "sample_s": dt, "sample_iterations": its}
+
+
+def _sample_text(r, its_target, source, setup_s):
+    return (f"{r['sample_iterations']} GMRES iteration(s) + the closing M dv / residual of the "
+            f"numpy/scipy oracle port (SuperLU slab solves like the reference) timed in "
+            f"{r['sample_s']:.1f} s, projected per iteration to a {its_target}-iteration solve "
+            f"({source}); oracle setup {setup_s:.0f} s untimed; 1 core used, host has "
+            f"{os.cpu_count()}")
 
 
 def run_reference(args):
@@ -258,26 +308,30 @@ def run_reference(args):
     hh = hb.build_hierarchy(p.mesh, p.model, fine_operator(p), hb.SmootherConfig(p.omega_jac, p.nu),
                             hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains),
                             device=False)
-    its_target = {0: 9, 1: 48}.get(args.config, 50) if args.scale == 1 else 30
+    its_ref = reference_iterations(p, args)
+    its_target = its_ref if its_ref is not None else 50
+    source = ("reference iteration count from tests/golden/large_anchors.json"
+              if its_ref is not None else "no reference anchor: 50 iterations assumed")
+    tg, setup_s = cpu_oracle(hh)
     vals = []
-    for s in range(args.warmup + args.steps):
-        r = cpu_sample(p, hh, its_target, args.cpu_iters)
-        if s >= args.warmup:
+    for s_ in range(args.warmup + args.steps):
+        r = cpu_sample(p, tg, its_target, args.cpu_iters)
+        if s_ >= args.warmup:
             vals.append(r)
     value = float(np.median([r["value"] for r in vals]))
     ms = float(np.median([r["projected_solve_s"] for r in vals])) * 1e3
-    cores = 1
+    med = sorted(vals, key=lambda r: r["value"])[len(vals) // 2]
     line = {
         "impl": "reference", "metric": "TGSP-GMRES fine DOF/s (solve to 1e-6 rel-res)",
         "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": workload_name(p), "fine_dof": p.n_fine},
-        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.cpu_iters} GMRES iterations of the numpy/scipy "
-                                   f"oracle (SuperLU slab solves, as the reference) "
-                                   f"extrapolated per iteration to a {its_target}-iteration "
-                                   f"solve; host has {os.cpu_count()} cores, 1 used"},
+        "scaling": "strong" if world > 1 and p.f.shape[0] == 1 else "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": bench_config(p, args, world),
+        "projection": True,
+        "reference_iterations": its_target,
+        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": 1, "kind": "port",
+                         "sample": _sample_text(med, its_target, source, setup_s)},
         "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -368,16 +422,18 @@ def run_ours(args):
     for _ in range(args.steps):
         for fd in f_dev:
             solve(fd)
-    prof = ctx.profile_read()
+    prof = ctx.profile_read() or {"none": {"ms": 0.0, "bytes": 0.0, "launches": 0}}
     ctx.profile(False)
     ms = reduce_over_ranks(ms_local, world, "max")
     solves = reduce_over_ranks(args.steps * len(f_dev), world, "sum")
     value = job_value(p.n_fine, solves, ms)
-    its = [r.iterations for r in reports]
+    its = [r.iterations for r in reports] or [0]
     # true residual of the last solve
-    u_h = u.cpu().numpy()
-    f0 = p.f[mine[-1]].ravel()
-    true_res = float(np.linalg.norm(f0 - cycle.fine_csr @ u_h) / np.linalg.norm(f0))
+    true_res = None
+    if f_dev:
+        u_h = u.cpu().numpy()
+        f0 = p.f[mine[-1]].ravel()
+        true_res = float(np.linalg.norm(f0 - cycle.fine_csr @ u_h) / np.linalg.norm(f0))
 
     # ---- e2e: public API with host buffers (H2D + D2H inside the timed region)
     f_host = [torch.from_numpy(p.f[r].ravel()).pin_memory().numpy() for r in mine]
@@ -436,8 +492,9 @@ def run_ours(args):
                 "bytes_per_launch": by / n, "ms_per_launch": ms_ / n, "launches": n}
 
     roofline = roof([dom])
-    roofline["kernel"] = dom
-    roofline["traffic"] = traffic
+    if roofline is not None:
+        roofline["kernel"] = dom
+        roofline["traffic"] = traffic
     stencil_roof = roof(["stencil", "residual", "jacobi", "jacobi2z"])
     fused_roof = roof(["pre_fused", "post_fused"])
     shares = {k: {"share": v["ms"] / total_ms, "ms": v["ms"], "launches": v["launches"],
@@ -446,16 +503,26 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = cpu_sample(p, cycle.hierarchy, int(np.median(its)), args.cpu_iters)
+        its_ref = reference_iterations(p, args)
+        its_t = its_ref if its_ref is not None else int(np.median(its))
+        src = ("reference iteration count from tests/golden/large_anchors.json"
+               if its_ref is not None else "this solve's iteration count")
+        tg, osetup = cpu_oracle(cycle.hierarchy)
+        r = cpu_sample(p, tg, its_t, args.cpu_iters)
+        tg = None
         cpu = {"value": r["value"], "unit": "DOF/s", "cores": 1, "kind": "port",
-               "sample": f"{r['sample_iterations']} GMRES iterations of the numpy/scipy oracle "
-                         f"(SuperLU slab solves like the reference) in {r['sample_s']:.1f} s, "
-                         f"extrapolated per iteration to the {int(np.median(its))}-iteration "
-                         f"solve; host has {os.cpu_count()} cores, 1 used",
+               "sample": _sample_text(r, its_t, src, osetup),
                "projected_solve_s": r["projected_solve_s"]}
 
     if rank == 0:
-        fac_gb = dev.sweep.factor_bytes / 1e9
+        fac = dev.sweep.factor_bytes
+        if roofline and roofline.get("kernel") == "sweep_front":
+            # bytes_per_launch above = SURVEY 8(d)'s banded-LU floor of the
+            # launch's slab solves; the own factor format streams factor_bytes
+            # per pass (each slab solved twice per X application)
+            roofline["bytes_basis"] = "SURVEY 8(d) banded no-pivot LU floor of the slabs solved"
+            roofline["own_format_bytes_per_application"] = 2 * fac
+            roofline["launches_per_application"] = dev.sweep.launches_per_apply()
         line = {
             "metric": "TGSP-GMRES fine DOF/s (solve to 1e-6 rel-res)",
             "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
@@ -463,14 +530,13 @@ def run_ours(args):
             "ms_steps_rank0": ms_steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "c128", "data": "synthetic",
-            "config": {"workload": workload_name(p), "fine_dof": p.n_fine,
-                       "coarse_dof": int(np.prod(cycle.coarse_op.shape)),
-                       "subdomains": p.subdomains, "rhs_per_rank": len(f_dev),
-                       "rhs_in_flight": min(args.lanes, len(f_dev)) if multi else 1,
-                       "parallelism": "replicas" if world > 1 else "single",
-                       "l2": f"working set > L2 (slab factors {fac_gb:.2f} GB + basis + operators "
-                             f"stream every step); no flush"},
-            "solve_s": ms / 1e3 / (args.steps * len(f_dev)),
+            "config": bench_config(p, args, world),
+            "coarse_dof": int(np.prod(cycle.coarse_op.shape)),
+            "slab_factor_bytes": fac,
+            "rhs_per_rank": len(f_dev),
+            "rhs_in_flight": min(args.lanes, len(f_dev)) if multi else 1,
+            "reference_iterations": reference_iterations(p, args),
+            "solve_s": ms / 1e3 / max(1, args.steps * len(f_dev)),
             "setup_s": setup_s,
             "iterations": int(np.median(its)),
             "true_residual": true_res,
@@ -551,10 +617,8 @@ def run_sharded(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "c128", "data": "synthetic",
-            "config": {"workload": workload_name(p), "fine_dof": p.n_fine,
-                       "parallelism": f"sweep-axis shards x{G}"
-                                      + (" (logical, one GPU)" if world == 1 else ""),
-                       "l2": "working set > L2; no flush"},
+            "config": bench_config(p, args, world),
+            "shards": G, "logical_shards_on_one_gpu": world == 1,
             "iterations": int(np.median([r.iterations for r in reps])),
             "true_residual": true_res, "setup_s": setup_s, "gpu_launches": launches,
             "clocks": clk.summary(),
@@ -566,6 +630,11 @@ def run_sharded(args):
 
 def main():
     args = parse()
+    world = dist_info()[0]
+    if not args.shard and world > 1 and args.impl == "ours":
+        from paper_1412_0464_b200.configs import config
+        # one right-hand side: no replicas -- the solve itself is sharded
+        args.shard = config(args.config, args.scale).f.shape[0] == 1
     if args.impl == "reference":
         run_reference(args)
     elif args.shard:

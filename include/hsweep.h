@@ -187,6 +187,13 @@ int hs_sweep_solve_one(hs_ctx* ctx, hs_sweep* s, int j, int64_t a, int64_t b, in
 int hs_exact_create(hs_ctx* ctx, const hs_stencil* op, hs_sweep** out);
 /* bytes of device memory held by the slab factors (diagnostic) */
 long long hs_sweep_factor_bytes(hs_sweep* s);
+/* slab-solve launches in one application of a variant's plan (diagnostic:
+ * the profiler's sweep_front launches per prec_x / prec_ud / prec_nx) */
+int hs_sweep_plan_launches(hs_sweep* s, int variant);
+/* 2-D slab-solve layout (diagnostic): face segments per front (clusters of
+ * the two-level partition, 1 = one cluster) and chunks (CTAs) per segment */
+int hs_sweep_segments(hs_sweep* s);
+int hs_sweep_chunks(hs_sweep* s);
 
 /* ---- two-grid cycle ------------------------------------------------------
  * TwoGridCycle(fine, P, smoother, SweepCoarseSolver)   twogrid.py:119-164, 196-229 */

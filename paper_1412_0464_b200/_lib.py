@@ -65,6 +65,9 @@ SIGNATURES = {
     "hs_sweep_destroy": (C.c_int, [_vp, _vp]),
     "hs_sweep_apply": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp]),
     "hs_sweep_factor_bytes": (C.c_longlong, [_vp]),
+    "hs_sweep_plan_launches": (C.c_int, [_vp, C.c_int]),
+    "hs_sweep_segments": (C.c_int, [_vp]),
+    "hs_sweep_chunks": (C.c_int, [_vp]),
     "hs_sweep_solve_one": (C.c_int, [_vp, _vp, C.c_int, C.c_int64, C.c_int64, C.c_int64,
                                      C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hs_exact_create": (C.c_int, [_vp, _vp, C.POINTER(_vp)]),

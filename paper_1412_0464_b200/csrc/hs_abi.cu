@@ -458,6 +458,16 @@ int hs_sweep_plan_nx(hs_ctx* c, hs_sweep* s, int ncell, const int64_t* j_cell,
 
 long long hs_sweep_factor_bytes(hs_sweep* s) { return s ? s->factor_bytes : 0; }
 
+int hs_sweep_segments(hs_sweep* s) { return s && !s->s3 ? s->G : 1; }
+int hs_sweep_chunks(hs_sweep* s) { return s && !s->s3 ? s->C : 0; }
+
+int hs_sweep_plan_launches(hs_sweep* s, int variant) {
+  if (!s || !s->has_plan(variant)) return 0;
+  int n = 0;
+  for (const auto& fl : s->plan[variant]) n += fl.kind == SweepLaunch::kSolve;
+  return n;
+}
+
 // ---------------------------------------------------------------------------
 int hs_cycle_create(hs_ctx* c, const hs_stencil* fine, const hs_transfer* t,
                     const hs_stencil* coarse, hs_sweep* sweep, double omega_jac, int nu,

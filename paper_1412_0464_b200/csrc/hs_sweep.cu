@@ -78,7 +78,9 @@ constexpr int kNA = 8;             // consumer warps of the back substitution wh
 #ifndef HS_SWEEP_G16       // tm 16: blocks per ring chunk (bulk copy)
 #define HS_SWEEP_G16 4
 #endif
-constexpr int kMaxC = 16;
+constexpr int kMaxC = 16;         // chunks (CTAs) per cluster
+constexpr int kMaxG = 8;          // face segments (clusters) per front
+constexpr int kMaxCh = 64;        // chunks over the whole face
 constexpr int kNR = 8;             // rows of a restricted (last-level / spike) update
 constexpr int kMaxTasks = 1024;    // slab solves per front per launch
 
@@ -101,14 +103,20 @@ struct SlabInfo {
   int slot[3][3];          // (o0+1, o1+1) -> coefficient slot or -1
 };
 
-// chunk geometry: chunk k covers face points [k M / C, (k+1) M / C)
+// chunk geometry: the face is cut into G segments of C chunks each (chunk
+// K = seg * C + rank covers face points [y0s[K], y0s[K+1])); one cluster of
+// C CTAs solves one segment, the G clusters of a front couple through a
+// second-level interface system (two-level SPIKE, see k_level2).
 struct Chunks {
   int M, C, L, kstride;
+  int G;                   // segments (clusters) per front
   int q;                   // dense top: blocks per chunk left after L levels
   int nr;                  // restricted level-0 / spike updates (kNR rows) or 0
   int koff[kMaxLevels];
-  int y0s[kMaxC + 1];      // chunk k covers face points [y0s[k], y0s[k+1])
+  int y0s[kMaxCh + 1];     // chunk K covers face points [y0s[K], y0s[K+1])
   int mmax;                // longest chunk
+  __host__ __device__ int nch() const { return C * G; }
+  __host__ __device__ int xstride() const { return G > 1 ? 1 + 4 * (G - 1) + 4 : 0; }
   __host__ __device__ int y0(int k) const { return y0s[k]; }
   __host__ __device__ int len(int k) const { return y0s[k + 1] - y0s[k]; }
   __host__ __device__ int chunk_of(int y) const {
@@ -148,11 +156,11 @@ k_bcr_init(const SlabInfo* __restrict__ slabs, Chunks g, double2* __restrict__ D
   double2 l = coef(c - r, -1), u = coef(c - r, 1);
   const int k = g.chunk_of(y);
   if (y == g.y0(k)) {
-    EL[((int64_t)s * g.C + k) * TM2 + r * TM + c] = l;
+    EL[((int64_t)s * g.nch() + k) * TM2 + r * TM + c] = l;
     l = czero();
   }
   if (y == g.y0(k + 1) - 1) {
-    EU[((int64_t)s * g.C + k) * TM2 + r * TM + c] = u;
+    EU[((int64_t)s * g.nch() + k) * TM2 + r * TM + c] = u;
     u = czero();
   }
   Lc[off] = l;
@@ -254,7 +262,7 @@ k_bcr_elim(int level, Chunks g, int top, double2* __restrict__ D,
            unsigned long long* __restrict__ err) {
   constexpr int TM2 = Geo<TM>::TM2;
   const int s_ = 1 << level;
-  const int slab = blockIdx.y / g.C, k = blockIdx.y % g.C;
+  const int slab = blockIdx.y / g.nch(), k = blockIdx.y % g.nch();
   const int yl = top ? 0 : (2 * blockIdx.x + 1) * s_;
   if (yl >= g.len(k)) return;
   const int y = g.y0(k) + yl, M = g.M;
@@ -291,7 +299,7 @@ k_bcr_keep(int level, Chunks g, double2* __restrict__ D, double2* __restrict__ L
            double2* __restrict__ Uc, double2* __restrict__ kr) {
   constexpr int TM2 = Geo<TM>::TM2;
   const int s_ = 1 << level;
-  const int slab = blockIdx.y / g.C, k = blockIdx.y % g.C;
+  const int slab = blockIdx.y / g.nch(), k = blockIdx.y % g.nch();
   const int j = blockIdx.x;
   const int yl = j * 2 * s_, m = g.len(k);
   if (yl >= m) return;
@@ -305,7 +313,7 @@ k_bcr_keep(int level, Chunks g, double2* __restrict__ D, double2* __restrict__ L
   double2(*Ga)[TM + 1] = Al + TM;
   const int r = threadIdx.x / TM, c = threadIdx.x % TM;
   auto at = [&](int yy) { return ((int64_t)slab * M + yy) * TM2; };
-  double2* kout = kr + (((int64_t)slab * g.C + k) * g.kstride + g.koff[level] + j) * 2 * TM2;
+  double2* kout = kr + (((int64_t)slab * g.nch() + k) * g.kstride + g.koff[level] + j) * 2 * TM2;
   Al[r][c] = czero();
   Ga[r][c] = czero();
   if (hl) {
@@ -364,7 +372,7 @@ k_dense_top(Chunks g, const double2* __restrict__ D, const double2* __restrict__
             unsigned long long* __restrict__ err) {
   constexpr int TM2 = Geo<TM>::TM2;
   constexpr int N = Q * TM;
-  const int slab = blockIdx.x / g.C, k = blockIdx.x % g.C, M = g.M;
+  const int slab = blockIdx.x / g.nch(), k = blockIdx.x % g.nch(), M = g.M;
   const int S = 1 << g.L, Y0 = g.y0(k);
   const int qk = (g.len(k) - 1) / S + 1;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -386,7 +394,7 @@ k_dense_top(Chunks g, const double2* __restrict__ D, const double2* __restrict__
   const unsigned long long code =
       ((unsigned long long)slab << 40) | ((unsigned long long)Y0 * TM & 0xffffffffffull);
   gj_invert<N, 1024>(A, Inv, &piv_row, &piv_abs, err, code);
-  double2* out = qd + ((int64_t)slab * g.C + k) * Q * Q * TM2;
+  double2* out = qd + ((int64_t)slab * g.nch() + k) * Q * Q * TM2;
   for (int e = threadIdx.x; e < N * N; e += blockDim.x) {
     const int R = e / N, Cc = e % N;
     out[((R / TM) * Q + Cc / TM) * TM2 + lm<TM>(R % TM, Cc % TM)] = Inv[R][Cc];
@@ -406,7 +414,7 @@ k_spikes(Chunks g, const double2* __restrict__ D, const double2* __restrict__ Lc
          double2* __restrict__ sp, double2* __restrict__ tips,
          unsigned long long* __restrict__ err) {
   constexpr int TM2 = Geo<TM>::TM2;
-  const int slab = blockIdx.x / g.C, k = blockIdx.x % g.C, M = g.M;
+  const int slab = blockIdx.x / g.nch(), k = blockIdx.x % g.nch(), M = g.M;
   const int Y0 = g.y0(k), Y1 = g.y0(k + 1);
   extern __shared__ __align__(16) unsigned char smraw[];
   double2(*A)[TM + 1] = reinterpret_cast<double2(*)[TM + 1]>(smraw);
@@ -420,9 +428,9 @@ k_spikes(Chunks g, const double2* __restrict__ D, const double2* __restrict__ Lc
   __shared__ double piv_abs;
   const int r = threadIdx.x / TM, c = threadIdx.x % TM;
   auto at = [&](int yy) { return ((int64_t)slab * M + yy) * TM2; };
-  const double2* el = EL + ((int64_t)slab * g.C + k) * TM2;
-  const double2* eu = EU + ((int64_t)slab * g.C + k) * TM2;
-  double2* tp = tips + ((int64_t)slab * g.C + k) * 4 * TM2;
+  const double2* el = EL + ((int64_t)slab * g.nch() + k) * TM2;
+  const double2* eu = EU + ((int64_t)slab * g.nch() + k) * TM2;
+  double2* tp = tips + ((int64_t)slab * g.nch() + k) * 4 * TM2;
   Hp[r][c] = czero();
   Zp[r][c] = czero();
   double2 zv_last = czero();
@@ -489,35 +497,37 @@ k_spikes(Chunks g, const double2* __restrict__ D, const double2* __restrict__ Lc
   }
 }
 
-// Inverse of the interface system (one CTA per slab).  Unknowns per boundary
-// b (between chunks b and b+1): xi_b = (alpha_b = x at the last point of chunk
-// b, beta_b = x at the first point of chunk b+1); right-hand side
-// tau_b = (g_b[last], g_{b+1}[first]):
+// Inverse of an interface system (one CTA per slab x group of C chunks: the
+// segment's chunks at level 1, the G segments of the face at level 2).
+// Unknowns per boundary b (between chunks b and b+1 of the group): xi_b =
+// (alpha_b = x at the last point of chunk b, beta_b = x at the first point of
+// chunk b+1); right-hand side tau_b = (g_b[last], g_{b+1}[first]):
 //   alpha_b + Vb[last] beta_b + Wb[last] alpha_{b-1}            = g_b[last]
 //   beta_b + W_{b+1}[first] alpha_b + V_{b+1}[first] beta_{b+1} = g_{b+1}[first]
-// Block Thomas over b with identity right-hand sides gives R = S^{-1}; CTA k
+// Block Thomas over b with identity right-hand sides gives R = S^{-1}; chunk k
 // keeps rows alpha_{k-1} and beta_k, stored per column block q (tm columns) as
-// 2tm x tm with the row index fastest.
+// 2tm x tm with the row index fastest.  tips: [slab][ngrp * C][4][tm^2],
+// rk: [slab][ngrp * C][2(C-1)][2 tm^2].
 template <int TM>
 __global__ void __launch_bounds__(1024)
-k_reduced(Chunks g, const double2* __restrict__ tips, double2* __restrict__ Gw,
+k_reduced(int C, int ngrp, const double2* __restrict__ tips, double2* __restrict__ Gw,
           double2* __restrict__ Zr, double2* __restrict__ rk,
           unsigned long long* __restrict__ err) {
   constexpr int TM2 = Geo<TM>::TM2;
   constexpr int N = 2 * TM;
-  const int slab = blockIdx.x, C = g.C, B = C - 1, NR = B * N;
+  const int grp = blockIdx.x, slab = grp / ngrp, B = C - 1, NR = B * N;
   extern __shared__ __align__(16) unsigned char smraw[];
   double2(*A)[N + 1] = reinterpret_cast<double2(*)[N + 1]>(smraw);
   double2(*Inv)[N + 1] = A + N;
   __shared__ int piv_row;
   __shared__ double piv_abs;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const double2* tp = tips + (int64_t)slab * C * 4 * TM2;
+  const double2* tp = tips + (int64_t)grp * C * 4 * TM2;
   auto tip = [&](int k, int which, int r, int c) -> double2 {   // 0 Wf 1 Wl 2 Vf 3 Vl
     return tp[((int64_t)k * 4 + which) * TM2 + r * TM + c];
   };
-  double2* G = Gw + (int64_t)slab * B * N * N;    // G_b = Dt_b^{-1} Up_b
-  double2* Z = Zr + (int64_t)slab * NR * NR;      // block row b: rows b*N.., all NR columns
+  double2* G = Gw + (int64_t)grp * B * N * N;    // G_b = Dt_b^{-1} Up_b
+  double2* Z = Zr + (int64_t)grp * NR * NR;      // block row b: rows b*N.., all NR columns
   for (int b = 0; b < B; ++b) {
     // D~_b = D_b - Lo_b G_{b-1};  D_b = [[I, V_b[l]], [W_{b+1}[f], I]]; Lo_b = [[W_b[l], 0],[0,0]]
     for (int e = tid; e < N * N; e += nt) {
@@ -568,7 +578,7 @@ k_reduced(Chunks g, const double2* __restrict__ tips, double2* __restrict__ Gw,
     }
     __syncthreads();
   }
-  // rows of CTA k: alpha_{k-1} (block k-1, rows 0..TM-1), beta_k (block k,
+  // rows of chunk k: alpha_{k-1} (block k-1, rows 0..TM-1), beta_k (block k,
   // rows TM..2TM-1); column block q of tm columns
   for (int e = tid; e < C * N * NR; e += nt) {
     const int k = e / (N * NR), rem = e % (N * NR);
@@ -577,7 +587,113 @@ k_reduced(Chunks g, const double2* __restrict__ tips, double2* __restrict__ Gw,
     if (r < TM && k > 0) v = Z[((int64_t)(k - 1) * N + r) * NR + col];
     if (r >= TM && k < B) v = Z[((int64_t)k * N + r) * NR + col];
     const int q = col / TM, cq = col % TM;
-    rk[(((int64_t)slab * C + k) * (2 * B) + q) * (2 * TM2) + cq * N + r] = v;
+    rk[(((int64_t)grp * C + k) * (2 * B) + q) * (2 * TM2) + cq * N + r] = v;
+  }
+}
+
+// Second level of the two-level partition (one CTA of tm x tm threads per
+// slab x segment, C >= 2 chunks per segment).  With P_s = x at the last
+// point of segment s-1 and Q_s = x at the first point of segment s+1 the
+// segment's level-1 unknowns are affine in them:
+//   (alpha_{k-1}, beta_k) = R_k tau - Pk P_s - Qk Q_s,
+//   Pk = R_k[:, alpha_0] W_{K0}[last],  Qk = R_k[:, beta_{C-2}] V_{KL}[first]
+// (K0 / KL the segment's first / last chunk), and its end values are
+//   x_last  = c_s + E_s P_s + F_s Q_s,   c_s = g_KL[last] - W_KL[last] (R tau)_alpha
+//   x_first = d_s + E'_s P_s + F'_s Q_s, d_s = g_K0[first] - V_K0[first] (R tau)_beta
+// which is the chunk-level relation x = g - W alpha - V beta one level up, with
+// segment "tips" Wf = -E', Wl = -E, Vf = -F', Vl = -F: k_reduced on them
+// gives every segment its rows (P_s, Q_s) of the G-segment interface inverse.
+// Writes tips2 [slab][G][4][tm^2] (natural layout) and, per chunk K, the
+// level-2 stream blocks x2[slab][K][xstride][tm^2]: block 0 the c / d tip
+// (W_KL[last] for the last chunk, V_K0[first] for the first, lane-major),
+// blocks 1 + 4(G-1) .. the column blocks of [Pk | Qk] (2tm x tm, row index
+// fastest, like R).  Blocks 1 .. 4(G-1) (the level-2 inverse rows of the
+// segment's first chunk) are copied in after k_reduced of level 2.
+template <int TM>
+__global__ void __launch_bounds__(TM * TM)
+k_level2(Chunks g, const double2* __restrict__ tips, const double2* __restrict__ rk,
+         double2* __restrict__ tips2, double2* __restrict__ x2) {
+  constexpr int TM2 = Geo<TM>::TM2;
+  constexpr int N = 2 * TM;
+  const int C = g.C, G = g.G, B = C - 1, nch = g.nch(), xs = g.xstride();
+  const int slab = blockIdx.x / G, seg = blockIdx.x % G;
+  const int K0 = seg * C, KL = K0 + C - 1;
+  const int r = threadIdx.x / TM, c = threadIdx.x % TM;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double2(*S0)[TM + 1] = reinterpret_cast<double2(*)[TM + 1]>(smraw);
+  double2(*S1)[TM + 1] = S0 + TM;
+  double2(*S2)[TM + 1] = S1 + TM;
+  double2(*S3)[TM + 1] = S2 + TM;
+  auto tip = [&](int K, int which) {   // 0 Wf 1 Wl 2 Vf 3 Vl, natural layout
+    return tips + (((int64_t)slab * nch + K) * 4 + which) * TM2;
+  };
+  // R column block q of chunk K, element (row rr of 2tm, column cq)
+  auto R = [&](int K, int q, int rr, int cq) {
+    return rk[(((int64_t)slab * nch + K) * (2 * B) + q) * (2 * TM2) + cq * N + rr];
+  };
+  auto mm = [&](double2 (*A)[TM + 1], double2 (*Bm)[TM + 1]) {
+    double2 acc = czero();
+    for (int k = 0; k < TM; ++k) acc = cfma(A[r][k], Bm[k][c], acc);
+    return acc;
+  };
+  const double2 wl0 = tip(K0, 1)[r * TM + c], vfL = tip(KL, 2)[r * TM + c];
+  // (P_{C-1})_alpha = R_KL[alpha rows, col 0] W_K0[last]; E = W_KL[last] (P_{C-1})_alpha
+  S0[r][c] = R(KL, 0, r, c);
+  S1[r][c] = wl0;
+  __syncthreads();
+  S2[r][c] = mm(S0, S1);
+  S3[r][c] = tip(KL, 1)[r * TM + c];
+  __syncthreads();
+  const double2 E = mm(S3, S2);
+  __syncthreads();
+  // (Q_{C-1})_alpha = R_KL[alpha rows, col 2B-1] V_KL[first]; F = W_KL[last] (.) - V_KL[last]
+  S0[r][c] = R(KL, 2 * B - 1, r, c);
+  S1[r][c] = vfL;
+  __syncthreads();
+  S2[r][c] = mm(S0, S1);
+  __syncthreads();
+  const double2 F = csub(mm(S3, S2), tip(KL, 3)[r * TM + c]);
+  __syncthreads();
+  // (P_0)_beta = R_K0[beta rows, col 0] W_K0[last]; E' = V_K0[first] (.) - W_K0[first]
+  S0[r][c] = R(K0, 0, TM + r, c);
+  S1[r][c] = wl0;
+  S3[r][c] = tip(K0, 2)[r * TM + c];
+  __syncthreads();
+  S2[r][c] = mm(S0, S1);
+  __syncthreads();
+  const double2 Ep = csub(mm(S3, S2), tip(K0, 0)[r * TM + c]);
+  __syncthreads();
+  // (Q_0)_beta = R_K0[beta rows, col 2B-1] V_KL[first]; F' = V_K0[first] (.)
+  S0[r][c] = R(K0, 2 * B - 1, TM + r, c);
+  S1[r][c] = vfL;
+  __syncthreads();
+  S2[r][c] = mm(S0, S1);
+  __syncthreads();
+  const double2 Fp = mm(S3, S2);
+  double2* t2 = tips2 + ((int64_t)slab * G + seg) * 4 * TM2;
+  t2[0 * TM2 + r * TM + c] = cscale(-1.0, Ep);
+  t2[1 * TM2 + r * TM + c] = cscale(-1.0, E);
+  t2[2 * TM2 + r * TM + c] = cscale(-1.0, Fp);
+  t2[3 * TM2 + r * TM + c] = cscale(-1.0, F);
+  // per chunk: the c / d tip block and [Pk | Qk]
+  for (int k = 0; k < C; ++k) {
+    const int K = K0 + k;
+    double2* xb = x2 + ((int64_t)slab * nch + K) * xs * TM2;
+    double2 tv = czero();
+    if (k == C - 1 && seg < G - 1) tv = tip(KL, 1)[r * TM + c];   // c_s: W_KL[last]
+    if (k == 0 && seg > 0) tv = tip(K0, 2)[r * TM + c];           // d_s: V_K0[first]
+    xb[lm<TM>(r, c)] = tv;
+    double2* pq = xb + (int64_t)(1 + 4 * (G - 1)) * TM2;
+    for (int h = 0; h < 2; ++h) {       // rows h*TM + r of the 2tm x tm column blocks
+      const int rr = h * TM + r;
+      double2 pa = czero(), qa = czero();
+      for (int q = 0; q < TM; ++q) {
+        pa = cfma(R(K, 0, rr, q), tip(K0, 1)[q * TM + c], pa);
+        qa = cfma(R(K, 2 * B - 1, rr, q), tip(KL, 2)[q * TM + c], qa);
+      }
+      pq[c * N + rr] = pa;
+      pq[2 * TM2 + c * N + rr] = qa;
+    }
   }
 }
 
@@ -600,6 +716,13 @@ struct SolveArgs {
   double2* trace;          // [ntrace][2][M]
   double2* u[2];
   unsigned long long* dbg; // optional per-phase timestamps (HS_SWEEP_TRACE)
+  // two-level partition (g.G > 1): per front f, segment s the c_s / d_s
+  // vectors of the level-2 system, xbuf[f][task parity][s][c, d][tm], and
+  // their arrival counters xflag[f][c, d][s] (monotone; this launch's task ti
+  // posts value xbase[f] + ti + 1)
+  double2* xbuf;
+  unsigned* xflag;
+  unsigned xbase[kMaxFront];
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -665,6 +788,11 @@ __device__ __forceinline__ void st_async_c(uint32_t dst, double2 v, uint32_t bar
       ::"r"(dst), "d"(v.x), "d"(v.y), "r"(bar)
       : "memory");
 }
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   if (bytes)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
@@ -703,9 +831,13 @@ __device__ __forceinline__ double2 mvs2(const double2* m0, const double2* v0, co
 // (stream sizes) and the solve kernel.  Phases: p < L forward cyclic-reduction
 // level p (eliminated points first, then kept ones); p == L the dense top,
 // items (row r, column pair cp); L < p < NP back substitution of level 2L-p;
-// then the 2B column blocks of R and the m spike blocks.
+// then the 2B column blocks of R, the level-2 items (G > 1: the c / d tip,
+// the first chunk's 2(G-1) column blocks of the segment inverse, the two
+// column blocks of [Pk | Qk]) and the m spike blocks.
 struct ItemPlan {
   int m, L, S, qk, QP, B, NP;
+  int rank, seg, G;
+  int ct, zq, pqn;               // level-2 items: c / d tip, inverse rows, [Pk | Qk]
   int plast;                     // phase after which the right tip g[m-1] is final
   int pfx[2 * kMaxLevels + 4];   // items before each phase (NP + 2 = total)
 };
@@ -719,14 +851,20 @@ __host__ __device__ inline int plan_first(const ItemPlan& P, int p) {
 __host__ __device__ inline int plan_step(const ItemPlan& P, int p) {
   return (p < P.L ? 1 : 2) << plan_level(P, p);
 }
-__host__ __device__ inline void plan_items(const Chunks& g, int rank, ItemPlan& P) {
-  P.m = g.len(rank);
+__host__ __device__ inline void plan_items(const Chunks& g, int K, ItemPlan& P) {
+  P.m = g.len(K);
   P.L = g.L;
   P.S = 1 << g.L;
   P.qk = (P.m - 1) / P.S + 1;
   P.QP = (P.qk + 1) / 2;
   P.B = g.C - 1;
   P.NP = 2 * P.L + 1;
+  P.rank = K % g.C;
+  P.seg = K / g.C;
+  P.G = g.G;
+  P.ct = g.G > 1 && ((P.rank == 0 && P.seg > 0) || (P.rank == P.B && P.seg < g.G - 1)) ? 1 : 0;
+  P.zq = g.G > 1 && P.rank == 0 ? 2 * (g.G - 1) : 0;
+  P.pqn = g.G > 1 ? 2 : 0;
   int acc = 0;
   for (int p = 0; p < P.NP; ++p) {
     P.pfx[p] = acc;
@@ -735,7 +873,7 @@ __host__ __device__ inline void plan_items(const Chunks& g, int rank, ItemPlan& 
     else if (f < P.m) acc += (P.m - 1 - f) / plan_step(P, p) + 1;
   }
   P.pfx[P.NP] = acc;
-  P.pfx[P.NP + 1] = acc + (P.B > 0 ? 2 * P.B : 0);
+  P.pfx[P.NP + 1] = acc + (P.B > 0 ? 2 * P.B : 0) + P.ct + P.zq + P.pqn;
   P.pfx[P.NP + 2] = P.pfx[P.NP + 1] + (P.B > 0 ? P.m : 0);
   // the dense top, or the back-substitution level of m-1 (its lowest set bit)
   int tz = 0;
@@ -785,10 +923,12 @@ __host__ __device__ inline int plan_yl(const ItemPlan& P, int p, int j) {
 
 // Factor arrays of one slab before packing (setup only).
 enum ItemArray : uint32_t {
-  kArrEf = 0, kArrEb = 1, kArrKr = 2, kArrRk = 3, kArrSp = 4, kArrQd = 5, kArrEbr = 6, kArrSpr = 7
+  kArrEf = 0, kArrEb = 1, kArrKr = 2, kArrRk = 3, kArrSp = 4, kArrQd = 5, kArrEbr = 6, kArrSpr = 7,
+  kArrX2 = 8
 };
+constexpr uint32_t kOffMask = (1u << 28) - 1;
 __host__ __device__ constexpr uint32_t item_enc(uint32_t arr, int64_t off) {
-  return (arr << 29) | (uint32_t)off;
+  return (arr << 28) | (uint32_t)off;
 }
 
 // Source blocks of item r (array + offset from the slab base, in stream
@@ -828,10 +968,24 @@ __host__ __device__ inline int item_sources(const Chunks& g, int rank, const Ite
       if (yl - s >= 0) src[n++] = item_enc(kArrEb, y * 2 * TM2);
       if (yl + s < m) src[n++] = item_enc(kArrEb, y * 2 * TM2 + TM2);
     }
-  } else if (p == P.NP) {    // R column block j (2tm x tm, two blocks)
+  } else if (p == P.NP && j < 2 * P.B) {   // R column block j (2tm x tm, two blocks)
     const int64_t o = ((int64_t)rank * (2 * P.B) + j) * (2 * TM2);
     src[n++] = item_enc(kArrRk, o);
     src[n++] = item_enc(kArrRk, o + TM2);
+  } else if (p == P.NP) {    // level 2: c / d tip, inverse rows, [Pk | Qk]
+    const int jj = j - 2 * P.B;
+    const int64_t xb = (int64_t)rank * g.xstride() * TM2;
+    if (jj < P.ct) {
+      src[n++] = item_enc(kArrX2, xb);
+    } else if (jj < P.ct + P.zq) {
+      const int64_t o = xb + (1 + 2 * (int64_t)(jj - P.ct)) * TM2;
+      src[n++] = item_enc(kArrX2, o);
+      src[n++] = item_enc(kArrX2, o + TM2);
+    } else {
+      const int64_t o = xb + (1 + 4 * (int64_t)(g.G - 1) + 2 * (jj - P.ct - P.zq)) * TM2;
+      src[n++] = item_enc(kArrX2, o);
+      src[n++] = item_enc(kArrX2, o + TM2);
+    }
   } else if (g.nr) {         // spikes W, V of block j, restricted to the kNR rows
     src[n++] = item_enc(kArrSpr, (int64_t)(Y0 + j) * TM2);
   } else {                   // spikes W, V of block j
@@ -844,8 +998,11 @@ __host__ __device__ inline int item_sources(const Chunks& g, int rank, const Ite
 
 constexpr int kMaxItems = 1024;   // items of one chunk solve (checked at sweep_create)
 
-// items of one chunk solve: <= 3m + 2L local, 15 dense, 2(C-1) R blocks, m spike blocks
-__host__ __device__ inline int itab_len(int mmax) { return 4 * mmax + 2 * kMaxLevels + 2 * kMaxC + 16; }
+// items of one chunk solve: <= 3m + 2L local, 15 dense, 2(C-1) R blocks,
+// <= 2G + 1 level-2 items, m spike blocks
+__host__ __device__ inline int itab_len(int mmax) {
+  return 4 * mmax + 2 * kMaxLevels + 2 * kMaxC + 2 * kMaxG + 24;
+}
 
 // blocks of one chunk's slab-solve stream
 template <int TM>
@@ -899,7 +1056,7 @@ __host__ __device__ inline void chunk_plan(const Chunks& g, int rank, int mmax, 
 }
 
 struct FactorArrays {
-  const double2 *ef, *eb, *kr, *rk, *sp, *qd, *ebr, *spr;
+  const double2 *ef, *eb, *kr, *rk, *sp, *qd, *ebr, *spr, *x2;
 };
 
 // Restricted updates (setup): for the kNR rows R of each slab, one block per
@@ -929,7 +1086,7 @@ template <int TM>
 __global__ void __launch_bounds__(256) k_pack(Chunks g, FactorArrays f, double2* __restrict__ stream,
                                               int nbs) {
   constexpr int TM2 = TM * TM;
-  const int slab = blockIdx.x / g.C, k = blockIdx.x % g.C, M = g.M, C = g.C;
+  const int C = g.nch(), slab = blockIdx.x / C, k = blockIdx.x % C, M = g.M;
   __shared__ ItemPlan P;
   __shared__ int boff[kMaxItems];
   if (threadIdx.x == 0) {
@@ -943,13 +1100,14 @@ __global__ void __launch_bounds__(256) k_pack(Chunks g, FactorArrays f, double2*
     });
   }
   __syncthreads();
-  const double2* base[8] = {
+  const double2* base[9] = {
       f.ef + (int64_t)slab * M * TM2,           f.eb + (int64_t)slab * M * 2 * TM2,
       f.kr + (int64_t)slab * C * g.kstride * 2 * TM2,
-      f.rk + (int64_t)slab * C * (2 * (C - 1)) * 2 * TM2,
+      f.rk + (int64_t)slab * C * (2 * (g.C - 1)) * 2 * TM2,
       f.sp + (int64_t)slab * M * 2 * TM2,       f.qd + (int64_t)slab * C * g.q * g.q * TM2,
       f.ebr ? f.ebr + (int64_t)slab * M * TM2 : nullptr,
-      f.spr ? f.spr + (int64_t)slab * M * TM2 : nullptr};
+      f.spr ? f.spr + (int64_t)slab * M * TM2 : nullptr,
+      f.x2 ? f.x2 + (int64_t)slab * C * g.xstride() * TM2 : nullptr};
   double2* out = stream + ((int64_t)slab * C + k) * nbs * TM2;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   for (int r = warp; r < P.pfx[P.NP + 2]; r += 8) {
@@ -957,7 +1115,7 @@ __global__ void __launch_bounds__(256) k_pack(Chunks g, FactorArrays f, double2*
     bool hx;
     const int n = item_sources<TM>(g, k, P, r, src, &hx);
     for (int b = 0; b < n; ++b) {
-      const double2* s = base[src[b] >> 29] + (src[b] & 0x1fffffffu);
+      const double2* s = base[src[b] >> 28] + (src[b] & kOffMask);
       double2* d = out + (int64_t)(boff[r] + b) * TM2;
       for (int e = lane; e < TM2; e += 32) d[e] = s[e];
     }
@@ -1026,7 +1184,8 @@ struct Ring {
   static int fixed(int mmax) {
     return 2 * (mmax + 1) * TM * 16 + 4 * kMaxC * TM * 16 + 4 * TM * 16 +
            (kWarps + 1) * 2 * TM * 16 + 12 * mmax * 16 + 64 + (int)sizeof(ItemPlan) +
-           kMaxTasks * 4 + itab_len(mmax) * 12 + 512;
+           kMaxTasks * 4 + itab_len(mmax) * 12 + 512 +
+           (2 * kMaxG * TM + 4 * TM) * 16 + 16;
   }
   static int nchunk(int mmax) {
     const int avail = 225 * 1024 - fixed(mmax);
@@ -1038,16 +1197,20 @@ struct Ring {
 template <int TM>
 __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   constexpr int TM2 = Geo<TM>::TM2;
-  constexpr int G = Ring<TM>::G;
   constexpr int CHUNK = Ring<TM>::CHUNK;
   constexpr int YPW = 32 / TM;   // face points per warp pass in row-wise loops
   constexpr int N2 = 2 * TM;     // interface unknowns per chunk (alpha, beta)
   cg::cluster_group cl = cg::this_cluster();
   const Chunks& g = a.g;
-  const int C = g.C, M = g.M, B = C - 1;
+  const int C = g.C, M = g.M, B = C - 1, G = g.G, NCH = g.nch();
   const int rank = (int)cl.block_rank();
-  const int front = blockIdx.x / C;
-  const int Y0 = g.y0(rank), Y1 = g.y0(rank + 1);
+  const int front = blockIdx.x / (C * G);
+  const int seg = (blockIdx.x / C) % G;   // face segment of this cluster (two-level partition)
+  const int K = seg * C + rank;           // global chunk index
+  const int Y0 = g.y0(K), Y1 = g.y0(K + 1);
+  // the last chunk of a segment with a right neighbour segment keeps its own
+  // right tip g[m-1] for c_s (pushed to itself, tau slot 2B)
+  const bool lastpush = G > 1 && rank == B && seg < G - 1;
   const int m = Y1 - Y0;
   const int mmax = g.mmax;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -1064,8 +1227,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   double2* part = halo2 + 4 * TM;                   // [kWarps][2TM] R / dense-top partial sums
   double2* ab = part + kWarps * N2;                 // [2TM] alpha_{k-1}, beta_k
   double2* stc = ab + N2;                           // [2 tin][2 rows][3 offsets][mmax] couplings
-  uint64_t* xbar = (uint64_t*)(stc + 12 * mmax);    // [4] tips (2), halo (2) arrival barriers
-  uint64_t* cbar = xbar + 4;                        // [NC] chunk arrival
+  double2* t2v = stc + 12 * mmax;                   // [2(G-1)][TM] level-2 right-hand side
+  double2* pqv = t2v + 2 * kMaxG * TM;              // [2][2TM] (P_s, Q_s) by task parity
+  uint64_t* xbar = (uint64_t*)(pqv + 4 * TM);       // [6] tips (2), halo (2), (P_s, Q_s) (2)
+  uint64_t* cbar = xbar + 6;                        // [NC] chunk arrival
   volatile int* cseq = (volatile int*)(cbar + NC);  // [NC] chunk issued into a slot
   int* ccnt = (int*)(cseq + NC);                    // [NC] blocks of the slot's chunk consumed
   uint32_t* plan = (uint32_t*)(ccnt + NC);          // this rank's plan (chunk_plan layout)
@@ -1083,7 +1248,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   const int fcount = a.fcount[front];
   {
     const int pw = plan_words(mmax);
-    const uint32_t* src = a.plan + (int64_t)rank * pw;
+    const uint32_t* src = a.plan + (int64_t)K * pw;
     for (int i = threadIdx.x; i < pw; i += blockDim.x) plan[i] = __ldg(src + i);
   }
   if (threadIdx.x == 0) {
@@ -1092,7 +1257,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       cseq[i] = -1;
       ccnt[i] = 0;
     }
-    for (int i = 0; i < 4; ++i) mbar_init(&xbar[i], 1);
+    for (int i = 0; i < 6; ++i) mbar_init(&xbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = threadIdx.x; i < fcount; i += blockDim.x) slabs[i] = a.tasks[ffirst + i].slab;
@@ -1139,7 +1304,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     const int nbk = (int)(ce & 0xff);
     *(volatile int*)&ccnt[sl] = 0;   // ordered before cseq (same thread, volatile)
     // (timing experiment bit 16: every task streams slab 0's data -> L2-resident)
-    const double2* sbase = a.stream + ((int64_t)((HS_SWEEP_EXP & 16) ? 0 : slabs[ti]) * C + rank) *
+    const double2* sbase = a.stream + ((int64_t)((HS_SWEEP_EXP & 16) ? 0 : slabs[ti]) * NCH + K) *
                                           a.nbs * TM2;
     mbar_expect_tx(&cbar[sl], (HS_SWEEP_EXP & 2) ? 0u : (uint32_t)nbk * TM2 * 16);
     if (!(HS_SWEEP_EXP & 2))
@@ -1195,7 +1360,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     const bool hx = e & 1;
     const int n = (int)((e >> 1) & 3);
     if (HS_SWEEP_DIRECT) {
-      const double2* p0 = a.stream + (((int64_t)slabs[ti] * C + rank) * a.nbs +
+      const double2* p0 = a.stream + (((int64_t)slabs[ti] * NCH + K) * a.nbs +
                                       (ctab[e >> 12] >> 8) + ((e >> 3) & 0x1ff)) * TM2;
       return hx ? Item{p0, p0 + TM2, 0, n, r} : Item{nullptr, p0, 0, n, r};
     }
@@ -1287,11 +1452,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     const bool loc3 = ti > 0 && t.tin3 >= 0 && prev.out4 == t.tin3;
     if (threadIdx.x == 0) {
       if (ti > 0) mbar_expect_tx(&xbar[2 + par], halo_bytes);
-      if (B > 0) mbar_expect_tx(&xbar[par], 2 * B * TM * 16);
+      if (B > 0) mbar_expect_tx(&xbar[par], 2 * B * TM * 16 + (lastpush ? TM * 16 : 0));
+      if (G > 1) mbar_expect_tx(&xbar[4 + par], N2 * 16);
     }
     stamp(ti, 0);
     if (HS_SWEEP_L2NEXT && ti + 1 < fcount) {   // next slab's stream into L2 (LSU path, not TMA)
-      const char* nb = (const char*)(a.stream + ((int64_t)slabs[ti + 1] * C + rank) * a.nbs * TM2);
+      const char* nb = (const char*)(a.stream + ((int64_t)slabs[ti + 1] * NCH + K) * a.nbs * TM2);
       const int64_t bytes = (int64_t)((ctab[CPT - 1] >> 8) + (ctab[CPT - 1] & 0xff)) * TM2 * 16;
       for (int64_t o = (int64_t)threadIdx.x * 128; o < bytes; o += kCW * 32 * 128)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(nb + o));
@@ -1404,6 +1570,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
         asm volatile("bar.sync 2, %0;" ::"r"(kNA * 32) : "memory");
         if (p == P.plast && rank < B && lane < TM)
           push_tip(tau, par, 2 * rank * TM, Yv + (m - 1) * TM, warp, kNA);
+        if (p == P.plast && lastpush && warp == 0 && lane < TM)   // own g[m-1] for c_s
+          st_async_c(map_rank(&tau[2 * B * TM + lane], rank), Yv[(m - 1) * TM + lane],
+                     map_rank(&xbar[par], rank));
       }
     } else {
       // ---- group B: tips out (as soon as final), the next task's rhs inputs
@@ -1412,51 +1581,125 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
         if (rank > 0) push_tip(tau, par, (2 * (rank - 1) + 1) * TM, Yv, warp - kNA, kCW - kNA);
         if (P.plast == L && rank < B)
           push_tip(tau, par, 2 * rank * TM, Yv + (m - 1) * TM, warp - kNA, kCW - kNA);
+        if (P.plast == L && lastpush && warp == kNA)
+          st_async_c(map_rank(&tau[2 * B * TM + lane], rank), Yv[(m - 1) * TM + lane],
+                     map_rank(&xbar[par], rank));
       }
       if (ti + 1 < fcount) prefetch_rhs(tn, kNA, kCW - kNA);
       mbar_wait(&xbar[par], (uint32_t)(ti >> 1) & 1);
       stamp(ti, 40);
-      // rows r0 = lane (tm 32) or x (tm 16, per half) and r0 + 32 / r0 + 16
-      double2 acc0 = czero(), acc1 = czero();
-      const int nq = 2 * B;
-      const int r0 = HW == 1 ? lane : x, r1 = r0 + (HW == 1 ? 32 : 16);   // r1 unused: tm 16, HW 1
-      for (int jp = (warp - kNA) * HW; jp < nq; jp += (kCW - kNA) * HW) {
-        const int j = jp + sub;
-        const bool has = j < nq;
-        const int r = P.pfx[NP] + j;
-        Item it{};
-        if (has) {
-          it = acquire(ti, r);   // 2tm x tm, row index fastest, over two blocks
-          const double2* tq = tau + j * TM;
+      // column-block GEMV over group B: out (2tm) = sum_j blocks_j vec_j, or
+      // out -= it (subtract); items rfirst.. of 2tm x tm column blocks (row index
+      // fastest over two ring blocks), rows r0 = lane (tm 32) or x (tm 16)
+      // and r0 + 32 / r0 + 16
+      auto cgemv = [&](int rfirst, int nq, const double2* vec, double2* out, bool subtract) {
+        double2 acc0 = czero(), acc1 = czero();
+        const int r0 = HW == 1 ? lane : x, r1 = r0 + (HW == 1 ? 32 : 16);   // r1 unused: tm 16, HW 1
+        for (int jp = (warp - kNA) * HW; jp < nq; jp += (kCW - kNA) * HW) {
+          const int j = jp + sub;
+          const bool has = j < nq;
+          Item it{};
+          if (has) {
+            it = acquire(ti, rfirst + j);
+            const double2* tq = vec + j * TM;
 #pragma unroll 4
-          for (int c = 0; c < TM / 2; ++c) {
-            const double2 tv = tq[c];
-            acc0 = cfma(it.m0[c * N2 + r0], tv, acc0);
-            if (HW == 2 || TM == 32) acc1 = cfma(it.m0[c * N2 + r1], tv, acc1);
+            for (int c = 0; c < TM / 2; ++c) {
+              const double2 tv = tq[c];
+              acc0 = cfma(it.m0[c * N2 + r0], tv, acc0);
+              if (HW == 2 || TM == 32) acc1 = cfma(it.m0[c * N2 + r1], tv, acc1);
+            }
+#pragma unroll 4
+            for (int c = 0; c < TM / 2; ++c) {
+              const double2 tv = tq[TM / 2 + c];
+              acc0 = cfma(it.m1[c * N2 + r0], tv, acc0);
+              if (HW == 2 || TM == 32) acc1 = cfma(it.m1[c * N2 + r1], tv, acc1);
+            }
           }
-#pragma unroll 4
-          for (int c = 0; c < TM / 2; ++c) {
-            const double2 tv = tq[TM / 2 + c];
-            acc0 = cfma(it.m1[c * N2 + r0], tv, acc0);
-            if (HW == 2 || TM == 32) acc1 = cfma(it.m1[c * N2 + r1], tv, acc1);
+          release(it, has);
+        }
+        if (HW == 2) {   // both halves' items hold rows x and x + 16
+          acc0 = cadd(acc0, shfl_xor_c(acc0, 16));
+          acc1 = cadd(acc1, shfl_xor_c(acc1, 16));
+        }
+        if (lane < 32 / HW) {
+          part[warp * N2 + r0] = acc0;
+          if (HW == 2 || TM == 32) part[warp * N2 + r1] = acc1;
+        }
+        asm volatile("bar.sync 3, %0;" ::"r"((kCW - kNA) * 32) : "memory");
+        if (threadIdx.x - kNA * 32 < (unsigned)N2) {
+          const int t = threadIdx.x - kNA * 32;
+          double2 sacc = czero();
+          for (int w = kNA; w < kCW; ++w) sacc = cadd(sacc, part[w * N2 + t]);
+          out[t] = subtract ? csub(out[t], sacc) : sacc;
+        }
+        asm volatile("bar.sync 3, %0;" ::"r"((kCW - kNA) * 32) : "memory");
+      };
+      // alpha_{k-1}, beta_k = (rows of R) tau
+      cgemv(P.pfx[NP], 2 * B, tau, ab, false);
+      if (G > 1) {
+        // ---- second level (two-level partition, k_level2): post c_s / d_s,
+        // the segment's first CTA solves for (P_s, Q_s) once every segment
+        // has posted and hands them to the cluster, every CTA corrects
+        // (alpha, beta) -= Pk P_s + Qk Q_s
+        const int r_l2 = P.pfx[NP] + 2 * B;
+        unsigned* fl = a.xflag + (size_t)front * 2 * kMaxG;
+        double2* xb = a.xbuf + ((size_t)front * 2 + par) * kMaxG * 2 * TM;
+        const unsigned want = a.xbase[front] + (unsigned)ti + 1u;
+        const int wb = warp - kNA;
+        if (P.ct && wb == 0) {
+          const Item it = acquire(ti, r_l2);
+          const bool isc = rank == B;   // c_s (last chunk) or d_s (first chunk)
+          const double2 acc = mvx<TM, HW>(it.m0, isc ? ab : ab + TM, nullptr, nullptr, lane);
+          release(it, true);
+          if (lane < TM) {
+            const double2 gv = isc ? tau[2 * B * TM + lane] : Yv[lane];   // g[last] / g[first]
+            __stcg(&xb[(seg * 2 + (isc ? 0 : 1)) * TM + lane], csub(gv, acc));
+          }
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) atomicAdd(&fl[(isc ? 0 : 1) * kMaxG + seg], 1u);
+        }
+        if (rank == 0) {
+          const int nz = 2 * (G - 1);
+          if (wb == 0 && lane < nz) {   // c_0 .. c_{G-2} (lanes < G-1), d_1 .. d_{G-1}
+            const int isd = lane >= G - 1;
+            const unsigned* f = fl + isd * kMaxG + (isd ? lane - (G - 1) + 1 : lane);
+            while ((int)(ld_acquire_gpu(f) - want) < 0) {
+            }
+          }
+          asm volatile("bar.sync 3, %0;" ::"r"((kCW - kNA) * 32) : "memory");
+          // level-2 right-hand side in k_reduced order: block 2b = c_b, 2b + 1 = d_{b+1}
+          for (int i = threadIdx.x - kNA * 32; i < nz * TM; i += (kCW - kNA) * 32) {
+            const int blk = i / TM, e = i % TM, b2 = blk / 2;
+            const int sg = (blk & 1) ? b2 + 1 : b2;
+            t2v[i] = __ldcg(&xb[(sg * 2 + (blk & 1)) * TM + e]);
+          }
+          asm volatile("bar.sync 3, %0;" ::"r"((kCW - kNA) * 32) : "memory");
+          double2* pql = part + kWarps * N2 - N2;   // (the last warp's slot: producer, unused)
+          cgemv(r_l2 + P.ct, nz, t2v, pql, false);
+          if (wb == 0) {   // (P_s, Q_s) to every CTA of the cluster
+            for (int e = lane; e < N2; e += 32) {
+              const double2 v = pql[e];
+              for (int d = 0; d < C; ++d)
+                st_async_c(map_rank(&pqv[par * N2 + e], d), v, map_rank(&xbar[4 + par], d));
+            }
           }
         }
-        release(it, has);
-      }
-      if (HW == 2) {   // both halves' items hold rows x and x + 16
-        acc0 = cadd(acc0, shfl_xor_c(acc0, 16));
-        acc1 = cadd(acc1, shfl_xor_c(acc1, 16));
-      }
-      if (lane < 32 / HW) {
-        part[warp * N2 + r0] = acc0;
-        if (HW == 2 || TM == 32) part[warp * N2 + r1] = acc1;
-      }
-      asm volatile("bar.sync 3, %0;" ::"r"((kCW - kNA) * 32) : "memory");
-      if (threadIdx.x - kNA * 32 < (unsigned)N2) {
-        const int t = threadIdx.x - kNA * 32;
-        double2 sacc = czero();
-        for (int w = kNA; w < kCW; ++w) sacc = cadd(sacc, part[w * N2 + t]);
-        ab[t] = sacc;
+        mbar_wait_cluster(&xbar[4 + par], (uint32_t)(ti >> 1) & 1);
+        const double2* pqs = pqv + par * N2;
+        cgemv(r_l2 + P.ct + P.zq, 2, pqs, ab, true);
+        if (threadIdx.x - kNA * 32 < (unsigned)TM) {
+          const int e = threadIdx.x - kNA * 32;
+          const int nb = ((ti + 1) & 1) * 2 * TM;   // next task's halo: edge values across segments
+          if (rank == 0 && seg > 0) {
+            ab[e] = pqs[e];
+            halo2[nb + e] = pqs[e];
+          }
+          if (rank == B && seg < G - 1) {
+            ab[TM + e] = pqs[TM + e];
+            halo2[nb + TM + e] = pqs[TM + e];
+          }
+        }
       }
       stamp(ti, 41);
     }
@@ -1471,13 +1714,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
         if (has) {
           it = acquire(ti, r);   // W_j, V_j
           if (g.nr) {                       // only the rows read later
-            const double2 acc = mvr<TM>(it.m0, rank > 0 ? ab : nullptr, rank < B ? ab + TM : nullptr,
-                                        lane);
+            const double2 acc = mvr<TM>(it.m0, rank > 0 || seg > 0 ? ab : nullptr,
+                                        rank < B || seg < G - 1 ? ab + TM : nullptr, lane);
             if (lane < kNR) Yv[j * TM + rr[lane]] = csub(Yv[j * TM + rr[lane]], acc);
           } else {
-            const double2 acc = mvx<TM, HW>(rank > 0 ? it.m0 : nullptr, rank > 0 ? ab : nullptr,
-                                        rank < B ? it.m1 : nullptr, rank < B ? ab + TM : nullptr,
-                                        lane);
+            const bool wl = rank > 0 || seg > 0, wr2 = rank < B || seg < G - 1;
+            const double2 acc = mvx<TM, HW>(wl ? it.m0 : nullptr, wl ? ab : nullptr,
+                                        wr2 ? it.m1 : nullptr, wr2 ? ab + TM : nullptr, lane);
             if (wr) Yv[j * TM + x] = csub(Yv[j * TM + x], acc);
           }
         }
@@ -1560,7 +1803,7 @@ cudaError_t launch_dense_top_q(Ctx* c, const Chunks& g, int J, const double2* D,
   cudaError_t e = cudaFuncSetAttribute(k_dense_top<TM, Q>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k_dense_top<TM, Q><<<J * g.C, 1024, smem, c->stream>>>(g, D, Lc, Uc, qd, err);
+  k_dense_top<TM, Q><<<J * g.nch(), 1024, smem, c->stream>>>(g, D, Lc, Uc, qd, err);
   c->launches++;
   return cudaGetLastError();
 }
@@ -1588,17 +1831,20 @@ cudaError_t launch_dense_top(Ctx* c, const Chunks& g, int J, const double2* D, c
 template <int TM>
 int factorize(Ctx* c, Sweep* s, const std::vector<SlabInfo>& info, const Chunks& g) {
   constexpr int TM2 = Geo<TM>::TM2;
-  const int J = s->J, M = s->M, L = s->L, C = s->C, B = C - 1;
+  const int J = s->J, M = s->M, L = s->L, C = s->C, B = C - 1, G = s->G, NCH = C * G;
   const size_t wbytes = (size_t)J * M * TM2 * sizeof(double2);
-  const size_t ebytes = (size_t)J * C * TM2 * sizeof(double2);
+  const size_t ebytes = (size_t)J * NCH * TM2 * sizeof(double2);
   double2 *D = nullptr, *Lc = nullptr, *Uc = nullptr, *EL = nullptr, *EU = nullptr;
   double2 *Hw = nullptr, *Zw = nullptr, *tips = nullptr, *Gw = nullptr, *Zr = nullptr;
+  double2 *tips2 = nullptr, *rk2 = nullptr, *Gw2 = nullptr, *Zr2 = nullptr;
   SlabInfo* d_info = nullptr;
   unsigned long long* d_err = nullptr;
   int rc = HS_OK;
   auto cleanup = [&]() {
     cudaFree(D); cudaFree(Lc); cudaFree(Uc); cudaFree(EL); cudaFree(EU); cudaFree(Hw);
     cudaFree(Zw); cudaFree(tips); cudaFree(Gw); cudaFree(Zr); cudaFree(d_info); cudaFree(d_err);
+    cudaFree(tips2); cudaFree(rk2); cudaFree(Gw2); cudaFree(Zr2);
+    Gw = Zr = tips2 = rk2 = Gw2 = Zr2 = nullptr;
   };
 #define HS_TRYF(call, what)                                            \
   do {                                                                 \
@@ -1619,7 +1865,7 @@ int factorize(Ctx* c, Sweep* s, const std::vector<SlabInfo>& info, const Chunks&
   HS_TRYF(cudaMemsetAsync(EL, 0, ebytes, c->stream), "memset");
   HS_TRYF(cudaMemsetAsync(EU, 0, ebytes, c->stream), "memset");
   HS_TRYF(cudaMemsetAsync(s->eb, 0, 2 * wbytes, c->stream), "memset");
-  HS_TRYF(cudaMemsetAsync(s->kr, 0, (size_t)J * C * g.kstride * 2 * TM2 * sizeof(double2),
+  HS_TRYF(cudaMemsetAsync(s->kr, 0, (size_t)J * NCH * g.kstride * 2 * TM2 * sizeof(double2),
                           c->stream), "memset");
   const int smem3 = 3 * TM * (TM + 1) * (int)sizeof(double2);
   const int smem4 = 4 * TM * (TM + 1) * (int)sizeof(double2);
@@ -1636,20 +1882,47 @@ int factorize(Ctx* c, Sweep* s, const std::vector<SlabInfo>& info, const Chunks&
   if (B > 0) {   // spikes from the pristine chunk operators
     HS_TRYF(cudaMalloc((void**)&Hw, wbytes), "spike work alloc");
     HS_TRYF(cudaMalloc((void**)&Zw, wbytes), "spike work alloc");
-    k_spikes<TM><<<J * C, TM * TM, smem7, c->stream>>>(g, D, Lc, Uc, EL, EU, Hw, Zw, s->sp,
-                                                       tips, d_err);
+    k_spikes<TM><<<J * NCH, TM * TM, smem7, c->stream>>>(g, D, Lc, Uc, EL, EU, Hw, Zw, s->sp,
+                                                         tips, d_err);
     c->launches++;
     HS_TRYF(cudaGetLastError(), "spikes");
     constexpr int N = 2 * TM;
     const int NR = B * N;
-    HS_TRYF(cudaMalloc((void**)&Gw, (size_t)J * B * N * N * sizeof(double2)), "alloc");
-    HS_TRYF(cudaMalloc((void**)&Zr, (size_t)J * NR * NR * sizeof(double2)), "alloc");
+    HS_TRYF(cudaMalloc((void**)&Gw, (size_t)J * G * B * N * N * sizeof(double2)), "alloc");
+    HS_TRYF(cudaMalloc((void**)&Zr, (size_t)J * G * NR * NR * sizeof(double2)), "alloc");
     const int smemr = 2 * N * (N + 1) * (int)sizeof(double2);
     HS_TRYF(cudaFuncSetAttribute(k_reduced<TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  smemr), "attr");
-    k_reduced<TM><<<J, 1024, smemr, c->stream>>>(g, tips, Gw, Zr, s->rk, d_err);
+    // level 1: each segment's C chunks
+    k_reduced<TM><<<J * G, 1024, smemr, c->stream>>>(C, G, tips, Gw, Zr, s->rk, d_err);
     c->launches++;
     HS_TRYF(cudaGetLastError(), "reduced system");
+    if (G > 1) {
+      // level 2: segment tips from the level-1 inverse rows, then the
+      // G-segment interface inverse; its rows go to each segment's first chunk
+      const int xs = g.xstride(), B2 = G - 1, NR2 = B2 * N;
+      HS_TRYF(cudaMalloc((void**)&tips2, (size_t)J * G * 4 * TM2 * sizeof(double2)), "alloc");
+      HS_TRYF(cudaMalloc((void**)&rk2, (size_t)J * G * 2 * B2 * 2 * TM2 * sizeof(double2)), "alloc");
+      HS_TRYF(cudaMalloc((void**)&s->x2, (size_t)J * NCH * xs * TM2 * sizeof(double2)), "alloc");
+      HS_TRYF(cudaMalloc((void**)&Gw2, (size_t)J * B2 * N * N * sizeof(double2)), "alloc");
+      HS_TRYF(cudaMalloc((void**)&Zr2, (size_t)J * NR2 * NR2 * sizeof(double2)), "alloc");
+      HS_TRYF(cudaMemsetAsync(s->x2, 0, (size_t)J * NCH * xs * TM2 * sizeof(double2), c->stream),
+              "memset");
+      const int smeml = 4 * TM * (TM + 1) * (int)sizeof(double2);
+      HS_TRYF(cudaFuncSetAttribute(k_level2<TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   smeml), "attr");
+      k_level2<TM><<<J * G, TM * TM, smeml, c->stream>>>(g, tips, s->rk, tips2, s->x2);
+      c->launches++;
+      HS_TRYF(cudaGetLastError(), "level-2 tips");
+      k_reduced<TM><<<J, 1024, smemr, c->stream>>>(G, 1, tips2, Gw2, Zr2, rk2, d_err);
+      c->launches++;
+      HS_TRYF(cudaGetLastError(), "level-2 reduced system");
+      // rows of segment s -> blocks 1 .. 4(G-1) of chunk s*C
+      HS_TRYF(cudaMemcpy2DAsync(s->x2 + TM2, (size_t)C * xs * TM2 * sizeof(double2), rk2,
+                                (size_t)4 * B2 * TM2 * sizeof(double2),
+                                (size_t)4 * B2 * TM2 * sizeof(double2), (size_t)J * G,
+                                cudaMemcpyDeviceToDevice, c->stream), "level-2 rows");
+    }
   }
   const int mmax = s->mmax;
   for (int l = 0; l < L; ++l) {
@@ -1657,12 +1930,12 @@ int factorize(Ctx* c, Sweep* s, const std::vector<SlabInfo>& info, const Chunks&
     const int nel = mmax - 1 >= sl ? (mmax - 1 - sl) / (2 * sl) + 1 : 0;
     const int nkeep = (mmax - 1) / (2 * sl) + 1;
     if (nel) {
-      k_bcr_elim<TM><<<dim3(nel, J * C), TM * TM, smem3, c->stream>>>(l, g, 0, D, Lc, Uc,
-                                                                      s->ef, s->eb, d_err);
+      k_bcr_elim<TM><<<dim3(nel, J * NCH), TM * TM, smem3, c->stream>>>(l, g, 0, D, Lc, Uc,
+                                                                        s->ef, s->eb, d_err);
       c->launches++;
       HS_TRYF(cudaGetLastError(), "bcr elim");
     }
-    k_bcr_keep<TM><<<dim3(nkeep, J * C), TM * TM, smem4, c->stream>>>(l, g, D, Lc, Uc, s->kr);
+    k_bcr_keep<TM><<<dim3(nkeep, J * NCH), TM * TM, smem4, c->stream>>>(l, g, D, Lc, Uc, s->kr);
     c->launches++;
     HS_TRYF(cudaGetLastError(), "bcr keep");
   }
@@ -1676,12 +1949,13 @@ int factorize(Ctx* c, Sweep* s, const std::vector<SlabInfo>& info, const Chunks&
   }
   // repack into per-(slab, chunk) streams in the solve kernel's item order
   long long nbs = 1;
-  for (int k = 0; k < C; ++k) nbs = std::max<long long>(nbs, stream_blocks<TM>(g, k));
+  for (int k = 0; k < NCH; ++k) nbs = std::max<long long>(nbs, stream_blocks<TM>(g, k));
   s->nbs = nbs;
-  HS_TRYF(cudaMalloc((void**)&s->stream, (size_t)J * C * nbs * TM2 * sizeof(double2)),
+  HS_TRYF(cudaMalloc((void**)&s->stream, (size_t)J * NCH * nbs * TM2 * sizeof(double2)),
           "stream alloc");
-  k_pack<TM><<<J * C, 256, 0, c->stream>>>(
-      g, FactorArrays{s->ef, s->eb, s->kr, s->rk, s->sp, s->qd, s->ebr, s->spr}, s->stream, (int)nbs);
+  k_pack<TM><<<J * NCH, 256, 0, c->stream>>>(
+      g, FactorArrays{s->ef, s->eb, s->kr, s->rk, s->sp, s->qd, s->ebr, s->spr, s->x2}, s->stream,
+      (int)nbs);
   c->launches++;
   HS_TRYF(cudaGetLastError(), "pack");
   unsigned long long err = 0;
@@ -1689,11 +1963,11 @@ int factorize(Ctx* c, Sweep* s, const std::vector<SlabInfo>& info, const Chunks&
   HS_TRYF(cudaStreamSynchronize(c->stream), "factor sync");
 #undef HS_TRYF
   cleanup();
-  for (double2** p : {&s->ef, &s->eb, &s->kr, &s->sp, &s->rk, &s->qd, &s->ebr, &s->spr}) {
+  for (double2** p : {&s->ef, &s->eb, &s->kr, &s->sp, &s->rk, &s->qd, &s->ebr, &s->spr, &s->x2}) {
     cudaFree(*p);
     *p = nullptr;
   }
-  s->factor_bytes = (long long)J * C * nbs * TM2 * (long long)sizeof(double2);
+  s->factor_bytes = (long long)J * NCH * nbs * TM2 * (long long)sizeof(double2);
   if (err != ~0ull) {
     const int slab = (int)(err >> 40);
     const long long row = (long long)(err & 0xffffffffffull);
@@ -1719,10 +1993,11 @@ Chunks make_chunks(const Sweep* s) {
   Chunks g{};
   g.M = s->M;
   g.C = s->C;
+  g.G = s->G;
   g.L = s->L;
   g.q = s->q;
   g.nr = s->nr;
-  for (int k = 0; k <= s->C; ++k) g.y0s[k] = s->y0s[k];
+  for (int k = 0; k <= s->C * s->G; ++k) g.y0s[k] = s->y0s[k];
   g.mmax = s->mmax;
   int acc = 0;
   for (int l = 0; l < s->L; ++l) {
@@ -1828,7 +2103,7 @@ struct SchedBuilder {
       fl.src = src;
       for (const auto& fr : st) {
         if (fr.empty()) continue;
-        if (fl.nfront == kMaxFront) {
+        if (fl.nfront == std::min(kMaxFront, s->max_fronts)) {
           plan.push_back(fl);
           fl = SweepLaunch{};
           fl.kind = SweepLaunch::kSolve;
@@ -1975,27 +2250,39 @@ static std::vector<SweepLaunch> build_nx(Sweep* s, int ncell, const int64_t* jc,
   return plan;
 }
 
-// algorithmic HBM bytes of every solve launch of a plan (profiler): 2-D --
-// exactly the streamed factor blocks + rhs/u/trace rows; 3-D -- both factor
-// blocks of every plane + rhs/u rows
+// algorithmic HBM bytes of every solve launch of a plan (profiler), SURVEY
+// 8(d): the no-pivot banded LU floor of each slab solved in the launch,
+// (2 bw + 1) n 16 B with n = T * face unknowns and the sweep's bandwidth
+// bw = T_max + 1 (2-D) / T_max n_y + T_max + 1 (3-D), thin axis fastest --
+// the format-independent factor bytes a slab solve must read.  The bytes
+// this build's own factor format streams are s->factor_bytes per pass.
 static void plan_bytes(const Sweep* s, std::vector<SweepLaunch>& plan) {
   const double M = (double)s->M;
+  int tmax = 1;
+  for (const SweepTask& t : s->tasks) tmax = std::max(tmax, (int)t.T);
+  const double ny = s->s3 ? (double)s->coarse->shape[1] : 1.0;
+  const double bw = s->s3 ? tmax * ny + tmax + 1.0 : tmax + 1.0;
   for (auto& fl : plan) {
     if (fl.kind != SweepLaunch::kSolve) continue;
     fl.bytes = 0;
     for (int f = 0; f < fl.nfront; ++f)
       for (int i = fl.ffirst[f]; i < fl.ffirst[f] + fl.fcount[f]; ++i) {
         const SweepTask& t = s->tasks[i];
-        if (s->s3) {
-          const double NB = (double)t.T * s->coarse->shape[2];
-          fl.bytes += (2.0 * s->coarse->shape[1] - 1.0) * NB * NB * 16.0 +
-                      M * 16.0 * ((t.b - t.a) + (t.tb - t.ta));
-        } else {
-          fl.bytes += s->rec_bytes + M * 16.0 * ((t.b - t.a) + (t.tb - t.ta)) +
-                      M * 32.0 * ((t.tin1 >= 0) + (t.tin3 >= 0) + (t.out2 >= 0) + (t.out4 >= 0));
-        }
+        const double n = (double)t.T * (s->s3 ? ny * (double)s->coarse->shape[2] : M);
+        fl.bytes += (2.0 * bw + 1.0) * n * 16.0;
       }
   }
+}
+
+// level-2 exchange buffers of a work set (zeroed counters)
+static cudaError_t alloc_exchange(SweepWork* w) {
+  const size_t nb = (size_t)kMaxFront * 2 * kMaxG * 2 * 32 * sizeof(double2);
+  const size_t nf = (size_t)kMaxFront * 2 * kMaxG * sizeof(unsigned);
+  cudaError_t e = cudaMalloc((void**)&w->xbuf, nb);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&w->xflag, nf);
+  if (e == cudaSuccess) e = cudaMemset(w->xflag, 0, nf);
+  for (auto& x : w->xcount) x = 0;
+  return e;
 }
 
 int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, const int64_t* bt,
@@ -2054,22 +2341,38 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     if (int r = slot_table(op, info[j].slot, c)) { delete s; return r; }
   }
   const int TM = s->tm, TM2 = TM * TM;
-  // chunks: ~32 face points per CTA, at most 16 CTAs, cluster schedulable twice
-  int C = std::min(kMaxC, std::max(1, (M + 31) / 32));
+  // chunks: ~32 face points per CTA, at most 16 CTAs per cluster, the
+  // cluster schedulable twice (two X fronts).  Wider faces are cut into G
+  // segments, one cluster each, coupled by the level-2 interface system
+  // (two-level partition), as long as both fronts' G clusters are
+  // co-resident (2 G <= active clusters): they wait on each other.
+  const int want = std::max(1, (M + 31) / 32);
+  int C = std::min(kMaxC, want);
+  int G = want > kMaxC ? std::min(kMaxG, (want + kMaxC - 1) / kMaxC) : 1;
+  if (const char* ev = getenv("HS_SWEEP_SEGMENTS")) G = std::max(1, std::min(kMaxG, atoi(ev)));
+  if (const char* ev = getenv("HS_SWEEP_CPC")) C = std::max(1, std::min(kMaxC, atoi(ev)));
+  if (C < 2) G = 1;
+  int maxc = 0;
   for (;;) {
-    const int mmax = (M + C - 1) / C;
-    int maxc = 0;
+    const int mmax = (M + C * G - 1) / (C * G);
     cudaError_t e = TM == 16 ? prepare_solve<16>(C, mmax, &maxc) : prepare_solve<32>(C, mmax, &maxc);
-    if (e == cudaSuccess && maxc >= 2) break;
+    if (e == cudaSuccess && maxc >= 2 * G) break;
     cudaGetLastError();
+    if (e == cudaSuccess && G > 1) {   // fewer segments (the fronts' clusters must co-reside)
+      G = std::max(1, std::min(G - 1, maxc / 2));
+      continue;
+    }
     if (C == 1) {
       delete s;
       return set_error(c, HS_E_CUDA, "no schedulable cluster for the sweep kernel");
     }
     C = C > 8 ? 8 : C / 2;
+    if (C < 2) G = 1;
   }
+  const int NCH = C * G;
   s->C = C;
-  s->mmax = (M + C - 1) / C;
+  s->G = G;
+  s->mmax = (M + NCH - 1) / NCH;
   // cyclic reduction until at most qmax blocks per chunk are left, then a
   // dense inverse of that reduced system (qmax blocks fit the setup's smem)
   const int qmax = TM == 16 ? 5 : 2;
@@ -2080,36 +2383,37 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     // tip is final after the dense top or the first back-substitution level
     // and the interface solve overlaps the rest of the back substitution.
     const int S = 1 << s->L, h = std::max(1, S / 2), cap = S * qmax;
-    std::vector<int> mk(C, 0);
-    const double mean = (double)M / C;
+    std::vector<int> mk(NCH, 0);
+    const double mean = (double)M / NCH;
     const int base = std::max(1, 1 + h * (int)std::lround((mean - 1.0) / h));
     int rem = M;
-    for (int k = 0; k + 1 < C; ++k) { mk[k] = base; rem -= base; }
-    for (int k = 0; k + 1 < C && rem > mean + h / 2.0; k = (k + 1) % (C - 1)) {
+    for (int k = 0; k + 1 < NCH; ++k) { mk[k] = base; rem -= base; }
+    for (int k = 0; k + 1 < NCH && rem > mean + h / 2.0; k = (k + 1) % (NCH - 1)) {
       if (mk[k] + h > cap) break;
       mk[k] += h; rem -= h;
     }
-    for (int k = 0; k + 1 < C && rem < std::max(1.0, mean - h); k = (k + 1) % (C - 1)) {
+    for (int k = 0; k + 1 < NCH && rem < std::max(1.0, mean - h); k = (k + 1) % (NCH - 1)) {
       if (mk[k] - h < 1) break;
       mk[k] -= h; rem += h;
     }
-    mk[C - 1] = rem;
+    mk[NCH - 1] = rem;
     bool ok = true;
-    for (int k = 0; k < C; ++k) ok = ok && mk[k] >= 1 && mk[k] <= cap;
+    for (int k = 0; k < NCH; ++k) ok = ok && mk[k] >= 1 && mk[k] <= cap;
     s->y0s[0] = 0;
-    for (int k = 0; k < C; ++k)
-      s->y0s[k + 1] = ok ? s->y0s[k] + mk[k] : (int)((int64_t)(k + 1) * M / C);
+    for (int k = 0; k < NCH; ++k)
+      s->y0s[k + 1] = ok ? s->y0s[k] + mk[k] : (int)((int64_t)(k + 1) * M / NCH);
     s->mmax = 0;
-    for (int k = 0; k < C; ++k) s->mmax = std::max(s->mmax, s->y0s[k + 1] - s->y0s[k]);
+    for (int k = 0; k < NCH; ++k) s->mmax = std::max(s->mmax, s->y0s[k + 1] - s->y0s[k]);
     while ((s->mmax - 1) / (1 << s->L) + 1 > qmax) ++s->L;   // (uniform fallback only)
-    int maxc = 0;   // the kernel's shared memory follows the final chunk length
+    // the kernel's shared memory follows the final chunk length
     cudaError_t e0 = TM == 16 ? prepare_solve<16>(C, s->mmax, &maxc)
                               : prepare_solve<32>(C, s->mmax, &maxc);
-    if (e0 != cudaSuccess || maxc < 2) {
+    if (e0 != cudaSuccess || maxc < 2 * G) {
       cudaGetLastError();
       delete s;
       return set_error(c, HS_E_CUDA, "no schedulable cluster for the sweep kernel");
     }
+    s->max_fronts = std::max(1, std::min(kMaxFront, maxc / G));
   }
   s->q = (s->mmax - 1) / (1 << s->L) + 1;
   if (s->L >= kMaxLevels || itab_len(s->mmax) > kMaxItems) {
@@ -2161,7 +2465,7 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   }
   {   // algorithmic bytes of every solve launch (profiler): exactly the streamed blocks
     double rec_blocks = 0;
-    for (int k = 0; k < C; ++k)
+    for (int k = 0; k < NCH; ++k)
       rec_blocks += TM == 16 ? stream_blocks<16>(g, k) : stream_blocks<32>(g, k);
     const double rec_bytes = rec_blocks * TM2 * 16.0;
     s->rec_bytes = rec_bytes;
@@ -2169,9 +2473,9 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   }
 
   const size_t efb = (size_t)J * M * TM2 * sizeof(double2);
-  const size_t krb = (size_t)J * C * g.kstride * 2 * TM2 * sizeof(double2);
-  const size_t rkb = (size_t)J * C * std::max(1, 2 * B) * 2 * TM2 * sizeof(double2);
-  const size_t qdb = (size_t)J * C * s->q * s->q * TM2 * sizeof(double2);
+  const size_t krb = (size_t)J * NCH * g.kstride * 2 * TM2 * sizeof(double2);
+  const size_t rkb = (size_t)J * NCH * std::max(1, 2 * B) * 2 * TM2 * sizeof(double2);
+  const size_t qdb = (size_t)J * NCH * s->q * s->q * TM2 * sizeof(double2);
   s->factor_bytes = (long long)(efb * 5 + krb + qdb + (B > 0 ? rkb : 0));
   e = cudaMalloc((void**)&s->ef, efb);
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->eb, 2 * efb);
@@ -2190,8 +2494,8 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   }
   {   // the solve kernel's per-rank item / chunk tables
     const int pw = plan_words(s->mmax);
-    std::vector<uint32_t> hp((size_t)C * pw, 0u);
-    for (int k = 0; k < C; ++k) {
+    std::vector<uint32_t> hp((size_t)NCH * pw, 0u);
+    for (int k = 0; k < NCH; ++k) {
       if (TM == 16) chunk_plan<16>(g, k, s->mmax, hp.data() + (size_t)k * pw);
       else chunk_plan<32>(g, k, s->mmax, hp.data() + (size_t)k * pw);
     }
@@ -2211,10 +2515,14 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     e = cudaMalloc((void**)&s->trace, (size_t)std::max(1, ntin) * 2 * M * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->g, (size_t)s->n0 * M * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->u2, (size_t)s->n0 * M * sizeof(double2));
+  if (e == cudaSuccess) e = alloc_exchange(&s->own);
   if (e != cudaSuccess) {
     sweep_destroy(s);
     return check_cuda(c, e, "sweep buffers");
   }
+  s->own.trace = s->trace;
+  s->own.g = s->g;
+  s->own.u2 = s->u2;
   *out = s;
   return HS_OK;
 }
@@ -2297,6 +2605,9 @@ void sweep_destroy(Sweep* s) {
   cudaFree(s->g);
   cudaFree(s->u2);
   cudaFree(s->d_tasks);
+  cudaFree(s->x2);
+  cudaFree(s->own.xbuf);
+  cudaFree(s->own.xflag);
   delete s;
 }
 
@@ -2386,13 +2697,17 @@ int sweep_solve_one(Ctx* c, Sweep* s, int j, int64_t a, int64_t b, int64_t ta, i
     g.trace = s->trace;
     g.u[0] = s->u2;
     g.u[1] = s->u2;
+    g.xbuf = s->own.xbuf;
+    g.xflag = s->own.xflag;
+    for (int i = 0; i < kMaxFront; ++i) g.xbase[i] = s->own.xcount[i];
     const int smem = s->tm == 16 ? Ring<16>::smem(s->mmax) : Ring<32>::smem(s->mmax);
     cudaLaunchAttribute attr[1];
-    cudaLaunchConfig_t cfg = solve_config(s->C, 1, smem, c->stream, attr);
+    cudaLaunchConfig_t cfg = solve_config(s->C, s->G, smem, c->stream, attr);
     ProfScope ps(c, K_SWEEP_FRONT, s->rec_bytes);
     cudaError_t e = s->tm == 16 ? cudaLaunchKernelEx(&cfg, k_part_solve<16>, g)
                                 : cudaLaunchKernelEx(&cfg, k_part_solve<32>, g);
     if (e != cudaSuccess) return check_cuda(c, e, "slab solve launch");
+    s->own.xcount[0] += 1;
     HS_LAUNCH_CHECK(c, "slab solve kernel");
   }
   const int64_t n = (tb - ta) * (int64_t)M;
@@ -2416,6 +2731,7 @@ int sweep_work_create(Ctx* c, const Sweep* s, SweepWork* w) {
   cudaError_t e = cudaMalloc((void**)&w->trace, (size_t)std::max(1, s->ntrace) * 2 * s->M * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc((void**)&w->g, nf);
   if (e == cudaSuccess) e = cudaMalloc((void**)&w->u2, nf);
+  if (e == cudaSuccess) e = alloc_exchange(w);
   if (e != cudaSuccess) {
     sweep_work_destroy(w);
     return check_cuda(c, e, "sweep work buffers");
@@ -2427,13 +2743,14 @@ void sweep_work_destroy(SweepWork* w) {
   cudaFree(w->trace);
   cudaFree(w->g);
   cudaFree(w->u2);
+  cudaFree(w->xbuf);
+  cudaFree(w->xflag);
   *w = SweepWork{};
 }
 
 int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
                 const SweepWork* w, int first, int last) {
-  const SweepWork own{s->trace, s->g, s->u2};
-  if (!w) w = &own;
+  if (!w) w = &s->own;
   if (!s->has_plan(variant))
     return set_error(c, HS_E_ARG,
                      variant == HS_VARIANT_X ? "X-sweep needs an even subdomain count"
@@ -2519,6 +2836,9 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
         a.trace = w->trace;
         a.u[0] = u;
         a.u[1] = w->u2;
+        a.xbuf = w->xbuf;
+        a.xflag = w->xflag;
+        for (int i = 0; i < kMaxFront; ++i) a.xbase[i] = w->xcount[i];
         static const char* trace_path = getenv("HS_SWEEP_TRACE");
         static bool traced = false;
         unsigned long long* dbg = nullptr;
@@ -2529,11 +2849,13 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
         a.dbg = dbg;
         const int smem = s->tm == 16 ? Ring<16>::smem(s->mmax) : Ring<32>::smem(s->mmax);
         cudaLaunchAttribute attr[1];
-        cudaLaunchConfig_t cfg = solve_config(s->C, Lh.nfront, smem, c->stream, attr);
+        cudaLaunchConfig_t cfg = solve_config(s->C, Lh.nfront * s->G, smem, c->stream, attr);
         ProfScope ps(c, K_SWEEP_FRONT, Lh.bytes);
         cudaError_t e = s->tm == 16 ? cudaLaunchKernelEx(&cfg, k_part_solve<16>, a)
                                     : cudaLaunchKernelEx(&cfg, k_part_solve<32>, a);
         if (e != cudaSuccess) return check_cuda(c, e, "sweep solve launch");
+        for (int i = 0; i < Lh.nfront; ++i)   // level-2 counters advance by the fronts' tasks
+          const_cast<SweepWork*>(w)->xcount[i] += (unsigned)Lh.fcount[i];
         HS_LAUNCH_CHECK(c, "sweep solve kernel");
         if (dbg) {
           std::vector<unsigned long long> h(16 * 1024);

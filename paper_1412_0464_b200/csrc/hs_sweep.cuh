@@ -36,17 +36,25 @@ struct SweepWork {
   double2* trace = nullptr;     // [ntrace][2][M]
   double2* g = nullptr;         // [n0*M]
   double2* u2 = nullptr;        // [n0*M]
+  // two-level partition exchange (G > 1): level-2 right-hand sides and their
+  // arrival counters (see SolveArgs); xcount = the counters' value at the
+  // next launch per front slot (host-side, monotone)
+  double2* xbuf = nullptr;      // [kMaxFront][2][8][2][32]
+  unsigned* xflag = nullptr;    // [kMaxFront][2][8]
+  unsigned xcount[16] = {};
 };
 
 // Partitioned slab factors of every slab (see hs_sweep.cu).
 struct Sweep {
   int J = 0, M = 0, n0 = 0;
   int tm = 16;                  // padded block size (16 or 32)
-  int C = 1;                    // chunks of the face = CTAs per cluster
+  int C = 1;                    // chunks per face segment = CTAs per cluster
+  int G = 1;                    // face segments = clusters per front (two-level partition)
+  int max_fronts = 16;          // fronts per solve launch (co-resident clusters / G)
   int L = 0;                    // local cyclic-reduction levels before the dense top
   int q = 1;                    // blocks left per chunk after L levels (dense inverse)
   int mmax = 0;                 // largest chunk (face points)
-  int y0s[17] = {};             // chunk boundaries (C + 1 entries)
+  int y0s[65] = {};             // chunk boundaries (G * C + 1 entries)
   int kstride = 0;              // kept-block records per chunk
   const Stencil* coarse = nullptr;
   double2* ef = nullptr;        // [J][M][tm^2]          Dinv at each block's elimination level
@@ -55,6 +63,7 @@ struct Sweep {
   double2* sp = nullptr;        // [J][M][2][tm^2]       spikes W, V of every block
   double2* rk = nullptr;        // [J][C][2(C-1)][2 tm^2] rows of the reduced-system inverse
   double2* qd = nullptr;        // [J][C][q][q][tm^2]    inverse of the level-L reduced chunk system
+  double2* x2 = nullptr;        // [J][GC][xstride][tm^2] level-2 blocks (packing only)
   double2* stream = nullptr;    // [J][C][nbs][tm^2]     all of the above in solve order (setup frees the rest)
   long long nbs = 0;            // blocks per (slab, chunk) stream
   uint32_t* ptab = nullptr;     // [C][plan words] solve-kernel item / chunk tables
@@ -65,6 +74,7 @@ struct Sweep {
   double2* trace = nullptr;     // [ntrace][2][M] interface traces
   double2* g = nullptr;         // [n0*M] mid-sweep residual
   double2* u2 = nullptr;        // [n0*M] second-pass contributions
+  SweepWork own;                // this sweep's own work set (trace/g/u2 + level-2 exchange)
   SweepTask* d_tasks = nullptr;
   std::vector<SweepTask> tasks;
   // launch plans by variant id: HS_VARIANT_UD, HS_VARIANT_X, then one per NX

@@ -116,6 +116,48 @@ __global__ void k3_rhs(SweepTask t, int n0, int n1, int n2, const double2* __res
   F[(int64_t)i1 * NB + r] = v;
 }
 
+// w_i = Dinv_i f_i for every plane i1 (row-major Dinv): the slab solve's
+// first step, independent of the block recursion.  One CTA per 32 rows of a
+// plane; each warp owns 4 rows (4 independent accumulators, 16-B lane loads
+// of contiguous row segments), the plane's f is staged in shared memory.
+// HBM-bound: n1 NB^2 16 B per call.  Fixed reduction order (bitwise
+// reproducible).
+constexpr int kGvRows = 32;
+__global__ void __launch_bounds__(256) k3_gemv(const double2* __restrict__ Dinv,
+                                              const double2* __restrict__ F, double2* __restrict__ Y,
+                                              int NB) {
+  extern __shared__ __align__(16) double2 fv[];
+  const int i1 = blockIdx.y;
+  const int64_t nb2 = (int64_t)NB * NB;
+  const double2* f = F + (int64_t)i1 * NB;
+  for (int c = threadIdx.x; c < NB; c += blockDim.x) fv[c] = __ldg(f + c);
+  __syncthreads();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int r0 = blockIdx.x * kGvRows + warp * 4;
+  const double2* A = Dinv + (int64_t)i1 * nb2;
+  double2 acc[4] = {czero(), czero(), czero(), czero()};
+  const int nr = max(0, min(4, NB - r0));
+  if (nr == 4) {
+    const double2* a0 = A + (int64_t)r0 * NB;
+    for (int c = lane; c < NB; c += 32) {
+      const double2 v = fv[c];
+      acc[0] = cfma(__ldcs(a0 + c), v, acc[0]);
+      acc[1] = cfma(__ldcs(a0 + NB + c), v, acc[1]);
+      acc[2] = cfma(__ldcs(a0 + 2 * NB + c), v, acc[2]);
+      acc[3] = cfma(__ldcs(a0 + 3 * NB + c), v, acc[3]);
+    }
+  } else {
+    for (int k = 0; k < nr; ++k) {
+      const double2* a = A + (int64_t)(r0 + k) * NB;
+      for (int c = lane; c < NB; c += 32) acc[k] = cfma(__ldcs(a + c), fv[c], acc[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    for (int m = 16; m > 0; m >>= 1) acc[k] = cadd(acc[k], shfl_xor_c(acc[k], m));
+  if (lane < nr) Y[(int64_t)i1 * NB + r0 + lane] = acc[lane];
+}
+
 // u rows [ta, tb) and the outgoing traces (subdom_solve steps 4-5)
 __global__ void k3_out(SweepTask t, int n1, int n2, const double2* __restrict__ X,
                        double2* __restrict__ u, double2* __restrict__ trace) {
@@ -542,8 +584,6 @@ int sweep3_tasks(Ctx* c, Sweep* s, const SweepTask* const* ts, int nt, const dou
   } else {
     nbuf[0] = s3->nbuf;
   }
-  cublasSetStream(s3->blas, c->stream);
-  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
   size_t smem = 0;
   K3Chain ch[2] = {};
   for (int k = 0; k < nt; ++k) {
@@ -554,14 +594,11 @@ int sweep3_tasks(Ctx* c, Sweep* s, const SweepTask* const* ts, int nt, const dou
     k3_rhs<<<(unsigned)((tot + kT3 - 1) / kT3), kT3, 0, c->stream>>>(
         t, s->n0, n1, n2, src, coarse_coeffs, coarse_n, to_slots(s3->cslot), s->trace, s3->F[k]);
     HS_LAUNCH_CHECK(c, "3-D rhs");
-    {   // w_i = Dinv_i f_i for every plane: one batched GEMV (Dinv stored row-major
+    {   // w_i = Dinv_i f_i for every plane: one batched GEMV (Dinv stored row-major)
       ProfScope ps(c, K_SWEEP_GATHER, (double)n1 * nb2 * 16.0);
-      if (cublasZgemvStridedBatched(s3->blas, CUBLAS_OP_T, nb, nb, &one,
-                                    (const cuDoubleComplex*)s3->dinv[j], nb, (long long)nb2,
-                                    (const cuDoubleComplex*)s3->F[k], 1, nb, &zero,
-                                    (cuDoubleComplex*)s3->Y[k], 1, nb, n1) != CUBLAS_STATUS_SUCCESS)
-        return set_error(c, HS_E_CUDA, "3-D batched GEMV failed");
-      c->launches++;
+      k3_gemv<<<dim3((unsigned)((nb + kGvRows - 1) / kGvRows), (unsigned)n1), 256,
+                (size_t)nb * sizeof(double2), c->stream>>>(s3->dinv[j], s3->F[k], s3->Y[k], nb);
+      HS_LAUNCH_CHECK(c, "3-D batched GEMV");
     }
     ch[k] = K3Chain{s3->T[j], s3->gf[j], s3->xf[j], s3->Y[k], s3->gbar + k, nbuf[k]};
     smem = std::max(smem, k3_smem(nb, nt == 2 ? (k ? G - g0 : g0) : G, nbuf[k]));

@@ -27,7 +27,8 @@ def to_device(x, n: int | None = None, ctx=None):
     ctx = ctx or context()
     if isinstance(x, torch.Tensor):
         t = x
-        if t.device.type != "cuda" or t.dtype != torch.complex128 or not t.is_contiguous():
+        if (t.device.type != "cuda" or t.device.index != ctx.device
+                or t.dtype != torch.complex128 or not t.is_contiguous()):
             t = t.to(device=f"cuda:{ctx.device}", dtype=torch.complex128).contiguous()
         t = t.reshape(-1)
         was_np = False
@@ -213,6 +214,19 @@ class DeviceSweep(_Handle):
     @property
     def factor_bytes(self) -> int:
         return int(self.ctx.lib.hs_sweep_factor_bytes(self.h))
+
+    @property
+    def segments(self) -> int:
+        """face segments per front (two-level partition; 1 = one cluster)"""
+        return int(self.ctx.lib.hs_sweep_segments(self.h))
+
+    @property
+    def chunks(self) -> int:
+        return int(self.ctx.lib.hs_sweep_chunks(self.h))
+
+    def launches_per_apply(self, variant="x") -> int:
+        """slab-solve launches of one application of the variant's plan"""
+        return int(self.ctx.lib.hs_sweep_plan_launches(self.h, self.variant_id(variant)))
 
     def variant_id(self, variant="x", cells=None) -> int:
         """C-ABI variant id: HS_VARIANT_X / HS_VARIANT_UD, or the plan of an

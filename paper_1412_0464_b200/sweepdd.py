@@ -84,14 +84,56 @@ def coarse_level(mesh_c: Mesh, cmap: CoarseningMap, model_c: WaveModel, op=None,
 
 
 # ---------------------------------------------------------------------------
-# transmission (data view; the device reads the global operator rows directly)
+# transmission (the sweep kernels read the global operator rows directly;
+# this object is the drop-in view, reference sweepdd.py:98-141)
 
 @dataclass
 class TransmissionMatrix:
+    """Two-layer interface map of the global operator at layers (b, b+1)
+    (reference ``sweepdd.py:98-118``): ``apply(buf)`` returns
+    ``[sign * A[b, b+1] buf[1], -sign * A[b+1, b] buf[0]]`` -- the face
+    blocks applied as (d-1)-dimensional compact stencils on the GPU."""
+
     point: int
     block01: dict
     block10: dict
     sign: int
+
+    def _face_ops(self, face):
+        """device stencils of the two blocks, the sign folded into the
+        coefficients (exact: a negation)"""
+        ops = self.__dict__.get("_dev")
+        if ops is None or ops[0] != face:
+            from .device import DeviceStencil
+            shape = face if face else (1,)
+            dev = []
+            for blk, sg in ((self.block01, self.sign), (self.block10, -self.sign)):
+                offs = sorted(blk) or [(0,) * len(face)]
+                co = [np.broadcast_to(np.asarray(blk[o], dtype=complex), face).reshape(-1) * sg
+                      if o in blk else np.zeros(int(np.prod(shape)), complex) for o in offs]
+                offs = [o if face else (0,) for o in offs]
+                dev.append(DeviceStencil(shape, offs, np.stack(co)))
+            ops = (face, dev[0], dev[1])
+            self.__dict__["_dev"] = ops
+        return ops[1], ops[2]
+
+    def apply(self, buf):
+        """out[0] = sign * A[b,:;b+1,:] buf[1], out[1] = -sign * A[b+1,:;b,:] buf[0]
+        (two face-stencil applications on the device).  numpy in -> numpy out;
+        a torch CUDA tensor in -> tensor out."""
+        import torch
+        is_t = isinstance(buf, torch.Tensor)
+        shp = tuple(buf.shape) if is_t else np.shape(np.asarray(buf))
+        if len(shp) < 1 or shp[0] != 2:
+            raise ValueError(f"transmission buffer must have 2 layers, got shape {shp}")
+        face = tuple(int(v) for v in shp[1:])
+        d01, d10 = self._face_ops(face)
+        b = buf if is_t else np.asarray(buf, dtype=complex)
+        o0 = d01.apply(b[1].reshape(-1) if is_t else np.ascontiguousarray(b[1]).ravel())
+        o1 = d10.apply(b[0].reshape(-1) if is_t else np.ascontiguousarray(b[0]).ravel())
+        if is_t:
+            return torch.stack([o0, o1]).reshape(shp)
+        return np.stack([np.asarray(o0), np.asarray(o1)]).reshape(shp)
 
     def dense(self):
         """Full 2m x 2m matrix (small sizes only; inspection helper)."""

@@ -301,8 +301,13 @@ def solve_many(cycle: TwoGridCycle, rhs, config=None, lanes: int = 4, orth: str 
 
 
 def _lane_capable(cycle: TwoGridCycle) -> bool:
-    """Lanes need a 2-D sweep coarse solver (private sweep scratch per lane)."""
-    return isinstance(cycle.coarse_solver, SweepCoarseSolver) and cycle.coarse_op.dim == 2
+    """Lanes need a 2-D sweep coarse solver (private sweep scratch per lane)
+    with one cluster per front: the G clusters of a two-level-partition front
+    wait on each other, so concurrent lanes could starve one another of
+    co-resident clusters."""
+    if not (isinstance(cycle.coarse_solver, SweepCoarseSolver) and cycle.coarse_op.dim == 2):
+        return False
+    return cycle.hierarchy.partition.device().segments == 1
 
 
 def vcycle(cycle: TwoGridCycle, f):

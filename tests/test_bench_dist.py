@@ -41,14 +41,30 @@ def test_bench_rank_logic_gloo(tmp_path):
     mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
                        join=True, start_method="spawn")
     res = [json.loads((tmp_path / f"r{r}.json").read_text()) for r in range(world)]
-    # right-hand sides: disjoint, complete cover; single rhs -> replicas
+    # right-hand sides: disjoint, complete cover; a single rhs is solved by
+    # one rank only (no replicas counted twice -- single-rhs configs shard)
     assert sorted(res[0]["mine"] + res[1]["mine"]) == list(range(8))
     assert not set(res[0]["mine"]) & set(res[1]["mine"])
-    assert res[0]["replica"] == res[1]["replica"] == [0]
+    assert res[0]["replica"] == [0] and res[1]["replica"] == []
     for r in res:
         assert r["ms"] == 15.0                      # max over ranks (slowest rank)
         assert r["solves"] == 24                    # 3 steps x 8 rhs over both ranks
         assert r["value"] == pytest.approx(1000 * 24 / 0.015)
+
+
+def test_bench_single_rhs_multi_rank_shards():
+    """bench.py --gpus N on a single-right-hand-side config selects the
+    sharded (strong-scaling) solve, and both arms print identical config
+    objects."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from paper_1412_0464_b200.configs import config
+    p = config(0)
+    args = type("A", (), {"scale": 1, "config": 0})()
+    c1, c2 = bench.bench_config(p, args, 2), bench.bench_config(p, args, 2)
+    assert c1 == c2 and c1["parallelism"] == "sweep-axis shards x2"
+    assert bench.bench_config(config(3, 8), args, 2)["parallelism"] == "rhs across 2 ranks"
+    assert bench.reference_iterations(p, args) == 9
 
 
 def test_bench_single_rank_identity():
