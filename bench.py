@@ -401,6 +401,9 @@ def run_ours(args):
         held = None
     with ClockSampler(local, args.clock_sampler) as clk:
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        # ncu --profile-from-start off captures exactly the timed region
+        # (cudaProfilerStart/Stop are no-ops without a profiler attached)
+        torch.cuda.cudart().cudaProfilerStart()
         ev0.record(stream)
         evs[0].record(stream)
         for s in range(args.steps):
@@ -409,6 +412,7 @@ def run_ours(args):
             evs[s + 1].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
     launches = ctx.launches - launches0
     if world > 1:
         torch.distributed.barrier()

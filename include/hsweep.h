@@ -185,6 +185,16 @@ int hs_sweep_solve_one(hs_ctx* ctx, hs_sweep* s, int j, int64_t a, int64_t b, in
  * hs_cycle_create with HS_VARIANT_UD for a two-grid cycle with an exact
  * coarse solve.  Fails with HS_E_ZERO_PIVOT on a singular pivot block. */
 int hs_exact_create(hs_ctx* ctx, const hs_stencil* op, hs_sweep** out);
+/* Exact solver of a general sparse n x n matrix given as host CSR (indptr
+ * [n+1], indices [nnz], interleaved complex128 values [nnz]) -- replaces
+ * Factorization(matrix) / factorize(scipy matrix), sparselin.py:40-68.
+ * block >= the matrix bandwidth max|i - j|: the matrix is factorised as
+ * block tridiagonal over ceil(n / block) block rows (padded with identity
+ * rows); vectors passed to hs_sweep_apply(HS_VARIANT_UD) hold
+ * ceil(n / block) * block entries (padding in = 0).  HS_E_ZERO_PIVOT on a
+ * singular pivot block, HS_E_SHAPE when the bandwidth exceeds block. */
+int hs_exact_create_csr(hs_ctx* ctx, int64_t n, int64_t nnz, const int64_t* indptr,
+                        const int64_t* indices, const double* vals, int block, hs_sweep** out);
 /* bytes of device memory held by the slab factors (diagnostic) */
 long long hs_sweep_factor_bytes(hs_sweep* s);
 /* slab-solve launches in one application of a variant's plan (diagnostic:

@@ -439,6 +439,16 @@ int hs_exact_create(hs_ctx* c, const hs_stencil* op, hs_sweep** out) {
   return HS_OK;
 }
 
+int hs_exact_create_csr(hs_ctx* c, int64_t n, int64_t nnz, const int64_t* indptr,
+                        const int64_t* indices, const double* vals, int block, hs_sweep** out) {
+  if (!c || !indptr || (nnz > 0 && (!indices || !vals)) || !out) return HS_E_ARG;
+  Sweep* s = nullptr;
+  int r = exact_create_csr(c, n, nnz, indptr, indices, (const double2*)vals, block, &s);
+  if (r) return r;
+  *out = reinterpret_cast<hs_sweep*>(s);
+  return HS_OK;
+}
+
 int hs_sweep_destroy(hs_ctx* c, hs_sweep* s) {
   (void)c;
   sweep_destroy(s);

@@ -2296,6 +2296,9 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     cudaError_t e = cudaMalloc((void**)&s->trace, (size_t)std::max(1, ntin) * 2 * s->M * sizeof(double2));
     if (e == cudaSuccess) e = cudaMalloc((void**)&s->g, (size_t)s->n0 * s->M * sizeof(double2));
     if (e == cudaSuccess) e = cudaMalloc((void**)&s->u2, (size_t)s->n0 * s->M * sizeof(double2));
+    s->own.trace = s->trace;   // the sweep's own work set (the default of sweep_apply)
+    s->own.g = s->g;
+    s->own.u2 = s->u2;
     return e == cudaSuccess ? HS_OK : check_cuda(c, e, "sweep buffers");
   };
   if (coarse->dim == 3) {   // block-LU slabs along face axis 1 (hs_sweep3.cu)
@@ -2306,7 +2309,7 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     s->coarse = coarse;
     const int ntin = std::max(4, build_schedule(s, J, beta, bt, lo, hi));
     s->ntrace = ntin;
-    int r = sweep3_create(c, s, coarse, slabs, lo, hi);
+    int r = sweep3_create(c, s, coarse, slabs, lo, hi, nullptr);
     if (!r) r = buffers(s, ntin);
     if (!r)
       for (auto& plan : s->plan) plan_bytes(s, plan);

@@ -110,8 +110,15 @@ int sweep_solve_one(Ctx* c, Sweep* s, int j, int64_t a, int64_t b, int64_t ta, i
 int sweep_work_create(Ctx* c, const Sweep* s, SweepWork* w);
 void sweep_work_destroy(SweepWork* w);
 
+// general sparse matrix rows (device CSR) for the exact solver's blocks
+struct CsrSource {
+  const int64_t* indptr = nullptr;
+  const int64_t* indices = nullptr;
+  const double2* vals = nullptr;
+  int64_t n = 0;
+};
 int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const* slabs,
-                  const int64_t* lo, const int64_t* hi);
+                  const int64_t* lo, const int64_t* hi, const CsrSource* csr);
 int sweep3_task(Ctx* c, Sweep* s, const SweepTask& t, const double2* src, double2* const* u,
                 const double2* coarse_coeffs, int64_t coarse_n);
 // one or two independent slab solves (two sweep fronts) in one chain launch
@@ -123,5 +130,9 @@ void sweep3_destroy(Sweep3* s3);
 // (hs_sweep3.cu) behind the sweep interface -- plan HS_VARIANT_UD is a single
 // slab solve over every row.
 int exact_create(Ctx* c, const Stencil* op, Sweep** out);
+// the same for a general sparse matrix in host CSR with block size NB >= its
+// bandwidth (factorize(scipy matrix)); vectors hold ceil(n / NB) * NB entries
+int exact_create_csr(Ctx* c, int64_t n, int64_t nnz, const int64_t* indptr, const int64_t* indices,
+                     const double2* vals, int NB, Sweep** out);
 
 }  // namespace hs

@@ -77,6 +77,30 @@ __global__ void k3_block(const double2* __restrict__ coef, Slots sl, int T, int 
     }
 }
 
+// dense block (o1 = -1, 0, +1 of block row i1) of a general sparse matrix
+// given in CSR, as the exact solver of factorize(scipy matrix) sees it: a
+// banded matrix cut into NB x NB blocks is block tridiagonal (NB >= the
+// bandwidth).  Rows past n (padding of the last block) are identity rows.
+// One thread per row of the block (no write races); duplicates summed.
+__global__ void k3_csr_block(const int64_t* __restrict__ indptr, const int64_t* __restrict__ indices,
+                             const double2* __restrict__ vals, int64_t n, int NB, int n1, int i1,
+                             int o1, double2* __restrict__ A) {
+  const int r = blockIdx.x * kT3 + threadIdx.x;
+  if (r >= NB || i1 + o1 < 0 || i1 + o1 >= n1) return;
+  const int64_t row = (int64_t)i1 * NB + r;
+  if (row >= n) {
+    if (o1 == 0) A[r + (int64_t)r * NB] = make_double2(1.0, 0.0);
+    return;
+  }
+  const int64_t cb0 = (int64_t)(i1 + o1) * NB;
+  for (int64_t e = indptr[row]; e < indptr[row + 1]; ++e) {
+    const int64_t col = indices[e] - cb0;
+    if (col < 0 || col >= NB) continue;
+    double2& a = A[r + col * NB];
+    a = cadd(a, vals[e]);
+  }
+}
+
 __global__ void k3_eye(double2* __restrict__ A, int NB) {
   const int64_t i = (int64_t)blockIdx.x * kT3 + threadIdx.x;
   if (i >= (int64_t)NB * NB) return;
@@ -406,7 +430,7 @@ void sweep3_destroy(Sweep3* s3) {
 // Factorise every slab (block LU along face axis 1).  `s` already holds J,
 // n0, M and the schedules.
 int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const* slabs,
-                  const int64_t* lo, const int64_t* hi) {
+                  const int64_t* lo, const int64_t* hi, const CsrSource* csr) {
   Sweep3* s3 = new Sweep3();
   s->s3 = s3;
   s3->n1 = (int)coarse->shape[1];
@@ -450,6 +474,17 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
                         zero = make_cuDoubleComplex(0.0, 0.0);
   s3->T.resize(J);
   s3->slot.resize(J);
+  // dense blocks of a slab: from its stencil coefficients, or (exact solve of
+  // a general sparse matrix) from the CSR rows of the block row
+  auto block = [&](const double2* cf, const Slots& sl, int T, int NB, int i1, int o1, double2* A) {
+    const unsigned gb = (unsigned)((NB + kT3 - 1) / kT3);
+    if (csr)
+      k3_csr_block<<<gb, kT3, 0, c->stream>>>(csr->indptr, csr->indices, csr->vals, csr->n, NB, n1,
+                                              i1, o1, A);
+    else
+      k3_block<<<gb, kT3, 0, c->stream>>>(cf, sl, T, n1, n2, i1, o1, A);
+    c->launches++;
+  };
   for (int j = 0; j < J; ++j) {
     const Stencil* op = slabs[j];
     const int T = (int)(hi[j] - lo[j] + 1), NB = T * n2;
@@ -459,9 +494,11 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
     if (int r = slots3(op, s3->slot[j], c)) return done(r);
     double2* cf = nullptr;
     const size_t cb = (size_t)op->d.S * op->d.n * sizeof(double2);
-    S3_TRY(cudaMalloc((void**)&cf, cb), "slab coefficients");
+    if (cb) {
+      S3_TRY(cudaMalloc((void**)&cf, cb), "slab coefficients");
+      S3_TRY(cudaMemcpyAsync(cf, op->d.coeffs, cb, cudaMemcpyDeviceToDevice, c->stream), "copy");
+    }
     s3->coef.push_back(cf);
-    S3_TRY(cudaMemcpyAsync(cf, op->d.coeffs, cb, cudaMemcpyDeviceToDevice, c->stream), "copy");
     double2 *dv = nullptr, *xv = nullptr;
     const size_t nb2 = (size_t)NB * NB;
     S3_TRY(cudaMalloc((void**)&dv, n1 * nb2 * sizeof(double2)), "3-D slab factors (Dinv)");
@@ -474,15 +511,12 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
     s3->gf.push_back(gv);
     s3->bytes += (long long)(3 * n1 - 2) * nb2 * sizeof(double2);
     const Slots sl = to_slots(s3->slot[j]);
-    const unsigned gb = (unsigned)((NB + kT3 - 1) / kT3);
     for (int i1 = 0; i1 < n1; ++i1) {
       S3_TRY(cudaMemsetAsync(D, 0, nb2 * sizeof(double2), c->stream), "memset");
-      k3_block<<<gb, kT3, 0, c->stream>>>(cf, sl, T, n1, n2, i1, 0, D);
-      c->launches++;
+      block(cf, sl, T, NB, i1, 0, D);
       if (i1 > 0) {   // D' = D - L_i X_{i-1}
         S3_TRY(cudaMemsetAsync(Lb, 0, nb2 * sizeof(double2), c->stream), "memset");
-        k3_block<<<gb, kT3, 0, c->stream>>>(cf, sl, T, n1, n2, i1, -1, Lb);
-        c->launches++;
+        block(cf, sl, T, NB, i1, -1, Lb);
         S3_BLAS(cublasZgemm(s3->blas, CUBLAS_OP_N, CUBLAS_OP_N, NB, NB, NB, &mone,
                             (cuDoubleComplex*)Lb, NB, (cuDoubleComplex*)Xc, NB,
                             &one, (cuDoubleComplex*)D, NB), "zgemm");
@@ -510,8 +544,7 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
       }
       if (i1 + 1 < n1) {   // X_i = Dinv_i U_i
         S3_TRY(cudaMemsetAsync(U, 0, nb2 * sizeof(double2), c->stream), "memset");
-        k3_block<<<gb, kT3, 0, c->stream>>>(cf, sl, T, n1, n2, i1, 1, U);
-        c->launches++;
+        block(cf, sl, T, NB, i1, 1, U);
         S3_BLAS(cublasZgemm(s3->blas, CUBLAS_OP_N, CUBLAS_OP_N, NB, NB, NB, &one,
                             (cuDoubleComplex*)Di, NB, (cuDoubleComplex*)U, NB, &zero,
                             (cuDoubleComplex*)Xc, NB), "zgemm");
@@ -690,13 +723,99 @@ int exact_create(Ctx* c, const Stencil* op, Sweep** out) {
   fl.ffirst[0] = 0;
   fl.fcount[0] = 1;
   const Stencil* slabs[1] = {v};
-  int r = sweep3_create(c, s, v, slabs, &lo, &hi);
+  int r = sweep3_create(c, s, v, slabs, &lo, &hi, nullptr);
   if (r) {
     sweep_destroy(s);
     return r;
   }
   fl.bytes = (2.0 * sh[1] - 1.0) * (double)sh[0] * sh[2] * (double)sh[0] * sh[2] * 16.0 +
              32.0 * (double)sh[0] * sh[1] * sh[2];
+  s->plan[HS_VARIANT_UD].push_back(fl);
+  *out = s;
+  return HS_OK;
+}
+
+// exact solver of a general sparse n x n matrix (factorize(scipy matrix),
+// sparselin.py:65-68): CSR rows on the device, cut into NB x NB blocks with
+// NB >= the matrix bandwidth, so the matrix is block tridiagonal over
+// nb = ceil(n / NB) block rows; the same block LU and chain kernel as a
+// slab, on the view (T = 1, n1 = nb, n2 = NB) padded with identity rows.
+// Vectors passed to the solve hold nb * NB entries.
+int exact_create_csr(Ctx* c, int64_t n, int64_t nnz, const int64_t* indptr, const int64_t* indices,
+                     const double2* vals, int NB, Sweep** out) {
+  if (n < 1 || NB < 1 || nnz < 0) return set_error(c, HS_E_ARG, "empty matrix");
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
+      const int64_t j = indices[e];
+      if (j < 0 || j >= n) return set_error(c, HS_E_SHAPE, "column index out of range");
+      if (j / NB - i / NB > 1 || i / NB - j / NB > 1)
+        return set_error(c, HS_E_SHAPE, "matrix bandwidth exceeds the block size");
+    }
+  const int64_t nb = (n + NB - 1) / NB;
+  if (nb > (int64_t)1 << 30) return set_error(c, HS_E_SHAPE, "too many block rows");
+  CsrSource src{};
+  src.n = n;
+  cudaError_t e = cudaMalloc((void**)&src.indptr, (n + 1) * sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&src.indices, std::max<int64_t>(1, nnz) * sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&src.vals, std::max<int64_t>(1, nnz) * sizeof(double2));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync((void*)src.indptr, indptr, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                        c->stream);
+  if (e == cudaSuccess && nnz)
+    e = cudaMemcpyAsync((void*)src.indices, indices, nnz * sizeof(int64_t), cudaMemcpyHostToDevice,
+                        c->stream);
+  if (e == cudaSuccess && nnz)
+    e = cudaMemcpyAsync((void*)src.vals, vals, nnz * sizeof(double2), cudaMemcpyHostToDevice, c->stream);
+  auto release = [&]() {
+    cudaStreamSynchronize(c->stream);
+    cudaFree((void*)src.indptr);
+    cudaFree((void*)src.indices);
+    cudaFree((void*)src.vals);
+  };
+  if (e != cudaSuccess) {
+    release();
+    return check_cuda(c, e, "CSR upload");
+  }
+  Stencil* v = new Stencil();
+  v->dim = 3;
+  v->shape[0] = 1; v->shape[1] = nb; v->shape[2] = NB;
+  v->d.n0 = 1; v->d.n1 = nb; v->d.n2 = NB;
+  v->d.n = nb * NB;
+  v->d.S = 0;
+  v->d.diag = -1;
+  Sweep* s = new Sweep();
+  s->view = v;
+  s->J = 1;
+  s->n0 = 1;
+  s->M = (int)(nb * NB);
+  s->coarse = v;
+  const int64_t lo = 1, hi = 1;
+  SweepTask t{};
+  t.slab = 0;
+  t.lo = 1;
+  t.T = 1;
+  t.a = 0;
+  t.b = 1;
+  t.ta = 0;
+  t.tb = 1;
+  t.tin1 = t.tin3 = t.out2 = t.out4 = -1;
+  t.row1 = t.row3 = t.orow2 = t.orow4 = -1;
+  t.dst = 0;
+  s->tasks.push_back(t);
+  SweepLaunch fl{};
+  fl.kind = SweepLaunch::kSolve;
+  fl.src = 0;
+  fl.nfront = 1;
+  fl.ffirst[0] = 0;
+  fl.fcount[0] = 1;
+  const Stencil* slabs[1] = {v};
+  int r = sweep3_create(c, s, v, slabs, &lo, &hi, &src);
+  release();
+  if (r) {
+    sweep_destroy(s);
+    return r;
+  }
+  fl.bytes = (2.0 * nb - 1.0) * (double)NB * NB * 16.0 + 32.0 * (double)nb * NB;
   s->plan[HS_VARIANT_UD].push_back(fl);
   *out = s;
   return HS_OK;

@@ -255,6 +255,44 @@ class DeviceSweep(_Handle):
         return u, was_np
 
 
+class DeviceExactCSR(_Handle):
+    """Exact solver of a general sparse matrix (hs_exact_create_csr): its CSR
+    rows cut into block rows of ``block`` >= bandwidth unknowns, factorised as
+    a block-tridiagonal chain on the device."""
+
+    _destroy = "hs_sweep_destroy"
+
+    def __init__(self, csr, ctx=None):
+        self.ctx = ctx or context()
+        a = csr.tocsr().astype(complex)
+        a.sum_duplicates()
+        self.n = int(a.shape[0])
+        coo = a.tocoo()
+        bw = int(np.abs(coo.row.astype(np.int64) - coo.col.astype(np.int64)).max()) if a.nnz else 0
+        self.block = max(1, bw)
+        self.n_pad = -(-self.n // self.block) * self.block
+        ip, pip = i64(a.indptr)
+        ix, pix = i64(a.indices)
+        vals = np.ascontiguousarray(a.data, dtype=complex)
+        h = C.c_void_p()
+        self.ctx.call("hs_exact_create_csr", self.n, int(a.nnz), pip, pix,
+                      vals.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)),
+                      self.block, C.byref(h))
+        self.h = h
+
+    def apply(self, f):
+        """x = A^{-1} f (flat, n entries); returns (tensor, was_numpy)."""
+        torch = _torch()
+        ft, was_np = to_device(f, self.n, self.ctx)
+        if self.n_pad != self.n:
+            fp = torch.zeros(self.n_pad, dtype=torch.complex128, device=ft.device)
+            fp[:self.n] = ft
+            ft = fp
+        u = empty(self.n_pad, self.ctx)
+        self.ctx.call("hs_sweep_apply", self.h, _lib.HS_VARIANT_UD, ptr(ft), ptr(u))
+        return (u[:self.n] if self.n_pad != self.n else u), was_np
+
+
 class DeviceExact(_Handle):
     """Exact solver of a whole stencil operator (hs_exact_create): one block-LU
     slab behind the sweep interface (variant HS_VARIANT_UD)."""

@@ -58,10 +58,18 @@ class Factorization:
     pivot block (sparselin.py:53-56)."""
 
     def __init__(self, op):
-        from .device import DeviceExact
+        from .device import DeviceExact, DeviceExactCSR
+        if sp.issparse(op) or isinstance(op, np.ndarray):
+            a = sp.csr_matrix(op, dtype=complex)
+            if a.shape[0] != a.shape[1]:
+                raise ValueError("matrix must be square")
+            self.shape = (int(a.shape[0]),)
+            self.n = self.shape[0]
+            self.device = DeviceExactCSR(a)
+            return
         if not hasattr(op, "device") or not hasattr(op, "shape"):
-            raise TypeError("factorize on the device takes a StencilOperator "
-                            f"(compact stencil), got {type(op).__name__}")
+            raise TypeError("factorize takes a StencilOperator or a scipy sparse matrix, "
+                            f"got {type(op).__name__}")
         self.shape = tuple(op.shape)
         self.n = int(np.prod(self.shape))
         self.device = DeviceExact(op.device())
@@ -95,10 +103,40 @@ def _stack(cols):
 
 
 def factorize(matrix) -> Factorization:
-    """Factorization of a stencil operator (sparselin.py:65-68)."""
+    """Factorization of a stencil operator or a scipy sparse matrix
+    (sparselin.py:65-68); both are factorised on the device."""
     return Factorization(matrix)
 
 
 def solve_factored(factor: Factorization, rhs):
     """Solve for one vector or a block of right-hand sides (sparselin.py:71-76)."""
     return factor.solve(rhs)
+
+
+_DENSE_CAP = 10_000
+
+
+def dense_solve(op, rhs):
+    """Dense LU solve of a small operator, the reference's ground-truth
+    checker (sparselin.py:79-87): the operator densified from its CSR rows
+    and solved on the device (torch.linalg.solve); capped at 10 000
+    unknowns so that it stays a checker, not a solver."""
+    import torch
+    n = int(np.prod(op.shape)) if hasattr(op, "coeffs") else int(op.shape[0])
+    if n > _DENSE_CAP:
+        raise ValueError(f"dense oracle capped at {_DENSE_CAP} unknowns, got {n}")
+    a = (to_csr(op) if hasattr(op, "coeffs") else sp.csr_matrix(op)).toarray()
+    b = np.asarray(rhs, dtype=complex).reshape(n, -1)
+    from ._lib import context
+    dev = f"cuda:{context().device}"
+    x = torch.linalg.solve(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)).cpu().numpy()
+    return x[:, 0] if b.shape[1] == 1 else x
+
+
+def write_matrix_market(path, matrix):
+    """Matrix Market coordinate dump, complex general, 1-based
+    (sparselin.py:90-94; host file I/O of the assembled matrix)."""
+    import scipy.io
+    if hasattr(matrix, "coeffs"):
+        matrix = to_csr(matrix)
+    scipy.io.mmwrite(path, matrix, field="complex")

@@ -25,8 +25,8 @@ import numpy as np
 
 from .discretize import (StencilOperator, WaveModel, assemble_fe_pml_coarse, assemble_fine,
                          assemble_opt_fd_coarse, assemble_sponge, default_table,
-                         interior_spacing, subdomain_fd_operator, subdomain_fe_operator,
-                         _nodes_to_cells)
+                         interior_spacing, robin1d_operator, subdomain_fd_operator,
+                         subdomain_fe_operator, subdomain_robin1d_operator, _nodes_to_cells)
 from .mesh import PML, SPONGE, CoarseningMap, Mesh
 
 
@@ -39,6 +39,8 @@ class HelmholtzLevel:
     cmap: CoarseningMap | None = None
     k_cells: np.ndarray | None = None
     table: object = None
+    k1d: float = 0.0
+    h1d: float = 0.0
 
     fields: object = None   # device wavenumbers (assembly.CoarseFields): slabs assembled on the GPU
 
@@ -54,6 +56,9 @@ class HelmholtzLevel:
         if self.kind == "fe":
             return subdomain_fe_operator(self.mesh, self.model, self.k_cells, self.table,
                                          core_lo, core_hi, w_dd, s_dd, open_left, open_right)
+        if self.kind == "robin1d":
+            return subdomain_robin1d_operator(self.k1d, self.h1d, core_lo, core_hi, open_left,
+                                              open_right)
         raise ValueError(f"unknown level kind {self.kind!r}")
 
 
@@ -62,6 +67,23 @@ def fine_level(mesh: Mesh, model: WaveModel, op: StencilOperator | None = None):
         sponge = any(s.kind == SPONGE for pair in mesh.layers for s in pair)
         op = assemble_sponge(mesh, model) if sponge else assemble_fine(mesh, model)
     return HelmholtzLevel(op, "fd", mesh=mesh, model=model)
+
+
+def robin_level_1d(k: float, h: float, n_cells: int) -> HelmholtzLevel:
+    """The 1-D line of ``n_cells`` cells (n_cells - 1 unknowns) with exact
+    radiating end closures (reference sweepdd.py:90-92): the sweep's
+    known-answer level, solved on the device like the 2-D/3-D levels."""
+    return HelmholtzLevel(robin1d_operator(k, h, n_cells - 1), "robin1d", k1d=k, h1d=h)
+
+
+def _lift_line(op):
+    """A 1-D line operator as the (n, 1, 1) 3-D stencil the device sweep
+    takes (same memory layout; the slab solve is the 3-D block chain with
+    one T x T block per slab)."""
+    if op.dim != 1:
+        return op
+    return StencilOperator((op.shape[0], 1, 1),
+                           {(o[0], 0, 0): c.reshape(-1, 1, 1) for o, c in op.coeffs.items()})
 
 
 def coarse_level(mesh_c: Mesh, cmap: CoarseningMap, model_c: WaveModel, op=None,
@@ -222,9 +244,13 @@ class Partition:
         if self._device is None:
             from .device import DeviceStencil, DeviceSweep
             from .assembly import DeviceOperator
-            coarse = self.level.op.device()
+            if self.level.op.dim == 1:     # the line: lifted to (n, 1, 1)
+                coarse = _lift_line(self.level.op).device()
+            else:
+                coarse = self.level.op.device()
             slab_ops = [sd.op.device() if isinstance(sd.op, DeviceOperator)
-                        else DeviceStencil.from_host(sd.op, coarse.ctx) for sd in self.subs]
+                        else DeviceStencil.from_host(_lift_line(sd.op), coarse.ctx)
+                        for sd in self.subs]
             self._device = DeviceSweep(coarse, self.J, self.beta, self.beta_tilde,
                                        [sd.pt_lo for sd in self.subs],
                                        [sd.pt_hi for sd in self.subs], slab_ops, coarse.ctx)

@@ -44,7 +44,7 @@ def kclass(name):
     return None
 
 
-def main(rep, out_csv, traffic_json="profiles/ncu_traffic.json"):
+def main(rep, out_csv, traffic_json="profiles/ncu_traffic.json", config=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -75,6 +75,8 @@ def main(rep, out_csv, traffic_json="profiles/ncu_traffic.json"):
             traffic.setdefault(cls, []).append(rd + wr)
     open(out_csv, "w").write("\n".join(lines) + "\n")
     tr = {k: sum(v) / len(v) for k, v in traffic.items()}
+    if config is not None:   # BASELINE configs index the capture ran on (bench.py checks it)
+        tr["config"] = int(config)
     json.dump(tr, open(traffic_json, "w"), indent=1)
     print("\n".join(lines))
     print(json.dumps(tr, indent=1))

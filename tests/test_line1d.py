@@ -1,0 +1,143 @@
+"""The 1-D line (robin_level_1d) and factorize() of general sparse matrices:
+the reference's line known-answer tests (test_sweepdd.py:192-210,
+test_acceptance.py:52-71) and SuperLU solves (sparselin.py:40-68), against
+golden vectors made by running the reference (tests/golden/make_line1d.py).
+
+CPU: operator coefficients (bitwise), partition geometry, dense transmission
+matrices.  GPU (through the C ABI): UD/X sweeps on the line vs the
+reference's outputs (1e-10) and the line exactness property (residual
+< 1e-10), general-matrix factorisations vs SuperLU (1e-10), zero pivots.
+"""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from conftest import GOLDEN, crand, rel
+
+LINES = ["a", "b", "c", "d"]
+
+
+@pytest.fixture(scope="module")
+def g():
+    with np.load(GOLDEN / "line1d.npz") as z:
+        return {k: z[k] for k in z.files}
+
+
+def _part(g, key, device=True):
+    import paper_1412_0464_b200 as hb
+    from paper_1412_0464_b200.sweepdd import build_partition
+    n, J, tr = (int(v) for v in g[f"{key}_meta"])
+    level = hb.robin_level_1d(float(g[f"{key}_k"]), 1.0 / n, n)
+    return level, build_partition(level, J=J, tilde_right=bool(tr), device=device)
+
+
+@pytest.mark.parametrize("key", LINES)
+def test_line_setup_matches_reference(g, key):
+    level, part = _part(g, key, device=False)
+    for o in (-1, 0, 1):
+        assert np.array_equal(level.op.coeffs[(o,)], g[f"{key}_op{o:+d}"])
+    assert np.array_equal(part.beta, g[f"{key}_beta"])
+    assert np.array_equal(part.beta_tilde, g[f"{key}_beta_tilde"])
+    assert np.array_equal([[s.pt_lo, s.pt_hi] for s in part.subs], g[f"{key}_lohi"])
+    import paper_1412_0464_b200 as hb
+    assert np.array_equal(hb.extract_transmission(part, 2, "forward").dense(), g[f"{key}_tfwd2"])
+    assert np.array_equal(hb.extract_transmission(part, 1, "backward").dense(), g[f"{key}_tbwd1"])
+
+
+def test_line_transmission_known_answer():
+    """test_sweepdd.py:68-77: forward block [[0, -1/h^2], [1/h^2, 0]], backward = -forward"""
+    import paper_1412_0464_b200 as hb
+    from paper_1412_0464_b200.sweepdd import build_partition
+    n = 40
+    level = hb.robin_level_1d(2 * np.pi * 4, 1.0 / n, n)
+    part = build_partition(level, J=2, device=False)
+    d = hb.extract_transmission(part, 2, "forward").dense()
+    a01 = -(n * n)
+    assert np.allclose(d, [[0, a01], [-a01, 0]])
+    assert np.allclose(hb.extract_transmission(part, 1, "backward").dense(), -d)
+
+
+def test_robin1d_operator_errors():
+    import paper_1412_0464_b200 as hb
+    with pytest.raises(ValueError, match="at least 2"):
+        hb.robin1d_operator(1.0, 0.1, 1)
+    with pytest.raises(ValueError, match="cannot carry"):
+        hb.robin1d_operator(30.0, 0.1, 10)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", LINES)
+def test_line_sweeps_match_reference(g, key):
+    import paper_1412_0464_b200 as hb
+    from paper_1412_0464_b200.sparselin import to_csr
+    level, part = _part(g, key)
+    f = g[f"{key}_f"]
+    a = to_csr(level.op)
+    ux = hb.SweepingPreconditioner(part, "x")(f)
+    uud = hb.SweepingPreconditioner(part, "ud")(f)
+    assert rel(ux, g[f"{key}_ux"]) < 1e-10
+    assert rel(uud, g[f"{key}_uud"]) < 1e-10
+    # the line is exact for constant k (test_sweepdd.py:194-210)
+    for u in (ux, uud):
+        assert np.linalg.norm(f - a @ u) / np.linalg.norm(f) < 1e-10
+
+
+@pytest.mark.gpu
+def test_line_subdom_solve_and_transmission_apply(g):
+    """public slab solve on the line + TransmissionMatrix.apply vs its dense form"""
+    import paper_1412_0464_b200 as hb
+    from paper_1412_0464_b200.sweepdd import forward_sweep, subdom_solve
+    level, part = _part(g, "d")
+    rng = np.random.default_rng(5)
+    f = crand(rng, part.shape)
+    u1 = np.zeros(part.shape, complex)
+    forward_sweep(part, u1, f, 1, 1)
+    u2 = np.zeros(part.shape, complex)
+    subdom_solve(part, u2, f, 1, part.beta[0], part.beta[1], part.beta[0], part.beta[1])
+    assert np.array_equal(u1, u2)
+    assert u1[part.beta[1]:].any() == False  # noqa: E712  (locality)
+    t = hb.extract_transmission(part, 3, "forward")
+    buf = crand(rng, (2,))
+    assert rel(t.apply(buf), t.dense() @ buf) < 1e-14
+
+
+def _csr(g, p):
+    a = sp.csr_matrix((g[p + "_data"], g[p + "_indices"], g[p + "_indptr"]))
+    return a
+
+
+@pytest.mark.gpu
+def test_factorize_scipy_matrices_match_superlu(g):
+    import paper_1412_0464_b200 as hb
+    a = _csr(g, "fine")
+    x = hb.factorize(a).solve(g["fine_b"])
+    assert rel(x, g["fine_x"]) < 1e-10
+    assert np.linalg.norm(a @ x - g["fine_b"]) / np.linalg.norm(g["fine_b"]) < 1e-10
+    band = _csr(g, "band")
+    xb = hb.solve_factored(hb.factorize(band), g["band_b"])
+    assert rel(xb, g["band_x"]) < 1e-10
+
+
+@pytest.mark.gpu
+def test_factorize_scipy_known_answers():
+    """test_sparselin.py:39-62: scalar, hand-solved tridiagonal, zero pivot"""
+    import paper_1412_0464_b200 as hb
+    f = hb.factorize(sp.csc_matrix(np.array([[2.0 + 0j]])))
+    assert abs(f.solve(np.array([4.0 + 0j]))[0] - 2.0) < 1e-15
+    tri = sp.diags([[-1.0] * 2, [2.0] * 3, [-1.0] * 2], [-1, 0, 1], format="csc")
+    assert np.allclose(hb.factorize(tri).solve(np.ones(3, complex)), [1.5, 2.0, 1.5])
+    with pytest.raises(ZeroDivisionError, match="zero pivot"):
+        hb.factorize(sp.csc_matrix(np.array([[1.0, 1.0], [1.0, 1.0]], dtype=complex)))
+    with pytest.raises(ValueError):
+        hb.factorize(tri).solve(np.ones(4, complex))
+
+
+@pytest.mark.gpu
+def test_dense_solve_checker():
+    import paper_1412_0464_b200 as hb
+    op = hb.StencilOperator((3,), {(0,): np.ones(3)})
+    assert np.allclose(hb.dense_solve(op, np.arange(3.0) + 0j), np.arange(3.0))
+    big = hb.StencilOperator((101, 101), {(0, 0): np.ones((101, 101))})
+    with pytest.raises(ValueError, match="capped"):
+        hb.dense_solve(big, np.zeros(big.n))
