@@ -14,7 +14,7 @@ inside the timed region).
                     [--config 2] [--scale 1]
 
 ``--impl reference`` times the CPU oracle port of the reference algorithm
-(oracle/, numpy + scipy SuperLU exactly like the reference, 1 core) on the
+(oracle/, numpy + scipy SuperLU exactly like the reference, 2 host threads: the X sweep's two fronts concurrently) on the
 same config: each step is a bounded sample of whole GMRES iterations,
 projected to a full solve with the reference's own iteration count
 (tests/golden/large_anchors.json, made by running the reference).
@@ -42,6 +42,7 @@ sys.path.insert(0, str(ROOT))
 
 HBM_FALLBACK_GBS = 6650.0   # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
 L2_BYTES = 126 * 2**20
+CPU_CORES = 2               # host threads the CPU oracle uses (the two X-sweep fronts)
 
 
 def parse():
@@ -63,6 +64,9 @@ def parse():
                    help="with --shard on one process: G logical shards on one GPU")
     p.add_argument("--lanes", type=int, default=4,
                    help="multi-RHS configs (C4): right-hand sides in flight at once per GPU")
+    p.add_argument("--segments", type=int, default=-1,
+                   help="face segments per sweep front (-1: 1 when several right-hand sides "
+                        "run as lanes, else automatic)")
     p.add_argument("--clock-sampler", choices=["smi", "nvml", "none"], default="smi")
     p.add_argument("--no-pipeline", action="store_true",
                    help="synchronous Arnoldi loop (A/B against the pipelined default)")
@@ -269,11 +273,13 @@ def cpu_oracle(hh):
     t0 = time.perf_counter()
     tg = orc.from_hierarchy(hh)
     tg.fine.csr, tg.part.op.csr        # assemble the CSR matrices outside the sample
+    if hasattr(tg.part, "parallel"):   # the X sweep's two fronts on two host threads
+        tg.part.parallel = True         # (the reference's prec_x(parallel=True))
     return tg, time.perf_counter() - t0
 
 
 def cpu_sample(problem, tg, its_target, iters):
-    """Bounded sample of the CPU oracle (reference algorithm, 1 core):
+    """Bounded sample of the CPU oracle (reference algorithm, the two X-sweep fronts on two threads):
     ``iters`` whole GMRES(restart) iterations on the config's right-hand
     side (each = one A M v + orthogonalisation) plus the solve's closing
     M dv and residual, timed, then projected per iteration to a solve of
@@ -294,8 +300,9 @@ def _sample_text(r, its_target, source, setup_s):
     return (f"{r['sample_iterations']} GMRES iteration(s) + the closing M dv / residual of the "
             f"numpy/scipy oracle port (SuperLU slab solves like the reference) timed in "
             f"{r['sample_s']:.1f} s, projected per iteration to a {its_target}-iteration solve "
-            f"({source}); oracle setup {setup_s:.0f} s untimed; 1 core used, host has "
-            f"{os.cpu_count()}")
+            f"({source}); oracle setup {setup_s:.0f} s untimed; 2 threads (the X sweep's two "
+            f"fronts run concurrently, the reference's prec_x(parallel=True); the rest is "
+            f"single-threaded like the reference), host has {os.cpu_count()} cores")
 
 
 def run_reference(args):
@@ -330,7 +337,7 @@ def run_reference(args):
         "config": bench_config(p, args, world),
         "projection": True,
         "reference_iterations": its_target,
-        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": 1, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": CPU_CORES, "kind": "port",
                          "sample": _sample_text(med, its_target, source, setup_s)},
         "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -351,20 +358,25 @@ def run_ours(args):
     from paper_1412_0464_b200.configs import config
 
     p = config(args.config, args.scale)
+    nrhs_total = p.f.shape[0]
+    mine = assign_rhs(nrhs_total, world, rank)
+    # several right-hand sides in flight as lanes: one cluster per sweep front
+    # (the lanes' sweeps run side by side); one at a time: the widest layout
+    segments = args.segments if args.segments >= 0 else (
+        1 if len(mine) > 1 and args.lanes > 1 else 0)
     t0 = time.perf_counter()
     keep = (rank == 0 and world == 1 and not args.no_cpu_baseline)
     cycle, _ = hb.build_two_grid(p.mesh, p.model, fine_op=fine_operator(p),
                                  smoother=hb.SmootherConfig(p.omega_jac, p.nu),
                                  coarse="sweep",
                                  sweep=hb.SweepOptions(p.w_dd, p.s_dd, "x",
-                                                       subdomains=p.subdomains),
+                                                       subdomains=p.subdomains,
+                                                       segments=segments),
                                  keep_slab_ops=keep)
     dev = cycle.device()
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
     ctx = context()
-    nrhs_total = p.f.shape[0]
-    mine = assign_rhs(nrhs_total, world, rank)
     f_dev = [torch.from_numpy(p.f[r].ravel()).cuda() for r in mine]
     cfg = hb.GmresConfig(p.tol, p.max_iter, p.restart)
     prec = cycle.as_preconditioner()
@@ -514,7 +526,7 @@ def run_ours(args):
         tg, osetup = cpu_oracle(cycle.hierarchy)
         r = cpu_sample(p, tg, its_t, args.cpu_iters)
         tg = None
-        cpu = {"value": r["value"], "unit": "DOF/s", "cores": 1, "kind": "port",
+        cpu = {"value": r["value"], "unit": "DOF/s", "cores": CPU_CORES, "kind": "port",
                "sample": _sample_text(r, its_t, src, osetup),
                "projected_solve_s": r["projected_solve_s"]}
 
@@ -537,6 +549,7 @@ def run_ours(args):
             "config": bench_config(p, args, world),
             "coarse_dof": int(np.prod(cycle.coarse_op.shape)),
             "slab_factor_bytes": fac,
+            "sweep_segments": dev.sweep.segments if p.mesh.dim == 2 else None,
             "rhs_per_rank": len(f_dev),
             "rhs_in_flight": min(args.lanes, len(f_dev)) if multi else 1,
             "reference_iterations": reference_iterations(p, args),

@@ -47,6 +47,11 @@ typedef struct hs_cycle hs_cycle;
 int hs_ctx_create(int device, hs_ctx** out);
 int hs_ctx_destroy(hs_ctx* ctx);
 int hs_ctx_set_stream(hs_ctx* ctx, void* cuda_stream);
+/* Face segments per sweep front of the 2-D sweeps this context creates next
+ * (two-level partition: one 16-CTA cluster per segment; 0 = automatic, the
+ * widest layout whose clusters co-reside -- the fastest single sweep; 1 = one
+ * cluster per front, which leaves room for concurrent sweep lanes). */
+int hs_ctx_set_sweep_segments(hs_ctx* ctx, int segments);
 const char* hs_last_error(hs_ctx* ctx);
 long long hs_last_error_index(hs_ctx* ctx);
 long long hs_launch_count(hs_ctx* ctx);           /* kernels launched so far */

@@ -238,13 +238,19 @@ class Partition:
         self.backward(u, self.residual(u, f), self.J, 1, B)
         return u
 
+    parallel = False   # run the X sweep's two half-sweeps on two threads
+
     def prec_x(self, f):
-        """sweepdd.py:322-359 (serial schedule)."""
+        """sweepdd.py:322-359; with ``parallel`` the two half-sweeps of each
+        pass run on two threads like the reference's ``parallel=True``
+        (:336-358; disjoint rows of u, results bitwise the serial ones)."""
         if self.J % 2:
             raise ValueError(f"X-sweep needs an even subdomain count, got {self.J}")
         f = np.asarray(f, complex).reshape(self.shape)
         u = np.zeros(self.shape, complex)
         jm = self.J // 2 + 1
+        if self.parallel:
+            return self._prec_x_parallel(f, u, jm)
         B1 = self.forward(u, f, 1, jm - 1)
         B2 = self.backward(u, f, self.J, jm + 1)
         self.solve(u, f, jm, self.beta[jm - 1], self.bt[jm], self.beta[jm - 1], self.bt[jm],
@@ -254,6 +260,22 @@ class Partition:
                             self.beta[jm], out2=True, out4=True)
         self.backward(u, g, jm - 1, 1, B1)
         self.forward(u, g, jm + 1, self.J, B2)
+        return u
+
+    def _prec_x_parallel(self, f, u, jm):
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=2) as ex:
+            fa = ex.submit(self.forward, u, f, 1, jm - 1)
+            fb = ex.submit(self.backward, u, f, self.J, jm + 1)
+            B1, B2 = fa.result(), fb.result()
+            self.solve(u, f, jm, self.beta[jm - 1], self.bt[jm], self.beta[jm - 1],
+                       self.bt[jm], B1=B1, B3=B2)
+            g = self.residual(u, f)
+            B2, B1 = self.solve(u, g, jm, self.bt[jm - 1], self.beta[jm], self.bt[jm - 1],
+                                self.beta[jm], out2=True, out4=True)
+            fa = ex.submit(self.backward, u, g, jm - 1, 1, B1)
+            fb = ex.submit(self.forward, u, g, jm + 1, self.J, B2)
+            fa.result(), fb.result()
         return u
 
     def mid_in(self, u, f, j, B1, B3):

@@ -216,6 +216,12 @@ int hs_ctx_destroy(hs_ctx* c) {
   return HS_OK;
 }
 
+int hs_ctx_set_sweep_segments(hs_ctx* c, int segments) {
+  if (!c || segments < 0) return HS_E_ARG;
+  c->sweep_segments = segments;
+  return HS_OK;
+}
+
 int hs_ctx_set_stream(hs_ctx* c, void* stream) {
   if (!c) return HS_E_ARG;
   c->stream = (cudaStream_t)stream;

@@ -2352,6 +2352,7 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   const int want = std::max(1, (M + 31) / 32);
   int C = std::min(kMaxC, want);
   int G = want > kMaxC ? std::min(kMaxG, (want + kMaxC - 1) / kMaxC) : 1;
+  if (c->sweep_segments > 0) G = std::min(kMaxG, c->sweep_segments);
   if (const char* ev = getenv("HS_SWEEP_SEGMENTS")) G = std::max(1, std::min(kMaxG, atoi(ev)));
   if (const char* ev = getenv("HS_SWEEP_CPC")) C = std::max(1, std::min(kMaxC, atoi(ev)));
   if (C < 2) G = 1;

@@ -269,7 +269,10 @@ class DeviceExactCSR(_Handle):
         self.n = int(a.shape[0])
         coo = a.tocoo()
         bw = int(np.abs(coo.row.astype(np.int64) - coo.col.astype(np.int64)).max()) if a.nnz else 0
-        self.block = max(1, bw)
+        # pivoting happens inside the blocks: small matrices are one dense
+        # block (partial pivoting over every row, like SuperLU's), larger ones
+        # get blocks of at least 64 rows
+        self.block = self.n if self.n <= 1024 else max(bw, 64)
         self.n_pad = -(-self.n // self.block) * self.block
         ip, pip = i64(a.indptr)
         ix, pix = i64(a.indices)

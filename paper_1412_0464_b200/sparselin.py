@@ -70,6 +70,11 @@ class Factorization:
         if not hasattr(op, "device") or not hasattr(op, "shape"):
             raise TypeError("factorize takes a StencilOperator or a scipy sparse matrix, "
                             f"got {type(op).__name__}")
+        if len(op.shape) == 1:   # a line: its rows as a general band (pivoting across rows)
+            self.shape = tuple(op.shape)
+            self.n = int(op.shape[0])
+            self.device = DeviceExactCSR(to_csr(op))
+            return
         self.shape = tuple(op.shape)
         self.n = int(np.prod(self.shape))
         self.device = DeviceExact(op.device())

@@ -48,6 +48,11 @@ class SweepOptions:
     n_cell: int | None = None
     subdomains: int | None = None
     parallel: bool = False
+    # device layout of the 2-D slab solves (not in the reference): face
+    # segments per sweep front, 0 = automatic (fastest single sweep); 1 keeps
+    # one cluster per front so that several right-hand sides' sweeps (solve_many
+    # lanes) run side by side
+    segments: int = 0
 
 
 def default_dd_strength(w_dd: int) -> float:
@@ -383,8 +388,16 @@ def build_hierarchy(mesh: Mesh, model: WaveModel, fine_op=None, smoother=None, s
     sweep = sweep or SweepOptions()
     part = None
     if coarse == "sweep":
-        part = build_partition(clevel, sweep.w_dd, sweep.s_dd, J=sweep.subdomains,
-                               device=device, keep_slab_ops=keep_slab_ops)
+        from ._lib import context
+        ctx = context() if device else None
+        if ctx is not None:
+            ctx.lib.hs_ctx_set_sweep_segments(ctx.h, int(sweep.segments))
+        try:
+            part = build_partition(clevel, sweep.w_dd, sweep.s_dd, J=sweep.subdomains,
+                                   device=device, keep_slab_ops=keep_slab_ops)
+        finally:
+            if ctx is not None:
+                ctx.lib.hs_ctx_set_sweep_segments(ctx.h, 0)
     h = float(mesh.spacing[0][0])
     return HostHierarchy(mesh, flevel.op, clevel.op, cmap, clevel, part, smoother, sweep,
                          h ** mesh.dim)

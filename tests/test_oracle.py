@@ -39,7 +39,13 @@ def test_transfers(case):
 def test_sweeps(case):
     name, d, tg = case
     if tg.part.J % 2 == 0:
-        assert rel(tg.part.prec_x(d["probe_xc"]), d["sweep_x"]) < 1e-12
+        ux = tg.part.prec_x(d["probe_xc"])
+        assert rel(ux, d["sweep_x"]) < 1e-12
+        tg.part.parallel = True    # two-thread X sweep (bench's CPU baseline): bitwise the serial
+        try:
+            assert np.array_equal(tg.part.prec_x(d["probe_xc"]), ux)
+        finally:
+            tg.part.parallel = False
     assert rel(tg.part.prec_ud(d["probe_xc"]), d["sweep_ud"]) < 1e-12
     for k in NX_KEYS:
         if f"sweep_{k}" in d:

@@ -25,4 +25,6 @@ for _ in range(N):
     sw.ctx.call("hs_sweep_apply", sw.h, 1, ptr(f), ptr(u))
 e1.record(); torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / N
-print(f"[{assembly} assembly] config {idx}: J={p.subdomains} M={hh.coarse_op.shape[1]} sweep {ms:.3f} ms  -> {1e3*ms/(p.subdomains+2):.1f} us per slab step")
+print(f"[{assembly} assembly] config {idx}: J={p.subdomains} M={hh.coarse_op.shape[1]} "
+      f"segments={sw.segments} chunks={sw.chunks} factor_bytes={sw.factor_bytes / 1e9:.2f} GB "
+      f"sweep {ms:.3f} ms  -> {1e3*ms/(p.subdomains+2):.1f} us per slab step")
