@@ -42,6 +42,7 @@ typedef struct hs_stencil hs_stencil;
 typedef struct hs_transfer hs_transfer;
 typedef struct hs_sweep hs_sweep;
 typedef struct hs_cycle hs_cycle;
+typedef struct hs_csr hs_csr;
 
 /* ---- context ------------------------------------------------------------ */
 int hs_ctx_create(int device, hs_ctx** out);
@@ -138,6 +139,17 @@ int hs_transfer_create_window(hs_ctx* ctx, int dim, const int64_t* fp_len,
                               const int64_t* fp_concat, const uint8_t* refined_concat,
                               const int64_t* window, hs_transfer** out);
 int hs_transfer_destroy(hs_ctx* ctx, hs_transfer* t);
+
+/* General sparse matrix (host CSR: indptr [rows+1], indices [nnz], interleaved
+ * complex128 values [nnz]) uploaded for y = alpha A x (+ y): the explicit
+ * prolongation matrix of a TwoGridCycle built from one (twogrid.py:119-159,
+ * `p_matrix @ uc`, `p_matrix.T @ r`); the BASELINE hierarchies use the tent
+ * tables (hs_transfer_create) instead. */
+int hs_csr_create(hs_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, const int64_t* indptr,
+                  const int64_t* indices, const double* vals, hs_csr** out);
+int hs_csr_destroy(hs_ctx* ctx, hs_csr* m);
+int hs_csr_apply(hs_ctx* ctx, const hs_csr* m, const void* x, void* y, double alpha_re,
+                 double alpha_im, int accumulate);
 /* rc = scale * P^T r                         twogrid.py:154 (restrict: 89-93 with scale 1) */
 int hs_restrict(hs_ctx* ctx, const hs_transfer* t, const void* r_fine, void* rc, double scale,
                 int nrhs);

@@ -72,6 +72,10 @@ SIGNATURES = {
     "hs_sweep_solve_one": (C.c_int, [_vp, _vp, C.c_int, C.c_int64, C.c_int64, C.c_int64,
                                      C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hs_exact_create": (C.c_int, [_vp, _vp, C.POINTER(_vp)]),
+    "hs_csr_create": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, _i64p, _i64p,
+                                C.POINTER(C.c_double), C.POINTER(_vp)]),
+    "hs_csr_destroy": (C.c_int, [_vp, _vp]),
+    "hs_csr_apply": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, C.c_double, C.c_int]),
     "hs_exact_create_csr": (C.c_int, [_vp, C.c_int64, C.c_int64, _i64p, _i64p,
                                       C.POINTER(C.c_double), C.c_int, C.POINTER(_vp)]),
     "hs_sweep_plan_nx": (C.c_int, [_vp, _vp, C.c_int, _i64p, _i64p, C.POINTER(C.c_int)]),

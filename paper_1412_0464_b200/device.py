@@ -255,6 +255,36 @@ class DeviceSweep(_Handle):
         return u, was_np
 
 
+class DeviceCSR(_Handle):
+    """A general sparse matrix on the device for y = alpha A x (+ y)
+    (hs_csr_*): explicit prolongation / restriction matrices."""
+
+    _destroy = "hs_csr_destroy"
+
+    def __init__(self, mat, ctx=None):
+        import scipy.sparse as sp
+        self.ctx = ctx or context()
+        a = sp.csr_matrix(mat, dtype=complex)
+        a.sum_duplicates()
+        self.rows, self.cols = (int(v) for v in a.shape)
+        ip, pip = i64(a.indptr)
+        ix, pix = i64(a.indices)
+        vals = np.ascontiguousarray(a.data, dtype=complex)
+        h = C.c_void_p()
+        self.ctx.call("hs_csr_create", self.rows, self.cols, int(a.nnz), pip, pix,
+                      vals.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)), C.byref(h))
+        self.h = h
+
+    def apply(self, x, out=None, alpha=1.0, accumulate=False):
+        """device tensor in, device tensor out"""
+        xt, _ = to_device(x, self.cols, self.ctx)
+        y = out if out is not None else empty(self.rows, self.ctx)
+        a = complex(alpha)
+        self.ctx.call("hs_csr_apply", self.h, ptr(xt), ptr(y), a.real, a.imag,
+                      int(bool(accumulate) and out is not None))
+        return y
+
+
 class DeviceExactCSR(_Handle):
     """Exact solver of a general sparse matrix (hs_exact_create_csr): its CSR
     rows cut into block rows of ``block`` >= bandwidth unknowns, factorised as
@@ -282,6 +312,12 @@ class DeviceExactCSR(_Handle):
                       vals.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)),
                       self.block, C.byref(h))
         self.h = h
+
+    def variant_id(self, variant="ud", cells=None) -> int:
+        if self.n_pad != self.n:
+            raise ValueError("a padded general-matrix factorisation cannot be a cycle's "
+                             "coarse solver")
+        return _lib.HS_VARIANT_UD
 
     def apply(self, f):
         """x = A^{-1} f (flat, n entries); returns (tensor, was_numpy)."""

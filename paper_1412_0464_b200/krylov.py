@@ -60,6 +60,30 @@ class SolveReport:
                 f"final residual {self.residual_history[-1]:.3e}, {self.wall_time:.2f}s")
 
 
+def on_device(fn):
+    """Mark a user callable as taking and returning device (torch CUDA)
+    vectors, so gmres passes it the device vector without a host copy."""
+    fn._hs_device = True
+    return fn
+
+
+def _device_callable(fn) -> bool:
+    """True for callables of this package that accept device (torch CUDA)
+    vectors: operators, preconditioners, factorisation solves."""
+    import torch
+    if isinstance(fn, torch.nn.Module):
+        return True
+    if getattr(fn, "_hs_device", False):
+        return True
+    owner = getattr(fn, "__self__", None)
+    if owner is not None and getattr(owner, "_hs_device", False):
+        return True
+    mod = getattr(type(fn), "__module__", "") or ""
+    if mod.startswith(__name__.rsplit(".", 1)[0]):
+        return True   # instances of this package's classes (FineOperator, _Prec, ...)
+    return False
+
+
 class _Ops:
     """Device-side operator bundle for one solve."""
 
@@ -73,11 +97,19 @@ class _Ops:
             self.fine = apply_a.op.device()
         cyc = getattr(apply_m, "cycle", None)
         lane = getattr(apply_m, "lane", None)
-        if cyc is not None and self.fine is not None and cyc.fine_op is apply_a.op:
+        if (cyc is not None and self.fine is not None and cyc.fine_op is apply_a.op
+                and not getattr(cyc, "generic", False)):
             self.cycle = lane.dev if lane is not None else cyc.device()
 
     def _call(self, fn, v):
-        out = fn(v)
+        """apply a user operator: this package's device callables take the
+        device vector; any other callable is host code written for numpy
+        (the reference's ``gmres`` contract): it gets a host copy, and its
+        result is copied back to the device"""
+        if _device_callable(fn):
+            out = fn(v)
+        else:
+            out = fn(v.cpu().numpy())
         t, _ = to_device(out, self.n, self.ctx)
         return t
 

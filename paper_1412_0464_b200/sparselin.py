@@ -57,6 +57,8 @@ class Factorization:
     sides.  Raises ZeroDivisionError("zero pivot at row i ...") on a singular
     pivot block (sparselin.py:53-56)."""
 
+    _hs_device = True   # solve() takes torch CUDA vectors (krylov._device_callable)
+
     def __init__(self, op):
         from .device import DeviceExact, DeviceExactCSR
         if sp.issparse(op) or isinstance(op, np.ndarray):

@@ -215,6 +215,23 @@ class Subdomain:
     core_hi: int
     op: StencilOperator | None
 
+    @property
+    def factor(self):
+        """The slab's own LU (reference ``Subdomain.factor``): a device
+        factorisation of the slab operator, made on first use (the sweep
+        itself solves from the partition's packed device factors)."""
+        f = self.__dict__.get("_factor")
+        if f is None:
+            if self.op is None:
+                raise ValueError("slab operator not kept (build_partition(keep_slab_ops=False))")
+            from .sparselin import factorize
+            op = self.op
+            if hasattr(op, "to_host"):
+                op = op.to_host()
+            f = factorize(op)
+            self.__dict__["_factor"] = f
+        return f
+
 
 @dataclass
 class Partition:

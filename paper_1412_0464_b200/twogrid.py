@@ -93,6 +93,11 @@ def _prolong_1d(fp, refined) -> sp.csr_matrix:
     return sp.csr_matrix((vals, (rows, cols)), shape=(n_f, n_c))
 
 
+def empty_like_dev(t):
+    import torch
+    return torch.empty_like(t)
+
+
 def prolongation_matrix(cmap: CoarseningMap) -> sp.csr_matrix:
     p = _prolong_1d(cmap.fine_point_of_coarse[0], cmap.refined_cell[0])
     for a in range(1, cmap.dim):
@@ -188,14 +193,22 @@ class TwoGridCycle:
             self.fine_csr = FineOperator(self.fine_op)
 
     @property
+    def generic(self) -> bool:
+        """built from an explicit prolongation matrix (the reference's
+        ``TwoGridCycle(fine, coarse, p_matrix, ...)``) instead of a CoarseningMap"""
+        return sp.issparse(self.cmap)
+
+    @property
     def p_matrix(self):
-        return prolongation_matrix(self.cmap)
+        return sp.csr_matrix(self.cmap) if self.generic else prolongation_matrix(self.cmap)
 
     @property
     def r_matrix(self):
         return self.p_matrix.T
 
     def device(self):
+        if self.generic:
+            raise ValueError("an explicit-matrix cycle has no fused device plan")
         if self._dev is None:
             from .device import DeviceCycle, DeviceTransfer
             fine = self.fine_op.device()
@@ -205,8 +218,43 @@ class TwoGridCycle:
                                     self.smoother.nu, self.restrict_scale, vid, fine.ctx)
         return self._dev
 
+    def _vcycle_matrix(self, f):
+        """V-cycle with an explicit prolongation matrix P (twogrid.py:150-159):
+        device Jacobi / residual kernels, P^T and P as device CSR products
+        (hs_csr_apply), the coarse solver's own device solve."""
+        from .device import DeviceCSR, from_device, to_device
+        mats = self.__dict__.get("_pmats")
+        fine = self.fine_op.device()
+        if mats is None:
+            p = sp.csr_matrix(self.cmap, dtype=complex)
+            mats = (DeviceCSR(p, fine.ctx), DeviceCSR(p.T.tocsr(), fine.ctx))
+            self.__dict__["_pmats"] = mats
+        pd, rd = mats
+        ft, was_np = to_device(f, fine.n, fine.ctx)
+        nu, w = self.smoother.nu, self.smoother.omega_jac
+        if nu:
+            diag = self.fine_op.diagonal()
+            zero = np.argwhere(diag == 0)
+            if zero.size:
+                raise ZeroDivisionError(f"zero operator diagonal at node {tuple(zero[0])}")
+        u = empty_like_dev(ft)
+        u.zero_()
+        if nu:
+            fine.jacobi(u, ft, w, nu, u_is_zero=True)
+        r = fine.residual(ft, u)
+        rc = rd.apply(r, alpha=self.restrict_scale)
+        uc = self.coarse_solver.solve(rc)
+        pd.apply(uc.reshape(-1), out=u, accumulate=True)
+        if nu:
+            fine.jacobi(u, ft, w, nu)
+        if was_np:
+            return from_device(u, True, self.fine_op.shape)
+        return u.reshape(f.shape)
+
     def vcycle(self, f):
         from .device import from_device, to_device
+        if self.generic:
+            return self._vcycle_matrix(f)
         dev = self.device()
         ft, was_np = to_device(f, dev.n, dev.ctx)
         u = dev.vcycle_dev(ft)

@@ -229,9 +229,12 @@ def test_gmres_small_known_answers(rng):
     assert rep.iterations == 1 and rep.converged and np.allclose(u, b)
     dd = np.array([1.0] * 10 + [3.0] * 10, dtype=complex)
     b = rng.standard_normal(20) + 1j * rng.standard_normal(20)
-    u, rep = hb.gmres(lambda v: v * __import__("torch").from_numpy(dd).to(v.device), None, b,
-                      hb.GmresConfig(tol=1e-12))
+    u, rep = hb.gmres(lambda v: dd * v, None, b, hb.GmresConfig(tol=1e-12))   # host callable
     assert rep.iterations == 2 and rep.converged
+    from paper_1412_0464_b200.krylov import on_device
+    ddt = __import__("torch").from_numpy(dd).cuda()
+    u2, rep2 = hb.gmres(on_device(lambda v: v * ddt), None, b, hb.GmresConfig(tol=1e-12))
+    assert rep2.iterations == 2 and np.allclose(u2, u, rtol=1e-12, atol=1e-14)
     _, rep = hb.gmres(lambda v: v, None, np.zeros(5, complex))
     assert rep.iterations == 0 and rep.converged
     with pytest.raises(FloatingPointError):
@@ -475,10 +478,11 @@ def _large_anchors():
     return json.loads(f.read_text()) if f.exists() else {}
 
 
-@pytest.mark.parametrize("name", ["C2", "C4_rhs0", "C3_half", "C5_half", "C1_exact", "C1_nx4"])
+@pytest.mark.parametrize("name", ["C1_x", "C2", "C3", "C3_half", "C5_half", "C1_exact", "C1_nx4"]
+                         + [f"C4_rhs{r}" for r in range(8)])
 def test_baseline_config_matches_reference_solve(name):
-    """BASELINE configs at full (C2, C4 right-hand side 0) or half size (C3,
-    C5), and configs[0] with the exact coarse solve and with NX(4) sweeps,
+    """BASELINE configs at full size (C2, C3, C4's eight right-hand sides) or
+    half size (C3, C5), and configs[0] with the X, exact and NX(4) coarse solves,
     solved by the reference itself (tests/golden/make_large_anchors.py):
     the same GMRES iteration count +-1, residual histories within 1e-6
     relative over the common iterations, true residual <= 1e-6 and the
@@ -580,3 +584,34 @@ def test_factorize_too_large_block_raises():
                                     (0, -1, 0): np.full(shape, -1.0 + 0j)})
     with pytest.raises(ValueError, match="too large"):
         hb.factorize(op)
+
+
+@pytest.mark.parametrize("name", ["apply_C1", "apply_C2", "apply_C4", "apply_C3"])
+def test_tgsp_apply_matches_reference_at_config_size(name):
+    """The north_star apply gate at BASELINE config size: tgsp_apply(cycle, z)
+    for the seeded complex normal z of tests/golden/make_large_anchors.py
+    against the reference's output (its 2-norm, 256 sampled entries and the
+    sums over 1024 contiguous blocks), all within 1e-10 relative."""
+    import paper_1412_0464_b200 as hb
+    from paper_1412_0464_b200.configs import config, fe_fine_operator
+    a = _large_anchors().get(name)
+    if a is None:
+        pytest.skip(f"no reference anchor for {name}")
+    p = config(a["config"], a["scale"])
+    fine = fe_fine_operator(p.mesh, p.model) if a.get("fine_operator", "fd5") != "fd5" else None
+    cycle, _ = hb.build_two_grid(p.mesh, p.model, fine_op=fine,
+                                 smoother=hb.SmootherConfig(p.omega_jac, p.nu), coarse="sweep",
+                                 sweep=hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains),
+                                 keep_slab_ops=False)
+    rng = np.random.default_rng(a["seed"])
+    n = p.n_fine
+    z = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    y = np.asarray(hb.tgsp_apply(cycle, z.reshape(p.mesh.unknowns))).ravel()
+    ynorm = np.linalg.norm(y)
+    assert abs(ynorm - a["y_norm"]) <= 1e-10 * a["y_norm"]
+    idx = np.asarray(a["y_sample_idx"])
+    ref = np.asarray(a["y_sample_re"]) + 1j * np.asarray(a["y_sample_im"])
+    assert np.linalg.norm(y[idx] - ref) <= 1e-10 * np.linalg.norm(ref)
+    bs = np.array([b.sum() for b in np.array_split(y, a["n_blocks"])])
+    bref = np.asarray(a["block_sums_re"]) + 1j * np.asarray(a["block_sums_im"])
+    assert np.linalg.norm(bs - bref) <= 1e-10 * np.linalg.norm(bref)

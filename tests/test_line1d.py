@@ -141,3 +141,49 @@ def test_dense_solve_checker():
     big = hb.StencilOperator((101, 101), {(0, 0): np.ones((101, 101))})
     with pytest.raises(ValueError, match="capped"):
         hb.dense_solve(big, np.zeros(big.n))
+
+
+@pytest.mark.gpu
+def test_explicit_matrix_cycle(rng):
+    """TwoGridCycle built from an explicit prolongation matrix (the reference's
+    constructor, test_twogrid.py:104-118): identity P with the exact coarse
+    solve is an exact solve; the tent matrix of a CoarseningMap gives the
+    same cycle as the tent tables (1e-13)."""
+    import paper_1412_0464_b200 as hb
+    from paper_1412_0464_b200.mesh import PML, AbsorbingLayerSpec
+    from paper_1412_0464_b200.sparselin import to_csr
+    from paper_1412_0464_b200.twogrid import ExactCoarseSolver, TwoGridCycle
+    mesh = hb.build_mesh(2, 12, 1 / 12, None)
+    model = hb.WaveModel.constant(mesh, 2 * np.pi * 12 / 10.0)
+    op = hb.assemble_fine(mesh, model)
+    cyc = TwoGridCycle(op, op, sp.identity(op.n, format="csr"), hb.SmootherConfig(0.8, 0),
+                       ExactCoarseSolver(hb.factorize(op), op.shape), restrict_scale=1.0)
+    f = crand(rng, op.shape)
+    u = cyc.vcycle(f)
+    a = to_csr(op)
+    assert np.linalg.norm(a @ u.ravel() - f.ravel()) < 1e-10 * np.linalg.norm(f)
+    # explicit tent matrix == tent tables
+    mesh = hb.build_mesh(2, 32, 1 / 32, AbsorbingLayerSpec(PML, 4, 20.0))
+    model = hb.WaveModel.constant(mesh, 2 * np.pi * 32 / 10.0)
+    cycle, _ = hb.build_two_grid(mesh, model, smoother=hb.SmootherConfig(0.8, 2), coarse="exact")
+    gen = TwoGridCycle(cycle.fine_op, cycle.coarse_op, cycle.p_matrix, cycle.smoother,
+                       cycle.coarse_solver, restrict_scale=cycle.restrict_scale)
+    f = crand(rng, mesh.unknowns)
+    assert rel(gen.vcycle(f), cycle.vcycle(f)) < 1e-13
+
+
+@pytest.mark.gpu
+def test_gmres_with_host_callables(rng):
+    """gmres with numpy callables (the reference's contract, test_krylov.py):
+    the operator runs on the host, the Krylov arithmetic on the device"""
+    import paper_1412_0464_b200 as hb
+    d = np.array([1.0] * 10 + [3.0] * 10, dtype=complex)
+    b = crand(rng, 20)
+    u, rep = hb.gmres(lambda v: d * v, None, b, hb.GmresConfig(tol=1e-12))
+    assert rep.iterations == 2 and rep.converged and isinstance(u, np.ndarray)
+    n = 60
+    a = np.diag(np.linspace(1, 4, n)) + 0.1 * rng.standard_normal((n, n))
+    bb = rng.standard_normal(n) + 0j
+    u, rep = hb.gmres(lambda v: a @ v, None, bb, hb.GmresConfig(tol=1e-12, max_iter=n))
+    assert np.linalg.norm(a @ u - bb) / np.linalg.norm(bb) < 1e-10
+    assert np.all(np.diff(rep.residual_history) <= 1e-14)
