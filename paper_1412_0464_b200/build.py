@@ -79,7 +79,7 @@ def build(verbose: bool = False, force: bool = False, defines=(), out: Path | No
                 print(f"--- {name}\n{log}")
     lib.parent.mkdir(parents=True, exist_ok=True)
     tmp = lib.with_suffix(".so.tmp")
-    cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcublas", "-lcusolver"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs)]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:
         raise RuntimeError(f"link failed:\n{p.stderr}")

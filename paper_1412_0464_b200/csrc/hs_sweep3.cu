@@ -19,8 +19,7 @@
 #include "hs_common.cuh"
 #include "hs_sweep.cuh"
 
-#include <cublas_v2.h>
-#include <cusolverDn.h>
+#include "hs_dense.cuh"
 
 #include <algorithm>
 #include <array>
@@ -40,7 +39,6 @@ struct Sweep3 {
   std::vector<double2*> coef;          // per slab: stencil coefficients [S][T n1 n2] (owned copy)
   std::vector<std::array<int, 27>> slot;   // per slab: (o0+1)*9 + (o1+1)*3 + (o2+1) -> slot
   std::array<int, 27> cslot{};         // coarse operator slots
-  cublasHandle_t blas = nullptr;
   double2* F[2] = {nullptr, nullptr};  // per concurrent chain: [n1][NBmax] right-hand side
   double2* Y[2] = {nullptr, nullptr};  // [n1][NBmax] forward solution, then x
   unsigned* gbar = nullptr;            // [2] grid barrier counters of the solve kernel
@@ -101,11 +99,6 @@ __global__ void k3_csr_block(const int64_t* __restrict__ indptr, const int64_t* 
   }
 }
 
-__global__ void k3_eye(double2* __restrict__ A, int NB) {
-  const int64_t i = (int64_t)blockIdx.x * kT3 + threadIdx.x;
-  if (i >= (int64_t)NB * NB) return;
-  A[i] = make_double2(i % NB == i / NB ? 1.0 : 0.0, 0.0);
-}
 
 // F[i1][t n2 + i2] = restriction rows of src + transmission terms (subdom_solve steps 1-2)
 __global__ void k3_rhs(SweepTask t, int n0, int n1, int n2, const double2* __restrict__ src,
@@ -405,10 +398,6 @@ int slots3(const Stencil* op, std::array<int, 27>& a, Ctx* c) {
     cudaError_t _e = (expr);                                                 \
     if (_e != cudaSuccess) return check_cuda(c, _e, what);                   \
   } while (0)
-#define S3_BLAS(expr, what)                                                  \
-  do {                                                                       \
-    if ((expr) != 0) return set_error(c, HS_E_CUDA, std::string(what) + " failed"); \
-  } while (0)
 
 }  // namespace
 
@@ -423,7 +412,6 @@ void sweep3_destroy(Sweep3* s3) {
     cudaFree(s3->Y[i]);
   }
   cudaFree(s3->gbar);
-  if (s3->blas) cublasDestroy(s3->blas);
   delete s3;
 }
 
@@ -437,41 +425,34 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
   s3->n2 = (int)coarse->shape[2];
   const int J = s->J, n1 = s3->n1, n2 = s3->n2;
   if (int r = slots3(coarse, s3->cslot, c)) return r;
-  if (cublasCreate(&s3->blas) != CUBLAS_STATUS_SUCCESS)
-    return set_error(c, HS_E_CUDA, "cublasCreate failed");
-  cusolverDnHandle_t sol = nullptr;
-  if (cusolverDnCreate(&sol) != CUSOLVER_STATUS_SUCCESS)
-    return set_error(c, HS_E_CUDA, "cusolverDnCreate failed");
-  cublasSetStream(s3->blas, c->stream);
-  cusolverDnSetStream(sol, c->stream);
   int NBmax = 0;
   for (int j = 0; j < J; ++j) NBmax = std::max(NBmax, (int)(hi[j] - lo[j] + 1) * n2);
-  double2 *D = nullptr, *Lb = nullptr, *U = nullptr, *work = nullptr, *Di = nullptr, *Xc = nullptr;
-  int *ipiv = nullptr, *info = nullptr;
-  const size_t blk = (size_t)NBmax * NBmax * sizeof(double2);
-  int lwork = 0;
+  // the solve kernel's limits first (nothing is factorised for a plane it cannot solve)
+  s3->grid = c->num_sms;
+  int optin = 0;
+  S3_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device),
+         "smem attr");
+  if ((NBmax + s3->grid - 1) / s3->grid > kR3 || k3_smem(NBmax, s3->grid, 1) > (size_t)optin)
+    return set_error(c, HS_E_SHAPE, "3-D slab planes too large for the solve kernel");
+  // per-slab work blocks (column-major NB x NB): D (factorised in place), L, U, Dinv
+  std::vector<double2*> Dw(J, nullptr), Lw(J, nullptr), Uw(J, nullptr), Iw(J, nullptr);
+  std::vector<int*> Pw(J, nullptr);
+  int* info = nullptr;
   auto done = [&](int rc) {
-    cudaFree(D); cudaFree(Lb); cudaFree(U); cudaFree(work); cudaFree(ipiv); cudaFree(info);
-    cudaFree(Di); cudaFree(Xc);
-    if (sol) cusolverDnDestroy(sol);
+    for (int j = 0; j < J; ++j) {
+      cudaFree(Dw[j]); cudaFree(Lw[j]); cudaFree(Uw[j]); cudaFree(Iw[j]); cudaFree(Pw[j]);
+    }
+    cudaFree(info);
     return rc;
   };
-  if (cudaMalloc((void**)&D, blk) || cudaMalloc((void**)&Lb, blk) || cudaMalloc((void**)&U, blk) ||
-      cudaMalloc((void**)&Di, blk) || cudaMalloc((void**)&Xc, blk) ||
-      cudaMalloc((void**)&s3->gbar, 2 * sizeof(unsigned)) ||
-      cudaMalloc((void**)&ipiv, NBmax * sizeof(int)) ||
+  if (cudaMalloc((void**)&s3->gbar, 2 * sizeof(unsigned)) ||
       cudaMalloc((void**)&info, ((size_t)n1 * J + 1) * sizeof(int)) ||
       cudaMalloc((void**)&s3->F[0], (size_t)n1 * NBmax * sizeof(double2)) ||
       cudaMalloc((void**)&s3->Y[0], (size_t)n1 * NBmax * sizeof(double2)) ||
       cudaMalloc((void**)&s3->F[1], (size_t)n1 * NBmax * sizeof(double2)) ||
       cudaMalloc((void**)&s3->Y[1], (size_t)n1 * NBmax * sizeof(double2)))
     return done(set_error(c, HS_E_CUDA, "3-D sweep work allocation failed"));
-  if (cusolverDnZgetrf_bufferSize(sol, NBmax, NBmax, (cuDoubleComplex*)D, NBmax, &lwork) != 0 ||
-      cudaMalloc((void**)&work, (size_t)std::max(1, lwork) * sizeof(double2)))
-    return done(set_error(c, HS_E_CUDA, "getrf workspace failed"));
-  cudaMemsetAsync(info, 0, (size_t)n1 * J * sizeof(int), c->stream);
-  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), mone = make_cuDoubleComplex(-1.0, 0.0),
-                        zero = make_cuDoubleComplex(0.0, 0.0);
+  S3_TRY(cudaMemsetAsync(info, 0, (size_t)n1 * J * sizeof(int), c->stream), "memset");
   s3->T.resize(J);
   s3->slot.resize(J);
   // dense blocks of a slab: from its stencil coefficients, or (exact solve of
@@ -485,12 +466,14 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
       k3_block<<<gb, kT3, 0, c->stream>>>(cf, sl, T, n1, n2, i1, o1, A);
     c->launches++;
   };
+  std::vector<int> NBs(J);
   for (int j = 0; j < J; ++j) {
     const Stencil* op = slabs[j];
     const int T = (int)(hi[j] - lo[j] + 1), NB = T * n2;
     if (op->dim != 3 || op->shape[0] != T || op->shape[1] != n1 || op->shape[2] != n2)
       return done(set_error(c, HS_E_SHAPE, "slab operator shape does not match the partition"));
     s3->T[j] = T;
+    NBs[j] = NB;
     if (int r = slots3(op, s3->slot[j], c)) return done(r);
     double2* cf = nullptr;
     const size_t cb = (size_t)op->d.S * op->d.n * sizeof(double2);
@@ -499,62 +482,88 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
       S3_TRY(cudaMemcpyAsync(cf, op->d.coeffs, cb, cudaMemcpyDeviceToDevice, c->stream), "copy");
     }
     s3->coef.push_back(cf);
-    double2 *dv = nullptr, *xv = nullptr;
+    double2 *dv = nullptr, *xv = nullptr, *gv = nullptr;
     const size_t nb2 = (size_t)NB * NB;
     S3_TRY(cudaMalloc((void**)&dv, n1 * nb2 * sizeof(double2)), "3-D slab factors (Dinv)");
     s3->dinv.push_back(dv);
     S3_TRY(cudaMalloc((void**)&xv, std::max(1, n1 - 1) * nb2 * sizeof(double2)),
            "3-D slab factors (X)");
     s3->xf.push_back(xv);
-    double2* gv = nullptr;
     S3_TRY(cudaMalloc((void**)&gv, n1 * nb2 * sizeof(double2)), "3-D slab factors (G)");
     s3->gf.push_back(gv);
     s3->bytes += (long long)(3 * n1 - 2) * nb2 * sizeof(double2);
-    const Slots sl = to_slots(s3->slot[j]);
-    for (int i1 = 0; i1 < n1; ++i1) {
-      S3_TRY(cudaMemsetAsync(D, 0, nb2 * sizeof(double2), c->stream), "memset");
-      block(cf, sl, T, NB, i1, 0, D);
-      if (i1 > 0) {   // D' = D - L_i X_{i-1}
-        S3_TRY(cudaMemsetAsync(Lb, 0, nb2 * sizeof(double2), c->stream), "memset");
-        block(cf, sl, T, NB, i1, -1, Lb);
-        S3_BLAS(cublasZgemm(s3->blas, CUBLAS_OP_N, CUBLAS_OP_N, NB, NB, NB, &mone,
-                            (cuDoubleComplex*)Lb, NB, (cuDoubleComplex*)Xc, NB,
-                            &one, (cuDoubleComplex*)D, NB), "zgemm");
+    S3_TRY(cudaMalloc((void**)&Dw[j], nb2 * sizeof(double2)), "factor work");
+    S3_TRY(cudaMalloc((void**)&Lw[j], nb2 * sizeof(double2)), "factor work");
+    S3_TRY(cudaMalloc((void**)&Uw[j], nb2 * sizeof(double2)), "factor work");
+    S3_TRY(cudaMalloc((void**)&Iw[j], nb2 * sizeof(double2)), "factor work");
+    S3_TRY(cudaMalloc((void**)&Pw[j], (size_t)NB * sizeof(int)), "factor work");
+  }
+  // Block LU along the planes, every slab at once (hand-written batched dense
+  // kernels, hs_dense.cu), per plane i:
+  //   D' = D_i - L_i X_{i-1};  LU(D') with partial pivoting, Dinv_i = D'^{-1};
+  //   G_i = Dinv_i L_i;  X_i = Dinv_i U_i   (all stored row-major)
+  std::vector<GemmJob> gj;
+  std::vector<LuJob> lj(J);
+  std::vector<TransposeJob> tj(J);
+  for (int i1 = 0; i1 < n1; ++i1) {
+    for (int j = 0; j < J; ++j) {
+      const int NB = NBs[j];
+      const size_t nb2 = (size_t)NB * NB;
+      const Slots sl = to_slots(s3->slot[j]);
+      S3_TRY(cudaMemsetAsync(Dw[j], 0, nb2 * sizeof(double2), c->stream), "memset");
+      block(s3->coef[j], sl, s3->T[j], NB, i1, 0, Dw[j]);
+      if (i1 > 0) {
+        S3_TRY(cudaMemsetAsync(Lw[j], 0, nb2 * sizeof(double2), c->stream), "memset");
+        block(s3->coef[j], sl, s3->T[j], NB, i1, -1, Lw[j]);
       }
-      // Dinv = D'^{-1} (partial pivoting inside the block)
-      S3_BLAS(cusolverDnZgetrf(sol, NB, NB, (cuDoubleComplex*)D, NB, (cuDoubleComplex*)work, ipiv,
-                               info + j * n1 + i1), "getrf");
-      k3_eye<<<(unsigned)((nb2 + kT3 - 1) / kT3), kT3, 0, c->stream>>>(Di, NB);
-      c->launches++;
-      // (getrs reports argument errors only: its own slot, so that getrf's
-      // singular-pivot code survives for the check below)
-      S3_BLAS(cusolverDnZgetrs(sol, CUBLAS_OP_N, NB, NB, (cuDoubleComplex*)D, NB, ipiv,
-                               (cuDoubleComplex*)Di, NB, info + (size_t)n1 * J), "getrs");
-      // stored row-major (= the column-major transpose) for the solve kernel's rows
-      S3_BLAS(cublasZgeam(s3->blas, CUBLAS_OP_T, CUBLAS_OP_N, NB, NB, &one, (cuDoubleComplex*)Di,
-                          NB, &zero, (cuDoubleComplex*)Di, NB, (cuDoubleComplex*)(dv + i1 * nb2),
-                          NB), "geam");
-      if (i1 > 0) {   // G_i = Dinv_i L_i (the forward chain's coupling), row-major
-        S3_BLAS(cublasZgemm(s3->blas, CUBLAS_OP_N, CUBLAS_OP_N, NB, NB, NB, &one,
-                            (cuDoubleComplex*)Di, NB, (cuDoubleComplex*)Lb, NB, &zero,
-                            (cuDoubleComplex*)U, NB), "zgemm");
-        S3_BLAS(cublasZgeam(s3->blas, CUBLAS_OP_T, CUBLAS_OP_N, NB, NB, &one,
-                            (cuDoubleComplex*)U, NB, &zero, (cuDoubleComplex*)U, NB,
-                            (cuDoubleComplex*)(gv + i1 * nb2), NB), "geam");
-      }
-      if (i1 + 1 < n1) {   // X_i = Dinv_i U_i
-        S3_TRY(cudaMemsetAsync(U, 0, nb2 * sizeof(double2), c->stream), "memset");
-        block(cf, sl, T, NB, i1, 1, U);
-        S3_BLAS(cublasZgemm(s3->blas, CUBLAS_OP_N, CUBLAS_OP_N, NB, NB, NB, &one,
-                            (cuDoubleComplex*)Di, NB, (cuDoubleComplex*)U, NB, &zero,
-                            (cuDoubleComplex*)Xc, NB), "zgemm");
-        S3_BLAS(cublasZgeam(s3->blas, CUBLAS_OP_T, CUBLAS_OP_N, NB, NB, &one,
-                            (cuDoubleComplex*)Xc, NB, &zero, (cuDoubleComplex*)Xc, NB,
-                            (cuDoubleComplex*)(xv + i1 * nb2), NB), "geam");
+      if (i1 + 1 < n1) {
+        S3_TRY(cudaMemsetAsync(Uw[j], 0, nb2 * sizeof(double2), c->stream), "memset");
+        block(s3->coef[j], sl, s3->T[j], NB, i1, 1, Uw[j]);
       }
     }
-    S3_TRY(cudaGetLastError(), "3-D factor kernels");
+    if (i1 > 0) {   // D' = D - L_i X_{i-1} (X_{i-1} stored row-major: op T)
+      gj.clear();
+      for (int j = 0; j < J; ++j) {
+        const int NB = NBs[j];
+        GemmJob q{};
+        q.m = q.n = q.k = NB;
+        q.A = Lw[j]; q.lda = NB;
+        q.B = s3->xf[j] + (size_t)(i1 - 1) * NB * NB; q.ldb = NB; q.opB = 1;
+        q.C = Dw[j]; q.ldc = NB;
+        q.alpha = make_double2(-1.0, 0.0); q.beta = make_double2(1.0, 0.0);
+        gj.push_back(q);
+      }
+      if (int r = dense_gemm(c, gj.data(), J)) return done(r);
+    }
+    for (int j = 0; j < J; ++j) {
+      lj[j] = LuJob{Dw[j], NBs[j], NBs[j], Pw[j], info + (size_t)j * n1 + i1, Iw[j], NBs[j]};
+      tj[j] = TransposeJob{Iw[j], NBs[j], s3->dinv[j] + (size_t)i1 * NBs[j] * NBs[j], NBs[j], NBs[j]};
+    }
+    if (int r = dense_lu_inverse(c, lj.data(), J)) return done(r);
+    if (int r = dense_transpose(c, tj.data(), J)) return done(r);
+    gj.clear();
+    for (int j = 0; j < J; ++j) {
+      const int NB = NBs[j];
+      GemmJob q{};
+      q.m = q.n = q.k = NB;
+      q.A = Iw[j]; q.lda = NB;
+      q.ldb = NB;
+      q.ldc = NB;
+      q.transC = 1;
+      if (i1 > 0) {   // G_i = Dinv_i L_i
+        q.B = Lw[j];
+        q.C = s3->gf[j] + (size_t)i1 * NB * NB;
+        gj.push_back(q);
+      }
+      if (i1 + 1 < n1) {   // X_i = Dinv_i U_i
+        q.B = Uw[j];
+        q.C = s3->xf[j] + (size_t)i1 * NB * NB;
+        gj.push_back(q);
+      }
+    }
+    if (int r = dense_gemm(c, gj.data(), (int)gj.size())) return done(r);
   }
+  S3_TRY(cudaGetLastError(), "3-D factor kernels");
   std::vector<int> hinfo((size_t)n1 * J);
   S3_TRY(cudaMemcpyAsync(hinfo.data(), info, hinfo.size() * sizeof(int), cudaMemcpyDeviceToHost,
                          c->stream), "info");
@@ -570,15 +579,7 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
   s->factor_bytes = s3->bytes;
   {   // the solve kernel: one CTA per SM, co-resident (cooperative launch); the
       // staged rows double-buffered when two planes' rows fit shared memory
-    s3->grid = c->num_sms;
-    int optin = 0;
-    S3_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device),
-           "smem attr");
-    if ((NBmax + s3->grid - 1) / s3->grid > kR3)
-      return done(set_error(c, HS_E_SHAPE, "3-D slab planes too large for the solve kernel"));
     s3->nbuf = k3_smem(NBmax, s3->grid, 2) <= (size_t)optin ? 2 : 1;
-    const int smem = (int)k3_smem(NBmax, s3->grid, s3->nbuf);
-    if (smem > optin) return done(set_error(c, HS_E_SHAPE, "3-D slab planes too large for the solve kernel"));
     s3->optin = optin;
     S3_TRY(cudaFuncSetAttribute(k3_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, optin), "attr");
     int per = 0;
