@@ -212,6 +212,13 @@ int hs_exact_create(hs_ctx* ctx, const hs_stencil* op, hs_sweep** out);
  * singular pivot block, HS_E_SHAPE when the bandwidth exceeds block. */
 int hs_exact_create_csr(hs_ctx* ctx, int64_t n, int64_t nnz, const int64_t* indptr,
                         const int64_t* indices, const double* vals, int block, hs_sweep** out);
+/* The X plan cut where each front passes from one sweep-axis shard's slabs
+ * to the next (slab j on shard (j-1)*shards/J), one launch per shard step:
+ * the critical path of a relay in which every GPU owns its region's slabs
+ * and the traces hop between GPUs (here through the trace buffers on one
+ * device).  Results equal HS_VARIANT_X; *variant is the id to pass to
+ * hs_sweep_apply.  (the measured relay vs replication.) */
+int hs_sweep_plan_relay(hs_ctx* ctx, hs_sweep* s, int shards, int* variant);
 /* bytes of device memory held by the slab factors (diagnostic) */
 long long hs_sweep_factor_bytes(hs_sweep* s);
 /* slab-solve launches in one application of a variant's plan (diagnostic:

@@ -79,6 +79,7 @@ SIGNATURES = {
     "hs_exact_create_csr": (C.c_int, [_vp, C.c_int64, C.c_int64, _i64p, _i64p,
                                       C.POINTER(C.c_double), C.c_int, C.POINTER(_vp)]),
     "hs_sweep_plan_nx": (C.c_int, [_vp, _vp, C.c_int, _i64p, _i64p, C.POINTER(C.c_int)]),
+    "hs_sweep_plan_relay": (C.c_int, [_vp, _vp, C.c_int, C.POINTER(C.c_int)]),
     "hs_cycle_create": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_double, C.c_int, C.c_double,
                                   C.c_int, C.POINTER(_vp)]),
     "hs_cycle_create_lane": (C.c_int, [_vp, _vp, C.POINTER(_vp)]),

@@ -472,6 +472,11 @@ int hs_sweep_plan_nx(hs_ctx* c, hs_sweep* s, int ncell, const int64_t* j_cell,
   return sweep_plan_nx(c, s, ncell, j_cell, j_mid, variant);
 }
 
+int hs_sweep_plan_relay(hs_ctx* c, hs_sweep* s, int shards, int* variant) {
+  if (!c || !s || !variant) return HS_E_ARG;
+  return sweep_plan_relay(c, s, shards, variant);
+}
+
 long long hs_sweep_factor_bytes(hs_sweep* s) { return s ? s->factor_bytes : 0; }
 
 int hs_sweep_segments(hs_sweep* s) { return s && !s->s3 ? s->G : 1; }

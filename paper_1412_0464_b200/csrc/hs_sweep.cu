@@ -2531,6 +2531,98 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   return HS_OK;
 }
 
+// Relay emulation of a sweep-axis shard layout:
+// the X plan with every front cut where its slabs pass from one shard's
+// range to the next (slab j on shard (j-1) G / J), one launch per shard
+// step, the traces crossing a cut through the trace buffers -- the
+// critical path of a relay whose shards own their slabs, without the P2P
+// hop.  Same tasks, same results as the X plan.
+static std::vector<SweepLaunch> build_relay(Sweep* s, int G, int* ntin) {
+  const int J = s->J;
+  SchedBuilder b{s, J, s->hbeta.data(), s->hbt.data(), s->hlo.data(), s->hhi.data()};
+  auto shard = [&](const SweepTask& t) { return (int)((int64_t)t.slab * G / J); };
+  auto runs = [&](const std::vector<SweepTask>& v) {
+    std::vector<std::vector<SweepTask>> r;
+    for (const SweepTask& t : v) {
+      if (r.empty() || shard(r.back().back()) != shard(t)) r.emplace_back();
+      r.back().push_back(t);
+    }
+    return r;
+  };
+  auto zip = [&](const std::vector<std::vector<SweepTask>>& a,
+                 const std::vector<std::vector<SweepTask>>& c2) {
+    std::vector<std::vector<std::vector<SweepTask>>> st;
+    for (size_t k = 0; k < std::max(a.size(), c2.size()); ++k) {
+      std::vector<std::vector<SweepTask>> fr;
+      if (k < a.size()) fr.push_back(a[k]);
+      if (k < c2.size()) fr.push_back(c2[k]);
+      st.push_back(fr);
+    }
+    return st;
+  };
+  std::vector<SweepLaunch> plan;
+  const int jm = J / 2 + 1;
+  std::vector<SweepTask> F = b.fwd_chain(1, jm - 1), Bk = b.bwd_chain(J, jm + 1);
+  SweepTask mi = b.mid_in(jm);
+  const int in1 = b.want1(mi), in3 = b.want3(mi);
+  if (!F.empty()) b.give2(F.back(), in1);
+  if (!Bk.empty()) b.give4(Bk.back(), in3);
+  auto st1 = zip(runs(F), runs(Bk));
+  st1.push_back({{mi}});
+  b.emit(plan, 0, st1);
+  plan.push_back(SweepLaunch{SweepLaunch::kResidual});
+  SweepTask mo = b.mid_out(jm);
+  std::vector<SweepTask> BB = b.bwd_chain(jm - 1, 1), FF = b.fwd_chain(jm + 1, J);
+  if (!FF.empty()) b.give2(mo, FF.front().tin1);
+  if (!BB.empty()) b.give4(mo, BB.front().tin3);
+  // the middle solve heads both outward fronts (as in the X plan): it joins
+  // each front's first run, whichever shard the run's slabs are on
+  auto headed = [&](const std::vector<SweepTask>& v) {
+    std::vector<std::vector<SweepTask>> r = runs(v);
+    if (r.empty()) r.emplace_back();
+    r[0].insert(r[0].begin(), mo);
+    return r;
+  };
+  b.emit(plan, 1, zip(headed(BB), headed(FF)));
+  plan.push_back(SweepLaunch{SweepLaunch::kCombine});
+  *ntin = b.ntin;
+  return plan;
+}
+
+static int register_plan(Ctx* c, Sweep* s, std::vector<SweepLaunch>&& plan, size_t t0, int* variant) {
+  plan_bytes(s, plan);
+  if (!s->s3) {   // re-upload the task list (the plan indexes it)
+    SweepTask* d = nullptr;
+    const size_t tb = s->tasks.size() * sizeof(SweepTask);
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&d, tb);
+    if (e == cudaSuccess) e = cudaMemcpy(d, s->tasks.data(), tb, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaFree(d);
+      s->tasks.resize(t0);
+      return check_cuda(c, e, "task upload");
+    }
+    cudaFree(s->d_tasks);
+    s->d_tasks = d;
+  }
+  s->plan.push_back(std::move(plan));
+  *variant = (int)s->plan.size() - 1;
+  return HS_OK;
+}
+
+int sweep_plan_relay(Ctx* c, Sweep* s, int shards, int* variant) {
+  if (s->J % 2) return set_error(c, HS_E_SHAPE, "X-sweep needs an even subdomain count");
+  if (shards < 1 || shards > s->J) return set_error(c, HS_E_SHAPE, "shards must be in [1, J]");
+  const size_t t0 = s->tasks.size();
+  int ntin = 0;
+  std::vector<SweepLaunch> plan = build_relay(s, shards, &ntin);
+  if (ntin > std::max(1, s->ntrace) || s->tasks.size() > (size_t)kMaxTasks * 64) {
+    s->tasks.resize(t0);
+    return set_error(c, HS_E_SHAPE, "relay plan does not fit the sweep's buffers");
+  }
+  return register_plan(c, s, std::move(plan), t0, variant);
+}
+
 int sweep_plan_nx(Ctx* c, Sweep* s, int ncell, const int64_t* jc, const int64_t* jm,
                   int* variant) {
   const int J = s->J;
@@ -2571,23 +2663,7 @@ int sweep_plan_nx(Ctx* c, Sweep* s, int ncell, const int64_t* jc, const int64_t*
   }
   if (s->tasks.size() > (size_t)kMaxTasks * 64)
     return undo(set_error(c, HS_E_SHAPE, "too many NX plans on one sweep"));
-  plan_bytes(s, plan);
-  if (!s->s3) {   // re-upload the task list (the plan indexes it)
-    SweepTask* d = nullptr;
-    const size_t tb = s->tasks.size() * sizeof(SweepTask);
-    cudaError_t e = cudaStreamSynchronize(c->stream);
-    if (e == cudaSuccess) e = cudaMalloc((void**)&d, tb);
-    if (e == cudaSuccess) e = cudaMemcpy(d, s->tasks.data(), tb, cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) {
-      cudaFree(d);
-      return undo(check_cuda(c, e, "NX task upload"));
-    }
-    cudaFree(s->d_tasks);
-    s->d_tasks = d;
-  }
-  s->plan.push_back(std::move(plan));
-  *variant = (int)s->plan.size() - 1;
-  return HS_OK;
+  return register_plan(c, s, std::move(plan), t0, variant);
 }
 
 void sweep_destroy(Sweep* s) {

@@ -130,6 +130,8 @@ void sweep3_destroy(Sweep3* s3);
 // (hs_sweep3.cu) behind the sweep interface -- plan HS_VARIANT_UD is a single
 // slab solve over every row.
 int exact_create(Ctx* c, const Stencil* op, Sweep** out);
+// X plan cut at sweep-axis shard boundaries (relay emulation; hs_sweep.cu)
+int sweep_plan_relay(Ctx* c, Sweep* s, int shards, int* variant);
 // the same for a general sparse matrix in host CSR with block size NB >= its
 // bandwidth (factorize(scipy matrix)); vectors hold ceil(n / NB) * NB entries
 int exact_create_csr(Ctx* c, int64_t n, int64_t nnz, const int64_t* indptr, const int64_t* indices,

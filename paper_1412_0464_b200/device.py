@@ -247,8 +247,19 @@ class DeviceSweep(_Handle):
             plans[key] = int(v.value)
         return plans[key]
 
+    def relay_variant(self, shards: int) -> int:
+        """Variant id of the X plan cut at `shards` sweep-axis shard
+        boundaries (hs_sweep_plan_relay: the relay's critical path on one
+        device); registered once per shard count."""
+        plans = self.__dict__.setdefault("_relay_plans", {})
+        if shards not in plans:
+            v = C.c_int()
+            self.ctx.call("hs_sweep_plan_relay", self.h, int(shards), C.byref(v))
+            plans[shards] = int(v.value)
+        return plans[shards]
+
     def apply(self, f, variant="x", cells=None):
-        v = self.variant_id(variant, cells)
+        v = variant if isinstance(variant, int) else self.variant_id(variant, cells)
         ft, was_np = to_device(f, self.n, self.ctx)
         u = empty(self.n, self.ctx)
         self.ctx.call("hs_sweep_apply", self.h, v, ptr(ft), ptr(u))

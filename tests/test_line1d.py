@@ -187,3 +187,34 @@ def test_gmres_with_host_callables(rng):
     u, rep = hb.gmres(lambda v: a @ v, None, bb, hb.GmresConfig(tol=1e-12, max_iter=n))
     assert np.linalg.norm(a @ u - bb) / np.linalg.norm(bb) < 1e-10
     assert np.all(np.diff(rep.residual_history) <= 1e-14)
+
+
+@pytest.mark.gpu
+def test_relay_plan_equals_x_sweep():
+    """the X plan cut at sweep-axis shard boundaries (hs_sweep_plan_relay,
+    the relay's critical path) gives bitwise the X sweep's result (one face
+    segment at C1); C2's two-segment layout agrees to rounding"""
+    import torch
+    import paper_1412_0464_b200 as hb
+    from paper_1412_0464_b200.configs import config
+    from paper_1412_0464_b200.device import empty, ptr, to_device
+    p = config(0)
+    hh = hb.build_hierarchy(p.mesh, p.model, None, hb.SmootherConfig(p.omega_jac, p.nu),
+                            hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains))
+    sw = hh.partition.device()
+    f, _ = to_device(crand(np.random.default_rng(3), sw.n), sw.n)
+    ux = sw.apply(f, "x")[0]
+    for g in (2, 3, 8):
+        u = sw.apply(f, sw.relay_variant(g))[0]
+        assert torch.equal(u, ux), g
+        assert sw.ctx.lib.hs_sweep_plan_launches(sw.h, sw.relay_variant(g)) > \
+            sw.ctx.lib.hs_sweep_plan_launches(sw.h, sw.variant_id("x"))
+    p = config(1)
+    hh = hb.build_hierarchy(p.mesh, p.model, None, hb.SmootherConfig(p.omega_jac, p.nu),
+                            hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains))
+    sw = hh.partition.device()
+    f, _ = to_device(crand(np.random.default_rng(4), sw.n), sw.n)
+    ux = sw.apply(f, "x")[0]
+    for g in (2, 4):
+        u = sw.apply(f, sw.relay_variant(g))[0]
+        assert float(torch.linalg.norm(u - ux) / torch.linalg.norm(ux)) < 1e-12, g
