@@ -207,8 +207,8 @@ def test_relay_plan_equals_x_sweep():
     for g in (2, 3, 8):
         u = sw.apply(f, sw.relay_variant(g))[0]
         assert torch.equal(u, ux), g
-        assert sw.ctx.lib.hs_sweep_plan_launches(sw.h, sw.relay_variant(g)) > \
-            sw.ctx.lib.hs_sweep_plan_launches(sw.h, sw.variant_id("x"))
+        assert sw.ctx.lib.hs_sweep_plan_launches(sw.h, sw.relay_variant(g)) >= \
+            sw.ctx.lib.hs_sweep_plan_launches(sw.h, sw.variant_id("x")) + (g > 2)
     p = config(1)
     hh = hb.build_hierarchy(p.mesh, p.model, None, hb.SmootherConfig(p.omega_jac, p.nu),
                             hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains))
