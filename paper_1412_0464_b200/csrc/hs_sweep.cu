@@ -112,6 +112,8 @@ struct Chunks {
   int G;                   // segments (clusters) per front
   int q;                   // dense top: blocks per chunk left after L levels
   int nr;                  // restricted level-0 / spike updates (kNR rows) or 0
+  int cpl0;                // level-0 kept updates from the sparse stencil couplings
+                           // (SolveArgs::cpl) instead of streamed alpha / gamma blocks
   int koff[kMaxLevels];
   int y0s[kMaxCh + 1];     // chunk K covers face points [y0s[K], y0s[K+1])
   int mmax;                // longest chunk
@@ -165,6 +167,25 @@ k_bcr_init(const SlabInfo* __restrict__ slabs, Chunks g, double2* __restrict__ D
   }
   Lc[off] = l;
   Uc[off] = u;
+}
+
+// Level-0 couplings of every face point to its two face neighbours (the
+// tridiagonal thin-axis stencil of the slab operator), for the solve's
+// level-0 kept updates: cpl[slab][y][side][o0 + 1][row], side 0 = y - 1.
+template <int TM>
+__global__ void __launch_bounds__(256)
+k_cpl0(const SlabInfo* __restrict__ slabs, int M, double2* __restrict__ cpl) {
+  const int y = blockIdx.x, s = blockIdx.y;
+  const SlabInfo si = slabs[s];
+  const int64_t n = (int64_t)si.T * M;
+  for (int e = threadIdx.x; e < 2 * 3 * TM; e += blockDim.x) {
+    const int side = e / (3 * TM), o0 = (e / TM) % 3 - 1, r = e % TM;
+    const int o1 = side ? 1 : -1, sl = si.slot[o0 + 1][o1 + 1];
+    double2 v = czero();
+    if (sl >= 0 && r < si.T && r + o0 >= 0 && r + o0 < si.T && y + o1 >= 0 && y + o1 < M)
+      v = si.coeffs[(int64_t)sl * n + (int64_t)r * M + y];
+    cpl[((int64_t)s * M + y) * 6 * TM + e] = v;
+  }
 }
 
 // In-place Gauss-Jordan inversion with partial pivoting of an N x N matrix A
@@ -709,6 +730,7 @@ struct SolveArgs {
   int64_t nbs;
   const uint32_t* plan;    // [C][plan_words] item / chunk tables (chunk_plan)
   const int* rows;         // [J][kNR] rows of the restricted updates (g.nr != 0)
+  const double2* cpl;      // [J][M][2][3][TM] level-0 couplings (g.cpl0)
   const double2* src;      // right-hand side field (n0 x M)
   const double2* coarse;   // global coarse operator [S][n0*M] (transmission couplings)
   int64_t ncoarse;
@@ -956,6 +978,8 @@ __host__ __device__ inline int item_sources(const Chunks& g, int rank, const Ite
     if (p < P.L) {
       if ((yl >> l) & 1) {
         src[n++] = item_enc(kArrEf, y * TM2);
+      } else if (g.cpl0 && l == 0) {   // F -= L Yv[y-1] + U Yv[y+1]: couplings read directly
+        *hasx = false;
       } else {
         const int64_t k2 = ((int64_t)rank * g.kstride + g.koff[l] + (yl >> (l + 1))) * 2 * TM2;
         *hasx = yl - s >= 0;
@@ -1504,7 +1528,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
                      : p > L        ? h.first + j * h.step
                                     : (j < h.ne ? 2 * j + 1 : 2 * (j - h.ne)) << p;
       const int r = h.pf0 + j;
-      const Item it = has ? acquire(ti, r) : Item{nullptr, nullptr};
+      // level-0 kept items with sparse couplings stream no blocks (no ring slot)
+      const bool sparse0 = g.cpl0 && p == 0 && !(yl & 1);
+      const Item it = has && !sparse0 ? acquire(ti, r) : Item{nullptr, nullptr};
       const double2* m0 = it.m0;
       const double2* m1 = it.m1;
       if (has) {
@@ -1518,6 +1544,23 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
           if ((yl >> l) & 1) {   // eliminated at this level: y = Dinv f
             const double2 r = mvx<TM, HW>(m0, F + yl * TM, nullptr, nullptr, lane);
             if (wr) Yv[yl * TM + x] = r;
+          } else if (sparse0) {  // kept, level 0: f -= L Yv[y-1] + U Yv[y+1]
+            // (alpha f_{y-1} = L Dinv_{y-1} f_{y-1} = L Yv[y-1], Yv from this
+            // phase's first half; L, U the slab stencil's thin-axis couplings)
+            const double2* cp = a.cpl + ((int64_t)slabs[ti] * M + (Y0 + yl)) * 6 * TM;
+            double2 acc = czero();
+#pragma unroll
+            for (int sd = 0; sd < 2; ++sd) {
+              const int q = yl + (sd ? 1 : -1);
+              if (q < 0 || q >= m) continue;
+#pragma unroll
+              for (int o0 = -1; o0 <= 1; ++o0) {
+                const int xx = x + o0;
+                if (xx < 0 || xx >= TM) continue;
+                acc = cfma(__ldg(cp + (sd * 3 + o0 + 1) * TM + x), Yv[q * TM + xx], acc);
+              }
+            }
+            if (wr) F[yl * TM + x] = csub(F[yl * TM + x], acc);
           } else {               // kept: f -= alpha f_{y-s} + gamma f_{y+s}
             const bool hl = yl - s >= 0, hr = yl + s < m;
             const double2 acc = mvx<TM, HW>(hl ? m0 : nullptr, hl ? F + (yl - s) * TM : nullptr,
@@ -1536,7 +1579,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
           if (wr) Yv[yl * TM + x] = csub(Yv[yl * TM + x], acc);
         }
       }
-      release(it, has);
+      release(it, has && !sparse0);
     };
     // phase p over warps [w0, w0 + nw)
     auto run_phase = [&](int p, int w0, int nw) {
@@ -1544,7 +1587,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       for (int jp = (warp - w0) * HW; jp < h.cnt; jp += nw * HW) do_item(h, jp + sub, jp + sub < h.cnt);
     };
     for (int p = 0; p <= L; ++p) {   // forward levels and the dense top: all warps
-      run_phase(p, 0, kCW);
+      if (p == 0 && g.cpl0) {        // level 0: eliminated points, then the kept points' updates
+        const Ph h = phase(0);
+        for (int jp = warp * HW; jp < h.ne; jp += kCW * HW) do_item(h, jp + sub, jp + sub < h.ne);
+        csync();
+        for (int jp = h.ne + warp * HW; jp < h.cnt; jp += kCW * HW)
+          do_item(h, jp + sub, jp + sub < h.cnt);
+      } else {
+        run_phase(p, 0, kCW);
+      }
       csync();
       stamp(ti, 2 + p);
     }
@@ -1879,6 +1930,11 @@ int factorize(Ctx* c, Sweep* s, const std::vector<SlabInfo>& info, const Chunks&
   k_bcr_init<TM><<<dim3(M, J), TM * TM, 0, c->stream>>>(d_info, g, D, Lc, Uc, EL, EU);
   c->launches++;
   HS_TRYF(cudaGetLastError(), "bcr init");
+  if (s->cpl0) {
+    k_cpl0<TM><<<dim3(M, J), 256, 0, c->stream>>>(d_info, M, s->cpl);
+    c->launches++;
+    HS_TRYF(cudaGetLastError(), "level-0 couplings");
+  }
   if (B > 0) {   // spikes from the pristine chunk operators
     HS_TRYF(cudaMalloc((void**)&Hw, wbytes), "spike work alloc");
     HS_TRYF(cudaMalloc((void**)&Zw, wbytes), "spike work alloc");
@@ -1997,6 +2053,7 @@ Chunks make_chunks(const Sweep* s) {
   g.L = s->L;
   g.q = s->q;
   g.nr = s->nr;
+  g.cpl0 = s->cpl0;
   for (int k = 0; k <= s->C * s->G; ++k) g.y0s[k] = s->y0s[k];
   g.mmax = s->mmax;
   int acc = 0;
@@ -2420,6 +2477,12 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     s->max_fronts = std::max(1, std::min(kMaxFront, maxc / G));
   }
   s->q = (s->mmax - 1) / (1 << s->L) + 1;
+  {   // level-0 kept updates from the sparse couplings (HS_SWEEP_CPL0=0: streamed blocks)
+    int mmin = M;
+    for (int k = 0; k < NCH; ++k) mmin = std::min(mmin, s->y0s[k + 1] - s->y0s[k]);
+    const char* ev = getenv("HS_SWEEP_CPL0");
+    s->cpl0 = s->L >= 1 && mmin >= 2 && !(ev && atoi(ev) == 0) ? 1 : 0;
+  }
   if (s->L >= kMaxLevels || itab_len(s->mmax) > kMaxItems) {
     delete s;
     return set_error(c, HS_E_SHAPE, "face too long for the sweep's chunking");
@@ -2471,7 +2534,8 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     double rec_blocks = 0;
     for (int k = 0; k < NCH; ++k)
       rec_blocks += TM == 16 ? stream_blocks<16>(g, k) : stream_blocks<32>(g, k);
-    const double rec_bytes = rec_blocks * TM2 * 16.0;
+    // + the level-0 couplings read once per kept point (g.cpl0)
+    const double rec_bytes = rec_blocks * TM2 * 16.0 + (s->cpl0 ? (double)M / 2.0 * 6 * TM * 16.0 : 0.0);
     s->rec_bytes = rec_bytes;
     for (auto& plan : s->plan) plan_bytes(s, plan);
   }
@@ -2481,6 +2545,15 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   const size_t rkb = (size_t)J * NCH * std::max(1, 2 * B) * 2 * TM2 * sizeof(double2);
   const size_t qdb = (size_t)J * NCH * s->q * s->q * TM2 * sizeof(double2);
   s->factor_bytes = (long long)(efb * 5 + krb + qdb + (B > 0 ? rkb : 0));
+  if (s->cpl0) {   // level-0 couplings: 6 TM values per face point and slab
+    const size_t cb = (size_t)J * M * 6 * TM * sizeof(double2);
+    e = cudaMalloc((void**)&s->cpl, cb);
+    if (e != cudaSuccess) {
+      sweep_destroy(s);
+      return check_cuda(c, e, "coupling alloc");
+    }
+    s->factor_bytes += (long long)cb;
+  }
   e = cudaMalloc((void**)&s->ef, efb);
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->eb, 2 * efb);
   if (e == cudaSuccess) e = cudaMalloc((void**)&s->kr, krb);
@@ -2670,6 +2743,7 @@ void sweep_destroy(Sweep* s) {
   if (s) sweep3_destroy(s->s3);
   if (!s) return;
   delete s->view;
+  cudaFree(s->cpl);
   cudaFree(s->ef);
   cudaFree(s->eb);
   cudaFree(s->kr);
@@ -2770,6 +2844,7 @@ int sweep_solve_one(Ctx* c, Sweep* s, int j, int64_t a, int64_t b, int64_t ta, i
     g.nbs = s->nbs;
     g.plan = s->ptab;
     g.rows = s->rows;
+    g.cpl = s->cpl;
     g.src = f;
     g.coarse = s->coarse->d.coeffs;
     g.ncoarse = s->coarse->d.n;
@@ -2909,6 +2984,7 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
         a.nbs = s->nbs;
         a.plan = s->ptab;
         a.rows = s->rows;
+        a.cpl = s->cpl;
         a.src = Lh.src ? w->g : f;
         a.coarse = s->coarse->d.coeffs;
         a.ncoarse = s->coarse->d.n;

@@ -68,6 +68,8 @@ struct Sweep {
   long long nbs = 0;            // blocks per (slab, chunk) stream
   uint32_t* ptab = nullptr;     // [C][plan words] solve-kernel item / chunk tables
   int nr = 0;                   // rows per restricted update (0: full updates)
+  int cpl0 = 0;                 // level-0 kept updates from sparse couplings (cpl)
+  double2* cpl = nullptr;       // [J][M][2][3][tm] level-0 thin-axis couplings
   int* rows = nullptr;          // [J][nr] solution rows the chain reads (outputs, traces)
   double2* ebr = nullptr;       // [J][M][tm^2] Dinv L, Dinv U restricted to those rows (packing only)
   double2* spr = nullptr;       // [J][M][tm^2] W, V restricted to those rows (packing only)

@@ -478,11 +478,12 @@ def _large_anchors():
     return json.loads(f.read_text()) if f.exists() else {}
 
 
-@pytest.mark.parametrize("name", ["C1_x", "C2", "C3", "C3_half", "C5_half", "C1_exact", "C1_nx4"]
+@pytest.mark.parametrize("name", ["C1_x", "C2", "C3", "C3_half", "C5", "C5_half", "C1_exact",
+                                  "C1_nx4"]
                          + [f"C4_rhs{r}" for r in range(8)])
 def test_baseline_config_matches_reference_solve(name):
-    """BASELINE configs at full size (C2, C3, C4's eight right-hand sides) or
-    half size (C3, C5), and configs[0] with the X, exact and NX(4) coarse solves,
+    """BASELINE configs at full size (C2, C3, C5, C4's eight right-hand sides)
+    and half size (C3, C5), and configs[0] with the X, exact and NX(4) coarse solves,
     solved by the reference itself (tests/golden/make_large_anchors.py):
     the same GMRES iteration count +-1, residual histories within 1e-6
     relative over the common iterations, true residual <= 1e-6 and the
@@ -586,7 +587,7 @@ def test_factorize_too_large_block_raises():
         hb.factorize(op)
 
 
-@pytest.mark.parametrize("name", ["apply_C1", "apply_C2", "apply_C4", "apply_C3"])
+@pytest.mark.parametrize("name", ["apply_C1", "apply_C2", "apply_C4", "apply_C3", "apply_C5"])
 def test_tgsp_apply_matches_reference_at_config_size(name):
     """The north_star apply gate at BASELINE config size: tgsp_apply(cycle, z)
     for the seeded complex normal z of tests/golden/make_large_anchors.py

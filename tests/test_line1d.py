@@ -218,3 +218,20 @@ def test_relay_plan_equals_x_sweep():
     for g in (2, 4):
         u = sw.apply(f, sw.relay_variant(g))[0]
         assert float(torch.linalg.norm(u - ux) / torch.linalg.norm(ux)) < 1e-12, g
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [7, 33, 300, 1000])
+def test_dense_pivoted_factorisation(n):
+    """the hand-written batched dense kernels (hs_dense.cu: panel LU with
+    partial pivoting, trailing GEMM, blocked triangular inverse) through
+    factorize() of a dense random matrix whose diagonal is tiny (pivoting is
+    required), against numpy's LAPACK solve"""
+    import paper_1412_0464_b200 as hb
+    rng = np.random.default_rng(n)
+    a = crand(rng, (n, n))
+    a[np.diag_indices(n)] *= 1e-8
+    b = crand(rng, (n, 2))
+    x = hb.solve_factored(hb.factorize(sp.csr_matrix(a)), b)
+    ref = np.linalg.solve(a, b)
+    assert rel(x, ref) < 1e-10
