@@ -45,6 +45,8 @@ struct Sweep3 {
   int optin = 0;                       // opt-in shared memory per block
   int grid = 0;                        // CTAs of the solve kernel (one per SM)
   int nbuf = 1;                        // staging buffers of the solve kernel
+  int nbmax = 0;                       // largest plane block
+  int gemv_grid = 0;                   // resident CTAs of k3_gemv (set on first use)
   long long bytes = 0;
 };
 
@@ -133,46 +135,60 @@ __global__ void k3_rhs(SweepTask t, int n0, int n1, int n2, const double2* __res
   F[(int64_t)i1 * NB + r] = v;
 }
 
-// w_i = Dinv_i f_i for every plane i1 (row-major Dinv): the slab solve's
-// first step, independent of the block recursion.  One CTA per 32 rows of a
-// plane; each warp owns 4 rows (4 independent accumulators, 16-B lane loads
-// of contiguous row segments), the plane's f is staged in shared memory.
-// HBM-bound: n1 NB^2 16 B per call.  Fixed reduction order (bitwise
-// reproducible).
+// w_i = Dinv_i f_i for every plane i1 (row-major Dinv) of one or two slab
+// solves (the two fronts' tasks): the slab solve's first step, independent
+// of the block recursion.  Persistent grid (a whole number of resident
+// waves) striding over (task, plane, 32-row block) items -- a launch of one
+// CTA per item left a 20%-full third wave; each warp owns 4 rows (4
+// independent accumulators, 16-B lane loads of contiguous row segments), the
+// plane's f is staged in shared memory.  HBM-bound: n1 NB^2 16 B per task.
+// Fixed reduction order (bitwise reproducible, the same sums as before).
 constexpr int kGvRows = 32;
-__global__ void __launch_bounds__(256) k3_gemv(const double2* __restrict__ Dinv,
-                                              const double2* __restrict__ F, double2* __restrict__ Y,
-                                              int NB) {
+struct GemvTask {
+  const double2* Dinv;
+  const double2* F;
+  double2* Y;
+  int NB, nrb;   // rows per plane, 32-row blocks per plane
+};
+__global__ void __launch_bounds__(256) k3_gemv(GemvTask t0, GemvTask t1, int n1, int64_t items0,
+                                              int64_t items) {
   extern __shared__ __align__(16) double2 fv[];
-  const int i1 = blockIdx.y;
-  const int64_t nb2 = (int64_t)NB * NB;
-  const double2* f = F + (int64_t)i1 * NB;
-  for (int c = threadIdx.x; c < NB; c += blockDim.x) fv[c] = __ldg(f + c);
-  __syncthreads();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int r0 = blockIdx.x * kGvRows + warp * 4;
-  const double2* A = Dinv + (int64_t)i1 * nb2;
-  double2 acc[4] = {czero(), czero(), czero(), czero()};
-  const int nr = max(0, min(4, NB - r0));
-  if (nr == 4) {
-    const double2* a0 = A + (int64_t)r0 * NB;
-    for (int c = lane; c < NB; c += 32) {
-      const double2 v = fv[c];
-      acc[0] = cfma(__ldcs(a0 + c), v, acc[0]);
-      acc[1] = cfma(__ldcs(a0 + NB + c), v, acc[1]);
-      acc[2] = cfma(__ldcs(a0 + 2 * NB + c), v, acc[2]);
-      acc[3] = cfma(__ldcs(a0 + 3 * NB + c), v, acc[3]);
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const bool second = it >= items0;
+    const GemvTask& t = second ? t1 : t0;
+    const int64_t loc = second ? it - items0 : it;
+    const int i1 = (int)(loc / t.nrb), rb = (int)(loc - (int64_t)i1 * t.nrb);
+    const int NB = t.NB;
+    const int64_t nb2 = (int64_t)NB * NB;
+    __syncthreads();   // the previous item's readers of fv are done
+    const double2* f = t.F + (int64_t)i1 * NB;
+    for (int c = threadIdx.x; c < NB; c += blockDim.x) fv[c] = __ldg(f + c);
+    __syncthreads();
+    const int r0 = rb * kGvRows + warp * 4;
+    const double2* A = t.Dinv + (int64_t)i1 * nb2;
+    double2 acc[4] = {czero(), czero(), czero(), czero()};
+    const int nr = max(0, min(4, NB - r0));
+    if (nr == 4) {
+      const double2* a0 = A + (int64_t)r0 * NB;
+      for (int c = lane; c < NB; c += 32) {
+        const double2 v = fv[c];
+        acc[0] = cfma(__ldcs(a0 + c), v, acc[0]);
+        acc[1] = cfma(__ldcs(a0 + NB + c), v, acc[1]);
+        acc[2] = cfma(__ldcs(a0 + 2 * NB + c), v, acc[2]);
+        acc[3] = cfma(__ldcs(a0 + 3 * NB + c), v, acc[3]);
+      }
+    } else {
+      for (int k = 0; k < nr; ++k) {
+        const double2* ar = A + (int64_t)(r0 + k) * NB;
+        for (int c = lane; c < NB; c += 32) acc[k] = cfma(__ldcs(ar + c), fv[c], acc[k]);
+      }
     }
-  } else {
-    for (int k = 0; k < nr; ++k) {
-      const double2* a = A + (int64_t)(r0 + k) * NB;
-      for (int c = lane; c < NB; c += 32) acc[k] = cfma(__ldcs(a + c), fv[c], acc[k]);
-    }
-  }
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
-    for (int m = 16; m > 0; m >>= 1) acc[k] = cadd(acc[k], shfl_xor_c(acc[k], m));
-  if (lane < nr) Y[(int64_t)i1 * NB + r0 + lane] = acc[lane];
+    for (int k = 0; k < 4; ++k)
+      for (int m = 16; m > 0; m >>= 1) acc[k] = cadd(acc[k], shfl_xor_c(acc[k], m));
+    if (lane < nr) t.Y[(int64_t)i1 * NB + r0 + lane] = acc[lane];
+  }
 }
 
 // u rows [ta, tb) and the outgoing traces (subdom_solve steps 4-5)
@@ -427,6 +443,7 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
   if (int r = slots3(coarse, s3->cslot, c)) return r;
   int NBmax = 0;
   for (int j = 0; j < J; ++j) NBmax = std::max(NBmax, (int)(hi[j] - lo[j] + 1) * n2);
+  s3->nbmax = NBmax;
   // the solve kernel's limits first (nothing is factorised for a plane it cannot solve)
   s3->grid = c->num_sms;
   int optin = 0;
@@ -620,6 +637,8 @@ int sweep3_tasks(Ctx* c, Sweep* s, const SweepTask* const* ts, int nt, const dou
   }
   size_t smem = 0;
   K3Chain ch[2] = {};
+  GemvTask gv[2] = {};
+  double gemv_bytes = 0;
   for (int k = 0; k < nt; ++k) {
     const SweepTask& t = *ts[k];
     const int j = t.slab, nb = NB[k];
@@ -628,16 +647,30 @@ int sweep3_tasks(Ctx* c, Sweep* s, const SweepTask* const* ts, int nt, const dou
     k3_rhs<<<(unsigned)((tot + kT3 - 1) / kT3), kT3, 0, c->stream>>>(
         t, s->n0, n1, n2, src, coarse_coeffs, coarse_n, to_slots(s3->cslot), s->trace, s3->F[k]);
     HS_LAUNCH_CHECK(c, "3-D rhs");
-    {   // w_i = Dinv_i f_i for every plane: one batched GEMV (Dinv stored row-major)
-      ProfScope ps(c, K_SWEEP_GATHER, (double)n1 * nb2 * 16.0);
-      k3_gemv<<<dim3((unsigned)((nb + kGvRows - 1) / kGvRows), (unsigned)n1), 256,
-                (size_t)nb * sizeof(double2), c->stream>>>(s3->dinv[j], s3->F[k], s3->Y[k], nb);
-      HS_LAUNCH_CHECK(c, "3-D batched GEMV");
-    }
+    gv[k] = GemvTask{s3->dinv[j], s3->F[k], s3->Y[k], nb, (nb + kGvRows - 1) / kGvRows};
+    gemv_bytes += (double)n1 * nb2 * 16.0;
     ch[k] = K3Chain{s3->T[j], s3->gf[j], s3->xf[j], s3->Y[k], s3->gbar + k, nbuf[k]};
     smem = std::max(smem, k3_smem(nb, nt == 2 ? (k ? G - g0 : g0) : G, nbuf[k]));
   }
   if (nt == 1) ch[1] = ch[0];
+  {   // w_i = Dinv_i f_i for every plane of both tasks: one persistent GEMV launch
+    ProfScope ps(c, K_SWEEP_GATHER, gemv_bytes);
+    const int64_t items0 = (int64_t)n1 * gv[0].nrb;
+    const int64_t items = items0 + (nt == 2 ? (int64_t)n1 * gv[1].nrb : 0);
+    if (nt == 1) gv[1] = gv[0];
+    const int nbm = std::max(gv[0].NB, gv[1].NB);
+    if (!s3->gemv_grid) {   // resident CTAs of the GEMV at the largest plane
+      int per = 0;
+      S3_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k3_gemv, 256,
+                                                           (size_t)s3->nbmax * sizeof(double2)),
+             "gemv occupancy");
+      s3->gemv_grid = std::max(1, per) * c->num_sms;
+    }
+    const unsigned grid = (unsigned)std::min<int64_t>(items, s3->gemv_grid);
+    k3_gemv<<<grid, 256, (size_t)nbm * sizeof(double2), c->stream>>>(gv[0], gv[1], n1, items0,
+                                                                      items);
+    HS_LAUNCH_CHECK(c, "3-D batched GEMV");
+  }
   // profiler: the chain kernel (and the output scatter) as sweep_front, with
   // its algorithmic bytes -- both factor planes of every step + Y in/out
   double chain_bytes = 0;
