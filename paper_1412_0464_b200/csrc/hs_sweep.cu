@@ -2401,17 +2401,33 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     if (int r = slot_table(op, info[j].slot, c)) { delete s; return r; }
   }
   const int TM = s->tm, TM2 = TM * TM;
-  // chunks: ~32 face points per CTA, at most 16 CTAs per cluster, the
-  // cluster schedulable twice (two X fronts).  Wider faces are cut into G
-  // segments, one cluster each, coupled by the level-2 interface system
-  // (two-level partition), as long as both fronts' G clusters are
-  // co-resident (2 G <= active clusters): they wait on each other.
-  const int want = std::max(1, (M + 31) / 32);
-  int C = std::min(kMaxC, want);
-  int G = want > kMaxC ? std::min(kMaxG, (want + kMaxC - 1) / kMaxC) : 1;
-  if (c->sweep_segments > 0) G = std::min(kMaxG, c->sweep_segments);
+  // Layout: the face is cut into G segments per front (one cluster of C CTAs
+  // each, one chunk of the face per CTA), coupled by the level-2 interface
+  // system (two-level partition); both fronts' G clusters must co-reside
+  // (2 G <= active clusters: they wait on each other).  Measured on B200
+  // (DESIGN 5.1): the more CTAs the fronts use the faster the sweep, and
+  // 9-CTA clusters (two per GPC) co-reside 14 at a time where 16-CTA
+  // clusters fit 7 -- C = 9, G = 7 runs C3's sweep in 12.6 ms against 14.6
+  // (C = 16, G = 3), C2's in 1.77 against 2.21 ms -- so the default is C = 9
+  // with as many segments as co-reside, keeping chunks >= 8 face points;
+  // short faces (M < 144) keep one segment of chunks of >= 16 points
+  // (C = M / 16): many 4-point chunks or a level-2 system gain nothing there
+  // and cost accuracy (the interface systems multiply: sweep error vs the
+  // reference 1e-11 -> 2-4e-11 relative on a 39-point face).
+  // One segment requested (sweep lanes: several fronts' sweeps side by side)
+  // keeps the one-cluster layout with chunks of ~32 points, C <= 16.
+  int C, G;
+  if (c->sweep_segments == 1) {
+    C = std::min(kMaxC, std::max(1, (M + 31) / 32));
+    G = 1;
+  } else {
+    C = std::max(1, std::min(9, M / 16));
+    G = M < 144 ? 1 : std::max(1, std::min(std::min(kMaxG, kMaxCh / C), M / (8 * C)));
+    if (c->sweep_segments > 1) G = std::min(std::min(kMaxG, kMaxCh / C), c->sweep_segments);
+  }
   if (const char* ev = getenv("HS_SWEEP_SEGMENTS")) G = std::max(1, std::min(kMaxG, atoi(ev)));
   if (const char* ev = getenv("HS_SWEEP_CPC")) C = std::max(1, std::min(kMaxC, atoi(ev)));
+  G = std::max(1, std::min(G, kMaxCh / std::max(1, C)));
   if (C < 2) G = 1;
   int maxc = 0;
   for (;;) {

@@ -192,8 +192,10 @@ def test_gmres_with_host_callables(rng):
 @pytest.mark.gpu
 def test_relay_plan_equals_x_sweep():
     """the X plan cut at sweep-axis shard boundaries (hs_sweep_plan_relay,
-    the relay's critical path) gives bitwise the X sweep's result (one face
-    segment at C1); C2's two-segment layout agrees to rounding"""
+    the relay's critical path) gives the X sweep's result (bitwise with one
+    face segment; with the two-level partition a front's first task after a
+    cut reads its trace from global memory instead of the level-2 edge
+    values: equal to rounding)"""
     import torch
     import paper_1412_0464_b200 as hb
     from paper_1412_0464_b200.configs import config
@@ -206,7 +208,10 @@ def test_relay_plan_equals_x_sweep():
     ux = sw.apply(f, "x")[0]
     for g in (2, 3, 8):
         u = sw.apply(f, sw.relay_variant(g))[0]
-        assert torch.equal(u, ux), g
+        if sw.segments == 1:
+            assert torch.equal(u, ux), g
+        else:
+            assert float(torch.linalg.norm(u - ux) / torch.linalg.norm(ux)) < 1e-12, g
         assert sw.ctx.lib.hs_sweep_plan_launches(sw.h, sw.relay_variant(g)) >= \
             sw.ctx.lib.hs_sweep_plan_launches(sw.h, sw.variant_id("x")) + (g > 2)
     p = config(1)
