@@ -55,7 +55,10 @@ namespace {
 constexpr int kMaxLevels = 16;     // local BCR levels: chunks up to 65536 points
 constexpr int kWarps = 16;        // 15 consumer warps + 1 TMA producer warp
 constexpr int kCW = kWarps - 1;
-constexpr int kNA = 8;             // consumer warps of the back substitution while the rest
+#ifndef HS_SWEEP_NA
+#define HS_SWEEP_NA 8
+#endif
+constexpr int kNA = HS_SWEEP_NA;   // consumer warps of the back substitution while the rest
                                    // run the interface GEMV (group B = kCW - kNA warps)
 #ifndef HS_SWEEP_PREFETCH
 #define HS_SWEEP_PREFETCH 0
