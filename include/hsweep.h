@@ -243,6 +243,13 @@ int hs_cycle_create_lane(hs_ctx* ctx, const hs_cycle* base, hs_cycle** out);
 int hs_cycle_destroy(hs_ctx* ctx, hs_cycle* c);
 /* u = M f : vcycle / tgsp_apply / as_preconditioner   twogrid.py:150-176 */
 int hs_vcycle(hs_ctx* ctx, hs_cycle* c, const void* f, void* u);
+/* GMRES operator application keeping the preconditioned vector: z = M f,
+ * w = A z, in parts like hs_vcycle_apply_a_part (0 pre-coarse into z, 1 the
+ * sweep's first launch, 2 the rest and w = A z) or whole (part 3).  With the
+ * z of every Arnoldi step kept, the end of a GMRES cycle updates u += Z y
+ * instead of applying M once more to V y (M is linear and fixed: the same
+ * update, one V-cycle fewer per restart cycle; krylov.py:96-101). */
+int hs_vcycle_apply_az_part(hs_ctx* ctx, hs_cycle* c, const void* f, void* z, void* w, int part);
 /* w = A M f (the GMRES operator, krylov.py:125-126) */
 int hs_vcycle_apply_a(hs_ctx* ctx, hs_cycle* c, const void* f, void* w);
 /* The same operator in two halves, so a host pipelining the Arnoldi loop can

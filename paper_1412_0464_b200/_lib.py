@@ -89,6 +89,7 @@ SIGNATURES = {
     "hs_vcycle_apply_a_begin": (C.c_int, [_vp, _vp, _vp]),
     "hs_vcycle_apply_a_end": (C.c_int, [_vp, _vp, _vp, _vp]),
     "hs_vcycle_apply_a_part": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int]),
+    "hs_vcycle_apply_az_part": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int]),
     "hs_block_dot": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, _vp, C.c_int64, _vp]),
     "hs_block_dot_gated": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, _vp, C.c_int64, _vp, _vp,
                                      _vp, C.c_double]),

@@ -605,6 +605,29 @@ int hs_vcycle_apply_a_part(hs_ctx* c, hs_cycle* cy, const void* f, void* w, int 
   }
 }
 
+int hs_vcycle_apply_az_part(hs_ctx* c, hs_cycle* cy, const void* f, void* z, void* w, int part) {
+  if (!c || !cy || !f || !z || (part != 1 && part != 0 && !w)) return HS_E_ARG;
+  switch (part) {
+    case 0:
+      return vcycle_begin(c, cy, (const double2*)f, (double2*)z);
+    case 1:
+      return sweep_apply(c, cy->sweep, cy->variant, cy->rc, cy->uc,
+                         cy->lane ? &cy->work : nullptr, 0, 1);
+    case 2: {
+      int r = vcycle_end(c, cy, (const double2*)f, (double2*)z, 1);
+      if (r) return r;
+      return stencil_apply(c, cy->fine, (const double2*)z, (double2*)w, 1, nullptr);
+    }
+    case 3: {   // the whole application: z = M f, w = A z
+      int r = vcycle(c, cy, (const double2*)f, (double2*)z);
+      if (r) return r;
+      return stencil_apply(c, cy->fine, (const double2*)z, (double2*)w, 1, nullptr);
+    }
+    default:
+      return set_error(c, HS_E_ARG, "apply_az part must be 0, 1, 2 or 3");
+  }
+}
+
 int hs_vcycle_apply_a_end(hs_ctx* c, hs_cycle* cy, const void* f, void* w) {
   if (!c || !cy || !f || !w) return HS_E_ARG;
   int r = vcycle_end(c, cy, (const double2*)f, cy->tmp);

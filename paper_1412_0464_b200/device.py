@@ -419,6 +419,12 @@ class DeviceCycle(_Handle):
                       else None, int(part))
         return w
 
+    def apply_az_part(self, f_dev, z, w, part):
+        """hs_vcycle_apply_az_part: z = M f kept, w = A z (parts 0/1/2, 3 = whole)."""
+        self.ctx.call("hs_vcycle_apply_az_part", self.h, ptr(f_dev), ptr(z),
+                      ptr(w) if w is not None else None, int(part))
+        return w
+
     def apply_a_end(self, f_dev, w):
         """Second half (sweep, prolongation, post-smoothing, fine matvec) into w."""
         self.ctx.call("hs_vcycle_apply_a_end", self.h, ptr(f_dev), ptr(w))

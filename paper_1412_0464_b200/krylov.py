@@ -255,7 +255,7 @@ def _basis_update(ctx, basis, hess, g, k, n, dev):
 
 
 def _gmres_cycle_pipelined(ops: _Ops, basis: _Basis, r0, r0_norm, bnorm, tol, max_steps,
-                           history):
+                           history, zb=None):
     """CGS2 Arnoldi cycle for this package's TGSP operator with the host one
     step behind the device.  Everything the next step needs is decided on the
     device (the DGKS second pass is gated there, v_{k+1} = w / ||w|| is scaled
@@ -297,16 +297,17 @@ def _gmres_cycle_pipelined(ops: _Ops, basis: _Basis, r0, r0_norm, bnorm, tol, ma
         pin[k].copy_(col, non_blocking=True)
         events[k].record(stream)
 
-    cyc.apply_a_begin(basis.row(0))
-    cyc.apply_a_end(basis.row(0), basis.row(1))
+    # z_k = M v_k is kept (zb): the cycle ends with u += Z y, no extra V-cycle
+    zb.ensure(max_steps)
+    cyc.apply_az_part(basis.row(0), zb.row(0), basis.row(1), 3)
     orthonormalise(0)
     k = 0
     converged = False
     for k in range(max_steps):
         ahead = k + 1 < max_steps
         if ahead:   # ~1 ms of the next step queued while the host trails
-            cyc.apply_a_part(basis.row(k + 1), None, 0)
-            cyc.apply_a_part(basis.row(k + 1), None, 1)
+            cyc.apply_az_part(basis.row(k + 1), zb.row(k + 1), None, 0)
+            cyc.apply_az_part(basis.row(k + 1), zb.row(k + 1), None, 1)
         events[k].synchronize()
         host = pin[k].numpy()
         hcol, w_norm0, nrm1 = host[:k + 1].copy(), host[k + 1].real, host[2 * W].real
@@ -329,16 +330,20 @@ def _gmres_cycle_pipelined(ops: _Ops, basis: _Basis, r0, r0_norm, bnorm, tol, ma
             k += 1
             break
         if ahead:
-            cyc.apply_a_part(basis.row(k + 1), basis.row(k + 2), 2)
+            cyc.apply_az_part(basis.row(k + 1), zb.row(k + 1), basis.row(k + 2), 2)
             orthonormalise(k + 1)
     else:
         k += 1
     if k == 0:
         return None, converged
-    return _basis_update(ctx, basis, hess, g, k, n, dev), converged
+    return _basis_update(ctx, zb, hess, g, k, n, dev), converged   # M dv = Z y
 
 
-def _gmres_cycle(ops: _Ops, basis: _Basis, r0, r0_norm, bnorm, tol, max_steps, history, orth):
+def _gmres_cycle(ops: _Ops, basis: _Basis, r0, r0_norm, bnorm, tol, max_steps, history, orth,
+                 zb=None):
+    """Synchronous Arnoldi cycle (the reference's _gmres_cycle, krylov.py:46-102).
+    Returns (update, converged): with ``zb`` (this package's TGSP operator)
+    the update is M dv = Z y from the kept z_k = M v_k, else dv = V y."""
     import torch
     ctx, n = ops.ctx, ops.n
     hess = np.zeros((max_steps + 1, max_steps), dtype=complex)
@@ -357,9 +362,14 @@ def _gmres_cycle(ops: _Ops, basis: _Basis, r0, r0_norm, bnorm, tol, max_steps, h
     nbuf = torch.zeros(2, dtype=torch.complex128, device=dev)
     k = 0
     converged = False
+    if zb is not None:
+        zb.ensure(max_steps)
     for k in range(max_steps):
         w = basis.row(k + 1)
-        ops.op(basis.row(k), w)
+        if zb is not None:
+            ops.cycle.apply_az_part(basis.row(k), zb.row(k), w, 3)
+        else:
+            ops.op(basis.row(k), w)
         if orth == "mgs":
             for i in range(k + 1):
                 ctx.call("hs_block_dot", ptr(basis.row(i)), basis.V.stride(0), 1, ptr(w), n,
@@ -405,7 +415,7 @@ def _gmres_cycle(ops: _Ops, basis: _Basis, r0, r0_norm, bnorm, tol, max_steps, h
         k += 1
     if k == 0:
         return None, converged
-    return _basis_update(ctx, basis, hess, g, k, n, dev), converged
+    return _basis_update(ctx, zb if zb is not None else basis, hess, g, k, n, dev), converged
 
 
 def _norm(ctx, x, n):
@@ -459,6 +469,10 @@ def _gmres(apply_a, apply_m, f, config: GmresConfig | None = None, orth: str = "
     ops = _Ops(apply_a, apply_m, n, ctx)
     steps0 = config.max_iter if config.restart is None else min(config.restart, config.max_iter)
     basis = _Basis(n, min(steps0, 64) + 1, ctx)
+    # the TGSP operator keeps z_k = M v_k (FGMRES-style storage of a fixed
+    # preconditioner): each cycle ends with u += Z y instead of one more
+    # V-cycle on V y -- the same update (M linear), one sweep fewer per cycle
+    zb = _Basis(n, min(steps0, 64), ctx) if ops.cycle is not None else None
     history = [1.0]
     u = empty(n, ctx).zero_()
     res = ft
@@ -470,12 +484,12 @@ def _gmres(apply_a, apply_m, f, config: GmresConfig | None = None, orth: str = "
             steps = min(steps, config.restart)
         if pipelined and orth == "cgs2" and ops.cycle is not None:
             dv, converged = _gmres_cycle_pipelined(ops, basis, res, res_norm, bnorm,
-                                                   config.tol, steps, history)
+                                                   config.tol, steps, history, zb)
         else:
             dv, converged = _gmres_cycle(ops, basis, res, res_norm, bnorm, config.tol, steps,
-                                         history, orth)
+                                         history, orth, zb)
         if dv is not None:
-            mdv = ops.apply_m(dv)
+            mdv = dv if zb is not None else ops.apply_m(dv)
             ctx.call("hs_axpby", 1.0, 0.0, ptr(mdv), 1.0, 0.0, ptr(u), n)
         res = ops.residual(ft, u)
         if config.restart is None:
