@@ -1301,8 +1301,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   __shared__ int rr[kNR];   // the current task's restricted-update rows
   // optional instrumentation: task 1 timestamps kept in shared memory, dumped at exit
   __shared__ unsigned long long tsm[128];
-  auto stamp = [&](int ti, int k) {
-    if (a.dbg && threadIdx.x == 0 && ti == 1 && k < 64) {
+  auto stamp = [&](int ti, int k) {   // k >= 40: group B's first thread stamps
+    if (a.dbg && threadIdx.x == (k >= 40 && k < 48 ? kNA * 32 : 0) && ti == 1 && k < 64) {
       unsigned long long tt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
       tsm[k] = tt;
@@ -1628,6 +1628,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
           st_async_c(map_rank(&tau[2 * B * TM + lane], rank), Yv[(m - 1) * TM + lane],
                      map_rank(&xbar[par], rank));
       }
+      stamp(ti, 48);
     } else {
       // ---- group B: tips out (as soon as final), the next task's rhs inputs
       // (F is free from here on), then alpha_{k-1}, beta_k = (rows of R) tau
@@ -1690,6 +1691,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       };
       // alpha_{k-1}, beta_k = (rows of R) tau
       cgemv(P.pfx[NP], 2 * B, tau, ab, false);
+      stamp(ti, 44);
       if (G > 1) {
         // ---- second level (two-level partition, k_level2): post c_s / d_s,
         // the segment's first CTA solves for (P_s, Q_s) once every segment
@@ -1712,6 +1714,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
           __threadfence();
           __syncwarp();
           if (lane == 0) atomicAdd(&fl[(isc ? 0 : 1) * kMaxG + seg], 1u);
+          stamp(ti, 45);
         }
         if (rank == 0) {
           const int nz = 2 * (G - 1);
@@ -1730,6 +1733,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
           }
           asm volatile("bar.sync 3, %0;" ::"r"((kCW - kNA) * 32) : "memory");
           double2* pql = part + kWarps * N2 - N2;   // (the last warp's slot: producer, unused)
+          stamp(ti, 46);
           cgemv(r_l2 + P.ct, nz, t2v, pql, false);
           if (wb == 0) {   // (P_s, Q_s) to every CTA of the cluster
             for (int e = lane; e < N2; e += 32) {
@@ -1740,6 +1744,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
           }
         }
         mbar_wait_cluster(&xbar[4 + par], (uint32_t)(ti >> 1) & 1);
+        stamp(ti, 47);
         const double2* pqs = pqv + par * N2;
         cgemv(r_l2 + P.ct + P.zq, 2, pqs, ab, true);
         if (threadIdx.x - kNA * 32 < (unsigned)TM) {
