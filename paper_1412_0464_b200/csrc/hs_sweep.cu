@@ -748,6 +748,10 @@ struct SolveArgs {
   double2* xbuf;
   unsigned* xflag;
   unsigned xbase[kMaxFront];
+  // several right-hand sides through one chain (k_part_solve<TM, NR>): element
+  // strides from one right-hand side's vectors to the next
+  int64_t vs_src, vs_u[2];   // src, u[0], u[1]
+  int64_t ts, xs;            // trace buffers, level-2 exchange buffers
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -1208,17 +1212,20 @@ struct Ring {
   static constexpr int G = ring_g<TM>();           // blocks per chunk copy (>= 2: whole items)
   static constexpr int CHUNK = G * TM2;            // double2 per chunk
   // F, Yv vectors + tau + halo + R partials + couplings + bookkeeping, then the ring
-  static int fixed(int mmax) {
-    return 2 * (mmax + 1) * TM * 16 + 4 * kMaxC * TM * 16 + 4 * TM * 16 +
-           (kWarps + 1) * 2 * TM * 16 + 12 * mmax * 16 + 64 + (int)sizeof(ItemPlan) +
-           kMaxTasks * 4 + itab_len(mmax) * 12 + 512 +
-           (2 * kMaxG * TM + 4 * TM) * 16 + 16;
+  // (nr right-hand sides: every vector array holds nr copies)
+  static int fixed(int mmax, int nr = 1) {
+    return nr * (2 * (mmax + 1) * TM * 16 + 4 * kMaxC * TM * 16 + 4 * TM * 16 +
+                 (kWarps + 1) * 2 * TM * 16 + (2 * kMaxG * TM + 4 * TM) * 16) +
+           12 * mmax * 16 + 64 + (int)sizeof(ItemPlan) +
+           kMaxTasks * 4 + itab_len(mmax) * 12 + 512 + 16;
   }
-  static int nchunk(int mmax) {
-    const int avail = 225 * 1024 - fixed(mmax);
+  static int nchunk(int mmax, int nr = 1) {
+    const int avail = 225 * 1024 - fixed(mmax, nr);
     return std::max(2, std::min(32, avail / (CHUNK * 16 + 16)));   // one producer lane per slot
   }
-  static int smem(int mmax) { return fixed(mmax) + nchunk(mmax) * (CHUNK * 16 + 16); }
+  static int smem(int mmax, int nr = 1) {
+    return fixed(mmax, nr) + nchunk(mmax, nr) * (CHUNK * 16 + 16);
+  }
 };
 
 template <int TM>
