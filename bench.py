@@ -64,6 +64,10 @@ def parse():
                    help="with --shard on one process: G logical shards on one GPU")
     p.add_argument("--lanes", type=int, default=4,
                    help="multi-RHS configs (C4): right-hand sides in flight at once per GPU")
+    p.add_argument("--batch", action="store_true",
+                   help="multi-RHS configs: the solves advance in lockstep and their coarse "
+                        "sweeps share one chain of slab solves per group (gmres_many) "
+                        "instead of running as concurrent lanes")
     p.add_argument("--segments", type=int, default=-1,
                    help="face segments per sweep front (-1: 1 when several right-hand sides "
                         "run as lanes, else automatic)")
@@ -366,7 +370,7 @@ def run_ours(args):
     # several right-hand sides in flight as lanes: one cluster per sweep front
     # (the lanes' sweeps run side by side); one at a time: the widest layout
     segments = args.segments if args.segments >= 0 else (
-        1 if len(mine) > 1 and args.lanes > 1 else 0)
+        1 if len(mine) > 1 and args.lanes > 1 and not args.batch else 0)
     t0 = time.perf_counter()
     keep = (rank == 0 and world == 1 and not args.no_cpu_baseline)
     cycle, _ = hb.build_two_grid(p.mesh, p.model, fine_op=fine_operator(p),
@@ -403,11 +407,12 @@ def run_ours(args):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     launches0 = ctx.launches
-    multi = len(f_dev) > 1 and args.lanes > 1
+    multi = len(f_dev) > 1 and (args.lanes > 1 or args.batch)
 
     def step(fs):
         if multi:
-            return hb.solve_many(cycle, fs, cfg, lanes=args.lanes, orth=args.orth)
+            return hb.solve_many(cycle, fs, cfg, lanes=args.lanes, orth=args.orth,
+                                 batch=args.batch)
         return [solve(fd) for fd in fs]
 
     if multi:   # (lanes) same holding pattern as the timed loop
@@ -554,7 +559,9 @@ def run_ours(args):
             "slab_factor_bytes": fac,
             "sweep_segments": dev.sweep.segments if p.mesh.dim == 2 else None,
             "rhs_per_rank": len(f_dev),
-            "rhs_in_flight": min(args.lanes, len(f_dev)) if multi else 1,
+            "rhs_in_flight": (len(f_dev) if args.batch else min(args.lanes, len(f_dev))) if multi else 1,
+            "rhs_mode": ("lockstep batch (several right-hand sides per chain of slab solves)"
+                         if args.batch else "lanes") if multi else "single",
             "reference_iterations": reference_iterations(p, args),
             "solve_s": ms / 1e3 / max(1, args.steps * len(f_dev)),
             "setup_s": setup_s,

@@ -174,6 +174,17 @@ int hs_sweep_destroy(hs_ctx* ctx, hs_sweep* s);
 /* u = Sweep(f); variant HS_VARIANT_X (prec_x, sweepdd.py:322-359) or
  * HS_VARIANT_UD (prec_ud, sweepdd.py:312-319).  f and u: device, coarse shape. */
 int hs_sweep_apply(hs_ctx* ctx, hs_sweep* s, int variant, const void* f, void* u);
+/* nrhs right-hand sides at once (the reference's multi-column
+ * Factorization.solve, sparselin.py:58-62; SURVEY 8(b)'s nrhs):
+ * right-hand side r at f + r * stride, its result at u + r * stride (stride
+ * in complex elements, >= the coarse size).  Groups of up to
+ * hs_sweep_rhs_width(s) right-hand sides (4, 2 or 1 by the face length) run
+ * through ONE chain of slab solves, every factor block streamed once per
+ * group; per right-hand side the result is bitwise hs_sweep_apply's.  3-D
+ * levels apply one right-hand side after another. */
+int hs_sweep_apply_many(hs_ctx* ctx, hs_sweep* s, int variant, int nrhs, const void* f, void* u,
+                        long long stride);
+int hs_sweep_rhs_width(hs_sweep* s);
 /* NX sweep (prec_nx, sweepdd.py:403-437; NxCells / make_nx_cells :362-401):
  * registers the launch plan of one cell grouping -- j_cell: ncell + 1 cell
  * boundaries with sentinels -1 and J + 1, j_mid: the slab where each cell's
@@ -243,6 +254,10 @@ int hs_cycle_create_lane(hs_ctx* ctx, const hs_cycle* base, hs_cycle** out);
 int hs_cycle_destroy(hs_ctx* ctx, hs_cycle* c);
 /* u = M f : vcycle / tgsp_apply / as_preconditioner   twogrid.py:150-176 */
 int hs_vcycle(hs_ctx* ctx, hs_cycle* c, const void* f, void* u);
+/* nrhs cycles u_r = M f_r (twogrid.py:150-176 per column): fine-level halves
+ * per right-hand side, the coarse sweeps through hs_sweep_apply_many.  Not
+ * for lanes (hs_cycle_create_lane). */
+int hs_vcycle_many(hs_ctx* ctx, hs_cycle* c, int nrhs, const void* f, void* u, long long stride);
 /* GMRES operator application keeping the preconditioned vector: z = M f,
  * w = A z, in parts like hs_vcycle_apply_a_part (0 pre-coarse into z, 1 the
  * sweep's first launch, 2 the rest and w = A z) or whole (part 3).  With the

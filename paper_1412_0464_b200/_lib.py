@@ -65,6 +65,8 @@ SIGNATURES = {
                                   C.POINTER(_vp), C.POINTER(_vp)]),
     "hs_sweep_destroy": (C.c_int, [_vp, _vp]),
     "hs_sweep_apply": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp]),
+    "hs_sweep_apply_many": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _vp, C.c_longlong]),
+    "hs_sweep_rhs_width": (C.c_int, [_vp]),
     "hs_sweep_factor_bytes": (C.c_longlong, [_vp]),
     "hs_sweep_plan_launches": (C.c_int, [_vp, C.c_int]),
     "hs_sweep_segments": (C.c_int, [_vp]),
@@ -85,6 +87,7 @@ SIGNATURES = {
     "hs_cycle_create_lane": (C.c_int, [_vp, _vp, C.POINTER(_vp)]),
     "hs_cycle_destroy": (C.c_int, [_vp, _vp]),
     "hs_vcycle": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "hs_vcycle_many": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp, C.c_longlong]),
     "hs_vcycle_apply_a": (C.c_int, [_vp, _vp, _vp, _vp]),
     "hs_vcycle_apply_a_begin": (C.c_int, [_vp, _vp, _vp]),
     "hs_vcycle_apply_a_end": (C.c_int, [_vp, _vp, _vp, _vp]),

@@ -99,6 +99,9 @@ struct Cycle {
   bool lane = false;
   bool fused = false;      // 2-D, nu = 2: fused pre / post kernels (u2 holds the pre-smoothed u)
   double2* u2 = nullptr;
+  // scratch of vcycle_many (lazy): nb right-hand sides' rc, uc and (fused) u2
+  int nb = 0;
+  double2 *brc = nullptr, *buc = nullptr, *bu2 = nullptr;
 };
 
 static bool want_fused(const Stencil* fine, const Transfer* t, int nu) {
@@ -143,6 +146,59 @@ static int vcycle_end(Ctx* c, Cycle* cy, const double2* f, double2* u, int sweep
 static int vcycle(Ctx* c, Cycle* cy, const double2* f, double2* u) {
   int r = vcycle_begin(c, cy, f, u);
   return r ? r : vcycle_end(c, cy, f, u);
+}
+
+// nrhs cycles u_r = M f_r (vectors at f + r * stride, u + r * stride): the
+// fine-level halves per right-hand side, the coarse sweeps of all of them
+// through one chain of slab solves (sweep_apply_many).  Per right-hand side
+// the kernels and their arithmetic are those of vcycle().
+static int vcycle_many(Ctx* c, Cycle* cy, int nrhs, const double2* f, double2* u, int64_t stride) {
+  if (nrhs == 1) return vcycle(c, cy, f, u);
+  if (cy->lane) return set_error(c, HS_E_ARG, "multi-right-hand-side cycles run on the base cycle");
+  const int64_t nf = cy->fine->d.n, nc = cy->coarse->d.n;
+  if (stride < nf) return set_error(c, HS_E_ARG, "right-hand-side stride shorter than a vector");
+  if (cy->nb < nrhs) {
+    cudaStreamSynchronize(c->stream);
+    cudaFree(cy->brc); cudaFree(cy->buc); cudaFree(cy->bu2);
+    cy->brc = cy->buc = cy->bu2 = nullptr;
+    cy->nb = 0;
+    cudaError_t e = cudaMalloc((void**)&cy->brc, (size_t)nrhs * nc * sizeof(double2));
+    if (e == cudaSuccess) e = cudaMalloc((void**)&cy->buc, (size_t)nrhs * nc * sizeof(double2));
+    if (e == cudaSuccess && cy->fused) e = cudaMalloc((void**)&cy->bu2, (size_t)nrhs * nf * sizeof(double2));
+    if (e != cudaSuccess) return check_cuda(c, e, "multi-right-hand-side cycle buffers");
+    cy->nb = nrhs;
+  }
+  int r;
+  for (int k = 0; k < nrhs; ++k) {   // pre-smoothing from zero, residual, restriction
+    const double2* fk = f + k * stride;
+    double2* uk = u + k * stride;
+    if (cy->fused) {
+      if ((r = stencil_pre2d(c, cy->fine, fk, cy->bu2 + k * nf, cy->r, cy->omega))) return r;
+    } else {
+      if (cy->nu > 0) {
+        r = stencil_jacobi(c, cy->fine, uk, fk, cy->omega, cy->nu, 1, 1);
+      } else {
+        cudaError_t e = cudaMemsetAsync(uk, 0, nf * sizeof(double2), c->stream);
+        r = e == cudaSuccess ? HS_OK : check_cuda(c, e, "memset");
+      }
+      if (r) return r;
+      if ((r = stencil_apply(c, cy->fine, uk, cy->r, 1, fk))) return r;
+    }
+    if ((r = transfer_restrict(c, cy->t, cy->r, cy->brc + k * nc, cy->scale, 1))) return r;
+  }
+  if ((r = sweep_apply_many(c, cy->sweep, cy->variant, nrhs, cy->brc, cy->buc, nc))) return r;
+  for (int k = 0; k < nrhs; ++k) {   // prolongation + correction, post-smoothing
+    const double2* fk = f + k * stride;
+    double2* uk = u + k * stride;
+    if (cy->fused) {
+      if ((r = stencil_post2d(c, cy->fine, cy->t, cy->buc + k * nc, fk, cy->bu2 + k * nf, uk, cy->omega)))
+        return r;
+    } else {
+      if ((r = transfer_prolong(c, cy->t, cy->buc + k * nc, uk, 1, 1))) return r;
+      if (cy->nu > 0 && (r = stencil_jacobi(c, cy->fine, uk, fk, cy->omega, cy->nu, 0, 1))) return r;
+    }
+  }
+  return HS_OK;
 }
 
 // Stencil descriptor from (dim, shape, offsets); coefficients not touched.
@@ -466,6 +522,14 @@ int hs_sweep_apply(hs_ctx* c, hs_sweep* s, int variant, const void* f, void* u) 
   return sweep_apply(c, s, variant, (const double2*)f, (double2*)u);
 }
 
+int hs_sweep_apply_many(hs_ctx* c, hs_sweep* s, int variant, int nrhs, const void* f, void* u,
+                        long long stride) {
+  if (!c || !s || !f || !u) return HS_E_ARG;
+  return sweep_apply_many(c, s, variant, nrhs, (const double2*)f, (double2*)u, stride);
+}
+
+int hs_sweep_rhs_width(hs_sweep* s) { return s && !s->s3 && !s->cpl0 ? s->max_nr : 1; }
+
 int hs_sweep_plan_nx(hs_ctx* c, hs_sweep* s, int ncell, const int64_t* j_cell,
                      const int64_t* j_mid, int* variant) {
   if (!c || !s || !j_cell || !j_mid || !variant) return HS_E_ARG;
@@ -565,6 +629,7 @@ int hs_cycle_destroy(hs_ctx* c, hs_cycle* cy) {
   (void)c;
   if (!cy) return HS_OK;
   cudaFree(cy->rc); cudaFree(cy->uc); cudaFree(cy->r); cudaFree(cy->tmp); cudaFree(cy->u2);
+  cudaFree(cy->brc); cudaFree(cy->buc); cudaFree(cy->bu2);
   if (cy->lane) sweep_work_destroy(&cy->work);
   delete cy;
   return HS_OK;
@@ -573,6 +638,11 @@ int hs_cycle_destroy(hs_ctx* c, hs_cycle* cy) {
 int hs_vcycle(hs_ctx* c, hs_cycle* cy, const void* f, void* u) {
   if (!c || !cy || !f || !u) return HS_E_ARG;
   return vcycle(c, cy, (const double2*)f, (double2*)u);
+}
+
+int hs_vcycle_many(hs_ctx* c, hs_cycle* cy, int nrhs, const void* f, void* u, long long stride) {
+  if (!c || !cy || !f || !u || nrhs < 1) return HS_E_ARG;
+  return vcycle_many(c, cy, nrhs, (const double2*)f, (double2*)u, stride);
 }
 
 int hs_vcycle_apply_a(hs_ctx* c, hs_cycle* cy, const void* f, void* w) {

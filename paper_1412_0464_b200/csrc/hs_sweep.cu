@@ -60,6 +60,8 @@ constexpr int kCW = kWarps - 1;
 #endif
 constexpr int kNA = HS_SWEEP_NA;   // consumer warps of the back substitution while the rest
                                    // run the interface GEMV (group B = kCW - kNA warps)
+static_assert(HS_SWEEP_NA >= 1 && HS_SWEEP_NA <= 8,
+              "group B's partial-sum slots also hold the dense top's 15 partials");
 #ifndef HS_SWEEP_PREFETCH
 #define HS_SWEEP_PREFETCH 0
 #endif
@@ -1206,6 +1208,103 @@ __device__ __forceinline__ double2 mvr(const double2* blk, const double2* v0, co
   return cadd(acc, shfl_xor_c(acc, 16));
 }
 
+// The same mat-vecs for NR right-hand sides at once: vectors of right-hand
+// side r at v + r * vs; each matrix element is read from shared memory once
+// per group of <= 4 right-hand sides (register budget) and every right-hand
+// side's sums are accumulated in mvs2 / mvr's order, so a batched solve is
+// bitwise the single one.
+template <int TM, int NR>
+__device__ __forceinline__ void mvs2n(const double2* m0, const double2* v0, const double2* m1,
+                                      const double2* v1, int vs, int lane, double2 (&out)[NR]) {
+  if constexpr (NR == 1) {
+    out[0] = mvs2<TM>(m0, v0, m1, v1, lane);
+  } else {
+    constexpr int CPL = Geo<TM>::CPL;
+    constexpr int GR = NR < 4 ? NR : 4;
+    const int hh = lane / TM;
+#pragma unroll
+    for (int r0 = 0; r0 < NR; r0 += GR) {
+      double2 a0[GR], a1[GR], a2[GR], a3[GR];
+#pragma unroll
+      for (int r = 0; r < GR; ++r) a0[r] = a1[r] = a2[r] = a3[r] = czero();
+      if (v0) {
+#pragma unroll
+        for (int k = 0; k < CPL; k += 2) {
+          const double2 ma = m0[k * 32 + lane], mb = m0[(k + 1) * 32 + lane];
+#pragma unroll
+          for (int r = 0; r < GR; ++r) {
+            a0[r] = cfma(ma, v0[(r0 + r) * vs + CPL * hh + k], a0[r]);
+            a1[r] = cfma(mb, v0[(r0 + r) * vs + CPL * hh + k + 1], a1[r]);
+          }
+        }
+      }
+      if (v1) {
+#pragma unroll
+        for (int k = 0; k < CPL; k += 2) {
+          const double2 ma = m1[k * 32 + lane], mb = m1[(k + 1) * 32 + lane];
+#pragma unroll
+          for (int r = 0; r < GR; ++r) {
+            a2[r] = cfma(ma, v1[(r0 + r) * vs + CPL * hh + k], a2[r]);
+            a3[r] = cfma(mb, v1[(r0 + r) * vs + CPL * hh + k + 1], a3[r]);
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < GR; ++r) {
+        double2 acc = cadd(cadd(a0[r], a1[r]), cadd(a2[r], a3[r]));
+        if (TM == 16) acc = cadd(acc, shfl_xor_c(acc, 16));
+        out[r0 + r] = (HS_SWEEP_EXP & 1) ? czero() : acc;
+      }
+    }
+  }
+}
+
+template <int TM, int NR>
+__device__ __forceinline__ void mvrn(const double2* blk, const double2* v0, const double2* v1,
+                                     int vs, int lane, double2 (&out)[NR]) {
+  if constexpr (NR == 1) {
+    out[0] = mvr<TM>(blk, v0, v1, lane);
+  } else {
+    constexpr int H = TM / 2;
+    constexpr int GR = NR < 4 ? NR : 4;
+    const int q = lane / 8;
+    const double2* v = q < 2 ? v0 : v1;
+#pragma unroll
+    for (int r0 = 0; r0 < NR; r0 += GR) {
+      double2 a0[GR], a1[GR];
+#pragma unroll
+      for (int r = 0; r < GR; ++r) a0[r] = a1[r] = czero();
+      if (v) {
+        const double2* vv = v + (q & 1) * H;
+#pragma unroll
+        for (int k = 0; k < H; k += 2) {
+          const double2 ma = blk[k * 32 + lane], mb = blk[(k + 1) * 32 + lane];
+#pragma unroll
+          for (int r = 0; r < GR; ++r) {
+            a0[r] = cfma(ma, vv[(r0 + r) * vs + k], a0[r]);
+            a1[r] = cfma(mb, vv[(r0 + r) * vs + k + 1], a1[r]);
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < GR; ++r) {
+        double2 acc = cadd(a0[r], a1[r]);
+        acc = cadd(acc, shfl_xor_c(acc, 8));
+        acc = cadd(acc, shfl_xor_c(acc, 16));
+        out[r0 + r] = (HS_SWEEP_EXP & 1) ? czero() : acc;
+      }
+    }
+  }
+}
+
+
+template <int TM, int HW, int NR>
+__device__ __forceinline__ void mvxn(const double2* m0, const double2* v0, const double2* m1,
+                                     const double2* v1, int vs, int lane, double2 (&out)[NR]) {
+  if constexpr (NR == 1) out[0] = mvx<TM, HW>(m0, v0, m1, v1, lane);
+  else mvs2n<TM, NR>(m0, v0, m1, v1, vs, lane, out);
+}
+
 template <int TM>
 struct Ring {
   static constexpr int TM2 = TM * TM;
@@ -1213,22 +1312,23 @@ struct Ring {
   static constexpr int CHUNK = G * TM2;            // double2 per chunk
   // F, Yv vectors + tau + halo + R partials + couplings + bookkeeping, then the ring
   // (nr right-hand sides: every vector array holds nr copies)
-  static int fixed(int mmax, int nr = 1) {
-    return nr * (2 * (mmax + 1) * TM * 16 + 4 * kMaxC * TM * 16 + 4 * TM * 16 +
-                 (kWarps + 1) * 2 * TM * 16 + (2 * kMaxG * TM + 4 * TM) * 16) +
+  // (C chunks per cluster; F, Yv; tau2; halo2; part + ab; t2v + pqv)
+  static int fixed(int mmax, int C, int nr) {
+    return nr * (2 * (mmax + 1) * TM * 16 + 4 * C * TM * 16 + 4 * TM * 16 +
+                 (kCW - kNA + 2) * 2 * TM * 16 + (2 * kMaxG * TM + 4 * TM) * 16) +
            12 * mmax * 16 + 64 + (int)sizeof(ItemPlan) +
            kMaxTasks * 4 + itab_len(mmax) * 12 + 512 + 16;
   }
-  static int nchunk(int mmax, int nr = 1) {
-    const int avail = 225 * 1024 - fixed(mmax, nr);
+  static int nchunk(int mmax, int C, int nr) {
+    const int avail = 225 * 1024 - fixed(mmax, C, nr);
     return std::max(2, std::min(32, avail / (CHUNK * 16 + 16)));   // one producer lane per slot
   }
-  static int smem(int mmax, int nr = 1) {
-    return fixed(mmax, nr) + nchunk(mmax, nr) * (CHUNK * 16 + 16);
+  static int smem(int mmax, int C, int nr) {
+    return fixed(mmax, C, nr) + nchunk(mmax, C, nr) * (CHUNK * 16 + 16);
   }
 };
 
-template <int TM>
+template <int TM, int NR>
 __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   constexpr int TM2 = Geo<TM>::TM2;
   constexpr int CHUNK = Ring<TM>::CHUNK;
@@ -1249,21 +1349,25 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   const int mmax = g.mmax;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int x = lane % TM, hh = lane / TM;
-  constexpr int HW = (TM == 16 && HS_SWEEP_HALF) ? 2 : 1;   // items per warp pass
+  constexpr int HW = (TM == 16 && HS_SWEEP_HALF && NR == 1) ? 2 : 1;   // items per warp pass
   const int sub = HW == 2 ? hh : 0;      // this lane's item within the pass
   const bool wr = HW == 2 || hh == 0;    // lane owns the result row it computed
   const int NC = a.nchunk;
   extern __shared__ __align__(128) double2 sm[];
-  double2* F = sm;                                  // [mmax+1][TM] rhs / reduced rhs
-  double2* Yv = F + (mmax + 1) * TM;                // [mmax+1][TM] Dinv f, then x
-  double2* tau2 = Yv + (mmax + 1) * TM;             // [2][2 kMaxC][TM] interface rhs (by task parity)
-  double2* halo2 = tau2 + 4 * kMaxC * TM;           // [2][2][TM] neighbours' edge blocks of x
-  double2* part = halo2 + 4 * TM;                   // [kWarps][2TM] R / dense-top partial sums
-  double2* ab = part + kWarps * N2;                 // [2TM] alpha_{k-1}, beta_k
-  double2* stc = ab + N2;                           // [2 tin][2 rows][3 offsets][mmax] couplings
-  double2* t2v = stc + 12 * mmax;                   // [2(G-1)][TM] level-2 right-hand side
-  double2* pqv = t2v + 2 * kMaxG * TM;              // [2][2TM] (P_s, Q_s) by task parity
-  uint64_t* xbar = (uint64_t*)(pqv + 4 * TM);       // [6] tips (2), halo (2), (P_s, Q_s) (2)
+  // vector arrays hold NR right-hand sides (strides FS, TS, HS, PS, N2, T2S)
+  const int FS = (mmax + 1) * TM;
+  const int TS = 2 * C * TM;
+  constexpr int HS = 2 * TM, PS = (kCW - kNA + 1) * N2, T2S = 2 * kMaxG * TM;
+  double2* F = sm;                                  // [NR][mmax+1][TM] rhs / reduced rhs
+  double2* Yv = F + NR * FS;                        // [NR][mmax+1][TM] Dinv f, then x
+  double2* tau2 = Yv + NR * FS;                     // [2][NR][2 C][TM] interface rhs (by task parity)
+  double2* halo2 = tau2 + 2 * NR * TS;              // [2][NR][2][TM] neighbours' edge blocks of x
+  double2* part = halo2 + 2 * NR * HS;              // [NR][group-B warps + 1][2TM] R / dense-top partial sums
+  double2* ab = part + NR * PS;                     // [NR][2TM] alpha_{k-1}, beta_k
+  double2* stc = ab + NR * N2;                      // [2 tin][2 rows][3 offsets][mmax] couplings
+  double2* t2v = stc + 12 * mmax;                   // [NR][2(G-1)][TM] level-2 right-hand side
+  double2* pqv = t2v + NR * T2S;                    // [2][NR][2TM] (P_s, Q_s) by task parity
+  uint64_t* xbar = (uint64_t*)(pqv + 2 * NR * N2);  // [6] tips (2), halo (2), (P_s, Q_s) (2)
   uint64_t* cbar = xbar + 6;                        // [NC] chunk arrival
   volatile int* cseq = (volatile int*)(cbar + NC);  // [NC] chunk issued into a slot
   int* ccnt = (int*)(cseq + NC);                    // [NC] blocks of the slot's chunk consumed
@@ -1422,7 +1526,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       const int y = Y0 + yl;
       const int gr = x + t.lo - 1;
       const bool ok = x < t.T && gr >= t.a && gr < t.b;
-      cp_async16(&F[yl * TM + x], a.src + (ok ? (int64_t)gr * M + y : 0), ok);
+#pragma unroll
+      for (int rh = 0; rh < NR; ++rh)
+        cp_async16(&F[rh * FS + yl * TM + x],
+                   a.src + (ok ? rh * a.vs_src + (int64_t)gr * M + y : 0), ok);
 #pragma unroll
       for (int tn_i = 0; tn_i < 2; ++tn_i) {
         const int tin = tn_i ? t.tin3 : t.tin1, row = tn_i ? t.row3 : t.row1;
@@ -1444,18 +1551,19 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   // task of this front without a trip through global memory (its x is still in
   // Yv, the neighbours' edge blocks arrive in halo by st.async), else from the
   // trace buffer written by an earlier launch.
-  auto transx = [&](int tn_i, bool local, const double2* halo, int buf, int prow, int sign,
+  auto transx = [&](int rh, int tn_i, bool local, const double2* halo, int buf, int prow, int sign,
                     int which, int yl) -> double2 {
     const int y = Y0 + yl;
     const int xr = prow + (which == 0 ? 1 : 0);   // trace row 1 feeds which 0, row 0 which 1
-    const double2* Bt = a.trace + (int64_t)buf * 2 * M + (which == 0 ? M : 0);   // L2 reads (__ldcg)
+    const double2* Bt = a.trace + rh * a.ts + (int64_t)buf * 2 * M + (which == 0 ? M : 0);   // L2 reads (__ldcg)
     double2 acc = czero();
 #pragma unroll
     for (int o = -1; o <= 1; ++o) {
       if (y + o < 0 || y + o >= M) continue;
       const int q = yl + o;
       const double2 bv = !local ? __ldcg(Bt + y + o)
-                         : q < 0 ? halo[xr] : q >= m ? halo[TM + xr] : Yv[q * TM + xr];
+                         : q < 0 ? halo[rh * HS + xr] : q >= m ? halo[rh * HS + TM + xr]
+                                                               : Yv[rh * FS + q * TM + xr];
       acc = cfma(stc[((tn_i * 2 + which) * 3 + o + 1) * mmax + yl], bv, acc);
     }
     return cscale(which == 0 ? (double)sign : (double)-sign, acc);
@@ -1464,9 +1572,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
   // tips g[first], g[last] of this chunk go to every CTA's tau:
   // tau block b = (g_b[last], g_{b+1}[first]) -> tm-slots 2b, 2b+1
   auto push_tip = [&](double2* tau, int par, int slot, const double2* v, int w, int nw) {
-    const double2 val = v[lane];   // lanes < TM; warp w of nw pushing warps
-    for (int d = w; d < C; d += nw)
-      st_async_c(map_rank(&tau[slot + lane], d), val, map_rank(&xbar[par], d));
+#pragma unroll
+    for (int rh = 0; rh < NR; ++rh) {
+      const double2 val = v[rh * FS + lane];   // lanes < TM; warp w of nw pushing warps
+      for (int d = w; d < C; d += nw)
+        st_async_c(map_rank(&tau[rh * TS + slot + lane], d), val, map_rank(&xbar[par], d));
+    }
   };
 
   SweepTask prev{}, t = fcount > 0 ? a.tasks[ffirst] : SweepTask{};
@@ -1479,15 +1590,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     task_r = ti * CPT - task_q * NC;
     if (ti + 1 < fcount) tn = a.tasks[ffirst + ti + 1];   // in flight early
     const int par = ti & 1;
-    double2* tau = tau2 + par * 2 * kMaxC * TM;
-    const double2* halo = halo2 + par * 2 * TM;
+    double2* tau = tau2 + par * NR * TS;
+    const double2* halo = halo2 + par * NR * HS;
     // previous task's traces consumed here straight from shared memory
     const bool loc1 = ti > 0 && t.tin1 >= 0 && prev.out2 == t.tin1;
     const bool loc3 = ti > 0 && t.tin3 >= 0 && prev.out4 == t.tin3;
     if (threadIdx.x == 0) {
-      if (ti > 0) mbar_expect_tx(&xbar[2 + par], halo_bytes);
-      if (B > 0) mbar_expect_tx(&xbar[par], 2 * B * TM * 16 + (lastpush ? TM * 16 : 0));
-      if (G > 1) mbar_expect_tx(&xbar[4 + par], N2 * 16);
+      if (ti > 0) mbar_expect_tx(&xbar[2 + par], NR * halo_bytes);
+      if (B > 0) mbar_expect_tx(&xbar[par], NR * (2 * B * TM * 16 + (lastpush ? TM * 16 : 0)));
+      if (G > 1) mbar_expect_tx(&xbar[4 + par], NR * N2 * 16);
     }
     stamp(ti, 0);
     if (HS_SWEEP_L2NEXT && ti + 1 < fcount) {   // next slab's stream into L2 (LSU path, not TMA)
@@ -1508,10 +1619,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       const bool r1 = t.tin1 >= 0 && (x == t.row1 || x == t.row1 + 1);
       const bool r3 = t.tin3 >= 0 && (x == t.row3 || x == t.row3 + 1);
       if (!r1 && !r3) continue;
-      double2 v = F[yl * TM + x];
-      if (r1) v = cadd(v, transx(0, loc1, halo, t.tin1, prev.orow2, 1, x - t.row1, yl));
-      if (r3) v = cadd(v, transx(1, loc3, halo, t.tin3, prev.orow4, -1, x - t.row3, yl));
-      F[yl * TM + x] = v;
+#pragma unroll
+      for (int rh = 0; rh < NR; ++rh) {
+        double2 v = F[rh * FS + yl * TM + x];
+        if (r1) v = cadd(v, transx(rh, 0, loc1, halo, t.tin1, prev.orow2, 1, x - t.row1, yl));
+        if (r3) v = cadd(v, transx(rh, 1, loc3, halo, t.tin3, prev.orow4, -1, x - t.row3, yl));
+        F[rh * FS + yl * TM + x] = v;
+      }
     }
     csync();
     stamp(ti, 1);
@@ -1544,21 +1658,28 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       const double2* m0 = it.m0;
       const double2* m1 = it.m1;
       if (has) {
+        double2 acc[NR];
         if (p == L) {            // partial x_r += Q[r][c0] f_c0 + Q[r][c0+1] f_c0+1
           const int c0 = 2 * (j % QP);
           const bool two = c0 + 1 < qk;
-          const double2 acc = mvx<TM, HW>(m0, F + c0 * S * TM, two ? m1 : nullptr,
-                                          two ? F + (c0 + 1) * S * TM : nullptr, lane);
-          if (wr) part[j * TM + x] = acc;
+          mvxn<TM, HW, NR>(m0, F + c0 * S * TM, two ? m1 : nullptr,
+                           two ? F + (c0 + 1) * S * TM : nullptr, FS, lane, acc);
+          if (wr) {
+#pragma unroll
+            for (int rh = 0; rh < NR; ++rh) part[rh * PS + j * TM + x] = acc[rh];
+          }
         } else if (p < L) {
           if ((yl >> l) & 1) {   // eliminated at this level: y = Dinv f
-            const double2 r = mvx<TM, HW>(m0, F + yl * TM, nullptr, nullptr, lane);
-            if (wr) Yv[yl * TM + x] = r;
-          } else if (sparse0) {  // kept, level 0: f -= L Yv[y-1] + U Yv[y+1]
+            mvxn<TM, HW, NR>(m0, F + yl * TM, nullptr, nullptr, FS, lane, acc);
+            if (wr) {
+#pragma unroll
+              for (int rh = 0; rh < NR; ++rh) Yv[rh * FS + yl * TM + x] = acc[rh];
+            }
+          } else if (NR == 1 && sparse0) {  // kept, level 0: f -= L Yv[y-1] + U Yv[y+1]
             // (alpha f_{y-1} = L Dinv_{y-1} f_{y-1} = L Yv[y-1], Yv from this
             // phase's first half; L, U the slab stencil's thin-axis couplings)
             const double2* cp = a.cpl + ((int64_t)slabs[ti] * M + (Y0 + yl)) * 6 * TM;
-            double2 acc = czero();
+            double2 acc0 = czero();
 #pragma unroll
             for (int sd = 0; sd < 2; ++sd) {
               const int q = yl + (sd ? 1 : -1);
@@ -1567,26 +1688,36 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
               for (int o0 = -1; o0 <= 1; ++o0) {
                 const int xx = x + o0;
                 if (xx < 0 || xx >= TM) continue;
-                acc = cfma(__ldg(cp + (sd * 3 + o0 + 1) * TM + x), Yv[q * TM + xx], acc);
+                acc0 = cfma(__ldg(cp + (sd * 3 + o0 + 1) * TM + x), Yv[q * TM + xx], acc0);
               }
             }
-            if (wr) F[yl * TM + x] = csub(F[yl * TM + x], acc);
+            if (wr) F[yl * TM + x] = csub(F[yl * TM + x], acc0);
           } else {               // kept: f -= alpha f_{y-s} + gamma f_{y+s}
             const bool hl = yl - s >= 0, hr = yl + s < m;
-            const double2 acc = mvx<TM, HW>(hl ? m0 : nullptr, hl ? F + (yl - s) * TM : nullptr,
-                                        hr ? m1 : nullptr, hr ? F + (yl + s) * TM : nullptr,
-                                        lane);
-            if (wr) F[yl * TM + x] = csub(F[yl * TM + x], acc);
+            mvxn<TM, HW, NR>(hl ? m0 : nullptr, hl ? F + (yl - s) * TM : nullptr,
+                             hr ? m1 : nullptr, hr ? F + (yl + s) * TM : nullptr, FS, lane, acc);
+            if (wr) {
+#pragma unroll
+              for (int rh = 0; rh < NR; ++rh)
+                F[rh * FS + yl * TM + x] = csub(F[rh * FS + yl * TM + x], acc[rh]);
+            }
           }
         } else if (g.nr && l == 0 && yl != m - 1) {   // level 0: only the rows read later
-          const double2 acc = mvr<TM>(m0, Yv + (yl - 1) * TM, Yv + (yl + 1) * TM, lane);
-          if (lane < kNR) Yv[yl * TM + rr[lane]] = csub(Yv[yl * TM + rr[lane]], acc);
+          mvrn<TM, NR>(m0, Yv + (yl - 1) * TM, Yv + (yl + 1) * TM, FS, lane, acc);
+          if (lane < kNR) {
+#pragma unroll
+            for (int rh = 0; rh < NR; ++rh)
+              Yv[rh * FS + yl * TM + rr[lane]] = csub(Yv[rh * FS + yl * TM + rr[lane]], acc[rh]);
+          }
         } else {                 // x_y = Dinv f - (Dinv L) x_{y-s} - (Dinv U) x_{y+s}
           const bool hl = yl - s >= 0, hr = yl + s < m;
-          const double2 acc = mvx<TM, HW>(hl ? m0 : nullptr, hl ? Yv + (yl - s) * TM : nullptr,
-                                      hr ? m1 : nullptr, hr ? Yv + (yl + s) * TM : nullptr,
-                                      lane);
-          if (wr) Yv[yl * TM + x] = csub(Yv[yl * TM + x], acc);
+          mvxn<TM, HW, NR>(hl ? m0 : nullptr, hl ? Yv + (yl - s) * TM : nullptr,
+                           hr ? m1 : nullptr, hr ? Yv + (yl + s) * TM : nullptr, FS, lane, acc);
+          if (wr) {
+#pragma unroll
+            for (int rh = 0; rh < NR; ++rh)
+              Yv[rh * FS + yl * TM + x] = csub(Yv[rh * FS + yl * TM + x], acc[rh]);
+          }
         }
       }
       release(it, has && !sparse0);
@@ -1610,11 +1741,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       stamp(ti, 2 + p);
     }
     {   // x at the level-L points = sum of the column-pair partials
-      for (int t = threadIdx.x; t < qk * TM; t += kCW * 32) {
-        const int r = t / TM, xx = t % TM;
+      for (int t = threadIdx.x; t < NR * qk * TM; t += kCW * 32) {
+        const int rh = t / (qk * TM), t1 = t - rh * qk * TM;
+        const int r = t1 / TM, xx = t1 % TM;
         double2 acc = czero();
-        for (int cp = 0; cp < QP; ++cp) acc = cadd(acc, part[(r * QP + cp) * TM + xx]);
-        Yv[r * S * TM + xx] = acc;
+        for (int cp = 0; cp < QP; ++cp) acc = cadd(acc, part[rh * PS + (r * QP + cp) * TM + xx]);
+        Yv[rh * FS + r * S * TM + xx] = acc;
       }
       csync();
     }
@@ -1631,9 +1763,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
         asm volatile("bar.sync 2, %0;" ::"r"(kNA * 32) : "memory");
         if (p == P.plast && rank < B && lane < TM)
           push_tip(tau, par, 2 * rank * TM, Yv + (m - 1) * TM, warp, kNA);
-        if (p == P.plast && lastpush && warp == 0 && lane < TM)   // own g[m-1] for c_s
-          st_async_c(map_rank(&tau[2 * B * TM + lane], rank), Yv[(m - 1) * TM + lane],
-                     map_rank(&xbar[par], rank));
+        if (p == P.plast && lastpush && warp == 0 && lane < TM) {   // own g[m-1] for c_s
+#pragma unroll
+          for (int rh = 0; rh < NR; ++rh)
+            st_async_c(map_rank(&tau[rh * TS + 2 * B * TM + lane], rank),
+                       Yv[rh * FS + (m - 1) * TM + lane], map_rank(&xbar[par], rank));
+        }
       }
       stamp(ti, 48);
     } else {
@@ -1643,9 +1778,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
         if (rank > 0) push_tip(tau, par, (2 * (rank - 1) + 1) * TM, Yv, warp - kNA, kCW - kNA);
         if (P.plast == L && rank < B)
           push_tip(tau, par, 2 * rank * TM, Yv + (m - 1) * TM, warp - kNA, kCW - kNA);
-        if (P.plast == L && lastpush && warp == kNA)
-          st_async_c(map_rank(&tau[2 * B * TM + lane], rank), Yv[(m - 1) * TM + lane],
-                     map_rank(&xbar[par], rank));
+        if (P.plast == L && lastpush && warp == kNA) {
+#pragma unroll
+          for (int rh = 0; rh < NR; ++rh)
+            st_async_c(map_rank(&tau[rh * TS + 2 * B * TM + lane], rank),
+                       Yv[rh * FS + (m - 1) * TM + lane], map_rank(&xbar[par], rank));
+        }
       }
       if (ti + 1 < fcount) prefetch_rhs(tn, kNA, kCW - kNA);
       mbar_wait(&xbar[par], (uint32_t)(ti >> 1) & 1);
@@ -1654,8 +1792,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
       // out -= it (subtract); items rfirst.. of 2tm x tm column blocks (row index
       // fastest over two ring blocks), rows r0 = lane (tm 32) or x (tm 16)
       // and r0 + 32 / r0 + 16
-      auto cgemv = [&](int rfirst, int nq, const double2* vec, double2* out, bool subtract) {
-        double2 acc0 = czero(), acc1 = czero();
+      // (right-hand side rh: vec + rh * vstr, out + rh * ostr)
+      auto cgemv = [&](int rfirst, int nq, const double2* vec, int vstr, double2* out, int ostr,
+                       bool subtract) {
+        double2 acc0[NR], acc1[NR];
+#pragma unroll
+        for (int rh = 0; rh < NR; ++rh) acc0[rh] = acc1[rh] = czero();
         const int r0 = HW == 1 ? lane : x, r1 = r0 + (HW == 1 ? 32 : 16);   // r1 unused: tm 16, HW 1
         for (int jp = (warp - kNA) * HW; jp < nq; jp += (kCW - kNA) * HW) {
           const int j = jp + sub;
@@ -1666,38 +1808,51 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
             const double2* tq = vec + j * TM;
 #pragma unroll 4
             for (int c = 0; c < TM / 2; ++c) {
-              const double2 tv = tq[c];
-              acc0 = cfma(it.m0[c * N2 + r0], tv, acc0);
-              if (HW == 2 || TM == 32) acc1 = cfma(it.m0[c * N2 + r1], tv, acc1);
+              const double2 ma = it.m0[c * N2 + r0];
+              const double2 mb = (HW == 2 || TM == 32) ? it.m0[c * N2 + r1] : czero();
+#pragma unroll
+              for (int rh = 0; rh < NR; ++rh) {
+                const double2 tv = tq[rh * vstr + c];
+                acc0[rh] = cfma(ma, tv, acc0[rh]);
+                if (HW == 2 || TM == 32) acc1[rh] = cfma(mb, tv, acc1[rh]);
+              }
             }
 #pragma unroll 4
             for (int c = 0; c < TM / 2; ++c) {
-              const double2 tv = tq[TM / 2 + c];
-              acc0 = cfma(it.m1[c * N2 + r0], tv, acc0);
-              if (HW == 2 || TM == 32) acc1 = cfma(it.m1[c * N2 + r1], tv, acc1);
+              const double2 ma = it.m1[c * N2 + r0];
+              const double2 mb = (HW == 2 || TM == 32) ? it.m1[c * N2 + r1] : czero();
+#pragma unroll
+              for (int rh = 0; rh < NR; ++rh) {
+                const double2 tv = tq[rh * vstr + TM / 2 + c];
+                acc0[rh] = cfma(ma, tv, acc0[rh]);
+                if (HW == 2 || TM == 32) acc1[rh] = cfma(mb, tv, acc1[rh]);
+              }
             }
           }
           release(it, has);
         }
         if (HW == 2) {   // both halves' items hold rows x and x + 16
-          acc0 = cadd(acc0, shfl_xor_c(acc0, 16));
-          acc1 = cadd(acc1, shfl_xor_c(acc1, 16));
+          acc0[0] = cadd(acc0[0], shfl_xor_c(acc0[0], 16));
+          acc1[0] = cadd(acc1[0], shfl_xor_c(acc1[0], 16));
         }
         if (lane < 32 / HW) {
-          part[warp * N2 + r0] = acc0;
-          if (HW == 2 || TM == 32) part[warp * N2 + r1] = acc1;
+#pragma unroll
+          for (int rh = 0; rh < NR; ++rh) {
+            part[rh * PS + (warp - kNA) * N2 + r0] = acc0[rh];
+            if (HW == 2 || TM == 32) part[rh * PS + (warp - kNA) * N2 + r1] = acc1[rh];
+          }
         }
         asm volatile("bar.sync 3, %0;" ::"r"((kCW - kNA) * 32) : "memory");
-        if (threadIdx.x - kNA * 32 < (unsigned)N2) {
-          const int t = threadIdx.x - kNA * 32;
+        for (int tt = threadIdx.x - kNA * 32; tt < NR * N2; tt += (kCW - kNA) * 32) {
+          const int rh = tt / N2, t = tt % N2;
           double2 sacc = czero();
-          for (int w = kNA; w < kCW; ++w) sacc = cadd(sacc, part[w * N2 + t]);
-          out[t] = subtract ? csub(out[t], sacc) : sacc;
+          for (int w = 0; w < kCW - kNA; ++w) sacc = cadd(sacc, part[rh * PS + w * N2 + t]);
+          out[rh * ostr + t] = subtract ? csub(out[rh * ostr + t], sacc) : sacc;
         }
         asm volatile("bar.sync 3, %0;" ::"r"((kCW - kNA) * 32) : "memory");
       };
       // alpha_{k-1}, beta_k = (rows of R) tau
-      cgemv(P.pfx[NP], 2 * B, tau, ab, false);
+      cgemv(P.pfx[NP], 2 * B, tau, TS, ab, N2, false);
       stamp(ti, 44);
       if (G > 1) {
         // ---- second level (two-level partition, k_level2): post c_s / d_s,
@@ -1706,17 +1861,22 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
         // (alpha, beta) -= Pk P_s + Qk Q_s
         const int r_l2 = P.pfx[NP] + 2 * B;
         unsigned* fl = a.xflag + (size_t)front * 2 * kMaxG;
-        double2* xb = a.xbuf + ((size_t)front * 2 + par) * kMaxG * 2 * TM;
+        double2* xb = a.xbuf + ((size_t)front * 2 + par) * kMaxG * 2 * TM;   // + rh * a.xs
         const unsigned want = a.xbase[front] + (unsigned)ti + 1u;
         const int wb = warp - kNA;
         if (P.ct && wb == 0) {
           const Item it = acquire(ti, r_l2);
           const bool isc = rank == B;   // c_s (last chunk) or d_s (first chunk)
-          const double2 acc = mvx<TM, HW>(it.m0, isc ? ab : ab + TM, nullptr, nullptr, lane);
+          double2 acc[NR];
+          mvxn<TM, HW, NR>(it.m0, isc ? ab : ab + TM, nullptr, nullptr, N2, lane, acc);
           release(it, true);
           if (lane < TM) {
-            const double2 gv = isc ? tau[2 * B * TM + lane] : Yv[lane];   // g[last] / g[first]
-            __stcg(&xb[(seg * 2 + (isc ? 0 : 1)) * TM + lane], csub(gv, acc));
+#pragma unroll
+            for (int rh = 0; rh < NR; ++rh) {
+              const double2 gv = isc ? tau[rh * TS + 2 * B * TM + lane]
+                                     : Yv[rh * FS + lane];   // g[last] / g[first]
+              __stcg(&xb[rh * a.xs + (seg * 2 + (isc ? 0 : 1)) * TM + lane], csub(gv, acc[rh]));
+            }
           }
           __threadfence();
           __syncwarp();
@@ -1733,37 +1893,40 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
           }
           asm volatile("bar.sync 3, %0;" ::"r"((kCW - kNA) * 32) : "memory");
           // level-2 right-hand side in k_reduced order: block 2b = c_b, 2b + 1 = d_{b+1}
-          for (int i = threadIdx.x - kNA * 32; i < nz * TM; i += (kCW - kNA) * 32) {
+          for (int ii = threadIdx.x - kNA * 32; ii < NR * nz * TM; ii += (kCW - kNA) * 32) {
+            const int rh = ii / (nz * TM), i = ii - rh * nz * TM;
             const int blk = i / TM, e = i % TM, b2 = blk / 2;
             const int sg = (blk & 1) ? b2 + 1 : b2;
-            t2v[i] = __ldcg(&xb[(sg * 2 + (blk & 1)) * TM + e]);
+            t2v[rh * T2S + i] = __ldcg(&xb[rh * a.xs + (sg * 2 + (blk & 1)) * TM + e]);
           }
           asm volatile("bar.sync 3, %0;" ::"r"((kCW - kNA) * 32) : "memory");
-          double2* pql = part + kWarps * N2 - N2;   // (the last warp's slot: producer, unused)
+          double2* pql = part + PS - N2;   // (the slot after group B's partials)
           stamp(ti, 46);
-          cgemv(r_l2 + P.ct, nz, t2v, pql, false);
+          cgemv(r_l2 + P.ct, nz, t2v, T2S, pql, PS, false);
           if (wb == 0) {   // (P_s, Q_s) to every CTA of the cluster
-            for (int e = lane; e < N2; e += 32) {
-              const double2 v = pql[e];
+            for (int ee = lane; ee < NR * N2; ee += 32) {
+              const int rh = ee / N2, e = ee % N2;
+              const double2 v = pql[rh * PS + e];
               for (int d = 0; d < C; ++d)
-                st_async_c(map_rank(&pqv[par * N2 + e], d), v, map_rank(&xbar[4 + par], d));
+                st_async_c(map_rank(&pqv[(par * NR + rh) * N2 + e], d), v,
+                           map_rank(&xbar[4 + par], d));
             }
           }
         }
         mbar_wait_cluster(&xbar[4 + par], (uint32_t)(ti >> 1) & 1);
         stamp(ti, 47);
-        const double2* pqs = pqv + par * N2;
-        cgemv(r_l2 + P.ct + P.zq, 2, pqs, ab, true);
-        if (threadIdx.x - kNA * 32 < (unsigned)TM) {
-          const int e = threadIdx.x - kNA * 32;
-          const int nb = ((ti + 1) & 1) * 2 * TM;   // next task's halo: edge values across segments
+        const double2* pqs = pqv + par * NR * N2;
+        cgemv(r_l2 + P.ct + P.zq, 2, pqs, N2, ab, N2, true);
+        for (int ee = threadIdx.x - kNA * 32; ee < NR * TM; ee += (kCW - kNA) * 32) {
+          const int rh = ee / TM, e = ee % TM;
+          const int nb = (((ti + 1) & 1) * NR + rh) * HS;   // next task's halo: edge values across segments
           if (rank == 0 && seg > 0) {
-            ab[e] = pqs[e];
-            halo2[nb + e] = pqs[e];
+            ab[rh * N2 + e] = pqs[rh * N2 + e];
+            halo2[nb + e] = pqs[rh * N2 + e];
           }
           if (rank == B && seg < G - 1) {
-            ab[TM + e] = pqs[TM + e];
-            halo2[nb + TM + e] = pqs[TM + e];
+            ab[rh * N2 + TM + e] = pqs[rh * N2 + TM + e];
+            halo2[nb + TM + e] = pqs[rh * N2 + TM + e];
           }
         }
       }
@@ -1779,15 +1942,24 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
         Item it{};
         if (has) {
           it = acquire(ti, r);   // W_j, V_j
+          double2 acc[NR];
           if (g.nr) {                       // only the rows read later
-            const double2 acc = mvr<TM>(it.m0, rank > 0 || seg > 0 ? ab : nullptr,
-                                        rank < B || seg < G - 1 ? ab + TM : nullptr, lane);
-            if (lane < kNR) Yv[j * TM + rr[lane]] = csub(Yv[j * TM + rr[lane]], acc);
+            mvrn<TM, NR>(it.m0, rank > 0 || seg > 0 ? ab : nullptr,
+                         rank < B || seg < G - 1 ? ab + TM : nullptr, N2, lane, acc);
+            if (lane < kNR) {
+#pragma unroll
+              for (int rh = 0; rh < NR; ++rh)
+                Yv[rh * FS + j * TM + rr[lane]] = csub(Yv[rh * FS + j * TM + rr[lane]], acc[rh]);
+            }
           } else {
             const bool wl = rank > 0 || seg > 0, wr2 = rank < B || seg < G - 1;
-            const double2 acc = mvx<TM, HW>(wl ? it.m0 : nullptr, wl ? ab : nullptr,
-                                        wr2 ? it.m1 : nullptr, wr2 ? ab + TM : nullptr, lane);
-            if (wr) Yv[j * TM + x] = csub(Yv[j * TM + x], acc);
+            mvxn<TM, HW, NR>(wl ? it.m0 : nullptr, wl ? ab : nullptr,
+                             wr2 ? it.m1 : nullptr, wr2 ? ab + TM : nullptr, N2, lane, acc);
+            if (wr) {
+#pragma unroll
+              for (int rh = 0; rh < NR; ++rh)
+                Yv[rh * FS + j * TM + x] = csub(Yv[rh * FS + j * TM + x], acc[rh]);
+            }
           }
         }
         release(it, has);
@@ -1797,24 +1969,31 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     }
     // ---- edge blocks of x to the neighbours (next task's transmission halo)
     if (ti + 1 < fcount && lane < TM) {
-      const int nb = ((ti + 1) & 1) * 2 * TM;
-      if (warp == 0 && rank > 0)
-        st_async_c(map_rank(&halo2[nb + TM + lane], rank - 1), Yv[lane],
-                   map_rank(&xbar[2 + ((ti + 1) & 1)], rank - 1));
-      if (warp == 1 && rank < B)
-        st_async_c(map_rank(&halo2[nb + lane], rank + 1), Yv[(m - 1) * TM + lane],
-                   map_rank(&xbar[2 + ((ti + 1) & 1)], rank + 1));
+#pragma unroll
+      for (int rh = 0; rh < NR; ++rh) {
+        const int nb = (((ti + 1) & 1) * NR + rh) * HS;
+        if (warp == 0 && rank > 0)
+          st_async_c(map_rank(&halo2[nb + TM + lane], rank - 1), Yv[rh * FS + lane],
+                     map_rank(&xbar[2 + ((ti + 1) & 1)], rank - 1));
+        if (warp == 1 && rank < B)
+          st_async_c(map_rank(&halo2[nb + lane], rank + 1), Yv[rh * FS + (m - 1) * TM + lane],
+                     map_rank(&xbar[2 + ((ti + 1) & 1)], rank + 1));
+      }
     }
     // ---- outputs: solution rows into u (one producer per row and pass), traces
     const int ur0 = t.ta + 1 - t.lo, ur1 = t.tb + 1 - t.lo;
     for (int yl = warp * YPW + hh; yl < m; yl += kCW * YPW) {
       const int y = Y0 + yl;
-      const double2 xv = Yv[yl * TM + x];
-      if (x >= ur0 && x < ur1) a.u[t.dst][(int64_t)(x + t.lo - 1) * M + y] = xv;
-      if (t.out2 >= 0 && (x == t.orow2 || x == t.orow2 + 1))
-        a.trace[((int64_t)t.out2 * 2 + (x - t.orow2)) * M + y] = xv;
-      if (t.out4 >= 0 && (x == t.orow4 || x == t.orow4 + 1))
-        a.trace[((int64_t)t.out4 * 2 + (x - t.orow4)) * M + y] = xv;
+#pragma unroll
+      for (int rh = 0; rh < NR; ++rh) {
+        const double2 xv = Yv[rh * FS + yl * TM + x];
+        if (x >= ur0 && x < ur1)
+          a.u[t.dst][rh * a.vs_u[t.dst] + (int64_t)(x + t.lo - 1) * M + y] = xv;
+        if (t.out2 >= 0 && (x == t.orow2 || x == t.orow2 + 1))
+          a.trace[rh * a.ts + ((int64_t)t.out2 * 2 + (x - t.orow2)) * M + y] = xv;
+        if (t.out4 >= 0 && (x == t.orow4 || x == t.orow4 + 1))
+          a.trace[rh * a.ts + ((int64_t)t.out4 * 2 + (x - t.orow4)) * M + y] = xv;
+      }
     }
     stamp(ti, 43);
     prev = t;
@@ -1848,17 +2027,59 @@ cudaLaunchConfig_t solve_config(int C, int nfront, int smem, cudaStream_t st,
   return cfg;
 }
 
-template <int TM>
-cudaError_t prepare_solve(int C, int mmax, int* max_clusters) {
-  cudaError_t e = cudaFuncSetAttribute(k_part_solve<TM>,
+template <int TM, int NR>
+cudaError_t prepare_solve_nr(int C, int mmax, int* max_clusters) {
+  cudaError_t e = cudaFuncSetAttribute(k_part_solve<TM, NR>,
                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
-  const int smem = Ring<TM>::smem(mmax);
-  e = cudaFuncSetAttribute(k_part_solve<TM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int smem = Ring<TM>::smem(mmax, C, NR);
+  e = cudaFuncSetAttribute(k_part_solve<TM, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchAttribute attr[1];
   cudaLaunchConfig_t cfg = solve_config(C, 1, smem, nullptr, attr);
-  return cudaOccupancyMaxActiveClusters(max_clusters, k_part_solve<TM>, &cfg);
+  return cudaOccupancyMaxActiveClusters(max_clusters, k_part_solve<TM, NR>, &cfg);
+}
+// every right-hand-side width of the kernel (kSolveWidths); *max_clusters: the
+// smallest co-residency over the widths (the fronts' clusters wait on each other)
+template <int TM>
+cudaError_t prepare_solve(int C, int mmax, int* max_clusters, int* max_nr = nullptr) {
+  cudaError_t e = prepare_solve_nr<TM, 1>(C, mmax, max_clusters);
+  if (e != cudaSuccess || !max_nr) return e;
+  // wider kernels are optional: available when their vectors leave room for
+  // a ring of >= 3 chunks and as many clusters co-reside
+  *max_nr = 1;
+  int mc = 0;
+  if (Ring<TM>::fixed(mmax, C, 2) + 3 * (Ring<TM>::CHUNK * 16 + 16) <= 225 * 1024 &&
+      prepare_solve_nr<TM, 2>(C, mmax, &mc) == cudaSuccess && mc >= *max_clusters) {
+    *max_nr = 2;
+    if (Ring<TM>::fixed(mmax, C, 4) + 3 * (Ring<TM>::CHUNK * 16 + 16) <= 225 * 1024 &&
+        prepare_solve_nr<TM, 4>(C, mmax, &mc) == cudaSuccess && mc >= *max_clusters)
+      *max_nr = 4;
+  }
+  cudaGetLastError();
+  return cudaSuccess;
+}
+// launch the slab-solve kernel for nr (1, 2 or 4) right-hand sides
+static cudaError_t launch_solve(int tm, int nr, int C, int nclusters, int mmax, cudaStream_t st,
+                                SolveArgs& a) {
+  const int smem = tm == 16 ? Ring<16>::smem(mmax, C, nr) : Ring<32>::smem(mmax, C, nr);
+  a.nchunk = tm == 16 ? Ring<16>::nchunk(mmax, C, nr) : Ring<32>::nchunk(mmax, C, nr);
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = solve_config(C, nclusters, smem, st, attr);
+  if (tm == 16) {
+    switch (nr) {
+      case 1: return cudaLaunchKernelEx(&cfg, k_part_solve<16, 1>, a);
+      case 2: return cudaLaunchKernelEx(&cfg, k_part_solve<16, 2>, a);
+      case 4: return cudaLaunchKernelEx(&cfg, k_part_solve<16, 4>, a);
+    }
+  } else {
+    switch (nr) {
+      case 1: return cudaLaunchKernelEx(&cfg, k_part_solve<32, 1>, a);
+      case 2: return cudaLaunchKernelEx(&cfg, k_part_solve<32, 2>, a);
+      case 4: return cudaLaunchKernelEx(&cfg, k_part_solve<32, 4>, a);
+    }
+  }
+  return cudaErrorInvalidValue;
 }
 
 template <int TM, int Q>
@@ -2347,8 +2568,9 @@ static void plan_bytes(const Sweep* s, std::vector<SweepLaunch>& plan) {
 }
 
 // level-2 exchange buffers of a work set (zeroed counters)
-static cudaError_t alloc_exchange(SweepWork* w) {
-  const size_t nb = (size_t)kMaxFront * 2 * kMaxG * 2 * 32 * sizeof(double2);
+constexpr int64_t kXStride = (int64_t)kMaxFront * 2 * kMaxG * 2 * 32;   // per right-hand side
+static cudaError_t alloc_exchange(SweepWork* w, int nrhs = 1) {
+  const size_t nb = (size_t)nrhs * kXStride * sizeof(double2);
   const size_t nf = (size_t)kMaxFront * 2 * kMaxG * sizeof(unsigned);
   cudaError_t e = cudaMalloc((void**)&w->xbuf, nb);
   if (e == cudaSuccess) e = cudaMalloc((void**)&w->xflag, nf);
@@ -2498,8 +2720,8 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     for (int k = 0; k < NCH; ++k) s->mmax = std::max(s->mmax, s->y0s[k + 1] - s->y0s[k]);
     while ((s->mmax - 1) / (1 << s->L) + 1 > qmax) ++s->L;   // (uniform fallback only)
     // the kernel's shared memory follows the final chunk length
-    cudaError_t e0 = TM == 16 ? prepare_solve<16>(C, s->mmax, &maxc)
-                              : prepare_solve<32>(C, s->mmax, &maxc);
+    cudaError_t e0 = TM == 16 ? prepare_solve<16>(C, s->mmax, &maxc, &s->max_nr)
+                              : prepare_solve<32>(C, s->mmax, &maxc, &s->max_nr);
     if (e0 != cudaSuccess || maxc < 2 * G) {
       cudaGetLastError();
       delete s;
@@ -2796,6 +3018,7 @@ void sweep_destroy(Sweep* s) {
   cudaFree(s->x2);
   cudaFree(s->own.xbuf);
   cudaFree(s->own.xflag);
+  if (s->batch.trace) sweep_work_destroy(&s->batch);
   delete s;
 }
 
@@ -2873,7 +3096,6 @@ int sweep_solve_one(Ctx* c, Sweep* s, int j, int64_t a, int64_t b, int64_t ta, i
     g.ffirst[0] = 0;
     g.fcount[0] = 1;
     g.g = make_chunks(s);
-    g.nchunk = s->tm == 16 ? Ring<16>::nchunk(s->mmax) : Ring<32>::nchunk(s->mmax);
     g.stream = s->stream;
     g.nbs = s->nbs;
     g.plan = s->ptab;
@@ -2889,12 +3111,8 @@ int sweep_solve_one(Ctx* c, Sweep* s, int j, int64_t a, int64_t b, int64_t ta, i
     g.xbuf = s->own.xbuf;
     g.xflag = s->own.xflag;
     for (int i = 0; i < kMaxFront; ++i) g.xbase[i] = s->own.xcount[i];
-    const int smem = s->tm == 16 ? Ring<16>::smem(s->mmax) : Ring<32>::smem(s->mmax);
-    cudaLaunchAttribute attr[1];
-    cudaLaunchConfig_t cfg = solve_config(s->C, s->G, smem, c->stream, attr);
     ProfScope ps(c, K_SWEEP_FRONT, s->rec_bytes);
-    cudaError_t e = s->tm == 16 ? cudaLaunchKernelEx(&cfg, k_part_solve<16>, g)
-                                : cudaLaunchKernelEx(&cfg, k_part_solve<32>, g);
+    cudaError_t e = launch_solve(s->tm, 1, s->C, s->G, s->mmax, c->stream, g);
     if (e != cudaSuccess) return check_cuda(c, e, "slab solve launch");
     s->own.xcount[0] += 1;
     HS_LAUNCH_CHECK(c, "slab solve kernel");
@@ -2913,14 +3131,17 @@ int sweep_solve_one(Ctx* c, Sweep* s, int j, int64_t a, int64_t b, int64_t ta, i
   return HS_OK;
 }
 
-int sweep_work_create(Ctx* c, const Sweep* s, SweepWork* w) {
+int sweep_work_create(Ctx* c, const Sweep* s, SweepWork* w, int nrhs) {
   if (s->s3) return set_error(c, HS_E_ARG, "sweep lanes need a 2-D level (the 3-D solve uses every SM)");
+  if (nrhs < 1) return set_error(c, HS_E_ARG, "a work set holds at least one right-hand side");
   *w = SweepWork{};
-  const size_t nf = (size_t)s->n0 * s->M * sizeof(double2);
-  cudaError_t e = cudaMalloc((void**)&w->trace, (size_t)std::max(1, s->ntrace) * 2 * s->M * sizeof(double2));
+  w->nrhs = nrhs;
+  const size_t nf = (size_t)nrhs * s->n0 * s->M * sizeof(double2);
+  cudaError_t e = cudaMalloc((void**)&w->trace,
+                             (size_t)nrhs * std::max(1, s->ntrace) * 2 * s->M * sizeof(double2));
   if (e == cudaSuccess) e = cudaMalloc((void**)&w->g, nf);
   if (e == cudaSuccess) e = cudaMalloc((void**)&w->u2, nf);
-  if (e == cudaSuccess) e = alloc_exchange(w);
+  if (e == cudaSuccess) e = alloc_exchange(w, nrhs);
   if (e != cudaSuccess) {
     sweep_work_destroy(w);
     return check_cuda(c, e, "sweep work buffers");
@@ -2937,9 +3158,43 @@ void sweep_work_destroy(SweepWork* w) {
   *w = SweepWork{};
 }
 
+// nr right-hand sides (f + r * stride -> u + r * stride) through the plan's
+// launches; nr > 1 needs a work set of at least nr and a 2-D level
+static int sweep_apply_nr(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
+                          const SweepWork* w, int first, int last, int nr, int64_t stride);
+
 int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
                 const SweepWork* w, int first, int last) {
+  return sweep_apply_nr(c, s, variant, f, u, w, first, last, 1, 0);
+}
+
+int sweep_apply_many(Ctx* c, Sweep* s, int variant, int nrhs, const double2* f, double2* u,
+                     int64_t stride) {
+  if (nrhs < 1) return set_error(c, HS_E_ARG, "nrhs must be at least 1");
+  if (nrhs > 1 && stride < (int64_t)s->n0 * s->M)
+    return set_error(c, HS_E_ARG, "right-hand-side stride shorter than a vector");
+  const int width = s->s3 || s->cpl0 ? 1 : s->max_nr;
+  if (width > 1 && nrhs > 1 && s->batch.nrhs < width) {
+    if (s->batch.trace) sweep_work_destroy(&s->batch);
+    if (int r = sweep_work_create(c, s, &s->batch, width)) return r;
+  }
+  for (int done = 0; done < nrhs;) {
+    int nr = 1;
+    while (nr * 2 <= width && done + nr * 2 <= nrhs) nr *= 2;
+    if (int r = sweep_apply_nr(c, s, variant, f + done * stride, u + done * stride,
+                               nr > 1 ? &s->batch : nullptr, 0, -1, nr, stride))
+      return r;
+    done += nr;
+  }
+  return HS_OK;
+}
+
+static int sweep_apply_nr(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
+                          const SweepWork* w, int first, int last, int nr, int64_t stride) {
   if (!w) w = &s->own;
+  if (nr > 1 && (s->s3 || w->nrhs < nr || nr > s->max_nr || s->cpl0))
+    return set_error(c, HS_E_ARG, "multi-right-hand-side sweep: unsupported level or work set");
+  const int64_t nlev = (int64_t)s->n0 * s->M;   // stride of the work set's g / u2
   if (!s->has_plan(variant))
     return set_error(c, HS_E_ARG,
                      variant == HS_VARIANT_X ? "X-sweep needs an even subdomain count"
@@ -2953,14 +3208,19 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
       case SweepLaunch::kCombine: {
         // u = u_pass1 + u_pass2 (the order of the reference's u[ta:tb] += ud)
         const int64_t n = (int64_t)s->n0 * M;
-        ProfScope ps(c, K_SWEEP_GATHER, 48.0 * n);
-        k_combine<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(u, w->u2, n);
-        HS_LAUNCH_CHECK(c, "combine kernel");
+        for (int rh = 0; rh < nr; ++rh) {
+          ProfScope ps(c, K_SWEEP_GATHER, 48.0 * n);
+          k_combine<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(u + rh * stride,
+                                                                          w->u2 + rh * nlev, n);
+          HS_LAUNCH_CHECK(c, "combine kernel");
+        }
         break;
       }
       case SweepLaunch::kResidual: {
-        int r = stencil_apply(c, s->coarse, u, w->g, 1, f);
-        if (r) return r;
+        for (int rh = 0; rh < nr; ++rh) {
+          int r = stencil_apply(c, s->coarse, u + rh * stride, w->g + rh * nlev, 1, f + rh * stride);
+          if (r) return r;
+        }
         break;
       }
       case SweepLaunch::kSolve: {
@@ -3013,7 +3273,6 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
           a.fcount[i] = i < Lh.nfront ? Lh.fcount[i] : 0;
         }
         a.g = make_chunks(s);
-        a.nchunk = s->tm == 16 ? Ring<16>::nchunk(s->mmax) : Ring<32>::nchunk(s->mmax);
         a.stream = s->stream;
         a.nbs = s->nbs;
         a.plan = s->ptab;
@@ -3029,6 +3288,11 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
         a.xbuf = w->xbuf;
         a.xflag = w->xflag;
         for (int i = 0; i < kMaxFront; ++i) a.xbase[i] = w->xcount[i];
+        a.vs_src = Lh.src ? nlev : stride;
+        a.vs_u[0] = stride;
+        a.vs_u[1] = nlev;
+        a.ts = (int64_t)std::max(1, s->ntrace) * 2 * M;
+        a.xs = kXStride;
         static const char* trace_path = getenv("HS_SWEEP_TRACE");
         static bool traced = false;
         unsigned long long* dbg = nullptr;
@@ -3037,12 +3301,8 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
           cudaMemsetAsync(dbg, 0, 16 * 1024 * sizeof(unsigned long long), c->stream);
         }
         a.dbg = dbg;
-        const int smem = s->tm == 16 ? Ring<16>::smem(s->mmax) : Ring<32>::smem(s->mmax);
-        cudaLaunchAttribute attr[1];
-        cudaLaunchConfig_t cfg = solve_config(s->C, Lh.nfront * s->G, smem, c->stream, attr);
         ProfScope ps(c, K_SWEEP_FRONT, Lh.bytes);
-        cudaError_t e = s->tm == 16 ? cudaLaunchKernelEx(&cfg, k_part_solve<16>, a)
-                                    : cudaLaunchKernelEx(&cfg, k_part_solve<32>, a);
+        cudaError_t e = launch_solve(s->tm, nr, s->C, Lh.nfront * s->G, s->mmax, c->stream, a);
         if (e != cudaSuccess) return check_cuda(c, e, "sweep solve launch");
         for (int i = 0; i < Lh.nfront; ++i)   // level-2 counters advance by the fronts' tasks
           const_cast<SweepWork*>(w)->xcount[i] += (unsigned)Lh.fcount[i];

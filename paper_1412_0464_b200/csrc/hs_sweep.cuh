@@ -33,6 +33,7 @@ struct Sweep3;   // 3-D levels (hs_sweep3.cu)
 // contributions.  The Sweep owns one; a cycle lane owns another so that
 // applications on different streams can run concurrently (2-D levels).
 struct SweepWork {
+  int nrhs = 1;                 // right-hand sides the buffers hold (each array nrhs copies)
   double2* trace = nullptr;     // [ntrace][2][M]
   double2* g = nullptr;         // [n0*M]
   double2* u2 = nullptr;        // [n0*M]
@@ -51,6 +52,8 @@ struct Sweep {
   int C = 1;                    // chunks per face segment = CTAs per cluster
   int G = 1;                    // face segments = clusters per front (two-level partition)
   int max_fronts = 16;          // fronts per solve launch (co-resident clusters / G)
+  int max_nr = 1;               // widest slab-solve kernel (right-hand sides per chain: 1, 2 or 4)
+  SweepWork batch;              // work set of the multi-right-hand-side applications (lazy)
   int L = 0;                    // local cyclic-reduction levels before the dense top
   int q = 1;                    // blocks left per chunk after L levels (dense inverse)
   int mmax = 0;                 // largest chunk (face points)
@@ -99,6 +102,11 @@ void sweep_destroy(Sweep* s);
 // launches [first, last) of the variant's plan (last < 0: to the end)
 int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
                 const SweepWork* w = nullptr, int first = 0, int last = -1);
+// nrhs right-hand sides f + r * stride -> u + r * stride through ONE chain of
+// slab solves per group of up to max_nr (every factor block streamed once
+// per group); per right-hand side bitwise the single application
+int sweep_apply_many(Ctx* c, Sweep* s, int variant, int nrhs, const double2* f, double2* u,
+                     int64_t stride);
 // allocate / free a SweepWork sized for s (2-D levels only)
 // NX schedule (prec_nx, sweepdd.py:403-437) for one cell grouping: j_cell
 // (ncell + 1 entries, sentinels -1 and J + 1) and j_mid (ncell entries);
@@ -109,7 +117,7 @@ int sweep_plan_nx(Ctx* c, Sweep* s, int ncell, const int64_t* j_cell, const int6
 int sweep_solve_one(Ctx* c, Sweep* s, int j, int64_t a, int64_t b, int64_t ta, int64_t tb,
                     const double2* B1, const double2* B3, double2* out2, double2* out4,
                     const double2* f, double2* u);
-int sweep_work_create(Ctx* c, const Sweep* s, SweepWork* w);
+int sweep_work_create(Ctx* c, const Sweep* s, SweepWork* w, int nrhs = 1);
 void sweep_work_destroy(SweepWork* w);
 
 // general sparse matrix rows (device CSR) for the exact solver's blocks

@@ -265,6 +265,24 @@ class DeviceSweep(_Handle):
         self.ctx.call("hs_sweep_apply", self.h, v, ptr(ft), ptr(u))
         return u, was_np
 
+    def rhs_width(self) -> int:
+        """right-hand sides one chain of slab solves carries (hs_sweep_rhs_width)"""
+        return int(self.ctx.lib.hs_sweep_rhs_width(self.h))
+
+    def apply_many(self, F, variant="x", cells=None):
+        """Rows of F (nrhs x n) through hs_sweep_apply_many: groups of up to
+        rhs_width() right-hand sides share one pass over the slab factors."""
+        v = variant if isinstance(variant, int) else self.variant_id(variant, cells)
+        torch = _torch()
+        was_np = not isinstance(F, torch.Tensor)
+        if was_np:
+            F = np.ascontiguousarray(np.asarray(F, dtype=complex))
+        nrhs = int(F.shape[0])
+        ft, _ = to_device(F, nrhs * self.n, self.ctx)
+        u = empty(nrhs * self.n, self.ctx)
+        self.ctx.call("hs_sweep_apply_many", self.h, v, nrhs, ptr(ft), ptr(u), self.n)
+        return u.reshape(nrhs, self.n), was_np
+
 
 class DeviceCSR(_Handle):
     """A general sparse matrix on the device for y = alpha A x (+ y)
@@ -407,6 +425,14 @@ class DeviceCycle(_Handle):
     def vcycle_dev(self, f_dev, out=None):
         u = out if out is not None else empty(self.n, self.ctx)
         self.ctx.call("hs_vcycle", self.h, ptr(f_dev), ptr(u))
+        return u
+
+    def vcycle_many_dev(self, F_dev, out=None):
+        """Rows of F_dev (nrhs x n, contiguous device tensor) through
+        hs_vcycle_many: one chain of slab solves for all of them."""
+        nrhs = int(F_dev.shape[0])
+        u = out if out is not None else empty(nrhs * self.n, self.ctx).reshape(nrhs, self.n)
+        self.ctx.call("hs_vcycle_many", self.h, nrhs, ptr(F_dev), ptr(u), self.n)
         return u
 
     def apply_a_begin(self, f_dev):

@@ -503,3 +503,184 @@ def _gmres(apply_a, apply_m, f, config: GmresConfig | None = None, orth: str = "
     if not was_np:
         out = out.reshape(f.shape)
     return out, report
+
+
+class _View:
+    """A right-hand side's rows of a shared (nrhs, rows, n) basis tensor."""
+
+    def __init__(self, V):
+        self.V = V
+
+    def ensure(self, rows):
+        if rows > self.V.shape[0]:
+            raise ValueError("lockstep basis too short")
+
+    def row(self, i):
+        return self.V[i]
+
+
+def _runs(idx):
+    """consecutive runs of a sorted index list: [(first, count)]"""
+    out = []
+    for i in idx:
+        if out and out[-1][0] + out[-1][1] == i:
+            out[-1][1] += 1
+        else:
+            out.append([i, 1])
+    return [(a, b) for a, b in out]
+
+
+def gmres_many(apply_a, apply_m, rhs, config: GmresConfig | None = None):
+    """Independent restarted GMRES solves of several right-hand sides in
+    lockstep on one stream: at every Arnoldi step the preconditioner of all
+    unconverged right-hand sides is ONE ``hs_vcycle_many`` call, so their
+    coarse sweeps share one pass over the slab factors (several right-hand
+    sides per chain of slab solves).  Everything else -- the fine matvec, the
+    CGS2 orthogonalisation with the device-gated DGKS pass, the host Givens
+    rotations, the restart logic of ``gmres`` (krylov.py:105-146) -- runs per
+    right-hand side with the kernels and operation order of ``gmres``: each
+    solution, iteration count and residual history is bitwise the
+    single-right-hand-side solve's.  Needs this package's fine operator and
+    TGSP preconditioner with a finite restart; anything else falls back to
+    one ``gmres`` per right-hand side.  Returns [(u, SolveReport)]."""
+    import torch
+    if config is None:
+        config = GmresConfig()
+    rhs = list(rhs)
+    ctx = context()
+    probe = None
+    if rhs:
+        ft0, _ = to_device(rhs[0], None, ctx)
+        probe = _Ops(apply_a, apply_m, ft0.numel(), ctx)
+    if (len(rhs) < 2 or probe.cycle is None or config.restart is None
+            or getattr(apply_m, "lane", None) is not None):
+        return [gmres(apply_a, apply_m, f, config) for f in rhs]
+    was = gc.isenabled()
+    gc.disable()
+    try:
+        return _gmres_many(probe, rhs, config)
+    finally:
+        if was:
+            gc.enable()
+
+
+def _gmres_many(ops: _Ops, rhs, config: GmresConfig):
+    import torch
+    ctx, n, cyc = ops.ctx, ops.n, ops.cycle
+    dev = torch.device(f"cuda:{ctx.device}")
+    R = len(rhs)
+    t0 = time.perf_counter()
+    steps0 = min(config.restart, config.max_iter)
+    rows = steps0 + 1
+    W = steps0 + 2
+    fts, was_np = [], []
+    for f in rhs:
+        t, w = to_device(f, n, ctx)
+        fts.append(t)
+        was_np.append(w)
+    Vall = torch.empty((R, rows, n), dtype=torch.complex128, device=dev)
+    Zall = torch.empty((R, rows, n), dtype=torch.complex128, device=dev)   # (same stride as Vall)
+    cols = torch.zeros((R, 2 * W + 2), dtype=torch.complex128, device=dev)
+    pins = torch.empty((R, 2 * W + 2), dtype=torch.complex128, pin_memory=True)
+    stream = torch.cuda.current_stream(dev)
+    event = torch.cuda.Event()
+    bases = [_View(Vall[r]) for r in range(R)]
+    zbs = [_View(Zall[r]) for r in range(R)]
+    us = [empty(n, ctx).zero_() for _ in range(R)]
+    hist = [[1.0] for _ in range(R)]
+    done = [False] * R
+    bnorm = [0.0] * R
+    res, res_norm = list(fts), [0.0] * R
+    for r in range(R):
+        bnorm[r], bad = _norm(ctx, fts[r], n)
+        if bad or not math.isfinite(bnorm[r]):
+            raise FloatingPointError("right-hand side contains non-finite values")
+        res_norm[r] = bnorm[r]
+        if bnorm[r] == 0.0:
+            hist[r] = [0.0]
+            done[r] = True
+
+    def orthonormalise(r, k):
+        basis, col = bases[r], cols[r]
+        hb, h2b, nb = col[:W], col[W:2 * W], col[2 * W:]
+        w = basis.row(k + 1)
+        _dot_pass(ctx, basis, k + 1, w, n, hb)
+        gate = (nb[0:], hb[k + 1:])
+        if not _update_dot_pass(ctx, basis, k + 1, hb, w, n, nb[0:], h2b):
+            _update_pass(ctx, basis, k + 1, hb, w, n, nb[0:])
+            _dot_pass(ctx, basis, k + 1, w, n, h2b, gate)
+        _update_pass(ctx, basis, k + 1, h2b, w, n, nb[1:], gate)
+        ctx.call("hs_scale_inv_sqrt", ptr(w), n, ptr(nb[1:]))
+
+    while True:
+        live = [r for r in range(R) if not done[r] and len(hist[r]) - 1 < config.max_iter]
+        if not live:
+            break
+        # ---- one restart cycle of every live right-hand side, in lockstep
+        steps = {r: min(config.max_iter - (len(hist[r]) - 1), config.restart) for r in live}
+        hess = {r: np.zeros((steps[r] + 1, steps[r]), dtype=complex) for r in live}
+        cs = {r: np.zeros(steps[r], dtype=complex) for r in live}
+        sn = {r: np.zeros(steps[r], dtype=complex) for r in live}
+        g = {r: np.zeros(steps[r] + 1, dtype=complex) for r in live}
+        kdone = {}
+        for r in live:
+            v0 = bases[r].row(0)
+            v0.copy_(res[r])
+            ctx.call("hs_scale", ptr(v0), n, 1.0 / res_norm[r], 0.0)
+            g[r][0] = res_norm[r]
+        active = list(live)
+        k = 0
+        while active:
+            for first, count in _runs(active):   # z_k = M v_k: one chain for the run
+                ctx.call("hs_vcycle_many", cyc.h, count, ptr(Vall[first, k]), ptr(Zall[first, k]),
+                         rows * n)
+            for r in active:
+                ctx.call("hs_stencil_apply", ops.fine.h, ptr(Zall[r, k]), ptr(Vall[r, k + 1]), 1)
+                orthonormalise(r, k)
+            for r in active:
+                pins[r].copy_(cols[r], non_blocking=True)
+            event.record(stream)
+            event.synchronize()
+            nxt = []
+            for r in active:
+                host = pins[r].numpy()
+                hcol, w_norm0, nrm1 = host[:k + 1].copy(), host[k + 1].real, host[2 * W].real
+                if not math.isfinite(w_norm0):
+                    raise FloatingPointError("operator produced non-finite values "
+                                             f"at iteration {len(hist[r])}")
+                if nrm1 < (_DGKS ** 2) * w_norm0:          # the device ran the DGKS pass
+                    hcol = hcol + host[W:W + k + 1]
+                nrm2 = host[2 * W + 1].real
+                if not (math.isfinite(nrm2) and np.all(np.isfinite(hcol))):
+                    raise FloatingPointError("operator produced non-finite values "
+                                             f"at iteration {len(hist[r])}")
+                hess[r][:k + 1, k] = hcol
+                hess[r][k + 1, k] = math.sqrt(max(nrm2, 0.0))
+                happy = hess[r][k + 1, k].real <= 1e-14 * res_norm[r]
+                _givens_column(hess[r], cs[r], sn[r], g[r], k)
+                hist[r].append(abs(g[r][k + 1]) / bnorm[r])
+                if hist[r][-1] <= config.tol or happy:
+                    kdone[r] = k + 1
+                elif k + 1 >= steps[r]:
+                    kdone[r] = k + 1
+                else:
+                    nxt.append(r)
+            active = nxt
+            k += 1
+        # ---- u += Z y, true residual (gmres' restart logic per right-hand side)
+        for r in live:
+            mdv = _basis_update(ctx, zbs[r], hess[r], g[r], kdone[r], n, dev)
+            ctx.call("hs_axpby", 1.0, 0.0, ptr(mdv), 1.0, 0.0, ptr(us[r]), n)
+            res[r] = ops.residual(fts[r], us[r])
+            res_norm[r], _ = _norm(ctx, res[r], n)
+            done[r] = res_norm[r] / bnorm[r] <= config.tol   # the true residual decides
+    out = []
+    wall = time.perf_counter() - t0
+    for r in range(R):
+        h = np.asarray(hist[r])
+        rep = SolveReport(len(h) - 1, h, bool(h[-1] <= config.tol), wall)
+        u = from_device(us[r], was_np[r])
+        if not was_np[r]:
+            u = u.reshape(rhs[r].shape)
+        out.append((u, rep))
+    return out

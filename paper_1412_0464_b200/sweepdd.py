@@ -436,6 +436,26 @@ def _apply(part: Partition, f, variant: str, cells=None):
     return u.reshape(f.shape) if hasattr(f, "shape") else u
 
 
+def prec_many(part: Partition, F, variant: str = "x", cells=None):
+    """The sweep applied to a stack of right-hand sides F[r] (shape
+    (nrhs,) + level shape, or (nrhs, n)): groups of up to
+    ``part.device().rhs_width()`` right-hand sides go through one chain of
+    slab solves, every factor block streamed once per group
+    (hs_sweep_apply_many; the reference solves multi-column right-hand sides
+    in one SuperLU call, sparselin.py:58-62).  Row r is bitwise
+    ``prec_x(part, F[r])`` / ``prec_ud`` / ``prec_nx``."""
+    from .device import from_device
+    if variant == "x" and part.J % 2 != 0:
+        raise ValueError(f"X-sweep needs an even subdomain count, got {part.J}")
+    nrhs = int(F.shape[0])
+    n = int(np.prod(part.shape))
+    flat = F.reshape(nrhs, n)
+    u, was_np = part.device().apply_many(flat, variant, cells)
+    if was_np:
+        return from_device(u, True, tuple(F.shape))
+    return u.reshape(F.shape)
+
+
 def prec_ud(part: Partition, f):
     return _apply(part, f, "ud")
 

@@ -262,6 +262,24 @@ class TwoGridCycle:
             return from_device(u, True, self.fine_op.shape)
         return u.reshape(f.shape)
 
+    def vcycle_many(self, F):
+        """One cycle per row of the stack F (nrhs, ...): the coarse sweeps of
+        all rows through one chain of slab solves (hs_vcycle_many); row r is
+        bitwise ``vcycle(F[r])``."""
+        from .device import from_device, to_device
+        if self.generic:
+            return np.stack([self._vcycle_matrix(F[r]) for r in range(F.shape[0])])
+        dev = self.device()
+        nrhs = int(F.shape[0])
+        was_np = not hasattr(F, "is_cuda")
+        if was_np:
+            F = np.ascontiguousarray(np.asarray(F, dtype=complex))
+        ft, _ = to_device(F, nrhs * dev.n, dev.ctx)
+        u = dev.vcycle_many_dev(ft.reshape(nrhs, dev.n))
+        if was_np:
+            return from_device(u, True, tuple(F.shape))
+        return u.reshape(F.shape)
+
     def as_preconditioner(self, lane=None):
         """The flat-vector preconditioner callable (twogrid.py:161-164);
         ``lane``: run on a :class:`Lane` (its own context and stream)."""
@@ -304,20 +322,27 @@ class Lane:
         return self.cycle.as_preconditioner(lane=self)
 
 
-def solve_many(cycle: TwoGridCycle, rhs, config=None, lanes: int = 4, orth: str = "cgs2"):
-    """Independent GMRES solves of several right-hand sides (C4's sources),
-    ``lanes`` of them in flight at once on one GPU (one host thread and one
-    CUDA stream per lane; the sweeps of different lanes run on disjoint
+def solve_many(cycle: TwoGridCycle, rhs, config=None, lanes: int = 4, orth: str = "cgs2",
+               batch: bool = False):
+    """Independent GMRES solves of several right-hand sides (C4's sources).
+    ``batch=True``: the solves advance in lockstep and every Arnoldi step's
+    coarse sweeps go through one chain of slab solves (``gmres_many``:
+    several right-hand sides per pass over the slab factors).  Otherwise
+    ``lanes`` of them are in flight at once on one GPU (one host thread and
+    one CUDA stream per lane; the sweeps of different lanes run on disjoint
     clusters).  Stream-ordered with the caller: the lanes start after the
     caller's current stream and the caller's stream waits for all of them.
+    Either way each solve is bitwise the sequential ``gmres``.
     Returns [(u, SolveReport)] in input order."""
     import concurrent.futures as cf
     import threading
     import torch
-    from .krylov import gmres
+    from .krylov import gmres, gmres_many
     rhs = list(rhs)
     if not rhs:
         return []
+    if batch and orth == "cgs2":
+        return gmres_many(cycle.fine_csr, cycle.as_preconditioner(), rhs, config)
     if lanes <= 1 or not _lane_capable(cycle):
         # 3-D levels and the exact coarse solve run one cooperative all-SM
         # chain per slab solve: no concurrent lanes, solves in order

@@ -616,3 +616,81 @@ def test_tgsp_apply_matches_reference_at_config_size(name):
     bs = np.array([b.sum() for b in np.array_split(y, a["n_blocks"])])
     bref = np.asarray(a["block_sums_re"]) + 1j * np.asarray(a["block_sums_im"])
     assert np.linalg.norm(bs - bref) <= 1e-10 * np.linalg.norm(bref)
+
+
+@pytest.mark.parametrize("name", ["pml2d", "wedge2d", "nx2d"])
+def test_sweep_many_rhs_bitwise(name):
+    """Several right-hand sides through one chain of slab solves
+    (hs_sweep_apply_many, the reference's multi-column solve
+    sparselin.py:58-62): each row bitwise the single application, for group
+    widths 4, 2 and 1 (5 = 4 + 1, 3 = 2 + 1) and every sweep variant."""
+    import torch
+    import paper_1412_0464_b200 as hb
+    hh = hierarchy(name)
+    part = hh.partition
+    shape = part.shape
+    rng = np.random.default_rng(11)
+    F = np.stack([crand(rng, shape) for _ in range(7)])
+    variants = [("x", None), ("ud", None)]
+    if name == "nx2d":
+        variants.append(("nx", hb.make_nx_cells(part.J, 2)))
+    for v, cells in variants:
+        single = [hb.prec_x(part, F[r]) if v == "x" else hb.prec_ud(part, F[r]) if v == "ud"
+                  else hb.prec_nx(part, F[r], cells) for r in range(7)]
+        for k in (2, 3, 5, 7):
+            many = hb.prec_many(part, F[:k], v, cells)
+            assert many.shape == (k,) + tuple(shape)
+            for r in range(k):
+                assert np.array_equal(many[r], single[r]), (v, k, r)
+    # device tensors in, tensor out
+    Ft = torch.from_numpy(F[:4]).cuda()
+    out = hb.prec_many(part, Ft, "x")
+    assert isinstance(out, torch.Tensor) and np.array_equal(out.cpu().numpy()[3], hb.prec_x(part, F[3]))
+
+
+def test_sweep_many_rhs_two_level_partition():
+    """The same on a face wide enough for the two-level partition (G > 1
+    clusters per front: level-2 exchange buffers per right-hand side) --
+    C2's recipe at 1/2 size -- and through the whole cycle (hs_vcycle_many)."""
+    import paper_1412_0464_b200 as hb
+    from paper_1412_0464_b200.configs import config
+    p = config(1, 2)
+    cycle, _ = hb.build_two_grid(p.mesh, p.model, smoother=hb.SmootherConfig(p.omega_jac, p.nu),
+                                 coarse="sweep",
+                                 sweep=hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains))
+    part = cycle.hierarchy.partition
+    sw = part.device()
+    assert sw.segments > 1 and sw.rhs_width() >= 2
+    rng = np.random.default_rng(5)
+    F = np.stack([crand(rng, part.shape) for _ in range(5)])
+    many = hb.prec_many(part, F, "x")
+    for r in range(5):
+        assert np.array_equal(many[r], hb.prec_x(part, F[r])), r
+    Z = np.stack([crand(rng, p.mesh.unknowns) for _ in range(3)])
+    out = cycle.vcycle_many(Z)
+    for r in range(3):
+        assert np.array_equal(out[r], cycle.vcycle(Z[r])), r
+
+
+def test_gmres_many_matches_sequential():
+    """Lockstep solves (gmres_many / solve_many(batch=True)): iteration
+    counts, residual histories and solutions bitwise the sequential gmres,
+    with right-hand sides that converge at different iterations."""
+    import paper_1412_0464_b200 as hb
+    cycle = _build("wedge2d")
+    mesh = case("wedge2d")[0]
+    rhs = []
+    for k in range(5):
+        f = np.zeros(mesh.unknowns, complex)
+        f[10 + 8 * k, 12 + 5 * k] = 1.0 / mesh.spacing[0][0] ** 2
+        rhs.append(f.ravel())
+    rhs.append(np.zeros(mesh.unknowns, complex).ravel())   # a zero right-hand side
+    for cfg in (hb.GmresConfig(1e-6, 200, 20), hb.GmresConfig(1e-8, 200, 5),
+                hb.GmresConfig(1e-6, 7, 5)):
+        seq = [hb.gmres(cycle.fine_csr, cycle.as_preconditioner(), f, cfg) for f in rhs]
+        par = hb.solve_many(cycle, rhs, cfg, batch=True)
+        assert len({r.iterations for _, r in seq}) > 1 or cfg.max_iter == 7
+        for (u0, r0), (u1, r1) in zip(seq, par):
+            assert r1.iterations == r0.iterations and r1.converged == r0.converged
+            assert np.array_equal(r1.residual_history, r0.residual_history)
+            assert np.array_equal(u1, u0)
