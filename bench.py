@@ -68,6 +68,8 @@ def parse():
                    help="multi-RHS configs: the solves advance in lockstep and their coarse "
                         "sweeps share one chain of slab solves per group (gmres_many) "
                         "instead of running as concurrent lanes")
+    p.add_argument("--batch-groups", type=int, default=2,
+                   help="with --batch: lockstep groups running side by side (one lane each)")
     p.add_argument("--segments", type=int, default=-1,
                    help="face segments per sweep front (-1: 1 when several right-hand sides "
                         "run as lanes, else automatic)")
@@ -369,8 +371,14 @@ def run_ours(args):
     mine = assign_rhs(nrhs_total, world, rank)
     # several right-hand sides in flight as lanes: one cluster per sweep front
     # (the lanes' sweeps run side by side); one at a time: the widest layout
+    # lockstep batches side by side: each group's two fronts get 7 // groups
+    # segments (14 nine-CTA clusters co-reside on a B200: 2 * groups * G <= 14)
+    groups = max(1, min(args.batch_groups, len(mine) // 2)) if args.batch else 1
+    if args.batch:
+        args.lanes = groups
     segments = args.segments if args.segments >= 0 else (
-        1 if len(mine) > 1 and args.lanes > 1 and not args.batch else 0)
+        (7 // groups if groups > 1 else 0) if args.batch
+        else 1 if len(mine) > 1 and args.lanes > 1 else 0)
     t0 = time.perf_counter()
     keep = (rank == 0 and world == 1 and not args.no_cpu_baseline)
     cycle, _ = hb.build_two_grid(p.mesh, p.model, fine_op=fine_operator(p),
@@ -560,8 +568,8 @@ def run_ours(args):
             "sweep_segments": dev.sweep.segments if p.mesh.dim == 2 else None,
             "rhs_per_rank": len(f_dev),
             "rhs_in_flight": (len(f_dev) if args.batch else min(args.lanes, len(f_dev))) if multi else 1,
-            "rhs_mode": ("lockstep batch (several right-hand sides per chain of slab solves)"
-                         if args.batch else "lanes") if multi else "single",
+            "rhs_mode": (f"{groups} lockstep batch(es) (several right-hand sides per chain of "
+                         "slab solves)" if args.batch else "lanes") if multi else "single",
             "reference_iterations": reference_iterations(p, args),
             "solve_s": ms / 1e3 / max(1, args.steps * len(f_dev)),
             "setup_s": setup_s,

@@ -185,6 +185,9 @@ int hs_sweep_apply(hs_ctx* ctx, hs_sweep* s, int variant, const void* f, void* u
 int hs_sweep_apply_many(hs_ctx* ctx, hs_sweep* s, int variant, int nrhs, const void* f, void* u,
                         long long stride);
 int hs_sweep_rhs_width(hs_sweep* s);
+/* Sweep fronts whose clusters can be co-resident on the device (2-D levels):
+ * concurrent lanes (hs_cycle_create_lane) need 2 fronts each. */
+int hs_sweep_max_fronts(hs_sweep* s);
 /* NX sweep (prec_nx, sweepdd.py:403-437; NxCells / make_nx_cells :362-401):
  * registers the launch plan of one cell grouping -- j_cell: ncell + 1 cell
  * boundaries with sentinels -1 and J + 1, j_mid: the slab where each cell's
@@ -255,8 +258,8 @@ int hs_cycle_destroy(hs_ctx* ctx, hs_cycle* c);
 /* u = M f : vcycle / tgsp_apply / as_preconditioner   twogrid.py:150-176 */
 int hs_vcycle(hs_ctx* ctx, hs_cycle* c, const void* f, void* u);
 /* nrhs cycles u_r = M f_r (twogrid.py:150-176 per column): fine-level halves
- * per right-hand side, the coarse sweeps through hs_sweep_apply_many.  Not
- * for lanes (hs_cycle_create_lane). */
+ * per right-hand side, the coarse sweeps through hs_sweep_apply_many (a lane,
+ * hs_cycle_create_lane, uses its own work set). */
 int hs_vcycle_many(hs_ctx* ctx, hs_cycle* c, int nrhs, const void* f, void* u, long long stride);
 /* GMRES operator application keeping the preconditioned vector: z = M f,
  * w = A z, in parts like hs_vcycle_apply_a_part (0 pre-coarse into z, 1 the

@@ -67,6 +67,7 @@ SIGNATURES = {
     "hs_sweep_apply": (C.c_int, [_vp, _vp, C.c_int, _vp, _vp]),
     "hs_sweep_apply_many": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _vp, C.c_longlong]),
     "hs_sweep_rhs_width": (C.c_int, [_vp]),
+    "hs_sweep_max_fronts": (C.c_int, [_vp]),
     "hs_sweep_factor_bytes": (C.c_longlong, [_vp]),
     "hs_sweep_plan_launches": (C.c_int, [_vp, C.c_int]),
     "hs_sweep_segments": (C.c_int, [_vp]),
@@ -124,6 +125,8 @@ def load_library(path: Path | str | None = None):
                           "`python -m paper_1412_0464_b200.build` (nvcc, sm_100a)")
         lib = C.CDLL(str(p))
         for name, (res, args) in SIGNATURES.items():
+            if not hasattr(lib, name) and "HS_LIB" in os.environ:
+                continue   # an A/B variant library built from older sources
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

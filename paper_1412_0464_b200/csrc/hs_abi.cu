@@ -7,6 +7,7 @@
 #include "hs_sweep.cuh"
 #include "hs_transfer.cuh"
 
+#include <algorithm>
 #include <cmath>
 #include <new>
 
@@ -154,7 +155,6 @@ static int vcycle(Ctx* c, Cycle* cy, const double2* f, double2* u) {
 // the kernels and their arithmetic are those of vcycle().
 static int vcycle_many(Ctx* c, Cycle* cy, int nrhs, const double2* f, double2* u, int64_t stride) {
   if (nrhs == 1) return vcycle(c, cy, f, u);
-  if (cy->lane) return set_error(c, HS_E_ARG, "multi-right-hand-side cycles run on the base cycle");
   const int64_t nf = cy->fine->d.n, nc = cy->coarse->d.n;
   if (stride < nf) return set_error(c, HS_E_ARG, "right-hand-side stride shorter than a vector");
   if (cy->nb < nrhs) {
@@ -186,7 +186,9 @@ static int vcycle_many(Ctx* c, Cycle* cy, int nrhs, const double2* f, double2* u
     }
     if ((r = transfer_restrict(c, cy->t, cy->r, cy->brc + k * nc, cy->scale, 1))) return r;
   }
-  if ((r = sweep_apply_many(c, cy->sweep, cy->variant, nrhs, cy->brc, cy->buc, nc))) return r;
+  if ((r = sweep_apply_many(c, cy->sweep, cy->variant, nrhs, cy->brc, cy->buc, nc,
+                            cy->lane ? &cy->work : nullptr)))
+    return r;
   for (int k = 0; k < nrhs; ++k) {   // prolongation + correction, post-smoothing
     const double2* fk = f + k * stride;
     double2* uk = u + k * stride;
@@ -529,6 +531,7 @@ int hs_sweep_apply_many(hs_ctx* c, hs_sweep* s, int variant, int nrhs, const voi
 }
 
 int hs_sweep_rhs_width(hs_sweep* s) { return s && !s->s3 && !s->cpl0 ? s->max_nr : 1; }
+int hs_sweep_max_fronts(hs_sweep* s) { return s && !s->s3 ? s->max_fronts : 0; }
 
 int hs_sweep_plan_nx(hs_ctx* c, hs_sweep* s, int ncell, const int64_t* j_cell,
                      const int64_t* j_mid, int* variant) {
@@ -605,7 +608,8 @@ int hs_cycle_create_lane(hs_ctx* c, const hs_cycle* base, hs_cycle** out) {
   cy->scale = base->scale;
   cy->variant = base->variant;
   cy->lane = true;
-  if (int r = sweep_work_create(c, cy->sweep, &cy->work)) {
+  // (as wide as the sweep's widest kernel: a lane can run hs_vcycle_many)
+  if (int r = sweep_work_create(c, cy->sweep, &cy->work, std::max(1, cy->sweep->max_nr))) {
     delete cy;
     return r;
   }

@@ -1742,7 +1742,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
     }
     {   // x at the level-L points = sum of the column-pair partials
       for (int t = threadIdx.x; t < NR * qk * TM; t += kCW * 32) {
-        const int rh = t / (qk * TM), t1 = t - rh * qk * TM;
+        const int rh = NR == 1 ? 0 : t / (qk * TM), t1 = t - rh * qk * TM;
         const int r = t1 / TM, xx = t1 % TM;
         double2 acc = czero();
         for (int cp = 0; cp < QP; ++cp) acc = cadd(acc, part[rh * PS + (r * QP + cp) * TM + xx]);
@@ -1843,7 +1843,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
           }
         }
         asm volatile("bar.sync 3, %0;" ::"r"((kCW - kNA) * 32) : "memory");
-        for (int tt = threadIdx.x - kNA * 32; tt < NR * N2; tt += (kCW - kNA) * 32) {
+        static_assert((kCW - kNA) * 32 >= N2, "one reduction thread per interface unknown");
+        for (int tt = threadIdx.x - kNA * 32; tt < NR * N2; tt += NR == 1 ? 1 << 20 : (kCW - kNA) * 32) {
           const int rh = tt / N2, t = tt % N2;
           double2 sacc = czero();
           for (int w = 0; w < kCW - kNA; ++w) sacc = cadd(sacc, part[rh * PS + w * N2 + t]);
@@ -1894,7 +1895,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
           asm volatile("bar.sync 3, %0;" ::"r"((kCW - kNA) * 32) : "memory");
           // level-2 right-hand side in k_reduced order: block 2b = c_b, 2b + 1 = d_{b+1}
           for (int ii = threadIdx.x - kNA * 32; ii < NR * nz * TM; ii += (kCW - kNA) * 32) {
-            const int rh = ii / (nz * TM), i = ii - rh * nz * TM;
+            const int rh = NR == 1 ? 0 : ii / (nz * TM), i = ii - rh * nz * TM;
             const int blk = i / TM, e = i % TM, b2 = blk / 2;
             const int sg = (blk & 1) ? b2 + 1 : b2;
             t2v[rh * T2S + i] = __ldcg(&xb[rh * a.xs + (sg * 2 + (blk & 1)) * TM + e]);
@@ -1917,7 +1918,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
         stamp(ti, 47);
         const double2* pqs = pqv + par * NR * N2;
         cgemv(r_l2 + P.ct + P.zq, 2, pqs, N2, ab, N2, true);
-        for (int ee = threadIdx.x - kNA * 32; ee < NR * TM; ee += (kCW - kNA) * 32) {
+        for (int ee = threadIdx.x - kNA * 32; ee < NR * TM; ee += NR == 1 ? 1 << 20 : (kCW - kNA) * 32) {
           const int rh = ee / TM, e = ee % TM;
           const int nb = (((ti + 1) & 1) * NR + rh) * HS;   // next task's halo: edge values across segments
           if (rank == 0 && seg > 0) {
@@ -2046,13 +2047,14 @@ cudaError_t prepare_solve(int C, int mmax, int* max_clusters, int* max_nr = null
   cudaError_t e = prepare_solve_nr<TM, 1>(C, mmax, max_clusters);
   if (e != cudaSuccess || !max_nr) return e;
   // wider kernels are optional: available when their vectors leave room for
-  // a ring of >= 3 chunks and as many clusters co-reside
+  // a ring of >= 5 chunks (C3's 34-point chunks with 3 slots: 4 right-hand
+  // sides per chain measured slower than 2) and as many clusters co-reside
   *max_nr = 1;
   int mc = 0;
-  if (Ring<TM>::fixed(mmax, C, 2) + 3 * (Ring<TM>::CHUNK * 16 + 16) <= 225 * 1024 &&
+  if (Ring<TM>::fixed(mmax, C, 2) + 5 * (Ring<TM>::CHUNK * 16 + 16) <= 225 * 1024 &&
       prepare_solve_nr<TM, 2>(C, mmax, &mc) == cudaSuccess && mc >= *max_clusters) {
     *max_nr = 2;
-    if (Ring<TM>::fixed(mmax, C, 4) + 3 * (Ring<TM>::CHUNK * 16 + 16) <= 225 * 1024 &&
+    if (Ring<TM>::fixed(mmax, C, 4) + 5 * (Ring<TM>::CHUNK * 16 + 16) <= 225 * 1024 &&
         prepare_solve_nr<TM, 4>(C, mmax, &mc) == cudaSuccess && mc >= *max_clusters)
       *max_nr = 4;
   }
@@ -3169,20 +3171,26 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
 }
 
 int sweep_apply_many(Ctx* c, Sweep* s, int variant, int nrhs, const double2* f, double2* u,
-                     int64_t stride) {
+                     int64_t stride, const SweepWork* w) {
   if (nrhs < 1) return set_error(c, HS_E_ARG, "nrhs must be at least 1");
   if (nrhs > 1 && stride < (int64_t)s->n0 * s->M)
     return set_error(c, HS_E_ARG, "right-hand-side stride shorter than a vector");
-  const int width = s->s3 || s->cpl0 ? 1 : s->max_nr;
-  if (width > 1 && nrhs > 1 && s->batch.nrhs < width) {
-    if (s->batch.trace) sweep_work_destroy(&s->batch);
-    if (int r = sweep_work_create(c, s, &s->batch, width)) return r;
+  int width = s->s3 || s->cpl0 ? 1 : s->max_nr;
+  if (w) {   // a lane's work set: as wide as it was created
+    width = std::min(width, w->nrhs);
+  } else if (width > 1 && nrhs > 1) {
+    if (s->batch.nrhs < width || !s->batch.trace) {
+      if (s->batch.trace) sweep_work_destroy(&s->batch);
+      if (int r = sweep_work_create(c, s, &s->batch, width)) return r;
+    }
+    w = &s->batch;
   }
   for (int done = 0; done < nrhs;) {
     int nr = 1;
     while (nr * 2 <= width && done + nr * 2 <= nrhs) nr *= 2;
+    // (a single right-hand side of the sweep's own stream: its own work set)
     if (int r = sweep_apply_nr(c, s, variant, f + done * stride, u + done * stride,
-                               nr > 1 ? &s->batch : nullptr, 0, -1, nr, stride))
+                               nr > 1 || (w && w != &s->batch) ? w : nullptr, 0, -1, nr, stride))
       return r;
     done += nr;
   }
@@ -3296,7 +3304,8 @@ static int sweep_apply_nr(Ctx* c, Sweep* s, int variant, const double2* f, doubl
         static const char* trace_path = getenv("HS_SWEEP_TRACE");
         static bool traced = false;
         unsigned long long* dbg = nullptr;
-        if (trace_path && !traced && Lh.nfront == 2) {
+        static const int trace_nr = getenv("HS_SWEEP_TRACE_NR") ? atoi(getenv("HS_SWEEP_TRACE_NR")) : 1;
+        if (trace_path && !traced && Lh.nfront == 2 && nr == trace_nr) {
           cudaMalloc((void**)&dbg, 16 * 1024 * sizeof(unsigned long long));
           cudaMemsetAsync(dbg, 0, 16 * 1024 * sizeof(unsigned long long), c->stream);
         }

@@ -106,7 +106,7 @@ int sweep_apply(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
 // slab solves per group of up to max_nr (every factor block streamed once
 // per group); per right-hand side bitwise the single application
 int sweep_apply_many(Ctx* c, Sweep* s, int variant, int nrhs, const double2* f, double2* u,
-                     int64_t stride);
+                     int64_t stride, const SweepWork* w = nullptr);
 // allocate / free a SweepWork sized for s (2-D levels only)
 // NX schedule (prec_nx, sweepdd.py:403-437) for one cell grouping: j_cell
 // (ncell + 1 entries, sentinels -1 and J + 1) and j_mid (ncell entries);

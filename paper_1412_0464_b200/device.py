@@ -224,6 +224,11 @@ class DeviceSweep(_Handle):
     def chunks(self) -> int:
         return int(self.ctx.lib.hs_sweep_chunks(self.h))
 
+    @property
+    def max_fronts(self) -> int:
+        """sweep fronts whose clusters co-reside on the device (hs_sweep_max_fronts)"""
+        return int(self.ctx.lib.hs_sweep_max_fronts(self.h))
+
     def launches_per_apply(self, variant="x") -> int:
         """slab-solve launches of one application of the variant's plan"""
         return int(self.ctx.lib.hs_sweep_plan_launches(self.h, self.variant_id(variant)))

@@ -547,13 +547,13 @@ def gmres_many(apply_a, apply_m, rhs, config: GmresConfig | None = None):
     if config is None:
         config = GmresConfig()
     rhs = list(rhs)
-    ctx = context()
+    lane = getattr(apply_m, "lane", None)
+    ctx = lane.ctx if lane is not None else context()
     probe = None
     if rhs:
         ft0, _ = to_device(rhs[0], None, ctx)
         probe = _Ops(apply_a, apply_m, ft0.numel(), ctx)
-    if (len(rhs) < 2 or probe.cycle is None or config.restart is None
-            or getattr(apply_m, "lane", None) is not None):
+    if len(rhs) < 2 or probe.cycle is None or config.restart is None:
         return [gmres(apply_a, apply_m, f, config) for f in rhs]
     was = gc.isenabled()
     gc.disable()

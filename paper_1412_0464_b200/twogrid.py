@@ -342,8 +342,35 @@ def solve_many(cycle: TwoGridCycle, rhs, config=None, lanes: int = 4, orth: str 
     if not rhs:
         return []
     if batch and orth == "cgs2":
-        return gmres_many(cycle.fine_csr, cycle.as_preconditioner(), rhs, config)
-    if lanes <= 1 or not _lane_capable(cycle):
+        groups = max(1, min(lanes, len(rhs) // 2))
+        if groups <= 1 or not _lane_capable(cycle, groups):
+            return gmres_many(cycle.fine_csr, cycle.as_preconditioner(), rhs, config)
+        # `groups` lockstep batches side by side, one lane (thread, stream,
+        # work set) each: one batch's fine-level kernels overlap the other's
+        # sweep, and the sweeps' clusters share the device
+        pool = getattr(cycle, "_lanes", [])
+        if len(pool) < groups:
+            pool = pool + cycle.lanes(groups - len(pool))
+            cycle._lanes = pool
+        pool = pool[:groups]
+        main = torch.cuda.current_stream(pool[0].ctx.device)
+        start = torch.cuda.Event()
+        start.record(main)
+        per = -(-len(rhs) // groups)
+        parts = [rhs[i * per:(i + 1) * per] for i in range(groups)]
+
+        def run(i):
+            ln = pool[i]
+            with torch.cuda.stream(ln.stream):
+                ln.stream.wait_event(start)
+                return gmres_many(cycle.fine_csr, ln.preconditioner(), parts[i], config)
+
+        with cf.ThreadPoolExecutor(max_workers=groups) as ex:
+            outs = list(ex.map(run, range(groups)))
+        for ln in pool:
+            main.wait_stream(ln.stream)
+        return [o for part in outs for o in part]
+    if lanes <= 1 or not _lane_capable(cycle, min(lanes, len(rhs))):
         # 3-D levels and the exact coarse solve run one cooperative all-SM
         # chain per slab solve: no concurrent lanes, solves in order
         prec = cycle.as_preconditioner()
@@ -378,14 +405,16 @@ def solve_many(cycle: TwoGridCycle, rhs, config=None, lanes: int = 4, orth: str 
     return out
 
 
-def _lane_capable(cycle: TwoGridCycle) -> bool:
-    """Lanes need a 2-D sweep coarse solver (private sweep scratch per lane)
-    with one cluster per front: the G clusters of a two-level-partition front
-    wait on each other, so concurrent lanes could starve one another of
-    co-resident clusters."""
+def _lane_capable(cycle: TwoGridCycle, lanes: int = 2) -> bool:
+    """Lanes need a 2-D sweep coarse solver (private sweep scratch per lane).
+    The G clusters of a two-level-partition front wait on each other, so
+    with G > 1 every lane's two fronts must be co-resident at once:
+    2 * lanes <= the fronts the device holds (hs_sweep_max_fronts); with one
+    cluster per front nothing waits across clusters and any lane count runs."""
     if not (isinstance(cycle.coarse_solver, SweepCoarseSolver) and cycle.coarse_op.dim == 2):
         return False
-    return cycle.hierarchy.partition.device().segments == 1
+    sw = cycle.hierarchy.partition.device()
+    return sw.segments == 1 or 2 * lanes <= sw.max_fronts
 
 
 def vcycle(cycle: TwoGridCycle, f):

@@ -694,3 +694,32 @@ def test_gmres_many_matches_sequential():
             assert r1.iterations == r0.iterations and r1.converged == r0.converged
             assert np.array_equal(r1.residual_history, r0.residual_history)
             assert np.array_equal(u1, u0)
+
+
+def test_solve_many_batches_on_lanes():
+    """Two lockstep batches side by side (solve_many(batch=True, lanes=2):
+    one lane per batch, fronts of G = 3 segments so that both batches'
+    clusters co-reside): bitwise the sequential solves."""
+    import paper_1412_0464_b200 as hb
+    from paper_1412_0464_b200.configs import config
+    from paper_1412_0464_b200.twogrid import _lane_capable
+    p = config(1, 2)
+    cycle, _ = hb.build_two_grid(p.mesh, p.model, smoother=hb.SmootherConfig(p.omega_jac, p.nu),
+                                 coarse="sweep",
+                                 sweep=hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains,
+                                                       segments=3))
+    sw = cycle.hierarchy.partition.device()
+    assert sw.segments == 3 and _lane_capable(cycle, 2)
+    n = p.mesh.unknowns
+    rhs = []
+    for k in range(5):
+        f = np.zeros(n, complex)
+        f[40 + 37 * k, 50 + 61 * k] = 1.0 / p.mesh.spacing[0][0] ** 2
+        rhs.append(f.ravel())
+    cfg = hb.GmresConfig(1e-6, 60, 20)
+    seq = [hb.gmres(cycle.fine_csr, cycle.as_preconditioner(), f, cfg) for f in rhs]
+    par = hb.solve_many(cycle, rhs, cfg, lanes=2, batch=True)
+    for (u0, r0), (u1, r1) in zip(seq, par):
+        assert r1.iterations == r0.iterations
+        assert np.array_equal(r1.residual_history, r0.residual_history)
+        assert np.array_equal(u1, u0)
