@@ -64,10 +64,10 @@ def parse():
                    help="with --shard on one process: G logical shards on one GPU")
     p.add_argument("--lanes", type=int, default=4,
                    help="multi-RHS configs (C4): right-hand sides in flight at once per GPU")
-    p.add_argument("--batch", action="store_true",
-                   help="multi-RHS configs: the solves advance in lockstep and their coarse "
-                        "sweeps share one chain of slab solves per group (gmres_many) "
-                        "instead of running as concurrent lanes")
+    p.add_argument("--no-batch", dest="batch", action="store_false",
+                   help="multi-RHS configs: independent solves on concurrent lanes instead of "
+                        "the default lockstep batches (gmres_many: the solves advance together "
+                        "and their coarse sweeps share one chain of slab solves per group)")
     p.add_argument("--batch-groups", type=int, default=2,
                    help="with --batch: lockstep groups running side by side (one lane each)")
     p.add_argument("--segments", type=int, default=-1,
