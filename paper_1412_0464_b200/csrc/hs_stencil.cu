@@ -294,7 +294,13 @@ namespace {
 #ifndef HS_FUSED_UNROLL
 #define HS_FUSED_UNROLL _Pragma("unroll")
 #endif
-constexpr int kBX = 32, kBY = 16;              // tile (fastest axis x rows)
+#ifndef HS_FUSED_BX
+#define HS_FUSED_BX 32
+#endif
+#ifndef HS_FUSED_BY
+#define HS_FUSED_BY 16
+#endif
+constexpr int kBX = HS_FUSED_BX, kBY = HS_FUSED_BY;   // tile (fastest axis x rows)
 constexpr int kR2X = kBX + 4, kR2Y = kBY + 4;  // tile + 2-point ring
 constexpr int kR1X = kBX + 2, kR1Y = kBY + 2;  // tile + 1-point ring
 
