@@ -3133,8 +3133,10 @@ int sweep_solve_one(Ctx* c, Sweep* s, int j, int64_t a, int64_t b, int64_t ta, i
   return HS_OK;
 }
 
-int sweep_work_create(Ctx* c, const Sweep* s, SweepWork* w, int nrhs) {
-  if (s->s3) return set_error(c, HS_E_ARG, "sweep lanes need a 2-D level (the 3-D solve uses every SM)");
+int sweep_work_create(Ctx* c, const Sweep* s, SweepWork* w, int nrhs, bool batch) {
+  // (3-D levels: a batch's work set only -- their solve uses every SM, so no lanes)
+  if (s->s3 && !batch)
+    return set_error(c, HS_E_ARG, "sweep lanes need a 2-D level (the 3-D solve uses every SM)");
   if (nrhs < 1) return set_error(c, HS_E_ARG, "a work set holds at least one right-hand side");
   *w = SweepWork{};
   w->nrhs = nrhs;
@@ -3175,13 +3177,13 @@ int sweep_apply_many(Ctx* c, Sweep* s, int variant, int nrhs, const double2* f, 
   if (nrhs < 1) return set_error(c, HS_E_ARG, "nrhs must be at least 1");
   if (nrhs > 1 && stride < (int64_t)s->n0 * s->M)
     return set_error(c, HS_E_ARG, "right-hand-side stride shorter than a vector");
-  int width = s->s3 || s->cpl0 ? 1 : s->max_nr;
+  int width = s->cpl0 ? 1 : s->max_nr;
   if (w) {   // a lane's work set: as wide as it was created
     width = std::min(width, w->nrhs);
   } else if (width > 1 && nrhs > 1) {
     if (s->batch.nrhs < width || !s->batch.trace) {
       if (s->batch.trace) sweep_work_destroy(&s->batch);
-      if (int r = sweep_work_create(c, s, &s->batch, width)) return r;
+      if (int r = sweep_work_create(c, s, &s->batch, width, true)) return r;
     }
     w = &s->batch;
   }
@@ -3200,7 +3202,7 @@ int sweep_apply_many(Ctx* c, Sweep* s, int variant, int nrhs, const double2* f, 
 static int sweep_apply_nr(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
                           const SweepWork* w, int first, int last, int nr, int64_t stride) {
   if (!w) w = &s->own;
-  if (nr > 1 && (s->s3 || w->nrhs < nr || nr > s->max_nr || s->cpl0))
+  if (nr > 1 && (w->nrhs < nr || nr > s->max_nr || s->cpl0))
     return set_error(c, HS_E_ARG, "multi-right-hand-side sweep: unsupported level or work set");
   const int64_t nlev = (int64_t)s->n0 * s->M;   // stride of the work set's g / u2
   if (!s->has_plan(variant))
@@ -3234,8 +3236,9 @@ static int sweep_apply_nr(Ctx* c, Sweep* s, int variant, const double2* f, doubl
       case SweepLaunch::kSolve: {
         if (s->s3) {   // 3-D: the fronts' slab solves in order (host-driven block LU;
                        // sweep3_tasks attributes the GEMV and chain kernels itself)
-          if (w->g != s->g) return set_error(c, HS_E_ARG, "sweep lanes need a 2-D level");
-          double2* us[2] = {u, s->u2};
+          double2* us[2] = {u, w->u2};
+          Sweep3Rhs mr{nr, Lh.src ? nlev : stride, {stride, nlev},
+                       (int64_t)std::max(1, s->ntrace) * 2 * M, w->trace};
           // fronts zipped in pairs (two chains per launch); a task identical
           // to one already run in this launch (a solve heading two fronts)
           // is not repeated -- its outputs are already in place
@@ -3266,8 +3269,8 @@ static int sweep_apply_nr(Ctx* c, Sweep* s, int variant, const double2* f, doubl
               }
               for (int k = 0; k < nt; ++k) done.push_back(ts[k]);
               if (nt) {
-                const int r2 = sweep3_tasks(c, s, ts, nt, Lh.src ? s->g : f, us,
-                                            s->coarse->d.coeffs, s->coarse->d.n);
+                const int r2 = sweep3_tasks(c, s, ts, nt, Lh.src ? w->g : f, us,
+                                            s->coarse->d.coeffs, s->coarse->d.n, &mr);
                 if (r2) return r2;
               }
             }

@@ -117,7 +117,7 @@ int sweep_plan_nx(Ctx* c, Sweep* s, int ncell, const int64_t* j_cell, const int6
 int sweep_solve_one(Ctx* c, Sweep* s, int j, int64_t a, int64_t b, int64_t ta, int64_t tb,
                     const double2* B1, const double2* B3, double2* out2, double2* out4,
                     const double2* f, double2* u);
-int sweep_work_create(Ctx* c, const Sweep* s, SweepWork* w, int nrhs = 1);
+int sweep_work_create(Ctx* c, const Sweep* s, SweepWork* w, int nrhs = 1, bool batch = false);
 void sweep_work_destroy(SweepWork* w);
 
 // general sparse matrix rows (device CSR) for the exact solver's blocks
@@ -131,9 +131,17 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
                   const int64_t* lo, const int64_t* hi, const CsrSource* csr);
 int sweep3_task(Ctx* c, Sweep* s, const SweepTask& t, const double2* src, double2* const* u,
                 const double2* coarse_coeffs, int64_t coarse_n);
+// several right-hand sides through the 3-D chains: element strides between
+// the right-hand sides' vectors (src, the two u destinations, trace buffers)
+struct Sweep3Rhs {
+  int nr;
+  int64_t vs_src, vs_u[2], ts;
+  double2* trace;
+};
 // one or two independent slab solves (two sweep fronts) in one chain launch
 int sweep3_tasks(Ctx* c, Sweep* s, const SweepTask* const* ts, int nt, const double2* src,
-                 double2* const* u, const double2* coarse_coeffs, int64_t coarse_n);
+                 double2* const* u, const double2* coarse_coeffs, int64_t coarse_n,
+                 const Sweep3Rhs* mr = nullptr);
 void sweep3_destroy(Sweep3* s3);
 // Exact solver of a whole operator (ExactCoarseSolver / factorize,
 // twogrid.py:99-105, sparselin.py:40-68): the operator as ONE block-LU slab

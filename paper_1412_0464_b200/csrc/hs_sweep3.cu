@@ -39,8 +39,9 @@ struct Sweep3 {
   std::vector<double2*> coef;          // per slab: stencil coefficients [S][T n1 n2] (owned copy)
   std::vector<std::array<int, 27>> slot;   // per slab: (o0+1)*9 + (o1+1)*3 + (o2+1) -> slot
   std::array<int, 27> cslot{};         // coarse operator slots
-  double2* F[2] = {nullptr, nullptr};  // per concurrent chain: [n1][NBmax] right-hand side
-  double2* Y[2] = {nullptr, nullptr};  // [n1][NBmax] forward solution, then x
+  double2* F[2] = {nullptr, nullptr};  // per concurrent chain: [nrcap][n1][NBmax] right-hand side
+  double2* Y[2] = {nullptr, nullptr};  // [nrcap][n1][NBmax] forward solution, then x
+  int nrcap = 1;                       // right-hand sides F / Y hold (grown by sweep3_reserve)
   unsigned* gbar = nullptr;            // [2] grid barrier counters of the solve kernel
   int optin = 0;                       // opt-in shared memory per block
   int grid = 0;                        // CTAs of the solve kernel (one per SM)
@@ -103,12 +104,18 @@ __global__ void k3_csr_block(const int64_t* __restrict__ indptr, const int64_t* 
 
 
 // F[i1][t n2 + i2] = restriction rows of src + transmission terms (subdom_solve steps 1-2)
+// (blockIdx.y: the right-hand side; its vectors at src + y * vs_src, trace +
+// y * ts, F + y * fs)
 __global__ void k3_rhs(SweepTask t, int n0, int n1, int n2, const double2* __restrict__ src,
                        const double2* __restrict__ cco, int64_t cn, Slots cs,
-                       const double2* __restrict__ trace, double2* __restrict__ F) {
+                       const double2* __restrict__ trace, double2* __restrict__ F,
+                       int64_t vs_src, int64_t ts, int64_t fs) {
   const int NB = t.T * n2;
   const int64_t e = (int64_t)blockIdx.x * kT3 + threadIdx.x;
   if (e >= (int64_t)n1 * NB) return;
+  src += blockIdx.y * vs_src;
+  trace += blockIdx.y * ts;
+  F += blockIdx.y * fs;
   const int i1 = (int)(e / NB), r = (int)(e - (int64_t)i1 * NB);
   const int x = r / n2, i2 = r - x * n2;
   const int64_t M = (int64_t)n1 * n2;
@@ -144,15 +151,19 @@ __global__ void k3_rhs(SweepTask t, int n0, int n1, int n2, const double2* __res
 // plane's f is staged in shared memory.  HBM-bound: n1 NB^2 16 B per task.
 // Fixed reduction order (bitwise reproducible, the same sums as before).
 constexpr int kGvRows = 32;
+// NR right-hand sides (template): the plane's NR vectors f + q * fs are staged
+// together and every matrix element is loaded once for all of them; per
+// right-hand side the sums are the single kernel's (bitwise the same).
 struct GemvTask {
   const double2* Dinv;
   const double2* F;
   double2* Y;
   int NB, nrb;   // rows per plane, 32-row blocks per plane
 };
+template <int NR>
 __global__ void __launch_bounds__(256) k3_gemv(GemvTask t0, GemvTask t1, int n1, int64_t items0,
-                                              int64_t items) {
-  extern __shared__ __align__(16) double2 fv[];
+                                              int64_t items, int64_t fs) {
+  extern __shared__ __align__(16) double2 fv[];   // [NR][NB]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
     const bool second = it >= items0;
@@ -162,41 +173,71 @@ __global__ void __launch_bounds__(256) k3_gemv(GemvTask t0, GemvTask t1, int n1,
     const int NB = t.NB;
     const int64_t nb2 = (int64_t)NB * NB;
     __syncthreads();   // the previous item's readers of fv are done
-    const double2* f = t.F + (int64_t)i1 * NB;
-    for (int c = threadIdx.x; c < NB; c += blockDim.x) fv[c] = __ldg(f + c);
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const double2* f = t.F + q * fs + (int64_t)i1 * NB;
+      for (int c = threadIdx.x; c < NB; c += blockDim.x) fv[q * NB + c] = __ldg(f + c);
+    }
     __syncthreads();
     const int r0 = rb * kGvRows + warp * 4;
     const double2* A = t.Dinv + (int64_t)i1 * nb2;
-    double2 acc[4] = {czero(), czero(), czero(), czero()};
+    double2 acc[4][NR];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int q = 0; q < NR; ++q) acc[k][q] = czero();
     const int nr = max(0, min(4, NB - r0));
     if (nr == 4) {
       const double2* a0 = A + (int64_t)r0 * NB;
       for (int c = lane; c < NB; c += 32) {
-        const double2 v = fv[c];
-        acc[0] = cfma(__ldcs(a0 + c), v, acc[0]);
-        acc[1] = cfma(__ldcs(a0 + NB + c), v, acc[1]);
-        acc[2] = cfma(__ldcs(a0 + 2 * NB + c), v, acc[2]);
-        acc[3] = cfma(__ldcs(a0 + 3 * NB + c), v, acc[3]);
+        const double2 m0 = __ldcs(a0 + c), m1 = __ldcs(a0 + NB + c);
+        const double2 m2 = __ldcs(a0 + 2 * NB + c), m3 = __ldcs(a0 + 3 * NB + c);
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          const double2 v = fv[q * NB + c];
+          acc[0][q] = cfma(m0, v, acc[0][q]);
+          acc[1][q] = cfma(m1, v, acc[1][q]);
+          acc[2][q] = cfma(m2, v, acc[2][q]);
+          acc[3][q] = cfma(m3, v, acc[3][q]);
+        }
       }
     } else {
-      for (int k = 0; k < nr; ++k) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (k >= nr) break;
         const double2* ar = A + (int64_t)(r0 + k) * NB;
-        for (int c = lane; c < NB; c += 32) acc[k] = cfma(__ldcs(ar + c), fv[c], acc[k]);
+        for (int c = lane; c < NB; c += 32) {
+          const double2 m = __ldcs(ar + c);
+#pragma unroll
+          for (int q = 0; q < NR; ++q) acc[k][q] = cfma(m, fv[q * NB + c], acc[k][q]);
+        }
       }
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      for (int m = 16; m > 0; m >>= 1) acc[k] = cadd(acc[k], shfl_xor_c(acc[k], m));
-    if (lane < nr) t.Y[(int64_t)i1 * NB + r0 + lane] = acc[lane];
+    for (int q = 0; q < NR; ++q) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        for (int m = 16; m > 0; m >>= 1) acc[k][q] = cadd(acc[k][q], shfl_xor_c(acc[k][q], m));
+      // (lane k stores row k: pick it without a dynamically indexed register array)
+      double2 mine = acc[0][q];
+      if (lane == 1) mine = acc[1][q];
+      if (lane == 2) mine = acc[2][q];
+      if (lane == 3) mine = acc[3][q];
+      if (lane < nr) t.Y[q * fs + (int64_t)i1 * NB + r0 + lane] = mine;
+    }
   }
 }
 
 // u rows [ta, tb) and the outgoing traces (subdom_solve steps 4-5)
 __global__ void k3_out(SweepTask t, int n1, int n2, const double2* __restrict__ X,
-                       double2* __restrict__ u, double2* __restrict__ trace) {
+                       double2* __restrict__ u, double2* __restrict__ trace, int64_t fs,
+                       int64_t vs_u, int64_t ts) {
   const int NB = t.T * n2;
   const int64_t e = (int64_t)blockIdx.x * kT3 + threadIdx.x;
   if (e >= (int64_t)n1 * NB) return;
+  X += blockIdx.y * fs;
+  u += blockIdx.y * vs_u;
+  trace += blockIdx.y * ts;
   const int i1 = (int)(e / NB), r = (int)(e - (int64_t)i1 * NB);
   const int x = r / n2, i2 = r - x * n2;
   const int64_t M = (int64_t)n1 * n2, f = (int64_t)i1 * n2 + i2;
@@ -284,8 +325,11 @@ constexpr int kR3 = 16;  // rows per CTA at most (NB <= 16 * CTAs of the task)
 // column-segment variant -- each warp all rows of a slice of v -- measured
 // 12% slower at C5.)
 __device__ __forceinline__ int rows_wpr(int nrow) { return max(1, kW3 / max(1, nrow)); }
+// NR right-hand sides: vectors v + q * NB, sums acc + q * as; every staged
+// matrix element is read once for all of them.
+template <int NR>
 __device__ __forceinline__ void cta_rows(const double2* A, const double2* v, int NB, int nrow,
-                                         double2* acc) {
+                                         double2* acc, int as) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (nrow == 0 || (HS_S3_EXP & 1)) return;
   const int wpr = rows_wpr(nrow);               // warps per row
@@ -294,18 +338,32 @@ __device__ __forceinline__ void cta_rows(const double2* A, const double2* v, int
     const int part = warp % wpr;
     const int c0 = part * seg, c1 = min(NB, c0 + seg);
     const double2* row = A + (int64_t)k * NB;
-    double2 a0 = czero(), a1 = czero(), a2 = czero(), a3 = czero();
+    double2 a0[NR], a1[NR], a2[NR], a3[NR];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) a0[q] = a1[q] = a2[q] = a3[q] = czero();
     int c = c0 + lane;
     for (; c + 96 < c1; c += 128) {
-      a0 = cfma(row[c], v[c], a0);
-      a1 = cfma(row[c + 32], v[c + 32], a1);
-      a2 = cfma(row[c + 64], v[c + 64], a2);
-      a3 = cfma(row[c + 96], v[c + 96], a3);
+      const double2 m0 = row[c], m1 = row[c + 32], m2 = row[c + 64], m3 = row[c + 96];
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        const double2* vq = v + q * NB;
+        a0[q] = cfma(m0, vq[c], a0[q]);
+        a1[q] = cfma(m1, vq[c + 32], a1[q]);
+        a2[q] = cfma(m2, vq[c + 64], a2[q]);
+        a3[q] = cfma(m3, vq[c + 96], a3[q]);
+      }
     }
-    for (; c < c1; c += 32) a0 = cfma(row[c], v[c], a0);
-    double2 t = cadd(cadd(a0, a1), cadd(a2, a3));
-    for (int m = 16; m > 0; m >>= 1) t = cadd(t, shfl_xor_c(t, m));
-    if (lane == 0) acc[k * wpr + part] = t;
+    for (; c < c1; c += 32) {
+      const double2 m0 = row[c];
+#pragma unroll
+      for (int q = 0; q < NR; ++q) a0[q] = cfma(m0, v[q * NB + c], a0[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      double2 t = cadd(cadd(a0[q], a1[q]), cadd(a2[q], a3[q]));
+      for (int m = 16; m > 0; m >>= 1) t = cadd(t, shfl_xor_c(t, m));
+      if (lane == 0) acc[q * as + k * wpr + part] = t;
+    }
   }
 }
 
@@ -323,9 +381,12 @@ struct K3Chain {
   int nbuf;
 };
 
+// NR right-hand sides per chain (template): Y + q * fs; the staged rows are
+// shared, the step's vector and the partial sums hold NR copies.
+template <int NR>
 __global__ void __launch_bounds__(kW3 * 32, 1)
-k3_solve(K3Chain c0, K3Chain c1, int g0, int n1, int n2) {
-  extern __shared__ __align__(128) double2 v3[];   // [NB] vector | [nbuf][rmax][NB] rows | sums
+k3_solve(K3Chain c0, K3Chain c1, int g0, int n1, int n2, int64_t fs) {
+  extern __shared__ __align__(128) double2 v3[];   // [NR][NB] vectors | [nbuf][rmax][NB] rows | sums
   const bool second = (int)blockIdx.x >= g0;
   const K3Chain& ch = second ? c1 : c0;
   const int lb = second ? (int)blockIdx.x - g0 : (int)blockIdx.x;   // CTA within the chain
@@ -339,13 +400,14 @@ k3_solve(K3Chain c0, K3Chain c1, int g0, int n1, int n2) {
   const int64_t nb2 = (int64_t)NB * NB;
   const int nrow = lb < NB ? (NB - 1 - lb) / G + 1 : 0;
   const int rmax = (NB + G - 1) / G;
-  double2* rows = v3 + NB;                          // nbuf (1 or 2) staging buffers
-  double2* racc = rows + nbuf * (int64_t)rmax * NB; // [rows][warps per row] partial row sums
-  uint64_t* rbar = (uint64_t*)(racc + rmax * kW3);  // [2] staging barriers
+  double2* rows = v3 + NR * NB;                     // nbuf (1 or 2) staging buffers
+  double2* racc = rows + nbuf * (int64_t)rmax * NB; // [NR][rows][warps per row] partial row sums
+  uint64_t* rbar = (uint64_t*)(racc + NR * rmax * kW3);  // [2] staging barriers
   const int wpr = rows_wpr(nrow);
-  auto row_sum = [&](int k) {
+  const int as = rmax * kW3;
+  auto row_sum = [&](int q, int k) {
     double2 a = czero();
-    for (int p = 0; p < wpr; ++p) a = cadd(a, racc[k * wpr + p]);
+    for (int p = 0; p < wpr; ++p) a = cadd(a, racc[q * as + k * wpr + p]);
     return a;
   };
   // step s: forward plane i = s + 1 (y_i = w_i - G_i y_{i-1}, Y_i holds w_i), then
@@ -369,27 +431,32 @@ k3_solve(K3Chain c0, K3Chain c1, int g0, int n1, int n2) {
     double2* Yi = Y + (int64_t)i1 * NB;
     const double2* Yin = fwd ? Yi - NB : Yi + NB;
     if (st > 0) barrier_wait(bar, (unsigned)st * G);
-    if (!(HS_S3_EXP & 2))
-      for (int r = threadIdx.x; r < NB; r += blockDim.x) v3[r] = __ldcg(Yin + r);
+    if (!(HS_S3_EXP & 2)) {
+#pragma unroll
+      for (int q = 0; q < NR; ++q)
+        for (int r = threadIdx.x; r < NB; r += blockDim.x) v3[q * NB + r] = __ldcg(Yin + q * fs + r);
+    }
     __syncthreads();
     const int b = nbuf == 2 ? (st & 1) : 0;
     double2* buf = rows + (int64_t)b * rmax * NB;
     if (nrow > 0) s3_mbar_wait(rbar + b, (uint32_t)(st / nbuf) & 1);
-    cta_rows(buf, v3, NB, nrow, racc);
+    cta_rows<NR>(buf, v3, NB, nrow, racc, as);
     __syncthreads();   // this buffer is consumed: stage the step after next into it
     if (threadIdx.x == 0 && nrow > 0 && st + nbuf < nsteps)
       stage_rows(mat(st + nbuf), NB, nrow, buf, rbar + b, lb, G);
-    for (int k = threadIdx.x; k < nrow; k += blockDim.x) {
+    for (int kk = threadIdx.x; kk < NR * nrow; kk += blockDim.x) {
+      const int q = NR == 1 ? 0 : kk / nrow, k = kk - q * nrow;
       const int r = lb + k * G;
-      Yi[r] = csub(__ldcg(Yi + r), row_sum(k));
+      Yi[q * fs + r] = csub(__ldcg(Yi + q * fs + r), row_sum(q, k));
     }
     barrier_arrive(bar);
   }
 }
 
-size_t k3_smem(int NB, int grid, int nbuf) {
+size_t k3_smem(int NB, int grid, int nbuf, int nr = 1) {
   const int rmax = (NB + grid - 1) / grid;
-  return (size_t)(NB + nbuf * (size_t)rmax * NB + (size_t)rmax * kW3) * sizeof(double2) + 16;
+  return (size_t)((size_t)nr * NB + nbuf * (size_t)rmax * NB + (size_t)nr * rmax * kW3) *
+             sizeof(double2) + 16;
 }
 
 Slots to_slots(const std::array<int, 27>& a) {
@@ -598,10 +665,26 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
       // staged rows double-buffered when two planes' rows fit shared memory
     s3->nbuf = k3_smem(NBmax, s3->grid, 2) <= (size_t)optin ? 2 : 1;
     s3->optin = optin;
-    S3_TRY(cudaFuncSetAttribute(k3_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, optin), "attr");
+    S3_TRY(cudaFuncSetAttribute(k3_solve<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin), "attr");
+    S3_TRY(cudaFuncSetAttribute(k3_solve<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin), "attr");
+    S3_TRY(cudaFuncSetAttribute(k3_solve<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin), "attr");
+    S3_TRY(cudaFuncSetAttribute(k3_gemv<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin), "attr");
+    S3_TRY(cudaFuncSetAttribute(k3_gemv<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin), "attr");
     int per = 0;
-    S3_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k3_solve, kW3 * 32, optin), "occ");
+    S3_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k3_solve<1>, kW3 * 32, optin), "occ");
     if (per < 1) return done(set_error(c, HS_E_CUDA, "3-D solve kernel does not fit an SM"));
+    // widest chain kernel (right-hand sides per chain): its vectors and sums
+    // must fit beside one staging buffer, co-resident on every SM
+    s->max_nr = 1;
+    for (int w : {2, 4}) {
+      int pw = 0;
+      const bool fits = k3_smem(NBmax, s3->grid, 1, w) <= (size_t)optin;
+      if (!fits) break;
+      cudaError_t e = w == 2 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pw, k3_solve<2>, kW3 * 32, optin)
+                             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pw, k3_solve<4>, kW3 * 32, optin);
+      if (e != cudaSuccess || pw < 1) { cudaGetLastError(); break; }
+      s->max_nr = w;
+    }
   }
   return done(HS_OK);
 }
@@ -611,11 +694,40 @@ int sweep3_create(Ctx* c, Sweep* s, const Stencil* coarse, const Stencil* const*
 // sides, the batched w = Dinv f GEMVs, then ONE cooperative chain launch --
 // two chains on disjoint CTA groups when both fit the group's shared memory
 // (CTAs split by NB^2, the per-step bytes) -- and the outputs.
+// F / Y of both chains for nr right-hand sides (grown on demand)
+static int sweep3_reserve(Ctx* c, Sweep3* s3, int nr) {
+  if (nr <= s3->nrcap) return HS_OK;
+  S3_TRY(cudaStreamSynchronize(c->stream), "sync");
+  const size_t bytes = (size_t)nr * s3->n1 * s3->nbmax * sizeof(double2);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(s3->F[i]);
+    cudaFree(s3->Y[i]);
+    s3->F[i] = s3->Y[i] = nullptr;
+  }
+  s3->nrcap = 0;
+  for (int i = 0; i < 2; ++i) {
+    S3_TRY(cudaMalloc((void**)&s3->F[i], bytes), "3-D right-hand sides");
+    S3_TRY(cudaMalloc((void**)&s3->Y[i], bytes), "3-D solutions");
+  }
+  s3->nrcap = nr;
+  return HS_OK;
+}
+
 int sweep3_tasks(Ctx* c, Sweep* s, const SweepTask* const* ts, int nt, const double2* src,
-                 double2* const* u, const double2* coarse_coeffs, int64_t coarse_n) {
+                 double2* const* u, const double2* coarse_coeffs, int64_t coarse_n,
+                 const Sweep3Rhs* mr) {
   Sweep3* s3 = s->s3;
   const int n1 = s3->n1, n2 = s3->n2;
   const int G = s3->grid;
+  // nr right-hand sides through the chains (1 unless mr): strides of src,
+  // of the two u destinations and of the trace buffers
+  const int nr = mr ? mr->nr : 1;
+  const int64_t vs_src = mr ? mr->vs_src : 0, ts_ = mr ? mr->ts : 0;
+  const int64_t vs_u[2] = {mr ? mr->vs_u[0] : 0, mr ? mr->vs_u[1] : 0};
+  double2* trace = mr ? mr->trace : s->trace;
+  const int64_t fs = (int64_t)n1 * s3->nbmax;   // F / Y stride between right-hand sides
+  if (nr != 1 && nr != 2 && nr != 4) return set_error(c, HS_E_ARG, "3-D chains carry 1, 2 or 4 right-hand sides");
+  if (int r = sweep3_reserve(c, s3, nr)) return r;
   int NB[2] = {0, 0}, g0 = G, nbuf[2] = {1, 1};
   for (int k = 0; k < nt; ++k) NB[k] = s3->T[ts[k]->slab] * n2;
   if (nt == 2) {   // CTA split by per-step bytes; both groups must fit
@@ -624,16 +736,17 @@ int sweep3_tasks(Ctx* c, Sweep* s, const SweepTask* const* ts, int nt, const dou
     bool ok = true;
     for (int k = 0; k < 2; ++k) {
       const int gk = k ? G - g0 : g0;
-      nbuf[k] = k3_smem(NB[k], gk, 2) <= (size_t)s3->optin ? 2 : 1;
-      ok = ok && (NB[k] + gk - 1) / gk <= kR3 && k3_smem(NB[k], gk, nbuf[k]) <= (size_t)s3->optin;
+      nbuf[k] = k3_smem(NB[k], gk, 2, nr) <= (size_t)s3->optin ? 2 : 1;
+      ok = ok && (NB[k] + gk - 1) / gk <= kR3 &&
+           k3_smem(NB[k], gk, nbuf[k], nr) <= (size_t)s3->optin;
     }
     if (!ok) {   // one chain at a time
       for (int k = 0; k < 2; ++k)
-        if (int r = sweep3_tasks(c, s, ts + k, 1, src, u, coarse_coeffs, coarse_n)) return r;
+        if (int r = sweep3_tasks(c, s, ts + k, 1, src, u, coarse_coeffs, coarse_n, mr)) return r;
       return HS_OK;
     }
   } else {
-    nbuf[0] = s3->nbuf;
+    nbuf[0] = k3_smem(NB[0], G, 2, nr) <= (size_t)s3->optin ? std::min(2, std::max(1, s3->nbuf)) : 1;
   }
   size_t smem = 0;
   K3Chain ch[2] = {};
@@ -644,13 +757,14 @@ int sweep3_tasks(Ctx* c, Sweep* s, const SweepTask* const* ts, int nt, const dou
     const int j = t.slab, nb = NB[k];
     const size_t nb2 = (size_t)nb * nb;
     const int64_t tot = (int64_t)n1 * nb;
-    k3_rhs<<<(unsigned)((tot + kT3 - 1) / kT3), kT3, 0, c->stream>>>(
-        t, s->n0, n1, n2, src, coarse_coeffs, coarse_n, to_slots(s3->cslot), s->trace, s3->F[k]);
+    k3_rhs<<<dim3((unsigned)((tot + kT3 - 1) / kT3), nr), kT3, 0, c->stream>>>(
+        t, s->n0, n1, n2, src, coarse_coeffs, coarse_n, to_slots(s3->cslot), trace, s3->F[k],
+        vs_src, ts_, fs);
     HS_LAUNCH_CHECK(c, "3-D rhs");
     gv[k] = GemvTask{s3->dinv[j], s3->F[k], s3->Y[k], nb, (nb + kGvRows - 1) / kGvRows};
     gemv_bytes += (double)n1 * nb2 * 16.0;
     ch[k] = K3Chain{s3->T[j], s3->gf[j], s3->xf[j], s3->Y[k], s3->gbar + k, nbuf[k]};
-    smem = std::max(smem, k3_smem(nb, nt == 2 ? (k ? G - g0 : g0) : G, nbuf[k]));
+    smem = std::max(smem, k3_smem(nb, nt == 2 ? (k ? G - g0 : g0) : G, nbuf[k], nr));
   }
   if (nt == 1) ch[1] = ch[0];
   {   // w_i = Dinv_i f_i for every plane of both tasks: one persistent GEMV launch
@@ -661,14 +775,24 @@ int sweep3_tasks(Ctx* c, Sweep* s, const SweepTask* const* ts, int nt, const dou
     const int nbm = std::max(gv[0].NB, gv[1].NB);
     if (!s3->gemv_grid) {   // resident CTAs of the GEMV at the largest plane
       int per = 0;
-      S3_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k3_gemv, 256,
+      S3_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k3_gemv<1>, 256,
                                                            (size_t)s3->nbmax * sizeof(double2)),
              "gemv occupancy");
       s3->gemv_grid = std::max(1, per) * c->num_sms;
     }
-    const unsigned grid = (unsigned)std::min<int64_t>(items, s3->gemv_grid);
-    k3_gemv<<<grid, 256, (size_t)nbm * sizeof(double2), c->stream>>>(gv[0], gv[1], n1, items0,
-                                                                      items);
+    int ggrid = s3->gemv_grid;
+    const size_t gsm = (size_t)nr * nbm * sizeof(double2);
+    if (nr > 1) {   // (wider kernels: their own residency)
+      int per = 0;
+      S3_TRY(nr == 2 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k3_gemv<2>, 256, gsm)
+                     : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k3_gemv<4>, 256, gsm),
+             "gemv occupancy");
+      ggrid = std::max(1, per) * c->num_sms;
+    }
+    const unsigned grid = (unsigned)std::min<int64_t>(items, ggrid);
+    if (nr == 1) k3_gemv<1><<<grid, 256, gsm, c->stream>>>(gv[0], gv[1], n1, items0, items, fs);
+    else if (nr == 2) k3_gemv<2><<<grid, 256, gsm, c->stream>>>(gv[0], gv[1], n1, items0, items, fs);
+    else k3_gemv<4><<<grid, 256, gsm, c->stream>>>(gv[0], gv[1], n1, items0, items, fs);
     HS_LAUNCH_CHECK(c, "3-D batched GEMV");
   }
   // profiler: the chain kernel (and the output scatter) as sweep_front, with
@@ -680,17 +804,19 @@ int sweep3_tasks(Ctx* c, Sweep* s, const SweepTask* const* ts, int nt, const dou
   {   // the chains: one cooperative launch
     S3_TRY(cudaMemsetAsync(s3->gbar, 0, 2 * sizeof(unsigned), c->stream), "memset");
     int g0_ = g0, n1_ = n1, n2_ = n2;
-    void* args[] = {(void*)&ch[0], (void*)&ch[1], (void*)&g0_, (void*)&n1_, (void*)&n2_};
-    S3_TRY(cudaLaunchCooperativeKernel((const void*)k3_solve, dim3(G), dim3(kW3 * 32), args, smem,
-                                       c->stream),
+    int64_t fs_ = fs;
+    void* args[] = {(void*)&ch[0], (void*)&ch[1], (void*)&g0_, (void*)&n1_, (void*)&n2_, (void*)&fs_};
+    const void* kern = nr == 1 ? (const void*)k3_solve<1> : nr == 2 ? (const void*)k3_solve<2>
+                                                                   : (const void*)k3_solve<4>;
+    S3_TRY(cudaLaunchCooperativeKernel(kern, dim3(G), dim3(kW3 * 32), args, smem, c->stream),
            "3-D solve launch");
     HS_LAUNCH_CHECK(c, "3-D solve kernel");
   }
   for (int k = 0; k < nt; ++k) {
     const SweepTask& t = *ts[k];
     const int64_t tot = (int64_t)n1 * NB[k];
-    k3_out<<<(unsigned)((tot + kT3 - 1) / kT3), kT3, 0, c->stream>>>(t, n1, n2, s3->Y[k],
-                                                                     u[t.dst], s->trace);
+    k3_out<<<dim3((unsigned)((tot + kT3 - 1) / kT3), nr), kT3, 0, c->stream>>>(
+        t, n1, n2, s3->Y[k], u[t.dst], trace, fs, vs_u[t.dst], ts_);
     HS_LAUNCH_CHECK(c, "3-D outputs");
   }
   return HS_OK;
@@ -699,7 +825,7 @@ int sweep3_tasks(Ctx* c, Sweep* s, const SweepTask* const* ts, int nt, const dou
 int sweep3_task(Ctx* c, Sweep* s, const SweepTask& t, const double2* src, double2* const* u,
                 const double2* coarse_coeffs, int64_t coarse_n) {
   const SweepTask* ts[1] = {&t};
-  return sweep3_tasks(c, s, ts, 1, src, u, coarse_coeffs, coarse_n);
+  return sweep3_tasks(c, s, ts, 1, src, u, coarse_coeffs, coarse_n, nullptr);
 }
 
 // ---------------------------------------------------------------------------

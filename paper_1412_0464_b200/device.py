@@ -365,6 +365,19 @@ class DeviceExactCSR(_Handle):
         self.ctx.call("hs_sweep_apply", self.h, _lib.HS_VARIANT_UD, ptr(ft), ptr(u))
         return (u[:self.n] if self.n_pad != self.n else u), was_np
 
+    def apply_many(self, F):
+        """Rows of the device tensor F (k x n) solved through
+        hs_sweep_apply_many (groups of right-hand sides per block chain);
+        returns a (k x n) device tensor."""
+        torch = _torch()
+        k = int(F.shape[0])
+        fp = torch.zeros((k, self.n_pad), dtype=torch.complex128, device=F.device)
+        fp[:, :self.n] = F
+        u = torch.empty_like(fp)
+        self.ctx.call("hs_sweep_apply_many", self.h, _lib.HS_VARIANT_UD, k, ptr(fp), ptr(u),
+                      self.n_pad)
+        return u[:, :self.n]
+
 
 class DeviceExact(_Handle):
     """Exact solver of a whole stencil operator (hs_exact_create): one block-LU
@@ -393,6 +406,19 @@ class DeviceExact(_Handle):
         u = empty(self.n, self.ctx)
         self.ctx.call("hs_sweep_apply", self.h, _lib.HS_VARIANT_UD, ptr(ft), ptr(u))
         return u, was_np
+
+    def apply_many(self, F):
+        """Rows of the contiguous device tensor F (k x n) through
+        hs_sweep_apply_many; returns a (k x n) device tensor."""
+        torch = _torch()
+        k = int(F.shape[0])
+        F = F.contiguous()
+        u = torch.empty_like(F)
+        self.ctx.call("hs_sweep_apply_many", self.h, _lib.HS_VARIANT_UD, k, ptr(F), ptr(u), self.n)
+        return u
+
+    def rhs_width(self) -> int:
+        return int(self.ctx.lib.hs_sweep_rhs_width(self.h))
 
 
 class DeviceCycle(_Handle):

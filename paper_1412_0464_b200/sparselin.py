@@ -89,24 +89,31 @@ class Factorization:
                 raise ValueError(f"rhs has {rhs.shape[0]} rows, expected {self.n}")
             if rhs.dim() == 1:
                 return self.device.apply(rhs)[0]
-            return _stack([self.device.apply(rhs[:, j].contiguous())[0]
-                           for j in range(rhs.shape[1])])
+            return self._solve_columns(rhs)
         rhs = np.asarray(rhs, dtype=complex)
         if rhs.shape[0] != self.n:
             raise ValueError(f"rhs has {rhs.shape[0]} rows, expected {self.n}")
         if rhs.ndim == 1:
             return self._solve1(rhs)
-        return np.column_stack([self._solve1(rhs[:, j]) for j in range(rhs.shape[1])])
+        import torch
+        from .device import from_device
+        dev = f"cuda:{self.device.ctx.device}"
+        x = self._solve_columns(torch.from_numpy(np.ascontiguousarray(rhs)).to(dev))
+        return from_device(x.contiguous(), True, tuple(rhs.shape))
+
+    def _solve_columns(self, rhs):
+        """(n, k) device tensor: the k columns as one multi-right-hand-side
+        solve (hs_sweep_apply_many: groups of columns per block chain, every
+        factor plane streamed once per group -- the reference's multi-column
+        SuperLU solve, sparselin.py:58-62); column j is bitwise solve(rhs[:, j])."""
+        import torch
+        x = self.device.apply_many(rhs.t().to(torch.complex128).contiguous())
+        return x.t().contiguous()
 
     def _solve1(self, b):
         from .device import from_device
         u, was_np = self.device.apply(np.ascontiguousarray(b))
         return from_device(u, True, (self.n,))
-
-
-def _stack(cols):
-    import torch
-    return torch.stack(cols, dim=1)
 
 
 def factorize(matrix) -> Factorization:
