@@ -319,12 +319,22 @@ __device__ __forceinline__ void stage_rows(const double2* __restrict__ A, int NB
 
 constexpr int kR3 = 16;  // rows per CTA at most (NB <= 16 * CTAs of the task)
 
-// rows k < nrow of (staged rows) x v: a row is split over wpr warps (4
-// independent partial sums per lane); partial sums land in acc[k][part],
-// summed in a fixed order by the caller: bitwise reproducible.  (A
-// column-segment variant -- each warp all rows of a slice of v -- measured
-// 12% slower at C5.)
-__device__ __forceinline__ int rows_wpr(int nrow) { return max(1, kW3 / max(1, nrow)); }
+// rows k < nrow of (staged rows) x v: (row, column segment) items go round
+// the warps (4 independent partial sums per lane); partial sums land in
+// acc[k][segment], summed in a fixed order by the caller: bitwise
+// reproducible.  (A column-slice variant -- each warp all rows of a slice of
+// v -- measured 12% slower at C5; 2 segments per row cost 0.7% over the
+// earlier rows-per-CTA-dependent split, 4 segments 3.5%, 8 segments 24%.)
+// Every row is cut into kSeg3 fixed column segments (boundaries depend on NB
+// only): (row, segment) items go round the warps, so a row's sum does not
+// depend on how many rows the CTA owns -- the same bits whether a chain runs
+// alone on every CTA or paired on a CTA group, for any number of
+// right-hand sides.
+#ifndef HS_S3_SEG
+#define HS_S3_SEG 2
+#endif
+constexpr int kSeg3 = HS_S3_SEG;
+static_assert(kSeg3 >= 1 && kSeg3 <= kW3, "partial sums: kW3 slots per row");
 // NR right-hand sides: vectors v + q * NB, sums acc + q * as; every staged
 // matrix element is read once for all of them.
 template <int NR>
@@ -332,10 +342,9 @@ __device__ __forceinline__ void cta_rows(const double2* A, const double2* v, int
                                          double2* acc, int as) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (nrow == 0 || (HS_S3_EXP & 1)) return;
-  const int wpr = rows_wpr(nrow);               // warps per row
-  const int seg = (NB + wpr - 1) / wpr;
-  for (int k = warp / wpr; k < nrow && warp / wpr < kW3 / wpr; k += kW3 / wpr) {
-    const int part = warp % wpr;
+  const int seg = (NB + kSeg3 - 1) / kSeg3;
+  for (int it = warp; it < nrow * kSeg3; it += kW3) {
+    const int k = it / kSeg3, part = it - k * kSeg3;
     const int c0 = part * seg, c1 = min(NB, c0 + seg);
     const double2* row = A + (int64_t)k * NB;
     double2 a0[NR], a1[NR], a2[NR], a3[NR];
@@ -362,7 +371,7 @@ __device__ __forceinline__ void cta_rows(const double2* A, const double2* v, int
     for (int q = 0; q < NR; ++q) {
       double2 t = cadd(cadd(a0[q], a1[q]), cadd(a2[q], a3[q]));
       for (int m = 16; m > 0; m >>= 1) t = cadd(t, shfl_xor_c(t, m));
-      if (lane == 0) acc[q * as + k * wpr + part] = t;
+      if (lane == 0) acc[q * as + k * kSeg3 + part] = t;
     }
   }
 }
@@ -403,11 +412,11 @@ k3_solve(K3Chain c0, K3Chain c1, int g0, int n1, int n2, int64_t fs) {
   double2* rows = v3 + NR * NB;                     // nbuf (1 or 2) staging buffers
   double2* racc = rows + nbuf * (int64_t)rmax * NB; // [NR][rows][warps per row] partial row sums
   uint64_t* rbar = (uint64_t*)(racc + NR * rmax * kW3);  // [2] staging barriers
-  const int wpr = rows_wpr(nrow);
   const int as = rmax * kW3;
   auto row_sum = [&](int q, int k) {
     double2 a = czero();
-    for (int p = 0; p < wpr; ++p) a = cadd(a, racc[q * as + k * wpr + p]);
+#pragma unroll
+    for (int p = 0; p < kSeg3; ++p) a = cadd(a, racc[q * as + k * kSeg3 + p]);
     return a;
   };
   // step s: forward plane i = s + 1 (y_i = w_i - G_i y_{i-1}, Y_i holds w_i), then
