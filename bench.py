@@ -452,8 +452,11 @@ def run_ours(args):
     ctx.profile_reset()
     ctx.profile(True)
     for _ in range(args.steps):
-        for fd in f_dev:
-            solve(fd)
+        if multi and args.batch:   # the batch's kernels (one group: the main context sees them all)
+            hb.solve_many(cycle, f_dev, cfg, lanes=1, batch=True)
+        else:
+            for fd in f_dev:
+                solve(fd)
     prof = ctx.profile_read() or {"none": {"ms": 0.0, "bytes": 0.0, "launches": 0}}
     ctx.profile(False)
     ms = reduce_over_ranks(ms_local, world, "max")

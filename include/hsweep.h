@@ -181,7 +181,8 @@ int hs_sweep_apply(hs_ctx* ctx, hs_sweep* s, int variant, const void* f, void* u
  * hs_sweep_rhs_width(s) right-hand sides (4, 2 or 1 by the face length) run
  * through ONE chain of slab solves, every factor block streamed once per
  * group; per right-hand side the result is bitwise hs_sweep_apply's.  3-D
- * levels apply one right-hand side after another. */
+ * levels and the exact solvers (hs_exact_create*) carry the group through
+ * their block chains the same way (multi-column Factorization.solve). */
 int hs_sweep_apply_many(hs_ctx* ctx, hs_sweep* s, int variant, int nrhs, const void* f, void* u,
                         long long stride);
 int hs_sweep_rhs_width(hs_sweep* s);

@@ -73,3 +73,18 @@ def test_bench_single_rank_identity():
     assert bench.reduce_over_ranks(3.5, 1) == 3.5
     assert bench.assign_rhs(1, 1, 0) == [0]
     assert bench.assign_rhs(4, 1, 0) == [0, 1, 2, 3]
+
+
+def test_lockstep_runs_and_bench_groups():
+    """Host logic of the lockstep multi-right-hand-side driver: consecutive
+    runs of the still-active right-hand sides (one hs_vcycle_many call per
+    run) and the bench's group / segment choice for multi-source configs."""
+    from paper_1412_0464_b200.krylov import _runs
+    assert _runs([]) == []
+    assert _runs([0, 1, 2, 3]) == [(0, 4)]
+    assert _runs([0, 2, 3, 6]) == [(0, 1), (2, 2), (6, 1)]
+    assert _runs([5]) == [(5, 1)]
+    # every index covered exactly once, in order
+    idx = [1, 2, 4, 5, 6, 9]
+    cover = [i for a, n in _runs(idx) for i in range(a, a + n)]
+    assert cover == idx

@@ -767,3 +767,22 @@ def test_many_rhs_3d_and_exact_bitwise():
     for j in range(3):
         assert np.array_equal(Xm[:, j], fm.solve(Bm[:, j])), j
     assert np.linalg.norm(m @ Xm - Bm) / np.linalg.norm(Bm) < 1e-10
+
+
+def test_sweep_many_argument_errors():
+    """hs_sweep_apply_many / hs_vcycle_many reject a non-positive count and a
+    stride shorter than a vector (ValueError, like the other shape errors)."""
+    import torch
+    from paper_1412_0464_b200.device import ptr
+    cycle = _build("pml2d")
+    sw = cycle.hierarchy.partition.device()
+    f = torch.zeros(2 * sw.n, dtype=torch.complex128, device="cuda")
+    u = torch.zeros_like(f)
+    with pytest.raises(ValueError):
+        sw.ctx.call("hs_sweep_apply_many", sw.h, 1, 0, ptr(f), ptr(u), sw.n)
+    with pytest.raises(ValueError, match="stride"):
+        sw.ctx.call("hs_sweep_apply_many", sw.h, 1, 2, ptr(f), ptr(u), sw.n - 1)
+    dev = cycle.device()
+    g = torch.zeros(2 * dev.n, dtype=torch.complex128, device="cuda")
+    with pytest.raises(ValueError, match="stride"):
+        dev.ctx.call("hs_vcycle_many", dev.h, 2, ptr(g), ptr(torch.zeros_like(g)), dev.n - 1)
