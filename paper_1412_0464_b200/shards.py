@@ -425,10 +425,11 @@ class ShardedTGSP:
             self.be.apply(g, x[g], out[g])
         return out
 
-    def op(self, v: dict, out: dict):
-        """out = A M v"""
-        self.vcycle(v, self._tmp)
-        return self.apply_a(self._tmp, out)
+    def op(self, v: dict, out: dict, z: dict | None = None):
+        """out = A M v; ``z`` keeps M v (the GMRES driver's z_k)"""
+        z = self._tmp if z is None else z
+        self.vcycle(v, z)
+        return self.apply_a(z, out)
 
     # -- reductions
     def _dots(self, V, k, w):
@@ -467,6 +468,9 @@ class ShardedTGSP:
         steps0 = config.max_iter if config.restart is None else min(config.restart,
                                                                      config.max_iter)
         V = {g: be.basis(g, steps0 + 1) for g in L}
+        # z_k = M v_k kept (as in krylov.gmres): a cycle ends with u += Z y
+        # instead of one more V-cycle on V y (M is linear and fixed)
+        Z = {g: be.basis(g, steps0) for g in L}
         history = [1.0]
         res = {g: f[g].clone() for g in L}
         res_norm = bnorm
@@ -475,10 +479,8 @@ class ShardedTGSP:
             steps = config.max_iter - (len(history) - 1)
             if config.restart is not None:
                 steps = min(steps, config.restart)
-            dv, converged = self._cycle(V, res, res_norm, bnorm, config.tol, steps, history)
-            if dv is not None:
-                mdv = {g: be.zeros(g) for g in L}
-                self.vcycle(dv, mdv)
+            mdv, converged = self._cycle(V, res, res_norm, bnorm, config.tol, steps, history, Z)
+            if mdv is not None:
                 for g in L:
                     be.axpby(g, 1.0, mdv[g], 1.0, u[g])
             # true residual between restarts
@@ -493,7 +495,7 @@ class ShardedTGSP:
         return u, SolveReport(len(history) - 1, hist, bool(hist[-1] <= config.tol),
                               time.perf_counter() - t0)
 
-    def _cycle(self, V, r0, beta, bnorm, tol, max_steps, history):
+    def _cycle(self, V, r0, beta, bnorm, tol, max_steps, history, Z):
         be, L = self.be, self.local
         hess = np.zeros((max_steps + 1, max_steps), dtype=complex)
         cs = np.zeros(max_steps, dtype=complex)
@@ -508,7 +510,7 @@ class ShardedTGSP:
         for k in range(max_steps):
             vk = {g: V[g][k] for g in L}
             w = {g: V[g][k + 1] for g in L}
-            self.op(vk, w)
+            self.op(vk, w, {g: Z[g][k] for g in L})
             h = self._dots(V, k + 1, w)
             hh = be.to_host(h[L[0]])
             hcol, w_norm0 = hh[:k + 1].copy(), hh[k + 1].real
@@ -541,7 +543,7 @@ class ShardedTGSP:
             return None, converged
         y = np.linalg.solve(hess[:k, :k], g_[:k])
         yd = be.from_host(y)
-        dv = {g: be.zeros(g) for g in L}
+        mdv = {g: be.zeros(g) for g in L}   # M dv = Z y
         for g in L:
-            be.lincomb(g, V[g], k, yd, dv[g])
-        return dv, converged
+            be.lincomb(g, Z[g], k, yd, mdv[g])
+        return mdv, converged
