@@ -530,7 +530,7 @@ int hs_sweep_apply_many(hs_ctx* c, hs_sweep* s, int variant, int nrhs, const voi
   return sweep_apply_many(c, s, variant, nrhs, (const double2*)f, (double2*)u, stride);
 }
 
-int hs_sweep_rhs_width(hs_sweep* s) { return s && !s->cpl0 ? s->max_nr : 1; }
+int hs_sweep_rhs_width(hs_sweep* s) { return s ? s->max_nr : 1; }
 int hs_sweep_max_fronts(hs_sweep* s) { return s && !s->s3 ? s->max_fronts : 0; }
 
 int hs_sweep_plan_nx(hs_ctx* c, hs_sweep* s, int ncell, const int64_t* j_cell,

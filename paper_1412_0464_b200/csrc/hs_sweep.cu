@@ -117,8 +117,8 @@ struct Chunks {
   int G;                   // segments (clusters) per front
   int q;                   // dense top: blocks per chunk left after L levels
   int nr;                  // restricted level-0 / spike updates (kNR rows) or 0
-  int cpl0;                // level-0 kept updates from the sparse stencil couplings
-                           // (SolveArgs::cpl) instead of streamed alpha / gamma blocks
+  int cpl0;                // level-0 kept updates from the sparse stencil couplings (one
+                           // streamed block of 6 tm values) instead of alpha / gamma blocks
   int koff[kMaxLevels];
   int y0s[kMaxCh + 1];     // chunk K covers face points [y0s[K], y0s[K+1])
   int mmax;                // longest chunk
@@ -189,7 +189,7 @@ k_cpl0(const SlabInfo* __restrict__ slabs, int M, double2* __restrict__ cpl) {
     double2 v = czero();
     if (sl >= 0 && r < si.T && r + o0 >= 0 && r + o0 < si.T && y + o1 >= 0 && y + o1 < M)
       v = si.coeffs[(int64_t)sl * n + (int64_t)r * M + y];
-    cpl[((int64_t)s * M + y) * 6 * TM + e] = v;
+    cpl[((int64_t)s * M + y) * TM * TM + e] = v;   // one (padded) block per face point
   }
 }
 
@@ -735,7 +735,7 @@ struct SolveArgs {
   int64_t nbs;
   const uint32_t* plan;    // [C][plan_words] item / chunk tables (chunk_plan)
   const int* rows;         // [J][kNR] rows of the restricted updates (g.nr != 0)
-  const double2* cpl;      // [J][M][2][3][TM] level-0 couplings (g.cpl0)
+  const double2* cpl;      // (unused: the level-0 couplings travel in the stream)
   const double2* src;      // right-hand side field (n0 x M)
   const double2* coarse;   // global coarse operator [S][n0*M] (transmission couplings)
   int64_t ncoarse;
@@ -955,7 +955,7 @@ __host__ __device__ inline int plan_yl(const ItemPlan& P, int p, int j) {
 // Factor arrays of one slab before packing (setup only).
 enum ItemArray : uint32_t {
   kArrEf = 0, kArrEb = 1, kArrKr = 2, kArrRk = 3, kArrSp = 4, kArrQd = 5, kArrEbr = 6, kArrSpr = 7,
-  kArrX2 = 8
+  kArrX2 = 8, kArrCpl = 9
 };
 constexpr uint32_t kOffMask = (1u << 28) - 1;
 __host__ __device__ constexpr uint32_t item_enc(uint32_t arr, int64_t off) {
@@ -987,8 +987,9 @@ __host__ __device__ inline int item_sources(const Chunks& g, int rank, const Ite
     if (p < P.L) {
       if ((yl >> l) & 1) {
         src[n++] = item_enc(kArrEf, y * TM2);
-      } else if (g.cpl0 && l == 0) {   // F -= L Yv[y-1] + U Yv[y+1]: couplings read directly
-        *hasx = false;
+      } else if (g.cpl0 && l == 0) {   // F -= L Yv[y-1] + U Yv[y+1]: the sparse couplings'
+        *hasx = false;                 // block (6 TM values) instead of alpha, gamma
+        src[n++] = item_enc(kArrCpl, y * TM2);
       } else {
         const int64_t k2 = ((int64_t)rank * g.kstride + g.koff[l] + (yl >> (l + 1))) * 2 * TM2;
         *hasx = yl - s >= 0;
@@ -1089,7 +1090,7 @@ __host__ __device__ inline void chunk_plan(const Chunks& g, int rank, int mmax, 
 }
 
 struct FactorArrays {
-  const double2 *ef, *eb, *kr, *rk, *sp, *qd, *ebr, *spr, *x2;
+  const double2 *ef, *eb, *kr, *rk, *sp, *qd, *ebr, *spr, *x2, *cpl;
 };
 
 // Restricted updates (setup): for the kNR rows R of each slab, one block per
@@ -1133,14 +1134,15 @@ __global__ void __launch_bounds__(256) k_pack(Chunks g, FactorArrays f, double2*
     });
   }
   __syncthreads();
-  const double2* base[9] = {
+  const double2* base[10] = {
       f.ef + (int64_t)slab * M * TM2,           f.eb + (int64_t)slab * M * 2 * TM2,
       f.kr + (int64_t)slab * C * g.kstride * 2 * TM2,
       f.rk + (int64_t)slab * C * (2 * (g.C - 1)) * 2 * TM2,
       f.sp + (int64_t)slab * M * 2 * TM2,       f.qd + (int64_t)slab * C * g.q * g.q * TM2,
       f.ebr ? f.ebr + (int64_t)slab * M * TM2 : nullptr,
       f.spr ? f.spr + (int64_t)slab * M * TM2 : nullptr,
-      f.x2 ? f.x2 + (int64_t)slab * C * g.xstride() * TM2 : nullptr};
+      f.x2 ? f.x2 + (int64_t)slab * C * g.xstride() * TM2 : nullptr,
+      f.cpl ? f.cpl + (int64_t)slab * M * TM2 : nullptr};
   double2* out = stream + ((int64_t)slab * C + k) * nbs * TM2;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   for (int r = warp; r < P.pfx[P.NP + 2]; r += 8) {
@@ -1652,9 +1654,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
                      : p > L        ? h.first + j * h.step
                                     : (j < h.ne ? 2 * j + 1 : 2 * (j - h.ne)) << p;
       const int r = h.pf0 + j;
-      // level-0 kept items with sparse couplings stream no blocks (no ring slot)
+      // level-0 kept items with sparse couplings: one block of 6 TM coupling values
       const bool sparse0 = g.cpl0 && p == 0 && !(yl & 1);
-      const Item it = has && !sparse0 ? acquire(ti, r) : Item{nullptr, nullptr};
+      const Item it = has ? acquire(ti, r) : Item{nullptr, nullptr};
       const double2* m0 = it.m0;
       const double2* m1 = it.m1;
       if (has) {
@@ -1675,10 +1677,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
 #pragma unroll
               for (int rh = 0; rh < NR; ++rh) Yv[rh * FS + yl * TM + x] = acc[rh];
             }
-          } else if (NR == 1 && sparse0) {  // kept, level 0: f -= L Yv[y-1] + U Yv[y+1]
+          } else if (sparse0) {  // kept, level 0: f -= L Yv[y-1] + U Yv[y+1]
             // (alpha f_{y-1} = L Dinv_{y-1} f_{y-1} = L Yv[y-1], Yv from this
             // phase's first half; L, U the slab stencil's thin-axis couplings)
-            const double2* cp = a.cpl + ((int64_t)slabs[ti] * M + (Y0 + yl)) * 6 * TM;
+            const double2* cp = m1;   // (hasx = false: the item's block)
+#pragma unroll
+            for (int rh = 0; rh < NR; ++rh) {
             double2 acc0 = czero();
 #pragma unroll
             for (int sd = 0; sd < 2; ++sd) {
@@ -1688,10 +1692,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
               for (int o0 = -1; o0 <= 1; ++o0) {
                 const int xx = x + o0;
                 if (xx < 0 || xx >= TM) continue;
-                acc0 = cfma(__ldg(cp + (sd * 3 + o0 + 1) * TM + x), Yv[q * TM + xx], acc0);
+                acc0 = cfma(cp[(sd * 3 + o0 + 1) * TM + x], Yv[rh * FS + q * TM + xx], acc0);
               }
             }
-            if (wr) F[yl * TM + x] = csub(F[yl * TM + x], acc0);
+            if (wr) F[rh * FS + yl * TM + x] = csub(F[rh * FS + yl * TM + x], acc0);
+            }
           } else {               // kept: f -= alpha f_{y-s} + gamma f_{y+s}
             const bool hl = yl - s >= 0, hr = yl + s < m;
             mvxn<TM, HW, NR>(hl ? m0 : nullptr, hl ? F + (yl - s) * TM : nullptr,
@@ -1720,7 +1725,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_part_solve(SolveArgs a) {
           }
         }
       }
-      release(it, has && !sparse0);
+      release(it, has);
     };
     // phase p over warps [w0, w0 + nw)
     auto run_phase = [&](int p, int w0, int nw) {
@@ -2248,7 +2253,8 @@ int factorize(Ctx* c, Sweep* s, const std::vector<SlabInfo>& info, const Chunks&
   HS_TRYF(cudaMalloc((void**)&s->stream, (size_t)J * NCH * nbs * TM2 * sizeof(double2)),
           "stream alloc");
   k_pack<TM><<<J * NCH, 256, 0, c->stream>>>(
-      g, FactorArrays{s->ef, s->eb, s->kr, s->rk, s->sp, s->qd, s->ebr, s->spr, s->x2}, s->stream,
+      g, FactorArrays{s->ef, s->eb, s->kr, s->rk, s->sp, s->qd, s->ebr, s->spr, s->x2, s->cpl},
+      s->stream,
       (int)nbs);
   c->launches++;
   HS_TRYF(cudaGetLastError(), "pack");
@@ -2257,7 +2263,8 @@ int factorize(Ctx* c, Sweep* s, const std::vector<SlabInfo>& info, const Chunks&
   HS_TRYF(cudaStreamSynchronize(c->stream), "factor sync");
 #undef HS_TRYF
   cleanup();
-  for (double2** p : {&s->ef, &s->eb, &s->kr, &s->sp, &s->rk, &s->qd, &s->ebr, &s->spr, &s->x2}) {
+  for (double2** p : {&s->ef, &s->eb, &s->kr, &s->sp, &s->rk, &s->qd, &s->ebr, &s->spr, &s->x2,
+                      &s->cpl}) {
     cudaFree(*p);
     *p = nullptr;
   }
@@ -2793,7 +2800,7 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
     for (int k = 0; k < NCH; ++k)
       rec_blocks += TM == 16 ? stream_blocks<16>(g, k) : stream_blocks<32>(g, k);
     // + the level-0 couplings read once per kept point (g.cpl0)
-    const double rec_bytes = rec_blocks * TM2 * 16.0 + (s->cpl0 ? (double)M / 2.0 * 6 * TM * 16.0 : 0.0);
+    const double rec_bytes = rec_blocks * TM2 * 16.0;
     s->rec_bytes = rec_bytes;
     for (auto& plan : s->plan) plan_bytes(s, plan);
   }
@@ -2804,8 +2811,9 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   const size_t qdb = (size_t)J * NCH * s->q * s->q * TM2 * sizeof(double2);
   s->factor_bytes = (long long)(efb * 5 + krb + qdb + (B > 0 ? rkb : 0));
   if (s->cpl0) {   // level-0 couplings: 6 TM values per face point and slab
-    const size_t cb = (size_t)J * M * 6 * TM * sizeof(double2);
+    const size_t cb = (size_t)J * M * TM2 * sizeof(double2);   // (packing only)
     e = cudaMalloc((void**)&s->cpl, cb);
+    if (e == cudaSuccess) e = cudaMemset(s->cpl, 0, cb);
     if (e != cudaSuccess) {
       sweep_destroy(s);
       return check_cuda(c, e, "coupling alloc");
@@ -3177,7 +3185,7 @@ int sweep_apply_many(Ctx* c, Sweep* s, int variant, int nrhs, const double2* f, 
   if (nrhs < 1) return set_error(c, HS_E_ARG, "nrhs must be at least 1");
   if (nrhs > 1 && stride < (int64_t)s->n0 * s->M)
     return set_error(c, HS_E_ARG, "right-hand-side stride shorter than a vector");
-  int width = s->cpl0 ? 1 : s->max_nr;
+  int width = s->max_nr;
   if (w) {   // a lane's work set: as wide as it was created
     width = std::min(width, w->nrhs);
   } else if (width > 1 && nrhs > 1) {
@@ -3202,7 +3210,7 @@ int sweep_apply_many(Ctx* c, Sweep* s, int variant, int nrhs, const double2* f, 
 static int sweep_apply_nr(Ctx* c, Sweep* s, int variant, const double2* f, double2* u,
                           const SweepWork* w, int first, int last, int nr, int64_t stride) {
   if (!w) w = &s->own;
-  if (nr > 1 && (w->nrhs < nr || nr > s->max_nr || s->cpl0))
+  if (nr > 1 && (w->nrhs < nr || nr > s->max_nr))
     return set_error(c, HS_E_ARG, "multi-right-hand-side sweep: unsupported level or work set");
   const int64_t nlev = (int64_t)s->n0 * s->M;   // stride of the work set's g / u2
   if (!s->has_plan(variant))
