@@ -555,7 +555,11 @@ def run_ours(args):
             # bytes_per_launch above = SURVEY 8(d)'s banded-LU floor of the
             # launch's slab solves; the own factor format streams factor_bytes
             # per pass (each slab solved twice per X application)
-            roofline["bytes_basis"] = "SURVEY 8(d) banded no-pivot LU floor of the slabs solved"
+            roofline["bytes_basis"] = (
+                "SURVEY 8(d) banded no-pivot LU floor of the slabs solved"
+                + (" x the right-hand sides a launch carries (each is one solve of every slab; "
+                   "the factor blocks themselves are read once per launch)"
+                   if multi and args.batch else ""))
             roofline["own_format_bytes_per_application"] = 2 * fac
             roofline["launches_per_application"] = dev.sweep.launches_per_apply()
         line = {

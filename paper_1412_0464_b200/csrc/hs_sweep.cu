@@ -3321,7 +3321,9 @@ static int sweep_apply_nr(Ctx* c, Sweep* s, int variant, const double2* f, doubl
           cudaMemsetAsync(dbg, 0, 16 * 1024 * sizeof(unsigned long long), c->stream);
         }
         a.dbg = dbg;
-        ProfScope ps(c, K_SWEEP_FRONT, Lh.bytes);
+        // (profiler: SURVEY 8(d)'s bytes per slab solve x the slab solves of the
+        // launch -- nr right-hand sides are nr solves of every slab)
+        ProfScope ps(c, K_SWEEP_FRONT, Lh.bytes * nr);
         cudaError_t e = launch_solve(s->tm, nr, s->C, Lh.nfront * s->G, s->mmax, c->stream, a);
         if (e != cudaSuccess) return check_cuda(c, e, "sweep solve launch");
         for (int i = 0; i < Lh.nfront; ++i)   // level-2 counters advance by the fronts' tasks
