@@ -786,3 +786,23 @@ def test_sweep_many_argument_errors():
     g = torch.zeros(2 * dev.n, dtype=torch.complex128, device="cuda")
     with pytest.raises(ValueError, match="stride"):
         dev.ctx.call("hs_vcycle_many", dev.h, 2, ptr(g), ptr(torch.zeros_like(g)), dev.n - 1)
+
+
+def test_gmres_many_on_3d_and_exact_cycles():
+    """Lockstep solves on a 3-D cycle and on a cycle with the exact coarse
+    solve (their preconditioner batches go through the 3-D block chains):
+    bitwise the sequential solves."""
+    import paper_1412_0464_b200 as hb
+    for name, coarse in (("pml3d_s", "sweep"), ("pml2d", "exact")):
+        mesh, model, fine_op, sm, sw = case(name)
+        cycle, _ = hb.build_two_grid(mesh, model, fine_op=fine_op, smoother=sm, coarse=coarse,
+                                     sweep=sw)
+        rng = np.random.default_rng(4)
+        rhs = [crand(rng, mesh.unknowns).ravel() for _ in range(3)]
+        cfg = hb.GmresConfig(1e-6, 60, 10)
+        seq = [hb.gmres(cycle.fine_csr, cycle.as_preconditioner(), f, cfg) for f in rhs]
+        par = hb.gmres_many(cycle.fine_csr, cycle.as_preconditioner(), rhs, cfg)
+        for (u0, r0), (u1, r1) in zip(seq, par):
+            assert r1.iterations == r0.iterations, name
+            assert np.array_equal(r1.residual_history, r0.residual_history), name
+            assert np.array_equal(u1, u0), name
