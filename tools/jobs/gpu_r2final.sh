@@ -23,3 +23,5 @@ timeout 600 python tools/time_many.py 3 1 4 > $O/many_c4_plain.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_part_solve -s 33 -c 3 \
     -o $O/prof_sweep_c4_nr4 -f python tools/time_many.py 3 1 4 > $O/ncu_nr4_fin.log 2>&1; echo "ncu nr4 rc=$?" >> $O/rc_fin.txt
 echo done >> $O/rc_fin.txt
+timeout 1200 bash tools/run_reference_tests.sh run > $O/reftests_fin.log 2>&1; echo "reftests rc=$?" >> $O/rc_fin.txt
+echo done2 >> $O/rc_fin.txt
