@@ -414,7 +414,10 @@ def run_ours(args):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    launches0 = ctx.launches
+    def all_launches():   # this context plus the lanes' (lanes / batch groups launch on their own)
+        return ctx.launches + sum(ln.ctx.launches for ln in getattr(cycle, "_lanes", []))
+
+    launches0 = None      # taken after the (lane-creating) warm-up below
     multi = len(f_dev) > 1 and (args.lanes > 1 or args.batch)
 
     def step(fs):
@@ -427,6 +430,7 @@ def run_ours(args):
         for _ in range(args.warmup):
             held = step(f_dev)
         held = None
+    launches0 = all_launches()
     with ClockSampler(local, args.clock_sampler) as clk:
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         # ncu --profile-from-start off captures exactly the timed region
@@ -441,7 +445,7 @@ def run_ours(args):
         ev1.record(stream)
         torch.cuda.synchronize()
         torch.cuda.cudart().cudaProfilerStop()
-    launches = ctx.launches - launches0
+    launches = all_launches() - launches0
     if world > 1:
         torch.distributed.barrier()
     ms_local = ev0.elapsed_time(ev1)

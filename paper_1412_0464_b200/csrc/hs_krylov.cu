@@ -222,7 +222,9 @@ int krylov_block_dot(Ctx* c, const double2* V, int64_t ldv, int k, const double2
   const int nb = grid_for(c, n);
   double2* part = (double2*)scratch(c, (size_t)nb * (k + 1) * sizeof(double2), 2);
   if (!part) return set_error(c, HS_E_CUDA, "scratch allocation failed");
-  ProfScope ps(c, K_KRYLOV_DOT, 16.0 * (k + 1) * (double)n);
+  // (a gated launch usually exits at once -- the host cannot know: its bytes
+  // are not counted, so the class's GB/s is that of the ungated passes)
+  ProfScope ps(c, K_KRYLOV_DOT, g_after ? 0.0 : 16.0 * (k + 1) * (double)n);
   switch (k) {
 #define HS_CASE(KK) \
   case KK: k_block_dot<KK><<<nb, kThreads, 0, c->stream>>>(V, ldv, w, n, part, gate); break;
@@ -247,7 +249,7 @@ int krylov_block_update(Ctx* c, const double2* V, int64_t ldv, int k, const doub
   const int nb = grid_for(c, n);
   double2* part = (double2*)scratch(c, (size_t)nb * sizeof(double2), 2);
   if (!part) return set_error(c, HS_E_CUDA, "scratch allocation failed");
-  ProfScope ps(c, K_KRYLOV_UPDATE, 16.0 * (k + 2) * (double)n);
+  ProfScope ps(c, K_KRYLOV_UPDATE, g_after ? 0.0 : 16.0 * (k + 2) * (double)n);
   switch (k) {
 #define HS_CASE(KK) \
   case KK: k_block_update<KK><<<nb, kThreads, 0, c->stream>>>(V, ldv, h, w, n, part, gate); \
