@@ -31,9 +31,10 @@ F, _ = to_device(Z, nmax * n)
 F = F.reshape(nmax, n)
 print(f"config {idx}/{scale}: J={p.subdomains} M={hh.coarse_op.shape[1]} segments={sw.segments} "
       f"chunks={sw.chunks} rhs_width={sw.rhs_width()}")
+only_many = os.environ.get("HS_MANY_ONLY") is not None   # (profiling: no single applications)
 for vname, vid in (("x", 1), ("ud", 0)):
     single = torch.empty_like(F)
-    for r in range(nmax):
+    for r in range(0 if only_many else nmax):
         sw.ctx.call("hs_sweep_apply", sw.h, vid, ptr(F[r]), ptr(single[r]))
     torch.cuda.synchronize()
 
@@ -50,7 +51,8 @@ for vname, vid in (("x", 1), ("ud", 0)):
         return e0.elapsed_time(e1) / N
 
     u1 = empty(n)
-    t1 = timed(lambda: sw.ctx.call("hs_sweep_apply", sw.h, vid, ptr(F[0]), ptr(u1)))
+    t1 = float("nan") if only_many else timed(
+        lambda: sw.ctx.call("hs_sweep_apply", sw.h, vid, ptr(F[0]), ptr(u1)))
     for k in counts:
         U = torch.full((k, n), float("nan"), dtype=torch.complex128, device=F.device)
         tk = timed(lambda: sw.ctx.call("hs_sweep_apply_many", sw.h, vid, k, ptr(F), ptr(U), n))
