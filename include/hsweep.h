@@ -182,7 +182,11 @@ int hs_sweep_apply(hs_ctx* ctx, hs_sweep* s, int variant, const void* f, void* u
  * through ONE chain of slab solves, every factor block streamed once per
  * group; per right-hand side the result is bitwise hs_sweep_apply's.  3-D
  * levels and the exact solvers (hs_exact_create*) carry the group through
- * their block chains the same way (multi-column Factorization.solve). */
+ * their block chains the same way (multi-column Factorization.solve).  The
+ * batch's work set (traces, mid-sweep residual, second-pass buffer) belongs
+ * to the sweep and is allocated on first use: one caller at a time per
+ * hs_sweep; concurrent callers go through lanes (hs_cycle_create_lane), whose
+ * work sets are private. */
 int hs_sweep_apply_many(hs_ctx* ctx, hs_sweep* s, int variant, int nrhs, const void* f, void* u,
                         long long stride);
 int hs_sweep_rhs_width(hs_sweep* s);
