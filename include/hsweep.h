@@ -49,9 +49,10 @@ int hs_ctx_create(int device, hs_ctx** out);
 int hs_ctx_destroy(hs_ctx* ctx);
 int hs_ctx_set_stream(hs_ctx* ctx, void* cuda_stream);
 /* Face segments per sweep front of the 2-D sweeps this context creates next
- * (two-level partition: one 16-CTA cluster per segment; 0 = automatic, the
- * widest layout whose clusters co-reside -- the fastest single sweep; 1 = one
- * cluster per front, which leaves room for concurrent sweep lanes). */
+ * (two-level partition: one cluster -- 9 CTAs by default -- per segment;
+ * 0 = automatic, the widest layout whose clusters co-reside -- the fastest
+ * single sweep; 1 = one cluster per front, which leaves room for any number
+ * of concurrent sweep lanes; G > 1 allows hs_sweep_max_fronts / 2 lanes). */
 int hs_ctx_set_sweep_segments(hs_ctx* ctx, int segments);
 const char* hs_last_error(hs_ctx* ctx);
 long long hs_last_error_index(hs_ctx* ctx);
@@ -65,6 +66,7 @@ int hs_version(void);
  *   0 stencil  1 residual  2 jacobi  3 jacobi2z (2 steps from zero)
  *   4 restrict 5 prolong   6 sweep_gather 7 sweep_front
  *   8 krylov_dot 9 krylov_update 10 krylov_other 11 setup
+ *   12 pre_fused 13 post_fused (the fused V-cycle halves of 2-D levels)
  * hs_profile_read synchronises, folds pending events in and copies per-class
  * milliseconds, algorithmic HBM bytes and launch counts (arrays of nclass). */
 int hs_profile_enable(hs_ctx* ctx, int on);
