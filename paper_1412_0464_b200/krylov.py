@@ -41,6 +41,9 @@ import os as _os
 # counts or residual histories; HS_DGKS_ETA=0.7071 restores it.  (The
 # reference's modified Gram-Schmidt never re-orthogonalises.)
 _DGKS = float(_os.environ.get("HS_DGKS_ETA", 0.1))
+# first-pass update fused with the second pass's dots (one read of the basis
+# when the second pass runs; HS_FUSE_UPDATE_DOT=0: separate kernels, A/B)
+_FUSE_UPDATE_DOT = _os.environ.get("HS_FUSE_UPDATE_DOT", "1") != "0"
 
 
 @dataclass(frozen=True)
@@ -221,7 +224,7 @@ def _update_dot_pass(ctx, basis, k, h, w, n, nbuf, h2):
     basis; bitwise the update then the dot pass): w -= V[0:k] h, h2[0:k] =
     V[0:k]^H w, ||w||^2 into nbuf[0] and h2[k].  False when k exceeds one
     kernel chunk (the caller then runs the two passes)."""
-    if k > _KCHUNK:
+    if k > _KCHUNK or not _FUSE_UPDATE_DOT:
         return False
     ctx.call("hs_block_update_dot", ptr(basis.V[0]), basis.V.stride(0), k, ptr(h), ptr(w), n,
              ptr(nbuf), ptr(h2))
