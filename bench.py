@@ -579,6 +579,8 @@ def run_ours(args):
             "sweep_segments": dev.sweep.segments if p.mesh.dim == 2 else None,
             "rhs_per_rank": len(f_dev),
             "rhs_in_flight": (len(f_dev) if args.batch else min(args.lanes, len(f_dev))) if multi else 1,
+            "rhs_per_chain": (min(dev.sweep.rhs_width(), max(1, len(f_dev) // groups))
+                              if multi and args.batch else 1),
             "rhs_mode": (f"{groups} lockstep batch(es) (several right-hand sides per chain of "
                          "slab solves)" if args.batch else "lanes") if multi else "single",
             "reference_iterations": reference_iterations(p, args),

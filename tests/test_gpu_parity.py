@@ -806,3 +806,39 @@ def test_gmres_many_on_3d_and_exact_cycles():
             assert r1.iterations == r0.iterations, name
             assert np.array_equal(r1.residual_history, r0.residual_history), name
             assert np.array_equal(u1, u0), name
+
+
+def test_c4_lockstep_batches_match_reference_solves():
+    """BASELINE configs[3] at full size the way bench.py runs it -- all eight
+    sources as two lockstep batches of four (fronts of G = 3 segments, each
+    batch's sweeps two right-hand sides per chain of slab solves) -- against the
+    reference's own solves of every source: iteration counts +-1, residual
+    histories within 1e-6, sampled solutions within 1e-5."""
+    import paper_1412_0464_b200 as hb
+    from paper_1412_0464_b200.configs import config
+    anchors = _large_anchors()
+    names = [f"C4_rhs{r}" for r in range(8)]
+    if any(n not in anchors for n in names):
+        pytest.skip("no reference anchors for C4")
+    a0 = anchors[names[0]]
+    p = config(a0["config"], a0["scale"])
+    cycle, _ = hb.build_two_grid(p.mesh, p.model, smoother=hb.SmootherConfig(p.omega_jac, p.nu),
+                                 coarse="sweep",
+                                 sweep=hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains,
+                                                       segments=3),
+                                 keep_slab_ops=False)
+    sw = cycle.hierarchy.partition.device()
+    assert sw.segments == 3 and sw.rhs_width() >= 2   # (39-point chunks: two vector sets fit)
+    rhs = [p.f[anchors[n]["rhs"]].ravel() for n in names]
+    out = hb.solve_many(cycle, rhs, hb.GmresConfig(p.tol, p.max_iter, p.restart), lanes=2,
+                        batch=True)
+    for n, f, (u, rep) in zip(names, rhs, out):
+        a = anchors[n]
+        assert abs(rep.iterations - a["iterations"]) <= 1, (n, rep.iterations, a["iterations"])
+        k = min(len(rep.residual_history), len(a["history"]))
+        h_ref = np.asarray(a["history"][:k])
+        assert np.all(np.abs(rep.residual_history[:k] - h_ref) <= 1e-6 * h_ref + 1e-14), n
+        assert rep.converged
+        idx = np.asarray(a["u_sample_idx"])
+        ref = np.asarray(a["u_sample_re"]) + 1j * np.asarray(a["u_sample_im"])
+        assert np.linalg.norm(u[idx] - ref) <= 1e-5 * np.linalg.norm(ref), n
