@@ -371,23 +371,39 @@ def run_ours(args):
     mine = assign_rhs(nrhs_total, world, rank)
     # several right-hand sides in flight as lanes: one cluster per sweep front
     # (the lanes' sweeps run side by side); one at a time: the widest layout
-    # lockstep batches side by side: each group's two fronts get 7 // groups
-    # segments (14 nine-CTA clusters co-reside on a B200: 2 * groups * G <= 14)
+    # lockstep batches side by side: two groups run fastest with 5 segments of
+    # 6-CTA clusters per front (20 clusters; measured against 9 x 3, 8 x 3,
+    # 6 x 4, 5 x 6, 4 x 8: profiles/r2/c4_layouts.log); if the device cannot
+    # hold them all at once, 7 // groups segments of the default 9-CTA
+    # clusters (14 of those co-reside on a B200: 2 * groups * G <= 14)
     groups = max(1, min(args.batch_groups, len(mine) // 2)) if args.batch else 1
     if args.batch:
         args.lanes = groups
-    segments = args.segments if args.segments >= 0 else (
-        (7 // groups if groups > 1 else 0) if args.batch
-        else 1 if len(mine) > 1 and args.lanes > 1 else 0)
+    cluster = 0
+    if args.segments >= 0:
+        segments = args.segments
+    elif args.batch:
+        segments, cluster = (5, 6) if groups == 2 else ((7 // groups, 0) if groups > 1 else (0, 0))
+    else:
+        segments = 1 if len(mine) > 1 and args.lanes > 1 else 0
     t0 = time.perf_counter()
     keep = (rank == 0 and world == 1 and not args.no_cpu_baseline)
-    cycle, _ = hb.build_two_grid(p.mesh, p.model, fine_op=fine_operator(p),
+    def build(segments, cluster):
+        return hb.build_two_grid(p.mesh, p.model, fine_op=fine_operator(p),
                                  smoother=hb.SmootherConfig(p.omega_jac, p.nu),
                                  coarse="sweep",
                                  sweep=hb.SweepOptions(p.w_dd, p.s_dd, "x",
                                                        subdomains=p.subdomains,
-                                                       segments=segments),
-                                 keep_slab_ops=keep)
+                                                       segments=segments, cluster=cluster),
+                                 keep_slab_ops=keep)[0]
+
+    cycle = build(segments, cluster)
+    if cluster and groups > 1:
+        from paper_1412_0464_b200.twogrid import _lane_capable
+        if not _lane_capable(cycle, groups):   # the 6-CTA layout does not co-reside here
+            cycle = None
+            segments, cluster = 7 // groups, 0
+            cycle = build(segments, cluster)
     dev = cycle.device()
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0

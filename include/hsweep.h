@@ -54,6 +54,11 @@ int hs_ctx_set_stream(hs_ctx* ctx, void* cuda_stream);
  * single sweep; 1 = one cluster per front, which leaves room for any number
  * of concurrent sweep lanes; G > 1 allows hs_sweep_max_fronts / 2 lanes). */
 int hs_ctx_set_sweep_segments(hs_ctx* ctx, int segments);
+/* CTAs (face chunks) per segment's cluster of the 2-D sweeps this context
+ * creates next (0 = automatic: 9).  Smaller clusters with more segments pack
+ * several concurrent sweeps better: two lockstep batches at C4 run fastest
+ * with 5 segments of 6 CTAs per front (DESIGN 5.2). */
+int hs_ctx_set_sweep_cluster(hs_ctx* ctx, int ctas);
 const char* hs_last_error(hs_ctx* ctx);
 long long hs_last_error_index(hs_ctx* ctx);
 long long hs_launch_count(hs_ctx* ctx);           /* kernels launched so far */

@@ -30,6 +30,7 @@ SIGNATURES = {
     "hs_ctx_destroy": (C.c_int, [_vp]),
     "hs_ctx_set_stream": (C.c_int, [_vp, _vp]),
     "hs_ctx_set_sweep_segments": (C.c_int, [_vp, C.c_int]),
+    "hs_ctx_set_sweep_cluster": (C.c_int, [_vp, C.c_int]),
     "hs_last_error": (C.c_char_p, [_vp]),
     "hs_last_error_index": (C.c_longlong, [_vp]),
     "hs_launch_count": (C.c_longlong, [_vp]),

@@ -280,6 +280,12 @@ int hs_ctx_set_sweep_segments(hs_ctx* c, int segments) {
   return HS_OK;
 }
 
+int hs_ctx_set_sweep_cluster(hs_ctx* c, int ctas) {
+  if (!c || ctas < 0) return HS_E_ARG;
+  c->sweep_cluster = ctas;
+  return HS_OK;
+}
+
 int hs_ctx_set_stream(hs_ctx* c, void* stream) {
   if (!c) return HS_E_ARG;
   c->stream = (cudaStream_t)stream;

@@ -81,6 +81,7 @@ struct Ctx {
   long long last_index = -1;
   long long launches = 0;
   int sweep_segments = 0;         // 2-D sweeps created next: face segments per front (0 = auto)
+  int sweep_cluster = 0;          // ... and CTAs (face chunks) per segment's cluster (0 = auto)
   void* scratch[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t scratch_bytes[4] = {0, 0, 0, 0};
   // profiler: CUDA events bracketing every launch when enabled

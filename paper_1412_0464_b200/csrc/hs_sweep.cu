@@ -2669,6 +2669,7 @@ int sweep_create(Ctx* c, const Stencil* coarse, int J, const int64_t* beta, cons
   } else {
     C = std::max(1, std::min(9, M / 16));
     G = M < 144 ? 1 : std::max(1, std::min(std::min(kMaxG, kMaxCh / C), M / (8 * C)));
+    if (c->sweep_cluster > 1) C = std::max(2, std::min(std::min(kMaxC, c->sweep_cluster), M / 8));
     if (c->sweep_segments > 1) G = std::min(std::min(kMaxG, kMaxCh / C), c->sweep_segments);
   }
   if (const char* ev = getenv("HS_SWEEP_SEGMENTS")) G = std::max(1, std::min(kMaxG, atoi(ev)));

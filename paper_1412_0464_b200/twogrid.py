@@ -53,6 +53,8 @@ class SweepOptions:
     # one cluster per front so that several right-hand sides' sweeps (solve_many
     # lanes) run side by side
     segments: int = 0
+    # CTAs (face chunks) per segment's cluster, 0 = automatic (9)
+    cluster: int = 0
 
 
 def default_dd_strength(w_dd: int) -> float:
@@ -494,12 +496,14 @@ def build_hierarchy(mesh: Mesh, model: WaveModel, fine_op=None, smoother=None, s
         ctx = context() if device else None
         if ctx is not None:
             ctx.lib.hs_ctx_set_sweep_segments(ctx.h, int(sweep.segments))
+            ctx.lib.hs_ctx_set_sweep_cluster(ctx.h, int(sweep.cluster))
         try:
             part = build_partition(clevel, sweep.w_dd, sweep.s_dd, J=sweep.subdomains,
                                    device=device, keep_slab_ops=keep_slab_ops)
         finally:
             if ctx is not None:
                 ctx.lib.hs_ctx_set_sweep_segments(ctx.h, 0)
+                ctx.lib.hs_ctx_set_sweep_cluster(ctx.h, 0)
     h = float(mesh.spacing[0][0])
     return HostHierarchy(mesh, flevel.op, clevel.op, cmap, clevel, part, smoother, sweep,
                          h ** mesh.dim)

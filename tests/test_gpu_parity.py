@@ -842,3 +842,35 @@ def test_c4_lockstep_batches_match_reference_solves():
         idx = np.asarray(a["u_sample_idx"])
         ref = np.asarray(a["u_sample_re"]) + 1j * np.asarray(a["u_sample_im"])
         assert np.linalg.norm(u[idx] - ref) <= 1e-5 * np.linalg.norm(ref), n
+
+
+def test_sweep_cluster_option():
+    """SweepOptions.cluster (hs_ctx_set_sweep_cluster): 6-CTA clusters with 4
+    segments per front give the default layout's sweep to rounding, and two
+    lockstep batches on that layout are bitwise the sequential solves."""
+    import paper_1412_0464_b200 as hb
+    from paper_1412_0464_b200.configs import config
+    p = config(1, 2)
+
+    def build(**kw):
+        return hb.build_two_grid(p.mesh, p.model, smoother=hb.SmootherConfig(p.omega_jac, p.nu),
+                                 coarse="sweep",
+                                 sweep=hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains,
+                                                       **kw))[0]
+
+    base, small = build(), build(segments=4, cluster=6)
+    sw = small.hierarchy.partition.device()
+    assert sw.chunks == 6 and sw.segments == 4
+    z = crand(np.random.default_rng(9), base.hierarchy.partition.shape)
+    assert rel(hb.prec_x(small.hierarchy.partition, z), hb.prec_x(base.hierarchy.partition, z)) < 1e-11
+    n = p.mesh.unknowns
+    rhs = []
+    for k in range(4):
+        f = np.zeros(n, complex)
+        f[60 + 41 * k, 70 + 53 * k] = 1.0 / p.mesh.spacing[0][0] ** 2
+        rhs.append(f.ravel())
+    cfg = hb.GmresConfig(1e-6, 40, 20)
+    seq = [hb.gmres(small.fine_csr, small.as_preconditioner(), f, cfg) for f in rhs]
+    par = hb.solve_many(small, rhs, cfg, lanes=2, batch=True)
+    for (u0, r0), (u1, r1) in zip(seq, par):
+        assert r1.iterations == r0.iterations and np.array_equal(u1, u0)
