@@ -68,7 +68,7 @@ def parse():
                    help="multi-RHS configs: independent solves on concurrent lanes instead of "
                         "the default lockstep batches (gmres_many: the solves advance together "
                         "and their coarse sweeps share one chain of slab solves per group)")
-    p.add_argument("--batch-groups", type=int, default=2,
+    p.add_argument("--batch-groups", type=int, default=4,
                    help="with --batch: lockstep groups running side by side (one lane each)")
     p.add_argument("--segments", type=int, default=-1,
                    help="face segments per sweep front (-1: 1 when several right-hand sides "
@@ -371,19 +371,22 @@ def run_ours(args):
     mine = assign_rhs(nrhs_total, world, rank)
     # several right-hand sides in flight as lanes: one cluster per sweep front
     # (the lanes' sweeps run side by side); one at a time: the widest layout
-    # lockstep batches side by side: two groups run fastest with 5 segments of
-    # 6-CTA clusters per front (20 clusters; measured against 9 x 3, 8 x 3,
-    # 6 x 4, 5 x 6, 4 x 8: profiles/r2/c4_layouts.log); if the device cannot
-    # hold them all at once, 7 // groups segments of the default 9-CTA
-    # clusters (14 of those co-reside on a B200: 2 * groups * G <= 14)
+    # lockstep batches side by side (one lane each): small clusters with
+    # several segments pack concurrent batches best (cluster CTAs x segments
+    # per front, measured at C4: profiles/r2/c4_layouts.log).  Candidates in
+    # order of speed; the first whose clusters all co-reside on this device
+    # (hs_sweep_max_fronts) is used, the last one always fits
     groups = max(1, min(args.batch_groups, len(mine) // 2)) if args.batch else 1
     if args.batch:
         args.lanes = groups
+    layouts = {4: [(4, 4), (3, 5)], 3: [(6, 3)], 2: [(6, 5)]}.get(groups, []) if args.batch else []
+    if groups > 1:
+        layouts = layouts + [(0, max(1, 7 // groups))]   # default 9-CTA clusters: 14 co-reside
     cluster = 0
     if args.segments >= 0:
-        segments = args.segments
+        segments, layouts = args.segments, []
     elif args.batch:
-        segments, cluster = (5, 6) if groups == 2 else ((7 // groups, 0) if groups > 1 else (0, 0))
+        cluster, segments = layouts.pop(0) if layouts else (0, 0)
     else:
         segments = 1 if len(mine) > 1 and args.lanes > 1 else 0
     t0 = time.perf_counter()
@@ -398,11 +401,11 @@ def run_ours(args):
                                  keep_slab_ops=keep)[0]
 
     cycle = build(segments, cluster)
-    if cluster and groups > 1:
+    if groups > 1:
         from paper_1412_0464_b200.twogrid import _lane_capable
-        if not _lane_capable(cycle, groups):   # the 6-CTA layout does not co-reside here
+        while layouts and not _lane_capable(cycle, groups):   # does not co-reside here: next
             cycle = None
-            segments, cluster = 7 // groups, 0
+            cluster, segments = layouts.pop(0)
             cycle = build(segments, cluster)
     dev = cycle.device()
     torch.cuda.synchronize()

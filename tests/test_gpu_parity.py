@@ -810,10 +810,11 @@ def test_gmres_many_on_3d_and_exact_cycles():
 
 def test_c4_lockstep_batches_match_reference_solves():
     """BASELINE configs[3] at full size the way bench.py runs it -- all eight
-    sources as two lockstep batches of four (fronts of G = 3 segments, each
-    batch's sweeps two right-hand sides per chain of slab solves) -- against the
-    reference's own solves of every source: iteration counts +-1, residual
-    histories within 1e-6, sampled solutions within 1e-5."""
+    sources as four lockstep batches of two (4 segments of 4-CTA clusters per
+    front, two right-hand sides per chain of slab solves; one batch of eight
+    where the device cannot hold the 32 clusters) -- against the reference's
+    own solves of every source: iteration counts +-1, residual histories
+    within 1e-6, sampled solutions within 1e-5."""
     import paper_1412_0464_b200 as hb
     from paper_1412_0464_b200.configs import config
     anchors = _large_anchors()
@@ -825,12 +826,12 @@ def test_c4_lockstep_batches_match_reference_solves():
     cycle, _ = hb.build_two_grid(p.mesh, p.model, smoother=hb.SmootherConfig(p.omega_jac, p.nu),
                                  coarse="sweep",
                                  sweep=hb.SweepOptions(p.w_dd, p.s_dd, "x", subdomains=p.subdomains,
-                                                       segments=3),
+                                                       segments=4, cluster=4),
                                  keep_slab_ops=False)
     sw = cycle.hierarchy.partition.device()
-    assert sw.segments == 3 and sw.rhs_width() >= 2   # (39-point chunks: two vector sets fit)
+    assert sw.segments == 4 and sw.chunks == 4 and sw.rhs_width() >= 2
     rhs = [p.f[anchors[n]["rhs"]].ravel() for n in names]
-    out = hb.solve_many(cycle, rhs, hb.GmresConfig(p.tol, p.max_iter, p.restart), lanes=2,
+    out = hb.solve_many(cycle, rhs, hb.GmresConfig(p.tol, p.max_iter, p.restart), lanes=4,
                         batch=True)
     for n, f, (u, rep) in zip(names, rhs, out):
         a = anchors[n]

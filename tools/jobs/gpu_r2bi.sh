@@ -1,0 +1,15 @@
+#!/bin/bash
+# C4 lockstep batches: four groups of two, smaller clusters
+mkdir -p gpurun_out
+O=gpurun_out
+run() {
+  label=$1; shift
+  env "$@" timeout 900 python bench.py --config 3 --steps 1 --warmup 2 --no-cpu-baseline $EXTRA 2>/dev/null | tail -n 1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('$label', round(d['ms_per_step'],1), d['iterations'], d.get('sweep_segments'), d.get('rhs_per_chain'), d.get('rhs_mode')[:22])" >> $O/c4_layouts4.log
+}
+EXTRA="--batch-groups 4 --segments 3" run "groups4_C4_G3" HS_SWEEP_CPC=4
+EXTRA="--batch-groups 4 --segments 4" run "groups4_C4_G4" HS_SWEEP_CPC=4
+EXTRA="--batch-groups 4 --segments 6" run "groups4_C3_G6" HS_SWEEP_CPC=3
+EXTRA="--batch-groups 4 --segments 5" run "groups4_C3_G5" HS_SWEEP_CPC=3
+EXTRA="--batch-groups 4 --segments 3" run "groups4_C5_G3" HS_SWEEP_CPC=5
+EXTRA="--batch-groups 4 --segments 4" run "groups4_C3_G4" HS_SWEEP_CPC=3
+echo done >> $O/c4_layouts4.log
